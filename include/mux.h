@@ -1,0 +1,201 @@
+/* mux.h — C ABI of libmux: MuxTune's spatially multiplexed LoRA linear layer
+ * (arXiv 2603.02885) on B200 (sm_100a).
+ *
+ * Citations: P:n = PAPER.md line n (the paper's LaTeX source).
+ *
+ * Operations
+ *   mux_pack_chunks  chunk-based data alignment, P:833-843 (§3.5): per-task
+ *                    packing of sequences, partition of packs into
+ *                    equal power-of-two chunks with KV-reuse dependency links
+ *                    (P:837-838), chunk size rule.
+ *   mux_pack_apply   gathers token-major rows into the packed row layout
+ *                    (the "Dispatch" sub-module), zero-filling pad rows.
+ *   mux_linear_fwd   BaseOp forward spatially batched over all segments,
+ *                    Eq. 1, plus each segment's LoRA adapter
+ *                    (north_star:  Y_t += s_t (X_t A_t^T) B_t^T ), fused
+ *                    "horizontally" per hTask.
+ *   mux_linear_bwd   BaseOp backward Eq. 2 plus the LoRA chain
+ *                    rule: dX = dY W + s_t (dY B_t) A_t, dA_t, dB_t; no
+ *                    backbone weight gradient (frozen backbone).
+ *
+ * Conventions (all functions)
+ *   - Pointers are DEVICE pointers unless marked [host].  The caller owns
+ *     every buffer; the library never allocates, frees or synchronizes.
+ *   - Every call only enqueues work on `stream` (graph-capturable: no host
+ *     reads of device data) and returns.
+ *   - Outputs are overwritten (beta = 0), inputs never written, outputs must
+ *     not alias inputs.
+ *   - Host-side validation runs before any launch: on failure nothing is
+ *     launched, outputs are untouched, the status is returned and
+ *     mux_last_error() holds a thread-local message.
+ *   - Layouts: row-major.  X [max_rows, K], W [N, K] (nn.Linear.weight),
+ *     A_t [rank, K] (PEFT lora_A.weight), B_t [N, rank] (lora_B.weight),
+ *     Y [max_rows, N], Hs [max_rows, r_cap], dY [max_rows, N], dX [max_rows, K].
+ *   - bf16 storage, fp32 accumulation; Hs/Gs are rounded to bf16; dA/dB fp32.
+ *   - A segment is the contiguous row range [seg_off[s], seg_off[s+1]) owned
+ *     by adapter seg_task[s]; several segments may share an adapter (its
+ *     gradients are then summed over all of them).
+ */
+#ifndef MUX_H_
+#define MUX_H_
+
+#include <stddef.h>
+#include <stdint.h>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+#if defined(__GNUC__)
+#define MUX_API __attribute__((visibility("default")))
+#else
+#define MUX_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MUX_MAX_SEGMENTS 64   /* per linear call (kernel parameter block <= 32 KB) */
+#define MUX_MAX_ADAPTERS 64
+#define MUX_MAX_RANK 64        /* LoRA ranks up to 64 in the paper's workloads */
+
+typedef enum {
+  MUX_OK = 0,
+  MUX_ERR_INVALID_ARGUMENT = 1,
+  MUX_ERR_UNSUPPORTED = 2,
+  MUX_ERR_INSUFFICIENT_BUFFER = 3,
+  MUX_ERR_CUDA = 4
+} mux_status;
+
+/* Thread-local message describing the last non-OK status of this thread. */
+MUX_API const char* mux_last_error(void);
+
+/* Library version string, e.g. "mux 0.1 sm_100a". */
+MUX_API const char* mux_version(void);
+
+/* ------------------------------------------------------------------ packing */
+
+/* Written by mux_pack_chunks (device struct).
+ *   chunk_size   c actually used (P:843 rule or the caller's value)
+ *   num_chunks   chunks emitted; total_rows = num_chunks * c = seg_off[M]
+ *   num_packs    packs over all tasks
+ *   valid_rows   sum of sequence lengths (effective tokens)
+ *   zero_pad_rows  rows the zero-pad-to-global-max strategy would execute
+ *                (num_seqs * max length, reported for comparison)
+ *   overflow     0 = ok; bit 1: total_rows > max_rows; bit 2: num_chunks >
+ *                max_chunks; bit 4: invalid device data (a length < 1 or a
+ *                capacity below a task's longest sequence).  When nonzero
+ *                nothing but this struct is written. */
+typedef struct {
+  int32_t chunk_size, num_chunks, num_packs, total_rows, valid_rows, zero_pad_rows, overflow;
+} mux_pack_info;
+
+/* [host] Worst-case packed rows for a call (every sequence alone in its own
+ * pack and rounded up to the largest possible chunk): lets the caller size
+ * max_rows without reading device data.  chunk_size_or_max = the explicit
+ * chunk size, or an upper bound on the rule's result (e.g. max capacity). */
+MUX_API int64_t mux_pack_bound_rows(int64_t total_tokens, int32_t num_seqs, int32_t chunk_size_or_max);
+
+/* Bytes of device workspace mux_pack_chunks needs. */
+MUX_API size_t mux_pack_workspace_size(int32_t num_tasks, int32_t num_seqs);
+
+/* Chunk-based alignment of one hTask.
+ *   num_tasks M >= 1, num_seqs >= 0                             [host]
+ *   task_seq_off [M+1]  CSR over seq_len, task-major caller order; a task may be empty
+ *   seq_len [num_seqs]  each >= 1
+ *   pack_capacity [M]   per-task pack capacity >= the task's longest sequence,
+ *                       or NULL = round_up(max(max len_t, c), c)
+ *   chunk_size          [host] 0 = rule of P:843: c = max(chunk_min, 2^{min_s v2(len_s)});
+ *                       else a power of two >= 64
+ *   chunk_min           [host] power of two >= 64 ("minimum threshold (typically 64)")
+ *   max_rows, max_chunks [host] capacities of row_src and of the chunk table
+ * Packing (reading Q5 in DESIGN.md): first-fit decreasing per task, sequences
+ * visited by (length desc, index asc), each into the lowest-index pack with
+ * room; chunks numbered task-major, then pack-creation order; row of chunk =
+ * id * c; seg_off[t] = first row of task t.
+ * Outputs: seg_off [M+1]; seq_row [num_seqs] (packed row of each sequence's
+ * token 0); chunk_task/chunk_pack/chunk_valid/chunk_dep [max_chunks] (dep =
+ * previous chunk of the same pack, -1 = none: the KV-reuse link of P:838);
+ * row_src [max_rows] (source token index, token = concatenation of sequences
+ * in (task, caller) order; -1 = pad or unused); info.
+ * Errors: MUX_ERR_INVALID_ARGUMENT (host-checkable arguments),
+ * MUX_ERR_INSUFFICIENT_BUFFER (workspace too small), MUX_ERR_CUDA.
+ * Device-data problems are reported in info->overflow (see above). */
+MUX_API mux_status mux_pack_chunks(int32_t num_tasks, int32_t num_seqs,
+                           const int32_t* task_seq_off, const int32_t* seq_len,
+                           const int32_t* pack_capacity, int32_t chunk_size, int32_t chunk_min,
+                           int32_t max_rows, int32_t max_chunks,
+                           int32_t* seg_off, int32_t* seq_row,
+                           int32_t* chunk_task, int32_t* chunk_pack, int32_t* chunk_valid,
+                           int32_t* chunk_dep, int32_t* row_src, mux_pack_info* info,
+                           void* workspace, size_t workspace_bytes, cudaStream_t stream);
+
+/* Dispatch: dst[r, :] = src[row_src[r], :] if row_src[r] >= 0 else 0, for
+ * r < max_rows.  src [num_tokens, cols], dst [max_rows, cols] bf16;
+ * cols a multiple of 8, pointers 16-byte aligned.  Indices >= num_tokens
+ * are treated as pad (0). */
+MUX_API mux_status mux_pack_apply(int32_t max_rows, int32_t cols, int32_t num_tokens,
+                          const int32_t* row_src, const __nv_bfloat16* src,
+                          __nv_bfloat16* dst, cudaStream_t stream);
+
+/* ------------------------------------------------------------------ linear */
+
+/* One adapter (task) of a linear layer.  [host] array; the pointers inside
+ * are device pointers. */
+typedef struct {
+  const __nv_bfloat16* A;  /* [rank, K] row-major (lora_A.weight) */
+  const __nv_bfloat16* B;  /* [N, rank] row-major (lora_B.weight) */
+  float* dA;               /* [rank, K] fp32, overwritten by bwd; NULL = skip */
+  float* dB;               /* [N, rank] fp32, overwritten by bwd; NULL = skip */
+  int32_t rank;            /* 0 (no adapter on this layer) .. 64 */
+  int32_t ldb;             /* leading dimension (elements) of B: 0 = rank; must be a
+                              multiple of 8 (16-byte rows for TMA), so ranks that are
+                              not multiples of 8 need a padded B (columns >= rank are
+                              never read).  dB is always [N, rank] contiguous. */
+  float scale;             /* s_t (LoRA alpha_t / rank_t, computed by the caller) */
+} mux_adapter;
+
+/* Bytes of device workspace mux_linear_fwd / mux_linear_bwd need. */
+MUX_API size_t mux_linear_workspace_size(int32_t num_segs, int32_t max_rows, int32_t K, int32_t N,
+                                 int32_t r_cap);
+
+/* Forward (Eq. 1 + LoRA).  For every row i of segment s, t = seg_task[s]:
+ *   Y[i,:]  = X[i,:] W^T + s_t (X[i,:] A_t^T) B_t^T
+ *   Hs[i,j] = bf16(s_t * X[i,:] A_t[j,:]^T) for j < rank_t, 0 for rank_t <= j < r_cap
+ * Arguments
+ *   num_segs S (1..64) [host]; seg_off [S+1] device, non-decreasing, every
+ *   entry a multiple of 64 (mux_pack_chunks guarantees it), seg_off[S] <=
+ *   max_rows; seg_task [S] [host] adapter index per segment;
+ *   num_adapters (1..64), adapters [host];
+ *   K, N multiples of 64; r_cap in {16,32,48,64} >= every rank;
+ *   X [max_rows, K] (pad rows inside segments must be 0: then Y's pad rows are 0);
+ *   W [N, K]; Y [max_rows, N]; Hs [max_rows, r_cap] or NULL (inference: kept
+ *   in the workspace).  Rows >= seg_off[S] of Y/Hs are not written.
+ * Errors: MUX_ERR_INVALID_ARGUMENT (shape, alignment (16 B), rank/scale,
+ * index checks), MUX_ERR_INSUFFICIENT_BUFFER, MUX_ERR_CUDA. */
+MUX_API mux_status mux_linear_fwd(int32_t num_segs, const int32_t* seg_off, const int32_t* seg_task,
+                          int32_t num_adapters, const mux_adapter* adapters,
+                          int32_t max_rows, int32_t K, int32_t N, int32_t r_cap,
+                          const __nv_bfloat16* X, const __nv_bfloat16* W,
+                          __nv_bfloat16* Y, __nv_bfloat16* Hs,
+                          void* workspace, size_t workspace_bytes, cudaStream_t stream);
+
+/* Backward (Eq. 2 + LoRA chain rule).  For rows i of segment s, t = seg_task[s]:
+ *   Gs[i,j]  = bf16(s_t * dY[i,:] B_t[:,j])                 (workspace)
+ *   dX[i,:]  = dY[i,:] W + Gs[i,:] A_t                      (NULL = skip)
+ *   dA_t     = sum over t's rows of Gs[i,:]^T X[i,:]         fp32 [rank, K]
+ *   dB_t     = sum over t's rows of dY[i,:]^T Hs[i,:]        fp32 [N, rank]
+ * Hs is the forward's output.  A task with no rows gets dA = dB = 0.
+ * Arguments as in mux_linear_fwd; dY [max_rows, N] (pad rows may be nonzero:
+ * they reach only dX's pad rows). */
+MUX_API mux_status mux_linear_bwd(int32_t num_segs, const int32_t* seg_off, const int32_t* seg_task,
+                          int32_t num_adapters, const mux_adapter* adapters,
+                          int32_t max_rows, int32_t K, int32_t N, int32_t r_cap,
+                          const __nv_bfloat16* dY, const __nv_bfloat16* X,
+                          const __nv_bfloat16* W, const __nv_bfloat16* Hs,
+                          __nv_bfloat16* dX,
+                          void* workspace, size_t workspace_bytes, cudaStream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MUX_H_ */

@@ -1,0 +1,68 @@
+// common.h — kernel parameter blocks shared by the host ABI (mux_abi.cu) and
+// the kernels.  Product code only; nothing here is shared with oracle/.
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "../../include/mux.h"
+
+namespace mux {
+
+// ---- fused linear GEMM (mux_linear_fwd / the dX part of mux_linear_bwd)
+constexpr int kBM = 128;        // rows per tile (TMEM lanes)
+constexpr int kBN = 256;        // output columns per tile (TMEM columns per accumulator)
+constexpr int kBK = 64;         // reduction depth per pipeline stage (one 128 B swizzle row)
+constexpr int kStages = 4;
+constexpr int kRowHalf = 64;    // segment granularity inside a tile (chunk minimum)
+constexpr int kSideN = 64;      // N of the shrink MMA (rank padded to 64)
+
+struct GemmParams {
+  // A operand of the main product: X (fwd) / dY (bwd): dims {Kred, rows}, box {64, 128}
+  CUtensorMap map_a;
+  // backbone W [N, K]: dims {K, N}, box {64, 64}
+  CUtensorMap map_w;
+  // side tensor Hs (fwd) / Gs (bwd): dims {r_cap, rows}, box {64, 128}
+  CUtensorMap map_side;
+  // output Y (fwd) / dX (bwd): dims {Nout, rows}, box {64, 32} (TMA store)
+  CUtensorMap map_out;
+  // per adapter: A_t dims {K, rank} box {64, 64};  B_t dims {rank, N} box {64, 64}
+  CUtensorMap map_lora_a[MUX_MAX_ADAPTERS];
+  CUtensorMap map_lora_b[MUX_MAX_ADAPTERS];
+  const int32_t* seg_off;        // device [num_segs + 1]
+  __nv_bfloat16* side_out;       // Hs / Gs [max_rows, r_cap]
+  int32_t* flags;                // [ceil(max_rows/128)] zeroed before launch
+  int32_t num_segs;
+  int32_t max_rows;
+  int32_t kred;                  // reduction length of the main product (K fwd, N bwd)
+  int32_t nout;                  // output columns (N fwd, K bwd)
+  int32_t r_cap;
+  int32_t has_main;              // 0: only the shrink (side) tiles
+  int32_t seg_adapter[MUX_MAX_SEGMENTS];
+  int32_t seg_rank[MUX_MAX_SEGMENTS];
+  float seg_scale[MUX_MAX_SEGMENTS];
+};
+
+// ---- segmented adapter gradients (dA_t, dB_t)
+constexpr int kGradBM = 128;     // output rows per unit (k for dA, n for dB)
+constexpr int kGradBK = 128;     // tokens per pipeline stage
+constexpr int kGradStages = 4;
+
+struct GradParams {
+  CUtensorMap map_x;    // X  dims {K, rows} box {64, 128}
+  CUtensorMap map_dy;   // dY dims {N, rows} box {64, 128}
+  CUtensorMap map_hs;   // Hs dims {r_cap, rows} box {64, 128}
+  CUtensorMap map_gs;   // Gs dims {r_cap, rows} box {64, 128}
+  const int32_t* seg_off;
+  int32_t num_segs;
+  int32_t K, N, r_cap;
+  int32_t num_tasks;                       // adapters with rank > 0 and a gradient to write
+  int32_t units_a;                         // ceil(K/128) dA units per task (0 if no task wants dA)
+  int32_t units_b;                         // ceil(N/128)
+  uint64_t task_segs[MUX_MAX_ADAPTERS];    // bit s set: segment s belongs to the task
+  int32_t task_rank[MUX_MAX_ADAPTERS];
+  float* task_dA[MUX_MAX_ADAPTERS];
+  float* task_dB[MUX_MAX_ADAPTERS];
+};
+
+}  // namespace mux

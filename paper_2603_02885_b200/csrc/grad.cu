@@ -1,0 +1,198 @@
+// grad.cu — segmented adapter-weight gradients on tcgen05 (sm_100a).
+//
+//   dA_t[j, k] = sum_{i in segments of t} Gs[i, j] X[i, k]     (fp32 [rank, K])
+//   dB_t[n, j] = sum_{i in segments of t} dY[i, n] Hs[i, j]    (fp32 [N, rank])
+//
+// (Gs = s_t dY B_t and Hs = s_t X A_t^T carry the LoRA scale; chain rule of
+// the north_star formula.)  Both are reductions over a task's
+// tokens with a small output, HBM-bound (arithmetic intensity ~ rank FLOP/B):
+// X and dY are each streamed from HBM exactly once.  A work unit is
+// (task, 128 output rows of k or n); it runs a TMA -> smem -> tcgen05 pipeline
+// over all 128-token blocks of the task's segments with M = 128 (k or n,
+// MN-major A operand), N = 64 (rank padded, MN-major B operand), K = tokens.
+// Token blocks never cross into another segment's rows: a block that extends
+// past its segment end (segments are multiples of 64) only issues the MMAs of
+// its valid 64 tokens.  Deterministic: one unit owns each output element and
+// sums tokens in ascending order.  Ranks < 16 still use the tensor cores
+// (zero-padded N = 64): the kernel is bound by streaming X/dY, not by MMA.
+#include "common.h"
+#include "ptx.cuh"
+
+namespace mux {
+
+constexpr uint32_t kGAtom = kGradBK * 128;            // 128 token rows x 128 B = 16 KB
+constexpr uint32_t kGStageA = 2 * kGAtom;             // 128 output rows = 2 MN atoms
+constexpr uint32_t kGStageB = kGAtom;                 // 64 rank columns = 1 MN atom
+constexpr uint32_t kGStageBytes = kGStageA + kGStageB;  // 48 KB
+constexpr uint32_t kGradSmemBytes = kGradStages * kGStageBytes + 1024 + 1024;
+constexpr uint32_t kGradTmemCols = 128;
+constexpr int kGradThreads = 256;
+
+__global__ void __launch_bounds__(kGradThreads, 1) mux_grad_kernel(const __grid_constant__ GradParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* pipe = smem;
+  uint8_t* misc = smem + kGradStages * kGStageBytes;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(misc);
+  uint64_t* empty_bar = full_bar + kGradStages;
+  uint64_t* tfull_bar = empty_bar + kGradStages;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  int* so = reinterpret_cast<int*>(misc + 256);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i <= p.num_segs; i += blockDim.x) so[i] = p.seg_off[i];
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&p.map_x);
+    tma_prefetch(&p.map_dy);
+    tma_prefetch(&p.map_hs);
+    tma_prefetch(&p.map_gs);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < kGradStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull_bar[a], 1);
+      mbar_init(&tempty_bar[a], 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<kGradTmemCols>(tmem_holder);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  const int per_task = p.units_a + p.units_b;
+  const int total_units = p.num_tasks * per_task;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
+        const int task = u / per_task;
+        const int sub = u - task * per_task;
+        const bool is_a = sub < p.units_a;
+        const int m0 = (is_a ? sub : sub - p.units_a) * kGradBM;
+        const CUtensorMap* ma = is_a ? &p.map_x : &p.map_dy;
+        const CUtensorMap* mb = is_a ? &p.map_gs : &p.map_hs;
+        const uint64_t segs = p.task_segs[task];
+        for (int s = 0; s < p.num_segs; ++s) {
+          if (!((segs >> s) & 1ull)) continue;
+          for (int tok = so[s]; tok < so[s + 1]; tok += kGradBK) {
+            mbar_wait(&empty_bar[stage], phase ^ 1u);
+            uint8_t* sa = pipe + stage * kGStageBytes;
+            mbar_arrive_expect_tx(&full_bar[stage], kGStageBytes);
+            tma_load_2d(ma, &full_bar[stage], sa, m0, tok);
+            tma_load_2d(ma, &full_bar[stage], sa + kGAtom, m0 + 64, tok);
+            tma_load_2d(mb, &full_bar[stage], sa + kGStageA, 0, tok);
+            if (++stage == kGradStages) { stage = 0; phase ^= 1u; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t kIdesc = idesc_bf16(kGradBM, 64, true, true);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
+        const int task = u / per_task;
+        const uint64_t segs = p.task_segs[task];
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1u);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * 64);
+        uint32_t accumulate = 0;
+        for (int s = 0; s < p.num_segs; ++s) {
+          if (!((segs >> s) & 1ull)) continue;
+          for (int tok = so[s]; tok < so[s + 1]; tok += kGradBK) {
+            const int nk = min(kGradBK, so[s + 1] - tok) / 16;
+            mbar_wait(&full_bar[stage], phase);
+            tc_fence_after();
+            const uint32_t a_base = smem_u32(pipe + stage * kGStageBytes);
+            const uint32_t b_base = a_base + kGStageA;
+            for (int k = 0; k < nk; ++k) {
+              const uint64_t ad = smem_desc(a_base + k * 16 * 128, kGAtom, 1024);
+              const uint64_t bd = smem_desc(b_base + k * 16 * 128, kGAtom, 1024);
+              mma_bf16(d_tmem, ad, bd, kIdesc, accumulate);
+              accumulate = 1;
+            }
+            mma_commit(&empty_bar[stage]);
+            if (++stage == kGradStages) { stage = 0; phase ^= 1u; }
+          }
+        }
+        mma_commit(&tfull_bar[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
+      const int task = u / per_task;
+      const int sub = u - task * per_task;
+      const bool is_a = sub < p.units_a;
+      const int m0 = (is_a ? sub : sub - p.units_a) * kGradBM;
+      const uint64_t segs = p.task_segs[task];
+      bool any = false;
+      for (int s = 0; s < p.num_segs; ++s)
+        if (((segs >> s) & 1ull) && so[s + 1] > so[s]) any = true;
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      uint32_t v0[32], v1[32];
+      const uint32_t t_addr = tmem_base + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(acc * 64);
+      tmem_ld32(t_addr, v0);
+      tmem_ld32(t_addr + 32, v1);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+      const int rank = p.task_rank[task];
+      const int m = m0 + 32 * q + lane;
+      if (is_a) {
+        float* dA = p.task_dA[task];
+        if (dA != nullptr && m < p.K) {
+#pragma unroll
+          for (int j = 0; j < 64; ++j)
+            if (j < rank) dA[static_cast<size_t>(j) * p.K + m] = any ? __uint_as_float(j < 32 ? v0[j & 31] : v1[j & 31]) : 0.f;
+        }
+      } else {
+        float* dB = p.task_dB[task];
+        if (dB != nullptr && m < p.N) {
+          float* row = dB + static_cast<size_t>(m) * rank;
+#pragma unroll
+          for (int j = 0; j < 64; ++j)
+            if (j < rank) row[j] = any ? __uint_as_float(j < 32 ? v0[j & 31] : v1[j & 31]) : 0.f;
+        }
+      }
+      if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<kGradTmemCols>(tmem_base);
+  }
+}
+
+cudaError_t launch_grad(const GradParams& p, int grid, cudaStream_t stream) {
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(mux_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kGradSmemBytes));
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  mux_grad_kernel<<<grid, kGradThreads, kGradSmemBytes, stream>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace mux

@@ -1,0 +1,391 @@
+// mux_abi.cu — the C ABI of libmux (include/mux.h): host-side validation,
+// workspace carving, TMA descriptor encoding and kernel launches.  Every
+// entry point only enqueues on the caller's stream; nothing reads device
+// data on the host, so whole layers can be captured in a CUDA graph.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "common.h"
+
+namespace mux {
+cudaError_t launch_gemm(const GemmParams& p, bool bwd, int grid, cudaStream_t stream);
+cudaError_t launch_grad(const GradParams& p, int grid, cudaStream_t stream);
+size_t pack_workspace_bytes(int M, int S);
+cudaError_t launch_pack(int M, int S, const int32_t* task_seq_off, const int32_t* seq_len,
+                        const int32_t* pack_capacity, int chunk_size, int chunk_min, int max_rows, int max_chunks,
+                        int32_t* seg_off, int32_t* seq_row, int32_t* chunk_task, int32_t* chunk_pack,
+                        int32_t* chunk_valid, int32_t* chunk_dep, int32_t* row_src, mux_pack_info* info,
+                        void* workspace, cudaStream_t stream);
+cudaError_t launch_pack_apply(int max_rows, int cols, int num_tokens, const int32_t* row_src,
+                              const __nv_bfloat16* src, __nv_bfloat16* dst, int num_sms, cudaStream_t stream);
+}  // namespace mux
+
+using namespace mux;
+
+namespace {
+
+thread_local std::string g_err;
+
+mux_status fail(mux_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+mux_status cuda_fail(cudaError_t e, const char* what) {
+  return fail(MUX_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// ---- cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, []() {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+struct MapKey {
+  const void* ptr;
+  uint64_t inner, outer, stride;
+  uint32_t box_inner, box_outer;
+  bool operator==(const MapKey& o) const {
+    return ptr == o.ptr && inner == o.inner && outer == o.outer && stride == o.stride &&
+           box_inner == o.box_inner && box_outer == o.box_outer;
+  }
+};
+struct MapKeyHash {
+  size_t operator()(const MapKey& k) const {
+    size_t h = reinterpret_cast<size_t>(k.ptr);
+    h ^= k.inner * 0x9E3779B97F4A7C15ull + (h << 6) + (h >> 2);
+    h ^= k.outer * 0xC2B2AE3D27D4EB4Full + (h << 6) + (h >> 2);
+    h ^= k.stride * 0x165667B19E3779F9ull + (h << 6) + (h >> 2);
+    h ^= (static_cast<uint64_t>(k.box_inner) << 32 | k.box_outer) + (h << 6) + (h >> 2);
+    return h;
+  }
+};
+
+// A tensor map is a pure function of (address, shape, stride, box): caching
+// by that key is exact, and saves the host ~1 us per descriptor per call.
+std::mutex g_map_mu;
+std::unordered_map<MapKey, CUtensorMap, MapKeyHash> g_maps;
+
+// 2D bf16 tensor [outer, inner] with row stride `stride` elements, box
+// {box_inner, box_outer}, 128 B swizzle, zero fill out of bounds.
+bool make_map(CUtensorMap* out, const void* ptr, uint64_t inner, uint64_t outer, uint64_t stride,
+              uint32_t box_inner, uint32_t box_outer) {
+  MapKey key{ptr, inner, outer, stride, box_inner, box_outer};
+  {
+    std::lock_guard<std::mutex> g(g_map_mu);
+    auto it = g_maps.find(key);
+    if (it != g_maps.end()) {
+      *out = it->second;
+      return true;
+    }
+  }
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {stride * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUtensorMap m;
+  CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return false;
+  *out = m;
+  std::lock_guard<std::mutex> g(g_map_mu);
+  if (g_maps.size() > 16384) g_maps.clear();
+  g_maps.emplace(key, m);
+  return true;
+}
+
+int num_sms() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  static int cached[64] = {0};
+  if (dev >= 0 && dev < 64 && cached[dev] > 0) return cached[dev];
+  int n = 148;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  if (dev >= 0 && dev < 64) cached[dev] = n;
+  return n;
+}
+
+// ---- linear-layer workspace: [flags][Gs][Hs scratch]
+struct LinearWs {
+  int32_t* flags;
+  __nv_bfloat16* gs;
+  __nv_bfloat16* hs;
+  size_t bytes;
+};
+LinearWs carve_linear_ws(void* base, int32_t max_rows, int32_t r_cap) {
+  LinearWs w{};
+  const size_t n_m = (static_cast<size_t>(max_rows) + kBM - 1) / kBM;
+  const size_t f = align256(n_m * sizeof(int32_t));
+  const size_t g = align256(static_cast<size_t>(max_rows) * r_cap * 2);
+  uint8_t* b = reinterpret_cast<uint8_t*>(base);
+  w.flags = reinterpret_cast<int32_t*>(b);
+  w.gs = reinterpret_cast<__nv_bfloat16*>(b ? b + f : nullptr);
+  w.hs = reinterpret_cast<__nv_bfloat16*>(b ? b + f + g : nullptr);
+  w.bytes = f + 2 * g;
+  return w;
+}
+
+mux_status validate_linear(int32_t num_segs, const int32_t* seg_off, const int32_t* seg_task,
+                           int32_t num_adapters, const mux_adapter* adapters, int32_t max_rows, int32_t K,
+                           int32_t N, int32_t r_cap) {
+  if (num_segs < 1 || num_segs > MUX_MAX_SEGMENTS)
+    return fail(MUX_ERR_INVALID_ARGUMENT, "num_segs=%d outside [1,%d]", num_segs, MUX_MAX_SEGMENTS);
+  if (num_adapters < 1 || num_adapters > MUX_MAX_ADAPTERS)
+    return fail(MUX_ERR_INVALID_ARGUMENT, "num_adapters=%d outside [1,%d]", num_adapters, MUX_MAX_ADAPTERS);
+  if (!seg_off || !seg_task || !adapters) return fail(MUX_ERR_INVALID_ARGUMENT, "null seg_off/seg_task/adapters");
+  if (max_rows < 1) return fail(MUX_ERR_INVALID_ARGUMENT, "max_rows=%d must be >= 1", max_rows);
+  if (K < 64 || N < 64 || (K % 64) || (N % 64))
+    return fail(MUX_ERR_INVALID_ARGUMENT, "K=%d, N=%d must be positive multiples of 64", K, N);
+  if (r_cap != 16 && r_cap != 32 && r_cap != 48 && r_cap != 64)
+    return fail(MUX_ERR_INVALID_ARGUMENT, "r_cap=%d must be one of 16, 32, 48, 64", r_cap);
+  for (int s = 0; s < num_segs; ++s)
+    if (seg_task[s] < 0 || seg_task[s] >= num_adapters)
+      return fail(MUX_ERR_INVALID_ARGUMENT, "seg_task[%d]=%d outside [0,%d)", s, seg_task[s], num_adapters);
+  for (int t = 0; t < num_adapters; ++t) {
+    const mux_adapter& a = adapters[t];
+    if (a.rank < 0 || a.rank > MUX_MAX_RANK)
+      return fail(MUX_ERR_INVALID_ARGUMENT, "adapter %d: rank=%d outside [0,64]", t, a.rank);
+    if (a.rank > r_cap) return fail(MUX_ERR_INVALID_ARGUMENT, "adapter %d: rank=%d > r_cap=%d", t, a.rank, r_cap);
+    if (!std::isfinite(a.scale)) return fail(MUX_ERR_INVALID_ARGUMENT, "adapter %d: scale is not finite", t);
+    if (a.rank > 0) {
+      if (!a.A || !a.B) return fail(MUX_ERR_INVALID_ARGUMENT, "adapter %d: null A or B", t);
+      if (!aligned16(a.A) || !aligned16(a.B))
+        return fail(MUX_ERR_INVALID_ARGUMENT, "adapter %d: A/B not 16-byte aligned", t);
+      const int ldb = a.ldb == 0 ? a.rank : a.ldb;
+      if (ldb < a.rank || (ldb % 8) != 0)
+        return fail(MUX_ERR_INVALID_ARGUMENT,
+                    "adapter %d: ldb=%d must be >= rank=%d and a multiple of 8 (16-byte rows for TMA)", t, ldb,
+                    a.rank);
+    }
+  }
+  return MUX_OK;
+}
+
+// Fill the per-adapter TMA descriptors (rank > 0 only).
+mux_status fill_adapter_maps(GemmParams& p, int32_t num_adapters, const mux_adapter* adapters, int32_t K,
+                             int32_t N) {
+  for (int t = 0; t < num_adapters; ++t) {
+    const mux_adapter& a = adapters[t];
+    if (a.rank == 0) continue;
+    const int ldb = a.ldb == 0 ? a.rank : a.ldb;
+    if (!make_map(&p.map_lora_a[t], a.A, K, a.rank, K, 64, 64))
+      return fail(MUX_ERR_CUDA, "cuTensorMapEncodeTiled failed for adapter %d A", t);
+    if (!make_map(&p.map_lora_b[t], a.B, a.rank, N, ldb, 64, 64))
+      return fail(MUX_ERR_CUDA, "cuTensorMapEncodeTiled failed for adapter %d B", t);
+  }
+  return MUX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* mux_last_error(void) { return g_err.c_str(); }
+
+const char* mux_version(void) { return "mux 0.1 sm_100a (tcgen05/TMEM/TMA)"; }
+
+int64_t mux_pack_bound_rows(int64_t total_tokens, int32_t num_seqs, int32_t chunk_size_or_max) {
+  if (total_tokens < 0 || num_seqs < 0 || chunk_size_or_max < 1) return -1;
+  // every sequence in its own pack, rounded up to the chunk: < total + num_seqs * c
+  return total_tokens + static_cast<int64_t>(num_seqs) * chunk_size_or_max;
+}
+
+size_t mux_pack_workspace_size(int32_t num_tasks, int32_t num_seqs) {
+  return pack_workspace_bytes(num_tasks, num_seqs);
+}
+
+mux_status mux_pack_chunks(int32_t num_tasks, int32_t num_seqs, const int32_t* task_seq_off,
+                           const int32_t* seq_len, const int32_t* pack_capacity, int32_t chunk_size,
+                           int32_t chunk_min, int32_t max_rows, int32_t max_chunks, int32_t* seg_off,
+                           int32_t* seq_row, int32_t* chunk_task, int32_t* chunk_pack, int32_t* chunk_valid,
+                           int32_t* chunk_dep, int32_t* row_src, mux_pack_info* info, void* workspace,
+                           size_t workspace_bytes, cudaStream_t stream) {
+  if (num_tasks < 1) return fail(MUX_ERR_INVALID_ARGUMENT, "num_tasks=%d must be >= 1", num_tasks);
+  if (num_seqs < 0) return fail(MUX_ERR_INVALID_ARGUMENT, "num_seqs=%d must be >= 0", num_seqs);
+  if (chunk_min < 64 || (chunk_min & (chunk_min - 1)))
+    return fail(MUX_ERR_INVALID_ARGUMENT, "chunk_min=%d must be a power of two >= 64", chunk_min);
+  if (chunk_size != 0 && (chunk_size < 64 || (chunk_size & (chunk_size - 1))))
+    return fail(MUX_ERR_INVALID_ARGUMENT, "chunk_size=%d must be 0 or a power of two >= 64", chunk_size);
+  if (max_rows < 0 || max_chunks < 0) return fail(MUX_ERR_INVALID_ARGUMENT, "negative capacity");
+  if (!task_seq_off || (num_seqs > 0 && !seq_len) || !seg_off || !info)
+    return fail(MUX_ERR_INVALID_ARGUMENT, "null required pointer");
+  if (num_seqs > 0 && (!seq_row || !chunk_task || !chunk_pack || !chunk_valid || !chunk_dep))
+    return fail(MUX_ERR_INVALID_ARGUMENT, "null output pointer");
+  if (max_rows > 0 && !row_src) return fail(MUX_ERR_INVALID_ARGUMENT, "null row_src");
+  const size_t need = pack_workspace_bytes(num_tasks, num_seqs);
+  if (!workspace || workspace_bytes < need)
+    return fail(MUX_ERR_INSUFFICIENT_BUFFER, "pack workspace %zu < %zu bytes", workspace_bytes, need);
+  cudaError_t e = launch_pack(num_tasks, num_seqs, task_seq_off, seq_len, pack_capacity, chunk_size, chunk_min,
+                              max_rows, max_chunks, seg_off, seq_row, chunk_task, chunk_pack, chunk_valid,
+                              chunk_dep, row_src, info, workspace, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "mux_pack_chunks launch");
+  return MUX_OK;
+}
+
+mux_status mux_pack_apply(int32_t max_rows, int32_t cols, int32_t num_tokens, const int32_t* row_src,
+                          const __nv_bfloat16* src, __nv_bfloat16* dst, cudaStream_t stream) {
+  if (max_rows < 0 || cols < 8 || (cols % 8) || num_tokens < 0)
+    return fail(MUX_ERR_INVALID_ARGUMENT, "bad shape max_rows=%d cols=%d num_tokens=%d", max_rows, cols,
+                num_tokens);
+  if (max_rows == 0) return MUX_OK;
+  if (!row_src || !dst || (num_tokens > 0 && !src)) return fail(MUX_ERR_INVALID_ARGUMENT, "null pointer");
+  if (!aligned16(src) || !aligned16(dst)) return fail(MUX_ERR_INVALID_ARGUMENT, "src/dst not 16-byte aligned");
+  cudaError_t e = launch_pack_apply(max_rows, cols, num_tokens, row_src, src, dst, num_sms(), stream);
+  if (e != cudaSuccess) return cuda_fail(e, "mux_pack_apply launch");
+  return MUX_OK;
+}
+
+size_t mux_linear_workspace_size(int32_t num_segs, int32_t max_rows, int32_t K, int32_t N, int32_t r_cap) {
+  (void)num_segs;
+  (void)K;
+  (void)N;
+  if (max_rows < 0 || r_cap < 0) return 0;
+  return carve_linear_ws(nullptr, max_rows, r_cap).bytes;
+}
+
+static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_off, const int32_t* seg_task,
+                                int32_t num_adapters, const mux_adapter* adapters, int32_t max_rows, int32_t K,
+                                int32_t N, int32_t r_cap, const __nv_bfloat16* a_in /*X or dY*/,
+                                const __nv_bfloat16* X, const __nv_bfloat16* W, __nv_bfloat16* out /*Y or dX*/,
+                                const __nv_bfloat16* Hs_in, __nv_bfloat16* Hs_out, void* workspace,
+                                size_t workspace_bytes, cudaStream_t stream) {
+  mux_status st = validate_linear(num_segs, seg_off, seg_task, num_adapters, adapters, max_rows, K, N, r_cap);
+  if (st != MUX_OK) return st;
+  if (!a_in || !W) return fail(MUX_ERR_INVALID_ARGUMENT, "null input pointer");
+  if (!aligned16(a_in) || !aligned16(W) || (out && !aligned16(out)) || (X && !aligned16(X)) ||
+      (Hs_in && !aligned16(Hs_in)) || (Hs_out && !aligned16(Hs_out)))
+    return fail(MUX_ERR_INVALID_ARGUMENT, "tensor pointers must be 16-byte aligned");
+  if (bwd && (!X || !Hs_in)) return fail(MUX_ERR_INVALID_ARGUMENT, "bwd needs X and Hs");
+  if (!bwd && !out) return fail(MUX_ERR_INVALID_ARGUMENT, "fwd needs Y");
+  const LinearWs need = carve_linear_ws(nullptr, max_rows, r_cap);
+  if (!workspace || workspace_bytes < need.bytes)
+    return fail(MUX_ERR_INSUFFICIENT_BUFFER, "linear workspace %zu < %zu bytes", workspace_bytes, need.bytes);
+  if (!aligned16(workspace)) return fail(MUX_ERR_INVALID_ARGUMENT, "workspace not 16-byte aligned");
+  const LinearWs ws = carve_linear_ws(workspace, max_rows, r_cap);
+
+  static thread_local GemmParams p;  // ~17 KB: keep it off the stack
+  std::memset(&p, 0, sizeof(p));
+  const int kred = bwd ? N : K;
+  const int nout = bwd ? K : N;
+  __nv_bfloat16* side = bwd ? ws.gs : (Hs_out ? Hs_out : ws.hs);
+  if (!make_map(&p.map_a, a_in, kred, max_rows, kred, 64, 128) || !make_map(&p.map_w, W, K, N, K, 64, 64) ||
+      !make_map(&p.map_side, side, r_cap, max_rows, r_cap, 64, 128) ||
+      (out && !make_map(&p.map_out, out, nout, max_rows, nout, 64, 32)))
+    return fail(MUX_ERR_CUDA, "cuTensorMapEncodeTiled failed (driver entry point missing?)");
+  st = fill_adapter_maps(p, num_adapters, adapters, K, N);
+  if (st != MUX_OK) return st;
+  p.seg_off = seg_off;
+  p.side_out = side;
+  p.flags = ws.flags;
+  p.num_segs = num_segs;
+  p.max_rows = max_rows;
+  p.kred = kred;
+  p.nout = nout;
+  p.r_cap = r_cap;
+  p.has_main = out != nullptr;
+  for (int s = 0; s < num_segs; ++s) {
+    const mux_adapter& a = adapters[seg_task[s]];
+    p.seg_adapter[s] = seg_task[s];
+    p.seg_rank[s] = a.rank;
+    p.seg_scale[s] = a.scale;
+  }
+  const int num_m_max = (max_rows + kBM - 1) / kBM;
+  const int num_n = (nout + kBN - 1) / kBN;
+  const long long tiles_max = static_cast<long long>(num_m_max) * (1 + (p.has_main ? num_n : 0));
+  const int grid = static_cast<int>(tiles_max < num_sms() ? tiles_max : num_sms());
+  cudaError_t e = cudaMemsetAsync(ws.flags, 0, sizeof(int32_t) * num_m_max, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "flag reset");
+  e = launch_gemm(p, bwd, grid, stream);
+  if (e != cudaSuccess) return cuda_fail(e, bwd ? "mux_linear_bwd dX launch" : "mux_linear_fwd launch");
+
+  if (bwd) {
+    static thread_local GradParams g;
+    std::memset(&g, 0, sizeof(g));
+    if (!make_map(&g.map_x, X, K, max_rows, K, 64, 128) || !make_map(&g.map_dy, a_in, N, max_rows, N, 64, 128) ||
+        !make_map(&g.map_hs, Hs_in, r_cap, max_rows, r_cap, 64, 128) ||
+        !make_map(&g.map_gs, ws.gs, r_cap, max_rows, r_cap, 64, 128))
+      return fail(MUX_ERR_CUDA, "cuTensorMapEncodeTiled failed (grad)");
+    g.seg_off = seg_off;
+    g.num_segs = num_segs;
+    g.K = K;
+    g.N = N;
+    g.r_cap = r_cap;
+    bool want_a = false, want_b = false;
+    int nt = 0;
+    for (int t = 0; t < num_adapters; ++t) {
+      const mux_adapter& a = adapters[t];
+      if (a.rank == 0 || (!a.dA && !a.dB)) continue;
+      uint64_t segs = 0;
+      for (int s = 0; s < num_segs; ++s)
+        if (seg_task[s] == t) segs |= 1ull << s;
+      g.task_segs[nt] = segs;
+      g.task_rank[nt] = a.rank;
+      g.task_dA[nt] = a.dA;
+      g.task_dB[nt] = a.dB;
+      want_a |= a.dA != nullptr;
+      want_b |= a.dB != nullptr;
+      ++nt;
+    }
+    g.num_tasks = nt;
+    g.units_a = want_a ? (K + kGradBM - 1) / kGradBM : 0;
+    g.units_b = want_b ? (N + kGradBM - 1) / kGradBM : 0;
+    const long long units = static_cast<long long>(nt) * (g.units_a + g.units_b);
+    if (units > 0) {
+      const int ggrid = static_cast<int>(units < num_sms() ? units : num_sms());
+      e = launch_grad(g, ggrid, stream);
+      if (e != cudaSuccess) return cuda_fail(e, "mux_linear_bwd grad launch");
+    }
+  }
+  return MUX_OK;
+}
+
+mux_status mux_linear_fwd(int32_t num_segs, const int32_t* seg_off, const int32_t* seg_task,
+                          int32_t num_adapters, const mux_adapter* adapters, int32_t max_rows, int32_t K, int32_t N,
+                          int32_t r_cap, const __nv_bfloat16* X, const __nv_bfloat16* W, __nv_bfloat16* Y,
+                          __nv_bfloat16* Hs, void* workspace, size_t workspace_bytes, cudaStream_t stream) {
+  return linear_common(false, num_segs, seg_off, seg_task, num_adapters, adapters, max_rows, K, N, r_cap, X, X, W,
+                       Y, nullptr, Hs, workspace, workspace_bytes, stream);
+}
+
+mux_status mux_linear_bwd(int32_t num_segs, const int32_t* seg_off, const int32_t* seg_task,
+                          int32_t num_adapters, const mux_adapter* adapters, int32_t max_rows, int32_t K, int32_t N,
+                          int32_t r_cap, const __nv_bfloat16* dY, const __nv_bfloat16* X, const __nv_bfloat16* W,
+                          const __nv_bfloat16* Hs, __nv_bfloat16* dX, void* workspace, size_t workspace_bytes,
+                          cudaStream_t stream) {
+  return linear_common(true, num_segs, seg_off, seg_task, num_adapters, adapters, max_rows, K, N, r_cap, dY, X, W,
+                       dX, Hs, nullptr, workspace, workspace_bytes, stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,340 @@
+// pack.cu — chunk-based data alignment (§3.5) as one integer kernel,
+// plus the Dispatch gather (token-major rows -> packed rows).
+//
+// mux_pack_kernel runs as a single 1024-thread CTA (the problem is tiny and
+// latency-bound: tens to thousands of sequences; one CTA avoids grid-wide
+// syncs and keeps every intermediate in L1/L2):
+//   1. chunk size  c = max(chunk_min, 2^{min_s v2(len_s)}) — block min-reduce
+//                  of __ffs(len)-1, or the caller's chunk_size;
+//   2. per-task order: rank of each sequence in (len desc, index asc) order
+//      (counting sort by comparison, all sequences in parallel);
+//   3. per-task first-fit decreasing: one warp per task; the first pack
+//      with room is found 32 packs at a time with __ballot_sync;
+//   4. chunk counts ceil(L_p / c) -> per-task scan -> seg_off, pack rows;
+//   5. fill: chunk table with KV-reuse links, seq_row, row_src.
+// Integer results are bit-exact with the fp64 oracle's pack (tests/test_gpu_pack.py).
+#include "common.h"
+#include "ptx.cuh"
+
+namespace mux {
+
+constexpr int kPackThreads = 1024;
+constexpr int kPackWarps = kPackThreads / 32;
+
+struct PackWs {  // carved from the caller's workspace
+  int32_t* order;       // [num_seqs] local index of the r-th sequence of its task in FFD order
+  int32_t* pack_of;     // [num_seqs]
+  int32_t* pack_off;    // [num_seqs] offset of the sequence inside its pack
+  int32_t* residual;    // [num_seqs] per-task packs at [task_seq_off[t] .. ) : residual capacity
+  int32_t* pack_len;    // [num_seqs] same indexing: pack length
+  int32_t* pack_row0;   // [num_seqs] same indexing: first row of the pack
+  int32_t* tok_off;     // [num_seqs + 1] exclusive prefix of lengths
+  int32_t* task_packs;  // [M]
+  int32_t* task_chunks; // [M]
+};
+
+__host__ __device__ inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+__host__ __device__ inline size_t pack_ws_bytes(int M, int S) {
+  const size_t s = align256(sizeof(int32_t) * (size_t)(S + 1));
+  return 7 * s + 2 * align256(sizeof(int32_t) * (size_t)(M > 0 ? M : 1));
+}
+
+__device__ inline PackWs carve_pack_ws(void* ws, int M, int S) {
+  uint8_t* b = reinterpret_cast<uint8_t*>(ws);
+  const size_t s = align256(sizeof(int32_t) * (size_t)(S + 1));
+  const size_t m = align256(sizeof(int32_t) * (size_t)(M > 0 ? M : 1));
+  PackWs w;
+  w.order = reinterpret_cast<int32_t*>(b); b += s;
+  w.pack_of = reinterpret_cast<int32_t*>(b); b += s;
+  w.pack_off = reinterpret_cast<int32_t*>(b); b += s;
+  w.residual = reinterpret_cast<int32_t*>(b); b += s;
+  w.pack_len = reinterpret_cast<int32_t*>(b); b += s;
+  w.pack_row0 = reinterpret_cast<int32_t*>(b); b += s;
+  w.tok_off = reinterpret_cast<int32_t*>(b); b += s;
+  w.task_packs = reinterpret_cast<int32_t*>(b); b += m;
+  w.task_chunks = reinterpret_cast<int32_t*>(b);
+  return w;
+}
+
+__device__ __forceinline__ int warp_sum(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ int warp_min(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ int warp_max(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__global__ void __launch_bounds__(kPackThreads, 1)
+    mux_pack_kernel(int M, int S, const int32_t* __restrict__ task_seq_off, const int32_t* __restrict__ seq_len,
+                    const int32_t* __restrict__ pack_capacity, int chunk_size, int chunk_min, int max_rows,
+                    int max_chunks, int32_t* seg_off, int32_t* seq_row, int32_t* chunk_task,
+                    int32_t* chunk_pack, int32_t* chunk_valid, int32_t* chunk_dep, int32_t* row_src,
+                    mux_pack_info* info, void* workspace) {
+  __shared__ int s_red[kPackWarps];
+  __shared__ int s_bad, s_c, s_total_chunks, s_maxlen, s_valid;
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int lane = tid & 31;
+  PackWs ws = carve_pack_ws(workspace, M, S);
+
+  // ---- 1. chunk size, validity, max length, valid rows -------------------
+  int v2min = 30, bad = 0, mx = 0, sum = 0;
+  for (int i = tid; i < S; i += kPackThreads) {
+    const int L = seq_len[i];
+    if (L < 1) bad = 1;
+    else {
+      v2min = min(v2min, __ffs(L) - 1);
+      mx = max(mx, L);
+      sum += L;
+    }
+  }
+  if (tid == 0) { s_bad = 0; s_maxlen = 0; s_valid = 0; }
+  __syncthreads();
+  v2min = warp_min(v2min);
+  if (lane == 0) s_red[warp] = v2min;
+  mx = warp_max(mx);
+  sum = warp_sum(sum);
+  if (lane == 0) { atomicMax(&s_maxlen, mx); atomicAdd(&s_valid, sum); }
+  if (bad) s_bad = 4;
+  __syncthreads();
+  if (warp == 0) {
+    int v = s_red[lane];
+    v = warp_min(v);
+    if (lane == 0) {
+      int c = chunk_size;
+      if (c == 0) c = (S == 0) ? chunk_min : max(chunk_min, 1 << v);
+      s_c = c;
+    }
+  }
+  __syncthreads();
+  const int c = s_c;
+  if (s_bad) {
+    if (tid == 0) {
+      mux_pack_info r{};
+      r.chunk_size = c;
+      r.overflow = s_bad;
+      *info = r;
+    }
+    return;
+  }
+
+  // ---- 2. FFD visit order per task: rank by (len desc, index asc) ---------
+  for (int i = tid; i < S; i += kPackThreads) {
+    // task of sequence i: binary search in task_seq_off
+    int lo = 0, hi = M;  // find t with off[t] <= i < off[t+1]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (task_seq_off[mid] <= i) lo = mid; else hi = mid;
+    }
+    const int t0 = task_seq_off[lo], t1 = task_seq_off[lo + 1];
+    const int L = seq_len[i];
+    int rank = 0;
+    for (int j = t0; j < t1; ++j) {
+      const int Lj = seq_len[j];
+      rank += (Lj > L) || (Lj == L && j < i);
+    }
+    ws.order[t0 + rank] = i - t0;
+  }
+  __syncthreads();
+
+  // ---- 3. first-fit decreasing, one warp per task -------------------------
+  for (int t = warp; t < M; t += kPackWarps) {
+    const int t0 = task_seq_off[t], n = task_seq_off[t + 1] - t0;
+    int mxl = 0;
+    for (int i = lane; i < n; i += 32) mxl = max(mxl, seq_len[t0 + i]);
+    mxl = warp_max(mxl);
+    int cap;
+    if (pack_capacity != nullptr) cap = pack_capacity[t];
+    else cap = ((max(mxl, c) + c - 1) / c) * c;
+    if (n > 0 && cap < mxl) {
+      if (lane == 0) atomicOr(&s_bad, 4);
+      continue;
+    }
+    int* resid = ws.residual + t0;
+    int npacks = 0;
+    for (int r = 0; r < n; ++r) {
+      const int li = ws.order[t0 + r];
+      const int L = seq_len[t0 + li];
+      int found = -1;
+      for (int base = 0; base < npacks && found < 0; base += 32) {
+        const int p = base + lane;
+        const bool fits = p < npacks && resid[p] >= L;
+        const unsigned bal = __ballot_sync(0xffffffffu, fits);
+        if (bal) found = base + __ffs(bal) - 1;
+      }
+      if (found < 0) {
+        found = npacks++;
+        if (lane == 0) resid[found] = cap;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        ws.pack_of[t0 + li] = found;
+        ws.pack_off[t0 + li] = cap - resid[found];
+        resid[found] -= L;
+      }
+      __syncwarp();
+    }
+    // pack lengths and chunk counts
+    int nch = 0;
+    for (int p = lane; p < npacks; p += 32) {
+      const int len = cap - resid[p];
+      ws.pack_len[t0 + p] = len;
+      nch += (len + c - 1) / c;
+    }
+    nch = warp_sum(nch);
+    if (lane == 0) {
+      ws.task_packs[t] = npacks;
+      ws.task_chunks[t] = nch;
+    }
+  }
+  __syncthreads();
+  if (s_bad) {
+    if (tid == 0) {
+      mux_pack_info r{};
+      r.chunk_size = c;
+      r.overflow = s_bad;
+      *info = r;
+    }
+    return;
+  }
+
+  // ---- 4. scan over tasks -> seg_off; overflow check ----------------------
+  if (tid == 0) {
+    int acc = 0, packs = 0;
+    for (int t = 0; t < M; ++t) {  // exclusive prefix of chunk counts
+      const int x = ws.task_chunks[t];
+      ws.task_chunks[t] = acc;
+      acc += x;
+      packs += ws.task_packs[t];
+    }
+    s_total_chunks = acc;
+
+    int ovf = 0;
+    if (acc * c > max_rows) ovf |= 1;
+    if (acc > max_chunks) ovf |= 2;
+    mux_pack_info r;
+    r.chunk_size = c;
+    r.num_chunks = acc;
+    r.num_packs = packs;
+    r.total_rows = acc * c;
+    r.valid_rows = s_valid;
+    r.zero_pad_rows = S * s_maxlen;
+    r.overflow = ovf;
+    *info = r;
+    s_bad = ovf;
+  }
+  __syncthreads();
+  if (s_bad) return;
+  const int total_chunks = s_total_chunks;
+  for (int t = tid; t <= M; t += kPackThreads) seg_off[t] = (t < M ? ws.task_chunks[t] : total_chunks) * c;
+
+  // per-task pack rows (serial over a task's packs; one warp per task)
+  for (int t = warp; t < M; t += kPackWarps) {
+    if (lane == 0) {
+      const int t0 = task_seq_off[t];
+      int ch = ws.task_chunks[t];
+      for (int p = 0; p < ws.task_packs[t]; ++p) {
+        ws.pack_row0[t0 + p] = ch * c;
+        ch += (ws.pack_len[t0 + p] + c - 1) / c;
+      }
+    }
+  }
+  // token offsets: exclusive prefix over all sequences (warp 0, 32 at a time)
+  if (warp == 0) {
+    int run = 0;
+    for (int base = 0; base < S; base += 32) {
+      const int i = base + lane;
+      int v = i < S ? seq_len[i] : 0;
+      int x = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (i < S) ws.tok_off[i] = run + x - v;
+      run += __shfl_sync(0xffffffffu, x, 31);
+    }
+  }
+  for (int r = tid; r < max_rows; r += kPackThreads) row_src[r] = -1;
+  __syncthreads();
+
+  // ---- 5. fill ------------------------------------------------------------
+  // chunk table: one thread per (task, pack)
+  for (int t = 0; t < M; ++t) {
+    const int t0 = task_seq_off[t];
+    for (int p = tid; p < ws.task_packs[t]; p += kPackThreads) {
+      const int len = ws.pack_len[t0 + p];
+      const int n_p = (len + c - 1) / c;
+      const int id0 = ws.pack_row0[t0 + p] / c;
+      for (int j = 0; j < n_p; ++j) {
+        chunk_task[id0 + j] = t;
+        chunk_pack[id0 + j] = p;
+        chunk_valid[id0 + j] = min(c, len - j * c);
+        chunk_dep[id0 + j] = j > 0 ? id0 + j - 1 : -1;
+      }
+    }
+  }
+  // seq_row and row_src: one warp per sequence
+  for (int t = 0; t < M; ++t) {
+    const int t0 = task_seq_off[t], t1 = task_seq_off[t + 1];
+    for (int s = t0 + warp; s < t1; s += kPackWarps) {
+      const int row = ws.pack_row0[t0 + ws.pack_of[s]] + ws.pack_off[s];
+      if (lane == 0) seq_row[s] = row;
+      const int L = seq_len[s];
+      const int tok = ws.tok_off[s];
+      for (int pos = lane; pos < L; pos += 32) row_src[row + pos] = tok + pos;
+    }
+  }
+}
+
+// Dispatch gather: 16-byte vectors, one warp-row at a time.
+__global__ void mux_pack_apply_kernel(int max_rows, int cols, int num_tokens, const int32_t* __restrict__ row_src,
+                                      const uint4* __restrict__ src, uint4* __restrict__ dst) {
+  const int vec_per_row = cols / 8;
+  const long long total = static_cast<long long>(max_rows) * vec_per_row;
+  for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(idx / vec_per_row);
+    const int v = static_cast<int>(idx - static_cast<long long>(r) * vec_per_row);
+    const int s = row_src[r];
+    uint4 val = make_uint4(0u, 0u, 0u, 0u);
+    if (s >= 0 && s < num_tokens) val = src[static_cast<long long>(s) * vec_per_row + v];
+    dst[idx] = val;
+  }
+}
+
+size_t pack_workspace_bytes(int M, int S) { return pack_ws_bytes(M, S); }
+
+cudaError_t launch_pack(int M, int S, const int32_t* task_seq_off, const int32_t* seq_len,
+                        const int32_t* pack_capacity, int chunk_size, int chunk_min, int max_rows, int max_chunks,
+                        int32_t* seg_off, int32_t* seq_row, int32_t* chunk_task, int32_t* chunk_pack,
+                        int32_t* chunk_valid, int32_t* chunk_dep, int32_t* row_src, mux_pack_info* info,
+                        void* workspace, cudaStream_t stream) {
+  mux_pack_kernel<<<1, kPackThreads, 0, stream>>>(M, S, task_seq_off, seq_len, pack_capacity, chunk_size,
+                                                  chunk_min, max_rows, max_chunks, seg_off, seq_row, chunk_task,
+                                                  chunk_pack, chunk_valid, chunk_dep, row_src, info, workspace);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_apply(int max_rows, int cols, int num_tokens, const int32_t* row_src,
+                              const __nv_bfloat16* src, __nv_bfloat16* dst, int num_sms, cudaStream_t stream) {
+  const long long total = static_cast<long long>(max_rows) * (cols / 8);
+  if (total == 0) return cudaSuccess;
+  long long blocks = (total + 255) / 256;
+  const long long cap = static_cast<long long>(num_sms) * 8;
+  if (blocks > cap) blocks = cap;
+  mux_pack_apply_kernel<<<static_cast<int>(blocks), 256, 0, stream>>>(
+      max_rows, cols, num_tokens, row_src, reinterpret_cast<const uint4*>(src), reinterpret_cast<uint4*>(dst));
+  return cudaGetLastError();
+}
+
+}  // namespace mux

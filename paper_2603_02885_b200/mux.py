@@ -1,0 +1,262 @@
+"""Thin Python binding of libmux (include/mux.h) — argument marshalling only.
+
+torch is used for device memory and the current stream; every step of the
+path runs in libmux's CUDA kernels.  There is no fallback: if libmux.so is
+missing or the GPU path fails, these functions raise.
+
+Names follow mux.h: pack_chunks, pack_apply, linear_fwd, linear_bwd.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+from typing import List, Optional, Sequence
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmux.so")
+
+MUX_OK = 0
+STATUS = {0: "MUX_OK", 1: "MUX_ERR_INVALID_ARGUMENT", 2: "MUX_ERR_UNSUPPORTED",
+          3: "MUX_ERR_INSUFFICIENT_BUFFER", 4: "MUX_ERR_CUDA"}
+MAX_SEGMENTS = 64
+MAX_ADAPTERS = 64
+
+EXPORTS = ("mux_last_error", "mux_version", "mux_pack_bound_rows", "mux_pack_workspace_size",
+           "mux_pack_chunks", "mux_pack_apply", "mux_linear_workspace_size", "mux_linear_fwd",
+           "mux_linear_bwd")
+
+
+class MuxError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class PackInfo(ctypes.Structure):
+    _fields_ = [("chunk_size", ctypes.c_int32), ("num_chunks", ctypes.c_int32),
+                ("num_packs", ctypes.c_int32), ("total_rows", ctypes.c_int32),
+                ("valid_rows", ctypes.c_int32), ("zero_pad_rows", ctypes.c_int32),
+                ("overflow", ctypes.c_int32)]
+
+
+PACK_INFO_FIELDS = [f[0] for f in PackInfo._fields_]
+
+
+class _Adapter(ctypes.Structure):
+    _fields_ = [("A", ctypes.c_void_p), ("B", ctypes.c_void_p), ("dA", ctypes.c_void_p),
+                ("dB", ctypes.c_void_p), ("rank", ctypes.c_int32), ("ldb", ctypes.c_int32),
+                ("scale", ctypes.c_float)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libmux.so (raises if it has not been built: no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"libmux.so not found at {LIB_PATH}: run __graft_entry__.build() "
+                               "(python -m paper_2603_02885_b200.build)")
+        L = ctypes.CDLL(LIB_PATH)
+        P, I32, I64, SZ = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
+        L.mux_last_error.restype = ctypes.c_char_p
+        L.mux_version.restype = ctypes.c_char_p
+        L.mux_pack_bound_rows.restype = I64
+        L.mux_pack_bound_rows.argtypes = [I64, I32, I32]
+        L.mux_pack_workspace_size.restype = SZ
+        L.mux_pack_workspace_size.argtypes = [I32, I32]
+        L.mux_pack_chunks.restype = ctypes.c_int
+        L.mux_pack_chunks.argtypes = [I32, I32, P, P, P, I32, I32, I32, I32, P, P, P, P, P, P, P, P, P, SZ, P]
+        L.mux_pack_apply.restype = ctypes.c_int
+        L.mux_pack_apply.argtypes = [I32, I32, I32, P, P, P, P]
+        L.mux_linear_workspace_size.restype = SZ
+        L.mux_linear_workspace_size.argtypes = [I32, I32, I32, I32, I32]
+        L.mux_linear_fwd.restype = ctypes.c_int
+        L.mux_linear_fwd.argtypes = [I32, P, P, I32, P, I32, I32, I32, I32, P, P, P, P, P, SZ, P]
+        L.mux_linear_bwd.restype = ctypes.c_int
+        L.mux_linear_bwd.argtypes = [I32, P, P, I32, P, I32, I32, I32, I32, P, P, P, P, P, P, SZ, P]
+        _lib = L
+    return _lib
+
+
+def version() -> str:
+    return lib().mux_version().decode()
+
+
+def _check(status: int):
+    if status != MUX_OK:
+        raise MuxError(status, lib().mux_last_error().decode())
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _dev_i32(x, device) -> torch.Tensor:
+    if isinstance(x, torch.Tensor):
+        assert x.dtype == torch.int32 and x.is_contiguous()
+        return x.to(device)
+    return torch.as_tensor(list(x), dtype=torch.int32, device=device)
+
+
+# ---------------------------------------------------------------- packing
+def pack_bound_rows(total_tokens: int, num_seqs: int, chunk_size_or_max: int) -> int:
+    return int(lib().mux_pack_bound_rows(total_tokens, num_seqs, chunk_size_or_max))
+
+
+def pack_chunks(task_seq_off, seq_len, pack_capacity=None, chunk_size: int = 0, chunk_min: int = 64,
+                max_rows: int = None, max_chunks: int = None, device="cuda", stream=None, out=None):
+    """mux_pack_chunks.  task_seq_off/seq_len/pack_capacity: int32 device tensors
+    (or host sequences, copied).  Returns a dict of device tensors; info is a
+    device int32 tensor of PACK_INFO_FIELDS (read it with read_info())."""
+    tso = _dev_i32(task_seq_off, device)
+    sl = _dev_i32(seq_len, device)
+    pc = None if pack_capacity is None else _dev_i32(pack_capacity, device)
+    M = tso.numel() - 1
+    S = sl.numel()
+    if max_rows is None or max_chunks is None:
+        raise ValueError("max_rows and max_chunks are required (host never reads device data)")
+    if out is None:
+        out = alloc_pack_outputs(M, S, max_rows, max_chunks, device)
+    o = out
+    _check(lib().mux_pack_chunks(M, S, _ptr(tso), _ptr(sl), _ptr(pc), chunk_size, chunk_min, max_rows,
+                                 max_chunks, _ptr(o["seg_off"]), _ptr(o["seq_row"]), _ptr(o["chunk_task"]),
+                                 _ptr(o["chunk_pack"]), _ptr(o["chunk_valid"]), _ptr(o["chunk_dep"]),
+                                 _ptr(o["row_src"]), _ptr(o["info"]), _ptr(o["workspace"]),
+                                 o["workspace"].numel(), _stream(stream)))
+    return o
+
+
+def alloc_pack_outputs(M: int, S: int, max_rows: int, max_chunks: int, device="cuda"):
+    i32 = dict(dtype=torch.int32, device=device)
+    ws = int(lib().mux_pack_workspace_size(M, S))
+    return {"seg_off": torch.empty(M + 1, **i32), "seq_row": torch.empty(max(S, 1), **i32),
+            "chunk_task": torch.empty(max(max_chunks, 1), **i32),
+            "chunk_pack": torch.empty(max(max_chunks, 1), **i32),
+            "chunk_valid": torch.empty(max(max_chunks, 1), **i32),
+            "chunk_dep": torch.empty(max(max_chunks, 1), **i32),
+            "row_src": torch.empty(max(max_rows, 1), **i32),
+            "info": torch.empty(len(PACK_INFO_FIELDS), **i32),
+            "workspace": torch.empty(ws, dtype=torch.uint8, device=device)}
+
+
+def read_info(info: torch.Tensor) -> dict:
+    v = info.cpu().tolist()
+    return dict(zip(PACK_INFO_FIELDS, v))
+
+
+def pack_apply(row_src: torch.Tensor, src: torch.Tensor, max_rows: int, out: torch.Tensor = None,
+               stream=None) -> torch.Tensor:
+    """mux_pack_apply: packed[r] = src[row_src[r]] or 0."""
+    assert src.dtype == torch.bfloat16 and src.is_contiguous() and src.dim() == 2
+    cols = src.shape[1]
+    if out is None:
+        out = torch.empty(max_rows, cols, dtype=torch.bfloat16, device=src.device)
+    _check(lib().mux_pack_apply(max_rows, cols, src.shape[0], _ptr(row_src), _ptr(src), _ptr(out),
+                                _stream(stream)))
+    return out
+
+
+# ---------------------------------------------------------------- linear
+@dataclass
+class Adapter:
+    """One task's LoRA adapter on one linear layer.  B is stored with a leading
+    dimension that is a multiple of 8 (TMA needs 16-byte rows): `B` is the
+    [N, rank] view of that padded storage, so no copy happens per call."""
+    A: Optional[torch.Tensor]          # [rank, K] bf16
+    B: Optional[torch.Tensor]          # [N, rank] bf16 view, row stride ldb
+    rank: int
+    scale: float
+    dA: Optional[torch.Tensor] = None  # [rank, K] fp32
+    dB: Optional[torch.Tensor] = None  # [N, rank] fp32
+
+    @property
+    def ldb(self) -> int:
+        if self.B is None or self.rank == 0:
+            return 0
+        return int(self.B.stride(0))
+
+
+def make_B_storage(N: int, rank: int, device="cuda") -> torch.Tensor:
+    """Zeroed [N, rank] bf16 view over [N, round_up(rank, 8)] storage."""
+    ld = max(8, -(-rank // 8) * 8)
+    return torch.zeros(N, ld, dtype=torch.bfloat16, device=device)[:, :rank]
+
+
+def _adapter_table(adapters: Sequence[Adapter], want_grads: bool):
+    tab = (_Adapter * len(adapters))()
+    for i, a in enumerate(adapters):
+        tab[i].A = a.A.data_ptr() if (a.A is not None and a.rank > 0) else None
+        tab[i].B = a.B.data_ptr() if (a.B is not None and a.rank > 0) else None
+        tab[i].dA = a.dA.data_ptr() if (want_grads and a.dA is not None) else None
+        tab[i].dB = a.dB.data_ptr() if (want_grads and a.dB is not None) else None
+        tab[i].rank = a.rank
+        tab[i].ldb = a.ldb
+        tab[i].scale = float(a.scale)
+    return tab
+
+
+def linear_workspace_size(num_segs: int, max_rows: int, K: int, N: int, r_cap: int) -> int:
+    return int(lib().mux_linear_workspace_size(num_segs, max_rows, K, N, r_cap))
+
+
+def _i32_host(seq_task):
+    arr = (ctypes.c_int32 * len(seq_task))(*[int(x) for x in seq_task])
+    return arr
+
+
+def linear_fwd(seg_off: torch.Tensor, seg_task: Sequence[int], adapters: Sequence[Adapter],
+               X: torch.Tensor, W: torch.Tensor, r_cap: int, Y: torch.Tensor = None,
+               Hs: torch.Tensor = None, workspace: torch.Tensor = None, want_hs: bool = True, stream=None):
+    """mux_linear_fwd.  Returns (Y, Hs)."""
+    max_rows, K = X.shape
+    N = W.shape[0]
+    dev = X.device
+    if Y is None:
+        Y = torch.empty(max_rows, N, dtype=torch.bfloat16, device=dev)
+    if Hs is None and want_hs:
+        Hs = torch.empty(max_rows, r_cap, dtype=torch.bfloat16, device=dev)
+    S = len(seg_task)
+    if workspace is None:
+        workspace = torch.empty(linear_workspace_size(S, max_rows, K, N, r_cap), dtype=torch.uint8, device=dev)
+    tab = _adapter_table(adapters, False)
+    st = _i32_host(seg_task)
+    _check(lib().mux_linear_fwd(S, _ptr(seg_off), st, len(adapters), tab, max_rows, K, N, r_cap,
+                                _ptr(X), _ptr(W), _ptr(Y), _ptr(Hs), _ptr(workspace), workspace.numel(),
+                                _stream(stream)))
+    return Y, Hs
+
+
+def linear_bwd(seg_off: torch.Tensor, seg_task: Sequence[int], adapters: Sequence[Adapter],
+               dY: torch.Tensor, X: torch.Tensor, W: torch.Tensor, Hs: torch.Tensor, r_cap: int,
+               dX: torch.Tensor = None, want_dx: bool = True, workspace: torch.Tensor = None, stream=None):
+    """mux_linear_bwd.  Writes adapters[i].dA / .dB (allocated if None); returns dX."""
+    max_rows, K = X.shape
+    N = W.shape[0]
+    dev = X.device
+    if dX is None and want_dx:
+        dX = torch.empty(max_rows, K, dtype=torch.bfloat16, device=dev)
+    for a in adapters:
+        if a.rank > 0:
+            if a.dA is None:
+                a.dA = torch.empty(a.rank, K, dtype=torch.float32, device=dev)
+            if a.dB is None:
+                a.dB = torch.empty(N, a.rank, dtype=torch.float32, device=dev)
+    S = len(seg_task)
+    if workspace is None:
+        workspace = torch.empty(linear_workspace_size(S, max_rows, K, N, r_cap), dtype=torch.uint8, device=dev)
+    tab = _adapter_table(adapters, True)
+    st = _i32_host(seg_task)
+    _check(lib().mux_linear_bwd(S, _ptr(seg_off), st, len(adapters), tab, max_rows, K, N, r_cap,
+                                _ptr(dY), _ptr(X), _ptr(W), _ptr(Hs), _ptr(dX), _ptr(workspace),
+                                workspace.numel(), _stream(stream)))
+    return dX

@@ -1,0 +1,100 @@
+"""GPU parity: mux_linear_fwd / mux_linear_bwd (through the C ABI) vs the fp64 oracle.
+
+Bar (north_star): max|gpu - oracle| / max|oracle| <= 2e-2 per tensor; integer
+inputs bit-exact.  Shapes span several 128x256 tiles, ragged tails, 64-row
+segments straddling 128-row tiles (two tasks in one tile), ranks 4..64 and 0,
+empty segments, a task owning two segments, NaN isolation.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from gpu_harness import Problem, compare, bf16_to_f64, TOL  # noqa: E402
+
+
+def _run(prob, rows=None, exact=False, bwd=True):
+    gpu = prob.run_gpu(bwd=bwd)
+    ref = prob.run_oracle(bwd=bwd, rows=rows)
+    return compare(prob, gpu, ref, rows=rows, exact=exact)
+
+
+def test_config1_shape():
+    """Config 1: d=256->256, 2 tasks rank 8, 64 tokens each."""
+    errs = _run(Problem(256, 256, [64, 64], [8, 8], seed=11))
+    print(errs)
+
+
+def test_integer_exact_single_task():
+    _run(Problem(256, 256, [128], [16], variant="int", scales=[2.0], seed=12), exact=True)
+
+
+def test_integer_exact_straddle():
+    """64-row segments: tiles 0 and 1 each hold two tasks (lane-masked adapter MMAs)."""
+    p = Problem(512, 768, [64, 128, 64, 192], [8, 16, 32, 64], variant="int",
+                scales=[1.0, 2.0, 1.0, 2.0], seed=13)
+    _run(p, exact=True)
+
+
+def test_multi_tile_ragged():
+    """Several N tiles with a ragged tail (N = 640 = 2.5 tiles), K not a multiple of 256."""
+    _run(Problem(320, 640, [192, 64, 256], [16, 4, 64], seed=14))
+
+
+def test_heterogeneous_ranks_and_rank0():
+    _run(Problem(256, 512, [128, 64, 64, 128], [4, 0, 48, 8], r_cap=48, seed=15))
+
+
+def test_empty_segment_and_shared_task():
+    """An empty segment (Q16) and task 0 owning two segments."""
+    p = Problem(256, 256, [128, 0, 64, 64], [16, 32], seg_task=[0, 1, 1, 0], seed=16)
+    errs = _run(p)
+    print(errs)
+
+
+def test_empty_task_grads_are_zero():
+    p = Problem(256, 256, [128, 0], [16, 8], seg_task=[0, 1], seed=17)
+    gpu = p.run_gpu()
+    assert np.all(gpu["dA"][1] == 0) and np.all(gpu["dB"][1] == 0)
+
+
+def test_zero_B_backbone():
+    _run(Problem(256, 512, [128, 128], [16, 16], variant="zeroB", seed=18))
+
+
+def test_max_rows_larger_than_rows():
+    """max_rows > seg_off[S]: rows beyond are never written."""
+    p = Problem(256, 256, [64, 64], [8, 8], seed=19, max_rows=384)
+    _run(p)
+
+
+def test_nan_isolation():
+    """NaN in task 1's X rows and in task 2's B never reach other tasks."""
+    p = Problem(256, 512, [64, 64, 128], [8, 16, 8], seed=20)
+    p.X[70, 5] = np.uint16(0x7FC0)               # row of segment 1 (task 1), shares tile 0 with task 0
+    p.B[2][3, 2] = np.uint16(0x7FC0)             # task 2's B
+    gpu = p.run_gpu()
+    Y = bf16_to_f64(gpu["Y"])
+    dX = bf16_to_f64(gpu["dX"])
+    assert np.all(np.isfinite(Y[:64])), "task 0 rows poisoned"
+    assert np.all(np.isfinite(dX[:64]))
+    assert np.all(np.isfinite(gpu["dA"][0])) and np.all(np.isfinite(gpu["dB"][0]))
+    assert np.isnan(Y[70]).any()
+    assert np.isnan(Y[128:]).any()               # task 2 (bad B) is itself affected
+
+
+@pytest.mark.parametrize("K,N", [(4096, 4096), (4096, 11008), (11008, 4096)])
+def test_config2_linears_sampled(K, N):
+    """Config-2 shapes at a reduced token count (full K/N; 4 tasks r=16), with
+    Y/dX compared on a sampled row set; Hs, dA, dB on every row."""
+    lens = [256, 192, 320, 256]
+    p = Problem(K, N, lens, [16] * 4, seed=21)
+    rng = np.random.default_rng(0)
+    rows = np.unique(np.concatenate([np.arange(0, 8), np.arange(p.R - 8, p.R),
+                                     rng.integers(0, p.R, 48)])).astype(np.int64)
+    errs = _run(p, rows=rows)
+    print(errs)
