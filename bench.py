@@ -1,0 +1,453 @@
+#!/usr/bin/env python
+"""bench.py — multiplexed valid tokens/s, fwd+bwd, of MuxTune's hot path on B200.
+
+Workload (BASELINE.json configs[1], "config 2"): LLaMA-7B-shaped decoder
+linears chained as one layer stack 4096->4096 -> 4096->11008 -> 11008->4096,
+4 LoRA tasks rank 16 (s = 2), 8 sequences per task, lengths U{128..512},
+pack capacity 512.  One step = the whole hot path over one batch:
+  mux_pack_chunks (chunk alignment)
+  -> mux_pack_apply (Dispatch of the token-major layer input into packed rows)
+  -> mux_linear_fwd x3 (fused backbone + LoRA, Eq. 1)
+  -> mux_pack_apply (Dispatch of the loss gradient dY)
+  -> mux_linear_bwd x3 (dX with LoRA + dA_t/dB_t, Eq. 2; dX of layer i is
+     dY of layer i-1).
+Metric: valid (non-pad) tokens / s (effective throughput).
+Algorithmic FLOPs per valid token per linear K->N, rank r: 4KN + 6r(K+N).
+
+N > 1 (torchrun): task-sharded replicas ("replicas only" for this path, see
+DESIGN.md §Multi-GPU): every rank runs its own hTask of the same shape with a
+rank-specific seed; no collective in the data path; scaling = weak; value =
+tokens of all ranks / max-over-ranks time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "multiplexed tokens/s fwd+bwd at 1/2/4/8 B200; % of BF16 tensor-core peak"
+UNIT = "tokens/s"
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return {"hbm_gbs": float(d["hbm_gbs"]), "bf16_tflops": float(d["bf16_tflops"]),
+                "bf16_tflops_sustained": float(d.get("bf16_tflops_sustained", d["bf16_tflops"])),
+                "source": "measured"}
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+                "source": "fallback (B200_PROFILING.md)"}
+
+
+def flops_per_token(K, N, r):
+    return 4 * K * N + 6 * r * (K + N)
+
+
+# ------------------------------------------------------------------ workload
+class Workload:
+    def __init__(self, cid="2", rank_seed=0):
+        self.wl = synth.workload(cid)
+        if rank_seed:
+            self.wl.seed = self.wl.seed + 1000 * rank_seed
+            st = synth.Stream(self.wl.seed, first=1000)
+            self.wl.task_lens = [synth.seq_lengths(self.wl.seed, st.take(), len(x), 128, 512)
+                                 for x in self.wl.task_lens]
+        wl = self.wl
+        self.off, self.lens = wl.csr()
+        self.T = wl.valid_tokens
+        self.M = wl.num_tasks
+        self.S = wl.num_seqs
+        self.cap = wl.pack_capacity
+        self.max_cap = max(self.cap) if self.cap else 512
+        self.linears = wl.linears
+        self.flops = sum(flops_per_token(L.K, L.N, max(wl.ranks)) for L in wl.linears) * self.T
+
+    def host_tensors(self):
+        wl = self.wl
+        h = {"X1": synth.token_input(wl, 0, "X", self.linears[0].K),
+             "dY3": synth.token_input(wl, len(self.linears) - 1, "dY", self.linears[-1].N)}
+        for li in range(len(self.linears)):
+            h[f"W{li}"] = synth.weight(wl, li)
+            for t in range(self.M):
+                h[f"A{li}_{t}"], h[f"B{li}_{t}"] = synth.adapter(wl, li, t)
+        return h
+
+
+def _bits_to_dev(bits, torch):
+    return torch.from_numpy(np.ascontiguousarray(bits).view(np.int16)).cuda().view(torch.bfloat16)
+
+
+class MuxStep:
+    """Device-resident buffers + one step of the hot path through the C ABI."""
+
+    def __init__(self, w: Workload, torch, mux):
+        self.w, self.torch, self.mux = w, torch, mux
+        h = w.host_tensors()
+        dev = "cuda"
+        i32 = dict(dtype=torch.int32, device=dev)
+        self.tso = torch.tensor(w.off, **i32)
+        self.sl = torch.tensor(w.lens, **i32)
+        self.cap = torch.tensor(w.cap, **i32) if w.cap else None
+        self.max_rows = int(mux.pack_bound_rows(w.T, w.S, 64))
+        self.max_chunks = self.max_rows // 64
+        self.pk = mux.alloc_pack_outputs(w.M, w.S, self.max_rows, self.max_chunks, dev)
+        self.X1tok = _bits_to_dev(h["X1"], torch)
+        self.dY3tok = _bits_to_dev(h["dY3"], torch)
+        self.r_cap = 16 * -(-max(w.wl.ranks) // 16)
+        self.seg_task = list(range(w.M))
+        self.layers = []
+        for li, L in enumerate(w.linears):
+            ads = []
+            for t in range(w.M):
+                r = w.wl.ranks[t]
+                B = mux.make_B_storage(L.N, r)
+                B.copy_(_bits_to_dev(h[f"B{li}_{t}"], torch))
+                ads.append(mux.Adapter(_bits_to_dev(h[f"A{li}_{t}"], torch), B, r, w.wl.scales[t],
+                                       torch.empty(r, L.K, dtype=torch.float32, device=dev),
+                                       torch.empty(L.N, r, dtype=torch.float32, device=dev)))
+            self.layers.append({
+                "L": L, "W": _bits_to_dev(h[f"W{li}"], torch), "ads": ads,
+                "Y": torch.empty(self.max_rows, L.N, dtype=torch.bfloat16, device=dev),
+                "Hs": torch.empty(self.max_rows, self.r_cap, dtype=torch.bfloat16, device=dev),
+                "dX": torch.empty(self.max_rows, L.K, dtype=torch.bfloat16, device=dev),
+                "ws": torch.empty(mux.linear_workspace_size(w.M, self.max_rows, L.K, L.N, self.r_cap),
+                                  dtype=torch.uint8, device=dev),
+            })
+        self.X1 = torch.empty(self.max_rows, w.linears[0].K, dtype=torch.bfloat16, device=dev)
+        self.dY3 = torch.empty(self.max_rows, w.linears[-1].N, dtype=torch.bfloat16, device=dev)
+        self.launches_per_step = 1 + 2 + len(self.layers) + 2 * len(self.layers)
+        self.fwd_events = None
+
+    def step(self, record=None):
+        mux, w = self.mux, self.w
+        mux.pack_chunks(self.tso, self.sl, self.cap, 0, 64, max_rows=self.max_rows,
+                        max_chunks=self.max_chunks, out=self.pk)
+        seg_off = self.pk["seg_off"]
+        mux.pack_apply(self.pk["row_src"], self.X1tok, self.max_rows, out=self.X1)
+        x = self.X1
+        for li, ly in enumerate(self.layers):
+            if record is not None:
+                record("fwd", li, 0)
+            mux.linear_fwd(seg_off, self.seg_task, ly["ads"], x, ly["W"], self.r_cap, Y=ly["Y"], Hs=ly["Hs"],
+                           workspace=ly["ws"])
+            if record is not None:
+                record("fwd", li, 1)
+            x = ly["Y"]
+        mux.pack_apply(self.pk["row_src"], self.dY3tok, self.max_rows, out=self.dY3)
+        dy = self.dY3
+        for li in reversed(range(len(self.layers))):
+            ly = self.layers[li]
+            xin = self.X1 if li == 0 else self.layers[li - 1]["Y"]
+            if record is not None:
+                record("bwd", li, 0)
+            mux.linear_bwd(seg_off, self.seg_task, ly["ads"], dy, xin, ly["W"], ly["Hs"], self.r_cap,
+                           dX=ly["dX"], workspace=ly["ws"])
+            if record is not None:
+                record("bwd", li, 1)
+            dy = ly["dX"]
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.p = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            os.makedirs(os.path.dirname(self.path), exist_ok=True)
+            self.f = open(self.path, "w")
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.close()
+        sm, smax, reasons, power = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+                power.append(float(parts[3]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        loaded = [s for s, p in zip(sm, power) if p > 250] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
+                "samples": len(sm), "power_w_max": max(power)}
+
+
+# ------------------------------------------------------------------ cpu / reference arm
+def oracle_sample(w: Workload, rows_per_task: int, seed_off=0):
+    """The oracle (as it stands) on a bounded sample of the workload: the same
+    three linear shapes, tasks and ranks, with `rows_per_task` rows per task;
+    full fwd (Y, Hs) + bwd (dX, dA_t, dB_t) on every sampled row."""
+    from oracle import linear as olin
+    wl = w.wl
+    M = w.M
+    seg_off = np.arange(M + 1, dtype=np.int32) * rows_per_task
+    R = int(seg_off[-1])
+    st = synth.Stream(wl.seed + 77 + seed_off)
+    ranks, scales = wl.ranks, wl.scales
+    r_cap = 16 * -(-max(ranks) // 16)
+    data = []
+    for li, L in enumerate(w.linears):
+        X = synth.normal_bf16(wl.seed, st.take(), (R, L.K))
+        dY = synth.normal_bf16(wl.seed, st.take(), (R, L.N))
+        W = synth.weight(wl, li)
+        A, B = zip(*[synth.adapter(wl, li, t) for t in range(M)])
+        data.append((X, dY, W, list(A), list(B)))
+
+    def run():
+        for (X, dY, W, A, B) in data:
+            olin.linear_fwd(seg_off, list(range(M)), A, B, ranks, scales, X, W, r_cap)
+            olin.linear_bwd(seg_off, list(range(M)), A, B, ranks, scales, dY, X, W, r_cap)
+    return run, R
+
+
+def cpu_baseline(w: Workload, target_s=12.0):
+    from oracle import linear as olin
+    olin.build()
+    run, R = oracle_sample(w, 2)
+    t0 = time.perf_counter()
+    run()
+    t1 = time.perf_counter() - t0
+    rows_per_task = max(2, min(512, int(2 * target_s / max(t1, 1e-3))))
+    run, R = oracle_sample(w, rows_per_task)
+    t0 = time.perf_counter()
+    run()
+    dt = time.perf_counter() - t0
+    return {"value": R / dt, "unit": UNIT, "cores": olin.num_threads(), "kind": "oracle",
+            "sample": f"{R} tokens ({w.M} tasks x {rows_per_task} rows, ranks {w.wl.ranks}) through the "
+                      f"3 config-2 linear shapes, full fp64 fwd+bwd (Y, Hs, dX, dA, dB); {dt:.1f} s",
+            "seconds": dt}
+
+
+def reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import linear as olin
+    olin.build()
+    w = Workload(args.config)
+    rows_per_task = args.ref_rows
+    run, R = oracle_sample(w, rows_per_task)
+    for _ in range(args.warmup):
+        run()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        run()
+    dt = (time.perf_counter() - t0) / args.steps
+    v = R / dt
+    cores = olin.num_threads()
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"config {args.config}: " + w.wl.description,
+                       "sample_tokens_per_step": R},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"{R} tokens per step ({w.M} tasks x {rows_per_task} rows) through "
+                                       "the 3 linear shapes, fp64 fwd+bwd"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ main arm
+def main_arm(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2603_02885_b200 import mux
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    mux.lib()
+
+    w = Workload(args.config, rank_seed=rank)
+    ms = MuxStep(w, torch, mux)
+    stream = torch.cuda.current_stream()
+
+    for _ in range(args.warmup):
+        ms.step()
+    torch.cuda.synchronize()
+    info = mux.read_info(ms.pk["info"])
+    assert info["overflow"] == 0 and info["valid_rows"] == w.T, info
+
+    # per-launch events for the fused GEMM (fwd calls) inside the timed region
+    ev_pairs = {"fwd": [], "bwd": []}
+    pending = {}
+
+    def record(kind, li, which):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(stream)
+        if which == 0:
+            pending[(kind, li)] = e
+        else:
+            ev_pairs[kind].append((li, pending.pop((kind, li)), e))
+
+    clocks = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for _ in range(args.steps):
+        ms.step(record=record)
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms_total = t_start.elapsed_time(t_end)
+    t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+
+    # roofline of the dominant kernel (fused tcgen05 GEMM, forward calls)
+    fwd_ms = sum(a.elapsed_time(b) for (_, a, b) in ev_pairs["fwd"])
+    bwd_ms = sum(a.elapsed_time(b) for (_, a, b) in ev_pairs["bwd"])
+    fwd_flops = sum((2 * L.K * L.N + 2 * max(w.wl.ranks) * (L.K + L.N)) * w.T for L in w.linears) * args.steps
+    bwd_flops = sum((2 * L.K * L.N + 4 * max(w.wl.ranks) * (L.K + L.N)) * w.T for L in w.linears) * args.steps
+    pk = peaks()
+    achieved = fwd_flops / (fwd_ms * 1e-3) / 1e12
+    roof = {"bound": "tensor", "achieved": achieved, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
+            "frac": achieved / pk["bf16_tflops"], "traffic": None,
+            "kernel": "mux_gemm_kernel<fwd> (fused backbone + LoRA; events around each mux_linear_fwd call)",
+            "peak_source": pk["source"] + " burst bf16 (cuBLAS 8192^3)"}
+
+    # ---------------- e2e: same step through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda t: t.cpu().pin_memory()  # noqa: E731
+        h_tso, h_sl = pin(ms.tso), pin(ms.sl)
+        h_X1, h_dY3 = pin(ms.X1tok), pin(ms.dY3tok)
+        grads = [a.dA for ly in ms.layers for a in ly["ads"]] + [a.dB for ly in ms.layers for a in ly["ads"]]
+        h_grads = [torch.empty(g.shape, dtype=g.dtype, pin_memory=True) for g in grads]
+        h2d = sum(x.numel() * x.element_size() for x in (h_tso, h_sl, h_X1, h_dY3))
+        d2h = sum(g.numel() * g.element_size() for g in grads)
+
+        def e2e_step():
+            ms.tso.copy_(h_tso, non_blocking=True)
+            ms.sl.copy_(h_sl, non_blocking=True)
+            ms.X1tok.copy_(h_X1, non_blocking=True)
+            ms.dY3tok.copy_(h_dY3, non_blocking=True)
+            ms.step()
+            for g, hg in zip(grads, h_grads):
+                hg.copy_(g, non_blocking=True)
+
+        for _ in range(max(1, args.warmup)):
+            e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e_ms = float(te.item()) / args.steps
+        e2e = {"value": world * w.T / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms,
+               "what": "pinned H2D of seq metadata + token-major layer input X and loss gradient dY; "
+                       "D2H of every adapter gradient dA_t/dB_t (fp32)"}
+
+    value = world * w.T / (ms_step * 1e-3)
+    tflops = w.flops / (ms_step * 1e-3) / 1e12
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": f"config {args.config}: " + w.wl.description,
+                   "layers": [f"{L.K}->{L.N}" for L in w.linears], "tasks": w.M, "ranks": w.wl.ranks,
+                   "valid_tokens_per_gpu": w.T, "packed_rows": info["total_rows"],
+                   "chunk_size": info["chunk_size"], "parallelism": f"replicas x{world} (task-sharded)",
+                   "l2": "inputs larger than L2 (weights 214 MB + activations per step > 126 MB)"},
+        "tflops_per_gpu_algorithmic": tflops,
+        "frac_of_peak": {"measured_burst": tflops / pk["bf16_tflops"],
+                         "measured_sustained": tflops / pk["bf16_tflops_sustained"],
+                         "datasheet_2250": tflops / 2250.0},
+        "kernels": {"fwd_calls_ms_per_step": fwd_ms / args.steps, "bwd_calls_ms_per_step": bwd_ms / args.steps,
+                    "bwd_tflops": bwd_flops / (bwd_ms * 1e-3) / 1e12},
+        "roofline": roof,
+        "clocks": clk,
+        "gpu_launches": ms.launches_per_step * args.steps,
+        "e2e": e2e,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(w, args.cpu_seconds)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="mux", choices=["mux", "reference"])
+    ap.add_argument("--config", default="2")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--ref-rows", type=int, default=4, help="rows per task per reference-arm step")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        main_arm(args)
+
+
+if __name__ == "__main__":
+    main()
