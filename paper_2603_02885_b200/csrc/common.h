@@ -10,12 +10,16 @@
 namespace mux {
 
 // ---- fused linear GEMM (mux_linear_fwd / the dX part of mux_linear_bwd)
-constexpr int kBM = 128;        // rows per tile (TMEM lanes)
+// A work tile is computed by a CTA pair (cluster of 2, tcgen05 cta_group::2):
+// 256 rows (128 per CTA = TMEM lanes) x 256 output columns (each CTA stages
+// half of the B operand), reduction in k-blocks of 64.
+constexpr int kBM = 128;        // rows per CTA
+constexpr int kPairRows = 256;  // rows per pair tile (MMA M = 256)
 constexpr int kBN = 256;        // output columns per tile (TMEM columns per accumulator)
 constexpr int kBK = 64;         // reduction depth per pipeline stage (one 128 B swizzle row)
-constexpr int kStages = 4;
-constexpr int kRowHalf = 64;    // segment granularity inside a tile (chunk minimum)
-constexpr int kSideN = 64;      // N of the shrink MMA (rank padded to 64)
+constexpr int kStages = 6;
+constexpr int kRowQuarter = 64; // segment granularity inside a pair tile (chunk minimum)
+constexpr int kSideN = 128;     // N of the shrink MMA (rank padded to 64 in CTA 0's half)
 
 struct GemmParams {
   // A operand of the main product: X (fwd) / dY (bwd): dims {Kred, rows}, box {64, 128}
@@ -31,7 +35,7 @@ struct GemmParams {
   CUtensorMap map_lora_b[MUX_MAX_ADAPTERS];
   const int32_t* seg_off;        // device [num_segs + 1]
   __nv_bfloat16* side_out;       // Hs / Gs [max_rows, r_cap]
-  int32_t* flags;                // [ceil(max_rows/128)] zeroed before launch
+  int32_t* flags;                // [ceil(max_rows/256)] zeroed before launch
   int32_t num_segs;
   int32_t max_rows;
   int32_t kred;                  // reduction length of the main product (K fwd, N bwd)

@@ -1,40 +1,49 @@
-// gemm.cu — fused multiplexed-LoRA linear for sm_100a (tcgen05 + TMEM + TMA).
+// gemm.cu — fused multiplexed-LoRA linear for sm_100a (tcgen05 cta_group::2 +
+// TMEM + TMA), one persistent warp-specialized kernel per call.
 //
-// One persistent, warp-specialized kernel computes, for all segments of an
-// hTask at once (spatial batching of the BaseOp, Eq. 1 P:484-489 / Eq. 2
-// P:491-498) plus every segment's LoRA adapter (north_star formula), fused
-// horizontally across tasks:
+// For all segments of an hTask at once (spatial batching of the BaseOp, Eq. 1
+// P:484-489 / Eq. 2) plus every segment's LoRA adapter (north_star
+// formula), fused horizontally across tasks:
 //
 //   fwd:  Y  = X W^T            + Hs B_t^T      Hs = bf16(s_t X A_t^T)
 //   bwd:  dX = dY W             + Gs A_t        Gs = bf16(s_t dY B_t)
 //
-// Work items ("tiles"), statically round-robined over a grid of #SMs CTAs:
-//   * side tiles  (one per 128-row block m): the shrink Hs/Gs[m] = s_t X_m A_t^T
-//     as a tcgen05 MMA with N = 64 (rank padded), written to global and
-//     published through flags[m];
-//   * main tiles  (m, n): the backbone product over the whole reduction, then
-//     one "extension" k-block per task present in the tile: A = Hs/Gs tile,
-//     B = B_t / A_t tile (the expand), accumulated into the same TMEM tile.
-// Segments are multiples of 64 rows, so a 128-row tile holds at most two
-// tasks; their adapter MMAs use the disable-output-lane mask so that a row is
-// only ever multiplied with its own task's weights (NaN isolation).
-// Side tiles come first in the schedule and never wait, so every main tile's
-// dependency is on a lower-indexed tile: with all CTAs resident the smallest
-// unfinished tile can always progress (no deadlock).
+// Execution unit = a CTA pair (cluster of 2 on one TPC).  The leader CTA's
+// single MMA thread issues tcgen05.mma.cta_group::2 with M = 256: each CTA
+// stages its own 128 rows of A and half (128 columns) of the B tile, and owns
+// 128 TMEM lanes of the fp32 accumulator.  Each CTA therefore streams 32 KB per
+// 64-deep k-block for a 128x256 output slab (half the B traffic of a 1-CTA
+// 128x256 tile), with a 6-stage TMA ring.
 //
-// Roles (256 threads): warp 0 = TMA producer, warp 1 = MMA issuer, warp 2 =
-// TMEM allocator, warps 4..7 = epilogue (TMEM -> regs -> bf16 -> smem ->
-// TMA store).  4-stage smem ring (48 KB/stage), 2 TMEM accumulators of 256
-// fp32 columns so the epilogue of tile i overlaps the mainloop of tile i+1.
+// Work items, static round-robin over clusters:
+//   * side tiles (one per 256-row block m): the shrink Hs/Gs[m] = s_t X_m A_t^T
+//     (MMA N = 128; CTA 0's half of B holds the rank-padded A_t, CTA 1's half
+//     is TMA zero fill), written to global and published by release-adds on
+//     flags[m] (8 = all epilogue warps of the pair);
+//   * main tiles (m, n): the backbone product over the whole reduction, then one
+//     "extension" k-block per task present in the tile: A = Hs/Gs tile,
+//     B = B_t / A_t tile (the expand), accumulated into the same TMEM tile.
+// Segments are multiples of 64 rows, so a 256-row tile holds at most four
+// tasks; their adapter MMAs carry the tcgen05 disable-output-lane mask of every
+// other task's rows, so a row is only ever multiplied by its own task's
+// weights (NaN isolation).
+// Side tiles come first in the schedule and never wait, so every dependency
+// points to a lower tile index: with all CTAs resident the lowest unfinished
+// tile always progresses (no deadlock).
+//
+// Roles (256 threads per CTA): warp 0 = TMA producer (both CTAs), warp 1 = MMA
+// issuer (leader CTA), warp 2 = TMEM allocator, warps 4..7 = epilogue
+// (TMEM -> regs -> bf16 -> swizzled smem -> TMA store).  Two 256-column TMEM
+// accumulators: the epilogue of tile i overlaps the mainloop of tile i+1.
 #include "common.h"
 #include "ptx.cuh"
 
 namespace mux {
 
-constexpr uint32_t kStageA = kBM * kBK * 2;          // 16 KB
+constexpr uint32_t kStageA = kBM * kBK * 2;          // 16 KB: this CTA's 128 rows
 constexpr uint32_t kSubB = 64 * kBK * 2;             // 8 KB: one {64 x 128 B} TMA box
-constexpr uint32_t kStageB = kBN * kBK * 2;          // 32 KB
-constexpr uint32_t kStageBytes = kStageA + kStageB;  // 48 KB
+constexpr uint32_t kStageB = (kBN / 2) * kBK * 2;    // 16 KB: this CTA's half of B
+constexpr uint32_t kStageBytes = kStageA + kStageB;  // 32 KB
 constexpr uint32_t kEpiBuf = 32 * 128;               // 32 rows x 64 bf16 (one TMA store box)
 constexpr uint32_t kSmemPipe = kStages * kStageBytes;
 constexpr uint32_t kSmemEpi = 4 * 2 * kEpiBuf;
@@ -42,18 +51,16 @@ constexpr uint32_t kSmemMisc = 1024;
 constexpr uint32_t kGemmSmemBytes = kSmemPipe + kSmemEpi + kSmemMisc + 1024;
 constexpr uint32_t kTmemCols = 512;
 constexpr int kGemmThreads = 256;
-constexpr int kGroupM = 8;  // raster: 8 row-blocks share a band of W tiles
+constexpr int kGroupM = 16;  // raster: 16 pair row-blocks (4096 rows) share a band of W tiles
+constexpr uint16_t kPairMask = 0x3;
 
-struct TileGroups {
-  int n;          // active groups (tasks with rank > 0) in the tile
-  int seg0, seg1;
-  int half0, half1;  // lanes the group owns: 0 = all 128, 1 = rows 0-63, 2 = rows 64-127
+// Tasks present in a 256-row pair tile.  hm = bit h set: the group owns rows
+// [64h, 64h+64) of the tile.
+struct PairGroups {
+  int n;
+  int seg[4];
+  int hm[4];
 };
-
-// disable-output-lane mask word w (lanes 32w..32w+31) for a group owning `half`
-__device__ __forceinline__ uint32_t lane_mask(int half, int w) {
-  return half == 0 ? 0u : (half == 1 ? (w >= 2 ? ~0u : 0u) : (w < 2 ? ~0u : 0u));
-}
 
 __device__ __forceinline__ int seg_containing(const int* so, int S, int row) {
   for (int s = 0; s < S; ++s)
@@ -61,34 +68,29 @@ __device__ __forceinline__ int seg_containing(const int* so, int S, int row) {
   return -1;
 }
 
-__device__ __forceinline__ TileGroups tile_groups(const GemmParams& p, const int* so, int m) {
-  TileGroups g;
+__device__ __forceinline__ PairGroups pair_groups(const GemmParams& p, const int* so, int m) {
+  PairGroups g;
   g.n = 0;
-  g.seg0 = g.seg1 = 0;
-  g.half0 = g.half1 = 0;
-  const int S = p.num_segs;
-  const int r0 = m * kBM;
-  const int s0 = seg_containing(so, S, r0);
-  const int s1 = seg_containing(so, S, r0 + kRowHalf);
-  if (s1 < 0 || s1 == s0) {
-    if (s0 >= 0 && p.seg_rank[s0] > 0) {
-      g.seg0 = s0;
-      g.half0 = 0;
-      g.n = 1;
+  for (int h = 0; h < 4; ++h) {
+    const int s = seg_containing(so, p.num_segs, m * kPairRows + kRowQuarter * h);
+    if (s < 0 || p.seg_rank[s] == 0) continue;
+    int f = -1;
+    for (int i = 0; i < g.n; ++i)
+      if (g.seg[i] == s) f = i;
+    if (f < 0) {
+      g.seg[g.n] = s;
+      g.hm[g.n] = 0;
+      f = g.n++;
     }
-  } else {
-    if (s0 >= 0 && p.seg_rank[s0] > 0) {
-      g.seg0 = s0;
-      g.half0 = 1;
-      g.n = 1;
-    }
-    if (p.seg_rank[s1] > 0) {
-      if (g.n == 0) { g.seg0 = s1; g.half0 = 2; }
-      else { g.seg1 = s1; g.half1 = 2; }
-      ++g.n;
-    }
+    g.hm[f] |= 1 << h;
   }
   return g;
+}
+
+// disable-output-lane mask of a group owning the quarters in `hm`
+__device__ __forceinline__ void lane_masks(int hm, uint32_t (&m)[8]) {
+#pragma unroll
+  for (int w = 0; w < 8; ++w) m[w] = ((hm >> (w >> 1)) & 1) ? 0u : ~0u;
 }
 
 struct Tile {
@@ -115,7 +117,8 @@ __device__ __forceinline__ Tile tile_at(int t, int num_m, int num_n) {
 }
 
 template <bool kBwd>
-__global__ void __launch_bounds__(kGemmThreads, 1) mux_gemm_kernel(const __grid_constant__ GemmParams p) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
+    mux_gemm_kernel(const __grid_constant__ GemmParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* pipe = smem;
@@ -130,6 +133,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1) mux_gemm_kernel(const __grid_
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const uint32_t crank = cluster_ctarank();
+  const bool leader = crank == 0;
+  const int cid = static_cast<int>(cluster_id_x());
+  const int ncl = static_cast<int>(nclusters_x());
 
   for (int i = threadIdx.x; i <= p.num_segs; i += blockDim.x) so[i] = p.seg_off[i];
   if (warp == 0 && lane == 0) {
@@ -145,90 +152,101 @@ __global__ void __launch_bounds__(kGemmThreads, 1) mux_gemm_kernel(const __grid_
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], 4);
+      mbar_init(&tempty_bar[a], 8);
     }
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc<kTmemCols>(tmem_holder);
+  if (warp == 2) tmem_alloc_pair<kTmemCols>(tmem_holder);
   tc_fence_before();
   __syncthreads();
+  cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
   const int total_rows = so[p.num_segs];
-  const int num_m = (total_rows + kBM - 1) / kBM;
+  const int num_m = (total_rows + kPairRows - 1) / kPairRows;
   const int num_n = (p.nout + kBN - 1) / kBN;
   const int total_tiles = num_m * (1 + (p.has_main ? num_n : 0));
   const int num_kb = p.kred / kBK;
 
   if (warp == 0) {
-    // =========================== TMA producer ===========================
+    // =========================== TMA producer (both CTAs) ===============
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
       auto advance = [&]() {
         if (++stage == kStages) { stage = 0; phase ^= 1u; }
       };
-      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      for (int t = cid; t < total_tiles; t += ncl) {
         const Tile tl = tile_at(t, num_m, num_n);
-        const TileGroups g = tile_groups(p, so, tl.m);
-        const int row0 = tl.m * kBM;
+        const PairGroups g = pair_groups(p, so, tl.m);
+        const int row_c = tl.m * kPairRows + kBM * static_cast<int>(crank);  // this CTA's rows
         if (tl.side) {
-          if (g.n == 0) continue;
-          for (int kb = 0; kb < num_kb; ++kb) {
-            mbar_wait(&empty_bar[stage], phase ^ 1u);
-            uint8_t* sa = pipe + stage * kStageBytes;
-            uint8_t* sb = sa + kStageA;
-            mbar_arrive_expect_tx(&full_bar[stage], kStageA + g.n * kSubB);
-            tma_load_2d(&p.map_a, &full_bar[stage], sa, kb * kBK, row0);
-            for (int i = 0; i < g.n; ++i) {
-              const int ad = p.seg_adapter[i == 0 ? g.seg0 : g.seg1];
-              if (!kBwd)  // A_t [r, K] K-major: box {64 k, 64 j}
-                tma_load_2d(&p.map_lora_a[ad], &full_bar[stage], sb + i * kSubB, kb * kBK, 0);
-              else        // B_t [N, r] as MN-major {64 j, 64 n}
-                tma_load_2d(&p.map_lora_b[ad], &full_bar[stage], sb + i * kSubB, 0, kb * kBK);
+          for (int g0 = 0; g0 < g.n; g0 += 2) {
+            const int ng = min(2, g.n - g0);
+            for (int kb = 0; kb < num_kb; ++kb) {
+              mbar_wait(&empty_bar[stage], phase ^ 1u);
+              uint8_t* sa = pipe + stage * kStageBytes;
+              uint8_t* sb = sa + kStageA;
+              const uint32_t fb = smem_u32(&full_bar[stage]);
+              if (leader) mbar_arrive_expect_tx_u32(fb, 2u * (kStageA + ng * kSubB));
+              const uint32_t fbl = mapa_shared(fb, 0);
+              tma_load_2d_pair(&p.map_a, fbl, sa, kb * kBK, row_c);
+              for (int i = 0; i < ng; ++i) {
+                const int ad = p.seg_adapter[g.seg[g0 + i]];
+                if (!kBwd)  // A_t [r, K] K-major rows j: CTA 1's rows 64.. are zero fill
+                  tma_load_2d_pair(&p.map_lora_a[ad], fbl, sb + i * kSubB, kb * kBK, 64 * static_cast<int>(crank));
+                else        // B_t [N, r] read MN-major {64 j, 64 n}
+                  tma_load_2d_pair(&p.map_lora_b[ad], fbl, sb + i * kSubB, 64 * static_cast<int>(crank), kb * kBK);
+              }
+              advance();
             }
-            advance();
           }
         } else {
-          const int col0 = tl.n * kBN;
+          const int col_c = tl.n * kBN + (kBN / 2) * static_cast<int>(crank);  // this CTA's half of N
           for (int kb = 0; kb < num_kb; ++kb) {
             mbar_wait(&empty_bar[stage], phase ^ 1u);
             uint8_t* sa = pipe + stage * kStageBytes;
             uint8_t* sb = sa + kStageA;
-            mbar_arrive_expect_tx(&full_bar[stage], kStageBytes);
-            tma_load_2d(&p.map_a, &full_bar[stage], sa, kb * kBK, row0);
-            for (int i = 0; i < 4; ++i) {
+            const uint32_t fb = smem_u32(&full_bar[stage]);
+            if (leader) mbar_arrive_expect_tx_u32(fb, 2u * kStageBytes);
+            const uint32_t fbl = mapa_shared(fb, 0);
+            tma_load_2d_pair(&p.map_a, fbl, sa, kb * kBK, row_c);
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
               if (!kBwd)  // W [N, K] K-major rows n
-                tma_load_2d(&p.map_w, &full_bar[stage], sb + i * kSubB, kb * kBK, col0 + 64 * i);
+                tma_load_2d_pair(&p.map_w, fbl, sb + i * kSubB, kb * kBK, col_c + 64 * i);
               else        // W viewed [k_out (MN), n (red)]: MN-major atoms of 64 k
-                tma_load_2d(&p.map_w, &full_bar[stage], sb + i * kSubB, col0 + 64 * i, kb * kBK);
+                tma_load_2d_pair(&p.map_w, fbl, sb + i * kSubB, col_c + 64 * i, kb * kBK);
             }
             advance();
           }
           if (g.n > 0) {
-            // wait until the side tile of this row block has published Hs/Gs
+            // the side tile of this row block must have published Hs/Gs
             const int* flag = p.flags + tl.m;
-            if (ld_acquire_gpu(flag) < 4) {
+            if (ld_acquire_gpu(flag) < 8) {
               const uint64_t t0 = globaltimer_ns();
-              while (ld_acquire_gpu(flag) < 4) {
+              while (ld_acquire_gpu(flag) < 8) {
                 if (globaltimer_ns() - t0 > kWatchdogNs) __trap();
               }
             }
             fence_async_global();
           }
           for (int i = 0; i < g.n; ++i) {
-            const int ad = p.seg_adapter[i == 0 ? g.seg0 : g.seg1];
+            const int ad = p.seg_adapter[g.seg[i]];
             mbar_wait(&empty_bar[stage], phase ^ 1u);
             uint8_t* sa = pipe + stage * kStageBytes;
             uint8_t* sb = sa + kStageA;
-            mbar_arrive_expect_tx(&full_bar[stage], kStageBytes);
-            tma_load_2d(&p.map_side, &full_bar[stage], sa, 0, row0);
-            for (int j = 0; j < 4; ++j) {
+            const uint32_t fb = smem_u32(&full_bar[stage]);
+            if (leader) mbar_arrive_expect_tx_u32(fb, 2u * kStageBytes);
+            const uint32_t fbl = mapa_shared(fb, 0);
+            tma_load_2d_pair(&p.map_side, fbl, sa, 0, row_c);
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
               if (!kBwd)  // B_t [N, r] K-major rows n: box {64 j, 64 n}
-                tma_load_2d(&p.map_lora_b[ad], &full_bar[stage], sb + j * kSubB, 0, col0 + 64 * j);
+                tma_load_2d_pair(&p.map_lora_b[ad], fbl, sb + j * kSubB, 0, col_c + 64 * j);
               else        // A_t [r, K] viewed [k_out (MN), j (red)]
-                tma_load_2d(&p.map_lora_a[ad], &full_bar[stage], sb + j * kSubB, col0 + 64 * j, 0);
+                tma_load_2d_pair(&p.map_lora_a[ad], fbl, sb + j * kSubB, col_c + 64 * j, 0);
             }
             advance();
           }
@@ -236,14 +254,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1) mux_gemm_kernel(const __grid_
       }
     }
   } else if (warp == 1) {
-    // =========================== MMA issuer =============================
-    if (lane == 0) {
-      constexpr uint32_t kIdescMain = idesc_bf16(kBM, kBN, false, kBwd);
-      constexpr uint32_t kIdescSide = idesc_bf16(kBM, kSideN, false, kBwd);
-      // B-operand descriptor parameters: K-major rows of 128 B (SBO 1024) or
-      // MN-major atoms of 64 elements x 64 K-rows (LBO 8 KB, SBO 1024).
+    // =========================== MMA issuer (leader CTA) ================
+    if (leader && lane == 0) {
+      constexpr uint32_t kIdescMain = idesc_bf16(kPairRows, kBN, false, kBwd);
+      constexpr uint32_t kIdescSide = idesc_bf16(kPairRows, kSideN, false, kBwd);
+      // B operand per CTA: K-major rows of 128 B (SBO 1024), or MN-major atoms
+      // of 64 elements x 64 K-rows (LBO 8 KB between atoms, SBO 1024).
       constexpr uint32_t kBLbo = kBwd ? kSubB : 16;
       constexpr uint32_t kBStepK = kBwd ? 16 * 128 : 32;
+      const uint32_t no_mask[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -251,31 +270,32 @@ __global__ void __launch_bounds__(kGemmThreads, 1) mux_gemm_kernel(const __grid_
       auto advance = [&]() {
         if (++stage == kStages) { stage = 0; phase ^= 1u; }
       };
-      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      for (int t = cid; t < total_tiles; t += ncl) {
         const Tile tl = tile_at(t, num_m, num_n);
-        const TileGroups g = tile_groups(p, so, tl.m);
+        const PairGroups g = pair_groups(p, so, tl.m);
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1u);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * kBN);
         if (tl.side) {
-          if (g.n > 0) {
+          for (int g0 = 0; g0 < g.n; g0 += 2) {
+            const int ng = min(2, g.n - g0);
+            uint32_t mk[2][8];
+            lane_masks(g.hm[g0], mk[0]);
+            lane_masks(ng > 1 ? g.hm[g0 + 1] : 0, mk[1]);
             for (int kb = 0; kb < num_kb; ++kb) {
               mbar_wait(&full_bar[stage], phase);
               tc_fence_after();
               const uint32_t a_base = smem_u32(pipe + stage * kStageBytes);
               const uint32_t b_base = a_base + kStageA;
-              for (int i = 0; i < g.n; ++i) {
-                const int half = i == 0 ? g.half0 : g.half1;
-                const uint32_t m0 = lane_mask(half, 0), m1 = lane_mask(half, 1);
-                const uint32_t m2 = lane_mask(half, 2), m3 = lane_mask(half, 3);
+              for (int i = 0; i < ng; ++i) {
 #pragma unroll
                 for (int k = 0; k < kBK / 16; ++k) {
                   const uint64_t ad = smem_desc(a_base + k * 32, 16, 1024);
                   const uint64_t bd = smem_desc(b_base + i * kSubB + k * kBStepK, kBLbo, 1024);
-                  mma_bf16_masked(d_tmem, ad, bd, kIdescSide, (kb | k) != 0, m0, m1, m2, m3);
+                  mma_bf16_pair(d_tmem, ad, bd, kIdescSide, (kb | k) != 0, mk[i]);
                 }
               }
-              mma_commit(&empty_bar[stage]);
+              mma_commit_pair_mc(&empty_bar[stage], kPairMask);
               advance();
             }
           }
@@ -289,9 +309,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1) mux_gemm_kernel(const __grid_
             for (int k = 0; k < kBK / 16; ++k) {
               const uint64_t ad = smem_desc(a_base + k * 32, 16, 1024);
               const uint64_t bd = smem_desc(b_base + k * kBStepK, kBLbo, 1024);
-              mma_bf16(d_tmem, ad, bd, kIdescMain, (kb | k) != 0);
+              mma_bf16_pair(d_tmem, ad, bd, kIdescMain, (kb | k) != 0, no_mask);
             }
-            mma_commit(&empty_bar[stage]);
+            mma_commit_pair_mc(&empty_bar[stage], kPairMask);
             advance();
           }
           for (int i = 0; i < g.n; ++i) {
@@ -299,36 +319,36 @@ __global__ void __launch_bounds__(kGemmThreads, 1) mux_gemm_kernel(const __grid_
             tc_fence_after();
             const uint32_t a_base = smem_u32(pipe + stage * kStageBytes);
             const uint32_t b_base = a_base + kStageA;
-            const int nk = (p.seg_rank[i == 0 ? g.seg0 : g.seg1] + 15) / 16;
-            const int half = i == 0 ? g.half0 : g.half1;
-            const uint32_t m0 = lane_mask(half, 0), m1 = lane_mask(half, 1);
-            const uint32_t m2 = lane_mask(half, 2), m3 = lane_mask(half, 3);
+            const int nk = (p.seg_rank[g.seg[i]] + 15) / 16;
+            uint32_t mk[8];
+            lane_masks(g.hm[i], mk);
             for (int k = 0; k < nk; ++k) {
               const uint64_t ad = smem_desc(a_base + k * 32, 16, 1024);
               const uint64_t bd = smem_desc(b_base + k * kBStepK, kBLbo, 1024);
-              mma_bf16_masked(d_tmem, ad, bd, kIdescMain, 1u, m0, m1, m2, m3);
+              mma_bf16_pair(d_tmem, ad, bd, kIdescMain, 1u, mk);
             }
-            mma_commit(&empty_bar[stage]);
+            mma_commit_pair_mc(&empty_bar[stage], kPairMask);
             advance();
           }
         }
-        mma_commit(&tfull_bar[acc]);
+        mma_commit_pair_mc(&tfull_bar[acc], kPairMask);
         if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
       }
     }
   } else if (warp >= 4) {
-    // =========================== epilogue ===============================
-    const int q = warp & 3;  // TMEM lane quadrant = rows 32q .. 32q+31
+    // =========================== epilogue (both CTAs) ===================
+    const int q = warp & 3;  // TMEM lane quadrant = this CTA's rows 32q .. 32q+31
     int acc = 0;
     uint32_t acc_phase = 0;
     uint8_t* bufs = epi + q * 2 * kEpiBuf;
     int buf_sel = 0;
-    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+    for (int t = cid; t < total_tiles; t += ncl) {
       const Tile tl = tile_at(t, num_m, num_n);
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
-      const int row_w = tl.m * kBM + 32 * q;  // first row of this warp
+      const int row_w = tl.m * kPairRows + kBM * static_cast<int>(crank) + 32 * q;  // first row of this warp
       const uint32_t t_addr = tmem_base + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(acc * kBN);
+      const uint32_t tempty_leader = mapa_shared(smem_u32(&tempty_bar[acc]), 0);
       if (tl.side) {
         uint32_t v0[32], v1[32];
         tmem_ld32(t_addr, v0);
@@ -336,7 +356,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) mux_gemm_kernel(const __grid_
         tmem_ld_wait();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+        if (lane == 0) mbar_arrive_cluster(tempty_leader);
         const int row = row_w + lane;
         if (row < total_rows) {
           const int s = seg_containing(so, p.num_segs, row);
@@ -376,7 +396,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) mux_gemm_kernel(const __grid_
           if (c == kBN / 64 - 1) {
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+            if (lane == 0) mbar_arrive_cluster(tempty_leader);
           }
           uint8_t* buf = bufs + buf_sel * kEpiBuf;
           if (lane == 0) tma_store_wait_read<1>();
@@ -409,9 +429,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1) mux_gemm_kernel(const __grid_
   }
   tc_fence_before();
   __syncthreads();
+  cluster_sync();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc<kTmemCols>(tmem_base);
+    tmem_dealloc_pair<kTmemCols>(tmem_base);
   }
 }
 
@@ -429,6 +450,7 @@ cudaError_t launch_gemm_impl(const GemmParams& p, int grid, cudaStream_t stream)
   return cudaGetLastError();
 }
 
+// grid must be even (clusters of 2)
 cudaError_t launch_gemm(const GemmParams& p, bool bwd, int grid, cudaStream_t stream) {
   return bwd ? launch_gemm_impl<true>(p, grid, stream) : launch_gemm_impl<false>(p, grid, stream);
 }

@@ -2,6 +2,7 @@
 // workspace carving, TMA descriptor encoding and kernel launches.  Every
 // entry point only enqueues on the caller's stream; nothing reads device
 // data on the host, so whole layers can be captured in a CUDA graph.
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -146,7 +147,7 @@ struct LinearWs {
 };
 LinearWs carve_linear_ws(void* base, int32_t max_rows, int32_t r_cap) {
   LinearWs w{};
-  const size_t n_m = (static_cast<size_t>(max_rows) + kBM - 1) / kBM;
+  const size_t n_m = (static_cast<size_t>(max_rows) + kPairRows - 1) / kPairRows;
   const size_t f = align256(n_m * sizeof(int32_t));
   const size_t g = align256(static_cast<size_t>(max_rows) * r_cap * 2);
   uint8_t* b = reinterpret_cast<uint8_t*>(base);
@@ -321,10 +322,12 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
     p.seg_rank[s] = a.rank;
     p.seg_scale[s] = a.scale;
   }
-  const int num_m_max = (max_rows + kBM - 1) / kBM;
+  const int num_m_max = (max_rows + kPairRows - 1) / kPairRows;
   const int num_n = (nout + kBN - 1) / kBN;
   const long long tiles_max = static_cast<long long>(num_m_max) * (1 + (p.has_main ? num_n : 0));
-  const int grid = static_cast<int>(tiles_max < num_sms() ? tiles_max : num_sms());
+  // one CTA pair (cluster of 2) per tile in flight; grid = #SMs rounded to pairs
+  const long long pairs = std::min<long long>(tiles_max, num_sms() / 2);
+  const int grid = static_cast<int>(2 * std::max<long long>(pairs, 1));
   cudaError_t e = cudaMemsetAsync(ws.flags, 0, sizeof(int32_t) * num_m_max, stream);
   if (e != cudaSuccess) return cuda_fail(e, "flag reset");
   e = launch_gemm(p, bwd, grid, stream);
