@@ -255,14 +255,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     }
   } else if (warp == 1) {
     // =========================== MMA issuer (leader CTA) ================
-    if (leader && lane == 0) {
+    // The whole warp runs the loop (warp-uniform values stay in uniform
+    // registers); one elected lane issues tcgen05.mma / tcgen05.commit.
+    if (leader) {
       constexpr uint32_t kIdescMain = idesc_bf16(kPairRows, kBN, false, kBwd);
       constexpr uint32_t kIdescSide = idesc_bf16(kPairRows, kSideN, false, kBwd);
       // B operand per CTA: K-major rows of 128 B (SBO 1024), or MN-major atoms
       // of 64 elements x 64 K-rows (LBO 8 KB between atoms, SBO 1024).
       constexpr uint32_t kBLbo = kBwd ? kSubB : 16;
-      constexpr uint32_t kBStepK = kBwd ? 16 * 128 : 32;
-      const uint32_t no_mask[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+      constexpr uint32_t kBStepK = (kBwd ? 16 * 128 : 32) >> 4;  // descriptor units (16 B)
+      constexpr uint32_t kAStepK = 32 >> 4;
+      constexpr uint32_t kHi = desc_hi(1024);
+      const uint32_t pipe_s = smem_u32(pipe);
+      const uint32_t a_lo0 = desc_lo(pipe_s, 16);
+      const uint32_t b_lo0 = desc_lo(pipe_s + kStageA, kBLbo);
+      constexpr uint32_t kStageStep = kStageBytes >> 4;
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -285,17 +292,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             for (int kb = 0; kb < num_kb; ++kb) {
               mbar_wait(&full_bar[stage], phase);
               tc_fence_after();
-              const uint32_t a_base = smem_u32(pipe + stage * kStageBytes);
-              const uint32_t b_base = a_base + kStageA;
-              for (int i = 0; i < ng; ++i) {
+              const uint32_t a_lo = a_lo0 + stage * kStageStep;
+              const uint32_t b_lo = b_lo0 + stage * kStageStep;
+              if (elect_one_sync()) {
+                for (int i = 0; i < ng; ++i) {
 #pragma unroll
-                for (int k = 0; k < kBK / 16; ++k) {
-                  const uint64_t ad = smem_desc(a_base + k * 32, 16, 1024);
-                  const uint64_t bd = smem_desc(b_base + i * kSubB + k * kBStepK, kBLbo, 1024);
-                  mma_bf16_pair(d_tmem, ad, bd, kIdescSide, (kb | k) != 0, mk[i]);
+                  for (int k = 0; k < kBK / 16; ++k)
+                    mma_bf16_pair(d_tmem, make_desc(a_lo + k * kAStepK, kHi),
+                                  make_desc(b_lo + i * (kSubB >> 4) + k * kBStepK, kHi), kIdescSide,
+                                  (kb | k) != 0, mk[i]);
                 }
+                mma_commit_pair_mc(&empty_bar[stage], kPairMask);
               }
-              mma_commit_pair_mc(&empty_bar[stage], kPairMask);
+              __syncwarp();
               advance();
             }
           }
@@ -303,35 +312,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           for (int kb = 0; kb < num_kb; ++kb) {
             mbar_wait(&full_bar[stage], phase);
             tc_fence_after();
-            const uint32_t a_base = smem_u32(pipe + stage * kStageBytes);
-            const uint32_t b_base = a_base + kStageA;
+            const uint32_t a_lo = a_lo0 + stage * kStageStep;
+            const uint32_t b_lo = b_lo0 + stage * kStageStep;
+            if (elect_one_sync()) {
 #pragma unroll
-            for (int k = 0; k < kBK / 16; ++k) {
-              const uint64_t ad = smem_desc(a_base + k * 32, 16, 1024);
-              const uint64_t bd = smem_desc(b_base + k * kBStepK, kBLbo, 1024);
-              mma_bf16_pair(d_tmem, ad, bd, kIdescMain, (kb | k) != 0, no_mask);
+              for (int k = 0; k < kBK / 16; ++k)
+                mma_bf16_pair_nomask(d_tmem, make_desc(a_lo + k * kAStepK, kHi),
+                                     make_desc(b_lo + k * kBStepK, kHi), kIdescMain, (kb | k) != 0);
+              mma_commit_pair_mc(&empty_bar[stage], kPairMask);
             }
-            mma_commit_pair_mc(&empty_bar[stage], kPairMask);
+            __syncwarp();
             advance();
           }
           for (int i = 0; i < g.n; ++i) {
             mbar_wait(&full_bar[stage], phase);
             tc_fence_after();
-            const uint32_t a_base = smem_u32(pipe + stage * kStageBytes);
-            const uint32_t b_base = a_base + kStageA;
+            const uint32_t a_lo = a_lo0 + stage * kStageStep;
+            const uint32_t b_lo = b_lo0 + stage * kStageStep;
             const int nk = (p.seg_rank[g.seg[i]] + 15) / 16;
             uint32_t mk[8];
             lane_masks(g.hm[i], mk);
-            for (int k = 0; k < nk; ++k) {
-              const uint64_t ad = smem_desc(a_base + k * 32, 16, 1024);
-              const uint64_t bd = smem_desc(b_base + k * kBStepK, kBLbo, 1024);
-              mma_bf16_pair(d_tmem, ad, bd, kIdescMain, 1u, mk);
+            if (elect_one_sync()) {
+              for (int k = 0; k < nk; ++k)
+                mma_bf16_pair(d_tmem, make_desc(a_lo + k * kAStepK, kHi), make_desc(b_lo + k * kBStepK, kHi),
+                              kIdescMain, 1u, mk);
+              mma_commit_pair_mc(&empty_bar[stage], kPairMask);
             }
-            mma_commit_pair_mc(&empty_bar[stage], kPairMask);
+            __syncwarp();
             advance();
           }
         }
-        mma_commit_pair_mc(&tfull_bar[acc], kPairMask);
+        if (elect_one_sync()) mma_commit_pair_mc(&tfull_bar[acc], kPairMask);
+        __syncwarp();
         if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
       }
     }

@@ -1,0 +1,152 @@
+"""Tensor parallelism of the frozen backbone for the multiplexed LoRA linear
+(Megatron column/row split, with sequence
+parallelism).  One process per GPU; torch.distributed process groups
+(NCCL on B200s) carry the collectives; every rank's compute is one
+mux_linear_fwd / mux_linear_bwd call on its shard.
+
+Shard placement (reading Q15 in DESIGN.md):
+  column-parallel (q, k, v, gate, up): W_p = W[N/p rows], A_t replicated,
+      B_{t,p} = B_t[N/p rows].  fwd: AG(X) -> local fwd -> Y_p [R, N/p].
+      bwd: local bwd -> RS(dX_partial) -> dX [R/p, K];  AR(dA_t).
+      (Gs_p = s dY_p B_{t,p} is a partial sum over ranks; dA_t = Gs^T X is
+      linear in Gs, so the per-rank dA_t are summed.)
+  row-parallel (o, down): W_p = W[:, K/p cols], A_{t,p} = A_t[:, K/p cols],
+      B_t replicated.  fwd: local fwd -> RS(Y_partial) -> Y [R/p, N]
+      (H = sum_p X_p A_{t,p}^T enters linearly, so the LoRA term folds into
+      the same reduce-scatter).  bwd: AG(dY) -> local bwd -> dX_p [R, K/p];
+      AR(dB_t) (dB_t = dY^T Hs is linear in Hs = sum_p Hs_p).
+Rows are split into p equal contiguous blocks (sequence parallel); R must be
+a multiple of p.  Segment offsets are global (the same on every rank).
+
+The per-rank compute is injected as a `backend` with
+  fwd(seg_off, seg_task, adapters, X, W, r_cap) -> (Y, Hs)
+  bwd(seg_off, seg_task, adapters, dY, X, W, Hs, r_cap) -> (dX, [dA_t], [dB_t])
+`MuxBackend` is the product (libmux through the binding); tests inject the
+fp64 oracle to check the collective orchestration on CPU with gloo.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import List, Optional, Sequence
+
+import torch
+import torch.distributed as dist
+
+
+# ------------------------------------------------------------------ collectives
+def _world(group=None):
+    return dist.get_world_size(group), dist.get_rank(group)
+
+
+def all_gather_rows(x: torch.Tensor, group=None) -> torch.Tensor:
+    p, _ = _world(group)
+    out = torch.empty((x.shape[0] * p,) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(out, x.contiguous(), group=group)
+    else:
+        parts = list(out.chunk(p, 0))
+        dist.all_gather(parts, x.contiguous(), group=group)
+        out = torch.cat(parts, 0)
+    return out
+
+
+def reduce_scatter_rows(x: torch.Tensor, group=None) -> torch.Tensor:
+    p, r = _world(group)
+    rows = x.shape[0] // p
+    if dist.get_backend(group) == "nccl":
+        out = torch.empty((rows,) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
+        dist.reduce_scatter_tensor(out, x.contiguous(), group=group)
+        return out
+    y = x.clone()
+    dist.all_reduce(y, group=group)
+    return y[r * rows:(r + 1) * rows].contiguous()
+
+
+def all_reduce_(x: torch.Tensor, group=None) -> torch.Tensor:
+    dist.all_reduce(x, group=group)
+    return x
+
+
+# ------------------------------------------------------------------ backends
+class MuxBackend:
+    """libmux kernels (the product path)."""
+
+    def __init__(self):
+        from . import mux
+        self.mux = mux
+
+    def fwd(self, seg_off, seg_task, adapters, X, W, r_cap):
+        return self.mux.linear_fwd(seg_off, seg_task, adapters, X, W, r_cap)
+
+    def bwd(self, seg_off, seg_task, adapters, dY, X, W, Hs, r_cap):
+        dX = self.mux.linear_bwd(seg_off, seg_task, adapters, dY, X, W, Hs, r_cap)
+        return dX, [a.dA for a in adapters], [a.dB for a in adapters]
+
+
+@dataclass
+class ShardAdapter:
+    """One task's adapter shard on this rank (same fields as mux.Adapter)."""
+    A: Optional[torch.Tensor]
+    B: Optional[torch.Tensor]
+    rank: int
+    scale: float
+    dA: Optional[torch.Tensor] = None
+    dB: Optional[torch.Tensor] = None
+
+
+def shard_column(W: torch.Tensor, adapters: Sequence, p: int, r: int, make_adapter):
+    """Column-parallel shard of (W [N,K], adapters) for rank r of p."""
+    N = W.shape[0]
+    n = N // p
+    Wp = W[r * n:(r + 1) * n].contiguous()
+    ads = [make_adapter(a.A, None if a.B is None else a.B[r * n:(r + 1) * n], a.rank, a.scale) for a in adapters]
+    return Wp, ads
+
+
+def shard_row(W: torch.Tensor, adapters: Sequence, p: int, r: int, make_adapter):
+    """Row-parallel shard of (W [N,K], adapters) for rank r of p."""
+    K = W.shape[1]
+    k = K // p
+    Wp = W[:, r * k:(r + 1) * k].contiguous()
+    ads = [make_adapter(None if a.A is None else a.A[:, r * k:(r + 1) * k].contiguous(), a.B, a.rank, a.scale)
+           for a in adapters]
+    return Wp, ads
+
+
+class ColumnParallelMuxLinear:
+    def __init__(self, backend, W_shard, adapters_shard, r_cap, group=None):
+        self.be, self.W, self.ads, self.r_cap, self.group = backend, W_shard, adapters_shard, r_cap, group
+
+    def forward(self, seg_off, seg_task, x_rows):
+        """x_rows [R/p, K] (this rank's row block) -> Y_p [R, N/p]."""
+        self.X = all_gather_rows(x_rows, self.group)
+        Y, self.Hs = self.be.fwd(seg_off, seg_task, self.ads, self.X, self.W, self.r_cap)
+        return Y
+
+    def backward(self, seg_off, seg_task, dY_cols):
+        """dY_p [R, N/p] -> dX rows [R/p, K]; dA_t all-reduced, dB_{t,p} local."""
+        dXp, dA, dB = self.be.bwd(seg_off, seg_task, self.ads, dY_cols, self.X, self.W, self.Hs, self.r_cap)
+        for g in dA:
+            if g is not None:
+                all_reduce_(g, self.group)
+        return reduce_scatter_rows(dXp, self.group), dA, dB
+
+
+class RowParallelMuxLinear:
+    def __init__(self, backend, W_shard, adapters_shard, r_cap, group=None):
+        self.be, self.W, self.ads, self.r_cap, self.group = backend, W_shard, adapters_shard, r_cap, group
+
+    def forward(self, seg_off, seg_task, x_cols):
+        """x_cols [R, K/p] (this rank's column shard) -> Y rows [R/p, N]."""
+        self.X = x_cols
+        Yp, self.Hs = self.be.fwd(seg_off, seg_task, self.ads, x_cols, self.W, self.r_cap)
+        return reduce_scatter_rows(Yp, self.group)
+
+    def backward(self, seg_off, seg_task, dy_rows):
+        """dY rows [R/p, N] -> dX_p [R, K/p]; dB_t all-reduced, dA_{t,p} local."""
+        dY = all_gather_rows(dy_rows, self.group)
+        dXp, dA, dB = self.be.bwd(seg_off, seg_task, self.ads, dY, self.X, self.W, self.Hs, self.r_cap)
+        for g in dB:
+            if g is not None:
+                all_reduce_(g, self.group)
+        return dXp, dA, dB
