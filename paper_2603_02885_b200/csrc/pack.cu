@@ -40,6 +40,14 @@ __host__ __device__ inline size_t pack_ws_bytes(int M, int S) {
   return 7 * s + 2 * align256(sizeof(int32_t) * (size_t)(M > 0 ? M : 1));
 }
 
+// Shared-memory variant: every per-sequence / per-task array lives in smem
+// when it fits (the common case: tens to a few thousand sequences).
+constexpr int kPackSmemMaxBytes = 200 * 1024;
+
+__host__ __device__ inline size_t pack_smem_bytes(int M, int S) {
+  return 7 * align256(sizeof(int32_t) * (size_t)(S + 1)) + 2 * align256(sizeof(int32_t) * (size_t)(M > 0 ? M : 1));
+}
+
 __device__ inline PackWs carve_pack_ws(void* ws, int M, int S) {
   uint8_t* b = reinterpret_cast<uint8_t*>(ws);
   const size_t s = align256(sizeof(int32_t) * (size_t)(S + 1));
@@ -78,13 +86,14 @@ __global__ void __launch_bounds__(kPackThreads, 1)
                     const int32_t* __restrict__ pack_capacity, int chunk_size, int chunk_min, int max_rows,
                     int max_chunks, int32_t* seg_off, int32_t* seq_row, int32_t* chunk_task,
                     int32_t* chunk_pack, int32_t* chunk_valid, int32_t* chunk_dep, int32_t* row_src,
-                    mux_pack_info* info, void* workspace) {
+                    mux_pack_info* info, void* workspace, int use_smem) {
   __shared__ int s_red[kPackWarps];
   __shared__ int s_bad, s_c, s_total_chunks, s_maxlen, s_valid;
+  extern __shared__ __align__(256) uint8_t pack_smem[];
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
   const int lane = tid & 31;
-  PackWs ws = carve_pack_ws(workspace, M, S);
+  PackWs ws = carve_pack_ws(use_smem ? static_cast<void*>(pack_smem) : workspace, M, S);
 
   // ---- 1. chunk size, validity, max length, valid rows -------------------
   int v2min = 30, bad = 0, mx = 0, sum = 0;
@@ -319,9 +328,18 @@ cudaError_t launch_pack(int M, int S, const int32_t* task_seq_off, const int32_t
                         int32_t* seg_off, int32_t* seq_row, int32_t* chunk_task, int32_t* chunk_pack,
                         int32_t* chunk_valid, int32_t* chunk_dep, int32_t* row_src, mux_pack_info* info,
                         void* workspace, cudaStream_t stream) {
-  mux_pack_kernel<<<1, kPackThreads, 0, stream>>>(M, S, task_seq_off, seq_len, pack_capacity, chunk_size,
-                                                  chunk_min, max_rows, max_chunks, seg_off, seq_row, chunk_task,
-                                                  chunk_pack, chunk_valid, chunk_dep, row_src, info, workspace);
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(mux_pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kPackSmemMaxBytes);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  const size_t smem = pack_smem_bytes(M, S);
+  const int use_smem = smem <= static_cast<size_t>(kPackSmemMaxBytes);
+  mux_pack_kernel<<<1, kPackThreads, use_smem ? smem : 0, stream>>>(
+      M, S, task_seq_off, seq_len, pack_capacity, chunk_size, chunk_min, max_rows, max_chunks, seg_off, seq_row,
+      chunk_task, chunk_pack, chunk_valid, chunk_dep, row_src, info, workspace, use_smem);
   return cudaGetLastError();
 }
 
