@@ -40,15 +40,30 @@
 
 namespace mux {
 
-constexpr uint32_t kStageA = kBM * kBK * 2;          // 16 KB: this CTA's 128 rows
-constexpr uint32_t kSubB = 64 * kBK * 2;             // 8 KB: one {64 x 128 B} TMA box
-constexpr uint32_t kStageB = (kBN / 2) * kBK * 2;    // 16 KB: this CTA's half of B
-constexpr uint32_t kStageBytes = kStageA + kStageB;  // 32 KB
+// Stage layout per CTA (all 128 B swizzled, 1024 B aligned):
+//   A: kKSub k-subtiles of [128 rows x 128 B] (16 KB each)
+//   B K-major (fwd): kKSub k-subtiles of [128 n-rows x 128 B]
+//   B MN-major (bwd): 2 MN atoms (64 columns each) of [kBK K-rows x 128 B]
+//   side-tile B per task group: [64 rows x 128 B] per k-subtile (8 KB each)
+constexpr uint32_t kBox = 64 * 128;                  // 8 KB: one {64 x 128 B} TMA box
+constexpr uint32_t kSubA = kBM * 128;                // 16 KB: one k-subtile of A
 constexpr uint32_t kEpiBuf = 32 * 128;               // 32 rows x 64 bf16 (one TMA store box)
-constexpr uint32_t kSmemPipe = kStages * kStageBytes;
 constexpr uint32_t kSmemEpi = 4 * 2 * kEpiBuf;
 constexpr uint32_t kSmemMisc = 1024;
-constexpr uint32_t kGemmSmemBytes = kSmemPipe + kSmemEpi + kSmemMisc + 1024;
+
+template <bool kBwd>
+struct GemmLayout {
+  static constexpr int kBK = GemmCfg<kBwd>::kBK;
+  static constexpr int kKSub = GemmCfg<kBwd>::kKSub;
+  static constexpr int kStages = GemmCfg<kBwd>::kStages;
+  static constexpr uint32_t kStageA = kKSub * kSubA;
+  static constexpr uint32_t kStageB = kKSub * 2 * kBox;     // this CTA's half of B (128 columns)
+  static constexpr uint32_t kStageBytes = kStageA + kStageB;
+  static constexpr uint32_t kAtomMN = kBK * 128;            // MN-major atom: kBK K-rows x 128 B
+  static constexpr uint32_t kSideGrp = kKSub * kBox;        // side-tile B of one task group
+  static constexpr uint32_t kSmemPipe = kStages * kStageBytes;
+  static constexpr uint32_t kSmemBytes = kSmemPipe + kSmemEpi + kSmemMisc + 1024;
+};
 constexpr uint32_t kTmemCols = 512;
 constexpr int kGemmThreads = 256;
 constexpr int kGroupM = 16;  // raster: 16 pair row-blocks (4096 rows) share a band of W tiles
@@ -119,6 +134,15 @@ __device__ __forceinline__ Tile tile_at(int t, int num_m, int num_n) {
 template <bool kBwd>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     mux_gemm_kernel(const __grid_constant__ GemmParams p) {
+  using Ly = GemmLayout<kBwd>;
+  constexpr int kBK = Ly::kBK;
+  constexpr int kKSub = Ly::kKSub;
+  constexpr int kStages = Ly::kStages;
+  constexpr uint32_t kStageA = Ly::kStageA;
+  constexpr uint32_t kStageBytes = Ly::kStageBytes;
+  constexpr uint32_t kAtomMN = Ly::kAtomMN;
+  constexpr uint32_t kSideGrp = Ly::kSideGrp;
+  constexpr uint32_t kSmemPipe = Ly::kSmemPipe;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* pipe = smem;
@@ -167,7 +191,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   const int num_m = (total_rows + kPairRows - 1) / kPairRows;
   const int num_n = (p.nout + kBN - 1) / kBN;
   const int total_tiles = num_m * (1 + (p.has_main ? num_n : 0));
-  const int num_kb = p.kred / kBK;
+  const int num_kb = (p.kred + kBK - 1) / kBK;  // a partial last block reads TMA zero fill
 
   if (warp == 0) {
     // =========================== TMA producer (both CTAs) ===============
@@ -177,10 +201,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       auto advance = [&]() {
         if (++stage == kStages) { stage = 0; phase ^= 1u; }
       };
+      const int rk = static_cast<int>(crank);
       for (int t = cid; t < total_tiles; t += ncl) {
         const Tile tl = tile_at(t, num_m, num_n);
         const PairGroups g = pair_groups(p, so, tl.m);
-        const int row_c = tl.m * kPairRows + kBM * static_cast<int>(crank);  // this CTA's rows
+        const int row_c = tl.m * kPairRows + kBM * rk;  // this CTA's rows
         if (tl.side) {
           for (int g0 = 0; g0 < g.n; g0 += 2) {
             const int ng = min(2, g.n - g0);
@@ -189,21 +214,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
               uint8_t* sa = pipe + stage * kStageBytes;
               uint8_t* sb = sa + kStageA;
               const uint32_t fb = smem_u32(&full_bar[stage]);
-              if (leader) mbar_arrive_expect_tx_u32(fb, 2u * (kStageA + ng * kSubB));
+              if (leader) mbar_arrive_expect_tx_u32(fb, 2u * (kStageA + ng * kSideGrp));
               const uint32_t fbl = mapa_shared(fb, 0);
-              tma_load_2d_pair(&p.map_a, fbl, sa, kb * kBK, row_c);
+              const int k0 = kb * kBK;
+#pragma unroll
+              for (int s2 = 0; s2 < kKSub; ++s2) tma_load_2d_pair(&p.map_a, fbl, sa + s2 * kSubA, k0 + 64 * s2, row_c);
               for (int i = 0; i < ng; ++i) {
                 const int ad = p.seg_adapter[g.seg[g0 + i]];
-                if (!kBwd)  // A_t [r, K] K-major rows j: CTA 1's rows 64.. are zero fill
-                  tma_load_2d_pair(&p.map_lora_a[ad], fbl, sb + i * kSubB, kb * kBK, 64 * static_cast<int>(crank));
-                else        // B_t [N, r] read MN-major {64 j, 64 n}
-                  tma_load_2d_pair(&p.map_lora_b[ad], fbl, sb + i * kSubB, 64 * static_cast<int>(crank), kb * kBK);
+#pragma unroll
+                for (int s2 = 0; s2 < kKSub; ++s2) {
+                  uint8_t* dst = sb + i * kSideGrp + s2 * kBox;
+                  if (!kBwd)  // A_t [r, K] K-major rows j: CTA 1's rows 64.. are zero fill
+                    tma_load_2d_pair(&p.map_lora_a[ad], fbl, dst, k0 + 64 * s2, 64 * rk);
+                  else        // B_t [N, r] read MN-major {64 j, 64 n}
+                    tma_load_2d_pair(&p.map_lora_b[ad], fbl, dst, 64 * rk, k0 + 64 * s2);
+                }
               }
               advance();
             }
           }
         } else {
-          const int col_c = tl.n * kBN + (kBN / 2) * static_cast<int>(crank);  // this CTA's half of N
+          const int col_c = tl.n * kBN + (kBN / 2) * rk;  // this CTA's half of N
           for (int kb = 0; kb < num_kb; ++kb) {
             mbar_wait(&empty_bar[stage], phase ^ 1u);
             uint8_t* sa = pipe + stage * kStageBytes;
@@ -211,13 +242,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             const uint32_t fb = smem_u32(&full_bar[stage]);
             if (leader) mbar_arrive_expect_tx_u32(fb, 2u * kStageBytes);
             const uint32_t fbl = mapa_shared(fb, 0);
-            tma_load_2d_pair(&p.map_a, fbl, sa, kb * kBK, row_c);
+            const int k0 = kb * kBK;
 #pragma unroll
-            for (int i = 0; i < 2; ++i) {
-              if (!kBwd)  // W [N, K] K-major rows n
-                tma_load_2d_pair(&p.map_w, fbl, sb + i * kSubB, kb * kBK, col_c + 64 * i);
-              else        // W viewed [k_out (MN), n (red)]: MN-major atoms of 64 k
-                tma_load_2d_pair(&p.map_w, fbl, sb + i * kSubB, col_c + 64 * i, kb * kBK);
+            for (int s2 = 0; s2 < kKSub; ++s2) {
+              tma_load_2d_pair(&p.map_a, fbl, sa + s2 * kSubA, k0 + 64 * s2, row_c);
+#pragma unroll
+              for (int i = 0; i < 2; ++i) {
+                if (!kBwd)  // W [N, K] K-major rows n: k-subtile s2, rows 64i..
+                  tma_load_2d_pair(&p.map_w, fbl, sb + s2 * kSubA + i * kBox, k0 + 64 * s2, col_c + 64 * i);
+                else        // W viewed [k_out (MN), n (red)]: atom i, K-rows 64*s2..
+                  tma_load_2d_pair(&p.map_w, fbl, sb + i * kAtomMN + s2 * kBox, col_c + 64 * i, k0 + 64 * s2);
+              }
             }
             advance();
           }
@@ -233,20 +268,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             fence_async_global();
           }
           for (int i = 0; i < g.n; ++i) {
+            // extension block: reduction = rank (<= 64): first k-subtile only
             const int ad = p.seg_adapter[g.seg[i]];
             mbar_wait(&empty_bar[stage], phase ^ 1u);
             uint8_t* sa = pipe + stage * kStageBytes;
             uint8_t* sb = sa + kStageA;
             const uint32_t fb = smem_u32(&full_bar[stage]);
-            if (leader) mbar_arrive_expect_tx_u32(fb, 2u * kStageBytes);
+            if (leader) mbar_arrive_expect_tx_u32(fb, 2u * (kSubA + 2 * kBox));
             const uint32_t fbl = mapa_shared(fb, 0);
             tma_load_2d_pair(&p.map_side, fbl, sa, 0, row_c);
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
               if (!kBwd)  // B_t [N, r] K-major rows n: box {64 j, 64 n}
-                tma_load_2d_pair(&p.map_lora_b[ad], fbl, sb + j * kSubB, 0, col_c + 64 * j);
-              else        // A_t [r, K] viewed [k_out (MN), j (red)]
-                tma_load_2d_pair(&p.map_lora_a[ad], fbl, sb + j * kSubB, col_c + 64 * j, 0);
+                tma_load_2d_pair(&p.map_lora_b[ad], fbl, sb + j * kBox, 0, col_c + 64 * j);
+              else        // A_t [r, K] viewed [k_out (MN), j (red)]: atom j, K-rows 0..63
+                tma_load_2d_pair(&p.map_lora_a[ad], fbl, sb + j * kAtomMN, col_c + 64 * j, 0);
             }
             advance();
           }
@@ -262,9 +298,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       constexpr uint32_t kIdescSide = idesc_bf16(kPairRows, kSideN, false, kBwd);
       // B operand per CTA: K-major rows of 128 B (SBO 1024), or MN-major atoms
       // of 64 elements x 64 K-rows (LBO 8 KB between atoms, SBO 1024).
-      constexpr uint32_t kBLbo = kBwd ? kSubB : 16;
-      constexpr uint32_t kBStepK = (kBwd ? 16 * 128 : 32) >> 4;  // descriptor units (16 B)
-      constexpr uint32_t kAStepK = 32 >> 4;
+      constexpr uint32_t kBLbo = kBwd ? kAtomMN : 16;
+      // start-address offset (16 B units) of k-step k (16 reduction elements)
+      auto a_off = [](int k) -> uint32_t { return ((k >> 2) * kSubA + (k & 3) * 32) >> 4; };
+      auto b_off = [](int k) -> uint32_t {
+        return kBwd ? (k * 16 * 128) >> 4 : ((k >> 2) * kSubA + (k & 3) * 32) >> 4;
+      };
+      auto side_b_off = [](int k) -> uint32_t {
+        return kBwd ? (k * 16 * 128) >> 4 : ((k >> 2) * kBox + (k & 3) * 32) >> 4;
+      };
       constexpr uint32_t kHi = desc_hi(1024);
       const uint32_t pipe_s = smem_u32(pipe);
       const uint32_t a_lo0 = desc_lo(pipe_s, 16);
@@ -298,8 +340,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                 for (int i = 0; i < ng; ++i) {
 #pragma unroll
                   for (int k = 0; k < kBK / 16; ++k)
-                    mma_bf16_pair(d_tmem, make_desc(a_lo + k * kAStepK, kHi),
-                                  make_desc(b_lo + i * (kSubB >> 4) + k * kBStepK, kHi), kIdescSide,
+                    mma_bf16_pair(d_tmem, make_desc(a_lo + a_off(k), kHi),
+                                  make_desc(b_lo + i * (kSideGrp >> 4) + side_b_off(k), kHi), kIdescSide,
                                   (kb | k) != 0, mk[i]);
                 }
                 mma_commit_pair_mc(&empty_bar[stage], kPairMask);
@@ -317,8 +359,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             if (elect_one_sync()) {
 #pragma unroll
               for (int k = 0; k < kBK / 16; ++k)
-                mma_bf16_pair_nomask(d_tmem, make_desc(a_lo + k * kAStepK, kHi),
-                                     make_desc(b_lo + k * kBStepK, kHi), kIdescMain, (kb | k) != 0);
+                mma_bf16_pair_nomask(d_tmem, make_desc(a_lo + a_off(k), kHi), make_desc(b_lo + b_off(k), kHi),
+                                     kIdescMain, (kb | k) != 0);
               mma_commit_pair_mc(&empty_bar[stage], kPairMask);
             }
             __syncwarp();
@@ -334,7 +376,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             lane_masks(g.hm[i], mk);
             if (elect_one_sync()) {
               for (int k = 0; k < nk; ++k)
-                mma_bf16_pair(d_tmem, make_desc(a_lo + k * kAStepK, kHi), make_desc(b_lo + k * kBStepK, kHi),
+                mma_bf16_pair(d_tmem, make_desc(a_lo + a_off(k), kHi), make_desc(b_lo + b_off(k), kHi),
                               kIdescMain, 1u, mk);
               mma_commit_pair_mc(&empty_bar[stage], kPairMask);
             }
@@ -454,11 +496,11 @@ cudaError_t launch_gemm_impl(const GemmParams& p, int grid, cudaStream_t stream)
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(mux_gemm_kernel<kBwd>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kGemmSmemBytes));
+                                         static_cast<int>(GemmLayout<kBwd>::kSmemBytes));
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  mux_gemm_kernel<kBwd><<<grid, kGemmThreads, kGemmSmemBytes, stream>>>(p);
+  mux_gemm_kernel<kBwd><<<grid, kGemmThreads, GemmLayout<kBwd>::kSmemBytes, stream>>>(p);
   return cudaGetLastError();
 }
 

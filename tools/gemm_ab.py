@@ -64,7 +64,7 @@ def main():
                 B.copy_(torch.randn(N, a.rank, device="cuda").bfloat16())
                 ads.append(mux.Adapter((torch.randn(a.rank, K, device="cuda") / K ** 0.5).bfloat16(), B,
                                        a.rank, 2.0))
-            r_cap = 16 * -(-a.rank // 16)
+            r_cap = max(16, 16 * -(-a.rank // 16))
             Y = torch.empty(R, N, dtype=torch.bfloat16, device="cuda")
             Hs = torch.empty(R, r_cap, dtype=torch.bfloat16, device="cuda")
             dX = torch.empty(R, K, dtype=torch.bfloat16, device="cuda")
