@@ -359,8 +359,15 @@ def main_arm(args):
     bwd_flops = sum((2 * L.K * L.N + 4 * max(w.wl.ranks) * (L.K + L.N)) * w.T for L in w.linears) * args.steps
     pk = peaks()
     achieved = fwd_flops / (fwd_ms * 1e-3) / 1e12
+    traffic, traffic_src = None, None
+    tp = os.path.join(ROOT, "profiles", "gemm_fwd_traffic.json")
+    if os.path.exists(tp):
+        tj = json.load(open(tp))
+        traffic, traffic_src = tj.get("mean_bytes_per_launch"), tj.get("source")
     roof = {"bound": "tensor", "achieved": achieved, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
-            "frac": achieved / pk["bf16_tflops"], "traffic": None,
+            "frac": achieved / pk["bf16_tflops"], "traffic": traffic, "traffic_source": traffic_src,
+            "algorithmic_bytes_per_launch": sum(2 * (w.T * (L.K + L.N) + L.K * L.N) for L in w.linears)
+            / len(w.linears),
             "kernel": "mux_gemm_kernel<fwd> (fused backbone + LoRA; events around each mux_linear_fwd call)",
             "peak_source": pk["source"] + " burst bf16 (cuBLAS 8192^3)"}
 
