@@ -123,7 +123,7 @@ class MuxStep:
                 "Y": torch.empty(self.max_rows, L.N, dtype=torch.bfloat16, device=dev),
                 "Hs": torch.empty(self.max_rows, self.r_cap, dtype=torch.bfloat16, device=dev),
                 "dX": torch.empty(self.max_rows, L.K, dtype=torch.bfloat16, device=dev),
-                "ws": torch.empty(mux.linear_workspace_size(w.M, self.max_rows, L.K, L.N, self.r_cap),
+                "ws": torch.zeros(mux.linear_workspace_size(w.M, self.max_rows, L.K, L.N, self.r_cap),
                                   dtype=torch.uint8, device=dev),
             })
         self.X1 = torch.empty(self.max_rows, w.linears[0].K, dtype=torch.bfloat16, device=dev)

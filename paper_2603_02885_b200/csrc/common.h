@@ -42,13 +42,16 @@ struct GemmParams {
   CUtensorMap map_lora_b[MUX_MAX_ADAPTERS];
   const int32_t* seg_off;        // device [num_segs + 1]
   __nv_bfloat16* side_out;       // Hs / Gs [max_rows, r_cap]
-  int32_t* flags;                // [ceil(max_rows/256)] zeroed before launch
+  unsigned long long* flags;     // [ceil(max_rows/256)] epoch-tagged (workspace, zeroed once)
+  unsigned long long* epoch;     // workspace launch epoch; bumped by the last CTA to finish
+  unsigned int* done;            // CTAs finished in this launch (reset by the last one)
   int32_t num_segs;
   int32_t max_rows;
   int32_t kred;                  // reduction length of the main product (K fwd, N bwd)
   int32_t nout;                  // output columns (N fwd, K bwd)
   int32_t r_cap;
   int32_t has_main;              // 0: only the shrink (side) tiles
+  int32_t group_m;               // raster band: pair row-blocks sharing a sweep over W tiles
   int32_t seg_adapter[MUX_MAX_SEGMENTS];
   int32_t seg_rank[MUX_MAX_SEGMENTS];
   float seg_scale[MUX_MAX_SEGMENTS];

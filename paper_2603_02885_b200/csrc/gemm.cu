@@ -66,7 +66,6 @@ struct GemmLayout {
 };
 constexpr uint32_t kTmemCols = 512;
 constexpr int kGemmThreads = 256;
-constexpr int kGroupM = 16;  // raster: 16 pair row-blocks (4096 rows) share a band of W tiles
 constexpr uint16_t kPairMask = 0x3;
 
 // Tasks present in a 256-row pair tile.  hm = bit h set: the group owns rows
@@ -113,17 +112,20 @@ struct Tile {
   bool side;
 };
 
-__device__ __forceinline__ Tile tile_at(int t, int num_m, int num_n) {
+// Raster: bands of `group_m` pair row-blocks; inside a band the row block
+// varies fastest, so the band's A rows stay L2-resident while W tiles stream
+// through once per band (group_m is sized on the host so the band fits L2).
+__device__ __forceinline__ Tile tile_at(int t, int num_m, int num_n, int group_m) {
   Tile r;
   if (t < num_m) {
     r.m = t; r.n = 0; r.side = true;
     return r;
   }
   const int v = t - num_m;
-  const int per_group = kGroupM * num_n;
+  const int per_group = group_m * num_n;
   const int grp = v / per_group;
-  const int first_m = grp * kGroupM;
-  const int gm = min(num_m - first_m, kGroupM);
+  const int first_m = grp * group_m;
+  const int gm = min(num_m - first_m, group_m);
   const int w = v - grp * per_group;
   r.m = first_m + w % gm;
   r.n = w / gm;
@@ -162,7 +164,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   const int cid = static_cast<int>(cluster_id_x());
   const int ncl = static_cast<int>(nclusters_x());
 
-  for (int i = threadIdx.x; i <= p.num_segs; i += blockDim.x) so[i] = p.seg_off[i];
   if (warp == 0 && lane == 0) {
     tma_prefetch(&p.map_a);
     tma_prefetch(&p.map_w);
@@ -181,6 +182,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc_pair<kTmemCols>(tmem_holder);
+  // --- everything above overlaps the previous kernel (PDL); inputs below ---
+  griddep_wait();
+  griddep_launch_dependents();
+  for (int i = threadIdx.x; i <= p.num_segs; i += blockDim.x) so[i] = p.seg_off[i];
+  const unsigned long long epoch = *reinterpret_cast<volatile unsigned long long*>(p.epoch) + 1ull;
   tc_fence_before();
   __syncthreads();
   cluster_sync();
@@ -203,7 +209,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       };
       const int rk = static_cast<int>(crank);
       for (int t = cid; t < total_tiles; t += ncl) {
-        const Tile tl = tile_at(t, num_m, num_n);
+        const Tile tl = tile_at(t, num_m, num_n, p.group_m);
         const PairGroups g = pair_groups(p, so, tl.m);
         const int row_c = tl.m * kPairRows + kBM * rk;  // this CTA's rows
         if (tl.side) {
@@ -258,10 +264,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           }
           if (g.n > 0) {
             // the side tile of this row block must have published Hs/Gs
-            const int* flag = p.flags + tl.m;
-            if (ld_acquire_gpu(flag) < 8) {
+            const unsigned long long* flag = p.flags + tl.m;
+            const unsigned long long want = (epoch << 8) | 8ull;
+            if (ld_acquire_gpu_u64(flag) != want) {
               const uint64_t t0 = globaltimer_ns();
-              while (ld_acquire_gpu(flag) < 8) {
+              while (ld_acquire_gpu_u64(flag) != want) {
                 if (globaltimer_ns() - t0 > kWatchdogNs) __trap();
               }
             }
@@ -320,7 +327,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         if (++stage == kStages) { stage = 0; phase ^= 1u; }
       };
       for (int t = cid; t < total_tiles; t += ncl) {
-        const Tile tl = tile_at(t, num_m, num_n);
+        const Tile tl = tile_at(t, num_m, num_n, p.group_m);
         const PairGroups g = pair_groups(p, so, tl.m);
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1u);
         tc_fence_after();
@@ -397,7 +404,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     uint8_t* bufs = epi + q * 2 * kEpiBuf;
     int buf_sel = 0;
     for (int t = cid; t < total_tiles; t += ncl) {
-      const Tile tl = tile_at(t, num_m, num_n);
+      const Tile tl = tile_at(t, num_m, num_n, p.group_m);
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const int row_w = tl.m * kPairRows + kBM * static_cast<int>(crank) + 32 * q;  // first row of this warp
@@ -437,7 +444,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         fence_async_global();
         __threadfence();
         __syncwarp();
-        if (lane == 0) red_release_gpu_add(p.flags + tl.m, 1);
+        if (lane == 0) flag_arrive(p.flags + tl.m, epoch);
       } else {
         const bool valid = row_w < total_rows;
         const int col_t = tl.n * kBN;
@@ -488,6 +495,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     tc_fence_after();
     tmem_dealloc_pair<kTmemCols>(tmem_base);
   }
+  if (threadIdx.x == 0) {
+    // the last CTA out advances the workspace epoch for the next launch
+    __threadfence();
+    if (atomicAdd(p.done, 1u) == gridDim.x - 1) {
+      *p.done = 0u;
+      *reinterpret_cast<volatile unsigned long long*>(p.epoch) = epoch;
+      __threadfence();
+    }
+  }
 }
 
 // ---------------------------------------------------------------- launchers
@@ -500,8 +516,17 @@ cudaError_t launch_gemm_impl(const GemmParams& p, int grid, cudaStream_t stream)
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  mux_gemm_kernel<kBwd><<<grid, kGemmThreads, GemmLayout<kBwd>::kSmemBytes, stream>>>(p);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = GemmLayout<kBwd>::kSmemBytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, mux_gemm_kernel<kBwd>, p);
 }
 
 // grid must be even (clusters of 2)

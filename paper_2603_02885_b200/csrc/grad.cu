@@ -42,7 +42,6 @@ __global__ void __launch_bounds__(kGradThreads, 1) mux_grad_kernel(const __grid_
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  for (int i = threadIdx.x; i <= p.num_segs; i += blockDim.x) so[i] = p.seg_off[i];
   if (warp == 0 && lane == 0) {
     tma_prefetch(&p.map_x);
     tma_prefetch(&p.map_dy);
@@ -61,6 +60,9 @@ __global__ void __launch_bounds__(kGradThreads, 1) mux_grad_kernel(const __grid_
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<kGradTmemCols>(tmem_holder);
+  griddep_wait();  // PDL: the prologue above overlaps the previous kernel
+  griddep_launch_dependents();
+  for (int i = threadIdx.x; i <= p.num_segs; i += blockDim.x) so[i] = p.seg_off[i];
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -191,8 +193,17 @@ cudaError_t launch_grad(const GradParams& p, int grid, cudaStream_t stream) {
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  mux_grad_kernel<<<grid, kGradThreads, kGradSmemBytes, stream>>>(p);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kGradThreads);
+  cfg.dynamicSmemBytes = kGradSmemBytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, mux_grad_kernel, p);
 }
 
 }  // namespace mux

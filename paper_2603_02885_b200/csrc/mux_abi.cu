@@ -138,9 +138,13 @@ int num_sms() {
   return n;
 }
 
-// ---- linear-layer workspace: [flags][Gs][Hs scratch]
+// ---- linear-layer workspace: [epoch, done][flags][Gs][Hs scratch]
+// Zero-filled once by the caller; the GEMM kernel keeps it consistent across
+// launches (epoch-tagged flags, see ptx.cuh flag_arrive), so no per-call memset.
 struct LinearWs {
-  int32_t* flags;
+  unsigned long long* epoch;
+  unsigned int* done;
+  unsigned long long* flags;
   __nv_bfloat16* gs;
   __nv_bfloat16* hs;
   size_t bytes;
@@ -148,13 +152,16 @@ struct LinearWs {
 LinearWs carve_linear_ws(void* base, int32_t max_rows, int32_t r_cap) {
   LinearWs w{};
   const size_t n_m = (static_cast<size_t>(max_rows) + kPairRows - 1) / kPairRows;
-  const size_t f = align256(n_m * sizeof(int32_t));
+  const size_t h = 256;
+  const size_t f = align256(n_m * sizeof(unsigned long long));
   const size_t g = align256(static_cast<size_t>(max_rows) * r_cap * 2);
   uint8_t* b = reinterpret_cast<uint8_t*>(base);
-  w.flags = reinterpret_cast<int32_t*>(b);
-  w.gs = reinterpret_cast<__nv_bfloat16*>(b ? b + f : nullptr);
-  w.hs = reinterpret_cast<__nv_bfloat16*>(b ? b + f + g : nullptr);
-  w.bytes = f + 2 * g;
+  w.epoch = reinterpret_cast<unsigned long long*>(b);
+  w.done = reinterpret_cast<unsigned int*>(b ? b + 8 : nullptr);
+  w.flags = reinterpret_cast<unsigned long long*>(b ? b + h : nullptr);
+  w.gs = reinterpret_cast<__nv_bfloat16*>(b ? b + h + f : nullptr);
+  w.hs = reinterpret_cast<__nv_bfloat16*>(b ? b + h + f + g : nullptr);
+  w.bytes = h + f + 2 * g;
   return w;
 }
 
@@ -310,12 +317,21 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
   p.seg_off = seg_off;
   p.side_out = side;
   p.flags = ws.flags;
+  p.epoch = ws.epoch;
+  p.done = ws.done;
   p.num_segs = num_segs;
   p.max_rows = max_rows;
   p.kred = kred;
   p.nout = nout;
   p.r_cap = r_cap;
   p.has_main = out != nullptr;
+  // raster band: keep the band's A rows (group_m * 256 rows * kred * 2 B)
+  // within ~48 MB of the 126 MB L2, leaving room for the streamed W tiles
+  {
+    const long long band_bytes = static_cast<long long>(kPairRows) * kred * 2;
+    long long g = (48ll << 20) / band_bytes;
+    p.group_m = static_cast<int32_t>(std::max(4ll, std::min(32ll, g)));
+  }
   for (int s = 0; s < num_segs; ++s) {
     const mux_adapter& a = adapters[seg_task[s]];
     p.seg_adapter[s] = seg_task[s];
@@ -328,9 +344,7 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
   // one CTA pair (cluster of 2) per tile in flight; grid = #SMs rounded to pairs
   const long long pairs = std::min<long long>(tiles_max, num_sms() / 2);
   const int grid = static_cast<int>(2 * std::max<long long>(pairs, 1));
-  cudaError_t e = cudaMemsetAsync(ws.flags, 0, sizeof(int32_t) * num_m_max, stream);
-  if (e != cudaSuccess) return cuda_fail(e, "flag reset");
-  e = launch_gemm(p, bwd, grid, stream);
+  cudaError_t e = launch_gemm(p, bwd, grid, stream);
   if (e != cudaSuccess) return cuda_fail(e, bwd ? "mux_linear_bwd dX launch" : "mux_linear_fwd launch");
 
   if (bwd) {

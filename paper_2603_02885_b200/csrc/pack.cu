@@ -94,6 +94,8 @@ __global__ void __launch_bounds__(kPackThreads, 1)
   const int warp = tid >> 5;
   const int lane = tid & 31;
   PackWs ws = carve_pack_ws(use_smem ? static_cast<void*>(pack_smem) : workspace, M, S);
+  griddep_wait();  // PDL: inputs may come from the previous kernel
+  griddep_launch_dependents();
 
   // ---- 1. chunk size, validity, max length, valid rows -------------------
   int v2min = 30, bad = 0, mx = 0, sum = 0;
@@ -308,6 +310,8 @@ __global__ void __launch_bounds__(kPackThreads, 1)
 // Dispatch gather: 16-byte vectors, one warp-row at a time.
 __global__ void mux_pack_apply_kernel(int max_rows, int cols, int num_tokens, const int32_t* __restrict__ row_src,
                                       const uint4* __restrict__ src, uint4* __restrict__ dst) {
+  griddep_wait();
+  griddep_launch_dependents();
   const int vec_per_row = cols / 8;
   const long long total = static_cast<long long>(max_rows) * vec_per_row;
   for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
@@ -337,10 +341,19 @@ cudaError_t launch_pack(int M, int S, const int32_t* task_seq_off, const int32_t
   }
   const size_t smem = pack_smem_bytes(M, S);
   const int use_smem = smem <= static_cast<size_t>(kPackSmemMaxBytes);
-  mux_pack_kernel<<<1, kPackThreads, use_smem ? smem : 0, stream>>>(
-      M, S, task_seq_off, seq_len, pack_capacity, chunk_size, chunk_min, max_rows, max_chunks, seg_off, seq_row,
-      chunk_task, chunk_pack, chunk_valid, chunk_dep, row_src, info, workspace, use_smem);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(kPackThreads);
+  cfg.dynamicSmemBytes = use_smem ? smem : 0;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, mux_pack_kernel, M, S, task_seq_off, seq_len, pack_capacity, chunk_size, chunk_min,
+                            max_rows, max_chunks, seg_off, seq_row, chunk_task, chunk_pack, chunk_valid, chunk_dep,
+                            row_src, info, workspace, use_smem);
 }
 
 cudaError_t launch_pack_apply(int max_rows, int cols, int num_tokens, const int32_t* row_src,
@@ -350,9 +363,18 @@ cudaError_t launch_pack_apply(int max_rows, int cols, int num_tokens, const int3
   long long blocks = (total + 255) / 256;
   const long long cap = static_cast<long long>(num_sms) * 8;
   if (blocks > cap) blocks = cap;
-  mux_pack_apply_kernel<<<static_cast<int>(blocks), 256, 0, stream>>>(
-      max_rows, cols, num_tokens, row_src, reinterpret_cast<const uint4*>(src), reinterpret_cast<uint4*>(dst));
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(blocks));
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, mux_pack_apply_kernel, max_rows, cols, num_tokens, row_src,
+                            reinterpret_cast<const uint4*>(src), reinterpret_cast<uint4*>(dst));
 }
 
 }  // namespace mux

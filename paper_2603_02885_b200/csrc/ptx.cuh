@@ -124,6 +124,38 @@ __device__ __forceinline__ void red_release_gpu_add(int* p, int v) {
   asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+
+// --------------------------------------------------------------- programmatic dependent launch
+// Wait until every grid this one depends on (the previous kernel in the
+// stream) has completed and its memory is visible; everything before this
+// call (smem carve-up, barrier init, TMEM alloc, descriptor prefetch)
+// overlaps the predecessor's tail.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Allow the next kernel in the stream to be scheduled (it still waits in its
+// own griddep_wait for this grid to complete).
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// --------------------------------------------------------------- epoch-tagged flags
+// A 64-bit flag = (epoch << 8) | count.  Publishing adds 1 to the count of the
+// current epoch (resetting the count when the stored epoch is older), so a
+// workspace is reused across launches without a memset.
+__device__ __forceinline__ void flag_arrive(unsigned long long* f, unsigned long long epoch) {
+  unsigned long long old = *reinterpret_cast<volatile unsigned long long*>(f);
+  while (true) {
+    const unsigned long long want = ((old >> 8) == epoch) ? old + 1 : ((epoch << 8) | 1ull);
+    const unsigned long long got = atomicCAS(f, old, want);
+    if (got == old) break;
+    old = got;
+  }
+}
+__device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
 // --------------------------------------------------------------- tcgen05
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem) {

@@ -227,7 +227,7 @@ def linear_fwd(seg_off: torch.Tensor, seg_task: Sequence[int], adapters: Sequenc
         Hs = torch.empty(max_rows, r_cap, dtype=torch.bfloat16, device=dev)
     S = len(seg_task)
     if workspace is None:
-        workspace = torch.empty(linear_workspace_size(S, max_rows, K, N, r_cap), dtype=torch.uint8, device=dev)
+        workspace = torch.zeros(linear_workspace_size(S, max_rows, K, N, r_cap), dtype=torch.uint8, device=dev)
     tab = _adapter_table(adapters, False)
     st = _i32_host(seg_task)
     _check(lib().mux_linear_fwd(S, _ptr(seg_off), st, len(adapters), tab, max_rows, K, N, r_cap,
@@ -253,7 +253,7 @@ def linear_bwd(seg_off: torch.Tensor, seg_task: Sequence[int], adapters: Sequenc
                 a.dB = torch.empty(N, a.rank, dtype=torch.float32, device=dev)
     S = len(seg_task)
     if workspace is None:
-        workspace = torch.empty(linear_workspace_size(S, max_rows, K, N, r_cap), dtype=torch.uint8, device=dev)
+        workspace = torch.zeros(linear_workspace_size(S, max_rows, K, N, r_cap), dtype=torch.uint8, device=dev)
     tab = _adapter_table(adapters, True)
     st = _i32_host(seg_task)
     _check(lib().mux_linear_bwd(S, _ptr(seg_off), st, len(adapters), tab, max_rows, K, N, r_cap,

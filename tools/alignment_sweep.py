@@ -117,7 +117,7 @@ def main():
                             ads.append(mux.Adapter((torch.randn(rank, K, device="cuda") / K ** 0.5).bfloat16(), B,
                                                    rank, 2.0))
                         layers.append({"W": (torch.randn(N, K, device="cuda") / K ** 0.5).bfloat16(), "ads": ads,
-                                       "ws": torch.empty(mux.linear_workspace_size(M, R, K, N, r_cap),
+                                       "ws": torch.zeros(mux.linear_workspace_size(M, R, K, N, r_cap),
                                                          dtype=torch.uint8, device="cuda")})
                     ms = run(mux, seg_off, R, layers, r_cap)
                     eff = T / (ms * 1e-3)

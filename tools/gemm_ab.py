@@ -68,7 +68,7 @@ def main():
             Y = torch.empty(R, N, dtype=torch.bfloat16, device="cuda")
             Hs = torch.empty(R, r_cap, dtype=torch.bfloat16, device="cuda")
             dX = torch.empty(R, K, dtype=torch.bfloat16, device="cuda")
-            ws = torch.empty(mux.linear_workspace_size(a.tasks, R, K, N, r_cap), dtype=torch.uint8, device="cuda")
+            ws = torch.zeros(mux.linear_workspace_size(a.tasks, R, K, N, r_cap), dtype=torch.uint8, device="cuda")
             st = list(range(a.tasks))
             f = lambda: mux.linear_fwd(seg_off, st, ads, X, W, r_cap, Y=Y, Hs=Hs, workspace=ws)  # noqa: E731
             ms = timeit(f, a.iters)
