@@ -131,7 +131,7 @@ class MuxStep:
         self.launches_per_step = 1 + 2 + len(self.layers) + 2 * len(self.layers)
         self.fwd_events = None
 
-    def step(self, record=None, slot=0):
+    def step(self, record=None, slot=0, before_bwd=None):
         mux, w = self.mux, self.w
         mux.pack_chunks(self.tso[slot], self.sl[slot], self.cap, 0, 64, max_rows=self.max_rows,
                         max_chunks=self.max_chunks, out=self.pk)
@@ -147,6 +147,8 @@ class MuxStep:
                 record("fwd", li, 1)
             x = ly["Y"]
         mux.pack_apply(self.pk["row_src"], self.dY3tok[slot], self.max_rows, out=self.dY3)
+        if before_bwd is not None:
+            before_bwd()
         dy = self.dY3
         for li in reversed(range(len(self.layers))):
             ly = self.layers[li]
@@ -388,6 +390,8 @@ def main_arm(args):
         copy_stream = torch.cuda.Stream()
         copied = [torch.cuda.Event() for _ in range(2)]
         consumed = [torch.cuda.Event() for _ in range(2)]
+        step_done = torch.cuda.Event()
+        d2h_done = torch.cuda.Event()
 
         def h2d_copy(i):
             slot = i % 2
@@ -400,16 +404,23 @@ def main_arm(args):
         def e2e_run(n):
             for ev in consumed:
                 ev.record(stream)
+            d2h_done.record(stream)
             h2d_copy(0)
             for i in range(n):
                 slot = i % 2
                 if i + 1 < n:
                     h2d_copy(i + 1)
                 stream.wait_event(copied[slot])
-                ms.step(slot=slot)
+                # the gradient read-back of step i-1 (copy stream) must finish
+                # before this step's backward overwrites dA/dB
+                ms.step(slot=slot, before_bwd=lambda: stream.wait_event(d2h_done))
                 consumed[slot].record(stream)
-                for g, hg in zip(grads, h_grads):
-                    hg.copy_(g, non_blocking=True)
+                step_done.record(stream)
+                with torch.cuda.stream(copy_stream):
+                    copy_stream.wait_event(step_done)
+                    for g, hg in zip(grads, h_grads):
+                        hg.copy_(g, non_blocking=True)
+                    d2h_done.record(copy_stream)
 
         e2e_run(max(1, args.warmup))
         torch.cuda.synchronize()
@@ -430,7 +441,8 @@ def main_arm(args):
         e2e = {"value": world * w.T / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms,
                "what": "pinned H2D of seq metadata + token-major layer input X and loss gradient dY (prefetched "
-                       "one step ahead on a copy stream); D2H of every adapter gradient dA_t/dB_t (fp32)"}
+                       "one step ahead on a copy stream); D2H of every adapter gradient dA_t/dB_t (fp32) on "
+                       "the copy stream, overlapped with the next step's forward"}
 
     value = world * w.T / (ms_step * 1e-3)
     tflops = w.flops / (ms_step * 1e-3) / 1e12

@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(kPackThreads, 1)
                     int32_t* chunk_pack, int32_t* chunk_valid, int32_t* chunk_dep, int32_t* row_src,
                     mux_pack_info* info, void* workspace, int use_smem) {
   __shared__ int s_red[kPackWarps];
-  __shared__ int s_bad, s_c, s_total_chunks, s_maxlen, s_valid;
+  __shared__ int s_bad, s_ovf, s_c, s_total_chunks, s_maxlen, s_valid;
   extern __shared__ __align__(256) uint8_t pack_smem[];
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
@@ -241,10 +241,10 @@ __global__ void __launch_bounds__(kPackThreads, 1)
     r.zero_pad_rows = S * s_maxlen;
     r.overflow = ovf;
     *info = r;
-    s_bad = ovf;
+    s_ovf = ovf;  // separate flag: other threads may still be reading s_bad above
   }
   __syncthreads();
-  if (s_bad) return;
+  if (s_ovf) return;
   const int total_chunks = s_total_chunks;
   for (int t = tid; t <= M; t += kPackThreads) seg_off[t] = (t < M ? ws.task_chunks[t] : total_chunks) * c;
 
