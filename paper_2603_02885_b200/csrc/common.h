@@ -19,12 +19,29 @@ constexpr int kBN = 256;        // output columns per tile (TMEM columns per acc
 // Reduction depth per pipeline stage: 64 (6 stages) for the forward kernel,
 // 128 (3 stages) for the backward dX kernel (measured best for each,
 // profiles/r01_gemm_ab_bk.jsonl).  Both keep 192 KB of operands in flight.
+#ifdef MUX_EPI_DIRECT
+// epilogue stores straight from registers: the 32 KB staging area becomes a 7th stage
+template <bool kBwd>
+struct GemmCfg {
+  static constexpr int kBK = 64;
+  static constexpr int kKSub = 1;
+  static constexpr int kStages = 7;
+};
+#elif defined(MUX_BWD_BK64)
+template <bool kBwd>
+struct GemmCfg {
+  static constexpr int kBK = 64;
+  static constexpr int kKSub = 1;
+  static constexpr int kStages = 6;
+};
+#else
 template <bool kBwd>
 struct GemmCfg {
   static constexpr int kBK = kBwd ? 128 : 64;
   static constexpr int kKSub = kBK / 64;  // 128 B swizzle rows (64 bf16) per stage row
   static constexpr int kStages = kBwd ? 3 : 6;
 };
+#endif
 constexpr int kRowQuarter = 64; // segment granularity inside a pair tile (chunk minimum)
 constexpr int kSideN = 128;     // N of the shrink MMA (rank padded to 64 in CTA 0's half)
 
@@ -42,6 +59,7 @@ struct GemmParams {
   CUtensorMap map_lora_b[MUX_MAX_ADAPTERS];
   const int32_t* seg_off;        // device [num_segs + 1]
   __nv_bfloat16* side_out;       // Hs / Gs [max_rows, r_cap]
+  __nv_bfloat16* out;            // Y / dX [max_rows, nout] (direct-store epilogue variant)
   unsigned long long* flags;     // [ceil(max_rows/256)] epoch-tagged (workspace, zeroed once)
   unsigned long long* epoch;     // workspace launch epoch; bumped by the last CTA to finish
   unsigned int* done;            // CTAs finished in this launch (reset by the last one)
@@ -52,6 +70,7 @@ struct GemmParams {
   int32_t r_cap;
   int32_t has_main;              // 0: only the shrink (side) tiles
   int32_t group_m;               // raster band: pair row-blocks sharing a sweep over W tiles
+  unsigned long long* dbg;       // MUX_PROFILE builds only: wait-cycle counters (see gemm.cu)
   int32_t seg_adapter[MUX_MAX_SEGMENTS];
   int32_t seg_rank[MUX_MAX_SEGMENTS];
   float seg_scale[MUX_MAX_SEGMENTS];

@@ -48,7 +48,11 @@ namespace mux {
 constexpr uint32_t kBox = 64 * 128;                  // 8 KB: one {64 x 128 B} TMA box
 constexpr uint32_t kSubA = kBM * 128;                // 16 KB: one k-subtile of A
 constexpr uint32_t kEpiBuf = 32 * 128;               // 32 rows x 64 bf16 (one TMA store box)
+#ifdef MUX_EPI_DIRECT
+constexpr uint32_t kSmemEpi = 0;
+#else
 constexpr uint32_t kSmemEpi = 4 * 2 * kEpiBuf;
+#endif
 constexpr uint32_t kSmemMisc = 1024;
 
 template <bool kBwd>
@@ -133,6 +137,18 @@ __device__ __forceinline__ Tile tile_at(int t, int num_m, int num_n, int group_m
   return r;
 }
 
+// Opt-in instrumentation (-DMUX_PROFILE, experiment builds only): per-role
+// cycles spent waiting on each barrier, accumulated into GemmParams::dbg:
+//   [0] MMA total  [1] MMA wait full  [2] MMA wait tmem-empty
+//   [3] producer total [4] producer wait empty  [5] epilogue total [6] epilogue wait tmem-full
+#ifdef MUX_PROFILE
+#define PROF_T0(v) const long long v = clock64()
+#define PROF_ADD(acc, t0) acc += clock64() - (t0)
+#else
+#define PROF_T0(v)
+#define PROF_ADD(acc, t0)
+#endif
+
 template <bool kBwd>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     mux_gemm_kernel(const __grid_constant__ GemmParams p) {
@@ -199,15 +215,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   const int total_tiles = num_m * (1 + (p.has_main ? num_n : 0));
   const int num_kb = (p.kred + kBK - 1) / kBK;  // a partial last block reads TMA zero fill
 
+#ifdef MUX_PROFILE
+  long long pw_empty = 0, mw_full = 0, mw_tempty = 0, ew_tfull = 0;
+  const long long t_role0 = clock64();
+#endif
   if (warp == 0) {
     // =========================== TMA producer (both CTAs) ===============
-    if (lane == 0) {
+    // Warp-uniform loop; one elected lane issues (operands stay in uniform
+    // registers: the producer's issue rate bounds the pipeline).
+    {
       int stage = 0;
       uint32_t phase = 0;
       auto advance = [&]() {
         if (++stage == kStages) { stage = 0; phase ^= 1u; }
       };
       const int rk = static_cast<int>(crank);
+      const uint32_t pipe_u = smem_u32(pipe);
+      const uint32_t full_u = smem_u32(full_bar);
+      const uint32_t full_leader = mapa_shared(full_u, 0);  // stage s barrier: + 8 s
       for (int t = cid; t < total_tiles; t += ncl) {
         const Tile tl = tile_at(t, num_m, num_n, p.group_m);
         const PairGroups g = pair_groups(p, so, tl.m);
@@ -215,82 +240,99 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         if (tl.side) {
           for (int g0 = 0; g0 < g.n; g0 += 2) {
             const int ng = min(2, g.n - g0);
+            const int ad0 = p.seg_adapter[g.seg[g0]];
+            const int ad1 = ng > 1 ? p.seg_adapter[g.seg[g0 + 1]] : ad0;
             for (int kb = 0; kb < num_kb; ++kb) {
+              PROF_T0(tw_);
               mbar_wait(&empty_bar[stage], phase ^ 1u);
-              uint8_t* sa = pipe + stage * kStageBytes;
-              uint8_t* sb = sa + kStageA;
-              const uint32_t fb = smem_u32(&full_bar[stage]);
-              if (leader) mbar_arrive_expect_tx_u32(fb, 2u * (kStageA + ng * kSideGrp));
-              const uint32_t fbl = mapa_shared(fb, 0);
-              const int k0 = kb * kBK;
+              PROF_ADD(pw_empty, tw_);
+              if (elect_one_sync()) {
+                const uint32_t sa = pipe_u + stage * kStageBytes;
+                const uint32_t sb = sa + kStageA;
+                const uint32_t fbl = full_leader + 8u * stage;
+                if (leader) mbar_arrive_expect_tx_u32(full_u + 8u * stage, 2u * (kStageA + ng * kSideGrp));
+                const int k0 = kb * kBK;
 #pragma unroll
-              for (int s2 = 0; s2 < kKSub; ++s2) tma_load_2d_pair(&p.map_a, fbl, sa + s2 * kSubA, k0 + 64 * s2, row_c);
-              for (int i = 0; i < ng; ++i) {
-                const int ad = p.seg_adapter[g.seg[g0 + i]];
+                for (int s2 = 0; s2 < kKSub; ++s2) tma_load_2d_pair_u32(&p.map_a, fbl, sa + s2 * kSubA, k0 + 64 * s2, row_c);
+                for (int i = 0; i < ng; ++i) {
+                  const int ad = i == 0 ? ad0 : ad1;
 #pragma unroll
-                for (int s2 = 0; s2 < kKSub; ++s2) {
-                  uint8_t* dst = sb + i * kSideGrp + s2 * kBox;
-                  if (!kBwd)  // A_t [r, K] K-major rows j: CTA 1's rows 64.. are zero fill
-                    tma_load_2d_pair(&p.map_lora_a[ad], fbl, dst, k0 + 64 * s2, 64 * rk);
-                  else        // B_t [N, r] read MN-major {64 j, 64 n}
-                    tma_load_2d_pair(&p.map_lora_b[ad], fbl, dst, 64 * rk, k0 + 64 * s2);
+                  for (int s2 = 0; s2 < kKSub; ++s2) {
+                    const uint32_t dst = sb + i * kSideGrp + s2 * kBox;
+                    if (!kBwd)  // A_t [r, K] K-major rows j: CTA 1's rows 64.. are zero fill
+                      tma_load_2d_pair_u32(&p.map_lora_a[ad], fbl, dst, k0 + 64 * s2, 64 * rk);
+                    else        // B_t [N, r] read MN-major {64 j, 64 n}
+                      tma_load_2d_pair_u32(&p.map_lora_b[ad], fbl, dst, 64 * rk, k0 + 64 * s2);
+                  }
                 }
               }
+              __syncwarp();
               advance();
             }
           }
         } else {
           const int col_c = tl.n * kBN + (kBN / 2) * rk;  // this CTA's half of N
           for (int kb = 0; kb < num_kb; ++kb) {
+            PROF_T0(tw_);
             mbar_wait(&empty_bar[stage], phase ^ 1u);
-            uint8_t* sa = pipe + stage * kStageBytes;
-            uint8_t* sb = sa + kStageA;
-            const uint32_t fb = smem_u32(&full_bar[stage]);
-            if (leader) mbar_arrive_expect_tx_u32(fb, 2u * kStageBytes);
-            const uint32_t fbl = mapa_shared(fb, 0);
-            const int k0 = kb * kBK;
+            PROF_ADD(pw_empty, tw_);
+            if (elect_one_sync()) {
+              const uint32_t sa = pipe_u + stage * kStageBytes;
+              const uint32_t sb = sa + kStageA;
+              const uint32_t fbl = full_leader + 8u * stage;
+              if (leader) mbar_arrive_expect_tx_u32(full_u + 8u * stage, 2u * kStageBytes);
+              const int k0 = kb * kBK;
 #pragma unroll
-            for (int s2 = 0; s2 < kKSub; ++s2) {
-              tma_load_2d_pair(&p.map_a, fbl, sa + s2 * kSubA, k0 + 64 * s2, row_c);
+              for (int s2 = 0; s2 < kKSub; ++s2) {
+                tma_load_2d_pair_u32(&p.map_a, fbl, sa + s2 * kSubA, k0 + 64 * s2, row_c);
 #pragma unroll
-              for (int i = 0; i < 2; ++i) {
-                if (!kBwd)  // W [N, K] K-major rows n: k-subtile s2, rows 64i..
-                  tma_load_2d_pair(&p.map_w, fbl, sb + s2 * kSubA + i * kBox, k0 + 64 * s2, col_c + 64 * i);
-                else        // W viewed [k_out (MN), n (red)]: atom i, K-rows 64*s2..
-                  tma_load_2d_pair(&p.map_w, fbl, sb + i * kAtomMN + s2 * kBox, col_c + 64 * i, k0 + 64 * s2);
+                for (int i = 0; i < 2; ++i) {
+                  if (!kBwd)  // W [N, K] K-major rows n: k-subtile s2, rows 64i..
+                    tma_load_2d_pair_u32(&p.map_w, fbl, sb + s2 * kSubA + i * kBox, k0 + 64 * s2, col_c + 64 * i);
+                  else        // W viewed [k_out (MN), n (red)]: atom i, K-rows 64*s2..
+                    tma_load_2d_pair_u32(&p.map_w, fbl, sb + i * kAtomMN + s2 * kBox, col_c + 64 * i, k0 + 64 * s2);
+                }
               }
             }
+            __syncwarp();
             advance();
           }
           if (g.n > 0) {
             // the side tile of this row block must have published Hs/Gs
-            const unsigned long long* flag = p.flags + tl.m;
-            const unsigned long long want = (epoch << 8) | 8ull;
-            if (ld_acquire_gpu_u64(flag) != want) {
-              const uint64_t t0 = globaltimer_ns();
-              while (ld_acquire_gpu_u64(flag) != want) {
-                if (globaltimer_ns() - t0 > kWatchdogNs) __trap();
+            if (elect_one_sync()) {
+              const unsigned long long* flag = p.flags + tl.m;
+              const unsigned long long want = (epoch << 8) | 8ull;
+              if (ld_acquire_gpu_u64(flag) != want) {
+                const uint64_t t0 = globaltimer_ns();
+                while (ld_acquire_gpu_u64(flag) != want) {
+                  if (globaltimer_ns() - t0 > kWatchdogNs) __trap();
+                }
               }
+              fence_async_global();
             }
-            fence_async_global();
+            __syncwarp();
           }
           for (int i = 0; i < g.n; ++i) {
             // extension block: reduction = rank (<= 64): first k-subtile only
             const int ad = p.seg_adapter[g.seg[i]];
+            PROF_T0(tw_);
             mbar_wait(&empty_bar[stage], phase ^ 1u);
-            uint8_t* sa = pipe + stage * kStageBytes;
-            uint8_t* sb = sa + kStageA;
-            const uint32_t fb = smem_u32(&full_bar[stage]);
-            if (leader) mbar_arrive_expect_tx_u32(fb, 2u * (kSubA + 2 * kBox));
-            const uint32_t fbl = mapa_shared(fb, 0);
-            tma_load_2d_pair(&p.map_side, fbl, sa, 0, row_c);
+            PROF_ADD(pw_empty, tw_);
+            if (elect_one_sync()) {
+              const uint32_t sa = pipe_u + stage * kStageBytes;
+              const uint32_t sb = sa + kStageA;
+              const uint32_t fbl = full_leader + 8u * stage;
+              if (leader) mbar_arrive_expect_tx_u32(full_u + 8u * stage, 2u * (kSubA + 2 * kBox));
+              tma_load_2d_pair_u32(&p.map_side, fbl, sa, 0, row_c);
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {
-              if (!kBwd)  // B_t [N, r] K-major rows n: box {64 j, 64 n}
-                tma_load_2d_pair(&p.map_lora_b[ad], fbl, sb + j * kBox, 0, col_c + 64 * j);
-              else        // A_t [r, K] viewed [k_out (MN), j (red)]: atom j, K-rows 0..63
-                tma_load_2d_pair(&p.map_lora_a[ad], fbl, sb + j * kAtomMN, col_c + 64 * j, 0);
+              for (int j = 0; j < 2; ++j) {
+                if (!kBwd)  // B_t [N, r] K-major rows n: box {64 j, 64 n}
+                  tma_load_2d_pair_u32(&p.map_lora_b[ad], fbl, sb + j * kBox, 0, col_c + 64 * j);
+                else        // A_t [r, K] viewed [k_out (MN), j (red)]: atom j, K-rows 0..63
+                  tma_load_2d_pair_u32(&p.map_lora_a[ad], fbl, sb + j * kAtomMN, col_c + 64 * j, 0);
+              }
             }
+            __syncwarp();
             advance();
           }
         }
@@ -329,7 +371,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       for (int t = cid; t < total_tiles; t += ncl) {
         const Tile tl = tile_at(t, num_m, num_n, p.group_m);
         const PairGroups g = pair_groups(p, so, tl.m);
+        PROF_T0(tw_);
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1u);
+        PROF_ADD(mw_tempty, tw_);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * kBN);
         if (tl.side) {
@@ -339,7 +383,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             lane_masks(g.hm[g0], mk[0]);
             lane_masks(ng > 1 ? g.hm[g0 + 1] : 0, mk[1]);
             for (int kb = 0; kb < num_kb; ++kb) {
+              PROF_T0(tw_);
               mbar_wait(&full_bar[stage], phase);
+              PROF_ADD(mw_full, tw_);
               tc_fence_after();
               const uint32_t a_lo = a_lo0 + stage * kStageStep;
               const uint32_t b_lo = b_lo0 + stage * kStageStep;
@@ -359,7 +405,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           }
         } else {
           for (int kb = 0; kb < num_kb; ++kb) {
+            PROF_T0(tw_);
             mbar_wait(&full_bar[stage], phase);
+            PROF_ADD(mw_full, tw_);
             tc_fence_after();
             const uint32_t a_lo = a_lo0 + stage * kStageStep;
             const uint32_t b_lo = b_lo0 + stage * kStageStep;
@@ -374,7 +422,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             advance();
           }
           for (int i = 0; i < g.n; ++i) {
+            PROF_T0(tw_);
             mbar_wait(&full_bar[stage], phase);
+            PROF_ADD(mw_full, tw_);
             tc_fence_after();
             const uint32_t a_lo = a_lo0 + stage * kStageStep;
             const uint32_t b_lo = b_lo0 + stage * kStageStep;
@@ -405,7 +455,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     int buf_sel = 0;
     for (int t = cid; t < total_tiles; t += ncl) {
       const Tile tl = tile_at(t, num_m, num_n, p.group_m);
+      PROF_T0(tw_);
       mbar_wait(&tfull_bar[acc], acc_phase);
+      PROF_ADD(ew_tfull, tw_);
       tc_fence_after();
       const int row_w = tl.m * kPairRows + kBM * static_cast<int>(crank) + 32 * q;  // first row of this warp
       const uint32_t t_addr = tmem_base + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(acc * kBN);
@@ -459,6 +511,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(tempty_leader);
           }
+#ifdef MUX_EPI_DIRECT
+          {
+            const int col = col_t + c * 64;
+            if (valid && col < p.nout) {
+              uint4* dst = reinterpret_cast<uint4*>(p.out + static_cast<size_t>(row_w + lane) * p.nout + col);
+#pragma unroll
+              for (int ch = 0; ch < 8; ++ch) {
+                const uint32_t* v = ch < 4 ? v0 : v1;
+                const int b = (ch & 3) * 8;
+                uint4 w;
+                w.x = pack_bf16x2(__uint_as_float(v[b + 0]), __uint_as_float(v[b + 1]));
+                w.y = pack_bf16x2(__uint_as_float(v[b + 2]), __uint_as_float(v[b + 3]));
+                w.z = pack_bf16x2(__uint_as_float(v[b + 4]), __uint_as_float(v[b + 5]));
+                w.w = pack_bf16x2(__uint_as_float(v[b + 6]), __uint_as_float(v[b + 7]));
+                dst[ch] = w;
+              }
+            }
+            continue;
+          }
+#endif
           uint8_t* buf = bufs + buf_sel * kEpiBuf;
           if (lane == 0) tma_store_wait_read<1>();
           __syncwarp();
@@ -488,6 +560,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     }
     if (lane == 0) tma_store_wait<0>();
   }
+#ifdef MUX_PROFILE
+  {
+    const long long tot = clock64() - t_role0;
+    if (warp == 1 && leader && lane == 0) {
+      atomicAdd(p.dbg + 0, static_cast<unsigned long long>(tot));
+      atomicAdd(p.dbg + 1, static_cast<unsigned long long>(mw_full));
+      atomicAdd(p.dbg + 2, static_cast<unsigned long long>(mw_tempty));
+    }
+    if (warp == 0 && lane == 0) {
+      atomicAdd(p.dbg + 3, static_cast<unsigned long long>(tot));
+      atomicAdd(p.dbg + 4, static_cast<unsigned long long>(pw_empty));
+    }
+    if (warp == 4 && lane == 0) {
+      atomicAdd(p.dbg + 5, static_cast<unsigned long long>(tot));
+      atomicAdd(p.dbg + 6, static_cast<unsigned long long>(ew_tfull));
+    }
+  }
+#endif
   tc_fence_before();
   __syncthreads();
   cluster_sync();

@@ -127,6 +127,17 @@ bool make_map(CUtensorMap* out, const void* ptr, uint64_t inner, uint64_t outer,
   return true;
 }
 
+#ifdef MUX_PROFILE
+unsigned long long* dbg_counters() {
+  static unsigned long long* d = nullptr;
+  if (!d) {
+    cudaMalloc(&d, 64 * sizeof(unsigned long long));
+    cudaMemset(d, 0, 64 * sizeof(unsigned long long));
+  }
+  return d;
+}
+#endif
+
 int num_sms() {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return 148;
@@ -316,6 +327,10 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
   if (st != MUX_OK) return st;
   p.seg_off = seg_off;
   p.side_out = side;
+  p.out = out;
+#ifdef MUX_PROFILE
+  p.dbg = dbg_counters();
+#endif
   p.flags = ws.flags;
   p.epoch = ws.epoch;
   p.done = ws.done;
@@ -404,5 +419,16 @@ mux_status mux_linear_bwd(int32_t num_segs, const int32_t* seg_off, const int32_
   return linear_common(true, num_segs, seg_off, seg_task, num_adapters, adapters, max_rows, K, N, r_cap, dY, X, W,
                        dX, Hs, nullptr, workspace, workspace_bytes, stream);
 }
+
+#ifdef MUX_PROFILE
+// [host] experiment builds only: synchronizes, copies and resets the wait-cycle counters.
+MUX_API int mux_debug_counters(unsigned long long* host_out, int n) {
+  unsigned long long* d = dbg_counters();
+  cudaDeviceSynchronize();
+  cudaMemcpy(host_out, d, sizeof(unsigned long long) * (n < 64 ? n : 64), cudaMemcpyDeviceToHost);
+  cudaMemset(d, 0, 64 * sizeof(unsigned long long));
+  return 0;
+}
+#endif
 
 }  // extern "C"

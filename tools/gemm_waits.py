@@ -1,0 +1,57 @@
+#!/usr/bin/env python
+"""Run the fused GEMM from a -DMUX_PROFILE build (libmux_prof.so) on the
+config-2 shapes and print where each role's cycles go (fraction of the role's
+lifetime spent waiting on each barrier)."""
+import ctypes
+import json
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    from paper_2603_02885_b200 import mux
+    mux.LIB_PATH = os.path.join(ROOT, "paper_2603_02885_b200", os.environ.get("MUX_PROF_LIB", "libmux_prof.so"))
+    mux._lib = None
+    L = mux.lib()
+    L.mux_debug_counters.argtypes = [ctypes.c_void_p, ctypes.c_int]
+    R = 11648
+    rank = int(sys.argv[1]) if len(sys.argv) > 1 else 16
+    for K, N in [(4096, 4096), (4096, 11008), (11008, 4096)]:
+        X = torch.randn(R, K, device="cuda").bfloat16()
+        W = (torch.randn(N, K, device="cuda") / K ** 0.5).bfloat16()
+        dY = torch.randn(R, N, device="cuda").bfloat16()
+        seg_off = torch.tensor([0, 2944, 5888, 8768, R], dtype=torch.int32, device="cuda")
+        ads = []
+        for t in range(4):
+            B = mux.make_B_storage(N, rank)
+            B.copy_(torch.randn(N, rank, device="cuda").bfloat16())
+            ads.append(mux.Adapter((torch.randn(rank, K, device="cuda") / K ** 0.5).bfloat16(), B, rank, 2.0))
+        r_cap = max(16, 16 * -(-rank // 16))
+        ws = torch.zeros(mux.linear_workspace_size(4, R, K, N, r_cap), dtype=torch.uint8, device="cuda")
+        Y = torch.empty(R, N, dtype=torch.bfloat16, device="cuda")
+        Hs = torch.empty(R, r_cap, dtype=torch.bfloat16, device="cuda")
+        dX = torch.empty(R, K, dtype=torch.bfloat16, device="cuda")
+        for name, fn in [("fwd", lambda: mux.linear_fwd(seg_off, [0, 1, 2, 3], ads, X, W, r_cap, Y=Y, Hs=Hs,
+                                                         workspace=ws)),
+                         ("bwd", lambda: mux.linear_bwd(seg_off, [0, 1, 2, 3], ads, dY, X, W, Hs, r_cap, dX=dX,
+                                                         workspace=ws))]:
+            fn()
+            buf = (ctypes.c_ulonglong * 64)()
+            L.mux_debug_counters(buf, 64)
+            for _ in range(5):
+                fn()
+            L.mux_debug_counters(buf, 64)
+            c = list(buf)[:7]
+            out = {"shape": f"{K}x{N}", "pass": name, "rank": rank,
+                   "mma_wait_full": c[1] / max(c[0], 1), "mma_wait_tmem_empty": c[2] / max(c[0], 1),
+                   "producer_wait_empty": c[4] / max(c[3], 1), "epilogue_wait_tmem_full": c[6] / max(c[5], 1)}
+            print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()
