@@ -45,7 +45,8 @@ __host__ __device__ inline size_t pack_ws_bytes(int M, int S) {
 constexpr int kPackSmemMaxBytes = 200 * 1024;
 
 __host__ __device__ inline size_t pack_smem_bytes(int M, int S) {
-  return 7 * align256(sizeof(int32_t) * (size_t)(S + 1)) + 2 * align256(sizeof(int32_t) * (size_t)(M > 0 ? M : 1));
+  // workspace arrays + staged copies of seq_len [S], task_seq_off [M+1], capacity [M]
+  return 8 * align256(sizeof(int32_t) * (size_t)(S + 1)) + 4 * align256(sizeof(int32_t) * (size_t)(M + 1));
 }
 
 __device__ inline PackWs carve_pack_ws(void* ws, int M, int S) {
@@ -96,11 +97,34 @@ __global__ void __launch_bounds__(kPackThreads, 1)
   PackWs ws = carve_pack_ws(use_smem ? static_cast<void*>(pack_smem) : workspace, M, S);
   griddep_wait();  // PDL: inputs may come from the previous kernel
   griddep_launch_dependents();
+  // Stage the (small) inputs in shared memory when they fit: every later
+  // phase re-reads them, and a dependent global round trip per phase was the
+  // kernel's critical path.
+  const int32_t* sl = seq_len;
+  const int32_t* tso = task_seq_off;
+  const int32_t* capp = pack_capacity;
+  if (use_smem) {
+    uint8_t* b = pack_smem + 7 * align256(sizeof(int32_t) * (size_t)(S + 1)) +
+                 2 * align256(sizeof(int32_t) * (size_t)(M > 0 ? M : 1));
+    int32_t* s_sl = reinterpret_cast<int32_t*>(b);
+    b += align256(sizeof(int32_t) * (size_t)(S + 1));
+    int32_t* s_tso = reinterpret_cast<int32_t*>(b);
+    b += align256(sizeof(int32_t) * (size_t)(M + 1));
+    int32_t* s_cap = reinterpret_cast<int32_t*>(b);
+    for (int i = tid; i < S; i += kPackThreads) s_sl[i] = seq_len[i];
+    for (int i = tid; i <= M; i += kPackThreads) s_tso[i] = task_seq_off[i];
+    if (pack_capacity != nullptr)
+      for (int i = tid; i < M; i += kPackThreads) s_cap[i] = pack_capacity[i];
+    __syncthreads();
+    sl = s_sl;
+    tso = s_tso;
+    capp = pack_capacity != nullptr ? s_cap : nullptr;
+  }
 
   // ---- 1. chunk size, validity, max length, valid rows -------------------
   int v2min = 30, bad = 0, mx = 0, sum = 0;
   for (int i = tid; i < S; i += kPackThreads) {
-    const int L = seq_len[i];
+    const int L = sl[i];
     if (L < 1) bad = 1;
     else {
       v2min = min(v2min, __ffs(L) - 1);
@@ -144,13 +168,13 @@ __global__ void __launch_bounds__(kPackThreads, 1)
     int lo = 0, hi = M;  // find t with off[t] <= i < off[t+1]
     while (hi - lo > 1) {
       const int mid = (lo + hi) >> 1;
-      if (task_seq_off[mid] <= i) lo = mid; else hi = mid;
+      if (tso[mid] <= i) lo = mid; else hi = mid;
     }
-    const int t0 = task_seq_off[lo], t1 = task_seq_off[lo + 1];
-    const int L = seq_len[i];
+    const int t0 = tso[lo], t1 = tso[lo + 1];
+    const int L = sl[i];
     int rank = 0;
     for (int j = t0; j < t1; ++j) {
-      const int Lj = seq_len[j];
+      const int Lj = sl[j];
       rank += (Lj > L) || (Lj == L && j < i);
     }
     ws.order[t0 + rank] = i - t0;
@@ -159,12 +183,12 @@ __global__ void __launch_bounds__(kPackThreads, 1)
 
   // ---- 3. first-fit decreasing, one warp per task -------------------------
   for (int t = warp; t < M; t += kPackWarps) {
-    const int t0 = task_seq_off[t], n = task_seq_off[t + 1] - t0;
+    const int t0 = tso[t], n = tso[t + 1] - t0;
     int mxl = 0;
-    for (int i = lane; i < n; i += 32) mxl = max(mxl, seq_len[t0 + i]);
+    for (int i = lane; i < n; i += 32) mxl = max(mxl, sl[t0 + i]);
     mxl = warp_max(mxl);
     int cap;
-    if (pack_capacity != nullptr) cap = pack_capacity[t];
+    if (capp != nullptr) cap = capp[t];
     else cap = ((max(mxl, c) + c - 1) / c) * c;
     if (n > 0 && cap < mxl) {
       if (lane == 0) atomicOr(&s_bad, 4);
@@ -174,7 +198,7 @@ __global__ void __launch_bounds__(kPackThreads, 1)
     int npacks = 0;
     for (int r = 0; r < n; ++r) {
       const int li = ws.order[t0 + r];
-      const int L = seq_len[t0 + li];
+      const int L = sl[t0 + li];
       int found = -1;
       for (int base = 0; base < npacks && found < 0; base += 32) {
         const int p = base + lane;
@@ -251,7 +275,7 @@ __global__ void __launch_bounds__(kPackThreads, 1)
   // per-task pack rows (serial over a task's packs; one warp per task)
   for (int t = warp; t < M; t += kPackWarps) {
     if (lane == 0) {
-      const int t0 = task_seq_off[t];
+      const int t0 = tso[t];
       int ch = ws.task_chunks[t];
       for (int p = 0; p < ws.task_packs[t]; ++p) {
         ws.pack_row0[t0 + p] = ch * c;
@@ -264,7 +288,7 @@ __global__ void __launch_bounds__(kPackThreads, 1)
     int run = 0;
     for (int base = 0; base < S; base += 32) {
       const int i = base + lane;
-      int v = i < S ? seq_len[i] : 0;
+      int v = i < S ? sl[i] : 0;
       int x = v;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -275,13 +299,14 @@ __global__ void __launch_bounds__(kPackThreads, 1)
       run += __shfl_sync(0xffffffffu, x, 31);
     }
   }
-  for (int r = tid; r < max_rows; r += kPackThreads) row_src[r] = -1;
+  // rows past the last chunk are unused
+  for (int r = total_chunks * c + tid; r < max_rows; r += kPackThreads) row_src[r] = -1;
   __syncthreads();
 
   // ---- 5. fill ------------------------------------------------------------
   // chunk table: one thread per (task, pack)
   for (int t = 0; t < M; ++t) {
-    const int t0 = task_seq_off[t];
+    const int t0 = tso[t];
     for (int p = tid; p < ws.task_packs[t]; p += kPackThreads) {
       const int len = ws.pack_len[t0 + p];
       const int n_p = (len + c - 1) / c;
@@ -292,15 +317,17 @@ __global__ void __launch_bounds__(kPackThreads, 1)
         chunk_valid[id0 + j] = min(c, len - j * c);
         chunk_dep[id0 + j] = j > 0 ? id0 + j - 1 : -1;
       }
+      // the pack's tail padding (its sequences fill [row0, row0 + len))
+      for (int r = id0 * c + len; r < (id0 + n_p) * c; ++r) row_src[r] = -1;
     }
   }
   // seq_row and row_src: one warp per sequence
   for (int t = 0; t < M; ++t) {
-    const int t0 = task_seq_off[t], t1 = task_seq_off[t + 1];
+    const int t0 = tso[t], t1 = tso[t + 1];
     for (int s = t0 + warp; s < t1; s += kPackWarps) {
       const int row = ws.pack_row0[t0 + ws.pack_of[s]] + ws.pack_off[s];
       if (lane == 0) seq_row[s] = row;
-      const int L = seq_len[s];
+      const int L = sl[s];
       const int tok = ws.tok_off[s];
       for (int pos = lane; pos < L; pos += 32) row_src[row + pos] = tok + pos;
     }
