@@ -280,14 +280,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
               const uint32_t sa = pipe_u + stage * kStageBytes;
               const uint32_t sb = sa + kStageA;
               const uint32_t fbl = full_leader + 8u * stage;
-#ifdef MUX_DIAG_NO_TMA
-              // timing diagnostic only: no operand loads (MMAs read stale smem)
-              if (leader) mbar_arrive_expect_tx_u32(full_u + 8u * stage, 0u);
-              if (false)
-#else
               if (leader) mbar_arrive_expect_tx_u32(full_u + 8u * stage, 2u * kStageBytes);
-#endif
-              {
               const int k0 = kb * kBK;
 #pragma unroll
               for (int s2 = 0; s2 < kKSub; ++s2) {
@@ -299,7 +292,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                   else        // W viewed [k_out (MN), n (red)]: atom i, K-rows 64*s2..
                     tma_load_2d_pair_u32(&p.map_w, fbl, sb + i * kAtomMN + s2 * kBox, col_c + 64 * i, k0 + 64 * s2);
                 }
-              }
               }
             }
             __syncwarp();
@@ -420,12 +412,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             const uint32_t a_lo = a_lo0 + stage * kStageStep;
             const uint32_t b_lo = b_lo0 + stage * kStageStep;
             if (elect_one_sync()) {
-#ifndef MUX_DIAG_NO_MMA
 #pragma unroll
               for (int k = 0; k < kBK / 16; ++k)
                 mma_bf16_pair_nomask(d_tmem, make_desc(a_lo + a_off(k), kHi), make_desc(b_lo + b_off(k), kHi),
                                      kIdescMain, (kb | k) != 0);
-#endif
               mma_commit_pair_mc(&empty_bar[stage], kPairMask);
             }
             __syncwarp();

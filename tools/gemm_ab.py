@@ -39,6 +39,7 @@ def main():
     ap.add_argument("--rank", type=int, default=16)
     ap.add_argument("--shapes", default="4096x4096,4096x11008,11008x4096")
     ap.add_argument("--no-cublas", action="store_true")
+    ap.add_argument("--fwd-only", action="store_true")
     a = ap.parse_args()
     from paper_2603_02885_b200 import mux
     handles = {}
@@ -82,7 +83,8 @@ def main():
                 mux.linear_bwd(seg_off, st, ads, dY, X, W, Hs, r_cap, dX=dX, workspace=ws)
             name = os.path.basename(lib)
             cands[(name, "fwd")] = (fwd, 2 * R * K * N + 2 * R * a.rank * (K + N))
-            cands[(name, "bwd(dX+grads)")] = (bwd, 2 * R * K * N + 4 * R * a.rank * (K + N))
+            if not a.fwd_only:
+                cands[(name, "bwd(dX+grads)")] = (bwd, 2 * R * K * N + 4 * R * a.rank * (K + N))
         for fn, _ in cands.values():
             for _ in range(3):
                 fn()
