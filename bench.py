@@ -474,6 +474,97 @@ def main_arm(args):
         dist.destroy_process_group()
 
 
+# ------------------------------------------------------------------ tensor-parallel arm
+def tp_arm(args):
+    """--mode tp: one config-2 hTask tensor-parallel over the N ranks (strong
+    scaling).  Megatron pairing over the 3-layer stack: L0 column-parallel
+    (AG of the row-sharded input), L1 row-parallel (RS of the output), L2
+    column-parallel; backward mirrors it (RS / AG / AR of dA or dB, see
+    paper_2603_02885_b200/tp.py).  Every rank's compute is the fused kernels."""
+    import torch
+    import torch.distributed as dist
+    from paper_2603_02885_b200 import mux, tp
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29511")
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
+    w = Workload(args.config)
+    h = w.host_tensors()
+    i32 = dict(dtype=torch.int32, device="cuda")
+    tso, sl = torch.tensor(w.off, **i32), torch.tensor(w.lens, **i32)
+    cap = torch.tensor(w.cap, **i32) if w.cap else None
+    bound = int(mux.pack_bound_rows(w.T, w.S, 64))
+    max_rows = -(-bound // (64 * world)) * 64 * world       # row blocks split evenly over ranks
+    pk = mux.alloc_pack_outputs(w.M, w.S, max_rows, max_rows // 64)
+    r_cap = 16 * -(-max(w.wl.ranks) // 16)
+    st = list(range(w.M))
+    be = tp.MuxBackend()
+    mk = lambda A, B, r, sc: mux.Adapter(A, B, r, sc)  # noqa: E731
+    kinds = ["col", "row", "col"]
+    layers = []
+    for li, L in enumerate(w.linears):
+        W = _bits_to_dev(h[f"W{li}"], torch)
+        ads = []
+        for t in range(w.M):
+            B = mux.make_B_storage(L.N, w.wl.ranks[t])
+            B.copy_(_bits_to_dev(h[f"B{li}_{t}"], torch))
+            ads.append(mux.Adapter(_bits_to_dev(h[f"A{li}_{t}"], torch), B, w.wl.ranks[t], w.wl.scales[t]))
+        if kinds[li] == "col":
+            Wp, ap_ = tp.shard_column(W, ads, world, rank, mk)
+            layers.append(tp.ColumnParallelMuxLinear(be, Wp, ap_, r_cap))
+        else:
+            Wp, ap_ = tp.shard_row(W, ads, world, rank, mk)
+            layers.append(tp.RowParallelMuxLinear(be, Wp, ap_, r_cap))
+        del W
+    X1tok = _bits_to_dev(h["X1"], torch)
+    rows = max_rows // world
+    x_rows = torch.empty(rows, w.linears[0].K, dtype=torch.bfloat16, device="cuda")
+    nl = w.linears[-1].N // world
+    dY = torch.randn(max_rows, nl, device="cuda", generator=torch.Generator(device="cuda").manual_seed(rank)).bfloat16()
+
+    def step():
+        mux.pack_chunks(tso, sl, cap, 0, 64, max_rows=max_rows, max_chunks=max_rows // 64, out=pk)
+        seg_off = pk["seg_off"]
+        mux.pack_apply(pk["row_src"][rank * rows:(rank + 1) * rows], X1tok, rows, out=x_rows)
+        y = layers[0].forward(seg_off, st, x_rows)     # [R, N0/p]
+        y = layers[1].forward(seg_off, st, y)          # [R/p, N1]
+        y = layers[2].forward(seg_off, st, y)          # [R, N2/p]
+        g, _, _ = layers[2].backward(seg_off, st, dY)  # [R/p, N1]
+        g, _, _ = layers[1].backward(seg_off, st, g)   # [R, N0/p]
+        g, _, _ = layers[0].backward(seg_off, st, g)   # [R/p, K0]
+        return g
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record()
+    for _ in range(args.steps):
+        step()
+    s1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([s0.elapsed_time(s1) / args.steps], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": w.T / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
+                          "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                          "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+                          "data": "synthetic", "mode": "tp",
+                          "config": {"workload": f"config {args.config}: " + w.wl.description,
+                                     "parallelism": f"tp{world} (L0 column, L1 row, L2 column; sequence-parallel "
+                                                    "AG/RS over NCCL)", "valid_tokens": w.T,
+                                     "max_rows": max_rows},
+                          "tflops_per_gpu_algorithmic": w.flops / (ms * 1e-3) / 1e12 / world}), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -485,11 +576,15 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-rows", type=int, default=4, help="rows per task per reference-arm step")
+    ap.add_argument("--mode", default="replicas", choices=["replicas", "tp"],
+                    help="N>1: task-sharded replicas (default, weak scaling) or tensor parallel (strong)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         reference_arm(args)
+    elif args.mode == "tp":
+        tp_arm(args)
     else:
         main_arm(args)
 

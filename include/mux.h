@@ -170,7 +170,8 @@ MUX_API size_t mux_linear_workspace_size(int32_t num_segs, int32_t max_rows, int
  *   entry a multiple of 64 (mux_pack_chunks guarantees it), seg_off[S] <=
  *   max_rows; seg_task [S] [host] adapter index per segment;
  *   num_adapters (1..64), adapters [host];
- *   K, N multiples of 64; r_cap in {16,32,48,64} >= every rank;
+ *   K, N multiples of 8 (e.g. 11008/8 = 1376 for an 8-way tensor-parallel shard);
+ *   r_cap in {16,32,48,64} >= every rank;
  *   X [max_rows, K] (pad rows inside segments must be 0: then Y's pad rows are 0);
  *   W [N, K]; Y [max_rows, N]; Hs [max_rows, r_cap] or NULL (inference: kept
  *   in the workspace).  Rows >= seg_off[S] of Y/Hs are not written.

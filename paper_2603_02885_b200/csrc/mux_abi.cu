@@ -185,8 +185,10 @@ mux_status validate_linear(int32_t num_segs, const int32_t* seg_off, const int32
     return fail(MUX_ERR_INVALID_ARGUMENT, "num_adapters=%d outside [1,%d]", num_adapters, MUX_MAX_ADAPTERS);
   if (!seg_off || !seg_task || !adapters) return fail(MUX_ERR_INVALID_ARGUMENT, "null seg_off/seg_task/adapters");
   if (max_rows < 1) return fail(MUX_ERR_INVALID_ARGUMENT, "max_rows=%d must be >= 1", max_rows);
-  if (K < 64 || N < 64 || (K % 64) || (N % 64))
-    return fail(MUX_ERR_INVALID_ARGUMENT, "K=%d, N=%d must be positive multiples of 64", K, N);
+  // multiples of 8: 16-byte TMA row strides; partial 64-wide tiles are handled
+  // by TMA zero fill (loads) and clipping (stores)
+  if (K < 8 || N < 8 || (K % 8) || (N % 8))
+    return fail(MUX_ERR_INVALID_ARGUMENT, "K=%d, N=%d must be positive multiples of 8", K, N);
   if (r_cap != 16 && r_cap != 32 && r_cap != 48 && r_cap != 64)
     return fail(MUX_ERR_INVALID_ARGUMENT, "r_cap=%d must be one of 16, 32, 48, 64", r_cap);
   for (int s = 0; s < num_segs; ++s)
@@ -395,7 +397,10 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
     g.units_b = want_b ? (N + kGradBM - 1) / kGradBM : 0;
     const long long units = static_cast<long long>(nt) * (g.units_a + g.units_b);
     if (units > 0) {
-      const int ggrid = static_cast<int>(units < num_sms() ? units : num_sms());
+      // HBM-bound: spread the units evenly (every CTA gets the same number of
+      // units) instead of leaving a ragged last wave on 148 CTAs
+      const long long waves = (units + num_sms() - 1) / num_sms();
+      const int ggrid = static_cast<int>((units + waves - 1) / waves);
       e = launch_grad(g, ggrid, stream);
       if (e != cudaSuccess) return cuda_fail(e, "mux_linear_bwd grad launch");
     }

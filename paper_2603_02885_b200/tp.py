@@ -69,17 +69,38 @@ def all_reduce_(x: torch.Tensor, group=None) -> torch.Tensor:
 
 # ------------------------------------------------------------------ backends
 class MuxBackend:
-    """libmux kernels (the product path)."""
+    """libmux kernels (the product path).  Output buffers and the (zeroed once,
+    reused) linear workspace are cached per layer key, so a step allocates
+    nothing."""
 
     def __init__(self):
         from . import mux
         self.mux = mux
+        self.cache = {}
+
+    def _buf(self, key, shape, dtype, device, zero=False):
+        t = self.cache.get(key)
+        if t is None or tuple(t.shape) != tuple(shape):
+            t = (torch.zeros if zero else torch.empty)(shape, dtype=dtype, device=device)
+            self.cache[key] = t
+        return t
+
+    def _ws(self, W, X, seg_task, r_cap):
+        R, K = X.shape
+        n = self.mux.linear_workspace_size(len(seg_task), R, K, W.shape[0], r_cap)
+        return self._buf(("ws", W.data_ptr()), (n,), torch.uint8, X.device, zero=True)
 
     def fwd(self, seg_off, seg_task, adapters, X, W, r_cap):
-        return self.mux.linear_fwd(seg_off, seg_task, adapters, X, W, r_cap)
+        R = X.shape[0]
+        Y = self._buf(("Y", W.data_ptr()), (R, W.shape[0]), torch.bfloat16, X.device)
+        Hs = self._buf(("Hs", W.data_ptr()), (R, r_cap), torch.bfloat16, X.device)
+        return self.mux.linear_fwd(seg_off, seg_task, adapters, X, W, r_cap, Y=Y, Hs=Hs,
+                                   workspace=self._ws(W, X, seg_task, r_cap))
 
     def bwd(self, seg_off, seg_task, adapters, dY, X, W, Hs, r_cap):
-        dX = self.mux.linear_bwd(seg_off, seg_task, adapters, dY, X, W, Hs, r_cap)
+        dX = self._buf(("dX", W.data_ptr()), tuple(X.shape), torch.bfloat16, X.device)
+        dX = self.mux.linear_bwd(seg_off, seg_task, adapters, dY, X, W, Hs, r_cap, dX=dX,
+                                 workspace=self._ws(W, X, seg_task, r_cap))
         return dX, [a.dA for a in adapters], [a.dB for a in adapters]
 
 

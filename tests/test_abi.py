@@ -77,8 +77,8 @@ def _fwd(mux, **kw):
 @pytest.mark.parametrize("kw,frag", [
     (dict(S=0), "num_segs"),
     (dict(S=65), "num_segs"),
-    (dict(K=100), "multiples of 64"),
-    (dict(N=0), "multiples of 64"),
+    (dict(K=100), "multiples of 8"),
+    (dict(N=0), "multiples of 8"),
     (dict(r_cap=24), "r_cap"),
     (dict(max_rows=0), "max_rows"),
     (dict(seg_task=(ctypes.c_int32 * 1)(3)), "seg_task"),

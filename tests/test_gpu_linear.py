@@ -45,6 +45,13 @@ def test_multi_tile_ragged():
     _run(Problem(320, 640, [192, 64, 256], [16, 4, 64], seed=14))
 
 
+def test_dims_multiple_of_8_not_64():
+    """K, N multiples of 8 only (e.g. an 8-way TP shard of 11008 = 1376):
+    partial 64-wide k-blocks read TMA zero fill, partial output boxes clip."""
+    _run(Problem(264, 200, [64, 128], [8, 16], seed=22))
+    _run(Problem(1376, 328, [128, 64], [16, 4], variant="int", scales=[2.0, 1.0], seed=23), exact=True)
+
+
 def test_heterogeneous_ranks_and_rank0():
     _run(Problem(256, 512, [128, 64, 64, 128], [4, 0, 48, 8], r_cap=48, seed=15))
 
