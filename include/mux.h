@@ -42,7 +42,6 @@
 #include <stddef.h>
 #include <stdint.h>
 #include <cuda_runtime.h>
-#include <cuda_bf16.h>
 
 #if defined(__GNUC__)
 #define MUX_API __attribute__((visibility("default")))
@@ -53,6 +52,10 @@
 #ifdef __cplusplus
 extern "C" {
 #endif
+
+/* bf16 tensors are passed as raw 16-bit patterns (bit-compatible with CUDA's
+ * __nv_bfloat16 and torch.bfloat16), so the header is plain C. */
+typedef uint16_t mux_bf16;
 
 #define MUX_MAX_SEGMENTS 64   /* per linear call (kernel parameter block <= 32 KB) */
 #define MUX_MAX_ADAPTERS 64
@@ -134,16 +137,16 @@ MUX_API mux_status mux_pack_chunks(int32_t num_tasks, int32_t num_seqs,
  * cols a multiple of 8, pointers 16-byte aligned.  Indices >= num_tokens
  * are treated as pad (0). */
 MUX_API mux_status mux_pack_apply(int32_t max_rows, int32_t cols, int32_t num_tokens,
-                          const int32_t* row_src, const __nv_bfloat16* src,
-                          __nv_bfloat16* dst, cudaStream_t stream);
+                          const int32_t* row_src, const mux_bf16* src,
+                          mux_bf16* dst, cudaStream_t stream);
 
 /* ------------------------------------------------------------------ linear */
 
 /* One adapter (task) of a linear layer.  [host] array; the pointers inside
  * are device pointers. */
 typedef struct {
-  const __nv_bfloat16* A;  /* [rank, K] row-major (lora_A.weight) */
-  const __nv_bfloat16* B;  /* [N, rank] row-major (lora_B.weight) */
+  const mux_bf16* A;  /* [rank, K] row-major (lora_A.weight) */
+  const mux_bf16* B;  /* [N, rank] row-major (lora_B.weight) */
   float* dA;               /* [rank, K] fp32, overwritten by bwd; NULL = skip */
   float* dB;               /* [N, rank] fp32, overwritten by bwd; NULL = skip */
   int32_t rank;            /* 0 (no adapter on this layer) .. 64 */
@@ -180,8 +183,8 @@ MUX_API size_t mux_linear_workspace_size(int32_t num_segs, int32_t max_rows, int
 MUX_API mux_status mux_linear_fwd(int32_t num_segs, const int32_t* seg_off, const int32_t* seg_task,
                           int32_t num_adapters, const mux_adapter* adapters,
                           int32_t max_rows, int32_t K, int32_t N, int32_t r_cap,
-                          const __nv_bfloat16* X, const __nv_bfloat16* W,
-                          __nv_bfloat16* Y, __nv_bfloat16* Hs,
+                          const mux_bf16* X, const mux_bf16* W,
+                          mux_bf16* Y, mux_bf16* Hs,
                           void* workspace, size_t workspace_bytes, cudaStream_t stream);
 
 /* Backward (Eq. 2 + LoRA chain rule).  For rows i of segment s, t = seg_task[s]:
@@ -195,9 +198,9 @@ MUX_API mux_status mux_linear_fwd(int32_t num_segs, const int32_t* seg_off, cons
 MUX_API mux_status mux_linear_bwd(int32_t num_segs, const int32_t* seg_off, const int32_t* seg_task,
                           int32_t num_adapters, const mux_adapter* adapters,
                           int32_t max_rows, int32_t K, int32_t N, int32_t r_cap,
-                          const __nv_bfloat16* dY, const __nv_bfloat16* X,
-                          const __nv_bfloat16* W, const __nv_bfloat16* Hs,
-                          __nv_bfloat16* dX,
+                          const mux_bf16* dY, const mux_bf16* X,
+                          const mux_bf16* W, const mux_bf16* Hs,
+                          mux_bf16* dX,
                           void* workspace, size_t workspace_bytes, cudaStream_t stream);
 
 #ifdef __cplusplus

@@ -6,6 +6,7 @@
 #include <cuda_bf16.h>
 
 #include "../../include/mux.h"
+#include <cuda_bf16.h>
 
 namespace mux {
 

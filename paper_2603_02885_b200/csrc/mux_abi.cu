@@ -276,7 +276,9 @@ mux_status mux_pack_chunks(int32_t num_tasks, int32_t num_seqs, const int32_t* t
 }
 
 mux_status mux_pack_apply(int32_t max_rows, int32_t cols, int32_t num_tokens, const int32_t* row_src,
-                          const __nv_bfloat16* src, __nv_bfloat16* dst, cudaStream_t stream) {
+                          const mux_bf16* src_, mux_bf16* dst_, cudaStream_t stream) {
+  const __nv_bfloat16* src = reinterpret_cast<const __nv_bfloat16*>(src_);
+  __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(dst_);
   if (max_rows < 0 || cols < 8 || (cols % 8) || num_tokens < 0)
     return fail(MUX_ERR_INVALID_ARGUMENT, "bad shape max_rows=%d cols=%d num_tokens=%d", max_rows, cols,
                 num_tokens);
@@ -410,17 +412,26 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
 
 mux_status mux_linear_fwd(int32_t num_segs, const int32_t* seg_off, const int32_t* seg_task,
                           int32_t num_adapters, const mux_adapter* adapters, int32_t max_rows, int32_t K, int32_t N,
-                          int32_t r_cap, const __nv_bfloat16* X, const __nv_bfloat16* W, __nv_bfloat16* Y,
-                          __nv_bfloat16* Hs, void* workspace, size_t workspace_bytes, cudaStream_t stream) {
+                          int32_t r_cap, const mux_bf16* X_, const mux_bf16* W_, mux_bf16* Y_,
+                          mux_bf16* Hs_, void* workspace, size_t workspace_bytes, cudaStream_t stream) {
+  auto X = reinterpret_cast<const __nv_bfloat16*>(X_);
+  auto W = reinterpret_cast<const __nv_bfloat16*>(W_);
+  auto Y = reinterpret_cast<__nv_bfloat16*>(Y_);
+  auto Hs = reinterpret_cast<__nv_bfloat16*>(Hs_);
   return linear_common(false, num_segs, seg_off, seg_task, num_adapters, adapters, max_rows, K, N, r_cap, X, X, W,
                        Y, nullptr, Hs, workspace, workspace_bytes, stream);
 }
 
 mux_status mux_linear_bwd(int32_t num_segs, const int32_t* seg_off, const int32_t* seg_task,
                           int32_t num_adapters, const mux_adapter* adapters, int32_t max_rows, int32_t K, int32_t N,
-                          int32_t r_cap, const __nv_bfloat16* dY, const __nv_bfloat16* X, const __nv_bfloat16* W,
-                          const __nv_bfloat16* Hs, __nv_bfloat16* dX, void* workspace, size_t workspace_bytes,
+                          int32_t r_cap, const mux_bf16* dY_, const mux_bf16* X_, const mux_bf16* W_,
+                          const mux_bf16* Hs_, mux_bf16* dX_, void* workspace, size_t workspace_bytes,
                           cudaStream_t stream) {
+  auto dY = reinterpret_cast<const __nv_bfloat16*>(dY_);
+  auto X = reinterpret_cast<const __nv_bfloat16*>(X_);
+  auto W = reinterpret_cast<const __nv_bfloat16*>(W_);
+  auto Hs = reinterpret_cast<const __nv_bfloat16*>(Hs_);
+  auto dX = reinterpret_cast<__nv_bfloat16*>(dX_);
   return linear_common(true, num_segs, seg_off, seg_task, num_adapters, adapters, max_rows, K, N, r_cap, dY, X, W,
                        dX, Hs, nullptr, workspace, workspace_bytes, stream);
 }

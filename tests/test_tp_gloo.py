@@ -90,7 +90,7 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("world", [2])
+@pytest.mark.parametrize("world", [2, 4])
 def test_tp_column_row_matches_single_process(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
