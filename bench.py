@@ -366,12 +366,16 @@ def main_arm(args):
     if os.path.exists(tp):
         tj = json.load(open(tp))
         traffic, traffic_src = tj.get("mean_bytes_per_launch"), tj.get("source")
-    roof = {"bound": "tensor", "achieved": achieved, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
-            "frac": achieved / pk["bf16_tflops"], "traffic": traffic, "traffic_source": traffic_src,
+    # the GEMM launches are timed inside a long back-to-back step (the whole
+    # timed region runs under the power cap), so the denominator is the
+    # measured *sustained* bf16 peak; the burst fraction is reported beside it
+    roof = {"bound": "tensor", "achieved": achieved, "peak": pk["bf16_tflops_sustained"], "unit": "TFLOP/s",
+            "frac": achieved / pk["bf16_tflops_sustained"], "frac_of_burst": achieved / pk["bf16_tflops"],
+            "traffic": traffic, "traffic_source": traffic_src,
             "algorithmic_bytes_per_launch": sum(2 * (w.T * (L.K + L.N) + L.K * L.N) for L in w.linears)
             / len(w.linears),
             "kernel": "mux_gemm_kernel<fwd> (fused backbone + LoRA; events around each mux_linear_fwd call)",
-            "peak_source": pk["source"] + " burst bf16 (cuBLAS 8192^3)"}
+            "peak_source": pk["source"] + " sustained bf16 (cuBLAS 8192^3 back to back for 4 s)"}
 
     # ---------------- e2e: same step through the public API with host buffers.
     # Every step copies its inputs host->device (pinned) and its result (all

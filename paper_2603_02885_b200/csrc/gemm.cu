@@ -27,7 +27,7 @@
 // tasks; their adapter MMAs carry the tcgen05 disable-output-lane mask of every
 // other task's rows, so a row is only ever multiplied by its own task's
 // weights (NaN isolation).
-// Side tiles come first in the schedule and never wait, so every dependency
+// Side tiles come first in their band and never wait, so every dependency
 // points to a lower tile index: with all CTAs resident the lowest unfinished
 // tile always progresses (no deadlock).
 //
@@ -116,23 +116,29 @@ struct Tile {
   bool side;
 };
 
-// Raster: bands of `group_m` pair row-blocks; inside a band the row block
-// varies fastest, so the band's A rows stay L2-resident while W tiles stream
-// through once per band (group_m is sized on the host so the band fits L2).
-__device__ __forceinline__ Tile tile_at(int t, int num_m, int num_n, int group_m) {
+// Raster: bands of `group_m` pair row-blocks.  Each band is [its side tiles]
+// then [its main tiles, row block fastest], so the side tiles' pass over the
+// band's A rows warms L2 right before the main tiles sweep W through it, and
+// every main tile still depends only on a lower-indexed side tile (group_m is
+// sized on the host so a band of A rows fits L2 next to the streamed W tiles).
+__device__ __forceinline__ Tile tile_at(int t, int num_m, int num_n, int group_m, bool has_main) {
   Tile r;
-  if (t < num_m) {
+  if (!has_main) {
     r.m = t; r.n = 0; r.side = true;
     return r;
   }
-  const int v = t - num_m;
-  const int per_group = group_m * num_n;
-  const int grp = v / per_group;
-  const int first_m = grp * group_m;
+  const int per_band = group_m * (num_n + 1);
+  const int band = t / per_band;
+  const int first_m = band * group_m;
   const int gm = min(num_m - first_m, group_m);
-  const int w = v - grp * per_group;
-  r.m = first_m + w % gm;
-  r.n = w / gm;
+  const int w = t - band * per_band;
+  if (w < gm) {
+    r.m = first_m + w; r.n = 0; r.side = true;
+    return r;
+  }
+  const int v = w - gm;
+  r.m = first_m + v % gm;
+  r.n = v / gm;
   r.side = false;
   return r;
 }
@@ -234,7 +240,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       const uint32_t full_u = smem_u32(full_bar);
       const uint32_t full_leader = mapa_shared(full_u, 0);  // stage s barrier: + 8 s
       for (int t = cid; t < total_tiles; t += ncl) {
-        const Tile tl = tile_at(t, num_m, num_n, p.group_m);
+        const Tile tl = tile_at(t, num_m, num_n, p.group_m, p.has_main != 0);
         const PairGroups g = pair_groups(p, so, tl.m);
         const int row_c = tl.m * kPairRows + kBM * rk;  // this CTA's rows
         if (tl.side) {
@@ -369,7 +375,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         if (++stage == kStages) { stage = 0; phase ^= 1u; }
       };
       for (int t = cid; t < total_tiles; t += ncl) {
-        const Tile tl = tile_at(t, num_m, num_n, p.group_m);
+        const Tile tl = tile_at(t, num_m, num_n, p.group_m, p.has_main != 0);
         const PairGroups g = pair_groups(p, so, tl.m);
         PROF_T0(tw_);
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1u);
@@ -454,7 +460,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     uint8_t* bufs = epi + q * 2 * kEpiBuf;
     int buf_sel = 0;
     for (int t = cid; t < total_tiles; t += ncl) {
-      const Tile tl = tile_at(t, num_m, num_n, p.group_m);
+      const Tile tl = tile_at(t, num_m, num_n, p.group_m, p.has_main != 0);
       PROF_T0(tw_);
       mbar_wait(&tfull_bar[acc], acc_phase);
       PROF_ADD(ew_tfull, tw_);
