@@ -8,3 +8,4 @@ from .mux import (  # noqa: F401
     Adapter, MuxError, pack_chunks, pack_apply, linear_fwd, linear_bwd, read_info,
     make_B_storage, linear_workspace_size, pack_bound_rows, version,
 )
+from .autograd import MuxLoRALinear  # noqa: F401,E402

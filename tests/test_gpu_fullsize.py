@@ -31,7 +31,8 @@ def _row_sample(seg_off, seed):
     return np.unique(np.array(rows, np.int64))
 
 
-CASES = [("2", 0), ("2", 1), ("2", 2), ("3a", 2), ("3b", 0), ("4", 0), ("4", 4), ("4", 6), ("5", 1)]
+CASES = [("2", 0), ("2", 1), ("2", 2), ("3a", 2), ("3b", 0), ("3c", 1), ("4", 0), ("4", 4), ("4", 6),
+         ("5", 0), ("5", 1)]
 
 
 @pytest.mark.parametrize("cid,li", CASES)
