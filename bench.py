@@ -480,14 +480,20 @@ def main_arm(args):
 
 # ------------------------------------------------------------------ tensor-parallel arm
 def tp_arm(args):
-    """--mode tp: one config-2 hTask tensor-parallel over the N ranks (strong
+    """--mode tp: the config-2 tasks tensor-parallel over the N ranks (strong
     scaling).  Megatron pairing over the 3-layer stack: L0 column-parallel
     (AG of the row-sharded input), L1 row-parallel (RS of the output), L2
     column-parallel; backward mirrors it (RS / AG / AR of dA or dB, see
-    paper_2603_02885_b200/tp.py).  Every rank's compute is the fused kernels."""
+    paper_2603_02885_b200/tp.py).  `--htasks g` splits the tasks into g
+    hTasks (contiguous task groups, each packed and multiplexed on its own)
+    whose subgraphs are interleaved by Alg. 1 so one hTask's collectives
+    overlap another's GEMMs (orchestrate.py, NEXT-1; `--comm-ctas c` caps
+    NCCL's CTAs).  Every rank's compute is the fused kernels."""
+    if args.comm_ctas:
+        os.environ["NCCL_MAX_CTAS"] = str(args.comm_ctas)
     import torch
     import torch.distributed as dist
-    from paper_2603_02885_b200 import mux, tp
+    from paper_2603_02885_b200 import mux, orchestrate, tp
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -500,48 +506,68 @@ def tp_arm(args):
     w = Workload(args.config)
     h = w.host_tensors()
     i32 = dict(dtype=torch.int32, device="cuda")
-    tso, sl = torch.tensor(w.off, **i32), torch.tensor(w.lens, **i32)
-    cap = torch.tensor(w.cap, **i32) if w.cap else None
-    bound = int(mux.pack_bound_rows(w.T, w.S, 64))
-    max_rows = -(-bound // (64 * world)) * 64 * world       # row blocks split evenly over ranks
-    pk = mux.alloc_pack_outputs(w.M, w.S, max_rows, max_rows // 64)
+    g = max(1, min(args.htasks, w.M))
+    groups = [list(range(w.M))[i * w.M // g:(i + 1) * w.M // g] for i in range(g)]
     r_cap = 16 * -(-max(w.wl.ranks) // 16)
-    st = list(range(w.M))
-    be = tp.MuxBackend()
-    mk = lambda A, B, r, sc: mux.Adapter(A, B, r, sc)  # noqa: E731
     kinds = ["col", "row", "col"]
-    layers = []
+    mk = lambda A, B, r, sc: mux.Adapter(A, B, r, sc)  # noqa: E731
+    Wsh = []
     for li, L in enumerate(w.linears):
         W = _bits_to_dev(h[f"W{li}"], torch)
-        ads = []
-        for t in range(w.M):
-            B = mux.make_B_storage(L.N, w.wl.ranks[t])
-            B.copy_(_bits_to_dev(h[f"B{li}_{t}"], torch))
-            ads.append(mux.Adapter(_bits_to_dev(h[f"A{li}_{t}"], torch), B, w.wl.ranks[t], w.wl.scales[t]))
         if kinds[li] == "col":
-            Wp, ap_ = tp.shard_column(W, ads, world, rank, mk)
-            layers.append(tp.ColumnParallelMuxLinear(be, Wp, ap_, r_cap))
+            Wsh.append(tp.shard_column(W, [], world, rank, mk)[0])
         else:
-            Wp, ap_ = tp.shard_row(W, ads, world, rank, mk)
-            layers.append(tp.RowParallelMuxLinear(be, Wp, ap_, r_cap))
+            Wsh.append(tp.shard_row(W, [], world, rank, mk)[0])
         del W
-    X1tok = _bits_to_dev(h["X1"], torch)
-    rows = max_rows // world
-    x_rows = torch.empty(rows, w.linears[0].K, dtype=torch.bfloat16, device="cuda")
-    nl = w.linears[-1].N // world
-    dY = torch.randn(max_rows, nl, device="cuda", generator=torch.Generator(device="cuda").manual_seed(rank)).bfloat16()
+    X1tok_all = _bits_to_dev(h["X1"], torch)
+    tok_off = np.concatenate([[0], np.cumsum([int(x.sum()) for x in w.wl.task_lens])])
+    htasks = []
+    for hi, tasks in enumerate(groups):
+        lens = [w.wl.task_lens[t] for t in tasks]
+        off = np.concatenate([[0], np.cumsum([len(x) for x in lens])]).astype(np.int32)
+        T_h = int(sum(int(x.sum()) for x in lens))
+        S_h = int(off[-1])
+        bound = int(mux.pack_bound_rows(T_h, S_h, 64))
+        max_rows = -(-bound // (64 * world)) * 64 * world       # row blocks split evenly over ranks
+        pk = mux.alloc_pack_outputs(len(tasks), S_h, max_rows, max_rows // 64)
+        be = tp.MuxBackend()
+        layers = []
+        for li, L in enumerate(w.linears):
+            ads = []
+            for t in tasks:
+                B = mux.make_B_storage(L.N, w.wl.ranks[t])
+                B.copy_(_bits_to_dev(h[f"B{li}_{t}"], torch))
+                ads.append(mux.Adapter(_bits_to_dev(h[f"A{li}_{t}"], torch), B, w.wl.ranks[t], w.wl.scales[t]))
+            shard = tp.shard_column if kinds[li] == "col" else tp.shard_row
+            _, ap_ = shard(torch.empty(L.N, L.K, dtype=torch.bfloat16, device="meta"), ads, world, rank, mk)
+            cls = tp.ColumnParallelMuxLinear if kinds[li] == "col" else tp.RowParallelMuxLinear
+            layers.append(cls(be, Wsh[li], ap_, r_cap))
+        rows = max_rows // world
+        nl = w.linears[-1].N // world
+        ht = {"tasks": tasks, "T": T_h, "max_rows": max_rows, "rows": rows, "pk": pk, "layers": layers,
+              "tso": torch.tensor(off, **i32),
+              "sl": torch.tensor(np.concatenate(lens).astype(np.int32), **i32),
+              "cap": torch.tensor([w.cap[t] for t in tasks], **i32) if w.cap else None,
+              "X1tok": X1tok_all[int(tok_off[tasks[0]]):int(tok_off[tasks[-1] + 1])],
+              "x_rows": torch.empty(rows, w.linears[0].K, dtype=torch.bfloat16, device="cuda"),
+              "dY": torch.randn(max_rows, nl, device="cuda",
+                                generator=torch.Generator(device="cuda").manual_seed(rank + 7 * hi)).bfloat16()}
+
+        def dispatch(e, ht=ht):
+            mux.pack_chunks(ht["tso"], ht["sl"], ht["cap"], 0, 64, max_rows=ht["max_rows"],
+                            max_chunks=ht["max_rows"] // 64, out=ht["pk"])
+            mux.pack_apply(ht["pk"]["row_src"][rank * ht["rows"]:(rank + 1) * ht["rows"]], ht["X1tok"],
+                           ht["rows"], out=ht["x_rows"])
+            return ht["x_rows"]
+        lat = [2.0 * max_rows * L.K * L.N / world for L in w.linears]   # modeled GEMM cost per layer pass
+        ht["ops"] = orchestrate.linear_chain_ops(layers, kinds, ht["pk"]["seg_off"], list(range(len(tasks))),
+                                                 dispatch, ht["dY"], lat)
+        htasks.append(ht)
+    dags = [orchestrate.build_subgraphs(i, ht["ops"]) for i, ht in enumerate(htasks)]
+    schedule = orchestrate.subgraph_schedule(dags)
 
     def step():
-        mux.pack_chunks(tso, sl, cap, 0, 64, max_rows=max_rows, max_chunks=max_rows // 64, out=pk)
-        seg_off = pk["seg_off"]
-        mux.pack_apply(pk["row_src"][rank * rows:(rank + 1) * rows], X1tok, rows, out=x_rows)
-        y = layers[0].forward(seg_off, st, x_rows)     # [R, N0/p]
-        y = layers[1].forward(seg_off, st, y)          # [R/p, N1]
-        y = layers[2].forward(seg_off, st, y)          # [R, N2/p]
-        g, _, _ = layers[2].backward(seg_off, st, dY)  # [R/p, N1]
-        g, _, _ = layers[1].backward(seg_off, st, g)   # [R, N0/p]
-        g, _, _ = layers[0].backward(seg_off, st, g)   # [R/p, K0]
-        return g
+        orchestrate.run_schedule(schedule, [dict() for _ in htasks])
 
     for _ in range(args.warmup):
         step()
@@ -564,7 +590,10 @@ def tp_arm(args):
                           "config": {"workload": f"config {args.config}: " + w.wl.description,
                                      "parallelism": f"tp{world} (L0 column, L1 row, L2 column; sequence-parallel "
                                                     "AG/RS over NCCL)", "valid_tokens": w.T,
-                                     "max_rows": max_rows},
+                                     "htasks": [ht["tasks"] for ht in htasks],
+                                     "schedule": [f"h{sg.htask}.{sg.index}" for sg, _ in schedule],
+                                     "nccl_max_ctas": args.comm_ctas or None,
+                                     "max_rows": [ht["max_rows"] for ht in htasks]},
                           "tflops_per_gpu_algorithmic": w.flops / (ms * 1e-3) / 1e12 / world}), flush=True)
     dist.destroy_process_group()
 
@@ -582,6 +611,8 @@ def main():
     ap.add_argument("--ref-rows", type=int, default=4, help="rows per task per reference-arm step")
     ap.add_argument("--mode", default="replicas", choices=["replicas", "tp"],
                     help="N>1: task-sharded replicas (default, weak scaling) or tensor parallel (strong)")
+    ap.add_argument("--htasks", type=int, default=1, help="--mode tp: hTasks interleaved by Alg. 1 (NEXT-1)")
+    ap.add_argument("--comm-ctas", type=int, default=0, help="--mode tp: NCCL_MAX_CTAS for the overlapped collectives")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

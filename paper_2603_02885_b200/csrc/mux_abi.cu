@@ -111,6 +111,15 @@ bool make_map(CUtensorMap* out, const void* ptr, uint64_t inner, uint64_t outer,
   }
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
+  // The driver call needs a current context on this thread.  A thread that has
+  // made no runtime call yet (e.g. PyTorch's autograd worker) has none: a
+  // no-op runtime call binds the current device's primary context (or keeps
+  // the caller's own current context).
+  static thread_local bool ctx_bound = false;
+  if (!ctx_bound) {
+    cudaFree(nullptr);
+    ctx_bound = true;
+  }
   cuuint64_t dims[2] = {inner, outer};
   cuuint64_t strides[1] = {stride * 2};
   cuuint32_t box[2] = {box_inner, box_outer};
@@ -323,10 +332,16 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
   const int kred = bwd ? N : K;
   const int nout = bwd ? K : N;
   __nv_bfloat16* side = bwd ? ws.gs : (Hs_out ? Hs_out : ws.hs);
-  if (!make_map(&p.map_a, a_in, kred, max_rows, kred, 64, 128) || !make_map(&p.map_w, W, K, N, K, 64, 64) ||
-      !make_map(&p.map_side, side, r_cap, max_rows, r_cap, 64, 128) ||
-      (out && !make_map(&p.map_out, out, nout, max_rows, nout, 64, 32)))
-    return fail(MUX_ERR_CUDA, "cuTensorMapEncodeTiled failed (driver entry point missing?)");
+  if (!make_map(&p.map_a, a_in, kred, max_rows, kred, 64, 128))
+    return fail(MUX_ERR_CUDA, "cuTensorMapEncodeTiled failed for %s %p [%d x %d]", bwd ? "dY" : "X", a_in, max_rows, kred);
+  if (!make_map(&p.map_w, W, K, N, K, 64, 64))
+    return fail(MUX_ERR_CUDA, "cuTensorMapEncodeTiled failed for W %p [%d x %d]", W, N, K);
+  if (!make_map(&p.map_side, side, r_cap, max_rows, r_cap, 64, 128))
+    return fail(MUX_ERR_CUDA, "cuTensorMapEncodeTiled failed for %s %p [%d x %d]", bwd ? "Gs" : "Hs", side, max_rows,
+                r_cap);
+  if (out && !make_map(&p.map_out, out, nout, max_rows, nout, 64, 32))
+    return fail(MUX_ERR_CUDA, "cuTensorMapEncodeTiled failed for %s %p [%d x %d]", bwd ? "dX" : "Y", out, max_rows,
+                nout);
   st = fill_adapter_maps(p, num_adapters, adapters, K, N);
   if (st != MUX_OK) return st;
   p.seg_off = seg_off;
@@ -372,7 +387,7 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
     if (!make_map(&g.map_x, X, K, max_rows, K, 64, 128) || !make_map(&g.map_dy, a_in, N, max_rows, N, 64, 128) ||
         !make_map(&g.map_hs, Hs_in, r_cap, max_rows, r_cap, 64, 128) ||
         !make_map(&g.map_gs, ws.gs, r_cap, max_rows, r_cap, 64, 128))
-      return fail(MUX_ERR_CUDA, "cuTensorMapEncodeTiled failed (grad)");
+      return fail(MUX_ERR_CUDA, "cuTensorMapEncodeTiled failed for a gradient-kernel operand (X, dY, Hs or Gs)");
     g.seg_off = seg_off;
     g.num_segs = num_segs;
     g.K = K;

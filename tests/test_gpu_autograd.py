@@ -41,3 +41,30 @@ def test_autograd_matches_binding():
     assert lin.B[1].stride(0) == 8 and not torch.equal(lin.B[1].detach(), before)
     Y3 = lin(X, seg_off, st)
     assert not torch.equal(Y3.view(torch.int16), Y.view(torch.int16))
+
+
+def test_call_from_fresh_thread():
+    """The ABI encodes TMA descriptors with a driver call; a thread that has
+    made no CUDA runtime call yet (PyTorch's autograd worker is one) must work."""
+    import threading
+    torch.manual_seed(1)
+    R, K, N = 256, 128, 192
+    W = (torch.randn(N, K, device="cuda") / K ** 0.5).bfloat16()
+    X = torch.randn(R, K, device="cuda").bfloat16()
+    seg_off = torch.tensor([0, 256], dtype=torch.int32, device="cuda")
+    B = mux.make_B_storage(N, 8)
+    B.copy_(torch.randn(N, 8, device="cuda").bfloat16())
+    ads = [mux.Adapter((torch.randn(8, K, device="cuda") / K ** 0.5).bfloat16(), B, 8, 2.0)]
+    ref, _ = mux.linear_fwd(seg_off, [0], ads, X, W, 16)
+    out = {}
+
+    def run():
+        Y = torch.empty_like(ref)   # a fresh output buffer: its descriptor is not cached yet
+        out["Y"], _ = mux.linear_fwd(seg_off, [0], ads, X, W, 16, Y=Y)
+        torch.cuda.synchronize()
+
+    th = threading.Thread(target=run)
+    th.start()
+    th.join()
+    torch.cuda.synchronize()
+    assert torch.equal(out["Y"].view(torch.int16), ref.view(torch.int16))

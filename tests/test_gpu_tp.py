@@ -14,19 +14,25 @@ if not torch.cuda.is_available():
 
 import torch.distributed as dist  # noqa: E402
 
-from paper_2603_02885_b200 import mux, tp  # noqa: E402
+from paper_2603_02885_b200 import mux, orchestrate, tp  # noqa: E402
 
 
 def _bits(t):
     return t.view(torch.int16) if t.dtype == torch.bfloat16 else t
 
 
-def test_tp_world1_equals_direct():
+@pytest.fixture(scope="module")
+def pg():
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     os.environ.setdefault("MASTER_PORT", "29533")
     if not dist.is_initialized():
         dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
-    try:
+    yield
+    dist.destroy_process_group()
+
+
+def test_tp_world1_equals_direct(pg):
+    if True:
         g = torch.Generator(device="cuda").manual_seed(3)
         R, K, N = 512, 256, 384
         seg_off = torch.tensor([0, 192, 320, 512], dtype=torch.int32, device="cuda")
@@ -68,5 +74,66 @@ def test_tp_world1_equals_direct():
         ref = [Y, dX] + [a.dA for a in a1] + [a.dB for a in a1] + [a.dA for a in a2] + [a.dB for a in a2]
         for a_, b_ in zip(got, ref):
             assert torch.equal(_bits(a_), _bits(b_))
-    finally:
-        dist.destroy_process_group()
+
+
+def test_orchestrated_htasks_world1_equals_direct(pg):
+    """Two hTasks through a column/row/column chain, interleaved by Alg. 1 with
+    asynchronous NCCL collectives (orchestrate.py, NEXT-1), equal each hTask
+    run through the binding directly, bit for bit."""
+    g = torch.Generator(device="cuda").manual_seed(11)
+    K, N = 256, 512
+    shapes = [(N, K), (K, N), (N, K)]
+    kinds = ["col", "row", "col"]
+    mk = lambda A, B, r, s: mux.Adapter(A, B, r, s)  # noqa: E731
+    Ws = [(torch.randn(n, k, device="cuda", generator=g) / k ** 0.5).bfloat16() for n, k in shapes]
+    cfgs = [([0, 256, 448], [16, 8]), ([0, 128, 192, 640], [4, 32, 16])]
+    hts = []
+    for so_l, ranks in cfgs:
+        so = torch.tensor(so_l, dtype=torch.int32, device="cuda")
+        ads_all = []
+        for n, k in shapes:
+            ads = []
+            for r in ranks:
+                B = mux.make_B_storage(n, r)
+                B.copy_(torch.randn(n, r, device="cuda", generator=g).bfloat16())
+                ads.append(mux.Adapter((torch.randn(r, k, device="cuda", generator=g) / k ** 0.5).bfloat16(),
+                                       B, r, 2.0))
+            ads_all.append(ads)
+        R = so_l[-1]
+        X = torch.randn(R, K, device="cuda", generator=g).bfloat16()
+        dY = torch.randn(R, N, device="cuda", generator=g).bfloat16()
+        be = tp.MuxBackend()
+        lays = []
+        for li, kind in enumerate(kinds):
+            shard = tp.shard_column if kind == "col" else tp.shard_row
+            Wp, ap = shard(Ws[li], ads_all[li], 1, 0, mk)
+            lays.append((tp.ColumnParallelMuxLinear if kind == "col" else tp.RowParallelMuxLinear)(be, Wp, ap, 32))
+        hts.append((so, list(range(len(ranks))), ads_all, X, dY, lays))
+    dags, envs = [], []
+    for i, (so, st, ads_all, X, dY, lays) in enumerate(hts):
+        ops = orchestrate.linear_chain_ops(lays, kinds, so, st, lambda e, X=X: X, dY, [1.0 + i] * 3)
+        dags.append(orchestrate.build_subgraphs(i, ops))
+        envs.append({})
+    orchestrate.run_schedule(orchestrate.subgraph_schedule(dags), envs)
+    torch.cuda.synchronize()
+    got = [(envs[i]["Y2"].clone(), envs[i]["dX0"].clone(),
+            [a.dA.clone() for li in range(3) for a in hts[i][5][li].ads],
+            [a.dB.clone() for li in range(3) for a in hts[i][5][li].ads]) for i in range(len(hts))]
+    for i, (so, st, ads_all, X, dY, lays) in enumerate(hts):
+        x, Hs = X, []
+        xs = []
+        for li in range(3):
+            xs.append(x)
+            x, hs = mux.linear_fwd(so, st, ads_all[li], x, Ws[li], 32)
+            Hs.append(hs)
+        y = x.clone()
+        d = dY
+        for li in reversed(range(3)):
+            d = mux.linear_bwd(so, st, ads_all[li], d, xs[li], Ws[li], Hs[li], 32)
+        torch.cuda.synchronize()
+        assert torch.equal(_bits(got[i][0]), _bits(y))
+        assert torch.equal(_bits(got[i][1]), _bits(d))
+        ref_dA = [a.dA for li in range(3) for a in ads_all[li]]
+        ref_dB = [a.dB for li in range(3) for a in ads_all[li]]
+        for a_, b_ in zip(got[i][2] + got[i][3], ref_dA + ref_dB):
+            assert torch.equal(a_, b_)
