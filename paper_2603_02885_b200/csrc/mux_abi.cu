@@ -361,10 +361,16 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
   p.has_main = out != nullptr;
   // raster band: keep the band's A rows (group_m * 256 rows * kred * 2 B)
   // within ~48 MB of the 126 MB L2, leaving room for the streamed W tiles
+#ifndef MUX_BAND_MB
+#define MUX_BAND_MB 48
+#endif
+#ifndef MUX_BAND_MIN
+#define MUX_BAND_MIN 4
+#endif
   {
     const long long band_bytes = static_cast<long long>(kPairRows) * kred * 2;
-    long long g = (48ll << 20) / band_bytes;
-    p.group_m = static_cast<int32_t>(std::max(4ll, std::min(32ll, g)));
+    long long g = (static_cast<long long>(MUX_BAND_MB) << 20) / band_bytes;
+    p.group_m = static_cast<int32_t>(std::max(static_cast<long long>(MUX_BAND_MIN), std::min(32ll, g)));
   }
   for (int s = 0; s < num_segs; ++s) {
     const mux_adapter& a = adapters[seg_task[s]];
