@@ -181,14 +181,16 @@ def load_profile(path: str) -> dict:
 
 def stage_from_profile(prof: dict, n_gpus: int = 1) -> Stage:
     """A single-stage model of the profiled layer stack: one BaseOp per linear
-    (rank-0 timings), adapters folded in as (extra latency of the rank-r run,
+    (rank-0 timings, halved to one pass), adapters folded in as (extra latency of the rank-r run,
     utilisation 1).  The adapters run inside the fused kernel (R18), so their
     cost is additive and fully utilised: max(sum, max) = sum."""
+    # Eq. 3 is one pass; Eq. 4's factor 2 adds the backward (fwd ~ bwd without
+    # dW, P:561, P:668).  The profile times fwd+bwd, so one pass = half.
     base, adap = [], []
     for lin in prof["linears"]:
         xs = lin["tokens"]
-        base.append(OpProfile(xs, lin["ms_rank0"]))
-        extra = [max(0.0, a - b) for a, b in zip(lin["ms_rank"], lin["ms_rank0"])]
+        base.append(OpProfile(xs, [0.5 * v for v in lin["ms_rank0"]]))
+        extra = [0.5 * max(0.0, a - b) for a, b in zip(lin["ms_rank"], lin["ms_rank0"])]
         # per-task adapter latency at k tokens: the extra cost scales with that task's rows
         adap.append((OpProfile(xs, extra), lambda k: 1.0))
     return Stage(base, adap, n_gpus)

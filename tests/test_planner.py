@@ -158,5 +158,8 @@ def test_stage_from_profile_roundtrip():
     prof = {"linears": [{"shape": [4096, 4096], "tokens": [512, 1024, 2048],
                          "ms_rank0": [0.1, 0.15, 0.25], "ms_rank": [0.12, 0.18, 0.3]}]}
     st = pl.stage_from_profile(prof)
-    # base 0.15 at 1024 tokens; adapters (u = 1): extra(512) + extra(512) = 0.02 + 0.02
-    assert pl.stage_latency(st, [512, 512]) == pytest.approx(0.15 + 0.04)
+    # one pass = half the fwd+bwd profile: base 0.15/2 at 1024 tokens;
+    # adapters (u = 1): (extra(512) + extra(512)) / 2 = (0.02 + 0.02) / 2
+    assert pl.stage_latency(st, [512, 512]) == pytest.approx(0.075 + 0.02)
+    # with S = 1, C = 1, Eq. 4 doubles it back to the fwd+bwd time
+    assert pl.htask_latency([st], C=1)([512, 512]) == pytest.approx(0.19)
