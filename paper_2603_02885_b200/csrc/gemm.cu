@@ -48,11 +48,7 @@ namespace mux {
 constexpr uint32_t kBox = 64 * 128;                  // 8 KB: one {64 x 128 B} TMA box
 constexpr uint32_t kSubA = kBM * 128;                // 16 KB: one k-subtile of A
 constexpr uint32_t kEpiBuf = 32 * 128;               // 32 rows x 64 bf16 (one TMA store box)
-#ifdef MUX_EPI_DIRECT
-constexpr uint32_t kSmemEpi = 0;
-#else
 constexpr uint32_t kSmemEpi = 4 * 2 * kEpiBuf;
-#endif
 constexpr uint32_t kSmemMisc = 1024;
 
 template <bool kBwd>
@@ -517,26 +513,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(tempty_leader);
           }
-#ifdef MUX_EPI_DIRECT
-          {
-            const int col = col_t + c * 64;
-            if (valid && col < p.nout) {
-              uint4* dst = reinterpret_cast<uint4*>(p.out + static_cast<size_t>(row_w + lane) * p.nout + col);
-#pragma unroll
-              for (int ch = 0; ch < 8; ++ch) {
-                const uint32_t* v = ch < 4 ? v0 : v1;
-                const int b = (ch & 3) * 8;
-                uint4 w;
-                w.x = pack_bf16x2(__uint_as_float(v[b + 0]), __uint_as_float(v[b + 1]));
-                w.y = pack_bf16x2(__uint_as_float(v[b + 2]), __uint_as_float(v[b + 3]));
-                w.z = pack_bf16x2(__uint_as_float(v[b + 4]), __uint_as_float(v[b + 5]));
-                w.w = pack_bf16x2(__uint_as_float(v[b + 6]), __uint_as_float(v[b + 7]));
-                dst[ch] = w;
-              }
-            }
-            continue;
-          }
-#endif
           uint8_t* buf = bufs + buf_sel * kEpiBuf;
           if (lane == 0) tma_store_wait_read<1>();
           __syncwarp();
