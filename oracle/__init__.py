@@ -10,6 +10,9 @@ Contents
   linear.c   multiplexed LoRA linear fwd/bwd (Eq. 1-2 + north_star
              LoRA formula) — plain C, fp64, fixed ascending summation order.
   linear.py  ctypes wrapper around liboracle.so (bf16 bits -> fp64 widening).
+  block.py   decoder-block ops around the linears (NEXT-3): causal attention
+             inside packed sequences (chunk KV reuse), RoPE,
+             RMSNorm, SwiGLU — numpy fp64, from the definitions.
 
 Pins (tests/test_oracle_*.py, `-m "not gpu"`): see DESIGN.md §"Oracle pins".
 Parity unpinned: none of the functions here (the paper's 0.07 MSD convergence
