@@ -17,6 +17,15 @@
  *   mux_linear_bwd   BaseOp backward Eq. 2 plus the LoRA chain
  *                    rule: dX = dY W + s_t (dY B_t) A_t, dA_t, dB_t; no
  *                    backbone weight gradient (frozen backbone).
+ *   Decoder-block ops around the linears (NEXT-3; LLaMA, the backbones of
+ *   the paper's workloads):
+ *   mux_pack_row_start  per packed row, the first row of its sequence
+ *   mux_attn_fwd/bwd    causal attention inside packed sequences: the chunk
+ *                       dependency "KV cache reuse in causal attention"
+ *                       (Fig. alignment), masked per sequence
+ *
+ *   mux_rope            rotary position embedding at in-sequence positions
+ *   mux_rmsnorm_fwd/bwd, mux_swiglu_fwd/bwd
  *
  * Conventions (all functions)
  *   - Pointers are DEVICE pointers unless marked [host].  The caller owns
@@ -202,6 +211,66 @@ MUX_API mux_status mux_linear_bwd(int32_t num_segs, const int32_t* seg_off, cons
                           const mux_bf16* W, const mux_bf16* Hs,
                           mux_bf16* dX,
                           void* workspace, size_t workspace_bytes, cudaStream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * Decoder-block ops (NEXT-3).  Row-major bf16 matrices with an explicit row
+ * stride `ld*` in ELEMENTS (a multiple of 8: 16-byte rows), so q/k/v or
+ * gate/up can be column slices of one fused projection output.  fp32 math.
+ * Errors: MUX_ERR_INVALID_ARGUMENT (sizes, strides, 16-byte alignment),
+ * MUX_ERR_INSUFFICIENT_BUFFER, MUX_ERR_CUDA.
+ * ------------------------------------------------------------------------- */
+
+/* row_start[r] for r < max_rows: the first packed row of row r's sequence,
+ * -1 for pad rows.  seq_len [num_seqs] and seq_row [num_seqs] are the
+ * mux_pack_chunks inputs/outputs (a sequence occupies rows
+ * [seq_row[s], seq_row[s] + seq_len[s]) of its pack). */
+MUX_API mux_status mux_pack_row_start(int32_t num_seqs, const int32_t* seq_len, const int32_t* seq_row,
+                                      int32_t max_rows, int32_t* row_start, cudaStream_t stream);
+
+/* Causal attention inside packed sequences, per head h (kv head h / (H/Hkv)):
+ *   o[r,h,:] = sum_{j = row_start[r]..r} softmax_j(scale <q[r,h,:], k[j,hk,:]>) v[j,hk,:]
+ *   lse[r,h] = log sum_j exp(scale <q, k>)   (fp32 [rows, H]; -inf, o = 0 for pad rows)
+ * q [rows, H*128] (row stride ldq), k, v [rows, Hkv*128]; head dim 128;
+ * H % Hkv == 0.  Warp-level tensor-core MMAs, flash-style (S never in HBM). */
+MUX_API mux_status mux_attn_fwd(int32_t rows, int32_t heads, int32_t kv_heads, int32_t head_dim,
+                                const mux_bf16* q, int64_t ldq, const mux_bf16* k, int64_t ldk,
+                                const mux_bf16* v, int64_t ldv, const int32_t* row_start, float scale,
+                                mux_bf16* o, int64_t ldo, float* lse, cudaStream_t stream);
+
+/* Gradients of the above for upstream dO: dq [rows, H*128], dk, dv
+ * [rows, Hkv*128] (overwritten; pad rows 0).  Deterministic (no atomics).
+ * workspace: >= mux_attn_workspace_size(rows, heads) bytes, no zeroing needed. */
+MUX_API size_t mux_attn_workspace_size(int32_t rows, int32_t heads);
+MUX_API mux_status mux_attn_bwd(int32_t rows, int32_t heads, int32_t kv_heads, int32_t head_dim,
+                                const mux_bf16* dO, int64_t lddo, const mux_bf16* q, int64_t ldq,
+                                const mux_bf16* k, int64_t ldk, const mux_bf16* v, int64_t ldv,
+                                const mux_bf16* o, int64_t ldo, const float* lse, const int32_t* row_start,
+                                float scale, mux_bf16* dq, int64_t lddq, mux_bf16* dk, int64_t lddk,
+                                mux_bf16* dv, int64_t lddv, void* workspace, size_t workspace_bytes,
+                                cudaStream_t stream);
+
+/* Rotary position embedding, IN PLACE on x [rows, heads*head_dim] (stride ld):
+ * pairs (i, i + d/2) of each head rotated by pos * base^(-2i/d), pos =
+ * r - row_start[r] (inverse != 0: by the negative angle = the backward).
+ * Pad rows (row_start -1) untouched.  head_dim a multiple of 16. */
+MUX_API mux_status mux_rope(int32_t rows, int32_t heads, int32_t head_dim, mux_bf16* x, int64_t ld,
+                            const int32_t* row_start, float base, int32_t inverse, cudaStream_t stream);
+
+/* RMSNorm y = x / sqrt(mean(x^2) + eps) * w; backward dx for upstream dy (w is
+ * frozen backbone: no dw).  x, y, dy, dx [rows, dim]; w [dim]; dim % 8 == 0. */
+MUX_API mux_status mux_rmsnorm_fwd(int32_t rows, int32_t dim, const mux_bf16* x, int64_t ldx, const mux_bf16* w,
+                                   float eps, mux_bf16* y, int64_t ldy, cudaStream_t stream);
+MUX_API mux_status mux_rmsnorm_bwd(int32_t rows, int32_t dim, const mux_bf16* dy, int64_t lddy,
+                                   const mux_bf16* x, int64_t ldx, const mux_bf16* w, float eps, mux_bf16* dx,
+                                   int64_t lddx, cudaStream_t stream);
+
+/* SwiGLU h = silu(g) * u; backward dg = dh u s (1 + g (1 - s)), du = dh silu(g),
+ * s = sigmoid(g).  All [rows, dim], dim % 8 == 0. */
+MUX_API mux_status mux_swiglu_fwd(int32_t rows, int32_t dim, const mux_bf16* g, int64_t ldg, const mux_bf16* u,
+                                  int64_t ldu, mux_bf16* h, int64_t ldh, cudaStream_t stream);
+MUX_API mux_status mux_swiglu_bwd(int32_t rows, int32_t dim, const mux_bf16* dh, int64_t lddh, const mux_bf16* g,
+                                  int64_t ldg, const mux_bf16* u, int64_t ldu, mux_bf16* dg, int64_t lddg,
+                                  mux_bf16* du, int64_t lddu, cudaStream_t stream);
 
 #ifdef __cplusplus
 }

@@ -1,0 +1,284 @@
+// block.cu — the HBM-bound decoder-block ops around the multiplexed linears
+// (SURVEY §8(f) NEXT-3): packed-row sequence map, RMSNorm, SwiGLU, RoPE.
+// LLaMA definitions (the backbones of the paper's workloads); the
+// backbone is frozen, so RMSNorm's weight gets no gradient.  Every
+// kernel moves 16-byte vectors (8 bf16) and accumulates in fp32.
+#include <algorithm>
+#include <cmath>
+
+#include "common.h"
+#include "launch.cuh"
+#include "ptx.cuh"
+
+namespace mux {
+
+// ------------------------------------------------------------------ row map
+// row_start[r] = first packed row of r's sequence, -1 for pad rows (the
+// chunk layout of P:837: a sequence occupies consecutive rows of its pack).
+__global__ void __launch_bounds__(256) mux_row_fill_kernel(int32_t* row_start, int n) {
+  griddep_wait();
+  griddep_launch_dependents();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) row_start[i] = -1;
+}
+
+__global__ void __launch_bounds__(256) mux_row_scatter_kernel(int num_seqs, const int32_t* seq_len,
+                                                             const int32_t* seq_row, int32_t* row_start,
+                                                             int max_rows) {
+  griddep_wait();
+  griddep_launch_dependents();
+  for (int s = blockIdx.x; s < num_seqs; s += gridDim.x) {
+    const int a = seq_row[s];
+    const int L = seq_len[s];
+    for (int i = threadIdx.x; i < L; i += blockDim.x)
+      if (a + i < max_rows) row_start[a + i] = a;
+  }
+}
+
+// ------------------------------------------------------------------ helpers
+__device__ __forceinline__ void bf16x8_to_f32(const uint4& v, float (&f)[8]) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    f[2 * i] = __uint_as_float(w[i] << 16);
+    f[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+  }
+}
+__device__ __forceinline__ uint4 f32_to_bf16x8(const float (&f)[8]) {
+  return make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]), pack_bf16x2(f[4], f[5]),
+                    pack_bf16x2(f[6], f[7]));
+}
+
+template <int kThreads>
+__device__ __forceinline__ float block_sum(float v, float* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) red[w] = v;
+  __syncthreads();
+  float t = 0.f;
+#pragma unroll
+  for (int i = 0; i < kThreads / 32; ++i) t += red[i];
+  __syncthreads();
+  return t;
+}
+
+// ------------------------------------------------------------------ RMSNorm
+// One CTA per row.  fwd: y = x * rstd * w, rstd = 1/sqrt(mean(x^2) + eps).
+constexpr int kNormThreads = 256;
+
+__global__ void __launch_bounds__(kNormThreads) mux_rmsnorm_fwd_kernel(int dim, const uint4* x, long long ldx,
+                                                                      const uint4* w, float eps, uint4* y,
+                                                                      long long ldy) {
+  __shared__ float red[kNormThreads / 32];
+  griddep_wait();
+  griddep_launch_dependents();
+  const int row = blockIdx.x;
+  const uint4* xr = x + static_cast<long long>(row) * ldx;
+  const int nc = dim / 8;
+  float ss = 0.f;
+  for (int c = threadIdx.x; c < nc; c += kNormThreads) {
+    float f[8];
+    bf16x8_to_f32(xr[c], f);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) ss = fmaf(f[i], f[i], ss);
+  }
+  const float rstd = rsqrtf(block_sum<kNormThreads>(ss, red) / static_cast<float>(dim) + eps);
+  uint4* yr = y + static_cast<long long>(row) * ldy;
+  for (int c = threadIdx.x; c < nc; c += kNormThreads) {
+    float f[8], g[8];
+    bf16x8_to_f32(xr[c], f);
+    bf16x8_to_f32(w[c], g);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) f[i] = f[i] * rstd * g[i];
+    yr[c] = f32_to_bf16x8(f);
+  }
+}
+
+// bwd (w frozen): g = dy * w;  dx = rstd * (g - x * rstd^2 * mean(g * x)).
+__global__ void __launch_bounds__(kNormThreads) mux_rmsnorm_bwd_kernel(int dim, const uint4* dy, long long lddy,
+                                                                      const uint4* x, long long ldx,
+                                                                      const uint4* w, float eps, uint4* dx,
+                                                                      long long lddx) {
+  __shared__ float red[kNormThreads / 32];
+  griddep_wait();
+  griddep_launch_dependents();
+  const int row = blockIdx.x;
+  const uint4* xr = x + static_cast<long long>(row) * ldx;
+  const uint4* dyr = dy + static_cast<long long>(row) * lddy;
+  const int nc = dim / 8;
+  float ss = 0.f, gx = 0.f;
+  for (int c = threadIdx.x; c < nc; c += kNormThreads) {
+    float f[8], d[8], g[8];
+    bf16x8_to_f32(xr[c], f);
+    bf16x8_to_f32(dyr[c], d);
+    bf16x8_to_f32(w[c], g);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      ss = fmaf(f[i], f[i], ss);
+      gx = fmaf(d[i] * g[i], f[i], gx);
+    }
+  }
+  const float inv_dim = 1.f / static_cast<float>(dim);
+  const float rstd = rsqrtf(block_sum<kNormThreads>(ss, red) * inv_dim + eps);
+  const float coef = rstd * rstd * block_sum<kNormThreads>(gx, red) * inv_dim;
+  uint4* dxr = dx + static_cast<long long>(row) * lddx;
+  for (int c = threadIdx.x; c < nc; c += kNormThreads) {
+    float f[8], d[8], g[8];
+    bf16x8_to_f32(xr[c], f);
+    bf16x8_to_f32(dyr[c], d);
+    bf16x8_to_f32(w[c], g);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) f[i] = rstd * (d[i] * g[i] - f[i] * coef);
+    dxr[c] = f32_to_bf16x8(f);
+  }
+}
+
+// ------------------------------------------------------------------ SwiGLU
+__device__ __forceinline__ float sigmoidf_(float z) { return 1.f / (1.f + __expf(-z)); }
+
+__global__ void __launch_bounds__(256) mux_swiglu_fwd_kernel(int rows, int dim, const uint4* g, long long ldg,
+                                                            const uint4* u, long long ldu, uint4* h,
+                                                            long long ldh) {
+  griddep_wait();
+  griddep_launch_dependents();
+  const int nc = dim / 8;
+  const long long total = static_cast<long long>(rows) * nc;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long r = i / nc;
+    const int c = static_cast<int>(i - r * nc);
+    float a[8], b[8];
+    bf16x8_to_f32(g[r * ldg + c], a);
+    bf16x8_to_f32(u[r * ldu + c], b);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = a[k] * sigmoidf_(a[k]) * b[k];
+    h[r * ldh + c] = f32_to_bf16x8(a);
+  }
+}
+
+// dg = dh * u * s (1 + g (1 - s)),  du = dh * g * s,  s = sigmoid(g)
+__global__ void __launch_bounds__(256) mux_swiglu_bwd_kernel(int rows, int dim, const uint4* dh, long long lddh,
+                                                            const uint4* g, long long ldg, const uint4* u,
+                                                            long long ldu, uint4* dg, long long lddg, uint4* du,
+                                                            long long lddu) {
+  griddep_wait();
+  griddep_launch_dependents();
+  const int nc = dim / 8;
+  const long long total = static_cast<long long>(rows) * nc;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long r = i / nc;
+    const int c = static_cast<int>(i - r * nc);
+    float d[8], a[8], b[8], o1[8], o2[8];
+    bf16x8_to_f32(dh[r * lddh + c], d);
+    bf16x8_to_f32(g[r * ldg + c], a);
+    bf16x8_to_f32(u[r * ldu + c], b);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float s = sigmoidf_(a[k]);
+      o1[k] = d[k] * b[k] * s * (1.f + a[k] * (1.f - s));
+      o2[k] = d[k] * a[k] * s;
+    }
+    dg[r * lddg + c] = f32_to_bf16x8(o1);
+    du[r * lddu + c] = f32_to_bf16x8(o2);
+  }
+}
+
+// ------------------------------------------------------------------ RoPE
+// In place on x [rows, heads * d] (row stride ld): pairs (i, i + d/2) of each
+// head rotated by theta_i = pos * base^(-2i/d), pos = r - row_start[r]
+// (inverse != 0: by -theta, the backward).  Pad rows are left untouched.
+__global__ void __launch_bounds__(256) mux_rope_kernel(int rows, int heads, int d, uint4* x, long long ld,
+                                                      const int32_t* row_start, float log2_base, int inverse) {
+  griddep_wait();
+  griddep_launch_dependents();
+  const int half_c = d / 16;  // 8-wide chunks per half head
+  const long long total = static_cast<long long>(rows) * heads * half_c;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long r = i / (heads * half_c);
+    const int rem = static_cast<int>(i - r * heads * half_c);
+    const int h = rem / half_c;
+    const int c = rem - h * half_c;
+    const int rs = row_start[r];
+    if (rs < 0) continue;
+    const float pos = static_cast<float>(r - rs);
+    uint4* base = x + r * ld + (static_cast<long long>(h) * d) / 8;
+    float a[8], b[8];
+    bf16x8_to_f32(base[c], a);
+    bf16x8_to_f32(base[c + half_c], b);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int idx = 8 * c + k;
+      const float inv_freq = exp2f(-2.f * static_cast<float>(idx) / static_cast<float>(d) * log2_base);
+      float sn, cs;
+      sincosf(pos * inv_freq, &sn, &cs);
+      if (inverse) sn = -sn;
+      const float x0 = a[k], x1 = b[k];
+      a[k] = x0 * cs - x1 * sn;
+      b[k] = x1 * cs + x0 * sn;
+    }
+    base[c] = f32_to_bf16x8(a);
+    base[c + half_c] = f32_to_bf16x8(b);
+  }
+}
+
+// ------------------------------------------------------------------ launchers
+static unsigned grid_for(long long work, int per_block, int num_sms) {
+  long long b = (work + per_block - 1) / per_block;
+  const long long cap = static_cast<long long>(num_sms) * 16;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return static_cast<unsigned>(b);
+}
+
+cudaError_t launch_row_start(int num_seqs, const int32_t* seq_len, const int32_t* seq_row, int max_rows,
+                             int32_t* row_start, int num_sms, cudaStream_t s) {
+  cudaError_t e = launch_pdl(mux_row_fill_kernel, dim3(grid_for(max_rows, 256, num_sms)), dim3(256), 0, s,
+                             row_start, max_rows);
+  if (e != cudaSuccess || num_seqs == 0) return e;
+  return launch_pdl(mux_row_scatter_kernel, dim3(std::min(num_seqs, num_sms * 8)), dim3(256), 0, s, num_seqs,
+                    seq_len, seq_row, row_start, max_rows);
+}
+
+cudaError_t launch_rmsnorm(bool bwd, int rows, int dim, const void* a, long long lda, const void* x, long long ldx,
+                           const void* w, float eps, void* out, long long ldo, cudaStream_t s) {
+  if (rows == 0) return cudaSuccess;
+  if (!bwd)
+    return launch_pdl(mux_rmsnorm_fwd_kernel, dim3(rows), dim3(kNormThreads), 0, s, dim,
+                      static_cast<const uint4*>(x), ldx / 8, static_cast<const uint4*>(w), eps,
+                      static_cast<uint4*>(out), ldo / 8);
+  return launch_pdl(mux_rmsnorm_bwd_kernel, dim3(rows), dim3(kNormThreads), 0, s, dim,
+                    static_cast<const uint4*>(a), lda / 8, static_cast<const uint4*>(x), ldx / 8,
+                    static_cast<const uint4*>(w), eps, static_cast<uint4*>(out), ldo / 8);
+}
+
+cudaError_t launch_swiglu_fwd(int rows, int dim, const void* g, long long ldg, const void* u, long long ldu, void* h,
+                              long long ldh, int num_sms, cudaStream_t s) {
+  const long long work = static_cast<long long>(rows) * (dim / 8);
+  if (work == 0) return cudaSuccess;
+  return launch_pdl(mux_swiglu_fwd_kernel, dim3(grid_for(work, 256, num_sms)), dim3(256), 0, s, rows, dim,
+                    static_cast<const uint4*>(g), ldg / 8, static_cast<const uint4*>(u), ldu / 8,
+                    static_cast<uint4*>(h), ldh / 8);
+}
+
+cudaError_t launch_swiglu_bwd(int rows, int dim, const void* dh, long long lddh, const void* g, long long ldg,
+                              const void* u, long long ldu, void* dg, long long lddg, void* du, long long lddu,
+                              int num_sms, cudaStream_t s) {
+  const long long work = static_cast<long long>(rows) * (dim / 8);
+  if (work == 0) return cudaSuccess;
+  return launch_pdl(mux_swiglu_bwd_kernel, dim3(grid_for(work, 256, num_sms)), dim3(256), 0, s, rows, dim,
+                    static_cast<const uint4*>(dh), lddh / 8, static_cast<const uint4*>(g), ldg / 8,
+                    static_cast<const uint4*>(u), ldu / 8, static_cast<uint4*>(dg), lddg / 8,
+                    static_cast<uint4*>(du), lddu / 8);
+}
+
+cudaError_t launch_rope(int rows, int heads, int d, void* x, long long ld, const int32_t* row_start, float base,
+                        bool inverse, int num_sms, cudaStream_t s) {
+  const long long work = static_cast<long long>(rows) * heads * (d / 16);
+  if (work == 0) return cudaSuccess;
+  return launch_pdl(mux_rope_kernel, dim3(grid_for(work, 256, num_sms)), dim3(256), 0, s, rows, heads, d,
+                    static_cast<uint4*>(x), ld / 8, row_start, log2f(base), inverse ? 1 : 0);
+}
+
+}  // namespace mux

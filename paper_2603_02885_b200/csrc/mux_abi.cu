@@ -27,6 +27,25 @@ cudaError_t launch_pack(int M, int S, const int32_t* task_seq_off, const int32_t
                         void* workspace, cudaStream_t stream);
 cudaError_t launch_pack_apply(int max_rows, int cols, int num_tokens, const int32_t* row_src,
                               const __nv_bfloat16* src, __nv_bfloat16* dst, int num_sms, cudaStream_t stream);
+cudaError_t launch_row_start(int num_seqs, const int32_t* seq_len, const int32_t* seq_row, int max_rows,
+                             int32_t* row_start, int num_sms, cudaStream_t s);
+cudaError_t launch_rmsnorm(bool bwd, int rows, int dim, const void* a, long long lda, const void* x, long long ldx,
+                           const void* w, float eps, void* out, long long ldo, cudaStream_t s);
+cudaError_t launch_swiglu_fwd(int rows, int dim, const void* g, long long ldg, const void* u, long long ldu, void* h,
+                              long long ldh, int num_sms, cudaStream_t s);
+cudaError_t launch_swiglu_bwd(int rows, int dim, const void* dh, long long lddh, const void* g, long long ldg,
+                              const void* u, long long ldu, void* dg, long long lddg, void* du, long long lddu,
+                              int num_sms, cudaStream_t s);
+cudaError_t launch_rope(int rows, int heads, int d, void* x, long long ld, const int32_t* row_start, float base,
+                        bool inverse, int num_sms, cudaStream_t s);
+cudaError_t launch_attn_fwd(int R, int H, int Hkv, const void* q, long long ldq, const void* k, long long ldk,
+                            const void* v, long long ldv, const int32_t* row_start, float scale, void* o,
+                            long long ldo, float* lse, cudaStream_t s);
+cudaError_t launch_attn_bwd(int R, int H, int Hkv, const void* dO, long long lddo, const void* q, long long ldq,
+                            const void* k, long long ldk, const void* v, long long ldv, const void* o,
+                            long long ldo, const float* lse, const int32_t* row_start, float scale, void* dq,
+                            long long lddq, void* dk, long long lddk, void* dv, long long lddv, float* Dws,
+                            cudaStream_t s);
 }  // namespace mux
 
 using namespace mux;
@@ -467,5 +486,150 @@ MUX_API int mux_debug_counters(unsigned long long* host_out, int n) {
   return 0;
 }
 #endif
+
+
+// ---------------------------------------------------------------- decoder-block ops (NEXT-3)
+static bool ld_ok(long long ld, int cols) { return ld >= cols && ld % 8 == 0; }
+
+mux_status mux_pack_row_start(int32_t num_seqs, const int32_t* seq_len, const int32_t* seq_row, int32_t max_rows,
+                              int32_t* row_start, cudaStream_t stream) {
+  if (num_seqs < 0 || max_rows < 0)
+    return fail(MUX_ERR_INVALID_ARGUMENT, "bad sizes num_seqs=%d max_rows=%d", num_seqs, max_rows);
+  if (max_rows == 0) return MUX_OK;
+  if (!row_start || (num_seqs > 0 && (!seq_len || !seq_row))) return fail(MUX_ERR_INVALID_ARGUMENT, "null pointer");
+  cudaError_t e = launch_row_start(num_seqs, seq_len, seq_row, max_rows, row_start, num_sms(), stream);
+  if (e != cudaSuccess) return cuda_fail(e, "mux_pack_row_start launch");
+  return MUX_OK;
+}
+
+static mux_status attn_check(int32_t rows, int32_t heads, int32_t kv_heads, int32_t head_dim) {
+  if (rows < 0 || heads < 1 || kv_heads < 1 || heads % kv_heads)
+    return fail(MUX_ERR_INVALID_ARGUMENT, "bad attention sizes rows=%d heads=%d kv_heads=%d", rows, heads, kv_heads);
+  if (head_dim != 128) return fail(MUX_ERR_UNSUPPORTED, "head_dim=%d (this build: 128)", head_dim);
+  return MUX_OK;
+}
+
+mux_status mux_attn_fwd(int32_t rows, int32_t heads, int32_t kv_heads, int32_t head_dim, const mux_bf16* q,
+                        int64_t ldq, const mux_bf16* k, int64_t ldk, const mux_bf16* v, int64_t ldv,
+                        const int32_t* row_start, float scale, mux_bf16* o, int64_t ldo, float* lse,
+                        cudaStream_t stream) {
+  mux_status st = attn_check(rows, heads, kv_heads, head_dim);
+  if (st != MUX_OK || rows == 0) return st;
+  if (!q || !k || !v || !row_start || !o || !lse) return fail(MUX_ERR_INVALID_ARGUMENT, "null pointer");
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o))
+    return fail(MUX_ERR_INVALID_ARGUMENT, "q/k/v/o not 16-byte aligned");
+  if (!ld_ok(ldq, heads * 128) || !ld_ok(ldo, heads * 128) || !ld_ok(ldk, kv_heads * 128) ||
+      !ld_ok(ldv, kv_heads * 128))
+    return fail(MUX_ERR_INVALID_ARGUMENT, "row strides must cover the heads and be multiples of 8");
+  if (!std::isfinite(scale)) return fail(MUX_ERR_INVALID_ARGUMENT, "scale not finite");
+  cudaError_t e = launch_attn_fwd(rows, heads, kv_heads, q, ldq, k, ldk, v, ldv, row_start, scale, o, ldo, lse,
+                                  stream);
+  if (e != cudaSuccess) return cuda_fail(e, "mux_attn_fwd launch");
+  return MUX_OK;
+}
+
+size_t mux_attn_workspace_size(int32_t rows, int32_t heads) {
+  if (rows < 0 || heads < 0) return 0;
+  return align256(sizeof(float) * static_cast<size_t>(rows) * heads);
+}
+
+mux_status mux_attn_bwd(int32_t rows, int32_t heads, int32_t kv_heads, int32_t head_dim, const mux_bf16* dO,
+                        int64_t lddo, const mux_bf16* q, int64_t ldq, const mux_bf16* k, int64_t ldk,
+                        const mux_bf16* v, int64_t ldv, const mux_bf16* o, int64_t ldo, const float* lse,
+                        const int32_t* row_start, float scale, mux_bf16* dq, int64_t lddq, mux_bf16* dk,
+                        int64_t lddk, mux_bf16* dv, int64_t lddv, void* workspace, size_t workspace_bytes,
+                        cudaStream_t stream) {
+  mux_status st = attn_check(rows, heads, kv_heads, head_dim);
+  if (st != MUX_OK || rows == 0) return st;
+  if (!dO || !q || !k || !v || !o || !lse || !row_start || !dq || !dk || !dv)
+    return fail(MUX_ERR_INVALID_ARGUMENT, "null pointer");
+  if (!aligned16(dO) || !aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o) || !aligned16(dq) ||
+      !aligned16(dk) || !aligned16(dv))
+    return fail(MUX_ERR_INVALID_ARGUMENT, "tensors must be 16-byte aligned");
+  const int qc = heads * 128, kc = kv_heads * 128;
+  if (!ld_ok(lddo, qc) || !ld_ok(ldq, qc) || !ld_ok(ldo, qc) || !ld_ok(lddq, qc) || !ld_ok(ldk, kc) ||
+      !ld_ok(ldv, kc) || !ld_ok(lddk, kc) || !ld_ok(lddv, kc))
+    return fail(MUX_ERR_INVALID_ARGUMENT, "row strides must cover the heads and be multiples of 8");
+  if (!std::isfinite(scale)) return fail(MUX_ERR_INVALID_ARGUMENT, "scale not finite");
+  const size_t need = mux_attn_workspace_size(rows, heads);
+  if (!workspace || workspace_bytes < need)
+    return fail(MUX_ERR_INSUFFICIENT_BUFFER, "attention workspace %zu < %zu bytes", workspace_bytes, need);
+  cudaError_t e = launch_attn_bwd(rows, heads, kv_heads, dO, lddo, q, ldq, k, ldk, v, ldv, o, ldo, lse, row_start,
+                                  scale, dq, lddq, dk, lddk, dv, lddv, static_cast<float*>(workspace), stream);
+  if (e != cudaSuccess) return cuda_fail(e, "mux_attn_bwd launch");
+  return MUX_OK;
+}
+
+mux_status mux_rope(int32_t rows, int32_t heads, int32_t head_dim, mux_bf16* x, int64_t ld,
+                    const int32_t* row_start, float base, int32_t inverse, cudaStream_t stream) {
+  if (rows < 0 || heads < 1 || head_dim < 16 || head_dim % 16)
+    return fail(MUX_ERR_INVALID_ARGUMENT, "bad rope sizes rows=%d heads=%d head_dim=%d", rows, heads, head_dim);
+  if (rows == 0) return MUX_OK;
+  if (!x || !row_start) return fail(MUX_ERR_INVALID_ARGUMENT, "null pointer");
+  if (!aligned16(x) || !ld_ok(ld, heads * head_dim)) return fail(MUX_ERR_INVALID_ARGUMENT, "x alignment/stride");
+  if (!(base > 1.f) || !std::isfinite(base)) return fail(MUX_ERR_INVALID_ARGUMENT, "rope base must be > 1");
+  cudaError_t e = launch_rope(rows, heads, head_dim, x, ld, row_start, base, inverse != 0, num_sms(), stream);
+  if (e != cudaSuccess) return cuda_fail(e, "mux_rope launch");
+  return MUX_OK;
+}
+
+static mux_status ew_check(int32_t rows, int32_t dim) {
+  if (rows < 0 || dim < 8 || dim % 8) return fail(MUX_ERR_INVALID_ARGUMENT, "bad sizes rows=%d dim=%d", rows, dim);
+  return MUX_OK;
+}
+
+mux_status mux_rmsnorm_fwd(int32_t rows, int32_t dim, const mux_bf16* x, int64_t ldx, const mux_bf16* w, float eps,
+                           mux_bf16* y, int64_t ldy, cudaStream_t stream) {
+  mux_status st = ew_check(rows, dim);
+  if (st != MUX_OK || rows == 0) return st;
+  if (!x || !w || !y) return fail(MUX_ERR_INVALID_ARGUMENT, "null pointer");
+  if (!aligned16(x) || !aligned16(w) || !aligned16(y) || !ld_ok(ldx, dim) || !ld_ok(ldy, dim))
+    return fail(MUX_ERR_INVALID_ARGUMENT, "alignment/stride");
+  if (!(eps >= 0.f) || !std::isfinite(eps)) return fail(MUX_ERR_INVALID_ARGUMENT, "eps must be finite and >= 0");
+  cudaError_t e = launch_rmsnorm(false, rows, dim, nullptr, 0, x, ldx, w, eps, y, ldy, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "mux_rmsnorm_fwd launch");
+  return MUX_OK;
+}
+
+mux_status mux_rmsnorm_bwd(int32_t rows, int32_t dim, const mux_bf16* dy, int64_t lddy, const mux_bf16* x,
+                           int64_t ldx, const mux_bf16* w, float eps, mux_bf16* dx, int64_t lddx,
+                           cudaStream_t stream) {
+  mux_status st = ew_check(rows, dim);
+  if (st != MUX_OK || rows == 0) return st;
+  if (!dy || !x || !w || !dx) return fail(MUX_ERR_INVALID_ARGUMENT, "null pointer");
+  if (!aligned16(dy) || !aligned16(x) || !aligned16(w) || !aligned16(dx) || !ld_ok(lddy, dim) || !ld_ok(ldx, dim) ||
+      !ld_ok(lddx, dim))
+    return fail(MUX_ERR_INVALID_ARGUMENT, "alignment/stride");
+  if (!(eps >= 0.f) || !std::isfinite(eps)) return fail(MUX_ERR_INVALID_ARGUMENT, "eps must be finite and >= 0");
+  cudaError_t e = launch_rmsnorm(true, rows, dim, dy, lddy, x, ldx, w, eps, dx, lddx, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "mux_rmsnorm_bwd launch");
+  return MUX_OK;
+}
+
+mux_status mux_swiglu_fwd(int32_t rows, int32_t dim, const mux_bf16* g, int64_t ldg, const mux_bf16* u, int64_t ldu,
+                          mux_bf16* h, int64_t ldh, cudaStream_t stream) {
+  mux_status st = ew_check(rows, dim);
+  if (st != MUX_OK || rows == 0) return st;
+  if (!g || !u || !h) return fail(MUX_ERR_INVALID_ARGUMENT, "null pointer");
+  if (!aligned16(g) || !aligned16(u) || !aligned16(h) || !ld_ok(ldg, dim) || !ld_ok(ldu, dim) || !ld_ok(ldh, dim))
+    return fail(MUX_ERR_INVALID_ARGUMENT, "alignment/stride");
+  cudaError_t e = launch_swiglu_fwd(rows, dim, g, ldg, u, ldu, h, ldh, num_sms(), stream);
+  if (e != cudaSuccess) return cuda_fail(e, "mux_swiglu_fwd launch");
+  return MUX_OK;
+}
+
+mux_status mux_swiglu_bwd(int32_t rows, int32_t dim, const mux_bf16* dh, int64_t lddh, const mux_bf16* g,
+                          int64_t ldg, const mux_bf16* u, int64_t ldu, mux_bf16* dg, int64_t lddg, mux_bf16* du,
+                          int64_t lddu, cudaStream_t stream) {
+  mux_status st = ew_check(rows, dim);
+  if (st != MUX_OK || rows == 0) return st;
+  if (!dh || !g || !u || !dg || !du) return fail(MUX_ERR_INVALID_ARGUMENT, "null pointer");
+  if (!aligned16(dh) || !aligned16(g) || !aligned16(u) || !aligned16(dg) || !aligned16(du) || !ld_ok(lddh, dim) ||
+      !ld_ok(ldg, dim) || !ld_ok(ldu, dim) || !ld_ok(lddg, dim) || !ld_ok(lddu, dim))
+    return fail(MUX_ERR_INVALID_ARGUMENT, "alignment/stride");
+  cudaError_t e = launch_swiglu_bwd(rows, dim, dh, lddh, g, ldg, u, ldu, dg, lddg, du, lddu, num_sms(), stream);
+  if (e != cudaSuccess) return cuda_fail(e, "mux_swiglu_bwd launch");
+  return MUX_OK;
+}
 
 }  // extern "C"

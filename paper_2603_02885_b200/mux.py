@@ -26,7 +26,8 @@ MAX_ADAPTERS = 64
 
 EXPORTS = ("mux_last_error", "mux_version", "mux_pack_bound_rows", "mux_pack_workspace_size",
            "mux_pack_chunks", "mux_pack_apply", "mux_linear_workspace_size", "mux_linear_fwd",
-           "mux_linear_bwd")
+           "mux_linear_bwd", "mux_pack_row_start", "mux_attn_fwd", "mux_attn_workspace_size", "mux_attn_bwd",
+           "mux_rope", "mux_rmsnorm_fwd", "mux_rmsnorm_bwd", "mux_swiglu_fwd", "mux_swiglu_bwd")
 
 
 class MuxError(RuntimeError):
@@ -79,6 +80,26 @@ def lib():
         L.mux_linear_fwd.argtypes = [I32, P, P, I32, P, I32, I32, I32, I32, P, P, P, P, P, SZ, P]
         L.mux_linear_bwd.restype = ctypes.c_int
         L.mux_linear_bwd.argtypes = [I32, P, P, I32, P, I32, I32, I32, I32, P, P, P, P, P, P, SZ, P]
+        F = ctypes.c_float
+        L.mux_pack_row_start.restype = ctypes.c_int
+        L.mux_pack_row_start.argtypes = [I32, P, P, I32, P, P]
+        L.mux_attn_fwd.restype = ctypes.c_int
+        L.mux_attn_fwd.argtypes = [I32, I32, I32, I32, P, I64, P, I64, P, I64, P, F, P, I64, P, P]
+        L.mux_attn_workspace_size.restype = SZ
+        L.mux_attn_workspace_size.argtypes = [I32, I32]
+        L.mux_attn_bwd.restype = ctypes.c_int
+        L.mux_attn_bwd.argtypes = [I32, I32, I32, I32, P, I64, P, I64, P, I64, P, I64, P, I64, P, P, F,
+                                   P, I64, P, I64, P, I64, P, SZ, P]
+        L.mux_rope.restype = ctypes.c_int
+        L.mux_rope.argtypes = [I32, I32, I32, P, I64, P, F, I32, P]
+        L.mux_rmsnorm_fwd.restype = ctypes.c_int
+        L.mux_rmsnorm_fwd.argtypes = [I32, I32, P, I64, P, F, P, I64, P]
+        L.mux_rmsnorm_bwd.restype = ctypes.c_int
+        L.mux_rmsnorm_bwd.argtypes = [I32, I32, P, I64, P, I64, P, F, P, I64, P]
+        L.mux_swiglu_fwd.restype = ctypes.c_int
+        L.mux_swiglu_fwd.argtypes = [I32, I32, P, I64, P, I64, P, I64, P]
+        L.mux_swiglu_bwd.restype = ctypes.c_int
+        L.mux_swiglu_bwd.argtypes = [I32, I32, P, I64, P, I64, P, I64, P, I64, P, I64, P]
         _lib = L
     return _lib
 
@@ -260,3 +281,98 @@ def linear_bwd(seg_off: torch.Tensor, seg_task: Sequence[int], adapters: Sequenc
                                 _ptr(dY), _ptr(X), _ptr(W), _ptr(Hs), _ptr(dX), _ptr(workspace),
                                 workspace.numel(), _stream(stream)))
     return dX
+
+
+# ---------------------------------------------------------------- decoder-block ops (NEXT-3)
+def _ld(t: torch.Tensor) -> int:
+    """row stride (elements) of a 2D bf16 view whose rows are contiguous."""
+    assert t.dim() == 2 and t.stride(1) == 1, "rows must be contiguous"
+    return int(t.stride(0))
+
+
+def row_start(seq_len: torch.Tensor, seq_row: torch.Tensor, max_rows: int, out: torch.Tensor = None,
+              stream=None) -> torch.Tensor:
+    """mux_pack_row_start: first packed row of each row's sequence (-1 = pad)."""
+    if out is None:
+        out = torch.empty(max_rows, dtype=torch.int32, device=seq_len.device)
+    _check(lib().mux_pack_row_start(seq_len.numel(), _ptr(seq_len), _ptr(seq_row), max_rows, _ptr(out),
+                                    _stream(stream)))
+    return out
+
+
+def attn_fwd(q, k, v, row_start_, heads: int, kv_heads: int, scale: float, o=None, lse=None, stream=None):
+    """mux_attn_fwd on 2D views q [R, H*128], k/v [R, Hkv*128] -> (o, lse)."""
+    R = q.shape[0]
+    if o is None:
+        o = torch.empty(R, heads * 128, dtype=torch.bfloat16, device=q.device)
+    if lse is None:
+        lse = torch.empty(R, heads, dtype=torch.float32, device=q.device)
+    _check(lib().mux_attn_fwd(R, heads, kv_heads, 128, _ptr(q), _ld(q), _ptr(k), _ld(k), _ptr(v), _ld(v),
+                              _ptr(row_start_), scale, _ptr(o), _ld(o), _ptr(lse), _stream(stream)))
+    return o, lse
+
+
+def attn_workspace_size(rows: int, heads: int) -> int:
+    return int(lib().mux_attn_workspace_size(rows, heads))
+
+
+def attn_bwd(dO, q, k, v, o, lse, row_start_, heads: int, kv_heads: int, scale: float, dq=None, dk=None, dv=None,
+             workspace=None, stream=None):
+    """mux_attn_bwd -> (dq, dk, dv)."""
+    R = q.shape[0]
+    dev = q.device
+    if dq is None:
+        dq = torch.empty(R, heads * 128, dtype=torch.bfloat16, device=dev)
+    if dk is None:
+        dk = torch.empty(R, kv_heads * 128, dtype=torch.bfloat16, device=dev)
+    if dv is None:
+        dv = torch.empty(R, kv_heads * 128, dtype=torch.bfloat16, device=dev)
+    if workspace is None:
+        workspace = torch.empty(attn_workspace_size(R, heads), dtype=torch.uint8, device=dev)
+    _check(lib().mux_attn_bwd(R, heads, kv_heads, 128, _ptr(dO), _ld(dO), _ptr(q), _ld(q), _ptr(k), _ld(k),
+                              _ptr(v), _ld(v), _ptr(o), _ld(o), _ptr(lse), _ptr(row_start_), scale,
+                              _ptr(dq), _ld(dq), _ptr(dk), _ld(dk), _ptr(dv), _ld(dv), _ptr(workspace),
+                              workspace.numel(), _stream(stream)))
+    return dq, dk, dv
+
+
+def rope_(x, row_start_, heads: int, head_dim: int = 128, base: float = 10000.0, inverse: bool = False,
+          stream=None):
+    """mux_rope, in place on x [R, heads*head_dim] (a 2D view, rows contiguous)."""
+    _check(lib().mux_rope(x.shape[0], heads, head_dim, _ptr(x), _ld(x), _ptr(row_start_), base, int(inverse),
+                          _stream(stream)))
+    return x
+
+
+def rmsnorm_fwd(x, w, eps: float, y=None, stream=None):
+    if y is None:
+        y = torch.empty(x.shape[0], x.shape[1], dtype=torch.bfloat16, device=x.device)
+    _check(lib().mux_rmsnorm_fwd(x.shape[0], x.shape[1], _ptr(x), _ld(x), _ptr(w), eps, _ptr(y), _ld(y),
+                                 _stream(stream)))
+    return y
+
+
+def rmsnorm_bwd(dy, x, w, eps: float, dx=None, stream=None):
+    if dx is None:
+        dx = torch.empty(x.shape[0], x.shape[1], dtype=torch.bfloat16, device=x.device)
+    _check(lib().mux_rmsnorm_bwd(x.shape[0], x.shape[1], _ptr(dy), _ld(dy), _ptr(x), _ld(x), _ptr(w), eps,
+                                 _ptr(dx), _ld(dx), _stream(stream)))
+    return dx
+
+
+def swiglu_fwd(g, u, h=None, stream=None):
+    if h is None:
+        h = torch.empty(g.shape[0], g.shape[1], dtype=torch.bfloat16, device=g.device)
+    _check(lib().mux_swiglu_fwd(g.shape[0], g.shape[1], _ptr(g), _ld(g), _ptr(u), _ld(u), _ptr(h), _ld(h),
+                                _stream(stream)))
+    return h
+
+
+def swiglu_bwd(dh, g, u, dg=None, du=None, stream=None):
+    if dg is None:
+        dg = torch.empty(g.shape[0], g.shape[1], dtype=torch.bfloat16, device=g.device)
+    if du is None:
+        du = torch.empty(g.shape[0], g.shape[1], dtype=torch.bfloat16, device=g.device)
+    _check(lib().mux_swiglu_bwd(g.shape[0], g.shape[1], _ptr(dh), _ld(dh), _ptr(g), _ld(g), _ptr(u), _ld(u),
+                                _ptr(dg), _ld(dg), _ptr(du), _ld(du), _stream(stream)))
+    return dg, du

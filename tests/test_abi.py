@@ -118,3 +118,54 @@ def test_missing_library_fails_loudly(monkeypatch, tmp_path):
     with pytest.raises(RuntimeError, match="libmux.so not found"):
         m.lib()
     importlib.reload(m)
+
+
+# ---------------------------------------------------------------- decoder-block ops: host validation
+A16 = 0x10000  # a 16-byte aligned fake device address (never dereferenced: validation fails first)
+
+
+def _attn_fwd(mux, R=128, H=4, Hkv=4, d=128, ldq=512, ldk=512, ldv=512, ldo=512, q=A16, scale=0.1):
+    L = mux.lib()
+    return L.mux_attn_fwd(R, H, Hkv, d, q, ldq, A16, ldk, A16, ldv, A16, scale, A16, ldo, A16, None), \
+        L.mux_last_error().decode()
+
+
+@pytest.mark.parametrize("kw,status,frag", [
+    (dict(d=64), 2, "head_dim"),
+    (dict(H=6, Hkv=4), 1, "heads"),
+    (dict(ldq=256), 1, "strides"),
+    (dict(ldk=508), 1, "strides"),
+    (dict(q=A16 + 8), 1, "aligned"),
+    (dict(scale=float("inf")), 1, "scale"),
+])
+def test_attn_fwd_rejects(mux, kw, status, frag):
+    st, msg = _attn_fwd(mux, **kw)
+    assert st == status and frag in msg, (st, msg)
+
+
+def test_attn_fwd_zero_rows_is_noop(mux):
+    st, _ = _attn_fwd(mux, R=0)
+    assert st == 0
+
+
+def test_attn_bwd_workspace_checked(mux):
+    L = mux.lib()
+    need = mux.attn_workspace_size(128, 4)
+    assert need >= 128 * 4 * 4
+    st = L.mux_attn_bwd(128, 4, 2, 128, A16, 512, A16, 512, A16, 256, A16, 256, A16, 512, A16, A16, 0.1,
+                        A16, 512, A16, 256, A16, 256, A16, need - 1, None)
+    assert st == 3 and "workspace" in L.mux_last_error().decode()
+
+
+def test_elementwise_ops_reject(mux):
+    L = mux.lib()
+    assert L.mux_rope(16, 2, 10, A16, 64, A16, 10000.0, 0, None) == 1            # head_dim % 16
+    assert L.mux_rope(16, 2, 64, A16, 64, A16, 10000.0, 0, None) == 1            # ld < heads * head_dim
+    assert L.mux_rope(16, 2, 64, A16, 128, A16, 1.0, 0, None) == 1               # base <= 1
+    assert L.mux_rmsnorm_fwd(4, 12, A16, 16, A16, 1e-5, A16, 16, None) == 1      # dim % 8
+    assert L.mux_rmsnorm_fwd(4, 16, A16, 16, A16, -1.0, A16, 16, None) == 1      # eps < 0
+    assert L.mux_rmsnorm_bwd(4, 16, A16, 16, A16, 8, A16, 1e-5, A16, 16, None) == 1  # ldx < dim
+    assert L.mux_swiglu_fwd(4, 16, A16 + 2, 16, A16, 16, A16, 16, None) == 1    # misaligned
+    assert L.mux_swiglu_bwd(4, 16, A16, 16, A16, 16, A16, 16, A16, 16, A16, 12, None) == 1
+    assert L.mux_pack_row_start(-1, A16, A16, 16, A16, None) == 1
+    assert L.mux_swiglu_fwd(0, 16, A16, 16, A16, 16, A16, 16, None) == 0        # empty: no-op
