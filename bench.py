@@ -598,6 +598,101 @@ def tp_arm(args):
     dist.destroy_process_group()
 
 
+def block_arm(args):
+    """--mode block: one LLaMA-7B decoder block (config 4: 16 tasks, ranks
+    8/16/32/64, LoRA on all seven linears) fwd+bwd per step, on one GPU:
+    pack -> row map -> Dispatch(X) -> block forward (RMSNorm, q/k/v, RoPE,
+    causal attention inside packed sequences, o + residual, RMSNorm,
+    gate/up, SwiGLU, down + residual) -> Dispatch(dY) -> block backward
+    (paper_2603_02885_b200/block.py; every step a libmux kernel).
+    Algorithmic FLOPs: each linear 4KN + 6 r_t (K+N) per valid token of task
+    t; attention 12 d H per causal (query, key) pair (fwd 2 + bwd 4 matmuls)."""
+    import torch
+    from paper_2603_02885_b200 import mux
+    from paper_2603_02885_b200.block import LINEARS, BlockShape, DecoderBlock
+
+    cfg = "4" if args.config == "2" else args.config
+    w = Workload(cfg)
+    wl = w.wl
+    assert [L.name for L in wl.linears] == list(LINEARS), "block mode needs a 7-linear decoder config"
+    hidden, ffn = wl.linears[0].K, wl.linears[4].N
+    heads = wl.linears[0].N // 128
+    kv_heads = wl.linears[1].N // 128
+    shape = BlockShape(hidden=hidden, ffn=ffn, heads=heads, kv_heads=kv_heads)
+    h = w.host_tensors()
+    dev = "cuda"
+    W = {n: _bits_to_dev(h[f"W{li}"], torch) for li, n in enumerate(LINEARS)}
+    W["norm1"] = _bits_to_dev(synth.norm_weight(wl, 0), torch)
+    W["norm2"] = _bits_to_dev(synth.norm_weight(wl, 1), torch)
+    ads = {}
+    for li, n in enumerate(LINEARS):
+        L = wl.linears[li]
+        ads[n] = []
+        for t in range(w.M):
+            B = mux.make_B_storage(L.N, wl.ranks[t])
+            B.copy_(_bits_to_dev(h[f"B{li}_{t}"], torch))
+            ads[n].append(mux.Adapter(_bits_to_dev(h[f"A{li}_{t}"], torch), B, wl.ranks[t], wl.scales[t]))
+    r_cap = 16 * -(-max(wl.ranks) // 16)
+    blk = DecoderBlock(shape, W, ads, r_cap)
+    i32 = dict(dtype=torch.int32, device=dev)
+    tso, sl = torch.tensor(w.off, **i32), torch.tensor(w.lens, **i32)
+    cap = torch.tensor(w.cap, **i32) if w.cap else None
+    max_rows = int(mux.pack_bound_rows(w.T, w.S, 64))
+    pk = mux.alloc_pack_outputs(w.M, w.S, max_rows, max_rows // 64)
+    rs = torch.empty(max_rows, **i32)
+    Xtok = _bits_to_dev(synth.token_input(wl, 0, "X", hidden), torch)
+    dYtok = _bits_to_dev(synth.token_input(wl, 6, "dY", hidden), torch)
+    X = torch.empty(max_rows, hidden, dtype=torch.bfloat16, device=dev)
+    dY = torch.empty(max_rows, hidden, dtype=torch.bfloat16, device=dev)
+    st = list(range(w.M))
+
+    def step():
+        mux.pack_chunks(tso, sl, cap, 0, 64, max_rows=max_rows, max_chunks=max_rows // 64, out=pk)
+        mux.row_start(sl, pk["seq_row"], max_rows, out=rs)
+        mux.pack_apply(pk["row_src"], Xtok, max_rows, out=X)
+        blk.forward(X, pk["seg_off"], st, rs)
+        mux.pack_apply(pk["row_src"], dYtok, max_rows, out=dY)
+        return blk.backward(dY)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    info = mux.read_info(pk["info"])
+    assert info["overflow"] == 0 and info["valid_rows"] == w.T, info
+    clk = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
+    clk.start()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    s0.record()
+    for _ in range(args.steps):
+        step()
+    s1.record()
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    ms = s0.elapsed_time(s1) / args.steps
+    # algorithmic FLOPs
+    lin = 0
+    for t in range(w.M):
+        Tt = int(wl.task_lens[t].sum())
+        lin += Tt * sum(flops_per_token(L.K, L.N, wl.ranks[t]) for L in wl.linears)
+    pairs = sum(int(L) * (int(L) + 1) // 2 for x in wl.task_lens for L in x)
+    attn = 12 * 128 * heads * pairs
+    pk_ = peaks()
+    tf = (lin + attn) / (ms * 1e-3) / 1e12
+    print(json.dumps({"metric": METRIC, "value": w.T / (ms * 1e-3), "unit": UNIT, "n_gpus": 1,
+                      "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+                      "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic", "mode": "block",
+                      "config": {"workload": f"config {cfg}: " + wl.description + " - one full decoder block "
+                                 "(RMSNorm, q/k/v/o, RoPE, causal attention, SwiGLU MLP) fwd+bwd",
+                                 "valid_tokens": w.T, "packed_rows": info["total_rows"], "tasks": w.M,
+                                 "hidden": hidden, "ffn": ffn, "heads": heads, "kv_heads": kv_heads,
+                                 "l2": "inputs larger than L2 (weights 405 MB)"},
+                      "tflops_algorithmic": tf, "frac_of_sustained_peak": tf / pk_["bf16_tflops_sustained"],
+                      "flops_split": {"linears": lin, "attention": attn},
+                      "gpu_launches": args.steps * (5 + DecoderBlock.LAUNCHES_FWD + DecoderBlock.LAUNCHES_BWD),
+                      "clocks": clocks}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -609,7 +704,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-rows", type=int, default=4, help="rows per task per reference-arm step")
-    ap.add_argument("--mode", default="replicas", choices=["replicas", "tp"],
+    ap.add_argument("--mode", default="replicas", choices=["replicas", "tp", "block"],
                     help="N>1: task-sharded replicas (default, weak scaling) or tensor parallel (strong)")
     ap.add_argument("--htasks", type=int, default=1, help="--mode tp: hTasks interleaved by Alg. 1 (NEXT-1)")
     ap.add_argument("--comm-ctas", type=int, default=0, help="--mode tp: NCCL_MAX_CTAS for the overlapped collectives")
@@ -620,6 +715,8 @@ def main():
         reference_arm(args)
     elif args.mode == "tp":
         tp_arm(args)
+    elif args.mode == "block":
+        block_arm(args)
     else:
         main_arm(args)
 

@@ -25,7 +25,7 @@
  *                       (Fig. alignment), masked per sequence
  *
  *   mux_rope            rotary position embedding at in-sequence positions
- *   mux_rmsnorm_fwd/bwd, mux_swiglu_fwd/bwd
+ *   mux_rmsnorm_fwd/bwd, mux_swiglu_fwd/bwd, mux_add (residual)
  *
  * Conventions (all functions)
  *   - Pointers are DEVICE pointers unless marked [host].  The caller owns
@@ -271,6 +271,10 @@ MUX_API mux_status mux_swiglu_fwd(int32_t rows, int32_t dim, const mux_bf16* g, 
 MUX_API mux_status mux_swiglu_bwd(int32_t rows, int32_t dim, const mux_bf16* dh, int64_t lddh, const mux_bf16* g,
                                   int64_t ldg, const mux_bf16* u, int64_t ldu, mux_bf16* dg, int64_t lddg,
                                   mux_bf16* du, int64_t lddu, cudaStream_t stream);
+
+/* Residual add y = a + b (fp32 add, bf16 out); y may alias a or b.  [rows, dim], dim % 8 == 0. */
+MUX_API mux_status mux_add(int32_t rows, int32_t dim, const mux_bf16* a, int64_t lda, const mux_bf16* b,
+                           int64_t ldb, mux_bf16* y, int64_t ldy, cudaStream_t stream);
 
 #ifdef __cplusplus
 }

@@ -1,0 +1,143 @@
+"""A LLaMA decoder block whose seven linears (q, k, v, o, gate, up, down) are
+multiplexed LoRA linears: one hTask's
+packed rows go through the whole block, forward and backward, with every
+step a libmux kernel (thin glue; no arithmetic here):
+
+  h1 = RMSNorm(x);  q, k, v = mux_linear(h1);  RoPE(q, k)
+  a  = causal attention inside packed sequences (chunk KV reuse)
+  x2 = x + mux_linear_o(a);  h2 = RMSNorm(x2)
+  y  = x2 + mux_linear_down(SwiGLU(mux_linear_gate(h2), mux_linear_up(h2)))
+
+The backbone (linears, norms) is frozen: backward returns dx and
+writes every adapter's dA/dB.  Attention, RMSNorm and SwiGLU are not BaseOps
+("Attention is excluded"): they carry no adapters.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Dict, List, Sequence
+
+import torch
+
+from . import mux
+
+LINEARS = ("q", "k", "v", "o", "gate", "up", "down")
+
+
+@dataclass
+class BlockShape:
+    hidden: int = 4096
+    ffn: int = 11008
+    heads: int = 32
+    kv_heads: int = 32
+    head_dim: int = 128
+    eps: float = 1e-5
+    rope_base: float = 10000.0
+
+    def linear_dims(self) -> Dict[str, tuple]:
+        """(K, N) of each linear."""
+        H, F, kv = self.hidden, self.ffn, self.kv_heads * self.head_dim
+        return {"q": (H, self.heads * self.head_dim), "k": (H, kv), "v": (H, kv),
+                "o": (self.heads * self.head_dim, H), "gate": (H, F), "up": (H, F), "down": (F, H)}
+
+
+class DecoderBlock:
+    """weights: {"q".."down": W [N, K] bf16, "norm1", "norm2": [hidden] bf16};
+    adapters: {"q".."down": [mux.Adapter per task]} (dA/dB allocated here)."""
+
+    def __init__(self, shape: BlockShape, weights: Dict[str, torch.Tensor], adapters: Dict[str, List[mux.Adapter]],
+                 r_cap: int):
+        self.s, self.w, self.ads, self.r_cap = shape, weights, adapters, r_cap
+        dims = shape.linear_dims()
+        for name in LINEARS:
+            K, N = dims[name]
+            assert tuple(weights[name].shape) == (N, K), (name, weights[name].shape)
+            for a in adapters[name]:
+                if a.rank and a.dA is None:
+                    a.dA = torch.empty(a.rank, K, dtype=torch.float32, device=weights[name].device)
+                if a.rank and a.dB is None:
+                    a.dB = torch.empty(N, a.rank, dtype=torch.float32, device=weights[name].device)
+        self._buf: Dict[str, torch.Tensor] = {}
+        self._rows = -1
+
+    def _b(self, name, cols, dtype=torch.bfloat16):
+        t = self._buf.get(name)
+        if t is None or t.shape[0] != self._rows or t.shape[1] != cols or t.dtype != dtype:
+            t = torch.empty(self._rows, cols, dtype=dtype, device=self.w["q"].device)
+            self._buf[name] = t
+        return t
+
+    def _ws(self, name, n_segs):
+        K, N = self.s.linear_dims()[name]
+        need = mux.linear_workspace_size(n_segs, self._rows, K, N, self.r_cap)
+        t = self._buf.get("ws_" + name)
+        if t is None or t.numel() < need:
+            t = torch.zeros(need, dtype=torch.uint8, device=self.w["q"].device)
+            self._buf["ws_" + name] = t
+        return t
+
+    def _lin_fwd(self, name, X):
+        N = self.w[name].shape[0]
+        Y, Hs = self._b(name + ".y", N), self._b(name + ".hs", self.r_cap)
+        mux.linear_fwd(self.seg_off, self.seg_task, self.ads[name], X, self.w[name], self.r_cap, Y=Y, Hs=Hs,
+                       workspace=self._ws(name, len(self.seg_task)))
+        return Y
+
+    def _lin_bwd(self, name, dY, X, out):
+        mux.linear_bwd(self.seg_off, self.seg_task, self.ads[name], dY, X, self.w[name],
+                       self._buf[name + ".hs"], self.r_cap, dX=out, workspace=self._ws(name, len(self.seg_task)))
+        return out
+
+    def forward(self, x: torch.Tensor, seg_off: torch.Tensor, seg_task: Sequence[int], row_start: torch.Tensor):
+        s = self.s
+        self._rows = x.shape[0]
+        self.seg_off, self.seg_task, self.row_start = seg_off, list(seg_task), row_start
+        self.x = x
+        h1 = mux.rmsnorm_fwd(x, self.w["norm1"], s.eps, y=self._b("h1", s.hidden))
+        q, k, v = self._lin_fwd("q", h1), self._lin_fwd("k", h1), self._lin_fwd("v", h1)
+        mux.rope_(q, row_start, s.heads, s.head_dim, s.rope_base)
+        mux.rope_(k, row_start, s.kv_heads, s.head_dim, s.rope_base)
+        a, lse = mux.attn_fwd(q, k, v, row_start, s.heads, s.kv_heads, s.head_dim ** -0.5,
+                              o=self._b("a", s.heads * s.head_dim), lse=self._b("lse", s.heads, torch.float32))
+        o = self._lin_fwd("o", a)
+        x2 = mux.add(x, o, y=self._b("x2", s.hidden))
+        h2 = mux.rmsnorm_fwd(x2, self.w["norm2"], s.eps, y=self._b("h2", s.hidden))
+        g, u = self._lin_fwd("gate", h2), self._lin_fwd("up", h2)
+        m = mux.swiglu_fwd(g, u, h=self._b("m", s.ffn))
+        d = self._lin_fwd("down", m)
+        self.saved = dict(h1=h1, q=q, k=k, v=v, a=a, lse=lse, x2=x2, h2=h2, g=g, u=u, m=m)
+        return mux.add(x2, d, y=self._b("y", s.hidden))
+
+    def backward(self, dy: torch.Tensor) -> torch.Tensor:
+        s, sv = self.s, self.saved
+        dm = self._lin_bwd("down", dy, sv["m"], self._b("dm", s.ffn))
+        dg, du = mux.swiglu_bwd(dm, sv["g"], sv["u"], dg=self._b("dg", s.ffn), du=self._b("du", s.ffn))
+        dh2 = self._lin_bwd("gate", dg, sv["h2"], self._b("dh2", s.hidden))
+        dh2u = self._lin_bwd("up", du, sv["h2"], self._b("dh2u", s.hidden))
+        mux.add(dh2, dh2u, y=dh2)
+        dx2 = mux.rmsnorm_bwd(dh2, sv["x2"], self.w["norm2"], s.eps, dx=self._b("dx2", s.hidden))
+        mux.add(dx2, dy, y=dx2)                                   # residual
+        da = self._lin_bwd("o", dx2, sv["a"], self._b("da", s.heads * s.head_dim))
+        need = mux.attn_workspace_size(self._rows, s.heads)
+        ws = self._buf.get("attn_ws")
+        if ws is None or ws.numel() < need:
+            ws = self._buf["attn_ws"] = torch.empty(need, dtype=torch.uint8, device=dy.device)
+        dq, dk, dv = mux.attn_bwd(da, sv["q"], sv["k"], sv["v"], sv["a"], sv["lse"], self.row_start, s.heads,
+                                  s.kv_heads, s.head_dim ** -0.5, dq=self._b("dq", s.heads * s.head_dim),
+                                  dk=self._b("dk", s.kv_heads * s.head_dim),
+                                  dv=self._b("dv", s.kv_heads * s.head_dim), workspace=ws)
+        mux.rope_(dq, self.row_start, s.heads, s.head_dim, s.rope_base, inverse=True)
+        mux.rope_(dk, self.row_start, s.kv_heads, s.head_dim, s.rope_base, inverse=True)
+        dh1 = self._lin_bwd("q", dq, sv["h1"], self._b("dh1", s.hidden))
+        t = self._lin_bwd("k", dk, sv["h1"], self._b("dh1k", s.hidden))
+        mux.add(dh1, t, y=dh1)
+        t = self._lin_bwd("v", dv, sv["h1"], t)
+        mux.add(dh1, t, y=dh1)
+        dx = mux.rmsnorm_bwd(dh1, self.x, self.w["norm1"], s.eps, dx=self._b("dx", s.hidden))
+        return mux.add(dx, dx2, y=dx)
+
+    # kernel launches: forward = 2 norms + 7 linears + 2 RoPE + attention + swiglu + 2 adds = 15;
+    # backward = 7 linears x (dX GEMM + adapter-gradient kernel) + swiglu + 2 norms + attention
+    # (D, dK/dV, dQ) + 2 RoPE + 5 adds = 27
+    LAUNCHES_FWD = 15
+    LAUNCHES_BWD = 27

@@ -184,6 +184,26 @@ __global__ void __launch_bounds__(256) mux_swiglu_bwd_kernel(int rows, int dim, 
   }
 }
 
+// ------------------------------------------------------------------ residual add
+__global__ void __launch_bounds__(256) mux_add_kernel(int rows, int dim, const uint4* a, long long lda,
+                                                     const uint4* b, long long ldb, uint4* y, long long ldy) {
+  griddep_wait();
+  griddep_launch_dependents();
+  const int nc = dim / 8;
+  const long long total = static_cast<long long>(rows) * nc;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long r = i / nc;
+    const int c = static_cast<int>(i - r * nc);
+    float x[8], z[8];
+    bf16x8_to_f32(a[r * lda + c], x);
+    bf16x8_to_f32(b[r * ldb + c], z);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] += z[k];
+    y[r * ldy + c] = f32_to_bf16x8(x);
+  }
+}
+
 // ------------------------------------------------------------------ RoPE
 // In place on x [rows, heads * d] (row stride ld): pairs (i, i + d/2) of each
 // head rotated by theta_i = pos * base^(-2i/d), pos = r - row_start[r]
@@ -271,6 +291,15 @@ cudaError_t launch_swiglu_bwd(int rows, int dim, const void* dh, long long lddh,
                     static_cast<const uint4*>(dh), lddh / 8, static_cast<const uint4*>(g), ldg / 8,
                     static_cast<const uint4*>(u), ldu / 8, static_cast<uint4*>(dg), lddg / 8,
                     static_cast<uint4*>(du), lddu / 8);
+}
+
+cudaError_t launch_add(int rows, int dim, const void* a, long long lda, const void* b, long long ldb, void* y,
+                       long long ldy, int num_sms, cudaStream_t s) {
+  const long long work = static_cast<long long>(rows) * (dim / 8);
+  if (work == 0) return cudaSuccess;
+  return launch_pdl(mux_add_kernel, dim3(grid_for(work, 256, num_sms)), dim3(256), 0, s, rows, dim,
+                    static_cast<const uint4*>(a), lda / 8, static_cast<const uint4*>(b), ldb / 8,
+                    static_cast<uint4*>(y), ldy / 8);
 }
 
 cudaError_t launch_rope(int rows, int heads, int d, void* x, long long ld, const int32_t* row_start, float base,

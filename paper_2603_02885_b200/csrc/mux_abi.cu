@@ -38,6 +38,8 @@ cudaError_t launch_swiglu_bwd(int rows, int dim, const void* dh, long long lddh,
                               int num_sms, cudaStream_t s);
 cudaError_t launch_rope(int rows, int heads, int d, void* x, long long ld, const int32_t* row_start, float base,
                         bool inverse, int num_sms, cudaStream_t s);
+cudaError_t launch_add(int rows, int dim, const void* a, long long lda, const void* b, long long ldb, void* y,
+                       long long ldy, int num_sms, cudaStream_t s);
 cudaError_t launch_attn_fwd(int R, int H, int Hkv, const void* q, long long ldq, const void* k, long long ldk,
                             const void* v, long long ldv, const int32_t* row_start, float scale, void* o,
                             long long ldo, float* lse, cudaStream_t s);
@@ -629,6 +631,18 @@ mux_status mux_swiglu_bwd(int32_t rows, int32_t dim, const mux_bf16* dh, int64_t
     return fail(MUX_ERR_INVALID_ARGUMENT, "alignment/stride");
   cudaError_t e = launch_swiglu_bwd(rows, dim, dh, lddh, g, ldg, u, ldu, dg, lddg, du, lddu, num_sms(), stream);
   if (e != cudaSuccess) return cuda_fail(e, "mux_swiglu_bwd launch");
+  return MUX_OK;
+}
+
+mux_status mux_add(int32_t rows, int32_t dim, const mux_bf16* a, int64_t lda, const mux_bf16* b, int64_t ldb,
+                   mux_bf16* y, int64_t ldy, cudaStream_t stream) {
+  mux_status st = ew_check(rows, dim);
+  if (st != MUX_OK || rows == 0) return st;
+  if (!a || !b || !y) return fail(MUX_ERR_INVALID_ARGUMENT, "null pointer");
+  if (!aligned16(a) || !aligned16(b) || !aligned16(y) || !ld_ok(lda, dim) || !ld_ok(ldb, dim) || !ld_ok(ldy, dim))
+    return fail(MUX_ERR_INVALID_ARGUMENT, "alignment/stride");
+  cudaError_t e = launch_add(rows, dim, a, lda, b, ldb, y, ldy, num_sms(), stream);
+  if (e != cudaSuccess) return cuda_fail(e, "mux_add launch");
   return MUX_OK;
 }
 

@@ -27,7 +27,7 @@ MAX_ADAPTERS = 64
 EXPORTS = ("mux_last_error", "mux_version", "mux_pack_bound_rows", "mux_pack_workspace_size",
            "mux_pack_chunks", "mux_pack_apply", "mux_linear_workspace_size", "mux_linear_fwd",
            "mux_linear_bwd", "mux_pack_row_start", "mux_attn_fwd", "mux_attn_workspace_size", "mux_attn_bwd",
-           "mux_rope", "mux_rmsnorm_fwd", "mux_rmsnorm_bwd", "mux_swiglu_fwd", "mux_swiglu_bwd")
+           "mux_rope", "mux_rmsnorm_fwd", "mux_rmsnorm_bwd", "mux_swiglu_fwd", "mux_swiglu_bwd", "mux_add")
 
 
 class MuxError(RuntimeError):
@@ -100,6 +100,8 @@ def lib():
         L.mux_swiglu_fwd.argtypes = [I32, I32, P, I64, P, I64, P, I64, P]
         L.mux_swiglu_bwd.restype = ctypes.c_int
         L.mux_swiglu_bwd.argtypes = [I32, I32, P, I64, P, I64, P, I64, P, I64, P, I64, P]
+        L.mux_add.restype = ctypes.c_int
+        L.mux_add.argtypes = [I32, I32, P, I64, P, I64, P, I64, P]
         _lib = L
     return _lib
 
@@ -376,3 +378,12 @@ def swiglu_bwd(dh, g, u, dg=None, du=None, stream=None):
     _check(lib().mux_swiglu_bwd(g.shape[0], g.shape[1], _ptr(dh), _ld(dh), _ptr(g), _ld(g), _ptr(u), _ld(u),
                                 _ptr(dg), _ld(dg), _ptr(du), _ld(du), _stream(stream)))
     return dg, du
+
+
+def add(a, b, y=None, stream=None):
+    """mux_add: y = a + b (y may alias a or b)."""
+    if y is None:
+        y = torch.empty(a.shape[0], a.shape[1], dtype=torch.bfloat16, device=a.device)
+    _check(lib().mux_add(a.shape[0], a.shape[1], _ptr(a), _ld(a), _ptr(b), _ld(b), _ptr(y), _ld(y),
+                         _stream(stream)))
+    return y

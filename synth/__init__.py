@@ -11,5 +11,5 @@ from .gen import (  # noqa: F401
     normal_bf16, int_bf16, sparse_int_bf16, seq_lengths, Stream,
 )
 from .configs import (  # noqa: F401
-    Workload, Linear, workload, CONFIG_IDS, base_seed, token_input, weight, adapter, int_scales,
+    Workload, Linear, workload, CONFIG_IDS, base_seed, token_input, weight, adapter, int_scales, norm_weight,
 )

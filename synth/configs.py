@@ -18,7 +18,7 @@ from typing import List, Optional
 
 import numpy as np
 
-from .gen import Stream, seq_lengths, normal_bf16, int_bf16, sparse_int_bf16
+from .gen import Stream, seq_lengths, normal, normal_bf16, int_bf16, sparse_int_bf16, bf16_bits_from_f64
 
 CONFIG_IDS = ("1", "2", "3a", "3b", "3c", "4", "5")
 
@@ -181,3 +181,11 @@ def adapter(wl: Workload, li: int, t: int, variant: str = "normal"):
 def int_scales(wl: Workload):
     """s in {1,2} for the integer fixture."""
     return [float(1 + (t % 2)) for t in range(wl.num_tasks)]
+
+
+def norm_weight(wl: Workload, i: int):
+    """RMSNorm weight [hidden] of the decoder block (i = 0: before attention,
+    1: before the MLP) ~ N(1, 0.1^2) (a trained norm's scale sits near 1)."""
+    hidden = wl.linears[0].K
+    z = normal(wl.seed, 900_000 + i, hidden)
+    return bf16_bits_from_f64(1.0 + 0.1 * z)

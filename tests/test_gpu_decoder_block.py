@@ -1,0 +1,192 @@
+"""GPU parity of a whole multiplexed LLaMA decoder block (NEXT-3; SURVEY §8(d)
+config 4 structure at a small width): pack -> Dispatch -> block forward
+(RMSNorm, q/k/v LoRA linears, RoPE, causal attention inside packed
+sequences, o linear + residual, RMSNorm, gate/up LoRA linears, SwiGLU, down
+linear + residual) -> block backward, all through libmux, against the fp64
+oracles composed in the same order (oracle/block.py + oracle/linear.c; the
+oracle keeps fp64 intermediates).  Output, input gradient and every adapter
+gradient of every linear within the north_star tolerance."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from synth import gen  # noqa: E402
+from oracle import block as ob  # noqa: E402
+from oracle import linear as olin  # noqa: E402
+from oracle import pack as opk  # noqa: E402
+from paper_2603_02885_b200 import mux  # noqa: E402
+from paper_2603_02885_b200.block import LINEARS, BlockShape, DecoderBlock  # noqa: E402
+from gpu_harness import TOL, bf16_to_f64, from_dev_bf16, rel_err, to_dev_bf16  # noqa: E402
+
+E2E_TOL = 5e-2
+
+
+def _oracle_block(shape, W, A, B, ranks, scales, seg_off, seg_task, rs, X, dY, r_cap):
+    """fp64 composition of the block, forward then backward (same order as block.py)."""
+    H, Hkv, d = shape.heads, shape.kv_heads, shape.head_dim
+    R = X.shape[0]
+    G = H // Hkv
+    lin = lambda n, x: olin.linear_fwd(seg_off, seg_task, A[n], B[n], ranks, scales, x, W[n], r_cap)[0]  # noqa
+    linb = lambda n, dy, x: olin.linear_bwd(seg_off, seg_task, A[n], B[n], ranks, scales, dy, x, W[n], r_cap)  # noqa
+    h1 = ob.rmsnorm_fwd(X, W["norm1"], shape.eps)
+    q, k, v = lin("q", h1), lin("k", h1), lin("v", h1)
+    qr = ob.rope_fwd(q.reshape(R, H, d), rs)
+    kr = ob.rope_fwd(k.reshape(R, Hkv, d), rs)
+    vv = v.reshape(R, Hkv, d)
+    Kf, Vf = np.repeat(kr, G, axis=1), np.repeat(vv, G, axis=1)
+    a, _ = ob.attention_fwd(qr, Kf, Vf, rs, d ** -0.5)
+    a2 = a.reshape(R, H * d)
+    x2 = X + lin("o", a2)
+    h2 = ob.rmsnorm_fwd(x2, W["norm2"], shape.eps)
+    g, u = lin("gate", h2), lin("up", h2)
+    m = ob.swiglu_fwd(g, u)
+    y = x2 + lin("down", m)
+    grads = {}
+    dm, _, grads["down"] = linb("down", dY, m)
+    dg, du = ob.swiglu_bwd(dm, g, u)
+    dh2g, _, grads["gate"] = linb("gate", dg, h2)
+    dh2u, _, grads["up"] = linb("up", du, h2)
+    dx2 = ob.rmsnorm_bwd(dh2g + dh2u, x2, W["norm2"], shape.eps) + dY
+    da, _, grads["o"] = linb("o", dx2, a2)
+    dq, dk, dv = ob.attention_bwd(da.reshape(R, H, d), qr, Kf, Vf, rs, d ** -0.5)
+    dk = dk.reshape(R, Hkv, G, d).sum(axis=2)
+    dv = dv.reshape(R, Hkv, G, d).sum(axis=2)
+    dq = ob.rope_bwd(dq, rs).reshape(R, H * d)
+    dk = ob.rope_bwd(dk, rs).reshape(R, Hkv * d)
+    dh1q, _, grads["q"] = linb("q", dq, h1)
+    dh1k, _, grads["k"] = linb("k", dk, h1)
+    dh1v, _, grads["v"] = linb("v", dv.reshape(R, Hkv * d), h1)
+    dx = ob.rmsnorm_bwd(dh1q + dh1k + dh1v, X, W["norm1"], shape.eps) + dx2
+    inter = dict(h1=h1, q=qr.reshape(R, H * d), k=kr.reshape(R, Hkv * d), v=v, a=a2, x2=x2, h2=h2, g=g, u=u, m=m,
+                 dm=dm, dx2=dx2, da=da)
+    return y, dx, grads, inter
+
+
+@pytest.mark.parametrize("kv_heads", [2, 1])
+def test_decoder_block_matches_oracle(kv_heads):
+    shape = BlockShape(hidden=256, ffn=384, heads=2, kv_heads=kv_heads)
+    task_lens = [np.array([100, 30], np.int32), np.array([200], np.int32), np.array([64, 1, 50], np.int32)]
+    ranks, scales = [4, 8, 16], [2.0, 2.0, 2.0]
+    r_cap = 16
+    M = len(task_lens)
+    off = np.concatenate([[0], np.cumsum([len(x) for x in task_lens])]).astype(np.int32)
+    lens = np.concatenate(task_lens).astype(np.int32)
+    T = int(lens.sum())
+    ref = opk.pack_chunks(off, lens, None, 0, 64)
+    max_rows = ref["info"]["total_rows"]
+    ref = opk.pack_chunks(off, lens, None, 0, 64, max_rows=max_rows, max_chunks=max_rows // 64)
+    seed = 21
+    st = gen.Stream(seed)
+    dims = shape.linear_dims()
+    # Attention turns relative errors of q, k into errors of the logits scaled by their magnitude, so the
+    # recipe keeps logits at the spread of a trained model (std ~ 1-2): W_q, W_k ~ N(0, 1/(4K)) (with the
+    # s = 2 LoRA term, q and k entries have std ~ 1.1); norm weights ~ 1 + N(0, 0.1^2).
+    wstd = {n: (0.5 if n in ("q", "k") else 1.0) * dims[n][0] ** -0.5 for n in LINEARS}
+    Wb = {n: gen.normal_bf16(seed, st.take(), (dims[n][1], dims[n][0]), wstd[n]) for n in LINEARS}
+    for nm in ("norm1", "norm2"):
+        Wb[nm] = gen.bf16_bits_from_f64(1.0 + 0.1 * gen.normal(seed, st.take(), shape.hidden))
+    Ab = {n: [gen.normal_bf16(seed, st.take(), (r, dims[n][0]), wstd[n]) for r in ranks] for n in LINEARS}
+    Bb = {n: [gen.normal_bf16(seed, st.take(), (dims[n][1], r), r ** -0.5) for r in ranks] for n in LINEARS}
+    Xtok = gen.normal_bf16(seed, st.take(), (T, shape.hidden), 1.0)
+    dYb = gen.normal_bf16(seed, st.take(), (max_rows, shape.hidden), 1.0)
+    dYb[ref["row_src"] < 0] = 0                       # loss gradient of pad rows is 0
+
+    # ---- GPU: pack, Dispatch, block fwd + bwd
+    pk = mux.pack_chunks(off, lens, None, 0, 64, max_rows=max_rows, max_chunks=max_rows // 64)
+    rs_dev = mux.row_start(torch.tensor(lens, dtype=torch.int32, device="cuda"), pk["seq_row"], max_rows)
+    x = mux.pack_apply(pk["row_src"], to_dev_bf16(Xtok), max_rows)
+    W = {n: to_dev_bf16(b) for n, b in Wb.items()}
+    ads = {}
+    for n in LINEARS:
+        ads[n] = []
+        for t, r in enumerate(ranks):
+            Bst = mux.make_B_storage(dims[n][1], r)
+            Bst.copy_(to_dev_bf16(Bb[n][t]))
+            ads[n].append(mux.Adapter(to_dev_bf16(Ab[n][t]), Bst, r, scales[t]))
+    blk = DecoderBlock(shape, W, ads, r_cap)
+    y = blk.forward(x, pk["seg_off"], list(range(M)), rs_dev)
+    dx = blk.backward(to_dev_bf16(dYb))
+    torch.cuda.synchronize()
+
+    # ---- oracle on the oracle's own pack (bit-identical layout, checked in test_gpu_pack)
+    f = bf16_to_f64
+    seg_off = ref["seg_off"]
+    rs = ob.row_seq_start(ref["seq_row"], lens, max_rows)
+    X = np.zeros((max_rows, shape.hidden))
+    X[ref["row_src"] >= 0] = f(Xtok)[ref["row_src"][ref["row_src"] >= 0]]
+    Wo = {n: f(b) for n, b in Wb.items()}
+    Ao = {n: [f(a) for a in Ab[n]] for n in LINEARS}
+    Bo = {n: [f(b) for b in Bb[n]] for n in LINEARS}
+    ry, rdx, rgrads, inter = _oracle_block(shape, Wo, Ao, Bo, ranks, scales, seg_off, list(range(M)), rs, X, f(dYb), r_cap)
+    valid = rs >= 0
+    G = lambda name: f(from_dev_bf16(blk.saved[name] if name in blk.saved else blk._buf[name]))  # noqa: E731
+    R, Hh, Hkv, d = max_rows, shape.heads, shape.kv_heads, shape.head_dim
+    st_ = list(range(M))
+    lin = lambda n, x_: olin.linear_fwd(seg_off, st_, Ao[n], Bo[n], ranks, scales, x_, Wo[n], r_cap)[0]  # noqa
+    linb = lambda n, dy_, x_: olin.linear_bwd(seg_off, st_, Ao[n], Bo[n], ranks, scales, dy_, x_, Wo[n], r_cap)  # noqa
+
+    # ---- stage-wise: every op of the block against the oracle fed with the GPU's own bf16 inputs of
+    # that stage (no error accumulation: the north_star bar applies to each op in its block context)
+    xg, h1, q, k, v, a_ = f(from_dev_bf16(x)), G("h1"), G("q"), G("k"), G("v"), G("a")
+    x2, h2, g, u, m = G("x2"), G("h2"), G("g"), G("u"), G("m")
+    dYf = f(dYb)
+    rep = Hh // Hkv
+    stage = {
+        "h1": (h1, ob.rmsnorm_fwd(xg, Wo["norm1"], shape.eps)),
+        "q": (q, ob.rope_fwd(lin("q", h1).reshape(R, Hh, d), rs).reshape(R, -1)),
+        "k": (k, ob.rope_fwd(lin("k", h1).reshape(R, Hkv, d), rs).reshape(R, -1)),
+        "v": (v, lin("v", h1)),
+        "a": (a_, ob.attention_fwd(q.reshape(R, Hh, d), np.repeat(k.reshape(R, Hkv, d), rep, axis=1),
+                                   np.repeat(v.reshape(R, Hkv, d), rep, axis=1), rs, d ** -0.5)[0].reshape(R, -1)),
+        "x2": (x2, xg + lin("o", a_)),
+        "h2": (h2, ob.rmsnorm_fwd(x2, Wo["norm2"], shape.eps)),
+        "g": (g, lin("gate", h2)), "u": (u, lin("up", h2)),
+        "m": (m, ob.swiglu_fwd(g, u)),
+        "y": (f(from_dev_bf16(y)), x2 + lin("down", m)),
+    }
+    sgrads = {}
+    dm_r, _, sgrads["down"] = linb("down", dYf, m)
+    dg_r, du_r = ob.swiglu_bwd(G("dm"), g, u)
+    dh2g, _, sgrads["gate"] = linb("gate", G("dg"), h2)
+    dh2u, _, sgrads["up"] = linb("up", G("du"), h2)
+    dx2_r = ob.rmsnorm_bwd(G("dh2"), x2, Wo["norm2"], shape.eps) + dYf
+    da_r, _, sgrads["o"] = linb("o", G("dx2"), a_)
+    dq_r, dk_r, dv_r = ob.attention_bwd(G("da").reshape(R, Hh, d), q.reshape(R, Hh, d),
+                                        np.repeat(k.reshape(R, Hkv, d), rep, axis=1),
+                                        np.repeat(v.reshape(R, Hkv, d), rep, axis=1), rs, d ** -0.5)
+    dk_r = dk_r.reshape(R, Hkv, rep, d).sum(axis=2)
+    dv_r = dv_r.reshape(R, Hkv, rep, d).sum(axis=2).reshape(R, -1)
+    dq_r = ob.rope_bwd(dq_r, rs).reshape(R, -1)
+    dk_r = ob.rope_bwd(dk_r, rs).reshape(R, -1)
+    dh1q, _, sgrads["q"] = linb("q", G("dq"), h1)
+    dh1k, _, sgrads["k"] = linb("k", G("dk"), h1)
+    dh1v, _, sgrads["v"] = linb("v", G("dv"), h1)
+    stage.update({
+        "dm": (G("dm"), dm_r), "dg": (G("dg"), dg_r), "du": (G("du"), du_r), "dh2": (G("dh2"), dh2g + dh2u),
+        "dx2": (G("dx2"), dx2_r), "da": (G("da"), da_r), "dq": (G("dq"), dq_r), "dk": (G("dk"), dk_r),
+        "dv": (G("dv"), dv_r), "dh1": (G("dh1"), dh1q + dh1k + dh1v),
+        "dx": (f(from_dev_bf16(dx)), ob.rmsnorm_bwd(G("dh1"), xg, Wo["norm1"], shape.eps) + G("dx2")),
+    })
+    serr = {n: rel_err(gv[valid], rv[valid]) for n, (gv, rv) in stage.items()}
+    for n in LINEARS:
+        for t in range(M):
+            serr[f"dA_{n}{t}"] = rel_err(ads[n][t].dA.cpu().numpy(), sgrads[n][t][0])
+            serr[f"dB_{n}{t}"] = rel_err(ads[n][t].dB.cpu().numpy(), sgrads[n][t][1])
+    print("stage-wise worst", sorted(serr.items(), key=lambda kv: -kv[1])[:6])
+    assert max(serr.values()) <= TOL, serr
+
+    # ---- end to end against the all-fp64 composition: ~40 bf16 roundings in sequence (DESIGN.md
+    # §11c), so the bound is the composition's, E2E_TOL
+    errs = {"y": rel_err(f(from_dev_bf16(y))[valid], ry[valid]), "dx": rel_err(f(from_dev_bf16(dx))[valid], rdx[valid])}
+    for n in LINEARS:
+        for t in range(M):
+            errs[f"dA_{n}{t}"] = rel_err(ads[n][t].dA.cpu().numpy(), rgrads[n][t][0])
+            errs[f"dB_{n}{t}"] = rel_err(ads[n][t].dB.cpu().numpy(), rgrads[n][t][1])
+    worst = max(errs.values())
+    print("end-to-end worst", worst, sorted(errs.items(), key=lambda kv: -kv[1])[:6])
+    assert worst <= E2E_TOL, errs
