@@ -208,38 +208,43 @@ __global__ void __launch_bounds__(256) mux_add_kernel(int rows, int dim, const u
 // In place on x [rows, heads * d] (row stride ld): pairs (i, i + d/2) of each
 // head rotated by theta_i = pos * base^(-2i/d), pos = r - row_start[r]
 // (inverse != 0: by -theta, the backward).  Pad rows are left untouched.
+// One thread per (row, 8 consecutive i): its 8 angles are computed once and
+// applied to every head of the row.
 __global__ void __launch_bounds__(256) mux_rope_kernel(int rows, int heads, int d, uint4* x, long long ld,
                                                       const int32_t* row_start, float log2_base, int inverse) {
   griddep_wait();
   griddep_launch_dependents();
   const int half_c = d / 16;  // 8-wide chunks per half head
-  const long long total = static_cast<long long>(rows) * heads * half_c;
+  const long long total = static_cast<long long>(rows) * half_c;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long r = i / (heads * half_c);
-    const int rem = static_cast<int>(i - r * heads * half_c);
-    const int h = rem / half_c;
-    const int c = rem - h * half_c;
+    const long long r = i / half_c;
+    const int c = static_cast<int>(i - r * half_c);
     const int rs = row_start[r];
     if (rs < 0) continue;
     const float pos = static_cast<float>(r - rs);
-    uint4* base = x + r * ld + (static_cast<long long>(h) * d) / 8;
-    float a[8], b[8];
-    bf16x8_to_f32(base[c], a);
-    bf16x8_to_f32(base[c + half_c], b);
+    float cs[8], sn[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      const int idx = 8 * c + k;
-      const float inv_freq = exp2f(-2.f * static_cast<float>(idx) / static_cast<float>(d) * log2_base);
-      float sn, cs;
-      sincosf(pos * inv_freq, &sn, &cs);
-      if (inverse) sn = -sn;
-      const float x0 = a[k], x1 = b[k];
-      a[k] = x0 * cs - x1 * sn;
-      b[k] = x1 * cs + x0 * sn;
+      const float inv_freq = exp2f(-2.f * static_cast<float>(8 * c + k) / static_cast<float>(d) * log2_base);
+      sincosf(pos * inv_freq, &sn[k], &cs[k]);
+      if (inverse) sn[k] = -sn[k];
     }
-    base[c] = f32_to_bf16x8(a);
-    base[c + half_c] = f32_to_bf16x8(b);
+    uint4* row = x + r * ld;
+    for (int h = 0; h < heads; ++h) {
+      uint4* base = row + (static_cast<long long>(h) * d) / 8;
+      float a[8], b[8];
+      bf16x8_to_f32(base[c], a);
+      bf16x8_to_f32(base[c + half_c], b);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float x0 = a[k], x1 = b[k];
+        a[k] = x0 * cs[k] - x1 * sn[k];
+        b[k] = x1 * cs[k] + x0 * sn[k];
+      }
+      base[c] = f32_to_bf16x8(a);
+      base[c + half_c] = f32_to_bf16x8(b);
+    }
   }
 }
 
@@ -304,8 +309,8 @@ cudaError_t launch_add(int rows, int dim, const void* a, long long lda, const vo
 
 cudaError_t launch_rope(int rows, int heads, int d, void* x, long long ld, const int32_t* row_start, float base,
                         bool inverse, int num_sms, cudaStream_t s) {
-  const long long work = static_cast<long long>(rows) * heads * (d / 16);
-  if (work == 0) return cudaSuccess;
+  const long long work = static_cast<long long>(rows) * (d / 16);
+  if (work == 0 || heads == 0) return cudaSuccess;
   return launch_pdl(mux_rope_kernel, dim3(grid_for(work, 256, num_sms)), dim3(256), 0, s, rows, heads, d,
                     static_cast<uint4*>(x), ld / 8, row_start, log2f(base), inverse ? 1 : 0);
 }
