@@ -1,4 +1,5 @@
-// attn.cu — causal attention inside packed sequences:
+// attn.cu — backward of the causal attention inside packed sequences (the
+// forward is attn_tc.cu, on tcgen05):
 // the chunk dependency of the paper's alignment ("KV cache reuse in causal
 // attention", Fig. alignment): the queries of a chunk attend to the
 // keys of the earlier chunks of the same pack, masked to their own sequence
@@ -13,7 +14,6 @@
 // swizzled shared-memory tiles fed by cp.async double buffering.  At the
 // paper's sequence lengths (<= 512) attention is < 1% of a decoder block's
 // FLOPs, so this warp-level design, not tcgen05, is used here.
-//   fwd : O, LSE per (row, head)
 //   bwd : D = rowsum(dO * O); dK, dV per key tile (loops over the query tiles
 //         that see it and over the q heads of its KV group); dQ per query tile
 //         — two kernels, no atomics: deterministic.
@@ -133,141 +133,6 @@ __device__ __forceinline__ void tile_key_range(const int32_t* row_start, int q0,
     }
   }
   __syncthreads();
-}
-
-// =========================================================================== forward
-// grid (ceil(R/64), H); smem: Q 16 KB | 2 x (K 16 KB, V 16 KB)
-__global__ void __launch_bounds__(kAttnThreads) mux_attn_fwd_kernel(
-    int R, int H, int Hkv, const __nv_bfloat16* q, long long ldq, const __nv_bfloat16* k, long long ldk,
-    const __nv_bfloat16* v, long long ldv, const int32_t* row_start, float scale_log2, __nv_bfloat16* o,
-    long long ldo, float* lse) {
-  extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ int s_lo, s_hi;
-  griddep_wait();
-  griddep_launch_dependents();
-  const int q0 = blockIdx.x * 64;
-  const int h = blockIdx.y;
-  const int hk = h / (H / Hkv);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = lane >> 2, t4 = lane & 3;
-  const uint32_t sQ = smem_u32(smem), sKV = sQ + 64 * kRowB;
-  tile_key_range(row_start, q0, R, &s_lo, &s_hi);
-  const int lo = s_lo, hi = s_hi;
-  const int r0 = q0 + warp * 16 + g, r1 = r0 + 8;
-  const int lo0 = r0 < R ? row_start[r0] : -1, lo1 = r1 < R ? row_start[r1] : -1;
-  float oacc[16][4];
-#pragma unroll
-  for (int i = 0; i < 16; ++i) oacc[i][0] = oacc[i][1] = oacc[i][2] = oacc[i][3] = 0.f;
-  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
-  if (hi >= 0) {
-    load_tile<64>(sQ, q + h * kHd, ldq, q0, R);
-    load_tile<64>(sKV, k + hk * kHd, ldk, lo, R);
-    load_tile<64>(sKV + 64 * kRowB, v + hk * kHd, ldv, lo, R);
-    cp_async_commit();
-    const int ntiles = (hi - lo) / 64 + 1;
-    for (int it = 0; it < ntiles; ++it) {
-      const int kt = lo + it * 64;
-      const uint32_t sK = sKV + (it & 1) * (128 * kRowB), sV = sK + 64 * kRowB;
-      if (it + 1 < ntiles) {
-        const uint32_t nK = sKV + ((it + 1) & 1) * (128 * kRowB);
-        load_tile<64>(nK, k + hk * kHd, ldk, kt + 64, R);
-        load_tile<64>(nK + 64 * kRowB, v + hk * kHd, ldv, kt + 64, R);
-        cp_async_commit();
-        cp_async_wait<1>();
-      } else {
-        cp_async_wait<0>();
-      }
-      __syncthreads();
-      // S = Q K^T (16 x 64 per warp)
-      float s[8][4];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) s[i][0] = s[i][1] = s[i][2] = s[i][3] = 0.f;
-#pragma unroll
-      for (int ks = 0; ks < 8; ++ks) {
-        uint32_t a[4];
-        ld_a(sQ, warp * 16, ks * 16, lane, a);
-#pragma unroll
-        for (int np = 0; np < 4; ++np) {
-          uint32_t b[4];
-          ld_b(sK, np * 16, ks * 16, lane, b);
-          mma16816(s[2 * np], a, b[0], b[1]);
-          mma16816(s[2 * np + 1], a, b[2], b[3]);
-        }
-      }
-      // mask to [row_start, row] and run the online softmax (log2 domain)
-      float mx0 = -INFINITY, mx1 = -INFINITY;
-#pragma unroll
-      for (int nt = 0; nt < 8; ++nt) {
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int j = kt + nt * 8 + 2 * t4 + e;
-          const bool v0 = lo0 >= 0 && j >= lo0 && j <= r0;
-          const bool v1 = lo1 >= 0 && j >= lo1 && j <= r1;
-          s[nt][e] = v0 ? s[nt][e] * scale_log2 : -INFINITY;
-          s[nt][2 + e] = v1 ? s[nt][2 + e] * scale_log2 : -INFINITY;
-          mx0 = fmaxf(mx0, s[nt][e]);
-          mx1 = fmaxf(mx1, s[nt][2 + e]);
-        }
-      }
-      mx0 = quad_max(mx0);
-      mx1 = quad_max(mx1);
-      const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
-      const float u0 = mn0 == -INFINITY ? 0.f : mn0, u1 = mn1 == -INFINITY ? 0.f : mn1;
-      const float al0 = exp2f(m0 - u0), al1 = exp2f(m1 - u1);
-      float ps0 = 0.f, ps1 = 0.f;
-#pragma unroll
-      for (int nt = 0; nt < 8; ++nt) {
-        s[nt][0] = exp2f(s[nt][0] - u0);
-        s[nt][1] = exp2f(s[nt][1] - u0);
-        s[nt][2] = exp2f(s[nt][2] - u1);
-        s[nt][3] = exp2f(s[nt][3] - u1);
-        ps0 += s[nt][0] + s[nt][1];
-        ps1 += s[nt][2] + s[nt][3];
-      }
-      l0 = l0 * al0 + ps0;
-      l1 = l1 * al1 + ps1;
-      m0 = mn0;
-      m1 = mn1;
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        oacc[i][0] *= al0;
-        oacc[i][1] *= al0;
-        oacc[i][2] *= al1;
-        oacc[i][3] *= al1;
-      }
-      // O += P V (k = 64 keys, n = 128 dims)
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
-        uint32_t a[4];
-        c_to_a(s[2 * kk], s[2 * kk + 1], a);
-#pragma unroll
-        for (int dn = 0; dn < 8; ++dn) {
-          uint32_t b[4];
-          ld_bt(sV, kk * 16, dn * 16, lane, b);
-          mma16816(oacc[2 * dn], a, b[0], b[1]);
-          mma16816(oacc[2 * dn + 1], a, b[2], b[3]);
-        }
-      }
-      __syncthreads();  // this buffer is refilled two iterations later
-    }
-  }
-  l0 = quad_sum(l0);
-  l1 = quad_sum(l1);
-  const float i0 = l0 > 0.f ? 1.f / l0 : 0.f, i1 = l1 > 0.f ? 1.f / l1 : 0.f;
-#pragma unroll
-  for (int dn = 0; dn < 16; ++dn) {
-    const int col = h * kHd + dn * 8 + 2 * t4;
-    if (r0 < R)
-      *reinterpret_cast<uint32_t*>(o + static_cast<long long>(r0) * ldo + col) =
-          pack_bf16x2(oacc[dn][0] * i0, oacc[dn][1] * i0);
-    if (r1 < R)
-      *reinterpret_cast<uint32_t*>(o + static_cast<long long>(r1) * ldo + col) =
-          pack_bf16x2(oacc[dn][2] * i1, oacc[dn][3] * i1);
-  }
-  if (t4 == 0) {
-    if (r0 < R) lse[static_cast<long long>(r0) * H + h] = l0 > 0.f ? (m0 + log2f(l0)) * kLn2 : -INFINITY;
-    if (r1 < R) lse[static_cast<long long>(r1) * H + h] = l1 > 0.f ? (m1 + log2f(l1)) * kLn2 : -INFINITY;
-  }
 }
 
 // =========================================================================== backward
@@ -583,26 +448,8 @@ __global__ void __launch_bounds__(kAttnThreads) mux_attn_bwd_dq_kernel(
 }
 
 // ------------------------------------------------------------------ launchers
-constexpr size_t kFwdSmem = 5 * 64 * kRowB;                   // 80 KB
 constexpr size_t kDkdvSmem = 2 * 64 * kRowB + 2 * 2 * kBQ * kRowB;  // 64 KB
 constexpr size_t kDqSmem = 6 * 64 * kRowB;                    // 96 KB
-
-cudaError_t launch_attn_fwd(int R, int H, int Hkv, const void* q, long long ldq, const void* k, long long ldk,
-                            const void* v, long long ldv, const int32_t* row_start, float scale, void* o,
-                            long long ldo, float* lse, cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(mux_attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kFwdSmem));
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
-  if (R == 0) return cudaSuccess;
-  return launch_pdl(mux_attn_fwd_kernel, dim3((R + 63) / 64, H), dim3(kAttnThreads), kFwdSmem, s, R, H, Hkv,
-                    static_cast<const __nv_bfloat16*>(q), ldq, static_cast<const __nv_bfloat16*>(k), ldk,
-                    static_cast<const __nv_bfloat16*>(v), ldv, row_start, scale * kLog2e,
-                    static_cast<__nv_bfloat16*>(o), ldo, lse);
-}
 
 cudaError_t launch_attn_bwd(int R, int H, int Hkv, const void* dO, long long lddo, const void* q, long long ldq,
                             const void* k, long long ldk, const void* v, long long ldv, const void* o,

@@ -82,4 +82,17 @@ struct GradParams {
   float* task_dB[MUX_MAX_ADAPTERS];
 };
 
+// ---- causal attention forward on tcgen05 (attn_tc.cu)
+struct AttnTcParams {
+  CUtensorMap map_q;  // q [R, H*128]: box {64 cols, 128 rows}, 128 B swizzle
+  CUtensorMap map_k;  // k [R, Hkv*128]: box {64 cols, 64 rows}
+  CUtensorMap map_v;  // v [R, Hkv*128]
+  const int32_t* row_start;
+  __nv_bfloat16* o;
+  long long ldo;
+  float* lse;
+  int R, H, Hkv;
+  float scale_log2;
+};
+
 }  // namespace mux

@@ -40,9 +40,7 @@ cudaError_t launch_rope(int rows, int heads, int d, void* x, long long ld, const
                         bool inverse, int num_sms, cudaStream_t s);
 cudaError_t launch_add(int rows, int dim, const void* a, long long lda, const void* b, long long ldb, void* y,
                        long long ldy, int num_sms, cudaStream_t s);
-cudaError_t launch_attn_fwd(int R, int H, int Hkv, const void* q, long long ldq, const void* k, long long ldk,
-                            const void* v, long long ldv, const int32_t* row_start, float scale, void* o,
-                            long long ldo, float* lse, cudaStream_t s);
+cudaError_t launch_attn_fwd_tc(const AttnTcParams& p, cudaStream_t s);
 cudaError_t launch_attn_bwd(int R, int H, int Hkv, const void* dO, long long lddo, const void* q, long long ldq,
                             const void* k, long long ldk, const void* v, long long ldv, const void* o,
                             long long ldo, const float* lse, const int32_t* row_start, float scale, void* dq,
@@ -524,8 +522,20 @@ mux_status mux_attn_fwd(int32_t rows, int32_t heads, int32_t kv_heads, int32_t h
       !ld_ok(ldv, kv_heads * 128))
     return fail(MUX_ERR_INVALID_ARGUMENT, "row strides must cover the heads and be multiples of 8");
   if (!std::isfinite(scale)) return fail(MUX_ERR_INVALID_ARGUMENT, "scale not finite");
-  cudaError_t e = launch_attn_fwd(rows, heads, kv_heads, q, ldq, k, ldk, v, ldv, row_start, scale, o, ldo, lse,
-                                  stream);
+  static thread_local AttnTcParams ap;
+  if (!make_map(&ap.map_q, q, heads * 128, rows, ldq, 64, 128) ||
+      !make_map(&ap.map_k, k, kv_heads * 128, rows, ldk, 64, 64) ||
+      !make_map(&ap.map_v, v, kv_heads * 128, rows, ldv, 64, 64))
+    return fail(MUX_ERR_CUDA, "cuTensorMapEncodeTiled failed for q/k/v");
+  ap.row_start = row_start;
+  ap.o = reinterpret_cast<__nv_bfloat16*>(o);
+  ap.ldo = ldo;
+  ap.lse = lse;
+  ap.R = rows;
+  ap.H = heads;
+  ap.Hkv = kv_heads;
+  ap.scale_log2 = scale * 1.4426950408889634f;
+  cudaError_t e = launch_attn_fwd_tc(ap, stream);
   if (e != cudaSuccess) return cuda_fail(e, "mux_attn_fwd launch");
   return MUX_OK;
 }
