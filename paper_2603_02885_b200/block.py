@@ -138,6 +138,6 @@ class DecoderBlock:
 
     # kernel launches: forward = 2 norms + 7 linears + 2 RoPE + attention + swiglu + 2 adds = 15;
     # backward = 7 linears x (dX GEMM + adapter-gradient kernel) + swiglu + 2 norms + attention
-    # (D, dK/dV, dQ) + 2 RoPE + 5 adds = 27
+    # (D, dV, dK, dQ) + 2 RoPE + 5 adds = 28
     LAUNCHES_FWD = 15
-    LAUNCHES_BWD = 27
+    LAUNCHES_BWD = 28

@@ -95,4 +95,23 @@ struct AttnTcParams {
   float scale_log2;
 };
 
+// ---- causal attention backward on tcgen05 (attn_bwd_tc.cu); boxes {64 cols, rows}
+struct AttnBwdTcParams {
+  CUtensorMap map_q128, map_do128;  // dQ kernel: 128-row query tiles
+  CUtensorMap map_k64, map_v64;     // dQ kernel: 64-row key tiles
+  CUtensorMap map_k128, map_v128;   // dK/dV kernel: 128-row key tiles
+  CUtensorMap map_q64, map_do64;    // dK/dV kernel: 64-row query tiles
+  const int32_t* row_start;
+  const float* lse;                 // [R, H]
+  const float* D;                   // [R, H] rowsum(dO * O)
+  __nv_bfloat16* dq;
+  long long lddq;
+  __nv_bfloat16* dk;
+  long long lddk;
+  __nv_bfloat16* dv;
+  long long lddv;
+  int R, H, Hkv;
+  float scale_log2, scale;
+};
+
 }  // namespace mux

@@ -41,11 +41,10 @@ cudaError_t launch_rope(int rows, int heads, int d, void* x, long long ld, const
 cudaError_t launch_add(int rows, int dim, const void* a, long long lda, const void* b, long long ldb, void* y,
                        long long ldy, int num_sms, cudaStream_t s);
 cudaError_t launch_attn_fwd_tc(const AttnTcParams& p, cudaStream_t s);
-cudaError_t launch_attn_bwd(int R, int H, int Hkv, const void* dO, long long lddo, const void* q, long long ldq,
-                            const void* k, long long ldk, const void* v, long long ldv, const void* o,
-                            long long ldo, const float* lse, const int32_t* row_start, float scale, void* dq,
-                            long long lddq, void* dk, long long lddk, void* dv, long long lddv, float* Dws,
-                            cudaStream_t s);
+cudaError_t launch_attn_bwd_pre(int R, int H, const void* dO, long long lddo, const void* o, long long ldo,
+                                float* D, cudaStream_t s);
+cudaError_t launch_attn_bwd_tc(const AttnBwdTcParams& p, cudaStream_t s);
+
 }  // namespace mux
 
 using namespace mux;
@@ -566,8 +565,29 @@ mux_status mux_attn_bwd(int32_t rows, int32_t heads, int32_t kv_heads, int32_t h
   const size_t need = mux_attn_workspace_size(rows, heads);
   if (!workspace || workspace_bytes < need)
     return fail(MUX_ERR_INSUFFICIENT_BUFFER, "attention workspace %zu < %zu bytes", workspace_bytes, need);
-  cudaError_t e = launch_attn_bwd(rows, heads, kv_heads, dO, lddo, q, ldq, k, ldk, v, ldv, o, ldo, lse, row_start,
-                                  scale, dq, lddq, dk, lddk, dv, lddv, static_cast<float*>(workspace), stream);
+  static thread_local AttnBwdTcParams bp;
+  const int qc2 = heads * 128, kc2 = kv_heads * 128;
+  if (!make_map(&bp.map_q128, q, qc2, rows, ldq, 64, 128) || !make_map(&bp.map_do128, dO, qc2, rows, lddo, 64, 128) ||
+      !make_map(&bp.map_q64, q, qc2, rows, ldq, 64, 64) || !make_map(&bp.map_do64, dO, qc2, rows, lddo, 64, 64) ||
+      !make_map(&bp.map_k64, k, kc2, rows, ldk, 64, 64) || !make_map(&bp.map_v64, v, kc2, rows, ldv, 64, 64) ||
+      !make_map(&bp.map_k128, k, kc2, rows, ldk, 64, 128) || !make_map(&bp.map_v128, v, kc2, rows, ldv, 64, 128))
+    return fail(MUX_ERR_CUDA, "cuTensorMapEncodeTiled failed for q/k/v/dO");
+  bp.row_start = row_start;
+  bp.lse = lse;
+  bp.D = static_cast<const float*>(workspace);
+  bp.dq = reinterpret_cast<__nv_bfloat16*>(dq);
+  bp.lddq = lddq;
+  bp.dk = reinterpret_cast<__nv_bfloat16*>(dk);
+  bp.lddk = lddk;
+  bp.dv = reinterpret_cast<__nv_bfloat16*>(dv);
+  bp.lddv = lddv;
+  bp.R = rows;
+  bp.H = heads;
+  bp.Hkv = kv_heads;
+  bp.scale_log2 = scale * 1.4426950408889634f;
+  bp.scale = scale;
+  cudaError_t e = launch_attn_bwd_pre(rows, heads, dO, lddo, o, ldo, static_cast<float*>(workspace), stream);
+  if (e == cudaSuccess) e = launch_attn_bwd_tc(bp, stream);
   if (e != cudaSuccess) return cuda_fail(e, "mux_attn_bwd launch");
   return MUX_OK;
 }
