@@ -256,13 +256,21 @@ MUX_API mux_status mux_attn_bwd(int32_t rows, int32_t heads, int32_t kv_heads, i
 MUX_API mux_status mux_rope(int32_t rows, int32_t heads, int32_t head_dim, mux_bf16* x, int64_t ld,
                             const int32_t* row_start, float base, int32_t inverse, cudaStream_t stream);
 
-/* RMSNorm y = x / sqrt(mean(x^2) + eps) * w; backward dx for upstream dy (w is
- * frozen backbone: no dw).  x, y, dy, dx [rows, dim]; w [dim]; dim % 8 == 0. */
-MUX_API mux_status mux_rmsnorm_fwd(int32_t rows, int32_t dim, const mux_bf16* x, int64_t ldx, const mux_bf16* w,
-                                   float eps, mux_bf16* y, int64_t ldy, cudaStream_t stream);
+/* RMSNorm with the pre-norm residual stream fused in (w is frozen backbone: no dw).
+ * fwd: xs = x + res (bf16; written to xsum) when res != NULL, else xs = x;
+ *      y = xs / sqrt(mean(xs^2) + eps) * w.   res and xsum may be NULL (plain RMSNorm).
+ * bwd: g = dy + dy2 + dy3 (dy2, dy3 may be NULL: the gradients of the linears that
+ *      read the normalised output, summed here), dx = d rmsnorm(x)/dx^T (g * w)
+ *      + resid (resid may be NULL: the residual path's gradient).
+ * All [rows, dim] with row strides in elements; w [dim]; dim % 8 == 0. */
+MUX_API mux_status mux_rmsnorm_fwd(int32_t rows, int32_t dim, const mux_bf16* x, int64_t ldx, const mux_bf16* res,
+                                   int64_t ldres, mux_bf16* xsum, int64_t ldxs, const mux_bf16* w, float eps,
+                                   mux_bf16* y, int64_t ldy, cudaStream_t stream);
 MUX_API mux_status mux_rmsnorm_bwd(int32_t rows, int32_t dim, const mux_bf16* dy, int64_t lddy,
-                                   const mux_bf16* x, int64_t ldx, const mux_bf16* w, float eps, mux_bf16* dx,
-                                   int64_t lddx, cudaStream_t stream);
+                                   const mux_bf16* dy2, int64_t lddy2, const mux_bf16* dy3, int64_t lddy3,
+                                   const mux_bf16* x, int64_t ldx, const mux_bf16* w, float eps,
+                                   const mux_bf16* resid, int64_t ldres, mux_bf16* dx, int64_t lddx,
+                                   cudaStream_t stream);
 
 /* SwiGLU h = silu(g) * u; backward dg = dh u s (1 + g (1 - s)), du = dh silu(g),
  * s = sigmoid(g).  All [rows, dim], dim % 8 == 0. */

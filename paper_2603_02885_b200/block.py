@@ -100,8 +100,9 @@ class DecoderBlock:
         a, lse = mux.attn_fwd(q, k, v, row_start, s.heads, s.kv_heads, s.head_dim ** -0.5,
                               o=self._b("a", s.heads * s.head_dim), lse=self._b("lse", s.heads, torch.float32))
         o = self._lin_fwd("o", a)
-        x2 = mux.add(x, o, y=self._b("x2", s.hidden))
-        h2 = mux.rmsnorm_fwd(x2, self.w["norm2"], s.eps, y=self._b("h2", s.hidden))
+        # residual add fused into the second RMSNorm: x2 = x + o, h2 = RMSNorm(x2)
+        h2, x2 = mux.rmsnorm_fwd(o, self.w["norm2"], s.eps, y=self._b("h2", s.hidden), res=x,
+                                 xsum=self._b("x2", s.hidden))
         g, u = self._lin_fwd("gate", h2), self._lin_fwd("up", h2)
         m = mux.swiglu_fwd(g, u, h=self._b("m", s.ffn))
         d = self._lin_fwd("down", m)
@@ -114,9 +115,9 @@ class DecoderBlock:
         dg, du = mux.swiglu_bwd(dm, sv["g"], sv["u"], dg=self._b("dg", s.ffn), du=self._b("du", s.ffn))
         dh2 = self._lin_bwd("gate", dg, sv["h2"], self._b("dh2", s.hidden))
         dh2u = self._lin_bwd("up", du, sv["h2"], self._b("dh2u", s.hidden))
-        mux.add(dh2, dh2u, y=dh2)
-        dx2 = mux.rmsnorm_bwd(dh2, sv["x2"], self.w["norm2"], s.eps, dx=self._b("dx2", s.hidden))
-        mux.add(dx2, dy, y=dx2)                                   # residual
+        # dx2 = RMSNorm'(x2)^T (dh2 + dh2u) + dy (residual): sum and residual fused into the norm
+        dx2 = mux.rmsnorm_bwd(dh2, sv["x2"], self.w["norm2"], s.eps, dx=self._b("dx2", s.hidden), dy2=dh2u,
+                              resid=dy)
         da = self._lin_bwd("o", dx2, sv["a"], self._b("da", s.heads * s.head_dim))
         need = mux.attn_workspace_size(self._rows, s.heads)
         ws = self._buf.get("attn_ws")
@@ -129,15 +130,15 @@ class DecoderBlock:
         mux.rope_(dq, self.row_start, s.heads, s.head_dim, s.rope_base, inverse=True)
         mux.rope_(dk, self.row_start, s.kv_heads, s.head_dim, s.rope_base, inverse=True)
         dh1 = self._lin_bwd("q", dq, sv["h1"], self._b("dh1", s.hidden))
-        t = self._lin_bwd("k", dk, sv["h1"], self._b("dh1k", s.hidden))
-        mux.add(dh1, t, y=dh1)
-        t = self._lin_bwd("v", dv, sv["h1"], t)
-        mux.add(dh1, t, y=dh1)
-        dx = mux.rmsnorm_bwd(dh1, self.x, self.w["norm1"], s.eps, dx=self._b("dx", s.hidden))
-        return mux.add(dx, dx2, y=dx)
+        dh1k = self._lin_bwd("k", dk, sv["h1"], self._b("dh1k", s.hidden))
+        dh1v = self._lin_bwd("v", dv, sv["h1"], self._b("dh1v", s.hidden))
+        # dx = RMSNorm'(x)^T (dh1 + dh1k + dh1v) + dx2 (residual), one fused pass
+        return mux.rmsnorm_bwd(dh1, self.x, self.w["norm1"], s.eps, dx=self._b("dx", s.hidden), dy2=dh1k, dy3=dh1v,
+                               resid=dx2)
 
-    # kernel launches: forward = 2 norms + 7 linears + 2 RoPE + attention + swiglu + 2 adds = 15;
-    # backward = 7 linears x (dX GEMM + adapter-gradient kernel) + swiglu + 2 norms + attention
-    # (D, dV, dK, dQ) + 2 RoPE + 5 adds = 28
-    LAUNCHES_FWD = 15
-    LAUNCHES_BWD = 28
+    # kernel launches: forward = 2 norms (the second fused with the residual add) + 7 linears +
+    # 2 RoPE + attention + swiglu + 1 residual add = 14; backward = 7 linears x (dX GEMM +
+    # adapter-gradient kernel) + swiglu + 2 norms (gradient sums and residuals fused) +
+    # attention (D, dV, dK, dQ) + 2 RoPE = 23
+    LAUNCHES_FWD = 14
+    LAUNCHES_BWD = 23

@@ -55,28 +55,38 @@ __device__ __forceinline__ void store_row64(uint8_t* tile, int row, const uint32
 }  // namespace
 
 // =========================================================================== D
-// D[r, h] = sum_d dO[r, h, d] O[r, h, d]  (one warp per (row, head))
+// D[r, h] = sum_d dO[r, h, d] O[r, h, d]: 16 threads per (row, head), 16-byte loads,
+// whole warps iterate together (a half-warp past the end contributes nothing),
+// half-warp shuffle reduction (grid-stride over rows x heads).
 __global__ void __launch_bounds__(256) mux_attn_bwd_pre_kernel(int R, int H, const __nv_bfloat16* dO,
                                                               long long lddo, const __nv_bfloat16* O,
                                                               long long ldo, float* D) {
   griddep_wait();
   griddep_launch_dependents();
-  const long long wid = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (wid >= static_cast<long long>(R) * H) return;
-  const long long r = wid / H;
-  const int h = static_cast<int>(wid - r * H);
-  const uint2 a = *reinterpret_cast<const uint2*>(dO + r * lddo + h * 128 + lane * 4);
-  const uint2 b = *reinterpret_cast<const uint2*>(O + r * ldo + h * 128 + lane * 4);
-  float acc = __uint_as_float(a.x << 16) * __uint_as_float(b.x << 16) +
-              __uint_as_float(a.x & 0xFFFF0000u) * __uint_as_float(b.x & 0xFFFF0000u) +
-              __uint_as_float(a.y << 16) * __uint_as_float(b.y << 16) +
-              __uint_as_float(a.y & 0xFFFF0000u) * __uint_as_float(b.y & 0xFFFF0000u);
+  const long long total = static_cast<long long>(R) * H * 16;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i - (threadIdx.x & 31) < total;
+       i += stride) {
+    const bool live = i < total;
+    const long long rh = i >> 4;
+    const int c = static_cast<int>(i & 15);
+    float acc = 0.f;
+    if (live) {
+      const long long r = rh / H;
+      const int h = static_cast<int>(rh - r * H);
+      const uint4 a = *reinterpret_cast<const uint4*>(dO + r * lddo + h * 128 + c * 8);
+      const uint4 b = *reinterpret_cast<const uint4*>(O + r * ldo + h * 128 + c * 8);
+      const uint32_t x[4] = {a.x, a.y, a.z, a.w}, y[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (lane == 0) D[wid] = acc;
+      for (int e = 0; e < 4; ++e)
+        acc += __uint_as_float(x[e] << 16) * __uint_as_float(y[e] << 16) +
+               __uint_as_float(x[e] & 0xFFFF0000u) * __uint_as_float(y[e] & 0xFFFF0000u);
+    }
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (live && c == 0) D[rh] = acc;
+  }
 }
-
 
 // =========================================================================== dQ
 // smem: Q 32 KB | dO 32 KB | dS 16 KB | K 16 KB, V 16 KB  (112 KB) | barriers
@@ -537,9 +547,11 @@ constexpr size_t dkdv_smem() {
 
 cudaError_t launch_attn_bwd_pre(int R, int H, const void* dO, long long lddo, const void* o, long long ldo,
                                 float* D, cudaStream_t s) {
-  const long long warps = static_cast<long long>(R) * H;
-  if (warps == 0) return cudaSuccess;
-  return launch_pdl(mux_attn_bwd_pre_kernel, dim3(static_cast<unsigned>((warps + 7) / 8)), dim3(256), 0, s, R, H,
+  const long long threads = static_cast<long long>(R) * H * 16;
+  if (threads == 0) return cudaSuccess;
+  long long blocks = (threads + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  return launch_pdl(mux_attn_bwd_pre_kernel, dim3(static_cast<unsigned>(blocks)), dim3(256), 0, s, R, H,
                     static_cast<const __nv_bfloat16*>(dO), lddo, static_cast<const __nv_bfloat16*>(o), ldo, D);
 }
 

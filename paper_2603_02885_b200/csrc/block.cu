@@ -63,30 +63,48 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 }
 
 // ------------------------------------------------------------------ RMSNorm
-// One CTA per row.  fwd: y = x * rstd * w, rstd = 1/sqrt(mean(x^2) + eps).
+// One CTA per row, fp32 sums.  The pre-norm residual stream is fused in:
+//   fwd: xs = x + res (rounded to bf16 and stored when res != null), y = xs * rstd * w,
+//        rstd = 1/sqrt(mean(xs^2) + eps)
+//   bwd: g = (dy + dy2 + dy3) * w (absent terms skipped),
+//        dx = rstd * (g - xs * rstd^2 * mean(g * xs)) + resid
+// so a decoder block's residual adds and gradient sums cost no extra pass.
 constexpr int kNormThreads = 256;
 
+__device__ __forceinline__ void load_sum(const uint4* x, const uint4* res, long long c, float (&f)[8]) {
+  bf16x8_to_f32(x[c], f);
+  if (res) {
+    float r[8];
+    bf16x8_to_f32(res[c], r);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) f[i] = __bfloat162float(__float2bfloat16_rn(f[i] + r[i]));
+  }
+}
+
 __global__ void __launch_bounds__(kNormThreads) mux_rmsnorm_fwd_kernel(int dim, const uint4* x, long long ldx,
-                                                                      const uint4* w, float eps, uint4* y,
-                                                                      long long ldy) {
+                                                                      const uint4* res, long long ldr,
+                                                                      uint4* xs_out, long long ldxs, const uint4* w,
+                                                                      float eps, uint4* y, long long ldy) {
   __shared__ float red[kNormThreads / 32];
   griddep_wait();
   griddep_launch_dependents();
-  const int row = blockIdx.x;
-  const uint4* xr = x + static_cast<long long>(row) * ldx;
+  const long long row = blockIdx.x;
+  const uint4* xr = x + row * ldx;
+  const uint4* rr = res ? res + row * ldr : nullptr;
   const int nc = dim / 8;
   float ss = 0.f;
   for (int c = threadIdx.x; c < nc; c += kNormThreads) {
     float f[8];
-    bf16x8_to_f32(xr[c], f);
+    load_sum(xr, rr, c, f);
+    if (xs_out) xs_out[row * ldxs + c] = f32_to_bf16x8(f);
 #pragma unroll
     for (int i = 0; i < 8; ++i) ss = fmaf(f[i], f[i], ss);
   }
   const float rstd = rsqrtf(block_sum<kNormThreads>(ss, red) / static_cast<float>(dim) + eps);
-  uint4* yr = y + static_cast<long long>(row) * ldy;
+  uint4* yr = y + row * ldy;
   for (int c = threadIdx.x; c < nc; c += kNormThreads) {
     float f[8], g[8];
-    bf16x8_to_f32(xr[c], f);
+    load_sum(xr, rr, c, f);
     bf16x8_to_f32(w[c], g);
 #pragma unroll
     for (int i = 0; i < 8; ++i) f[i] = f[i] * rstd * g[i];
@@ -94,23 +112,40 @@ __global__ void __launch_bounds__(kNormThreads) mux_rmsnorm_fwd_kernel(int dim, 
   }
 }
 
-// bwd (w frozen): g = dy * w;  dx = rstd * (g - x * rstd^2 * mean(g * x)).
-__global__ void __launch_bounds__(kNormThreads) mux_rmsnorm_bwd_kernel(int dim, const uint4* dy, long long lddy,
-                                                                      const uint4* x, long long ldx,
-                                                                      const uint4* w, float eps, uint4* dx,
-                                                                      long long lddx) {
+struct NormBwdIn {
+  const uint4* dy[3];  // up to three upstream gradients, summed (null = absent)
+  long long lddy[3];
+  const uint4* resid;  // residual-path gradient added to dx (null = none)
+  long long ldr;
+};
+
+__device__ __forceinline__ void load_dy(const NormBwdIn& in, long long row, int c, float (&d)[8]) {
+  bf16x8_to_f32(in.dy[0][row * in.lddy[0] + c], d);
+#pragma unroll
+  for (int k = 1; k < 3; ++k) {
+    if (in.dy[k]) {
+      float e[8];
+      bf16x8_to_f32(in.dy[k][row * in.lddy[k] + c], e);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) d[i] += e[i];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kNormThreads) mux_rmsnorm_bwd_kernel(int dim, NormBwdIn in, const uint4* x,
+                                                                      long long ldx, const uint4* w, float eps,
+                                                                      uint4* dx, long long lddx) {
   __shared__ float red[kNormThreads / 32];
   griddep_wait();
   griddep_launch_dependents();
-  const int row = blockIdx.x;
-  const uint4* xr = x + static_cast<long long>(row) * ldx;
-  const uint4* dyr = dy + static_cast<long long>(row) * lddy;
+  const long long row = blockIdx.x;
+  const uint4* xr = x + row * ldx;
   const int nc = dim / 8;
   float ss = 0.f, gx = 0.f;
   for (int c = threadIdx.x; c < nc; c += kNormThreads) {
     float f[8], d[8], g[8];
     bf16x8_to_f32(xr[c], f);
-    bf16x8_to_f32(dyr[c], d);
+    load_dy(in, row, c, d);
     bf16x8_to_f32(w[c], g);
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -121,14 +156,20 @@ __global__ void __launch_bounds__(kNormThreads) mux_rmsnorm_bwd_kernel(int dim, 
   const float inv_dim = 1.f / static_cast<float>(dim);
   const float rstd = rsqrtf(block_sum<kNormThreads>(ss, red) * inv_dim + eps);
   const float coef = rstd * rstd * block_sum<kNormThreads>(gx, red) * inv_dim;
-  uint4* dxr = dx + static_cast<long long>(row) * lddx;
+  uint4* dxr = dx + row * lddx;
   for (int c = threadIdx.x; c < nc; c += kNormThreads) {
     float f[8], d[8], g[8];
     bf16x8_to_f32(xr[c], f);
-    bf16x8_to_f32(dyr[c], d);
+    load_dy(in, row, c, d);
     bf16x8_to_f32(w[c], g);
 #pragma unroll
     for (int i = 0; i < 8; ++i) f[i] = rstd * (d[i] * g[i] - f[i] * coef);
+    if (in.resid) {
+      float r[8];
+      bf16x8_to_f32(in.resid[row * in.ldr + c], r);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) f[i] += r[i];
+    }
     dxr[c] = f32_to_bf16x8(f);
   }
 }
@@ -266,16 +307,29 @@ cudaError_t launch_row_start(int num_seqs, const int32_t* seq_len, const int32_t
                     seq_len, seq_row, row_start, max_rows);
 }
 
-cudaError_t launch_rmsnorm(bool bwd, int rows, int dim, const void* a, long long lda, const void* x, long long ldx,
-                           const void* w, float eps, void* out, long long ldo, cudaStream_t s) {
+cudaError_t launch_rmsnorm_fwd(int rows, int dim, const void* x, long long ldx, const void* res, long long ldr,
+                               void* xs, long long ldxs, const void* w, float eps, void* y, long long ldy,
+                               cudaStream_t s) {
   if (rows == 0) return cudaSuccess;
-  if (!bwd)
-    return launch_pdl(mux_rmsnorm_fwd_kernel, dim3(rows), dim3(kNormThreads), 0, s, dim,
-                      static_cast<const uint4*>(x), ldx / 8, static_cast<const uint4*>(w), eps,
-                      static_cast<uint4*>(out), ldo / 8);
-  return launch_pdl(mux_rmsnorm_bwd_kernel, dim3(rows), dim3(kNormThreads), 0, s, dim,
-                    static_cast<const uint4*>(a), lda / 8, static_cast<const uint4*>(x), ldx / 8,
-                    static_cast<const uint4*>(w), eps, static_cast<uint4*>(out), ldo / 8);
+  return launch_pdl(mux_rmsnorm_fwd_kernel, dim3(rows), dim3(kNormThreads), 0, s, dim, static_cast<const uint4*>(x),
+                    ldx / 8, static_cast<const uint4*>(res), ldr / 8, static_cast<uint4*>(xs), ldxs / 8,
+                    static_cast<const uint4*>(w), eps, static_cast<uint4*>(y), ldy / 8);
+}
+
+cudaError_t launch_rmsnorm_bwd(int rows, int dim, const void* const* dy, const long long* lddy, const void* resid,
+                               long long ldr, const void* x, long long ldx, const void* w, float eps, void* dx,
+                               long long lddx, cudaStream_t s) {
+  if (rows == 0) return cudaSuccess;
+  NormBwdIn in;
+  for (int k = 0; k < 3; ++k) {
+    in.dy[k] = static_cast<const uint4*>(dy[k]);
+    in.lddy[k] = lddy[k] / 8;
+  }
+  in.resid = static_cast<const uint4*>(resid);
+  in.ldr = ldr / 8;
+  return launch_pdl(mux_rmsnorm_bwd_kernel, dim3(rows), dim3(kNormThreads), 0, s, dim, in,
+                    static_cast<const uint4*>(x), ldx / 8, static_cast<const uint4*>(w), eps, static_cast<uint4*>(dx),
+                    lddx / 8);
 }
 
 cudaError_t launch_swiglu_fwd(int rows, int dim, const void* g, long long ldg, const void* u, long long ldu, void* h,

@@ -29,8 +29,12 @@ cudaError_t launch_pack_apply(int max_rows, int cols, int num_tokens, const int3
                               const __nv_bfloat16* src, __nv_bfloat16* dst, int num_sms, cudaStream_t stream);
 cudaError_t launch_row_start(int num_seqs, const int32_t* seq_len, const int32_t* seq_row, int max_rows,
                              int32_t* row_start, int num_sms, cudaStream_t s);
-cudaError_t launch_rmsnorm(bool bwd, int rows, int dim, const void* a, long long lda, const void* x, long long ldx,
-                           const void* w, float eps, void* out, long long ldo, cudaStream_t s);
+cudaError_t launch_rmsnorm_fwd(int rows, int dim, const void* x, long long ldx, const void* res, long long ldr,
+                               void* xs, long long ldxs, const void* w, float eps, void* y, long long ldy,
+                               cudaStream_t s);
+cudaError_t launch_rmsnorm_bwd(int rows, int dim, const void* const* dy, const long long* lddy, const void* resid,
+                               long long ldr, const void* x, long long ldx, const void* w, float eps, void* dx,
+                               long long lddx, cudaStream_t s);
 cudaError_t launch_swiglu_fwd(int rows, int dim, const void* g, long long ldg, const void* u, long long ldu, void* h,
                               long long ldh, int num_sms, cudaStream_t s);
 cudaError_t launch_swiglu_bwd(int rows, int dim, const void* dh, long long lddh, const void* g, long long ldg,
@@ -610,30 +614,37 @@ static mux_status ew_check(int32_t rows, int32_t dim) {
   return MUX_OK;
 }
 
-mux_status mux_rmsnorm_fwd(int32_t rows, int32_t dim, const mux_bf16* x, int64_t ldx, const mux_bf16* w, float eps,
-                           mux_bf16* y, int64_t ldy, cudaStream_t stream) {
+mux_status mux_rmsnorm_fwd(int32_t rows, int32_t dim, const mux_bf16* x, int64_t ldx, const mux_bf16* res,
+                           int64_t ldres, mux_bf16* xsum, int64_t ldxs, const mux_bf16* w, float eps, mux_bf16* y,
+                           int64_t ldy, cudaStream_t stream) {
   mux_status st = ew_check(rows, dim);
   if (st != MUX_OK || rows == 0) return st;
   if (!x || !w || !y) return fail(MUX_ERR_INVALID_ARGUMENT, "null pointer");
-  if (!aligned16(x) || !aligned16(w) || !aligned16(y) || !ld_ok(ldx, dim) || !ld_ok(ldy, dim))
+  if (!aligned16(x) || !aligned16(w) || !aligned16(y) || !ld_ok(ldx, dim) || !ld_ok(ldy, dim) ||
+      (res && (!aligned16(res) || !ld_ok(ldres, dim))) || (xsum && (!aligned16(xsum) || !ld_ok(ldxs, dim))))
     return fail(MUX_ERR_INVALID_ARGUMENT, "alignment/stride");
+  if (xsum && !res) return fail(MUX_ERR_INVALID_ARGUMENT, "xsum needs res");
   if (!(eps >= 0.f) || !std::isfinite(eps)) return fail(MUX_ERR_INVALID_ARGUMENT, "eps must be finite and >= 0");
-  cudaError_t e = launch_rmsnorm(false, rows, dim, nullptr, 0, x, ldx, w, eps, y, ldy, stream);
+  cudaError_t e = launch_rmsnorm_fwd(rows, dim, x, ldx, res, ldres, xsum, ldxs, w, eps, y, ldy, stream);
   if (e != cudaSuccess) return cuda_fail(e, "mux_rmsnorm_fwd launch");
   return MUX_OK;
 }
 
-mux_status mux_rmsnorm_bwd(int32_t rows, int32_t dim, const mux_bf16* dy, int64_t lddy, const mux_bf16* x,
-                           int64_t ldx, const mux_bf16* w, float eps, mux_bf16* dx, int64_t lddx,
-                           cudaStream_t stream) {
+mux_status mux_rmsnorm_bwd(int32_t rows, int32_t dim, const mux_bf16* dy, int64_t lddy, const mux_bf16* dy2,
+                           int64_t lddy2, const mux_bf16* dy3, int64_t lddy3, const mux_bf16* x, int64_t ldx,
+                           const mux_bf16* w, float eps, const mux_bf16* resid, int64_t ldres, mux_bf16* dx,
+                           int64_t lddx, cudaStream_t stream) {
   mux_status st = ew_check(rows, dim);
   if (st != MUX_OK || rows == 0) return st;
-  if (!dy || !x || !w || !dx) return fail(MUX_ERR_INVALID_ARGUMENT, "null pointer");
+  if (!dy || !x || !w || !dx || (dy3 && !dy2)) return fail(MUX_ERR_INVALID_ARGUMENT, "null pointer");
   if (!aligned16(dy) || !aligned16(x) || !aligned16(w) || !aligned16(dx) || !ld_ok(lddy, dim) || !ld_ok(ldx, dim) ||
-      !ld_ok(lddx, dim))
+      !ld_ok(lddx, dim) || (dy2 && (!aligned16(dy2) || !ld_ok(lddy2, dim))) ||
+      (dy3 && (!aligned16(dy3) || !ld_ok(lddy3, dim))) || (resid && (!aligned16(resid) || !ld_ok(ldres, dim))))
     return fail(MUX_ERR_INVALID_ARGUMENT, "alignment/stride");
   if (!(eps >= 0.f) || !std::isfinite(eps)) return fail(MUX_ERR_INVALID_ARGUMENT, "eps must be finite and >= 0");
-  cudaError_t e = launch_rmsnorm(true, rows, dim, dy, lddy, x, ldx, w, eps, dx, lddx, stream);
+  const void* dys[3] = {dy, dy2, dy3};
+  const long long lds[3] = {lddy, lddy2, lddy3};
+  cudaError_t e = launch_rmsnorm_bwd(rows, dim, dys, lds, resid, ldres, x, ldx, w, eps, dx, lddx, stream);
   if (e != cudaSuccess) return cuda_fail(e, "mux_rmsnorm_bwd launch");
   return MUX_OK;
 }

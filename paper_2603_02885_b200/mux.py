@@ -93,9 +93,9 @@ def lib():
         L.mux_rope.restype = ctypes.c_int
         L.mux_rope.argtypes = [I32, I32, I32, P, I64, P, F, I32, P]
         L.mux_rmsnorm_fwd.restype = ctypes.c_int
-        L.mux_rmsnorm_fwd.argtypes = [I32, I32, P, I64, P, F, P, I64, P]
+        L.mux_rmsnorm_fwd.argtypes = [I32, I32, P, I64, P, I64, P, I64, P, F, P, I64, P]
         L.mux_rmsnorm_bwd.restype = ctypes.c_int
-        L.mux_rmsnorm_bwd.argtypes = [I32, I32, P, I64, P, I64, P, F, P, I64, P]
+        L.mux_rmsnorm_bwd.argtypes = [I32, I32, P, I64, P, I64, P, I64, P, I64, P, F, P, I64, P, I64, P]
         L.mux_swiglu_fwd.restype = ctypes.c_int
         L.mux_swiglu_fwd.argtypes = [I32, I32, P, I64, P, I64, P, I64, P]
         L.mux_swiglu_bwd.restype = ctypes.c_int
@@ -346,19 +346,26 @@ def rope_(x, row_start_, heads: int, head_dim: int = 128, base: float = 10000.0,
     return x
 
 
-def rmsnorm_fwd(x, w, eps: float, y=None, stream=None):
+def rmsnorm_fwd(x, w, eps: float, y=None, res=None, xsum=None, stream=None):
+    """mux_rmsnorm_fwd: y = RMSNorm(x [+ res]) * w; with res, x + res is also written to xsum."""
     if y is None:
         y = torch.empty(x.shape[0], x.shape[1], dtype=torch.bfloat16, device=x.device)
-    _check(lib().mux_rmsnorm_fwd(x.shape[0], x.shape[1], _ptr(x), _ld(x), _ptr(w), eps, _ptr(y), _ld(y),
+    if res is not None and xsum is None:
+        xsum = torch.empty(x.shape[0], x.shape[1], dtype=torch.bfloat16, device=x.device)
+    _check(lib().mux_rmsnorm_fwd(x.shape[0], x.shape[1], _ptr(x), _ld(x), _ptr(res), _ld(res) if res is not None else 0,
+                                 _ptr(xsum), _ld(xsum) if xsum is not None else 0, _ptr(w), eps, _ptr(y), _ld(y),
                                  _stream(stream)))
-    return y
+    return y if res is None else (y, xsum)
 
 
-def rmsnorm_bwd(dy, x, w, eps: float, dx=None, stream=None):
+def rmsnorm_bwd(dy, x, w, eps: float, dx=None, dy2=None, dy3=None, resid=None, stream=None):
+    """mux_rmsnorm_bwd: dx = RMSNorm'(x)^T ((dy [+ dy2 [+ dy3]]) * w) [+ resid]."""
     if dx is None:
         dx = torch.empty(x.shape[0], x.shape[1], dtype=torch.bfloat16, device=x.device)
-    _check(lib().mux_rmsnorm_bwd(x.shape[0], x.shape[1], _ptr(dy), _ld(dy), _ptr(x), _ld(x), _ptr(w), eps,
-                                 _ptr(dx), _ld(dx), _stream(stream)))
+    ld = lambda t: _ld(t) if t is not None else 0  # noqa: E731
+    _check(lib().mux_rmsnorm_bwd(x.shape[0], x.shape[1], _ptr(dy), _ld(dy), _ptr(dy2), ld(dy2), _ptr(dy3), ld(dy3),
+                                 _ptr(x), _ld(x), _ptr(w), eps, _ptr(resid), ld(resid), _ptr(dx), _ld(dx),
+                                 _stream(stream)))
     return dx
 
 

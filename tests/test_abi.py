@@ -162,9 +162,14 @@ def test_elementwise_ops_reject(mux):
     assert L.mux_rope(16, 2, 10, A16, 64, A16, 10000.0, 0, None) == 1            # head_dim % 16
     assert L.mux_rope(16, 2, 64, A16, 64, A16, 10000.0, 0, None) == 1            # ld < heads * head_dim
     assert L.mux_rope(16, 2, 64, A16, 128, A16, 1.0, 0, None) == 1               # base <= 1
-    assert L.mux_rmsnorm_fwd(4, 12, A16, 16, A16, 1e-5, A16, 16, None) == 1      # dim % 8
-    assert L.mux_rmsnorm_fwd(4, 16, A16, 16, A16, -1.0, A16, 16, None) == 1      # eps < 0
-    assert L.mux_rmsnorm_bwd(4, 16, A16, 16, A16, 8, A16, 1e-5, A16, 16, None) == 1  # ldx < dim
+    assert L.mux_rmsnorm_fwd(4, 12, A16, 16, None, 0, None, 0, A16, 1e-5, A16, 16, None) == 1      # dim % 8
+    assert L.mux_rmsnorm_fwd(4, 16, A16, 16, None, 0, None, 0, A16, -1.0, A16, 16, None) == 1      # eps < 0
+    assert L.mux_rmsnorm_fwd(4, 16, A16, 16, None, 0, A16, 16, A16, 1e-5, A16, 16, None) == 1      # xsum w/o res
+    assert L.mux_rmsnorm_fwd(4, 16, A16, 16, A16 + 4, 16, A16, 16, A16, 1e-5, A16, 16, None) == 1  # res misaligned
+    assert L.mux_rmsnorm_bwd(4, 16, A16, 16, None, 0, None, 0, A16, 8, A16, 1e-5, None, 0, A16, 16,
+                             None) == 1                                                           # ldx < dim
+    assert L.mux_rmsnorm_bwd(4, 16, A16, 16, None, 0, A16, 16, A16, 16, A16, 1e-5, None, 0, A16, 16,
+                             None) == 1                                                           # dy3 w/o dy2
     assert L.mux_swiglu_fwd(4, 16, A16 + 2, 16, A16, 16, A16, 16, None) == 1    # misaligned
     assert L.mux_swiglu_bwd(4, 16, A16, 16, A16, 16, A16, 16, A16, 16, A16, 12, None) == 1
     assert L.mux_pack_row_start(-1, A16, A16, 16, A16, None) == 1

@@ -59,6 +59,18 @@ def test_rmsnorm(rows, dim):
     X, Wt, DY = bf16_to_f64(xb), bf16_to_f64(wb), bf16_to_f64(dyb)
     assert rel_err(_f64(y), ob.rmsnorm_fwd(X, Wt, 1e-5)) <= TOL
     assert rel_err(_f64(dx), ob.rmsnorm_bwd(DY, X, Wt, 1e-5)) <= TOL
+    # fused residual stream: xs = x + res (bf16, written), y = RMSNorm(xs); gradient sums + residual
+    rb = gen.normal_bf16(7, st.take(), (rows, dim), 1.0)
+    d2b, d3b, gb = (gen.normal_bf16(7, st.take(), (rows, dim), 1.0) for _ in range(3))
+    res, d2, d3, gres = to_dev_bf16(rb), to_dev_bf16(d2b), to_dev_bf16(d3b), to_dev_bf16(gb)
+    y2, xs = mux.rmsnorm_fwd(x, w, 1e-5, res=res)
+    dx2 = mux.rmsnorm_bwd(dy, xs, w, 1e-5, dy2=d2, dy3=d3, resid=gres)
+    torch.cuda.synchronize()
+    XS = X + bf16_to_f64(rb)
+    assert rel_err(_f64(xs), XS) <= TOL
+    assert rel_err(_f64(y2), ob.rmsnorm_fwd(XS, Wt, 1e-5)) <= TOL
+    ref = ob.rmsnorm_bwd(DY + bf16_to_f64(d2b) + bf16_to_f64(d3b), _f64(xs), Wt, 1e-5) + bf16_to_f64(gb)
+    assert rel_err(_f64(dx2), ref) <= TOL
 
 
 def test_swiglu_on_fused_gate_up():

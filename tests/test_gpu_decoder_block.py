@@ -154,7 +154,7 @@ def test_decoder_block_matches_oracle(kv_heads):
     dg_r, du_r = ob.swiglu_bwd(G("dm"), g, u)
     dh2g, _, sgrads["gate"] = linb("gate", G("dg"), h2)
     dh2u, _, sgrads["up"] = linb("up", G("du"), h2)
-    dx2_r = ob.rmsnorm_bwd(G("dh2"), x2, Wo["norm2"], shape.eps) + dYf
+    dx2_r = ob.rmsnorm_bwd(G("dh2") + G("dh2u"), x2, Wo["norm2"], shape.eps) + dYf
     da_r, _, sgrads["o"] = linb("o", G("dx2"), a_)
     dq_r, dk_r, dv_r = ob.attention_bwd(G("da").reshape(R, Hh, d), q.reshape(R, Hh, d),
                                         np.repeat(k.reshape(R, Hkv, d), rep, axis=1),
@@ -167,10 +167,11 @@ def test_decoder_block_matches_oracle(kv_heads):
     dh1k, _, sgrads["k"] = linb("k", G("dk"), h1)
     dh1v, _, sgrads["v"] = linb("v", G("dv"), h1)
     stage.update({
-        "dm": (G("dm"), dm_r), "dg": (G("dg"), dg_r), "du": (G("du"), du_r), "dh2": (G("dh2"), dh2g + dh2u),
+        "dm": (G("dm"), dm_r), "dg": (G("dg"), dg_r), "du": (G("du"), du_r), "dh2": (G("dh2"), dh2g), "dh2u": (G("dh2u"), dh2u),
         "dx2": (G("dx2"), dx2_r), "da": (G("da"), da_r), "dq": (G("dq"), dq_r), "dk": (G("dk"), dk_r),
-        "dv": (G("dv"), dv_r), "dh1": (G("dh1"), dh1q + dh1k + dh1v),
-        "dx": (f(from_dev_bf16(dx)), ob.rmsnorm_bwd(G("dh1"), xg, Wo["norm1"], shape.eps) + G("dx2")),
+        "dv": (G("dv"), dv_r), "dh1": (G("dh1"), dh1q), "dh1k": (G("dh1k"), dh1k), "dh1v": (G("dh1v"), dh1v),
+        "dx": (f(from_dev_bf16(dx)),
+               ob.rmsnorm_bwd(G("dh1") + G("dh1k") + G("dh1v"), xg, Wo["norm1"], shape.eps) + G("dx2")),
     })
     serr = {n: rel_err(gv[valid], rv[valid]) for n, (gv, rv) in stage.items()}
     for n in LINEARS:
