@@ -13,7 +13,7 @@
 //   TMEM: S 64 | dP 64 | dQ 128 columns.
 // dV and dK kernels (one template, two launches) — CTA = 128 key rows of one
 //   KV head (TMEM lanes = keys); query tiles of 64 of every q head of the
-//   group through a 2-stage TMA ring.  Per tile: S^T = K Q^T (and, for dK,
+//   group through a TMA ring (2 stages for dV, 1 for dK).  Per tile: S^T = K Q^T (and, for dK,
 //   dP^T = V dO^T) (M=128, N=64), one thread per key row forms P^T (dV) or
 //   dS^T (dK) in bf16 (K-major smem), then dV += P^T dO or dK += dS^T Q
 //   (M=128, N=128, K=64; dO, Q read MN-major).  Splitting dV from dK costs
@@ -294,14 +294,16 @@ __global__ void __launch_bounds__(kThreadsB, 2) mux_attn_dq_tc_kernel(const __gr
 
 // =========================================================================== dK, dV
 // smem: K 32 KB | [dK: V 32 KB] | P^T or dS^T 16 KB | Q 16 KB, dO 16 KB (one stage) | scalars | barriers
-constexpr int kQDStages = 1;  // <= 112 KB of smem: two CTAs per SM (they overlap each other's loads)
+// Q/dO ring depth: dV (no V tile) fits two stages in 112 KB, dK one; either way two CTAs share an SM
+template <bool kDK>
+constexpr int qd_stages() { return kDK ? 1 : 2; }
 template <bool kDK>
 __global__ void __launch_bounds__(kThreadsB, 2) mux_attn_dkdv_tc_kernel(const __grid_constant__ AttnBwdTcParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   if ((smem_u32(smem) & 1023u) != 0) __trap();
   constexpr uint32_t oK = 0, oV = 2 * kSub128, oT = (kDK ? 4 : 2) * kSub128, oQD = oT + kSub128;
   constexpr uint32_t kStage = 4 * kSub64;  // Q 16 KB + dO 16 KB
-  constexpr int kNS = kQDStages;
+  constexpr int kNS = qd_stages<kDK>();
   float* sc = reinterpret_cast<float*>(smem + oQD + kNS * kStage);  // [3][64]: lse2, D, row_start
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + oQD + kNS * kStage + 3 * 64 * 4);
   uint64_t* kv_full = bars + 0;
@@ -542,7 +544,7 @@ __global__ void __launch_bounds__(kThreadsB, 2) mux_attn_dkdv_tc_kernel(const __
 constexpr size_t kDqSmemTc = 5 * kSub128 + kDqStages * 4 * kSub64 + 256;
 template <bool kDK>
 constexpr size_t dkdv_smem() {
-  return ((kDK ? 4 : 2) + 1) * kSub128 + kQDStages * 4 * kSub64 + 3 * 64 * 4 + 256;  // dK: 115712 B = half an SM
+  return ((kDK ? 4 : 2) + 1) * kSub128 + qd_stages<kDK>() * 4 * kSub64 + 3 * 64 * 4 + 256;  // 115712 B = half an SM
 }
 
 cudaError_t launch_attn_bwd_pre(int R, int H, const void* dO, long long lddo, const void* o, long long ldo,
@@ -565,17 +567,17 @@ cudaError_t configure_dkdv() {
 }
 
 cudaError_t launch_attn_bwd_tc(const AttnBwdTcParams& p, cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
+  static std::atomic<uint64_t> configured{0};
+  cudaError_t ce = once_per_device(configured, [] {
     cudaError_t e = cudaFuncSetAttribute(mux_attn_dq_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(kDqSmemTc));
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(mux_attn_dq_tc_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e == cudaSuccess) e = configure_dkdv<false>();
     if (e == cudaSuccess) e = configure_dkdv<true>();
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+    return e;
+  });
+  if (ce != cudaSuccess) return ce;
   if (p.R == 0) return cudaSuccess;
   const dim3 gk((p.R + 127) / 128, p.Hkv);
   cudaError_t e = launch_pdl(mux_attn_dkdv_tc_kernel<false>, gk, dim3(kThreadsB), dkdv_smem<false>(), s, p);

@@ -301,15 +301,15 @@ __global__ void __launch_bounds__(kThreads, 2) mux_attn_fwd_tc_kernel(const __gr
 }
 
 cudaError_t launch_attn_fwd_tc(const AttnTcParams& p, cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
+  static std::atomic<uint64_t> configured{0};
+  cudaError_t ce = once_per_device(configured, [] {
     cudaError_t e = cudaFuncSetAttribute(mux_attn_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(kSmemBytes));
     if (e == cudaSuccess)  // the whole 228 KB as shared memory: two CTAs per SM
       e = cudaFuncSetAttribute(mux_attn_fwd_tc_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+    return e;
+  });
+  if (ce != cudaSuccess) return ce;
   if (p.R == 0) return cudaSuccess;
   return launch_pdl(mux_attn_fwd_tc_kernel, dim3((p.R + kT - 1) / kT, p.H), dim3(kThreads), kSmemBytes, s, p);
 }

@@ -36,6 +36,7 @@
 // (TMEM -> regs -> bf16 -> swizzled smem -> TMA store).  Two 256-column TMEM
 // accumulators: the epilogue of tile i overlaps the mainloop of tile i+1.
 #include "common.h"
+#include "launch.cuh"
 #include "ptx.cuh"
 
 namespace mux {
@@ -581,13 +582,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
 // ---------------------------------------------------------------- launchers
 template <bool kBwd>
 cudaError_t launch_gemm_impl(const GemmParams& p, int grid, cudaStream_t stream) {
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(mux_gemm_kernel<kBwd>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(GemmLayout<kBwd>::kSmemBytes));
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  static std::atomic<uint64_t> configured{0};
+  cudaError_t ce = once_per_device(configured, [] {
+    return cudaFuncSetAttribute(mux_gemm_kernel<kBwd>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(GemmLayout<kBwd>::kSmemBytes));
+  });
+  if (ce != cudaSuccess) return ce;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kGemmThreads);

@@ -16,6 +16,7 @@
 // sums tokens in ascending order.  Ranks < 16 still use the tensor cores
 // (zero-padded N = 64): the kernel is bound by streaming X/dY, not by MMA.
 #include "common.h"
+#include "launch.cuh"
 #include "ptx.cuh"
 
 namespace mux {
@@ -186,13 +187,12 @@ __global__ void __launch_bounds__(kGradThreads, 1) mux_grad_kernel(const __grid_
 }
 
 cudaError_t launch_grad(const GradParams& p, int grid, cudaStream_t stream) {
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(mux_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kGradSmemBytes));
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  static std::atomic<uint64_t> configured{0};
+  cudaError_t ce = once_per_device(configured, [] {
+    return cudaFuncSetAttribute(mux_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(kGradSmemBytes));
+  });
+  if (ce != cudaSuccess) return ce;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kGradThreads);

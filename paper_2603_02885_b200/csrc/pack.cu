@@ -14,6 +14,7 @@
 //   5. fill: chunk table with KV-reuse links, seq_row, row_src.
 // Integer results are bit-exact with the fp64 oracle's pack (tests/test_gpu_pack.py).
 #include "common.h"
+#include "launch.cuh"
 #include "ptx.cuh"
 
 namespace mux {
@@ -359,13 +360,11 @@ cudaError_t launch_pack(int M, int S, const int32_t* task_seq_off, const int32_t
                         int32_t* seg_off, int32_t* seq_row, int32_t* chunk_task, int32_t* chunk_pack,
                         int32_t* chunk_valid, int32_t* chunk_dep, int32_t* row_src, mux_pack_info* info,
                         void* workspace, cudaStream_t stream) {
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(mux_pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         kPackSmemMaxBytes);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  static std::atomic<uint64_t> configured{0};
+  cudaError_t ce = once_per_device(configured, [] {
+    return cudaFuncSetAttribute(mux_pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPackSmemMaxBytes);
+  });
+  if (ce != cudaSuccess) return ce;
   const size_t smem = pack_smem_bytes(M, S);
   const int use_smem = smem <= static_cast<size_t>(kPackSmemMaxBytes);
   cudaLaunchConfig_t cfg{};
