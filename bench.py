@@ -130,6 +130,11 @@ class MuxStep:
         self.dY3 = torch.empty(self.max_rows, w.linears[-1].N, dtype=torch.bfloat16, device=dev)
         self.launches_per_step = 1 + 2 + len(self.layers) + 2 * len(self.layers)
         self.fwd_events = None
+        # adapter gradients of layer l (HBM-bound) run on a side stream, in the tail of
+        # the dX GEMM of layer l-1 (tensor-bound; its PDL-launched CTAs claim the SMs first)
+        self.overlap_grads = True
+        self.side = torch.cuda.Stream()
+        self.gemm_done = [torch.cuda.Event() for _ in self.layers]
 
     def step(self, record=None, slot=0, before_bwd=None):
         mux, w = self.mux, self.w
@@ -155,11 +160,22 @@ class MuxStep:
             xin = self.X1 if li == 0 else self.layers[li - 1]["Y"]
             if record is not None:
                 record("bwd", li, 0)
-            mux.linear_bwd(seg_off, self.seg_task, ly["ads"], dy, xin, ly["W"], ly["Hs"], self.r_cap,
-                           dX=ly["dX"], workspace=ly["ws"])
+            if not self.overlap_grads:
+                mux.linear_bwd(seg_off, self.seg_task, ly["ads"], dy, xin, ly["W"], ly["Hs"], self.r_cap,
+                               dX=ly["dX"], workspace=ly["ws"])
+            else:
+                main = self.torch.cuda.current_stream()
+                mux.linear_bwd(seg_off, self.seg_task, ly["ads"], dy, xin, ly["W"], ly["Hs"], self.r_cap,
+                               dX=ly["dX"], workspace=ly["ws"], part=mux.BWD_DX)
+                self.gemm_done[li].record(main)
+                self.side.wait_event(self.gemm_done[li])
+                mux.linear_bwd(seg_off, self.seg_task, ly["ads"], dy, xin, ly["W"], ly["Hs"], self.r_cap,
+                               dX=ly["dX"], workspace=ly["ws"], part=mux.BWD_GRADS, stream=self.side)
             if record is not None:
                 record("bwd", li, 1)
             dy = ly["dX"]
+        if self.overlap_grads:
+            self.torch.cuda.current_stream().wait_stream(self.side)
 
 
 # ------------------------------------------------------------------ clocks
@@ -312,6 +328,7 @@ def main_arm(args):
 
     w = Workload(args.config, rank_seed=rank)
     ms = MuxStep(w, torch, mux)
+    ms.overlap_grads = not args.no_overlap_grads
     stream = torch.cuda.current_stream()
 
     for _ in range(args.warmup):
@@ -358,7 +375,11 @@ def main_arm(args):
     fwd_ms = sum(a.elapsed_time(b) for (_, a, b) in ev_pairs["fwd"])
     bwd_ms = sum(a.elapsed_time(b) for (_, a, b) in ev_pairs["bwd"])
     fwd_flops = sum((2 * L.K * L.N + 2 * max(w.wl.ranks) * (L.K + L.N)) * w.T for L in w.linears) * args.steps
-    bwd_flops = sum((2 * L.K * L.N + 4 * max(w.wl.ranks) * (L.K + L.N)) * w.T for L in w.linears) * args.steps
+    # the events bracket each layer's backward call on the main stream: with the adapter gradients
+    # overlapped on the side stream that is the dX GEMM (2KN + 2r(K+N) per token), else dX + gradients
+    r_ = max(w.wl.ranks)
+    bwd_flops = sum((2 * L.K * L.N + (2 if ms.overlap_grads else 4) * r_ * (L.K + L.N)) * w.T
+                    for L in w.linears) * args.steps
     pk = peaks()
     achieved = fwd_flops / (fwd_ms * 1e-3) / 1e12
     traffic, traffic_src = None, None
@@ -464,7 +485,9 @@ def main_arm(args):
                          "measured_sustained": tflops / pk["bf16_tflops_sustained"],
                          "datasheet_2250": tflops / 2250.0},
         "kernels": {"fwd_calls_ms_per_step": fwd_ms / args.steps, "bwd_calls_ms_per_step": bwd_ms / args.steps,
-                    "bwd_tflops": bwd_flops / (bwd_ms * 1e-3) / 1e12},
+                    "bwd_tflops": bwd_flops / (bwd_ms * 1e-3) / 1e12,
+                    "bwd_calls": "dX GEMM only (adapter gradients overlapped on a side stream)"
+                    if ms.overlap_grads else "dX GEMM + adapter gradients"},
         "roofline": roof,
         "clocks": clk,
         "gpu_launches": ms.launches_per_step * args.steps,
@@ -701,6 +724,8 @@ def main():
     ap.add_argument("--impl", default="mux", choices=["mux", "reference"])
     ap.add_argument("--config", default="2")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-overlap-grads", action="store_true",
+                    help="run each layer's adapter gradients on the main stream (no side-stream overlap)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-rows", type=int, default=4, help="rows per task per reference-arm step")

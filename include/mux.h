@@ -212,6 +212,22 @@ MUX_API mux_status mux_linear_bwd(int32_t num_segs, const int32_t* seg_off, cons
                           mux_bf16* dX,
                           void* workspace, size_t workspace_bytes, cudaStream_t stream);
 
+/* The two halves of mux_linear_bwd, for callers that overlap them on two
+ * streams (the HBM-bound adapter gradients of layer l run in the tail of the
+ * tensor-bound dX GEMM of layer l-1):
+ *   MUX_BWD_DX     the fused GEMM: Gs into the workspace and dX (dX may be NULL)
+ *   MUX_BWD_GRADS  dA_t, dB_t from X, dY, Hs and the Gs that MUX_BWD_DX left in
+ *                  the SAME workspace; must run after it (stream order or an
+ *                  event), and nothing may reuse that workspace in between.
+ * Arguments as mux_linear_bwd; part 1 + part 2 == mux_linear_bwd bit for bit. */
+#define MUX_BWD_DX 1
+#define MUX_BWD_GRADS 2
+MUX_API mux_status mux_linear_bwd_part(int32_t part, int32_t num_segs, const int32_t* seg_off,
+                                       const int32_t* seg_task, int32_t num_adapters, const mux_adapter* adapters,
+                                       int32_t max_rows, int32_t K, int32_t N, int32_t r_cap, const mux_bf16* dY,
+                                       const mux_bf16* X, const mux_bf16* W, const mux_bf16* Hs, mux_bf16* dX,
+                                       void* workspace, size_t workspace_bytes, cudaStream_t stream);
+
 /* ---------------------------------------------------------------------------
  * Decoder-block ops (NEXT-3).  Row-major bf16 matrices with an explicit row
  * stride `ld*` in ELEMENTS (a multiple of 8: 16-byte rows), so q/k/v or

@@ -334,7 +334,7 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
                                 int32_t N, int32_t r_cap, const __nv_bfloat16* a_in /*X or dY*/,
                                 const __nv_bfloat16* X, const __nv_bfloat16* W, __nv_bfloat16* out /*Y or dX*/,
                                 const __nv_bfloat16* Hs_in, __nv_bfloat16* Hs_out, void* workspace,
-                                size_t workspace_bytes, cudaStream_t stream) {
+                                size_t workspace_bytes, cudaStream_t stream, int parts = 3) {
   mux_status st = validate_linear(num_segs, seg_off, seg_task, num_adapters, adapters, max_rows, K, N, r_cap);
   if (st != MUX_OK) return st;
   if (!a_in || !W) return fail(MUX_ERR_INVALID_ARGUMENT, "null input pointer");
@@ -406,10 +406,13 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
   // one CTA pair (cluster of 2) per tile in flight; grid = #SMs rounded to pairs
   const long long pairs = std::min<long long>(tiles_max, num_sms() / 2);
   const int grid = static_cast<int>(2 * std::max<long long>(pairs, 1));
-  cudaError_t e = launch_gemm(p, bwd, grid, stream);
-  if (e != cudaSuccess) return cuda_fail(e, bwd ? "mux_linear_bwd dX launch" : "mux_linear_fwd launch");
+  cudaError_t e = cudaSuccess;
+  if (parts & 1) {
+    e = launch_gemm(p, bwd, grid, stream);
+    if (e != cudaSuccess) return cuda_fail(e, bwd ? "mux_linear_bwd dX launch" : "mux_linear_fwd launch");
+  }
 
-  if (bwd) {
+  if (bwd && (parts & 2)) {
     static thread_local GradParams g;
     std::memset(&g, 0, sizeof(g));
     if (!make_map(&g.map_x, X, K, max_rows, K, 64, 128) || !make_map(&g.map_dy, a_in, N, max_rows, N, 64, 128) ||
@@ -477,6 +480,20 @@ mux_status mux_linear_bwd(int32_t num_segs, const int32_t* seg_off, const int32_
   auto dX = reinterpret_cast<__nv_bfloat16*>(dX_);
   return linear_common(true, num_segs, seg_off, seg_task, num_adapters, adapters, max_rows, K, N, r_cap, dY, X, W,
                        dX, Hs, nullptr, workspace, workspace_bytes, stream);
+}
+
+mux_status mux_linear_bwd_part(int32_t part, int32_t num_segs, const int32_t* seg_off, const int32_t* seg_task,
+                               int32_t num_adapters, const mux_adapter* adapters, int32_t max_rows, int32_t K,
+                               int32_t N, int32_t r_cap, const mux_bf16* dY_, const mux_bf16* X_, const mux_bf16* W_,
+                               const mux_bf16* Hs_, mux_bf16* dX_, void* workspace, size_t workspace_bytes,
+                               cudaStream_t stream) {
+  if (part != MUX_BWD_DX && part != MUX_BWD_GRADS)
+    return fail(MUX_ERR_INVALID_ARGUMENT, "part=%d must be MUX_BWD_DX (1) or MUX_BWD_GRADS (2)", part);
+  return linear_common(true, num_segs, seg_off, seg_task, num_adapters, adapters, max_rows, K, N, r_cap,
+                       reinterpret_cast<const __nv_bfloat16*>(dY_), reinterpret_cast<const __nv_bfloat16*>(X_),
+                       reinterpret_cast<const __nv_bfloat16*>(W_), reinterpret_cast<__nv_bfloat16*>(dX_),
+                       reinterpret_cast<const __nv_bfloat16*>(Hs_), nullptr, workspace, workspace_bytes, stream,
+                       part);
 }
 
 #ifdef MUX_PROFILE

@@ -24,9 +24,11 @@ STATUS = {0: "MUX_OK", 1: "MUX_ERR_INVALID_ARGUMENT", 2: "MUX_ERR_UNSUPPORTED",
 MAX_SEGMENTS = 64
 MAX_ADAPTERS = 64
 
+BWD_DX, BWD_GRADS = 1, 2
+
 EXPORTS = ("mux_last_error", "mux_version", "mux_pack_bound_rows", "mux_pack_workspace_size",
            "mux_pack_chunks", "mux_pack_apply", "mux_linear_workspace_size", "mux_linear_fwd",
-           "mux_linear_bwd", "mux_pack_row_start", "mux_attn_fwd", "mux_attn_workspace_size", "mux_attn_bwd",
+           "mux_linear_bwd", "mux_linear_bwd_part", "mux_pack_row_start", "mux_attn_fwd", "mux_attn_workspace_size", "mux_attn_bwd",
            "mux_rope", "mux_rmsnorm_fwd", "mux_rmsnorm_bwd", "mux_swiglu_fwd", "mux_swiglu_bwd", "mux_add")
 
 
@@ -80,6 +82,8 @@ def lib():
         L.mux_linear_fwd.argtypes = [I32, P, P, I32, P, I32, I32, I32, I32, P, P, P, P, P, SZ, P]
         L.mux_linear_bwd.restype = ctypes.c_int
         L.mux_linear_bwd.argtypes = [I32, P, P, I32, P, I32, I32, I32, I32, P, P, P, P, P, P, SZ, P]
+        L.mux_linear_bwd_part.restype = ctypes.c_int
+        L.mux_linear_bwd_part.argtypes = [I32, I32, P, P, I32, P, I32, I32, I32, I32, P, P, P, P, P, P, SZ, P]
         F = ctypes.c_float
         L.mux_pack_row_start.restype = ctypes.c_int
         L.mux_pack_row_start.argtypes = [I32, P, P, I32, P, P]
@@ -261,8 +265,11 @@ def linear_fwd(seg_off: torch.Tensor, seg_task: Sequence[int], adapters: Sequenc
 
 def linear_bwd(seg_off: torch.Tensor, seg_task: Sequence[int], adapters: Sequence[Adapter],
                dY: torch.Tensor, X: torch.Tensor, W: torch.Tensor, Hs: torch.Tensor, r_cap: int,
-               dX: torch.Tensor = None, want_dx: bool = True, workspace: torch.Tensor = None, stream=None):
-    """mux_linear_bwd.  Writes adapters[i].dA / .dB (allocated if None); returns dX."""
+               dX: torch.Tensor = None, want_dx: bool = True, workspace: torch.Tensor = None, stream=None,
+               part: int = 0):
+    """mux_linear_bwd (part 0), or one half of it: part 1 = the dX GEMM (and Gs), part 2 = the
+    adapter gradients (after part 1, same workspace).  Writes adapters[i].dA / .dB (allocated
+    if None); returns dX."""
     max_rows, K = X.shape
     N = W.shape[0]
     dev = X.device
@@ -279,9 +286,14 @@ def linear_bwd(seg_off: torch.Tensor, seg_task: Sequence[int], adapters: Sequenc
         workspace = torch.zeros(linear_workspace_size(S, max_rows, K, N, r_cap), dtype=torch.uint8, device=dev)
     tab = _adapter_table(adapters, True)
     st = _i32_host(seg_task)
-    _check(lib().mux_linear_bwd(S, _ptr(seg_off), st, len(adapters), tab, max_rows, K, N, r_cap,
-                                _ptr(dY), _ptr(X), _ptr(W), _ptr(Hs), _ptr(dX), _ptr(workspace),
-                                workspace.numel(), _stream(stream)))
+    if part == 0:
+        _check(lib().mux_linear_bwd(S, _ptr(seg_off), st, len(adapters), tab, max_rows, K, N, r_cap,
+                                    _ptr(dY), _ptr(X), _ptr(W), _ptr(Hs), _ptr(dX), _ptr(workspace),
+                                    workspace.numel(), _stream(stream)))
+    else:
+        _check(lib().mux_linear_bwd_part(part, S, _ptr(seg_off), st, len(adapters), tab, max_rows, K, N, r_cap,
+                                         _ptr(dY), _ptr(X), _ptr(W), _ptr(Hs), _ptr(dX), _ptr(workspace),
+                                         workspace.numel(), _stream(stream)))
     return dX
 
 

@@ -105,3 +105,45 @@ def test_config2_linears_sampled(K, N):
                                      rng.integers(0, p.R, 48)])).astype(np.int64)
     errs = _run(p, rows=rows)
     print(errs)
+
+
+def test_bwd_parts_overlapped_equal_combined():
+    """mux_linear_bwd_part: the dX GEMM on one stream and the adapter gradients on a
+    second stream (after an event) == mux_linear_bwd, bit for bit."""
+    import torch
+    from paper_2603_02885_b200 import mux
+    g = torch.Generator(device="cuda").manual_seed(5)
+    R, K, N = 1024, 512, 768
+    seg_off = torch.tensor([0, 256, 640, 1024], dtype=torch.int32, device="cuda")
+    st = [0, 1, 2]
+    ranks = [16, 4, 32]
+    W = (torch.randn(N, K, device="cuda", generator=g) / K ** 0.5).bfloat16()
+    X = torch.randn(R, K, device="cuda", generator=g).bfloat16()
+    dY = torch.randn(R, N, device="cuda", generator=g).bfloat16()
+
+    def adapters():
+        out = []
+        gg = torch.Generator(device="cuda").manual_seed(9)
+        for r in ranks:
+            B = mux.make_B_storage(N, r)
+            B.copy_(torch.randn(N, r, device="cuda", generator=gg).bfloat16())
+            out.append(mux.Adapter((torch.randn(r, K, device="cuda", generator=gg) / K ** 0.5).bfloat16(), B, r, 2.0))
+        return out
+
+    a1, a2 = adapters(), adapters()
+    _, Hs = mux.linear_fwd(seg_off, st, a1, X, W, 32)
+    dX1 = mux.linear_bwd(seg_off, st, a1, dY, X, W, Hs, 32)
+    ws = torch.zeros(mux.linear_workspace_size(3, R, K, N, 32), dtype=torch.uint8, device="cuda")
+    side = torch.cuda.Stream()
+    ev = torch.cuda.Event()
+    dX2 = mux.linear_bwd(seg_off, st, a2, dY, X, W, Hs, 32, workspace=ws, part=mux.BWD_DX)
+    ev.record()
+    side.wait_event(ev)
+    mux.linear_bwd(seg_off, st, a2, dY, X, W, Hs, 32, dX=dX2, workspace=ws, part=mux.BWD_GRADS, stream=side)
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+    assert torch.equal(dX1.view(torch.int16), dX2.view(torch.int16))
+    for x, y in zip(a1, a2):
+        assert torch.equal(x.dA, y.dA) and torch.equal(x.dB, y.dB)
+    with pytest.raises(mux.MuxError):
+        mux.linear_bwd(seg_off, st, a2, dY, X, W, Hs, 32, dX=dX2, workspace=ws, part=3)
