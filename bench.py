@@ -529,8 +529,19 @@ def tp_arm(args):
     w = Workload(args.config)
     h = w.host_tensors()
     i32 = dict(dtype=torch.int32, device="cuda")
-    g = max(1, min(args.htasks, w.M))
-    groups = [list(range(w.M))[i * w.M // g:(i + 1) * w.M // g] for i in range(g)]
+    plan_note = None
+    if args.htasks == 0:
+        # NEXT-4 feeding NEXT-1: the planner's Eq. 6 fusion over the measured operator profile
+        from paper_2603_02885_b200 import planner
+        prof = planner.load_profile(os.path.join(ROOT, "profiles", "r01_op_profile.json"))
+        L = planner.htask_latency([planner.stage_from_profile(prof, n_gpus=world)], C=1)
+        tasks_ = [planner.Task(str(t), int(w.wl.task_lens[t].sum()), w.wl.ranks[t]) for t in range(w.M)]
+        plan = planner.fuse_tasks(tasks_, L, S=1)
+        groups = [[int(t.name) for t in h] for h in plan.htasks]
+        plan_note = {"planner_cost_ms": plan.cost, "groups": groups}
+    else:
+        g = max(1, min(args.htasks, w.M))
+        groups = [list(range(w.M))[i * w.M // g:(i + 1) * w.M // g] for i in range(g)]
     r_cap = 16 * -(-max(w.wl.ranks) // 16)
     kinds = ["col", "row", "col"]
     mk = lambda A, B, r, sc: mux.Adapter(A, B, r, sc)  # noqa: E731
@@ -571,7 +582,7 @@ def tp_arm(args):
               "tso": torch.tensor(off, **i32),
               "sl": torch.tensor(np.concatenate(lens).astype(np.int32), **i32),
               "cap": torch.tensor([w.cap[t] for t in tasks], **i32) if w.cap else None,
-              "X1tok": X1tok_all[int(tok_off[tasks[0]]):int(tok_off[tasks[-1] + 1])],
+              "X1tok": torch.cat([X1tok_all[int(tok_off[t]):int(tok_off[t + 1])] for t in tasks]).contiguous(),
               "x_rows": torch.empty(rows, w.linears[0].K, dtype=torch.bfloat16, device="cuda"),
               "dY": torch.randn(max_rows, nl, device="cuda",
                                 generator=torch.Generator(device="cuda").manual_seed(rank + 7 * hi)).bfloat16()}
@@ -615,7 +626,7 @@ def tp_arm(args):
                                                     "AG/RS over NCCL)", "valid_tokens": w.T,
                                      "htasks": [ht["tasks"] for ht in htasks],
                                      "schedule": [f"h{sg.htask}.{sg.index}" for sg, _ in schedule],
-                                     "nccl_max_ctas": args.comm_ctas or None,
+                                     "nccl_max_ctas": args.comm_ctas or None, "planner": plan_note,
                                      "max_rows": [ht["max_rows"] for ht in htasks]},
                           "tflops_per_gpu_algorithmic": w.flops / (ms * 1e-3) / 1e12 / world}), flush=True)
     dist.destroy_process_group()
@@ -731,7 +742,8 @@ def main():
     ap.add_argument("--ref-rows", type=int, default=4, help="rows per task per reference-arm step")
     ap.add_argument("--mode", default="replicas", choices=["replicas", "tp", "block"],
                     help="N>1: task-sharded replicas (default, weak scaling) or tensor parallel (strong)")
-    ap.add_argument("--htasks", type=int, default=1, help="--mode tp: hTasks interleaved by Alg. 1 (NEXT-1)")
+    ap.add_argument("--htasks", type=int, default=1,
+                    help="--mode tp: hTasks interleaved by Alg. 1 (NEXT-1); 0 = chosen by the planner (NEXT-4)")
     ap.add_argument("--comm-ctas", type=int, default=0, help="--mode tp: NCCL_MAX_CTAS for the overlapped collectives")
     args = ap.parse_args()
     if args.warmup < 3:
