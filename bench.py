@@ -562,7 +562,9 @@ def tp_arm(args):
         T_h = int(sum(int(x.sum()) for x in lens))
         S_h = int(off[-1])
         bound = int(mux.pack_bound_rows(T_h, S_h, 64))
-        max_rows = -(-bound // (64 * world)) * 64 * world       # row blocks split evenly over ranks
+        # row blocks split evenly over ranks (256-row blocks for the fused reduce-scatter)
+        blk = 256 if args.fused_rs else 64
+        max_rows = -(-bound // (blk * world)) * blk * world
         pk = mux.alloc_pack_outputs(len(tasks), S_h, max_rows, max_rows // 64)
         be = tp.MuxBackend()
         layers = []
@@ -575,7 +577,7 @@ def tp_arm(args):
             shard = tp.shard_column if kinds[li] == "col" else tp.shard_row
             _, ap_ = shard(torch.empty(L.N, L.K, dtype=torch.bfloat16, device="meta"), ads, world, rank, mk)
             cls = tp.ColumnParallelMuxLinear if kinds[li] == "col" else tp.RowParallelMuxLinear
-            layers.append(cls(be, Wsh[li], ap_, r_cap))
+            layers.append(cls(be, Wsh[li], ap_, r_cap, fused_rs=args.fused_rs))
         rows = max_rows // world
         nl = w.linears[-1].N // world
         ht = {"tasks": tasks, "T": T_h, "max_rows": max_rows, "rows": rows, "pk": pk, "layers": layers,
@@ -627,6 +629,8 @@ def tp_arm(args):
                                      "htasks": [ht["tasks"] for ht in htasks],
                                      "schedule": [f"h{sg.htask}.{sg.index}" for sg, _ in schedule],
                                      "nccl_max_ctas": args.comm_ctas or None, "planner": plan_note,
+                                     "reduce_scatter": "fused into the GEMM epilogue (peer stores)" if args.fused_rs
+                                     else "NCCL",
                                      "max_rows": [ht["max_rows"] for ht in htasks]},
                           "tflops_per_gpu_algorithmic": w.flops / (ms * 1e-3) / 1e12 / world}), flush=True)
     dist.destroy_process_group()
@@ -745,6 +749,8 @@ def main():
     ap.add_argument("--htasks", type=int, default=1,
                     help="--mode tp: hTasks interleaved by Alg. 1 (NEXT-1); 0 = chosen by the planner (NEXT-4)")
     ap.add_argument("--comm-ctas", type=int, default=0, help="--mode tp: NCCL_MAX_CTAS for the overlapped collectives")
+    ap.add_argument("--fused-rs", action="store_true",
+                    help="--mode tp: reduce-scatters fused into the GEMMs (peer stores via symmetric memory)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

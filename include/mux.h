@@ -68,6 +68,7 @@ typedef uint16_t mux_bf16;
 
 #define MUX_MAX_SEGMENTS 64   /* per linear call (kernel parameter block <= 32 KB) */
 #define MUX_MAX_ADAPTERS 64
+#define MUX_RS_MAX_WORLD 8    /* ranks of a fused reduce-scatter (one 8-GPU NVSwitch box) */
 #define MUX_MAX_RANK 64        /* LoRA ranks up to 64 in the paper's workloads */
 
 typedef enum {
@@ -227,6 +228,50 @@ MUX_API mux_status mux_linear_bwd_part(int32_t part, int32_t num_segs, const int
                                        int32_t max_rows, int32_t K, int32_t N, int32_t r_cap, const mux_bf16* dY,
                                        const mux_bf16* X, const mux_bf16* W, const mux_bf16* Hs, mux_bf16* dX,
                                        void* workspace, size_t workspace_bytes, cudaStream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * Fused GEMM -> reduce-scatter for tensor parallelism (NEXT-1:
+ * the row-parallel forward Y = sum_p X_p W_p^T and the column-parallel dX =
+ * sum_p dY_p W_p both end in a reduce-scatter over rows).  Instead of writing
+ * a local partial and calling a collective, the fused GEMM's epilogue stores
+ * every output tile straight into the receive slot of the rank that owns the
+ * tile's rows (peer memory over NVLink), tile by tile as the GEMM runs;
+ * mux_rs_reduce on the owner then sums the `world` slots.  Rows are owned in
+ * contiguous blocks of rows_per_rank (a multiple of 256; world *
+ * rows_per_rank == max_rows).  Each rank allocates, once, a receive buffer of
+ * world * rows_per_rank * cols bf16 and a flag block of mux_rs_flags_elems()
+ * zeroed uint64, and every rank gets all ranks' pointers (e.g. by CUDA IPC or
+ * symmetric memory).  seq numbers the calls (1, 2, ...) and is the same on
+ * all ranks: a GEMM waits until every owner has reduced call seq - 1 before
+ * overwriting its slot, and publishes call seq when its last tile landed;
+ * mux_rs_reduce waits for all sources' call seq, then acknowledges.  Both are
+ * stream-ordered (no host synchronisation).
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  int32_t world;                                  /* 1 .. MUX_RS_MAX_WORLD */
+  int32_t rank;                                   /* this rank */
+  int32_t rows_per_rank;                          /* multiple of 256 */
+  uint64_t seq;                                   /* > 0, increasing per call */
+  mux_bf16* recv[MUX_RS_MAX_WORLD];               /* rank d's receive buffer [world][rows_per_rank][cols] */
+  unsigned long long* flags[MUX_RS_MAX_WORLD];    /* rank d's flag block [mux_rs_flags_elems(world)] */
+} mux_rs;
+MUX_API size_t mux_rs_flags_elems(int32_t world);
+/* forward of a row-parallel layer: mux_linear_fwd with Y replaced by the fused reduce-scatter */
+MUX_API mux_status mux_linear_fwd_rs(int32_t num_segs, const int32_t* seg_off, const int32_t* seg_task,
+                                     int32_t num_adapters, const mux_adapter* adapters, int32_t max_rows,
+                                     int32_t K, int32_t N, int32_t r_cap, const mux_bf16* X, const mux_bf16* W,
+                                     mux_bf16* Hs, const mux_rs* rs, void* workspace, size_t workspace_bytes,
+                                     cudaStream_t stream);
+/* dX GEMM of a column-parallel layer (mux_linear_bwd_part(MUX_BWD_DX) with dX reduce-scattered);
+ * the adapter gradients follow with mux_linear_bwd_part(MUX_BWD_GRADS) on the same workspace */
+MUX_API mux_status mux_linear_bwd_dx_rs(int32_t num_segs, const int32_t* seg_off, const int32_t* seg_task,
+                                        int32_t num_adapters, const mux_adapter* adapters, int32_t max_rows,
+                                        int32_t K, int32_t N, int32_t r_cap, const mux_bf16* dY,
+                                        const mux_bf16* X, const mux_bf16* W, const mux_bf16* Hs,
+                                        const mux_rs* rs, void* workspace, size_t workspace_bytes,
+                                        cudaStream_t stream);
+/* owner side: out[rows_per_rank, cols] = sum over sources of their slots (fp32, ascending source order) */
+MUX_API mux_status mux_rs_reduce(const mux_rs* rs, int32_t cols, mux_bf16* out, int64_t ldo, cudaStream_t stream);
 
 /* ---------------------------------------------------------------------------
  * Decoder-block ops (NEXT-3).  Row-major bf16 matrices with an explicit row

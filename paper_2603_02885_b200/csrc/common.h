@@ -55,6 +55,18 @@ struct GemmParams {
   int32_t has_main;              // 0: only the shrink (side) tiles
   int32_t group_m;               // raster band: pair row-blocks sharing a sweep over W tiles
   unsigned long long* dbg;       // MUX_PROFILE builds only: wait-cycle counters (see gemm.cu)
+  // Fused reduce-scatter output (tensor parallel, mux_linear_*_rs): rs_world > 0 sends each
+  // output tile straight to the rank that owns its rows (rs_rows per rank, contiguous blocks):
+  // map_out_rs[d] = rank d's receive slot for this rank ([rs_rows, nout], box {64, 32}).
+  // Handshake (all values = the call's sequence number rs_seq): before its first store the
+  // epilogue waits rs_ack[d] >= rs_seq - 1 (rank d reduced the previous call); after the last
+  // store the last CTA sets rs_ready[d] = rs_seq on every rank d.
+  int32_t rs_world;
+  int32_t rs_rows;
+  unsigned long long rs_seq;
+  const unsigned long long* rs_ack;          // this rank's ack flags [rs_world] (written by the dests)
+  unsigned long long* rs_ready[MUX_RS_MAX_WORLD];  // rank d's ready flag for this source (peer)
+  CUtensorMap map_out_rs[MUX_RS_MAX_WORLD];
   int32_t seg_adapter[MUX_MAX_SEGMENTS];
   int32_t seg_rank[MUX_MAX_SEGMENTS];
   float seg_scale[MUX_MAX_SEGMENTS];
@@ -112,6 +124,17 @@ struct AttnBwdTcParams {
   long long lddv;
   int R, H, Hkv;
   float scale_log2, scale;
+};
+
+// ---- receive side of the fused GEMM -> reduce-scatter (rs.cu)
+struct RsReduceParams {
+  int world, rank, rows, cols;
+  unsigned long long seq;
+  const uint4* recv;                      // this rank's receive buffer [world][rows][cols]
+  unsigned long long* flags;              // this rank's flag block
+  unsigned long long* ack[MUX_RS_MAX_WORLD];  // rank s's ack slot for this rank (peer)
+  uint4* out;                             // [rows, cols], row stride ldo8 * 8 elements
+  long long ldo8;
 };
 
 }  // namespace mux

@@ -452,6 +452,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   } else if (warp >= 4) {
     // =========================== epilogue (both CTAs) ===================
     const int q = warp & 3;  // TMEM lane quadrant = this CTA's rows 32q .. 32q+31
+    if (p.rs_world > 0 && p.has_main) {
+      // fused reduce-scatter: every destination rank must have consumed the previous call's
+      // partials from its receive slot before this call overwrites them
+      if (lane == 0) {
+        for (int d = 0; d < p.rs_world; ++d) {
+          const unsigned long long* f = p.rs_ack + d;
+          if (ld_acquire_sys_u64(f) + 1ull < p.rs_seq) {
+            const uint64_t t0 = globaltimer_ns();
+            while (ld_acquire_sys_u64(f) + 1ull < p.rs_seq)
+              if (globaltimer_ns() - t0 > kWatchdogNs) __trap();
+          }
+        }
+      }
+      __syncwarp();
+    }
     int acc = 0;
     uint32_t acc_phase = 0;
     uint8_t* bufs = epi + q * 2 * kEpiBuf;
@@ -533,7 +548,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           __syncwarp();
           if (lane == 0) {
             const int col = col_t + c * 64;
-            if (valid && col < p.nout) tma_store_2d(&p.map_out, buf, col, row_w);
+            if (valid && col < p.nout) {
+              if (p.rs_world > 0) {  // the rows' owner rank receives this partial tile
+                const int owner = row_w / p.rs_rows;
+                tma_store_2d(&p.map_out_rs[owner], buf, col, row_w - owner * p.rs_rows);
+              } else {
+                tma_store_2d(&p.map_out, buf, col, row_w);
+              }
+            }
             tma_store_commit();
           }
           buf_sel ^= 1;
@@ -541,7 +563,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       }
       if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
     }
-    if (lane == 0) tma_store_wait<0>();
+    if (lane == 0) {
+      tma_store_wait<0>();
+      if (p.rs_world > 0) fence_async_global();  // bulk stores -> generic-proxy release below
+    }
   }
 #ifdef MUX_PROFILE
   {
@@ -569,12 +594,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     tmem_dealloc_pair<kTmemCols>(tmem_base);
   }
   if (threadIdx.x == 0) {
-    // the last CTA out advances the workspace epoch for the next launch
-    __threadfence();
+    // the last CTA out advances the workspace epoch for the next launch (and, for a fused
+    // reduce-scatter, tells every destination rank that this rank's partials have landed)
+    if (p.rs_world > 0) __threadfence_system();
+    else __threadfence();
     if (atomicAdd(p.done, 1u) == gridDim.x - 1) {
       *p.done = 0u;
       *reinterpret_cast<volatile unsigned long long*>(p.epoch) = epoch;
-      __threadfence();
+      __threadfence_system();
+      for (int d = 0; d < p.rs_world; ++d) st_release_sys_u64(p.rs_ready[d], p.rs_seq);
     }
   }
 }

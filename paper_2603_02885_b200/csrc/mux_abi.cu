@@ -45,6 +45,7 @@ cudaError_t launch_rope(int rows, int heads, int d, void* x, long long ld, const
 cudaError_t launch_add(int rows, int dim, const void* a, long long lda, const void* b, long long ldb, void* y,
                        long long ldy, int num_sms, cudaStream_t s);
 cudaError_t launch_attn_fwd_tc(const AttnTcParams& p, cudaStream_t s);
+cudaError_t launch_rs_reduce(const RsReduceParams& p, int num_sms, cudaStream_t s);
 cudaError_t launch_attn_bwd_pre(int R, int H, const void* dO, long long lddo, const void* o, long long ldo,
                                 float* D, cudaStream_t s);
 cudaError_t launch_attn_bwd_tc(const AttnBwdTcParams& p, cudaStream_t s);
@@ -334,7 +335,8 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
                                 int32_t N, int32_t r_cap, const __nv_bfloat16* a_in /*X or dY*/,
                                 const __nv_bfloat16* X, const __nv_bfloat16* W, __nv_bfloat16* out /*Y or dX*/,
                                 const __nv_bfloat16* Hs_in, __nv_bfloat16* Hs_out, void* workspace,
-                                size_t workspace_bytes, cudaStream_t stream, int parts = 3) {
+                                size_t workspace_bytes, cudaStream_t stream, int parts = 3,
+                                const mux_rs* rs = nullptr) {
   mux_status st = validate_linear(num_segs, seg_off, seg_task, num_adapters, adapters, max_rows, K, N, r_cap);
   if (st != MUX_OK) return st;
   if (!a_in || !W) return fail(MUX_ERR_INVALID_ARGUMENT, "null input pointer");
@@ -342,7 +344,7 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
       (Hs_in && !aligned16(Hs_in)) || (Hs_out && !aligned16(Hs_out)))
     return fail(MUX_ERR_INVALID_ARGUMENT, "tensor pointers must be 16-byte aligned");
   if (bwd && (!X || !Hs_in)) return fail(MUX_ERR_INVALID_ARGUMENT, "bwd needs X and Hs");
-  if (!bwd && !out) return fail(MUX_ERR_INVALID_ARGUMENT, "fwd needs Y");
+  if (!bwd && !out && !rs) return fail(MUX_ERR_INVALID_ARGUMENT, "fwd needs Y");
   const LinearWs need = carve_linear_ws(nullptr, max_rows, r_cap);
   if (!workspace || workspace_bytes < need.bytes)
     return fail(MUX_ERR_INSUFFICIENT_BUFFER, "linear workspace %zu < %zu bytes", workspace_bytes, need.bytes);
@@ -380,7 +382,29 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
   p.kred = kred;
   p.nout = nout;
   p.r_cap = r_cap;
-  p.has_main = out != nullptr;
+  p.has_main = out != nullptr || rs != nullptr;
+  if (rs) {
+    if (rs->world < 1 || rs->world > MUX_RS_MAX_WORLD || rs->rank < 0 || rs->rank >= rs->world)
+      return fail(MUX_ERR_INVALID_ARGUMENT, "rs: world=%d rank=%d", rs->world, rs->rank);
+    if (rs->rows_per_rank <= 0 || rs->rows_per_rank % kPairRows ||
+        static_cast<long long>(rs->rows_per_rank) * rs->world != max_rows)
+      return fail(MUX_ERR_INVALID_ARGUMENT, "rs: rows_per_rank=%d must be a multiple of 256 with world * it == "
+                  "max_rows=%d", rs->rows_per_rank, max_rows);
+    if (rs->seq == 0) return fail(MUX_ERR_INVALID_ARGUMENT, "rs: seq must be > 0");
+    for (int d = 0; d < rs->world; ++d) {
+      if (!rs->recv[d] || !rs->flags[d] || !aligned16(rs->recv[d]))
+        return fail(MUX_ERR_INVALID_ARGUMENT, "rs: recv/flags of rank %d null or misaligned", d);
+      const __nv_bfloat16* slot = reinterpret_cast<const __nv_bfloat16*>(rs->recv[d]) +
+                                  static_cast<size_t>(rs->rank) * rs->rows_per_rank * nout;
+      if (!make_map(&p.map_out_rs[d], slot, nout, rs->rows_per_rank, nout, 64, 32))
+        return fail(MUX_ERR_CUDA, "cuTensorMapEncodeTiled failed for the receive slot on rank %d", d);
+      p.rs_ready[d] = rs->flags[d] + rs->rank;
+    }
+    p.rs_world = rs->world;
+    p.rs_rows = rs->rows_per_rank;
+    p.rs_seq = rs->seq;
+    p.rs_ack = rs->flags[rs->rank] + rs->world;
+  }
   // raster band: keep the band's A rows (group_m * 256 rows * kred * 2 B)
   // within ~48 MB of the 126 MB L2, leaving room for the streamed W tiles
 #ifndef MUX_BAND_MB
@@ -703,5 +727,58 @@ mux_status mux_add(int32_t rows, int32_t dim, const mux_bf16* a, int64_t lda, co
   if (e != cudaSuccess) return cuda_fail(e, "mux_add launch");
   return MUX_OK;
 }
+
+// ---------------------------------------------------------------- fused GEMM -> reduce-scatter
+mux_status mux_linear_fwd_rs(int32_t num_segs, const int32_t* seg_off, const int32_t* seg_task, int32_t num_adapters,
+                             const mux_adapter* adapters, int32_t max_rows, int32_t K, int32_t N, int32_t r_cap,
+                             const mux_bf16* X_, const mux_bf16* W_, mux_bf16* Hs_, const mux_rs* rs,
+                             void* workspace, size_t workspace_bytes, cudaStream_t stream) {
+  if (!rs) return fail(MUX_ERR_INVALID_ARGUMENT, "rs is null");
+  auto X = reinterpret_cast<const __nv_bfloat16*>(X_);
+  return linear_common(false, num_segs, seg_off, seg_task, num_adapters, adapters, max_rows, K, N, r_cap, X, X,
+                       reinterpret_cast<const __nv_bfloat16*>(W_), nullptr, nullptr,
+                       reinterpret_cast<__nv_bfloat16*>(Hs_), workspace, workspace_bytes, stream, 3, rs);
+}
+
+mux_status mux_linear_bwd_dx_rs(int32_t num_segs, const int32_t* seg_off, const int32_t* seg_task,
+                                int32_t num_adapters, const mux_adapter* adapters, int32_t max_rows, int32_t K,
+                                int32_t N, int32_t r_cap, const mux_bf16* dY_, const mux_bf16* X_,
+                                const mux_bf16* W_, const mux_bf16* Hs_, const mux_rs* rs, void* workspace,
+                                size_t workspace_bytes, cudaStream_t stream) {
+  if (!rs) return fail(MUX_ERR_INVALID_ARGUMENT, "rs is null");
+  return linear_common(true, num_segs, seg_off, seg_task, num_adapters, adapters, max_rows, K, N, r_cap,
+                       reinterpret_cast<const __nv_bfloat16*>(dY_), reinterpret_cast<const __nv_bfloat16*>(X_),
+                       reinterpret_cast<const __nv_bfloat16*>(W_), nullptr,
+                       reinterpret_cast<const __nv_bfloat16*>(Hs_), nullptr, workspace, workspace_bytes, stream,
+                       MUX_BWD_DX, rs);
+}
+
+mux_status mux_rs_reduce(const mux_rs* rs, int32_t cols, mux_bf16* out, int64_t ldo, cudaStream_t stream) {
+  if (!rs || !out) return fail(MUX_ERR_INVALID_ARGUMENT, "null pointer");
+  if (rs->world < 1 || rs->world > MUX_RS_MAX_WORLD || rs->rank < 0 || rs->rank >= rs->world || rs->seq == 0 ||
+      rs->rows_per_rank <= 0 || cols < 8 || cols % 8 || !ld_ok(ldo, cols))
+    return fail(MUX_ERR_INVALID_ARGUMENT, "rs_reduce: world=%d rank=%d seq=%llu rows=%d cols=%d", rs->world,
+                rs->rank, static_cast<unsigned long long>(rs->seq), rs->rows_per_rank, cols);
+  for (int d = 0; d < rs->world; ++d)
+    if (!rs->flags[d]) return fail(MUX_ERR_INVALID_ARGUMENT, "rs: flags of rank %d null", d);
+  if (!rs->recv[rs->rank] || !aligned16(rs->recv[rs->rank]) || !aligned16(out))
+    return fail(MUX_ERR_INVALID_ARGUMENT, "rs_reduce: receive buffer / out null or misaligned");
+  static thread_local RsReduceParams q;
+  q.world = rs->world;
+  q.rank = rs->rank;
+  q.rows = rs->rows_per_rank;
+  q.cols = cols;
+  q.seq = rs->seq;
+  q.recv = reinterpret_cast<const uint4*>(rs->recv[rs->rank]);
+  q.flags = rs->flags[rs->rank];
+  for (int s2 = 0; s2 < rs->world; ++s2) q.ack[s2] = rs->flags[s2] + rs->world + rs->rank;
+  q.out = reinterpret_cast<uint4*>(out);
+  q.ldo8 = ldo / 8;
+  cudaError_t e = launch_rs_reduce(q, num_sms(), stream);
+  if (e != cudaSuccess) return cuda_fail(e, "mux_rs_reduce launch");
+  return MUX_OK;
+}
+
+size_t mux_rs_flags_elems(int32_t world) { return world > 0 ? static_cast<size_t>(2 * world + 1) : 0; }
 
 }  // extern "C"

@@ -29,7 +29,8 @@ BWD_DX, BWD_GRADS = 1, 2
 EXPORTS = ("mux_last_error", "mux_version", "mux_pack_bound_rows", "mux_pack_workspace_size",
            "mux_pack_chunks", "mux_pack_apply", "mux_linear_workspace_size", "mux_linear_fwd",
            "mux_linear_bwd", "mux_linear_bwd_part", "mux_pack_row_start", "mux_attn_fwd", "mux_attn_workspace_size", "mux_attn_bwd",
-           "mux_rope", "mux_rmsnorm_fwd", "mux_rmsnorm_bwd", "mux_swiglu_fwd", "mux_swiglu_bwd", "mux_add")
+           "mux_rope", "mux_rmsnorm_fwd", "mux_rmsnorm_bwd", "mux_swiglu_fwd", "mux_swiglu_bwd", "mux_add", "mux_rs_flags_elems", "mux_linear_fwd_rs",
+           "mux_linear_bwd_dx_rs", "mux_rs_reduce")
 
 
 class MuxError(RuntimeError):
@@ -106,6 +107,14 @@ def lib():
         L.mux_swiglu_bwd.argtypes = [I32, I32, P, I64, P, I64, P, I64, P, I64, P, I64, P]
         L.mux_add.restype = ctypes.c_int
         L.mux_add.argtypes = [I32, I32, P, I64, P, I64, P, I64, P]
+        L.mux_rs_flags_elems.restype = SZ
+        L.mux_rs_flags_elems.argtypes = [I32]
+        L.mux_linear_fwd_rs.restype = ctypes.c_int
+        L.mux_linear_fwd_rs.argtypes = [I32, P, P, I32, P, I32, I32, I32, I32, P, P, P, P, P, SZ, P]
+        L.mux_linear_bwd_dx_rs.restype = ctypes.c_int
+        L.mux_linear_bwd_dx_rs.argtypes = [I32, P, P, I32, P, I32, I32, I32, I32, P, P, P, P, P, P, SZ, P]
+        L.mux_rs_reduce.restype = ctypes.c_int
+        L.mux_rs_reduce.argtypes = [P, I32, P, I64, P]
         _lib = L
     return _lib
 
@@ -406,3 +415,61 @@ def add(a, b, y=None, stream=None):
     _check(lib().mux_add(a.shape[0], a.shape[1], _ptr(a), _ld(a), _ptr(b), _ld(b), _ptr(y), _ld(y),
                          _stream(stream)))
     return y
+
+
+# ---------------------------------------------------------------- fused GEMM -> reduce-scatter
+RS_MAX_WORLD = 8
+
+
+class _Rs(ctypes.Structure):
+    _fields_ = [("world", ctypes.c_int32), ("rank", ctypes.c_int32), ("rows_per_rank", ctypes.c_int32),
+                ("seq", ctypes.c_uint64), ("recv", ctypes.c_void_p * RS_MAX_WORLD),
+                ("flags", ctypes.c_void_p * RS_MAX_WORLD)]
+
+
+def rs_flags_elems(world: int) -> int:
+    return int(lib().mux_rs_flags_elems(world))
+
+
+def make_rs(world: int, rank: int, rows_per_rank: int, seq: int, recv: Sequence, flags: Sequence) -> _Rs:
+    """mux_rs descriptor: recv[d] / flags[d] are rank d's receive buffer and flag block — tensors on
+    this device, or raw (peer-mapped) device addresses: [world * rows_per_rank * cols] bf16 and
+    [rs_flags_elems(world)] int64, zeroed once."""
+    r = _Rs()
+    r.world, r.rank, r.rows_per_rank, r.seq = world, rank, rows_per_rank, seq
+    for d in range(world):
+        r.recv[d] = recv[d] if isinstance(recv[d], int) else recv[d].data_ptr()
+        r.flags[d] = flags[d] if isinstance(flags[d], int) else flags[d].data_ptr()
+    return r
+
+
+def linear_fwd_rs(rs: _Rs, seg_off, seg_task, adapters, X, W, r_cap: int, Hs=None, workspace=None, stream=None):
+    """mux_linear_fwd_rs: forward whose output rows go straight to their owner ranks."""
+    max_rows, K = X.shape
+    N = W.shape[0]
+    if Hs is None:
+        Hs = torch.empty(max_rows, r_cap, dtype=torch.bfloat16, device=X.device)
+    S = len(seg_task)
+    if workspace is None:
+        workspace = torch.zeros(linear_workspace_size(S, max_rows, K, N, r_cap), dtype=torch.uint8, device=X.device)
+    _check(lib().mux_linear_fwd_rs(S, _ptr(seg_off), _i32_host(seg_task), len(adapters),
+                                   _adapter_table(adapters, False), max_rows, K, N, r_cap, _ptr(X), _ptr(W),
+                                   _ptr(Hs), ctypes.byref(rs), _ptr(workspace), workspace.numel(), _stream(stream)))
+    return Hs
+
+
+def linear_bwd_dx_rs(rs: _Rs, seg_off, seg_task, adapters, dY, X, W, Hs, r_cap: int, workspace, stream=None):
+    """mux_linear_bwd_dx_rs: the dX GEMM whose output rows go straight to their owner ranks
+    (follow with linear_bwd(..., part=BWD_GRADS) on the same workspace for dA/dB)."""
+    max_rows, K = X.shape
+    N = W.shape[0]
+    _check(lib().mux_linear_bwd_dx_rs(len(seg_task), _ptr(seg_off), _i32_host(seg_task), len(adapters),
+                                      _adapter_table(adapters, True), max_rows, K, N, r_cap, _ptr(dY), _ptr(X),
+                                      _ptr(W), _ptr(Hs), ctypes.byref(rs), _ptr(workspace), workspace.numel(),
+                                      _stream(stream)))
+
+
+def rs_reduce(rs: _Rs, out: torch.Tensor, stream=None) -> torch.Tensor:
+    """mux_rs_reduce: out [rows_per_rank, cols] = sum of the world partial slots (owner side)."""
+    _check(lib().mux_rs_reduce(ctypes.byref(rs), out.shape[1], _ptr(out), _ld(out), _stream(stream)))
+    return out

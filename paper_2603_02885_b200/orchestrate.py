@@ -251,6 +251,13 @@ def linear_chain_ops(layers: Sequence, kinds: Sequence[str], seg_off, seg_task, 
                 e[f"Y{i}"] = Y
             comp(f"fwd{i}", (f"X{i}",), (f"Y{i}",), fwd, flops_per_layer[i])
             cur = f"Y{i}"
+        elif kind == "row" and getattr(lay, "fused_rs", False):
+            # the reduce-scatter happens inside the GEMM (peer stores) + the owner-side sum
+            def fwd(e, i=i, src=cur, lay=lay):
+                lay.X = e[src]
+                e[f"Y{i}"], lay.Hs = lay.be.fwd_rs(lay, seg_off, seg_task, lay.X)
+            comp(f"fwd{i}", (cur,), (f"Y{i}",), fwd, flops_per_layer[i])
+            cur = f"Y{i}"
         elif kind == "row":
             def fwd(e, i=i, src=cur, lay=lay):
                 lay.X = e[src]
@@ -272,7 +279,13 @@ def linear_chain_ops(layers: Sequence, kinds: Sequence[str], seg_off, seg_task, 
     g = f"dY{L - 1}"
     for i in reversed(range(L)):
         lay, kind = layers[i], kinds[i]
-        if kind == "col":
+        if kind == "col" and getattr(lay, "fused_rs", False):
+            def bwd(e, i=i, src=g, lay=lay):
+                e[f"dX{i}"], e[f"dA{i}"], e[f"dB{i}"] = lay.be.bwd_rs(lay, seg_off, seg_task, e[src])
+            comp(f"bwd{i}", (g,), (f"dX{i}", f"dA{i}", f"dB{i}"), bwd, flops_per_layer[i])
+            comm(f"AR(dA{i})", (f"dA{i}",), (f"dA{i}:sum",), lambda e, i=i: all_reduce_async(e[f"dA{i}"], group))
+            g = f"dX{i}"
+        elif kind == "col":
             def bwd(e, i=i, src=g, lay=lay):
                 dXp, dA, dB = lay.be.bwd(seg_off, seg_task, lay.ads, e[src], lay.X, lay.W, lay.Hs, lay.r_cap)
                 e[f"dXp{i}"], e[f"dA{i}"], e[f"dB{i}"] = dXp, dA, dB

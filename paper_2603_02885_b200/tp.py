@@ -23,6 +23,14 @@ The per-rank compute is injected as a `backend` with
   bwd(seg_off, seg_task, adapters, dY, X, W, Hs, r_cap) -> (dX, [dA_t], [dB_t])
 `MuxBackend` is the product (libmux through the binding); tests inject the
 fp64 oracle to check the collective orchestration on CPU with gloo.
+
+Fused reduce-scatter (`fused_rs=True` on the layer classes, NCCL groups with
+torch symmetric memory): the row-parallel forward and the column-parallel dX
+GEMM store their output tiles straight into the owner rank's receive slot
+over NVLink (mux_linear_fwd_rs / mux_linear_bwd_dx_rs) and the owner sums the
+slots (mux_rs_reduce) — no separate collective launch, and the transfer of a
+tile overlaps the GEMM of the next ones.  `FusedRs` allocates the peer
+buffers once per (layer, direction).
 """
 from __future__ import annotations
 
@@ -67,6 +75,34 @@ def all_reduce_(x: torch.Tensor, group=None) -> torch.Tensor:
     return x
 
 
+class FusedRs:
+    """Receive buffers and flags of mux's fused GEMM -> reduce-scatter, allocated with torch
+    symmetric memory (every rank maps every rank's buffers over NVLink)."""
+
+    def __init__(self, group, rows_per_rank: int, cols: int, device):
+        import torch.distributed._symmetric_memory as symm
+        from . import mux
+        self.mux = mux
+        self.world, self.rank = _world(group)
+        self.rows = rows_per_rank
+        self.cols = cols
+        gname = group.group_name if group is not None else dist.group.WORLD.group_name
+        self.recv = symm.empty(self.world * rows_per_rank * cols, dtype=torch.bfloat16, device=device)
+        self.flags = symm.empty(mux.rs_flags_elems(self.world), dtype=torch.int64, device=device)
+        self.flags.zero_()
+        h1 = symm.rendezvous(self.recv, gname)
+        h2 = symm.rendezvous(self.flags, gname)
+        self.recv_ptrs = list(h1.buffer_ptrs)
+        self.flag_ptrs = list(h2.buffer_ptrs)
+        torch.cuda.synchronize()
+        dist.barrier(group)
+        self.seq = 0
+
+    def next(self):
+        self.seq += 1
+        return self.mux.make_rs(self.world, self.rank, self.rows, self.seq, self.recv_ptrs, self.flag_ptrs)
+
+
 # ------------------------------------------------------------------ backends
 class MuxBackend:
     """libmux kernels (the product path).  Output buffers and the (zeroed once,
@@ -103,6 +139,34 @@ class MuxBackend:
                                  workspace=self._ws(W, X, seg_task, r_cap))
         return dX, [a.dA for a in adapters], [a.dB for a in adapters]
 
+    # fused GEMM -> reduce-scatter (peer stores + owner-side sum; see FusedRs)
+    def _rs_for(self, lay, rows, cols, device):
+        if lay._rs is None or lay._rs.rows != rows or lay._rs.cols != cols:
+            lay._rs = FusedRs(lay.group, rows, cols, device)
+        return lay._rs
+
+    def fwd_rs(self, lay, seg_off, seg_task, X):
+        p, _ = _world(lay.group)
+        R, N = X.shape[0], lay.W.shape[0]
+        rs = self._rs_for(lay, R // p, N, X.device).next()
+        Hs = self._buf(("Hs", lay.W.data_ptr()), (R, lay.r_cap), torch.bfloat16, X.device)
+        self.mux.linear_fwd_rs(rs, seg_off, seg_task, lay.ads, X, lay.W, lay.r_cap, Hs=Hs,
+                               workspace=self._ws(lay.W, X, seg_task, lay.r_cap))
+        Y = self._buf(("Yrs", lay.W.data_ptr()), (R // p, N), torch.bfloat16, X.device)
+        return self.mux.rs_reduce(rs, Y), Hs
+
+    def bwd_rs(self, lay, seg_off, seg_task, dY):
+        p, _ = _world(lay.group)
+        X = lay.X
+        R, K = X.shape
+        rs = self._rs_for(lay, R // p, K, X.device).next()
+        ws = self._ws(lay.W, X, seg_task, lay.r_cap)
+        self.mux.linear_bwd_dx_rs(rs, seg_off, seg_task, lay.ads, dY, X, lay.W, lay.Hs, lay.r_cap, ws)
+        self.mux.linear_bwd(seg_off, seg_task, lay.ads, dY, X, lay.W, lay.Hs, lay.r_cap, workspace=ws,
+                            part=self.mux.BWD_GRADS)
+        dX = self._buf(("dXrs", lay.W.data_ptr()), (R // p, K), torch.bfloat16, X.device)
+        return self.mux.rs_reduce(rs, dX), [a.dA for a in lay.ads], [a.dB for a in lay.ads]
+
 
 @dataclass
 class ShardAdapter:
@@ -135,8 +199,10 @@ def shard_row(W: torch.Tensor, adapters: Sequence, p: int, r: int, make_adapter)
 
 
 class ColumnParallelMuxLinear:
-    def __init__(self, backend, W_shard, adapters_shard, r_cap, group=None):
+    def __init__(self, backend, W_shard, adapters_shard, r_cap, group=None, fused_rs=False):
         self.be, self.W, self.ads, self.r_cap, self.group = backend, W_shard, adapters_shard, r_cap, group
+        self.fused_rs = fused_rs
+        self._rs = None
 
     def forward(self, seg_off, seg_task, x_rows):
         """x_rows [R/p, K] (this rank's row block) -> Y_p [R, N/p]."""
@@ -146,20 +212,29 @@ class ColumnParallelMuxLinear:
 
     def backward(self, seg_off, seg_task, dY_cols):
         """dY_p [R, N/p] -> dX rows [R/p, K]; dA_t all-reduced, dB_{t,p} local."""
-        dXp, dA, dB = self.be.bwd(seg_off, seg_task, self.ads, dY_cols, self.X, self.W, self.Hs, self.r_cap)
+        if self.fused_rs:
+            dX_rows, dA, dB = self.be.bwd_rs(self, seg_off, seg_task, dY_cols)
+        else:
+            dXp, dA, dB = self.be.bwd(seg_off, seg_task, self.ads, dY_cols, self.X, self.W, self.Hs, self.r_cap)
+            dX_rows = None
         for g in dA:
             if g is not None:
                 all_reduce_(g, self.group)
-        return reduce_scatter_rows(dXp, self.group), dA, dB
+        return (reduce_scatter_rows(dXp, self.group) if dX_rows is None else dX_rows), dA, dB
 
 
 class RowParallelMuxLinear:
-    def __init__(self, backend, W_shard, adapters_shard, r_cap, group=None):
+    def __init__(self, backend, W_shard, adapters_shard, r_cap, group=None, fused_rs=False):
         self.be, self.W, self.ads, self.r_cap, self.group = backend, W_shard, adapters_shard, r_cap, group
+        self.fused_rs = fused_rs
+        self._rs = None
 
     def forward(self, seg_off, seg_task, x_cols):
         """x_cols [R, K/p] (this rank's column shard) -> Y rows [R/p, N]."""
         self.X = x_cols
+        if self.fused_rs:
+            Y_rows, self.Hs = self.be.fwd_rs(self, seg_off, seg_task, x_cols)
+            return Y_rows
         Yp, self.Hs = self.be.fwd(seg_off, seg_task, self.ads, x_cols, self.W, self.r_cap)
         return reduce_scatter_rows(Yp, self.group)
 

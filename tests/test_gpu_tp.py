@@ -137,3 +137,49 @@ def test_orchestrated_htasks_world1_equals_direct(pg):
         ref_dB = [a.dB for li in range(3) for a in ads_all[li]]
         for a_, b_ in zip(got[i][2] + got[i][3], ref_dA + ref_dB):
             assert torch.equal(a_, b_)
+
+
+def test_tp_fused_rs_world1_equals_direct(pg):
+    """The tp.py layers with the reduce-scatter fused into the GEMMs (peer-store path through torch
+    symmetric memory; at world 1 the 'peer' is this GPU) == direct binding calls, bit for bit."""
+    g = torch.Generator(device="cuda").manual_seed(21)
+    R, K, N = 512, 256, 384
+    seg_off = torch.tensor([0, 192, 320, 512], dtype=torch.int32, device="cuda")
+    st = [0, 1, 2]
+    ranks = [16, 8, 32]
+
+    def make(KK, NN):
+        W = (torch.randn(NN, KK, device="cuda", generator=g) / KK ** 0.5).bfloat16()
+        ads = []
+        for r in ranks:
+            B = mux.make_B_storage(NN, r)
+            B.copy_(torch.randn(NN, r, device="cuda", generator=g).bfloat16())
+            ads.append(mux.Adapter((torch.randn(r, KK, device="cuda", generator=g) / KK ** 0.5).bfloat16(),
+                                   B, r, 2.0))
+        return W, ads
+
+    W1, a1 = make(K, N)
+    W2, a2 = make(N, K)
+    X = torch.randn(R, K, device="cuda", generator=g).bfloat16()
+    dY = torch.randn(R, K, device="cuda", generator=g).bfloat16()
+    mk = lambda A, B, r, s: mux.Adapter(A, B, r, s)  # noqa: E731
+    be = tp.MuxBackend()
+    W1p, a1p = tp.shard_column(W1, a1, 1, 0, mk)
+    W2p, a2p = tp.shard_row(W2, a2, 1, 0, mk)
+    up = tp.ColumnParallelMuxLinear(be, W1p, a1p, 32, fused_rs=True)
+    down = tp.RowParallelMuxLinear(be, W2p, a2p, 32, fused_rs=True)
+    for _ in range(2):   # twice: the receive slots and flags are reused (seq 1, 2)
+        h = up.forward(seg_off, st, X)
+        y = down.forward(seg_off, st, h)
+        dh, dA2, dB2 = down.backward(seg_off, st, dY)
+        dx, dA1, dB1 = up.backward(seg_off, st, dh)
+    torch.cuda.synchronize()
+    got = [y.clone(), dx.clone()] + [t.clone() for t in dA1 + dB1 + dA2 + dB2]
+    H, Hs1 = mux.linear_fwd(seg_off, st, a1, X, W1, 32)
+    Y, Hs2 = mux.linear_fwd(seg_off, st, a2, H, W2, 32)
+    dH = mux.linear_bwd(seg_off, st, a2, dY, H, W2, Hs2, 32)
+    dX = mux.linear_bwd(seg_off, st, a1, dH, X, W1, Hs1, 32)
+    torch.cuda.synchronize()
+    ref = [Y, dX] + [a.dA for a in a1] + [a.dB for a in a1] + [a.dA for a in a2] + [a.dB for a in a2]
+    for a_, b_ in zip(got, ref):
+        assert torch.equal(_bits(a_), _bits(b_))
