@@ -147,3 +147,28 @@ def test_bwd_parts_overlapped_equal_combined():
         assert torch.equal(x.dA, y.dA) and torch.equal(x.dB, y.dB)
     with pytest.raises(mux.MuxError):
         mux.linear_bwd(seg_off, st, a2, dY, X, W, Hs, 32, dX=dX2, workspace=ws, part=3)
+
+
+@pytest.mark.parametrize("case", range(16))
+def test_fuzz_random_problems(case):
+    """Seeded random problems across the ABI's legal space: K, N multiples of 8 (not of 64),
+    1-12 segments of multiples of 64 rows (empty ones included), tasks owning several segments,
+    ranks 0-64 (r_cap the smallest legal), integer-valued inputs half of the time (then bit-exact)."""
+    rng = np.random.default_rng(1000 + case)
+    K = int(rng.integers(1, 48)) * 8
+    N = int(rng.integers(1, 48)) * 8
+    S = int(rng.integers(1, 13))
+    seg_lens = [int(rng.integers(0, 7)) * 64 for _ in range(S)]
+    if sum(seg_lens) == 0:
+        seg_lens[0] = 64
+    T = int(rng.integers(1, min(S, 6) + 1))
+    ranks = [int(rng.choice([0, 1, 4, 8, 16, 17, 32, 48, 64])) for _ in range(T)]
+    if max(ranks) == 0:
+        ranks[0] = 8
+    seg_task = [int(rng.integers(0, T)) for _ in range(S)]
+    variant = "int" if case % 2 else "normal"
+    scales = [float(rng.choice([1.0, 2.0])) for _ in range(T)] if variant == "int" else \
+        [float(rng.uniform(0.25, 4.0)) for _ in range(T)]
+    prob = Problem(K, N, seg_lens, ranks, seg_task=seg_task, scales=scales, variant=variant, seed=3000 + case)
+    errs = compare(prob, prob.run_gpu(), prob.run_oracle(), exact=(variant == "int"))
+    assert max(errs.values()) <= TOL, errs
