@@ -180,7 +180,9 @@ MUX_API size_t mux_linear_workspace_size(int32_t num_segs, int32_t max_rows, int
  *   Hs[i,j] = bf16(s_t * X[i,:] A_t[j,:]^T) for j < rank_t, 0 for rank_t <= j < r_cap
  * Arguments
  *   num_segs S (1..64) [host]; seg_off [S+1] device, non-decreasing, every
- *   entry a multiple of 64 (mux_pack_chunks guarantees it), seg_off[S] <=
+ *   entry a multiple of 64 (mux_pack_chunks guarantees it; the host cannot
+ *   check device data without a sync: a -DMUX_DEBUG_CHECKS build checks it on
+ *   the device and traps), seg_off[S] <=
  *   max_rows; seg_task [S] [host] adapter index per segment;
  *   num_adapters (1..64), adapters [host];
  *   K, N multiples of 8 (e.g. 11008/8 = 1376 for an 8-way tensor-parallel shard);

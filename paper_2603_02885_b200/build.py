@@ -30,10 +30,11 @@ def headers():
                   + glob.glob(os.path.join(ROOT, "include", "*.h")))
 
 
-def stale() -> bool:
-    if not os.path.exists(LIB):
+def stale(lib: str = None) -> bool:
+    lib = lib or LIB
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     return any(os.path.getmtime(f) > t for f in sources() + headers())
 
 
@@ -41,8 +42,8 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str = Non
     """Build libmux.so; `defines`/`out` build an experiment variant (A/B
     timing only, e.g. defines=("MUX_BK=128",), out="libmux_bk128.so")."""
     lib = LIB if out is None else os.path.join(HERE, out)
-    if out is None and not force and not stale():
-        return LIB
+    if not force and not stale(lib):
+        return lib
     objs = []
     bdir = os.path.join(HERE, "build" if out is None else "build_" + os.path.splitext(out)[0])
     os.makedirs(bdir, exist_ok=True)

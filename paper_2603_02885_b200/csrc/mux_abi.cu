@@ -46,6 +46,7 @@ cudaError_t launch_add(int rows, int dim, const void* a, long long lda, const vo
                        long long ldy, int num_sms, cudaStream_t s);
 cudaError_t launch_attn_fwd_tc(const AttnTcParams& p, cudaStream_t s);
 cudaError_t launch_rs_reduce(const RsReduceParams& p, int num_sms, cudaStream_t s);
+cudaError_t launch_check_segments(int num_segs, const int32_t* seg_off, int max_rows, cudaStream_t s);
 cudaError_t launch_attn_bwd_pre(int R, int H, const void* dO, long long lddo, const void* o, long long ldo,
                                 float* D, cudaStream_t s);
 cudaError_t launch_attn_bwd_tc(const AttnBwdTcParams& p, cudaStream_t s);
@@ -431,6 +432,10 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
   const long long pairs = std::min<long long>(tiles_max, num_sms() / 2);
   const int grid = static_cast<int>(2 * std::max<long long>(pairs, 1));
   cudaError_t e = cudaSuccess;
+#ifdef MUX_DEBUG_CHECKS
+  e = launch_check_segments(num_segs, seg_off, max_rows, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "debug segment check launch");
+#endif
   if (parts & 1) {
     e = launch_gemm(p, bwd, grid, stream);
     if (e != cudaSuccess) return cuda_fail(e, bwd ? "mux_linear_bwd dX launch" : "mux_linear_fwd launch");

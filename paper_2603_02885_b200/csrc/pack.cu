@@ -13,6 +13,8 @@
 //   4. chunk counts ceil(L_p / c) -> per-task scan -> seg_off, pack rows;
 //   5. fill: chunk table with KV-reuse links, seq_row, row_src.
 // Integer results are bit-exact with the fp64 oracle's pack (tests/test_gpu_pack.py).
+#include <cstdio>
+
 #include "common.h"
 #include "launch.cuh"
 #include "ptx.cuh"
@@ -403,4 +405,29 @@ cudaError_t launch_pack_apply(int max_rows, int cols, int num_tokens, const int3
                             reinterpret_cast<const uint4*>(src), reinterpret_cast<uint4*>(dst));
 }
 
+}  // namespace mux
+
+namespace mux {
+// Debug builds (-DMUX_DEBUG_CHECKS): the device-side preconditions of the
+// linear calls that the host cannot check without a synchronisation
+// (include/mux.h): seg_off non-decreasing, every entry a multiple of 64,
+// seg_off[S] <= max_rows.  A violation prints the offending entry and traps.
+__global__ void mux_check_segments_kernel(int num_segs, const int32_t* seg_off, int max_rows) {
+  griddep_wait();
+  griddep_launch_dependents();
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  for (int s = 0; s <= num_segs; ++s) {
+    const int v = seg_off[s];
+    const bool bad = (v % kRowQuarter) != 0 || v < 0 || v > max_rows || (s > 0 && v < seg_off[s - 1]);
+    if (bad) {
+      printf("mux: bad seg_off[%d] = %d (max_rows %d): must be non-decreasing multiples of 64 <= max_rows\n", s,
+             v, max_rows);
+      __trap();
+    }
+  }
+}
+
+cudaError_t launch_check_segments(int num_segs, const int32_t* seg_off, int max_rows, cudaStream_t s) {
+  return launch_pdl(mux_check_segments_kernel, dim3(1), dim3(32), 0, s, num_segs, seg_off, max_rows);
+}
 }  // namespace mux

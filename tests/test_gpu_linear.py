@@ -172,3 +172,34 @@ def test_fuzz_random_problems(case):
     prob = Problem(K, N, seg_lens, ranks, seg_task=seg_task, scales=scales, variant=variant, seed=3000 + case)
     errs = compare(prob, prob.run_gpu(), prob.run_oracle(), exact=(variant == "int"))
     assert max(errs.values()) <= TOL, errs
+
+
+def test_debug_build_traps_on_bad_segment_offsets():
+    """A -DMUX_DEBUG_CHECKS build checks the device-side preconditions the host cannot see
+    (seg_off non-decreasing multiples of 64 <= max_rows) and traps; a valid call passes."""
+    import subprocess
+    import sys
+    import os
+    from paper_2603_02885_b200 import build as mbuild
+    lib = mbuild.build(defines=("MUX_DEBUG_CHECKS",), out="libmux_debug.so")
+    code = f"""
+import torch, sys
+sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})
+from paper_2603_02885_b200 import mux
+mux.LIB_PATH = {lib!r}
+mux._lib = None
+X = torch.randn(256, 64, device='cuda').bfloat16()
+W = torch.randn(64, 64, device='cuda').bfloat16()
+ads = [mux.Adapter(None, None, 0, 0.0), mux.Adapter(None, None, 0, 0.0)]
+mux.linear_fwd(torch.tensor([0, 128, 256], dtype=torch.int32, device='cuda'), [0, 1], ads, X, W, 16)
+torch.cuda.synchronize()
+print('valid ok', flush=True)
+mux.linear_fwd(torch.tensor([0, 100, 256], dtype=torch.int32, device='cuda'), [0, 1], ads, X, W, 16)
+torch.cuda.synchronize()
+print('not trapped', flush=True)
+"""
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+    out = r.stdout + r.stderr
+    assert "valid ok" in out, out
+    assert "not trapped" not in out and r.returncode != 0, out
+    assert "bad seg_off[1] = 100" in out, out
