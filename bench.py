@@ -672,6 +672,7 @@ def block_arm(args):
             ads[n].append(mux.Adapter(_bits_to_dev(h[f"A{li}_{t}"], torch), B, wl.ranks[t], wl.scales[t]))
     r_cap = 16 * -(-max(wl.ranks) // 16)
     blk = DecoderBlock(shape, W, ads, r_cap)
+    blk.overlap_grads = not args.no_overlap_grads
     i32 = dict(dtype=torch.int32, device=dev)
     tso, sl = torch.tensor(w.off, **i32), torch.tensor(w.lens, **i32)
     cap = torch.tensor(w.cap, **i32) if w.cap else None

@@ -59,6 +59,9 @@ class DecoderBlock:
                     a.dB = torch.empty(N, a.rank, dtype=torch.float32, device=weights[name].device)
         self._buf: Dict[str, torch.Tensor] = {}
         self._rows = -1
+        self.overlap_grads = True
+        self._side = torch.cuda.Stream(device=weights["q"].device)
+        self._events: Dict[str, torch.cuda.Event] = {}
 
     def _b(self, name, cols, dtype=torch.bfloat16):
         t = self._buf.get(name)
@@ -84,8 +87,19 @@ class DecoderBlock:
         return Y
 
     def _lin_bwd(self, name, dY, X, out):
-        mux.linear_bwd(self.seg_off, self.seg_task, self.ads[name], dY, X, self.w[name],
-                       self._buf[name + ".hs"], self.r_cap, dX=out, workspace=self._ws(name, len(self.seg_task)))
+        """dX GEMM on the caller's stream; the adapter gradients (HBM-bound) on a side stream, where
+        they fill the tail of the next tensor-bound GEMM (joined at the end of backward())."""
+        ws = self._ws(name, len(self.seg_task))
+        args = (self.seg_off, self.seg_task, self.ads[name], dY, X, self.w[name], self._buf[name + ".hs"], self.r_cap)
+        if not self.overlap_grads:
+            mux.linear_bwd(*args, dX=out, workspace=ws)
+            return out
+        main = torch.cuda.current_stream()
+        mux.linear_bwd(*args, dX=out, workspace=ws, part=mux.BWD_DX)
+        ev = self._events.setdefault(name, torch.cuda.Event())
+        ev.record(main)
+        self._side.wait_event(ev)
+        mux.linear_bwd(*args, dX=out, workspace=ws, part=mux.BWD_GRADS, stream=self._side)
         return out
 
     def forward(self, x: torch.Tensor, seg_off: torch.Tensor, seg_task: Sequence[int], row_start: torch.Tensor):
@@ -133,8 +147,11 @@ class DecoderBlock:
         dh1k = self._lin_bwd("k", dk, sv["h1"], self._b("dh1k", s.hidden))
         dh1v = self._lin_bwd("v", dv, sv["h1"], self._b("dh1v", s.hidden))
         # dx = RMSNorm'(x)^T (dh1 + dh1k + dh1v) + dx2 (residual), one fused pass
-        return mux.rmsnorm_bwd(dh1, self.x, self.w["norm1"], s.eps, dx=self._b("dx", s.hidden), dy2=dh1k, dy3=dh1v,
-                               resid=dx2)
+        dx = mux.rmsnorm_bwd(dh1, self.x, self.w["norm1"], s.eps, dx=self._b("dx", s.hidden), dy2=dh1k, dy3=dh1v,
+                             resid=dx2)
+        if self.overlap_grads:
+            torch.cuda.current_stream().wait_stream(self._side)   # dA/dB complete with the returned dx
+        return dx
 
     # kernel launches: forward = 2 norms (the second fused with the residual add) + 7 linears +
     # 2 RoPE + attention + swiglu + 1 residual add = 14; backward = 7 linears x (dX GEMM +
