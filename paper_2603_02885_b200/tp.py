@@ -79,21 +79,29 @@ class FusedRs:
     """Receive buffers and flags of mux's fused GEMM -> reduce-scatter, allocated with torch
     symmetric memory (every rank maps every rank's buffers over NVLink)."""
 
-    def __init__(self, group, rows_per_rank: int, cols: int, device):
-        import torch.distributed._symmetric_memory as symm
+    def __init__(self, group, rows_per_rank: int, cols: int, device, exchange=None):
+        """`exchange(recv, flags) -> (recv_ptrs, flag_ptrs)` maps every rank's buffers by other
+        means (e.g. CUDA IPC handles); default: torch symmetric memory rendezvous."""
         from . import mux
         self.mux = mux
         self.world, self.rank = _world(group)
         self.rows = rows_per_rank
         self.cols = cols
-        gname = group.group_name if group is not None else dist.group.WORLD.group_name
-        self.recv = symm.empty(self.world * rows_per_rank * cols, dtype=torch.bfloat16, device=device)
-        self.flags = symm.empty(mux.rs_flags_elems(self.world), dtype=torch.int64, device=device)
-        self.flags.zero_()
-        h1 = symm.rendezvous(self.recv, gname)
-        h2 = symm.rendezvous(self.flags, gname)
-        self.recv_ptrs = list(h1.buffer_ptrs)
-        self.flag_ptrs = list(h2.buffer_ptrs)
+        n_recv, n_flags = self.world * rows_per_rank * cols, mux.rs_flags_elems(self.world)
+        if exchange is None:
+            import torch.distributed._symmetric_memory as symm
+            gname = group.group_name if group is not None else dist.group.WORLD.group_name
+            self.recv = symm.empty(n_recv, dtype=torch.bfloat16, device=device)
+            self.flags = symm.empty(n_flags, dtype=torch.int64, device=device)
+            self.flags.zero_()
+            h1 = symm.rendezvous(self.recv, gname)
+            h2 = symm.rendezvous(self.flags, gname)
+            self.recv_ptrs = list(h1.buffer_ptrs)
+            self.flag_ptrs = list(h2.buffer_ptrs)
+        else:
+            self.recv = torch.zeros(n_recv, dtype=torch.bfloat16, device=device)
+            self.flags = torch.zeros(n_flags, dtype=torch.int64, device=device)
+            self.recv_ptrs, self.flag_ptrs = exchange(self.recv, self.flags)
         torch.cuda.synchronize()
         dist.barrier(group)
         self.seq = 0
@@ -140,9 +148,11 @@ class MuxBackend:
         return dX, [a.dA for a in adapters], [a.dB for a in adapters]
 
     # fused GEMM -> reduce-scatter (peer stores + owner-side sum; see FusedRs)
+    rs_exchange = None  # optional buffer-mapping hook for FusedRs (default: symmetric memory)
+
     def _rs_for(self, lay, rows, cols, device):
         if lay._rs is None or lay._rs.rows != rows or lay._rs.cols != cols:
-            lay._rs = FusedRs(lay.group, rows, cols, device)
+            lay._rs = FusedRs(lay.group, rows, cols, device, exchange=self.rs_exchange)
         return lay._rs
 
     def fwd_rs(self, lay, seg_off, seg_task, X):
