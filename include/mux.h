@@ -276,6 +276,37 @@ MUX_API mux_status mux_linear_bwd_dx_rs(int32_t num_segs, const int32_t* seg_off
 MUX_API mux_status mux_rs_reduce(const mux_rs* rs, int32_t cols, mux_bf16* out, int64_t ldo, cudaStream_t stream);
 
 /* ---------------------------------------------------------------------------
+ * All-gather -> GEMM for tensor parallelism (the column-parallel forward's
+ * AG(X) and the row-parallel backward's AG(dY)).  Every
+ * rank pushes its own rows into every rank's gather buffer with the copy
+ * engines (mux_ag_push: no SMs, so it runs under the GEMMs) and signals each
+ * destination with a stream memory write; the fused GEMM's TMA producer waits
+ * on a row block's owner flag just before its first load of those rows, so
+ * the GEMM starts on whatever rows have landed (its own at once) while the
+ * rest are in flight.  The gather buffer stays valid until the caller
+ * releases it (mux_ag_release, e.g. after the backward that re-reads X),
+ * which allows the owners to push the next call's rows.
+ * mux_ag has mux_rs's fields: recv[d] = rank d's gather buffer
+ * [world * rows_per_rank][cols] (the full A operand on rank d), flags[d] =
+ * rank d's flag block [mux_rs_flags_elems(world)], zeroed once. */
+typedef mux_rs mux_ag;
+MUX_API mux_status mux_ag_push(const mux_ag* ag, const mux_bf16* rows, int64_t ld, int32_t cols,
+                               cudaStream_t stream);
+MUX_API mux_status mux_ag_release(const mux_ag* ag, cudaStream_t stream);
+/* mux_linear_fwd with X = ag->recv[ag->rank], each row block read once it has landed */
+MUX_API mux_status mux_linear_fwd_ag(int32_t num_segs, const int32_t* seg_off, const int32_t* seg_task,
+                                     int32_t num_adapters, const mux_adapter* adapters, int32_t max_rows,
+                                     int32_t K, int32_t N, int32_t r_cap, const mux_ag* ag, const mux_bf16* W,
+                                     mux_bf16* Y, mux_bf16* Hs, void* workspace, size_t workspace_bytes,
+                                     cudaStream_t stream);
+/* mux_linear_bwd with dY = ag->recv[ag->rank] */
+MUX_API mux_status mux_linear_bwd_ag(int32_t num_segs, const int32_t* seg_off, const int32_t* seg_task,
+                                     int32_t num_adapters, const mux_adapter* adapters, int32_t max_rows,
+                                     int32_t K, int32_t N, int32_t r_cap, const mux_ag* ag, const mux_bf16* X,
+                                     const mux_bf16* W, const mux_bf16* Hs, mux_bf16* dX, void* workspace,
+                                     size_t workspace_bytes, cudaStream_t stream);
+
+/* ---------------------------------------------------------------------------
  * Decoder-block ops (NEXT-3).  Row-major bf16 matrices with an explicit row
  * stride `ld*` in ELEMENTS (a multiple of 8: 16-byte rows), so q/k/v or
  * gate/up can be column slices of one fused projection output.  fp32 math.

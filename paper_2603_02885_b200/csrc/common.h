@@ -67,6 +67,13 @@ struct GemmParams {
   const unsigned long long* rs_ack;          // this rank's ack flags [rs_world] (written by the dests)
   unsigned long long* rs_ready[MUX_RS_MAX_WORLD];  // rank d's ready flag for this source (peer)
   CUtensorMap map_out_rs[MUX_RS_MAX_WORLD];
+  // Fused all-gather input (tensor parallel, mux_linear_*_ag): the A operand (X or dY) is the
+  // local gather buffer that every rank pushes its own rows into (copy engines, mux_ag_push);
+  // before loading a row block the producer waits until ag_flags[owner] >= ag_seq.
+  int32_t ag_world;
+  int32_t ag_rows;
+  unsigned long long ag_seq;
+  const unsigned long long* ag_flags;
   int32_t seg_adapter[MUX_MAX_SEGMENTS];
   int32_t seg_rank[MUX_MAX_SEGMENTS];
   float seg_scale[MUX_MAX_SEGMENTS];

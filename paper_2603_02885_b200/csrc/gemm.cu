@@ -236,10 +236,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       const uint32_t pipe_u = smem_u32(pipe);
       const uint32_t full_u = smem_u32(full_bar);
       const uint32_t full_leader = mapa_shared(full_u, 0);  // stage s barrier: + 8 s
+      uint32_t ag_ok = 0;  // owners whose rows have landed in the gather buffer (fused all-gather)
       for (int t = cid; t < total_tiles; t += ncl) {
         const Tile tl = tile_at(t, num_m, num_n, p.group_m, p.has_main != 0);
         const PairGroups g = pair_groups(p, so, tl.m);
         const int row_c = tl.m * kPairRows + kBM * rk;  // this CTA's rows
+        if (p.ag_world > 0) {
+          const int owner = (tl.m * kPairRows) / p.ag_rows;
+          if (!((ag_ok >> owner) & 1u)) {
+            if (elect_one_sync()) {
+              const unsigned long long* f = p.ag_flags + owner;
+              if (ld_acquire_sys_u64(f) < p.ag_seq) {
+                const uint64_t t0 = globaltimer_ns();
+                while (ld_acquire_sys_u64(f) < p.ag_seq)
+                  if (globaltimer_ns() - t0 > kWatchdogNs) __trap();
+              }
+              fence_async_global();  // the rows the copy engine wrote -> this CTA's TMA reads
+            }
+            __syncwarp();
+            ag_ok |= 1u << owner;
+          }
+        }
         if (tl.side) {
           for (int g0 = 0; g0 < g.n; g0 += 2) {
             const int ng = min(2, g.n - g0);

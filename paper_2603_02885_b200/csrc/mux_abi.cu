@@ -95,6 +95,24 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
+// stream memory operations (copy-engine all-gather signalling) through the driver entry points
+typedef CUresult (*StreamValueFn)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+StreamValueFn stream_value_fn(const char* name) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) == cudaSuccess && q == cudaDriverEntryPointSuccess)
+    return reinterpret_cast<StreamValueFn>(p);
+  return nullptr;
+}
+StreamValueFn wait_value64() {
+  static StreamValueFn fn = stream_value_fn("cuStreamWaitValue64");
+  return fn;
+}
+StreamValueFn write_value64() {
+  static StreamValueFn fn = stream_value_fn("cuStreamWriteValue64");
+  return fn;
+}
+
 struct MapKey {
   const void* ptr;
   uint64_t inner, outer, stride;
@@ -337,7 +355,7 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
                                 const __nv_bfloat16* X, const __nv_bfloat16* W, __nv_bfloat16* out /*Y or dX*/,
                                 const __nv_bfloat16* Hs_in, __nv_bfloat16* Hs_out, void* workspace,
                                 size_t workspace_bytes, cudaStream_t stream, int parts = 3,
-                                const mux_rs* rs = nullptr) {
+                                const mux_rs* rs = nullptr, const mux_ag* ag = nullptr) {
   mux_status st = validate_linear(num_segs, seg_off, seg_task, num_adapters, adapters, max_rows, K, N, r_cap);
   if (st != MUX_OK) return st;
   if (!a_in || !W) return fail(MUX_ERR_INVALID_ARGUMENT, "null input pointer");
@@ -384,6 +402,17 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
   p.nout = nout;
   p.r_cap = r_cap;
   p.has_main = out != nullptr || rs != nullptr;
+  if (ag) {
+    if (ag->world < 1 || ag->world > MUX_RS_MAX_WORLD || ag->rank < 0 || ag->rank >= ag->world || ag->seq == 0 ||
+        ag->rows_per_rank <= 0 || ag->rows_per_rank % kPairRows ||
+        static_cast<long long>(ag->rows_per_rank) * ag->world != max_rows || !ag->flags[ag->rank])
+      return fail(MUX_ERR_INVALID_ARGUMENT, "ag: world=%d rank=%d rows_per_rank=%d (multiple of 256, world * it == "
+                  "max_rows=%d), seq > 0, flags", ag->world, ag->rank, ag->rows_per_rank, max_rows);
+    p.ag_world = ag->world;
+    p.ag_rows = ag->rows_per_rank;
+    p.ag_seq = ag->seq;
+    p.ag_flags = ag->flags[ag->rank];
+  }
   if (rs) {
     if (rs->world < 1 || rs->world > MUX_RS_MAX_WORLD || rs->rank < 0 || rs->rank >= rs->world)
       return fail(MUX_ERR_INVALID_ARGUMENT, "rs: world=%d rank=%d", rs->world, rs->rank);
@@ -785,5 +814,72 @@ mux_status mux_rs_reduce(const mux_rs* rs, int32_t cols, mux_bf16* out, int64_t 
 }
 
 size_t mux_rs_flags_elems(int32_t world) { return world > 0 ? static_cast<size_t>(2 * world + 1) : 0; }
+
+// ---------------------------------------------------------------- fused all-gather -> GEMM
+mux_status mux_ag_push(const mux_ag* ag, const mux_bf16* rows, int64_t ld, int32_t cols, cudaStream_t stream) {
+  if (!ag || !rows) return fail(MUX_ERR_INVALID_ARGUMENT, "null pointer");
+  if (ag->world < 1 || ag->world > MUX_RS_MAX_WORLD || ag->rank < 0 || ag->rank >= ag->world || ag->seq == 0 ||
+      ag->rows_per_rank <= 0 || cols < 8 || cols % 8 || !ld_ok(ld, cols))
+    return fail(MUX_ERR_INVALID_ARGUMENT, "ag_push: world=%d rank=%d rows=%d cols=%d", ag->world, ag->rank,
+                ag->rows_per_rank, cols);
+  StreamValueFn wait = wait_value64(), write = write_value64();
+  if (!wait || !write) return fail(MUX_ERR_UNSUPPORTED, "stream memory operations unavailable");
+  const unsigned long long* ack = ag->flags[ag->rank] + ag->world;  // readers' acks, this rank's block
+  for (int d = 0; d < ag->world; ++d) {
+    if (!ag->recv[d] || !ag->flags[d]) return fail(MUX_ERR_INVALID_ARGUMENT, "ag: rank %d buffers null", d);
+    // rank d must have released this rank's rows of the previous call
+    if (ag->seq > 1 && wait(reinterpret_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(ack + d),
+                            ag->seq - 1, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+      return fail(MUX_ERR_CUDA, "cuStreamWaitValue64 failed");
+    mux_bf16* dst = ag->recv[d] + static_cast<size_t>(ag->rank) * ag->rows_per_rank * cols;
+    cudaError_t e = cudaMemcpy2DAsync(dst, static_cast<size_t>(cols) * 2, rows, static_cast<size_t>(ld) * 2,
+                                      static_cast<size_t>(cols) * 2, ag->rows_per_rank, cudaMemcpyDeviceToDevice,
+                                      stream);
+    if (e != cudaSuccess) return cuda_fail(e, "mux_ag_push copy");
+    // ordered after the copy (stream order; the write carries a memory fence)
+    if (write(reinterpret_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(ag->flags[d] + ag->rank), ag->seq,
+              0) != CUDA_SUCCESS)
+      return fail(MUX_ERR_CUDA, "cuStreamWriteValue64 failed");
+  }
+  return MUX_OK;
+}
+
+mux_status mux_ag_release(const mux_ag* ag, cudaStream_t stream) {
+  if (!ag) return fail(MUX_ERR_INVALID_ARGUMENT, "null pointer");
+  if (ag->world < 1 || ag->world > MUX_RS_MAX_WORLD || ag->rank < 0 || ag->rank >= ag->world || ag->seq == 0)
+    return fail(MUX_ERR_INVALID_ARGUMENT, "ag_release: world=%d rank=%d", ag->world, ag->rank);
+  StreamValueFn write = write_value64();
+  if (!write) return fail(MUX_ERR_UNSUPPORTED, "stream memory operations unavailable");
+  for (int s2 = 0; s2 < ag->world; ++s2) {
+    if (!ag->flags[s2]) return fail(MUX_ERR_INVALID_ARGUMENT, "ag: rank %d flags null", s2);
+    if (write(reinterpret_cast<CUstream>(stream),
+              reinterpret_cast<CUdeviceptr>(ag->flags[s2] + ag->world + ag->rank), ag->seq, 0) != CUDA_SUCCESS)
+      return fail(MUX_ERR_CUDA, "cuStreamWriteValue64 failed");
+  }
+  return MUX_OK;
+}
+
+mux_status mux_linear_fwd_ag(int32_t num_segs, const int32_t* seg_off, const int32_t* seg_task, int32_t num_adapters,
+                             const mux_adapter* adapters, int32_t max_rows, int32_t K, int32_t N, int32_t r_cap,
+                             const mux_ag* ag, const mux_bf16* W_, mux_bf16* Y_, mux_bf16* Hs_, void* workspace,
+                             size_t workspace_bytes, cudaStream_t stream) {
+  if (!ag || ag->rank < 0 || ag->rank >= MUX_RS_MAX_WORLD) return fail(MUX_ERR_INVALID_ARGUMENT, "ag is null/bad");
+  auto X = reinterpret_cast<const __nv_bfloat16*>(ag->recv[ag->rank]);
+  return linear_common(false, num_segs, seg_off, seg_task, num_adapters, adapters, max_rows, K, N, r_cap, X, X,
+                       reinterpret_cast<const __nv_bfloat16*>(W_), reinterpret_cast<__nv_bfloat16*>(Y_), nullptr,
+                       reinterpret_cast<__nv_bfloat16*>(Hs_), workspace, workspace_bytes, stream, 3, nullptr, ag);
+}
+
+mux_status mux_linear_bwd_ag(int32_t num_segs, const int32_t* seg_off, const int32_t* seg_task, int32_t num_adapters,
+                             const mux_adapter* adapters, int32_t max_rows, int32_t K, int32_t N, int32_t r_cap,
+                             const mux_ag* ag, const mux_bf16* X_, const mux_bf16* W_, const mux_bf16* Hs_,
+                             mux_bf16* dX_, void* workspace, size_t workspace_bytes, cudaStream_t stream) {
+  if (!ag || ag->rank < 0 || ag->rank >= MUX_RS_MAX_WORLD) return fail(MUX_ERR_INVALID_ARGUMENT, "ag is null/bad");
+  return linear_common(true, num_segs, seg_off, seg_task, num_adapters, adapters, max_rows, K, N, r_cap,
+                       reinterpret_cast<const __nv_bfloat16*>(ag->recv[ag->rank]),
+                       reinterpret_cast<const __nv_bfloat16*>(X_), reinterpret_cast<const __nv_bfloat16*>(W_),
+                       reinterpret_cast<__nv_bfloat16*>(dX_), reinterpret_cast<const __nv_bfloat16*>(Hs_), nullptr,
+                       workspace, workspace_bytes, stream, 3, nullptr, ag);
+}
 
 }  // extern "C"

@@ -30,7 +30,8 @@ EXPORTS = ("mux_last_error", "mux_version", "mux_pack_bound_rows", "mux_pack_wor
            "mux_pack_chunks", "mux_pack_apply", "mux_linear_workspace_size", "mux_linear_fwd",
            "mux_linear_bwd", "mux_linear_bwd_part", "mux_pack_row_start", "mux_attn_fwd", "mux_attn_workspace_size", "mux_attn_bwd",
            "mux_rope", "mux_rmsnorm_fwd", "mux_rmsnorm_bwd", "mux_swiglu_fwd", "mux_swiglu_bwd", "mux_add", "mux_rs_flags_elems", "mux_linear_fwd_rs",
-           "mux_linear_bwd_dx_rs", "mux_rs_reduce")
+           "mux_linear_bwd_dx_rs", "mux_rs_reduce", "mux_ag_push", "mux_ag_release", "mux_linear_fwd_ag",
+           "mux_linear_bwd_ag")
 
 
 class MuxError(RuntimeError):
@@ -115,6 +116,14 @@ def lib():
         L.mux_linear_bwd_dx_rs.argtypes = [I32, P, P, I32, P, I32, I32, I32, I32, P, P, P, P, P, P, SZ, P]
         L.mux_rs_reduce.restype = ctypes.c_int
         L.mux_rs_reduce.argtypes = [P, I32, P, I64, P]
+        L.mux_ag_push.restype = ctypes.c_int
+        L.mux_ag_push.argtypes = [P, P, I64, I32, P]
+        L.mux_ag_release.restype = ctypes.c_int
+        L.mux_ag_release.argtypes = [P, P]
+        L.mux_linear_fwd_ag.restype = ctypes.c_int
+        L.mux_linear_fwd_ag.argtypes = [I32, P, P, I32, P, I32, I32, I32, I32, P, P, P, P, P, SZ, P]
+        L.mux_linear_bwd_ag.restype = ctypes.c_int
+        L.mux_linear_bwd_ag.argtypes = [I32, P, P, I32, P, I32, I32, I32, I32, P, P, P, P, P, P, SZ, P]
         _lib = L
     return _lib
 
@@ -473,3 +482,61 @@ def rs_reduce(rs: _Rs, out: torch.Tensor, stream=None) -> torch.Tensor:
     """mux_rs_reduce: out [rows_per_rank, cols] = sum of the world partial slots (owner side)."""
     _check(lib().mux_rs_reduce(ctypes.byref(rs), out.shape[1], _ptr(out), _ld(out), _stream(stream)))
     return out
+
+
+# ---------------------------------------------------------------- fused all-gather -> GEMM
+make_ag = make_rs   # same descriptor layout: recv[d] = rank d's gather buffer
+
+
+def ag_push(ag: _Rs, rows: torch.Tensor, stream=None):
+    """mux_ag_push: copy this rank's rows [rows_per_rank, cols] into every rank's gather buffer
+    (copy engines) and signal each destination."""
+    _check(lib().mux_ag_push(ctypes.byref(ag), _ptr(rows), _ld(rows), rows.shape[1], _stream(stream)))
+
+
+def ag_release(ag: _Rs, stream=None):
+    """mux_ag_release: this rank is done with its gather buffer for call ag.seq."""
+    _check(lib().mux_ag_release(ctypes.byref(ag), _stream(stream)))
+
+
+def linear_fwd_ag(ag: _Rs, seg_off, seg_task, adapters, K: int, W, r_cap: int, Y=None, Hs=None, workspace=None,
+                  stream=None):
+    """mux_linear_fwd_ag: forward on the gather buffer (rows read as they land)."""
+    max_rows = ag.world * ag.rows_per_rank
+    N = W.shape[0]
+    dev = W.device
+    if Y is None:
+        Y = torch.empty(max_rows, N, dtype=torch.bfloat16, device=dev)
+    if Hs is None:
+        Hs = torch.empty(max_rows, r_cap, dtype=torch.bfloat16, device=dev)
+    S = len(seg_task)
+    if workspace is None:
+        workspace = torch.zeros(linear_workspace_size(S, max_rows, K, N, r_cap), dtype=torch.uint8, device=dev)
+    _check(lib().mux_linear_fwd_ag(S, _ptr(seg_off), _i32_host(seg_task), len(adapters),
+                                   _adapter_table(adapters, False), max_rows, K, N, r_cap, ctypes.byref(ag),
+                                   _ptr(W), _ptr(Y), _ptr(Hs), _ptr(workspace), workspace.numel(), _stream(stream)))
+    return Y, Hs
+
+
+def linear_bwd_ag(ag: _Rs, seg_off, seg_task, adapters, X, W, Hs, r_cap: int, dX=None, workspace=None,
+                  stream=None):
+    """mux_linear_bwd_ag: backward with dY = the gather buffer (rows read as they land)."""
+    max_rows, K = X.shape
+    N = W.shape[0]
+    dev = X.device
+    if dX is None:
+        dX = torch.empty(max_rows, K, dtype=torch.bfloat16, device=dev)
+    for a in adapters:
+        if a.rank > 0:
+            if a.dA is None:
+                a.dA = torch.empty(a.rank, K, dtype=torch.float32, device=dev)
+            if a.dB is None:
+                a.dB = torch.empty(N, a.rank, dtype=torch.float32, device=dev)
+    S = len(seg_task)
+    if workspace is None:
+        workspace = torch.zeros(linear_workspace_size(S, max_rows, K, N, r_cap), dtype=torch.uint8, device=dev)
+    _check(lib().mux_linear_bwd_ag(S, _ptr(seg_off), _i32_host(seg_task), len(adapters),
+                                   _adapter_table(adapters, True), max_rows, K, N, r_cap, ctypes.byref(ag),
+                                   _ptr(X), _ptr(W), _ptr(Hs), _ptr(dX), _ptr(workspace), workspace.numel(),
+                                   _stream(stream)))
+    return dX

@@ -141,3 +141,51 @@ def test_rs_rejects_bad_layout():
         mux.linear_fwd_rs(mux.make_rs(2, 0, 256, 1, recv, flags), so, [0], ads, X[:256], W, 16)
     with pytest.raises(mux.MuxError):   # seq 0
         mux.linear_fwd_rs(mux.make_rs(2, 0, 256, 0, recv, flags), so, [0], ads, X, W, 16)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_all_gather_fused_gemm(world):
+    """mux_ag_push (copy engines, on a copy stream) + mux_linear_fwd_ag / mux_linear_bwd_ag (the
+    producer waits per row block for its owner's rows) + mux_ag_release, world simulated ranks on
+    one GPU, three calls reusing the gather buffers: every rank's result == the plain kernels on the
+    full input, bit for bit (the gather buffer holds exactly the full input)."""
+    g = torch.Generator(device="cuda").manual_seed(300 + world)
+    rows_per_rank = 256
+    R, K, N = world * rows_per_rank, 192, 320
+    seg_off = torch.tensor([0, 128, 320, R], dtype=torch.int32, device="cuda")
+    st, ranks = [0, 1, 2], [16, 4, 8]
+    W = (torch.randn(N, K, device="cuda", generator=g) / K ** 0.5).bfloat16()
+    ads = _adapters(g, ranks, K, N)
+    gx = [torch.zeros(R * K, dtype=torch.bfloat16, device="cuda") for _ in range(world)]    # gather X
+    gd = [torch.zeros(R * N, dtype=torch.bfloat16, device="cuda") for _ in range(world)]    # gather dY
+    fx = [torch.zeros(mux.rs_flags_elems(world), dtype=torch.int64, device="cuda") for _ in range(world)]
+    fd = [torch.zeros(mux.rs_flags_elems(world), dtype=torch.int64, device="cuda") for _ in range(world)]
+    copy = torch.cuda.Stream()
+    for seq in (1, 2, 3):
+        X = torch.randn(R, K, device="cuda", generator=g).bfloat16()
+        dY = torch.randn(R, N, device="cuda", generator=g).bfloat16()
+        agx = [mux.make_ag(world, p, rows_per_rank, seq, gx, fx) for p in range(world)]
+        agd = [mux.make_ag(world, p, rows_per_rank, seq, gd, fd) for p in range(world)]
+        ev = torch.cuda.Event()
+        ev.record()
+        copy.wait_event(ev)   # the inputs of this call are ready
+        for p in range(world):
+            mux.ag_push(agx[p], X[p * rows_per_rank:(p + 1) * rows_per_rank], stream=copy)
+            mux.ag_push(agd[p], dY[p * rows_per_rank:(p + 1) * rows_per_rank], stream=copy)
+        outs = []
+        for p in range(world):
+            pads = [mux.Adapter(a.A, a.B, a.rank, a.scale) for a in ads]
+            Y, Hs = mux.linear_fwd_ag(agx[p], seg_off, st, pads, K, W, 16)
+            dX = mux.linear_bwd_ag(agd[p], seg_off, st, pads, gx[p].view(R, K), W, Hs, 16)
+            mux.ag_release(agx[p])
+            mux.ag_release(agd[p])
+            outs.append((Y, dX, pads))
+        Yr, Hsr = mux.linear_fwd(seg_off, st, ads, X, W, 16)
+        dXr = mux.linear_bwd(seg_off, st, ads, dY, X, W, Hsr, 16)
+        torch.cuda.synchronize()
+        for p, (Y, dX, pads) in enumerate(outs):
+            assert torch.equal(_bits(Y), _bits(Yr)), (seq, p)
+            assert torch.equal(_bits(dX), _bits(dXr)), (seq, p)
+            for a, b in zip(pads, ads):
+                assert torch.equal(a.dA, b.dA) and torch.equal(a.dB, b.dB)
+    torch.cuda.current_stream().wait_stream(copy)
