@@ -563,7 +563,7 @@ def tp_arm(args):
         S_h = int(off[-1])
         bound = int(mux.pack_bound_rows(T_h, S_h, 64))
         # row blocks split evenly over ranks (256-row blocks for the fused reduce-scatter)
-        blk = 256 if args.fused_rs else 64
+        blk = 256 if (args.fused_rs or args.fused_ag) else 64
         max_rows = -(-bound // (blk * world)) * blk * world
         pk = mux.alloc_pack_outputs(len(tasks), S_h, max_rows, max_rows // 64)
         be = tp.MuxBackend()
@@ -577,7 +577,7 @@ def tp_arm(args):
             shard = tp.shard_column if kinds[li] == "col" else tp.shard_row
             _, ap_ = shard(torch.empty(L.N, L.K, dtype=torch.bfloat16, device="meta"), ads, world, rank, mk)
             cls = tp.ColumnParallelMuxLinear if kinds[li] == "col" else tp.RowParallelMuxLinear
-            layers.append(cls(be, Wsh[li], ap_, r_cap, fused_rs=args.fused_rs))
+            layers.append(cls(be, Wsh[li], ap_, r_cap, fused_rs=args.fused_rs, fused_ag=args.fused_ag))
         rows = max_rows // world
         nl = w.linears[-1].N // world
         ht = {"tasks": tasks, "T": T_h, "max_rows": max_rows, "rows": rows, "pk": pk, "layers": layers,
@@ -631,6 +631,8 @@ def tp_arm(args):
                                      "nccl_max_ctas": args.comm_ctas or None, "planner": plan_note,
                                      "reduce_scatter": "fused into the GEMM epilogue (peer stores)" if args.fused_rs
                                      else "NCCL",
+                                     "all_gather": "copy-engine push, consumed per row block by the GEMM"
+                                     if args.fused_ag else "NCCL",
                                      "max_rows": [ht["max_rows"] for ht in htasks]},
                           "tflops_per_gpu_algorithmic": w.flops / (ms * 1e-3) / 1e12 / world}), flush=True)
     dist.destroy_process_group()
@@ -752,6 +754,8 @@ def main():
     ap.add_argument("--comm-ctas", type=int, default=0, help="--mode tp: NCCL_MAX_CTAS for the overlapped collectives")
     ap.add_argument("--fused-rs", action="store_true",
                     help="--mode tp: reduce-scatters fused into the GEMMs (peer stores via symmetric memory)")
+    ap.add_argument("--fused-ag", action="store_true",
+                    help="--mode tp: all-gathers pushed by the copy engines, consumed inside the GEMMs")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

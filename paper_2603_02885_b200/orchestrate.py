@@ -236,7 +236,13 @@ def linear_chain_ops(layers: Sequence, kinds: Sequence[str], seg_off, seg_task, 
     comp("dispatch", (), ("x_rows",), lambda e: e.__setitem__("x_rows", x_rows_fn(e)))
     cur = "x_rows"
     for i, (lay, kind) in enumerate(zip(layers, kinds)):
-        if kind == "col":
+        if kind == "col" and getattr(lay, "fused_ag", False):
+            # the all-gather is pushed by the copy engines and consumed inside the GEMM
+            def fwd(e, i=i, src=cur, lay=lay):
+                e[f"Y{i}"], lay.Hs, lay.X = lay.be.fwd_ag(lay, seg_off, seg_task, e[src])
+            comp(f"fwd{i}", (cur,), (f"Y{i}",), fwd, flops_per_layer[i])
+            cur = f"Y{i}"
+        elif kind == "col":
             def ag(e, i=i, src=cur, lay=lay):
                 x = e[src]
                 p = dist.get_world_size(group)
@@ -282,6 +288,7 @@ def linear_chain_ops(layers: Sequence, kinds: Sequence[str], seg_off, seg_task, 
         if kind == "col" and getattr(lay, "fused_rs", False):
             def bwd(e, i=i, src=g, lay=lay):
                 e[f"dX{i}"], e[f"dA{i}"], e[f"dB{i}"] = lay.be.bwd_rs(lay, seg_off, seg_task, e[src])
+                lay.release_ag()
             comp(f"bwd{i}", (g,), (f"dX{i}", f"dA{i}", f"dB{i}"), bwd, flops_per_layer[i])
             comm(f"AR(dA{i})", (f"dA{i}",), (f"dA{i}:sum",), lambda e, i=i: all_reduce_async(e[f"dA{i}"], group))
             g = f"dX{i}"
@@ -289,6 +296,8 @@ def linear_chain_ops(layers: Sequence, kinds: Sequence[str], seg_off, seg_task, 
             def bwd(e, i=i, src=g, lay=lay):
                 dXp, dA, dB = lay.be.bwd(seg_off, seg_task, lay.ads, e[src], lay.X, lay.W, lay.Hs, lay.r_cap)
                 e[f"dXp{i}"], e[f"dA{i}"], e[f"dB{i}"] = dXp, dA, dB
+                if hasattr(lay, "release_ag"):
+                    lay.release_ag()
             comp(f"bwd{i}", (g,), (f"dXp{i}", f"dA{i}", f"dB{i}"), bwd, flops_per_layer[i])
             comm(f"AR(dA{i})", (f"dA{i}",), (f"dA{i}:sum",), lambda e, i=i: all_reduce_async(e[f"dA{i}"], group))
 
@@ -299,6 +308,12 @@ def linear_chain_ops(layers: Sequence, kinds: Sequence[str], seg_off, seg_task, 
                 e[f"dX{i}"] = out
                 return reduce_scatter_rows_async(d, out, group)
             comm(f"RS(dx{i})", (f"dXp{i}",), (f"dX{i}",), rs)
+            g = f"dX{i}"
+        elif getattr(lay, "fused_ag", False):
+            def bwd(e, i=i, src=g, lay=lay):
+                e[f"dX{i}"], e[f"dA{i}"], e[f"dB{i}"] = lay.be.bwd_ag(lay, seg_off, seg_task, e[src])
+            comp(f"bwd{i}", (g,), (f"dX{i}", f"dA{i}", f"dB{i}"), bwd, flops_per_layer[i])
+            comm(f"AR(dB{i})", (f"dB{i}",), (f"dB{i}:sum",), lambda e, i=i: all_reduce_async(e[f"dB{i}"], group))
             g = f"dX{i}"
         else:
             def ag(e, i=i, src=g):

@@ -155,6 +155,49 @@ class MuxBackend:
             lay._rs = FusedRs(lay.group, rows, cols, device, exchange=self.rs_exchange)
         return lay._rs
 
+    # fused all-gather (copy-engine push + per-row-block waits in the GEMM producer)
+    def _ag_for(self, lay, attr, rows, cols, device):
+        cur = getattr(lay, attr, None)
+        if cur is None or cur.rows != rows or cur.cols != cols:
+            cur = FusedRs(lay.group, rows, cols, device, exchange=self.rs_exchange)
+            setattr(lay, attr, cur)
+        return cur
+
+    def _push(self, ag, rows_t):
+        if getattr(self, "copy_stream", None) is None:
+            self.copy_stream = torch.cuda.Stream()
+        ev = torch.cuda.Event()
+        ev.record()
+        self.copy_stream.wait_event(ev)           # this rank's rows are ready
+        self.mux.ag_push(ag, rows_t, stream=self.copy_stream)
+
+    def fwd_ag(self, lay, seg_off, seg_task, x_rows):
+        p, _ = _world(lay.group)
+        rows, K = x_rows.shape
+        fb = self._ag_for(lay, "_ag", rows, K, x_rows.device)
+        ag = fb.next()
+        self._push(ag, x_rows)
+        R, N = rows * p, lay.W.shape[0]
+        Y = self._buf(("Y", lay.W.data_ptr()), (R, N), torch.bfloat16, x_rows.device)
+        Hs = self._buf(("Hs", lay.W.data_ptr()), (R, lay.r_cap), torch.bfloat16, x_rows.device)
+        ws = self._ws(lay.W, fb.recv.view(R, K), seg_task, lay.r_cap)
+        self.mux.linear_fwd_ag(ag, seg_off, seg_task, lay.ads, K, lay.W, lay.r_cap, Y=Y, Hs=Hs, workspace=ws)
+        lay._ag_held = ag                         # released after the backward re-read X
+        return Y, Hs, fb.recv.view(R, K)
+
+    def bwd_ag(self, lay, seg_off, seg_task, dy_rows):
+        p, _ = _world(lay.group)
+        rows, N = dy_rows.shape
+        fb = self._ag_for(lay, "_ag", rows, N, dy_rows.device)
+        ag = fb.next()
+        self._push(ag, dy_rows)
+        X = lay.X
+        dX = self._buf(("dX", lay.W.data_ptr()), tuple(X.shape), torch.bfloat16, X.device)
+        self.mux.linear_bwd_ag(ag, seg_off, seg_task, lay.ads, X, lay.W, lay.Hs, lay.r_cap, dX=dX,
+                               workspace=self._ws(lay.W, X, seg_task, lay.r_cap))
+        self.mux.ag_release(ag)                   # dY fully consumed (dX GEMM + gradients)
+        return dX, [a.dA for a in lay.ads], [a.dB for a in lay.ads]
+
     def fwd_rs(self, lay, seg_off, seg_task, X):
         p, _ = _world(lay.group)
         R, N = X.shape[0], lay.W.shape[0]
@@ -209,13 +252,16 @@ def shard_row(W: torch.Tensor, adapters: Sequence, p: int, r: int, make_adapter)
 
 
 class ColumnParallelMuxLinear:
-    def __init__(self, backend, W_shard, adapters_shard, r_cap, group=None, fused_rs=False):
+    def __init__(self, backend, W_shard, adapters_shard, r_cap, group=None, fused_rs=False, fused_ag=False):
         self.be, self.W, self.ads, self.r_cap, self.group = backend, W_shard, adapters_shard, r_cap, group
-        self.fused_rs = fused_rs
-        self._rs = None
+        self.fused_rs, self.fused_ag = fused_rs, fused_ag
+        self._rs = self._ag = self._ag_held = None
 
     def forward(self, seg_off, seg_task, x_rows):
         """x_rows [R/p, K] (this rank's row block) -> Y_p [R, N/p]."""
+        if self.fused_ag:
+            Y, self.Hs, self.X = self.be.fwd_ag(self, seg_off, seg_task, x_rows)
+            return Y
         self.X = all_gather_rows(x_rows, self.group)
         Y, self.Hs = self.be.fwd(seg_off, seg_task, self.ads, self.X, self.W, self.r_cap)
         return Y
@@ -230,14 +276,21 @@ class ColumnParallelMuxLinear:
         for g in dA:
             if g is not None:
                 all_reduce_(g, self.group)
+        self.release_ag()
         return (reduce_scatter_rows(dXp, self.group) if dX_rows is None else dX_rows), dA, dB
+
+    def release_ag(self):
+        """The gathered X is no longer needed (after the backward): its owners may push again."""
+        if self._ag_held is not None:
+            self.be.mux.ag_release(self._ag_held)
+            self._ag_held = None
 
 
 class RowParallelMuxLinear:
-    def __init__(self, backend, W_shard, adapters_shard, r_cap, group=None, fused_rs=False):
+    def __init__(self, backend, W_shard, adapters_shard, r_cap, group=None, fused_rs=False, fused_ag=False):
         self.be, self.W, self.ads, self.r_cap, self.group = backend, W_shard, adapters_shard, r_cap, group
-        self.fused_rs = fused_rs
-        self._rs = None
+        self.fused_rs, self.fused_ag = fused_rs, fused_ag
+        self._rs = self._ag = None
 
     def forward(self, seg_off, seg_task, x_cols):
         """x_cols [R, K/p] (this rank's column shard) -> Y rows [R/p, N]."""
@@ -250,8 +303,11 @@ class RowParallelMuxLinear:
 
     def backward(self, seg_off, seg_task, dy_rows):
         """dY rows [R/p, N] -> dX_p [R, K/p]; dB_t all-reduced, dA_{t,p} local."""
-        dY = all_gather_rows(dy_rows, self.group)
-        dXp, dA, dB = self.be.bwd(seg_off, seg_task, self.ads, dY, self.X, self.W, self.Hs, self.r_cap)
+        if self.fused_ag:
+            dXp, dA, dB = self.be.bwd_ag(self, seg_off, seg_task, dy_rows)
+        else:
+            dY = all_gather_rows(dy_rows, self.group)
+            dXp, dA, dB = self.be.bwd(seg_off, seg_task, self.ads, dY, self.X, self.W, self.Hs, self.r_cap)
         for g in dB:
             if g is not None:
                 all_reduce_(g, self.group)

@@ -1,5 +1,7 @@
 """Two processes, one GPU: tensor parallelism with the reduce-scatter fused
-into the GEMM epilogue (tp.py fused_rs=True), across real process boundaries.
+into the GEMM epilogue (tp.py fused_rs=True) and, optionally, the all-gather
+pushed by the copy engines and consumed inside the GEMM (fused_ag=True),
+across real process boundaries.
 Both ranks live on cuda:0 (the box has one GPU), so the "peer" stores go
 through CUDA IPC mappings of the other process's buffers instead of NVLink,
 and the ready/ack flags are exchanged between processes exactly as between
@@ -52,7 +54,7 @@ def _problem():
     return W1, a1, W2, a2, X, dY
 
 
-def _worker(rank, world, port, q, boxes):
+def _worker(rank, world, port, q, boxes, fused_ag):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch.distributed as dist
     torch.cuda.set_device(0)
@@ -80,8 +82,8 @@ def _worker(rank, world, port, q, boxes):
         be.rs_exchange = exchange
         W1p, a1p = tp.shard_column(W1, a1, world, rank, mk)
         W2p, a2p = tp.shard_row(W2, a2, world, rank, mk)
-        up = tp.ColumnParallelMuxLinear(be, W1p, a1p, 32, fused_rs=True)
-        down = tp.RowParallelMuxLinear(be, W2p, a2p, 32, fused_rs=True)
+        up = tp.ColumnParallelMuxLinear(be, W1p, a1p, 32, fused_rs=True, fused_ag=fused_ag)
+        down = tp.RowParallelMuxLinear(be, W2p, a2p, 32, fused_rs=True, fused_ag=fused_ag)
         rows = R // world
         for _ in range(2):   # twice: receive slots and flags reused
             h = up.forward(seg_off, st, X[rank * rows:(rank + 1) * rows].contiguous())
@@ -106,7 +108,8 @@ def _free_port():
     return p
 
 
-def test_fused_rs_two_processes_one_gpu():
+@pytest.mark.parametrize("fused_ag", [False, True])
+def test_fused_rs_two_processes_one_gpu(fused_ag):
     from paper_2603_02885_b200 import mux
     from gpu_harness import TOL, rel_err
     world = 2
@@ -114,7 +117,7 @@ def test_fused_rs_two_processes_one_gpu():
     q = ctx.Queue()
     port = _free_port()
     boxes = [ctx.Queue() for _ in range(world)]
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q, boxes)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, boxes, fused_ag)) for r in range(world)]
     for p in procs:
         p.start()
     res = sorted([q.get(timeout=300) for _ in range(world)], key=lambda x: x[0])
