@@ -19,6 +19,7 @@
 namespace mux {
 cudaError_t launch_gemm(const GemmParams& p, bool bwd, int grid, cudaStream_t stream);
 cudaError_t launch_grad(const GradParams& p, int grid, cudaStream_t stream);
+cudaError_t launch_grad_simt(const GradParams& p, int grid, cudaStream_t stream);
 size_t pack_workspace_bytes(int M, int S);
 cudaError_t launch_pack(int M, int S, const int32_t* task_seq_off, const int32_t* seq_len,
                         const int32_t* pack_capacity, int chunk_size, int chunk_min, int max_rows, int max_chunks,
@@ -437,6 +438,9 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
   }
   // raster band: keep the band's A rows (group_m * 256 rows * kred * 2 B)
   // within ~48 MB of the 126 MB L2, leaving room for the streamed W tiles
+#ifndef MUX_GRAD_SIMT_MAX_RANK
+#define MUX_GRAD_SIMT_MAX_RANK 0
+#endif
 #ifndef MUX_BAND_MB
 #define MUX_BAND_MB 48
 #endif
@@ -484,6 +488,7 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
     g.r_cap = r_cap;
     bool want_a = false, want_b = false;
     int nt = 0;
+    int max_rank = 0;
     for (int t = 0; t < num_adapters; ++t) {
       const mux_adapter& a = adapters[t];
       if (a.rank == 0 || (!a.dA && !a.dB)) continue;
@@ -496,6 +501,7 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
       g.task_dB[nt] = a.dB;
       want_a |= a.dA != nullptr;
       want_b |= a.dB != nullptr;
+      max_rank = std::max(max_rank, a.rank);
       ++nt;
     }
     g.num_tasks = nt;
@@ -507,7 +513,9 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
       // units) instead of leaving a ragged last wave on 148 CTAs
       const long long waves = (units + num_sms() - 1) / num_sms();
       const int ggrid = static_cast<int>((units + waves - 1) / waves);
-      e = launch_grad(g, ggrid, stream);
+      // tensor cores (grad.cu) unless every rank is at most MUX_GRAD_SIMT_MAX_RANK, then
+      // the CUDA-core kernel (grad_simt.cu); the default comes from the A/B in DESIGN §6.2
+      e = max_rank <= MUX_GRAD_SIMT_MAX_RANK ? launch_grad_simt(g, ggrid, stream) : launch_grad(g, ggrid, stream);
       if (e != cudaSuccess) return cuda_fail(e, "mux_linear_bwd grad launch");
     }
   }

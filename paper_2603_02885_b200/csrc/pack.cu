@@ -22,6 +22,14 @@
 namespace mux {
 
 constexpr int kPackThreads = 1024;
+
+// -DMUX_PACK_PROFILE: thread 0 records clock64() at each phase boundary and
+// prints the deltas (diagnostic builds only, tools/pack_time.py).
+#ifdef MUX_PACK_PROFILE
+#define PACK_MARK(i) do { if (threadIdx.x == 0) _pt[i] = clock64(); } while (0)
+#else
+#define PACK_MARK(i) do { } while (0)
+#endif
 constexpr int kPackWarps = kPackThreads / 32;
 
 struct PackWs {  // carved from the caller's workspace
@@ -32,6 +40,7 @@ struct PackWs {  // carved from the caller's workspace
   int32_t* pack_len;    // [num_seqs] same indexing: pack length
   int32_t* pack_row0;   // [num_seqs] same indexing: first row of the pack
   int32_t* tok_off;     // [num_seqs + 1] exclusive prefix of lengths
+  int32_t* seq_task;    // [num_seqs] task of sequence i (= task of pack slot i)
   int32_t* task_packs;  // [M]
   int32_t* task_chunks; // [M]
 };
@@ -40,7 +49,7 @@ __host__ __device__ inline size_t align256(size_t x) { return (x + 255) & ~size_
 
 __host__ __device__ inline size_t pack_ws_bytes(int M, int S) {
   const size_t s = align256(sizeof(int32_t) * (size_t)(S + 1));
-  return 7 * s + 2 * align256(sizeof(int32_t) * (size_t)(M > 0 ? M : 1));
+  return 8 * s + 2 * align256(sizeof(int32_t) * (size_t)(M > 0 ? M : 1));
 }
 
 // Shared-memory variant: every per-sequence / per-task array lives in smem
@@ -49,7 +58,7 @@ constexpr int kPackSmemMaxBytes = 200 * 1024;
 
 __host__ __device__ inline size_t pack_smem_bytes(int M, int S) {
   // workspace arrays + staged copies of seq_len [S], task_seq_off [M+1], capacity [M]
-  return 8 * align256(sizeof(int32_t) * (size_t)(S + 1)) + 4 * align256(sizeof(int32_t) * (size_t)(M + 1));
+  return 9 * align256(sizeof(int32_t) * (size_t)(S + 1)) + 4 * align256(sizeof(int32_t) * (size_t)(M + 1));
 }
 
 __device__ inline PackWs carve_pack_ws(void* ws, int M, int S) {
@@ -64,6 +73,7 @@ __device__ inline PackWs carve_pack_ws(void* ws, int M, int S) {
   w.pack_len = reinterpret_cast<int32_t*>(b); b += s;
   w.pack_row0 = reinterpret_cast<int32_t*>(b); b += s;
   w.tok_off = reinterpret_cast<int32_t*>(b); b += s;
+  w.seq_task = reinterpret_cast<int32_t*>(b); b += s;
   w.task_packs = reinterpret_cast<int32_t*>(b); b += m;
   w.task_chunks = reinterpret_cast<int32_t*>(b);
   return w;
@@ -98,7 +108,11 @@ __global__ void __launch_bounds__(kPackThreads, 1)
   const int warp = tid >> 5;
   const int lane = tid & 31;
   PackWs ws = carve_pack_ws(use_smem ? static_cast<void*>(pack_smem) : workspace, M, S);
+#ifdef MUX_PACK_PROFILE
+  long long _pt[10] = {0};
+#endif
   griddep_wait();  // PDL: inputs may come from the previous kernel
+  PACK_MARK(0);
   griddep_launch_dependents();
   // Stage the (small) inputs in shared memory when they fit: every later
   // phase re-reads them, and a dependent global round trip per phase was the
@@ -107,7 +121,7 @@ __global__ void __launch_bounds__(kPackThreads, 1)
   const int32_t* tso = task_seq_off;
   const int32_t* capp = pack_capacity;
   if (use_smem) {
-    uint8_t* b = pack_smem + 7 * align256(sizeof(int32_t) * (size_t)(S + 1)) +
+    uint8_t* b = pack_smem + 8 * align256(sizeof(int32_t) * (size_t)(S + 1)) +
                  2 * align256(sizeof(int32_t) * (size_t)(M > 0 ? M : 1));
     int32_t* s_sl = reinterpret_cast<int32_t*>(b);
     b += align256(sizeof(int32_t) * (size_t)(S + 1));
@@ -124,6 +138,7 @@ __global__ void __launch_bounds__(kPackThreads, 1)
     capp = pack_capacity != nullptr ? s_cap : nullptr;
   }
 
+  PACK_MARK(1);
   // ---- 1. chunk size, validity, max length, valid rows -------------------
   int v2min = 30, bad = 0, mx = 0, sum = 0;
   for (int i = tid; i < S; i += kPackThreads) {
@@ -165,6 +180,7 @@ __global__ void __launch_bounds__(kPackThreads, 1)
     return;
   }
 
+  PACK_MARK(2);
   // ---- 2. FFD visit order per task: rank by (len desc, index asc) ---------
   for (int i = tid; i < S; i += kPackThreads) {
     // task of sequence i: binary search in task_seq_off
@@ -174,6 +190,7 @@ __global__ void __launch_bounds__(kPackThreads, 1)
       if (tso[mid] <= i) lo = mid; else hi = mid;
     }
     const int t0 = tso[lo], t1 = tso[lo + 1];
+    ws.seq_task[i] = lo;
     const int L = sl[i];
     int rank = 0;
     for (int j = t0; j < t1; ++j) {
@@ -184,6 +201,7 @@ __global__ void __launch_bounds__(kPackThreads, 1)
   }
   __syncthreads();
 
+  PACK_MARK(3);
   // ---- 3. first-fit decreasing, one warp per task -------------------------
   for (int t = warp; t < M; t += kPackWarps) {
     const int t0 = tso[t], n = tso[t + 1] - t0;
@@ -245,30 +263,39 @@ __global__ void __launch_bounds__(kPackThreads, 1)
     return;
   }
 
+  PACK_MARK(4);
   // ---- 4. scan over tasks -> seg_off; overflow check ----------------------
-  if (tid == 0) {
+  if (warp == 0) {  // exclusive prefix of chunk counts, 32 tasks at a time
     int acc = 0, packs = 0;
-    for (int t = 0; t < M; ++t) {  // exclusive prefix of chunk counts
-      const int x = ws.task_chunks[t];
-      ws.task_chunks[t] = acc;
-      acc += x;
-      packs += ws.task_packs[t];
+    for (int base = 0; base < M; base += 32) {
+      const int t = base + lane;
+      const int v = t < M ? ws.task_chunks[t] : 0;
+      int x = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (t < M) ws.task_chunks[t] = acc + x - v;
+      acc += __shfl_sync(0xffffffffu, x, 31);
+      packs += warp_sum(t < M ? ws.task_packs[t] : 0);
     }
-    s_total_chunks = acc;
-
-    int ovf = 0;
-    if (acc * c > max_rows) ovf |= 1;
-    if (acc > max_chunks) ovf |= 2;
-    mux_pack_info r;
-    r.chunk_size = c;
-    r.num_chunks = acc;
-    r.num_packs = packs;
-    r.total_rows = acc * c;
-    r.valid_rows = s_valid;
-    r.zero_pad_rows = S * s_maxlen;
-    r.overflow = ovf;
-    *info = r;
-    s_ovf = ovf;  // separate flag: other threads may still be reading s_bad above
+    if (lane == 0) {
+      s_total_chunks = acc;
+      int ovf = 0;
+      if (acc * c > max_rows) ovf |= 1;
+      if (acc > max_chunks) ovf |= 2;
+      mux_pack_info r;
+      r.chunk_size = c;
+      r.num_chunks = acc;
+      r.num_packs = packs;
+      r.total_rows = acc * c;
+      r.valid_rows = s_valid;
+      r.zero_pad_rows = S * s_maxlen;
+      r.overflow = ovf;
+      *info = r;
+      s_ovf = ovf;  // separate flag: other threads may still be reading s_bad above
+    }
   }
   __syncthreads();
   if (s_ovf) return;
@@ -306,35 +333,53 @@ __global__ void __launch_bounds__(kPackThreads, 1)
   for (int r = total_chunks * c + tid; r < max_rows; r += kPackThreads) row_src[r] = -1;
   __syncthreads();
 
+  PACK_MARK(5);
   // ---- 5. fill ------------------------------------------------------------
-  // chunk table: one thread per (task, pack)
-  for (int t = 0; t < M; ++t) {
-    const int t0 = tso[t];
-    for (int p = tid; p < ws.task_packs[t]; p += kPackThreads) {
-      const int len = ws.pack_len[t0 + p];
-      const int n_p = (len + c - 1) / c;
-      const int id0 = ws.pack_row0[t0 + p] / c;
-      for (int j = 0; j < n_p; ++j) {
-        chunk_task[id0 + j] = t;
-        chunk_pack[id0 + j] = p;
-        chunk_valid[id0 + j] = min(c, len - j * c);
-        chunk_dep[id0 + j] = j > 0 ? id0 + j - 1 : -1;
-      }
-      // the pack's tail padding (its sequences fill [row0, row0 + len))
-      for (int r = id0 * c + len; r < (id0 + n_p) * c; ++r) row_src[r] = -1;
+  // Flat over all tasks at once (a serial loop over tasks was the kernel's
+  // critical path at 16-32 tasks): one warp per pack slot, then one warp per
+  // sequence; the lanes write a pack's chunks / tail rows and a sequence's
+  // rows in parallel.  Pack slot j of task t is ws.*[tso[t] + p], p < task_packs[t].
+  for (int j = warp; j < S; j += kPackWarps) {
+    const int t = ws.seq_task[j];
+    const int p = j - tso[t];
+    if (p >= ws.task_packs[t]) continue;
+    const int len = ws.pack_len[j];
+    const int n_p = (len + c - 1) / c;
+    const int id0 = ws.pack_row0[j] / c;
+    for (int q = lane; q < n_p; q += 32) {
+      chunk_task[id0 + q] = t;
+      chunk_pack[id0 + q] = p;
+      chunk_valid[id0 + q] = min(c, len - q * c);
+      chunk_dep[id0 + q] = q > 0 ? id0 + q - 1 : -1;
     }
+    // the pack's tail padding (its sequences fill [row0, row0 + len))
+    for (int r = id0 * c + len + lane; r < (id0 + n_p) * c; r += 32) row_src[r] = -1;
   }
   // seq_row and row_src: one warp per sequence
-  for (int t = 0; t < M; ++t) {
-    const int t0 = tso[t], t1 = tso[t + 1];
-    for (int s = t0 + warp; s < t1; s += kPackWarps) {
-      const int row = ws.pack_row0[t0 + ws.pack_of[s]] + ws.pack_off[s];
-      if (lane == 0) seq_row[s] = row;
-      const int L = sl[s];
-      const int tok = ws.tok_off[s];
-      for (int pos = lane; pos < L; pos += 32) row_src[row + pos] = tok + pos;
+  for (int s = warp; s < S; s += kPackWarps) {
+    const int row = ws.pack_row0[tso[ws.seq_task[s]] + ws.pack_of[s]] + ws.pack_off[s];
+    if (lane == 0) seq_row[s] = row;
+    const int L = sl[s];
+    const int tok = ws.tok_off[s];
+    // head up to a 16-byte boundary, then 4 rows per lane per int4 store, then the tail
+    const int head = min(L, static_cast<int>(((16u - (reinterpret_cast<uintptr_t>(row_src + row) & 15u)) & 15u) >> 2));
+    if (lane < head) row_src[row + lane] = tok + lane;
+    const int nvec = (L - head) >> 2;
+    int4* body = reinterpret_cast<int4*>(row_src + row + head);
+    for (int q = lane; q < nvec; q += 32) {
+      const int v = tok + head + 4 * q;
+      body[q] = make_int4(v, v + 1, v + 2, v + 3);
     }
+    const int done = head + 4 * nvec;
+    if (done + lane < L) row_src[row + done + lane] = tok + done + lane;
   }
+#ifdef MUX_PACK_PROFILE
+  __syncthreads();
+  PACK_MARK(6);
+  if (threadIdx.x == 0)
+    printf("pack_profile M=%d S=%d cycles: stage %lld chunk %lld order %lld ffd %lld scan+rows %lld fill %lld\n", M, S,
+           _pt[1] - _pt[0], _pt[2] - _pt[1], _pt[3] - _pt[2], _pt[4] - _pt[3], _pt[5] - _pt[4], _pt[6] - _pt[5]);
+#endif
 }
 
 // Dispatch gather: 16-byte vectors, one warp-row at a time.
