@@ -370,6 +370,12 @@ def main_arm(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_total = float(t.item())
     ms_step = ms_total / args.steps
+    # every rank packs its own tasks (own seed): value counts the valid tokens of all ranks
+    T_all = w.T
+    if world > 1:
+        tt = torch.tensor([w.T], dtype=torch.int64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.SUM)
+        T_all = int(tt.item())
 
     # roofline of the dominant kernel (fused tcgen05 GEMM, forward calls)
     fwd_ms = sum(a.elapsed_time(b) for (_, a, b) in ev_pairs["fwd"])
@@ -463,13 +469,13 @@ def main_arm(args):
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e_ms = float(te.item()) / args.steps
-        e2e = {"value": world * w.T / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+        e2e = {"value": T_all / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms,
                "what": "pinned H2D of seq metadata + token-major layer input X and loss gradient dY (prefetched "
                        "one step ahead on a copy stream); D2H of every adapter gradient dA_t/dB_t (fp32) on "
                        "the copy stream, overlapped with the next step's forward"}
 
-    value = world * w.T / (ms_step * 1e-3)
+    value = T_all / (ms_step * 1e-3)
     tflops = w.flops / (ms_step * 1e-3) / 1e12
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
