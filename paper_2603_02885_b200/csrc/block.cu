@@ -177,72 +177,104 @@ __global__ void __launch_bounds__(kNormThreads) mux_rmsnorm_bwd_kernel(int dim, 
 // ------------------------------------------------------------------ SwiGLU
 __device__ __forceinline__ float sigmoidf_(float z) { return 1.f / (1.f + __expf(-z)); }
 
-__global__ void __launch_bounds__(256) mux_swiglu_fwd_kernel(int rows, int dim, const uint4* g, long long ldg,
-                                                            const uint4* u, long long ldu, uint4* h,
-                                                            long long ldh) {
+// Elementwise kernels: blocks stride over rows, threads over 16-byte column
+// chunks, two chunks per thread per step so each thread has 2 x (inputs)
+// loads in flight (no 64-bit index division in the loop).
+#define MUX_ROWWISE_LOOP(body)                                                       \
+  const int nc = dim / 8;                                                            \
+  for (int r = blockIdx.x; r < rows; r += gridDim.x) {                               \
+    for (int c0 = threadIdx.x; c0 < nc; c0 += 2 * blockDim.x) {                      \
+      const int c1 = c0 + blockDim.x;                                                \
+      body(c0, c1 < nc, c1)                                                          \
+    }                                                                                \
+  }
+
+__global__ void __launch_bounds__(256) mux_swiglu_fwd_kernel(int rows, int dim, const uint4* __restrict__ g,
+                                                            long long ldg, const uint4* __restrict__ u,
+                                                            long long ldu, uint4* __restrict__ h, long long ldh) {
   griddep_wait();
   griddep_launch_dependents();
-  const int nc = dim / 8;
-  const long long total = static_cast<long long>(rows) * nc;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long r = i / nc;
-    const int c = static_cast<int>(i - r * nc);
-    float a[8], b[8];
-    bf16x8_to_f32(g[r * ldg + c], a);
-    bf16x8_to_f32(u[r * ldu + c], b);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) a[k] = a[k] * sigmoidf_(a[k]) * b[k];
-    h[r * ldh + c] = f32_to_bf16x8(a);
+#define SWIGLU_FWD(c0, two, c1)                                                       \
+  const uint4 g0 = g[r * ldg + c0], u0 = u[r * ldu + c0];                             \
+  uint4 g1 = make_uint4(0, 0, 0, 0), u1 = g1;                                          \
+  if (two) { g1 = g[r * ldg + c1]; u1 = u[r * ldu + c1]; }                             \
+  float a[8], b[8];                                                                    \
+  bf16x8_to_f32(g0, a);                                                                \
+  bf16x8_to_f32(u0, b);                                                                \
+  _Pragma("unroll") for (int k = 0; k < 8; ++k) a[k] = a[k] * sigmoidf_(a[k]) * b[k];  \
+  h[r * ldh + c0] = f32_to_bf16x8(a);                                                  \
+  if (two) {                                                                           \
+    bf16x8_to_f32(g1, a);                                                              \
+    bf16x8_to_f32(u1, b);                                                              \
+    _Pragma("unroll") for (int k = 0; k < 8; ++k) a[k] = a[k] * sigmoidf_(a[k]) * b[k];\
+    h[r * ldh + c1] = f32_to_bf16x8(a);                                                \
   }
+  MUX_ROWWISE_LOOP(SWIGLU_FWD)
+#undef SWIGLU_FWD
 }
 
 // dg = dh * u * s (1 + g (1 - s)),  du = dh * g * s,  s = sigmoid(g)
-__global__ void __launch_bounds__(256) mux_swiglu_bwd_kernel(int rows, int dim, const uint4* dh, long long lddh,
-                                                            const uint4* g, long long ldg, const uint4* u,
-                                                            long long ldu, uint4* dg, long long lddg, uint4* du,
-                                                            long long lddu) {
+__device__ __forceinline__ void swiglu_bwd8(const uint4 dh, const uint4 g, const uint4 u, uint4& dg, uint4& du) {
+  float d[8], a[8], b[8], o1[8], o2[8];
+  bf16x8_to_f32(dh, d);
+  bf16x8_to_f32(g, a);
+  bf16x8_to_f32(u, b);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const float s = sigmoidf_(a[k]);
+    o1[k] = d[k] * b[k] * s * (1.f + a[k] * (1.f - s));
+    o2[k] = d[k] * a[k] * s;
+  }
+  dg = f32_to_bf16x8(o1);
+  du = f32_to_bf16x8(o2);
+}
+
+__global__ void __launch_bounds__(256) mux_swiglu_bwd_kernel(int rows, int dim, const uint4* __restrict__ dh,
+                                                            long long lddh, const uint4* __restrict__ g,
+                                                            long long ldg, const uint4* __restrict__ u,
+                                                            long long ldu, uint4* __restrict__ dg, long long lddg,
+                                                            uint4* __restrict__ du, long long lddu) {
   griddep_wait();
   griddep_launch_dependents();
-  const int nc = dim / 8;
-  const long long total = static_cast<long long>(rows) * nc;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long r = i / nc;
-    const int c = static_cast<int>(i - r * nc);
-    float d[8], a[8], b[8], o1[8], o2[8];
-    bf16x8_to_f32(dh[r * lddh + c], d);
-    bf16x8_to_f32(g[r * ldg + c], a);
-    bf16x8_to_f32(u[r * ldu + c], b);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const float s = sigmoidf_(a[k]);
-      o1[k] = d[k] * b[k] * s * (1.f + a[k] * (1.f - s));
-      o2[k] = d[k] * a[k] * s;
-    }
-    dg[r * lddg + c] = f32_to_bf16x8(o1);
-    du[r * lddu + c] = f32_to_bf16x8(o2);
+#define SWIGLU_BWD(c0, two, c1)                                                       \
+  const uint4 d0 = dh[r * lddh + c0], g0 = g[r * ldg + c0], u0 = u[r * ldu + c0];      \
+  uint4 d1 = make_uint4(0, 0, 0, 0), g1 = d1, u1 = d1;                                 \
+  if (two) { d1 = dh[r * lddh + c1]; g1 = g[r * ldg + c1]; u1 = u[r * ldu + c1]; }     \
+  uint4 o1, o2;                                                                        \
+  swiglu_bwd8(d0, g0, u0, o1, o2);                                                     \
+  dg[r * lddg + c0] = o1;                                                              \
+  du[r * lddu + c0] = o2;                                                              \
+  if (two) {                                                                           \
+    swiglu_bwd8(d1, g1, u1, o1, o2);                                                   \
+    dg[r * lddg + c1] = o1;                                                            \
+    du[r * lddu + c1] = o2;                                                            \
   }
+  MUX_ROWWISE_LOOP(SWIGLU_BWD)
+#undef SWIGLU_BWD
 }
 
 // ------------------------------------------------------------------ residual add
+__device__ __forceinline__ uint4 add8(const uint4 a, const uint4 b) {
+  float x[8], z[8];
+  bf16x8_to_f32(a, x);
+  bf16x8_to_f32(b, z);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] += z[k];
+  return f32_to_bf16x8(x);
+}
+
 __global__ void __launch_bounds__(256) mux_add_kernel(int rows, int dim, const uint4* a, long long lda,
                                                      const uint4* b, long long ldb, uint4* y, long long ldy) {
   griddep_wait();
   griddep_launch_dependents();
-  const int nc = dim / 8;
-  const long long total = static_cast<long long>(rows) * nc;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long r = i / nc;
-    const int c = static_cast<int>(i - r * nc);
-    float x[8], z[8];
-    bf16x8_to_f32(a[r * lda + c], x);
-    bf16x8_to_f32(b[r * ldb + c], z);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) x[k] += z[k];
-    y[r * ldy + c] = f32_to_bf16x8(x);
-  }
+#define ADD_BODY(c0, two, c1)                                                         \
+  const uint4 a0 = a[r * lda + c0], b0 = b[r * ldb + c0];                              \
+  uint4 a1 = make_uint4(0, 0, 0, 0), b1 = a1;                                          \
+  if (two) { a1 = a[r * lda + c1]; b1 = b[r * ldb + c1]; }                             \
+  y[r * ldy + c0] = add8(a0, b0);                                                      \
+  if (two) y[r * ldy + c1] = add8(a1, b1);
+  MUX_ROWWISE_LOOP(ADD_BODY)
+#undef ADD_BODY
 }
 
 // ------------------------------------------------------------------ RoPE
@@ -290,6 +322,12 @@ __global__ void __launch_bounds__(256) mux_rope_kernel(int rows, int heads, int 
 }
 
 // ------------------------------------------------------------------ launchers
+// row-strided elementwise kernels: 8 resident 256-thread blocks per SM
+static unsigned grid_rows(int rows, int num_sms) {
+  const int cap = num_sms * 8;
+  return static_cast<unsigned>(rows < 1 ? 1 : (rows < cap ? rows : cap));
+}
+
 static unsigned grid_for(long long work, int per_block, int num_sms) {
   long long b = (work + per_block - 1) / per_block;
   const long long cap = static_cast<long long>(num_sms) * 16;
@@ -336,7 +374,7 @@ cudaError_t launch_swiglu_fwd(int rows, int dim, const void* g, long long ldg, c
                               long long ldh, int num_sms, cudaStream_t s) {
   const long long work = static_cast<long long>(rows) * (dim / 8);
   if (work == 0) return cudaSuccess;
-  return launch_pdl(mux_swiglu_fwd_kernel, dim3(grid_for(work, 256, num_sms)), dim3(256), 0, s, rows, dim,
+  return launch_pdl(mux_swiglu_fwd_kernel, dim3(grid_rows(rows, num_sms)), dim3(256), 0, s, rows, dim,
                     static_cast<const uint4*>(g), ldg / 8, static_cast<const uint4*>(u), ldu / 8,
                     static_cast<uint4*>(h), ldh / 8);
 }
@@ -346,7 +384,7 @@ cudaError_t launch_swiglu_bwd(int rows, int dim, const void* dh, long long lddh,
                               int num_sms, cudaStream_t s) {
   const long long work = static_cast<long long>(rows) * (dim / 8);
   if (work == 0) return cudaSuccess;
-  return launch_pdl(mux_swiglu_bwd_kernel, dim3(grid_for(work, 256, num_sms)), dim3(256), 0, s, rows, dim,
+  return launch_pdl(mux_swiglu_bwd_kernel, dim3(grid_rows(rows, num_sms)), dim3(256), 0, s, rows, dim,
                     static_cast<const uint4*>(dh), lddh / 8, static_cast<const uint4*>(g), ldg / 8,
                     static_cast<const uint4*>(u), ldu / 8, static_cast<uint4*>(dg), lddg / 8,
                     static_cast<uint4*>(du), lddu / 8);
@@ -356,7 +394,7 @@ cudaError_t launch_add(int rows, int dim, const void* a, long long lda, const vo
                        long long ldy, int num_sms, cudaStream_t s) {
   const long long work = static_cast<long long>(rows) * (dim / 8);
   if (work == 0) return cudaSuccess;
-  return launch_pdl(mux_add_kernel, dim3(grid_for(work, 256, num_sms)), dim3(256), 0, s, rows, dim,
+  return launch_pdl(mux_add_kernel, dim3(grid_rows(rows, num_sms)), dim3(256), 0, s, rows, dim,
                     static_cast<const uint4*>(a), lda / 8, static_cast<const uint4*>(b), ldb / 8,
                     static_cast<uint4*>(y), ldy / 8);
 }
