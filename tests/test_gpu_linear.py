@@ -203,3 +203,15 @@ print('not trapped', flush=True)
     assert "valid ok" in out, out
     assert "not trapped" not in out and r.returncode != 0, out
     assert "bad seg_off[1] = 100" in out, out
+
+
+def test_maximum_segments_and_adapters():
+    """The ABI's maxima: 64 segments (MUX_MAX_SEGMENTS) over 64 adapters (MUX_MAX_ADAPTERS), ranks
+    cycling 1..64 (r_cap 64), some segments empty, several 64-row segments per 256-row pair tile;
+    integer inputs, so Y, dX, Hs and every dA_t / dB_t must be bit-exact."""
+    rng = np.random.default_rng(77)
+    seg_lens = [int(rng.choice([0, 64, 64, 128])) for _ in range(64)]
+    ranks = [1 + (t * 7) % 64 for t in range(64)]
+    scales = [1.0 if t % 2 else 2.0 for t in range(64)]
+    p = Problem(256, 192, seg_lens, ranks, seg_task=list(range(64)), scales=scales, variant="int", seed=78)
+    _run(p, exact=True)

@@ -16,6 +16,8 @@ scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 per = []
 for vals in rows[2:]:
     d = dict(zip(hdr, vals))
+    if "<0>" not in d["Kernel Name"]:  # forward launches only (the capture may hold the dX GEMMs too)
+        continue
     u = dict(zip(hdr, units))
     b = sum(float(d[k]) * scale[u[k]] for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
     per.append({"kernel": d["Kernel Name"], "grid": d.get("launch__grid_size"), "dram_bytes": b,
