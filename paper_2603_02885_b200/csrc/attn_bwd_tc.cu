@@ -232,20 +232,36 @@ __global__ void __launch_bounds__(kThreadsB, 2) mux_attn_dq_tc_kernel(const __gr
       }
       tmem_ld_wait();
       uint32_t w[32];
+      // interior tile (no key of it masked for any row of the warp): no per-element mask
+      if (__all_sync(0xffffffffu, rlo >= 0 && kt >= rlo && kt + 63 <= r)) {
 #pragma unroll
-      for (int c = 0; c < 2; ++c)
+        for (int c = 0; c < 2; ++c)
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          float d2[2];
+          for (int i = 0; i < 16; ++i) {
+            float d2[2];
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int key = kt + 32 * c + 2 * i + e;
-            const bool ok = rlo >= 0 && key >= rlo && key <= r;
-            const float pr = ok ? exp2f(__uint_as_float(sv[c][2 * i + e]) * p.scale_log2 - l2) : 0.f;
-            d2[e] = pr * (__uint_as_float(pv[c][2 * i + e]) - Dr);
+            for (int e = 0; e < 2; ++e) {
+              const float pr = ex2_approx(fmaf(__uint_as_float(sv[c][2 * i + e]), p.scale_log2, -l2));
+              d2[e] = pr * (__uint_as_float(pv[c][2 * i + e]) - Dr);
+            }
+            w[16 * c + i] = pack_bf16x2(d2[0], d2[1]);
           }
-          w[16 * c + i] = pack_bf16x2(d2[0], d2[1]);
-        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            float d2[2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int key = kt + 32 * c + 2 * i + e;
+              const bool ok = rlo >= 0 && key >= rlo && key <= r;
+              const float pr = ok ? ex2_approx(fmaf(__uint_as_float(sv[c][2 * i + e]), p.scale_log2, -l2)) : 0.f;
+              d2[e] = pr * (__uint_as_float(pv[c][2 * i + e]) - Dr);
+            }
+            w[16 * c + i] = pack_bf16x2(d2[0], d2[1]);
+          }
+      }
       if (j > 0) {  // dQ += dS_{j-1} K_{j-1} must have read the dS buffer
         mbar_wait(dq_done, (j - 1) & 1);
         tc_fence_after();
@@ -479,22 +495,57 @@ __global__ void __launch_bounds__(kThreadsB, 2) mux_attn_dkdv_tc_kernel(const __
       }
       tmem_ld_wait();
       uint32_t w[32];  // P^T (dV) or dS^T = P^T o (dP^T - D) (dK), bf16 pairs
+      // interior tile: every query of the tile sees every key row of the warp
+      // (kr <= qt, kr >= max row_start, no invalid query): no per-element mask
+      int rs_max = max(rss[lane], rss[32 + lane]);
+      int rs_min = min(rss[lane], rss[32 + lane]);
 #pragma unroll
-      for (int c = 0; c < 2; ++c)
+      for (int o = 16; o > 0; o >>= 1) {
+        rs_max = max(rs_max, __shfl_xor_sync(0xffffffffu, rs_max, o));
+        rs_min = min(rs_min, __shfl_xor_sync(0xffffffffu, rs_min, o));
+      }
+      if (__all_sync(0xffffffffu, rs_min >= 0 && kr >= rs_max && kr <= qt)) {
+        const float4* lse4 = reinterpret_cast<const float4*>(scs);
+        const float4* d4 = reinterpret_cast<const float4*>(scs + 64);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          float x[2];
+        for (int c = 0; c < 2; ++c)
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int col = 32 * c + 2 * i + e;
-            const int qr = qt + col;
-            const int rs = rss[col];
-            const bool ok = rs >= 0 && rs <= kr && kr <= qr;
-            const float pr = ok ? exp2f(__uint_as_float(sv[c][2 * i + e]) * p.scale_log2 - scs[col]) : 0.f;
-            x[e] = kDK ? pr * (__uint_as_float(pv[c][2 * i + e]) - scs[64 + col]) : pr;
+          for (int i = 0; i < 16; i += 2) {
+            const float4 l4 = lse4[(32 * c + 2 * i) >> 2];
+            const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
+            float dv[4] = {0.f, 0.f, 0.f, 0.f};
+            if (kDK) {
+              const float4 t = d4[(32 * c + 2 * i) >> 2];
+              dv[0] = t.x; dv[1] = t.y; dv[2] = t.z; dv[3] = t.w;
+            }
+            float x[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float pr = ex2_approx(fmaf(__uint_as_float(sv[c][2 * i + e]), p.scale_log2, -lv[e]));
+              x[e] = kDK ? pr * (__uint_as_float(pv[c][2 * i + e]) - dv[e]) : pr;
+            }
+            w[16 * c + i] = pack_bf16x2(x[0], x[1]);
+            w[16 * c + i + 1] = pack_bf16x2(x[2], x[3]);
           }
-          w[16 * c + i] = pack_bf16x2(x[0], x[1]);
-        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            float x[2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int col = 32 * c + 2 * i + e;
+              const int qr = qt + col;
+              const int rs = rss[col];
+              const bool ok = rs >= 0 && rs <= kr && kr <= qr;
+              const float pr =
+                  ok ? ex2_approx(fmaf(__uint_as_float(sv[c][2 * i + e]), p.scale_log2, -scs[col])) : 0.f;
+              x[e] = kDK ? pr * (__uint_as_float(pv[c][2 * i + e]) - scs[64 + col]) : pr;
+            }
+            w[16 * c + i] = pack_bf16x2(x[0], x[1]);
+          }
+      }
       if (j > 0) {  // the previous tile's accumulate MMA must have read the P^T / dS^T tile
         mbar_wait(mm_done, (j - 1) & 1);
         tc_fence_after();

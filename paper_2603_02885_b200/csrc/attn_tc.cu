@@ -204,17 +204,28 @@ __global__ void __launch_bounds__(kThreads, 2) mux_attn_fwd_tc_kernel(const __gr
 #pragma unroll
       for (int c = 0; c < 2; ++c) tmem_ld32(tS + 32 * c, sv[c]);
       tmem_ld_wait();
+      // Interior tiles (every key of the tile visible to every row of the warp) skip the
+      // per-element mask: the kernel is instruction-bound, and the mask was most of it.
+      const bool interior = __all_sync(0xffffffffu, rlo >= 0 && kt >= rlo && kt + kTN - 1 <= r);
       float mx = -INFINITY;
+      if (interior) {
 #pragma unroll
-      for (int c = 0; c < 2; ++c)
+        for (int c = 0; c < 2; ++c)
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const int key = kt + 32 * c + i;
-          const bool ok = rlo >= 0 && key >= rlo && key <= r;
-          const float x = ok ? __uint_as_float(sv[c][i]) * p.scale_log2 : -INFINITY;
-          sv[c][i] = __float_as_uint(x);
-          mx = fmaxf(mx, x);
-        }
+          for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(sv[c][i]));
+        mx *= p.scale_log2;  // scale > 0: max commutes with the scaling
+      } else {
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const int key = kt + 32 * c + i;
+            const bool ok = rlo >= 0 && key >= rlo && key <= r;
+            const float x = ok ? __uint_as_float(sv[c][i]) * p.scale_log2 : -INFINITY;
+            sv[c][i] = __float_as_uint(x);
+            mx = fmaxf(mx, x);
+          }
+      }
       // lazy rescaling: keep the running max unless it grew by more than kLazy (log2 units)
       float alpha = 1.f;
       const bool grow = mx > m_used + kLazy || (m_used == -INFINITY && mx > -INFINITY);
@@ -225,12 +236,14 @@ __global__ void __launch_bounds__(kThreads, 2) mux_attn_fwd_tc_kernel(const __gr
       const float mu = m_used == -INFINITY ? 0.f : m_used;
       uint32_t pw[32];
       float sum = 0.f;
+      // interior: sv holds raw scores, P = 2^(s * scale - mu) in one FFMA + one SFU op
+      const float sc = interior ? p.scale_log2 : 1.f;
 #pragma unroll
       for (int c = 0; c < 2; ++c)
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const float a = exp2f(__uint_as_float(sv[c][2 * i]) - mu);
-          const float b = exp2f(__uint_as_float(sv[c][2 * i + 1]) - mu);
+          const float a = ex2_approx(fmaf(__uint_as_float(sv[c][2 * i]), sc, -mu));
+          const float b = ex2_approx(fmaf(__uint_as_float(sv[c][2 * i + 1]), sc, -mu));
           sum += a + b;
           pw[16 * c + i] = pack_bf16x2(a, b);
         }
