@@ -7,14 +7,16 @@
 // columns per CTA: two CTAs share an SM, so one's prologue, softmax and
 // epilogue overlap the other's MMAs).  Per key tile j:
 //   S_j = Q K_j^T           tcgen05.mma M=128 N=64, A = Q (K-major smem),
-//                           B = K_j (K-major smem)          -> TMEM cols [0,64)
+//                           B = K_j (K-major smem)          -> TMEM cols [64 (j&1), +64)
 //   softmax (one thread per query row, tcgen05.ld of its S row): mask to
 //   [row_start, row], running max with lazy rescaling (the O accumulator is
 //   rescaled in TMEM only when the max grows by more than 2^8), P_j = exp2(.)
 //   as bf16 into a 128 B-swizzled K-major smem tile
 //   O += P_j V_j            tcgen05.mma M=128 N=128 K=64, A = P_j (smem),
 //                           B = V_j (MN-major smem)         -> TMEM cols [128,256)
-// S_{j+1} is issued as soon as softmax j has read S_j, so it overlaps P_j V_j.
+// S is double-buffered in TMEM: S_{j+1} is computed while softmax j runs (it
+// only needs softmax j-1 to have read its buffer), so the tensor core and the
+// softmax overlap instead of alternating.
 // Warps 0-3: softmax + epilogue (TMEM lane quadrants), warp 4: MMA issuer,
 // warp 5: TMA producer and TMEM allocator.
 #include <climits>
@@ -61,11 +63,12 @@ __global__ void __launch_bounds__(kThreads, 2) mux_attn_fwd_tc_kernel(const __gr
   uint64_t* q_full = bars + 0;
   uint64_t* kv_full = bars + 1;   // [2]
   uint64_t* kv_empty = bars + 3;  // [2]
-  uint64_t* s_full = bars + 5;
-  uint64_t* p_full = bars + 6;
-  uint64_t* o_done = bars + 7;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 8);
-  int* s_lohi = reinterpret_cast<int*>(bars + 9);
+  uint64_t* s_full = bars + 5;   // [2] S buffer b holds S_j (j & 1 == b)
+  uint64_t* s_free = bars + 7;   // [2] the 4 softmax warps have read S buffer b
+  uint64_t* p_full = bars + 9;
+  uint64_t* o_done = bars + 10;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 11);
+  int* s_lohi = reinterpret_cast<int*>(bars + 12);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q0 = blockIdx.x * kT;
@@ -77,7 +80,10 @@ __global__ void __launch_bounds__(kThreads, 2) mux_attn_fwd_tc_kernel(const __gr
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
     }
-    mbar_init(s_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&s_full[b], 1);
+      mbar_init(&s_free[b], 4);
+    }
     mbar_init(p_full, 4);
     mbar_init(o_done, 1);
     fence_mbar_init();
@@ -148,7 +154,7 @@ __global__ void __launch_bounds__(kThreads, 2) mux_attn_fwd_tc_kernel(const __gr
       constexpr uint32_t kIdS = idesc_bf16(128, kTN, false, false);  // Q K^T: both K-major
       constexpr uint32_t kIdO = idesc_bf16(128, 128, false, true);   // P V: V is MN-major (d contiguous)
       constexpr uint32_t kHi = desc_hi(1024);
-      const uint32_t tS = tmem, tO = tmem + 128;
+      const uint32_t tO = tmem + 128;  // S_j in TMEM columns [64 (j & 1), +64)
       // K-major operand = subtiles of 64 elems (128 B rows) `sub` bytes apart; k-step k (16 elems)
       auto kmaj = [&](uint32_t base, uint32_t sub, int k) {
         return make_desc(desc_lo(base + (k >> 2) * sub + (k & 3) * 32, 16), kHi);
@@ -160,14 +166,15 @@ __global__ void __launch_bounds__(kThreads, 2) mux_attn_fwd_tc_kernel(const __gr
       for (int j = 0; j <= ntiles; ++j) {
         if (j < ntiles) {
           mbar_wait(&kv_full[j & 1], (j >> 1) & 1);
-          if (j > 0) mbar_wait(p_full, (j - 1) & 1);  // softmax j-1 read S and wrote P
+          if (j >= 2) mbar_wait(&s_free[j & 1], ((j >> 1) - 1) & 1);  // softmax j-2 read this buffer
           tc_fence_after();
           const uint32_t sk = sbase + kSmemKV + (j & 1) * 2 * kTileK;
+          const uint32_t tS = tmem + 64u * static_cast<uint32_t>(j & 1);
           if (elect_one_sync()) {
 #pragma unroll
             for (int k = 0; k < 8; ++k)
               mma_bf16(tS, kmaj(sbase + kSmemQ, kSubQ, k), kmaj(sk, kSubK, k), kIdS, k > 0 ? 1u : 0u);
-            mma_commit(s_full);
+            mma_commit(&s_full[j & 1]);
           }
           __syncwarp();
         } else {
@@ -176,6 +183,10 @@ __global__ void __launch_bounds__(kThreads, 2) mux_attn_fwd_tc_kernel(const __gr
         }
         if (j > 0) {
           const int jp = j - 1;
+          if (j < ntiles) {  // softmax j-1 wrote P (the last iteration waited above)
+            mbar_wait(p_full, jp & 1);
+            tc_fence_after();
+          }
           const uint32_t sv = sbase + kSmemKV + (jp & 1) * 2 * kTileK + kTileK;
           if (elect_one_sync()) {
 #pragma unroll
@@ -194,16 +205,21 @@ __global__ void __launch_bounds__(kThreads, 2) mux_attn_fwd_tc_kernel(const __gr
     const int r = q0 + row;
     const int rlo = r < p.R ? p.row_start[r] : -1;
     const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
-    const uint32_t tS = tmem + lane_off, tO = tmem + lane_off + 128;
+    const uint32_t tO = tmem + lane_off + 128;
     float m_used = -INFINITY, l = 0.f;
     for (int j = 0; j < ntiles; ++j) {
       const int kt = lo + j * kTN;
-      mbar_wait(s_full, j & 1);
+      mbar_wait(&s_full[j & 1], (j >> 1) & 1);
       tc_fence_after();
       uint32_t sv[2][32];
+      const uint32_t tS = tmem + lane_off + 64u * static_cast<uint32_t>(j & 1);
 #pragma unroll
       for (int c = 0; c < 2; ++c) tmem_ld32(tS + 32 * c, sv[c]);
       tmem_ld_wait();
+      // S_j is in registers: its TMEM buffer may take S_{j+2} while this softmax runs
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_free[j & 1]);
       // Interior tiles (every key of the tile visible to every row of the warp) skip the
       // per-element mask: the kernel is instruction-bound, and the mask was most of it.
       const bool interior = __all_sync(0xffffffffu, rlo >= 0 && kt >= rlo && kt + kTN - 1 <= r);

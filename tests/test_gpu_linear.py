@@ -215,3 +215,28 @@ def test_maximum_segments_and_adapters():
     scales = [1.0 if t % 2 else 2.0 for t in range(64)]
     p = Problem(256, 192, seg_lens, ranks, seg_task=list(range(64)), scales=scales, variant="int", seed=78)
     _run(p, exact=True)
+
+
+def test_all_segments_empty():
+    """Degenerate call: every segment empty (seg_off[S] = 0).  Nothing is computed, no row is
+    written, and every adapter's dA/dB is written as exact zeros (Q16)."""
+    from paper_2603_02885_b200 import mux
+    K, N, R = 256, 192, 128
+    seg_off = torch.zeros(3, dtype=torch.int32, device="cuda")
+    X = torch.randn(R, K, device="cuda").bfloat16()
+    W = torch.randn(N, K, device="cuda").bfloat16()
+    dY = torch.randn(R, N, device="cuda").bfloat16()
+    ads = []
+    for r in (8, 16):
+        B = mux.make_B_storage(N, r)
+        B.copy_(torch.randn(N, r, device="cuda").bfloat16())
+        ads.append(mux.Adapter(torch.randn(r, K, device="cuda").bfloat16(), B, r, 2.0,
+                               torch.full((r, K), 7.0, device="cuda"), torch.full((N, r), 7.0, device="cuda")))
+    Y = torch.full((R, N), 3.0, device="cuda").bfloat16()
+    Y, Hs = mux.linear_fwd(seg_off, [0, 1], ads, X, W, 16, Y=Y)
+    dX = torch.full((R, K), 5.0, device="cuda").bfloat16()
+    mux.linear_bwd(seg_off, [0, 1], ads, dY, X, W, Hs, 16, dX=dX)
+    torch.cuda.synchronize()
+    assert torch.all(Y == 3.0) and torch.all(dX == 5.0)
+    for a in ads:
+        assert torch.all(a.dA == 0) and torch.all(a.dB == 0)

@@ -111,3 +111,10 @@ def test_pack_apply_gather():
     got = packed.view(torch.int16).cpu().numpy().view(np.uint16)
     assert np.array_equal(got, expect)
     assert T == int((rs >= 0).sum())
+
+
+def test_no_sequences_at_all():
+    """Degenerate micro-batch: every task empty (num_seqs = 0): c = chunk_min, total_rows = 0,
+    seg_off all zero, every row_src entry -1 — bit-exact with the oracle."""
+    _check([0, 0, 0, 0], [], None, 0, 64)
+    _check([0, 0], [], [128], 0, 128)
