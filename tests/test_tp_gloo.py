@@ -1,5 +1,5 @@
 """Tensor-parallel orchestration (paper_2603_02885_b200/tp.py) on
-CPU: world_size 2 over gloo, with the fp64 oracle injected as each rank's
+CPU: world_size 2, 4 and 8 over gloo, with the fp64 oracle injected as each rank's
 local linear.  The TP result (gathered) must equal the single-process oracle
 on the full problem: a column-parallel layer followed by a row-parallel layer
 (e.g. up -> down), forward and backward, including dA_t / dB_t."""
@@ -90,7 +90,7 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 def test_tp_column_row_matches_single_process(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
