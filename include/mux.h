@@ -199,6 +199,35 @@ MUX_API mux_status mux_linear_fwd(int32_t num_segs, const int32_t* seg_off, cons
                           mux_bf16* Y, mux_bf16* Hs,
                           void* workspace, size_t workspace_bytes, cudaStream_t stream);
 
+/* Forward with the shrink supplied by the caller (tensor parallelism, SURVEY
+ * §8(e)): Y[i,:] = X[i,:] W^T + Hs[i,:] B_t^T for rows i of segment s,
+ * t = seg_task[s] — the same as mux_linear_fwd except that Hs [max_rows, r_cap]
+ * is an INPUT (bf16, columns >= rank_t zero, e.g. from mux_linear_shrink on
+ * each rank's own rows, then all-gathered) and no shrink tiles run.  With the
+ * Hs of mux_linear_fwd, Y is bit-identical to mux_linear_fwd's.  Arguments and
+ * errors as mux_linear_fwd; Hs must be non-NULL and 16-byte aligned. */
+MUX_API mux_status mux_linear_fwd_hs(int32_t num_segs, const int32_t* seg_off, const int32_t* seg_task,
+                          int32_t num_adapters, const mux_adapter* adapters,
+                          int32_t max_rows, int32_t K, int32_t N, int32_t r_cap,
+                          const mux_bf16* X, const mux_bf16* W, mux_bf16* Y, const mux_bf16* Hs,
+                          void* workspace, size_t workspace_bytes, cudaStream_t stream);
+
+/* Shrink only, over a row range: Hs[i,j] = bf16(s_t * X[i,:] A_t[j,:]^T)
+ * (0 for rank_t <= j < r_cap) for the pair row blocks overlapping packed rows
+ * [row_begin, row_end) — the per-rank part of a column-parallel forward under
+ * sequence parallelism (each rank shrinks only the rows it owns; the Hs rows,
+ * T x r_cap, are then all-gathered instead of every rank recomputing all of
+ * them inside mux_linear_fwd).  Values equal mux_linear_fwd's Hs bit for bit.
+ * row_begin a multiple of 256; row_end a multiple of 256 or >= max_rows; rows
+ * outside the range or >= seg_off[S] are not written.  Arguments as
+ * mux_linear_fwd without W/Y (N still sizes the adapters' B_t); Hs output
+ * non-NULL.  Errors as mux_linear_fwd. */
+MUX_API mux_status mux_linear_shrink(int32_t num_segs, const int32_t* seg_off, const int32_t* seg_task,
+                          int32_t num_adapters, const mux_adapter* adapters,
+                          int32_t max_rows, int32_t K, int32_t N, int32_t r_cap,
+                          const mux_bf16* X, int32_t row_begin, int32_t row_end, mux_bf16* Hs,
+                          void* workspace, size_t workspace_bytes, cudaStream_t stream);
+
 /* Backward (Eq. 2 + LoRA chain rule).  For rows i of segment s, t = seg_task[s]:
  *   Gs[i,j]  = bf16(s_t * dY[i,:] B_t[:,j])                 (workspace)
  *   dX[i,:]  = dY[i,:] W + Gs[i,:] A_t                      (NULL = skip)

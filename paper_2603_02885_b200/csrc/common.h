@@ -52,7 +52,10 @@ struct GemmParams {
   int32_t kred;                  // reduction length of the main product (K fwd, N bwd)
   int32_t nout;                  // output columns (N fwd, K bwd)
   int32_t r_cap;
-  int32_t has_main;              // 0: only the shrink (side) tiles
+  int32_t has_main;              // 0: only the shrink (side) tiles, over row blocks [side_m_lo, side_m_hi)
+  int32_t has_side;              // 0: no side tiles, Hs given (mux_linear_fwd_hs)
+  int32_t side_m_lo, side_m_hi;  // shrink-only launches: pair row-block range
+  int32_t side_first;            // 1: all side tiles before the main tiles (short reductions)
   int32_t group_m;               // raster band: pair row-blocks sharing a sweep over W tiles
   unsigned long long* dbg;       // MUX_PROFILE builds only: wait-cycle counters (see gemm.cu)
   // Fused reduce-scatter output (tensor parallel, mux_linear_*_rs): rs_world > 0 sends each

@@ -118,22 +118,38 @@ struct Tile {
 // band's A rows warms L2 right before the main tiles sweep W through it, and
 // every main tile still depends only on a lower-indexed side tile (group_m is
 // sized on the host so a band of A rows fits L2 next to the streamed W tiles).
-__device__ __forceinline__ Tile tile_at(int t, int num_m, int num_n, int group_m, bool has_main) {
+// Without main tiles (shrink only) the side tiles cover row blocks [side_lo, ..);
+// without side tiles (Hs given by the caller) the bands hold main tiles only.
+// side_first (short reductions, chosen on the host): every side tile first, then the main tiles
+// band by band.  With short main tiles, a band's main tiles otherwise reach their extension
+// block while that band's side tiles (same wave) are still in their epilogue, and the producer
+// stalls on the flag (profiles/r01_gemm_ab_sidefirst.jsonl).
+__device__ __forceinline__ Tile tile_at(int t, int num_m, int num_n, int group_m, bool has_main, bool has_side,
+                                       int side_lo, bool side_first) {
   Tile r;
   if (!has_main) {
-    r.m = t; r.n = 0; r.side = true;
+    r.m = side_lo + t; r.n = 0; r.side = true;
     return r;
   }
-  const int per_band = group_m * (num_n + 1);
+  if (has_side && side_first) {
+    if (t < num_m) {
+      r.m = t; r.n = 0; r.side = true;
+      return r;
+    }
+    t -= num_m;
+    has_side = false;
+  }
+  const int ns = has_side ? 1 : 0;
+  const int per_band = group_m * (num_n + ns);
   const int band = t / per_band;
   const int first_m = band * group_m;
   const int gm = min(num_m - first_m, group_m);
   const int w = t - band * per_band;
-  if (w < gm) {
+  if (w < gm * ns) {
     r.m = first_m + w; r.n = 0; r.side = true;
     return r;
   }
-  const int v = w - gm;
+  const int v = w - gm * ns;
   r.m = first_m + v % gm;
   r.n = v / gm;
   r.side = false;
@@ -185,9 +201,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&p.map_a);
-    tma_prefetch(&p.map_w);
     tma_prefetch(&p.map_side);
-    tma_prefetch(&p.map_out);
+    if (p.has_main) {  // shrink-only launches leave these maps unencoded
+      tma_prefetch(&p.map_w);
+      tma_prefetch(&p.map_out);
+    }
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -215,7 +233,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   const int total_rows = so[p.num_segs];
   const int num_m = (total_rows + kPairRows - 1) / kPairRows;
   const int num_n = (p.nout + kBN - 1) / kBN;
-  const int total_tiles = num_m * (1 + (p.has_main ? num_n : 0));
+  const int side_lo = min(p.side_m_lo, num_m);
+  const int total_tiles = p.has_main ? num_m * (num_n + (p.has_side ? 1 : 0))
+                                     : max(0, min(p.side_m_hi, num_m) - side_lo);
   const int num_kb = (p.kred + kBK - 1) / kBK;  // a partial last block reads TMA zero fill
 
 #ifdef MUX_PROFILE
@@ -238,7 +258,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       const uint32_t full_leader = mapa_shared(full_u, 0);  // stage s barrier: + 8 s
       uint32_t ag_ok = 0;  // owners whose rows have landed in the gather buffer (fused all-gather)
       for (int t = cid; t < total_tiles; t += ncl) {
-        const Tile tl = tile_at(t, num_m, num_n, p.group_m, p.has_main != 0);
+        const Tile tl = tile_at(t, num_m, num_n, p.group_m, p.has_main != 0, p.has_side != 0, side_lo, p.side_first != 0);
         const PairGroups g = pair_groups(p, so, tl.m);
         const int row_c = tl.m * kPairRows + kBM * rk;  // this CTA's rows
         if (p.ag_world > 0) {
@@ -317,8 +337,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             __syncwarp();
             advance();
           }
-          if (g.n > 0) {
-            // the side tile of this row block must have published Hs/Gs
+          if (g.n > 0 && p.has_side) {
+            // the side tile of this row block must have published Hs/Gs (a caller-given
+            // Hs was written by an earlier kernel in stream order)
             if (elect_one_sync()) {
               const unsigned long long* flag = p.flags + tl.m;
               const unsigned long long want = (epoch << 8) | 8ull;
@@ -389,7 +410,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         if (++stage == kStages) { stage = 0; phase ^= 1u; }
       };
       for (int t = cid; t < total_tiles; t += ncl) {
-        const Tile tl = tile_at(t, num_m, num_n, p.group_m, p.has_main != 0);
+        const Tile tl = tile_at(t, num_m, num_n, p.group_m, p.has_main != 0, p.has_side != 0, side_lo, p.side_first != 0);
         const PairGroups g = pair_groups(p, so, tl.m);
         PROF_T0(tw_);
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1u);
@@ -489,7 +510,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     uint8_t* bufs = epi + q * 2 * kEpiBuf;
     int buf_sel = 0;
     for (int t = cid; t < total_tiles; t += ncl) {
-      const Tile tl = tile_at(t, num_m, num_n, p.group_m, p.has_main != 0);
+      const Tile tl = tile_at(t, num_m, num_n, p.group_m, p.has_main != 0, p.has_side != 0, side_lo, p.side_first != 0);
       PROF_T0(tw_);
       mbar_wait(&tfull_bar[acc], acc_phase);
       PROF_ADD(ew_tfull, tw_);

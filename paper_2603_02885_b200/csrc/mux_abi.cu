@@ -14,6 +14,11 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+// fused GEMM: reductions this short schedule every shrink tile before the main tiles
+#ifndef MUX_SIDE_FIRST_MAX_KRED
+#define MUX_SIDE_FIRST_MAX_KRED 2048
+#endif
+
 #include "common.h"
 
 namespace mux {
@@ -356,15 +361,23 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
                                 const __nv_bfloat16* X, const __nv_bfloat16* W, __nv_bfloat16* out /*Y or dX*/,
                                 const __nv_bfloat16* Hs_in, __nv_bfloat16* Hs_out, void* workspace,
                                 size_t workspace_bytes, cudaStream_t stream, int parts = 3,
-                                const mux_rs* rs = nullptr, const mux_ag* ag = nullptr) {
+                                const mux_rs* rs = nullptr, const mux_ag* ag = nullptr, bool hs_given = false,
+                                bool shrink_only = false, int32_t side_row_lo = 0,
+                                int32_t side_row_hi = INT32_MAX) {
   mux_status st = validate_linear(num_segs, seg_off, seg_task, num_adapters, adapters, max_rows, K, N, r_cap);
   if (st != MUX_OK) return st;
-  if (!a_in || !W) return fail(MUX_ERR_INVALID_ARGUMENT, "null input pointer");
-  if (!aligned16(a_in) || !aligned16(W) || (out && !aligned16(out)) || (X && !aligned16(X)) ||
+  if (!a_in || (!W && !shrink_only)) return fail(MUX_ERR_INVALID_ARGUMENT, "null input pointer");
+  if (hs_given && !Hs_in) return fail(MUX_ERR_INVALID_ARGUMENT, "Hs (input) is null");
+  if (shrink_only && !Hs_out) return fail(MUX_ERR_INVALID_ARGUMENT, "Hs (output) is null");
+  if (shrink_only && (side_row_lo < 0 || side_row_lo % kPairRows || side_row_hi < side_row_lo ||
+                      (side_row_hi % kPairRows && side_row_hi < max_rows)))
+    return fail(MUX_ERR_INVALID_ARGUMENT, "row range [%d, %d): begin a multiple of 256, end a multiple of 256 or "
+                ">= max_rows (%d)", side_row_lo, side_row_hi, max_rows);
+  if (!aligned16(a_in) || (W && !aligned16(W)) || (out && !aligned16(out)) || (X && !aligned16(X)) ||
       (Hs_in && !aligned16(Hs_in)) || (Hs_out && !aligned16(Hs_out)))
     return fail(MUX_ERR_INVALID_ARGUMENT, "tensor pointers must be 16-byte aligned");
   if (bwd && (!X || !Hs_in)) return fail(MUX_ERR_INVALID_ARGUMENT, "bwd needs X and Hs");
-  if (!bwd && !out && !rs) return fail(MUX_ERR_INVALID_ARGUMENT, "fwd needs Y");
+  if (!bwd && !out && !rs && !shrink_only) return fail(MUX_ERR_INVALID_ARGUMENT, "fwd needs Y");
   const LinearWs need = carve_linear_ws(nullptr, max_rows, r_cap);
   if (!workspace || workspace_bytes < need.bytes)
     return fail(MUX_ERR_INSUFFICIENT_BUFFER, "linear workspace %zu < %zu bytes", workspace_bytes, need.bytes);
@@ -375,10 +388,10 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
   std::memset(&p, 0, sizeof(p));
   const int kred = bwd ? N : K;
   const int nout = bwd ? K : N;
-  __nv_bfloat16* side = bwd ? ws.gs : (Hs_out ? Hs_out : ws.hs);
+  __nv_bfloat16* side = bwd ? ws.gs : hs_given ? const_cast<__nv_bfloat16*>(Hs_in) : (Hs_out ? Hs_out : ws.hs);
   if (!make_map(&p.map_a, a_in, kred, max_rows, kred, 64, 128))
     return fail(MUX_ERR_CUDA, "cuTensorMapEncodeTiled failed for %s %p [%d x %d]", bwd ? "dY" : "X", a_in, max_rows, kred);
-  if (!make_map(&p.map_w, W, K, N, K, 64, 64))
+  if (W && !make_map(&p.map_w, W, K, N, K, 64, 64))
     return fail(MUX_ERR_CUDA, "cuTensorMapEncodeTiled failed for W %p [%d x %d]", W, N, K);
   if (!make_map(&p.map_side, side, r_cap, max_rows, r_cap, 64, 128))
     return fail(MUX_ERR_CUDA, "cuTensorMapEncodeTiled failed for %s %p [%d x %d]", bwd ? "Gs" : "Hs", side, max_rows,
@@ -403,6 +416,11 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
   p.nout = nout;
   p.r_cap = r_cap;
   p.has_main = out != nullptr || rs != nullptr;
+  p.has_side = hs_given ? 0 : 1;
+  // short reductions: side tiles first (A/B in DESIGN §12: +3-9 % at kred <= 1376, neutral at 4096+)
+  p.side_first = kred <= MUX_SIDE_FIRST_MAX_KRED ? 1 : 0;
+  p.side_m_lo = side_row_lo / kPairRows;
+  p.side_m_hi = side_row_hi == INT32_MAX ? INT32_MAX : (side_row_hi + kPairRows - 1) / kPairRows;
   if (ag) {
     if (ag->world < 1 || ag->world > MUX_RS_MAX_WORLD || ag->rank < 0 || ag->rank >= ag->world || ag->seq == 0 ||
         ag->rows_per_rank <= 0 || ag->rows_per_rank % kPairRows ||
@@ -460,7 +478,9 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
   }
   const int num_m_max = (max_rows + kPairRows - 1) / kPairRows;
   const int num_n = (nout + kBN - 1) / kBN;
-  const long long tiles_max = static_cast<long long>(num_m_max) * (1 + (p.has_main ? num_n : 0));
+  const long long side_blocks = p.has_main ? (p.has_side ? num_m_max : 0)
+                                           : std::max(0, std::min(p.side_m_hi, num_m_max) - std::min(p.side_m_lo, num_m_max));
+  const long long tiles_max = side_blocks + (p.has_main ? static_cast<long long>(num_m_max) * num_n : 0);
   // one CTA pair (cluster of 2) per tile in flight; grid = #SMs rounded to pairs
   const long long pairs = std::min<long long>(tiles_max, num_sms() / 2);
   const int grid = static_cast<int>(2 * std::max<long long>(pairs, 1));
@@ -532,6 +552,27 @@ mux_status mux_linear_fwd(int32_t num_segs, const int32_t* seg_off, const int32_
   auto Hs = reinterpret_cast<__nv_bfloat16*>(Hs_);
   return linear_common(false, num_segs, seg_off, seg_task, num_adapters, adapters, max_rows, K, N, r_cap, X, X, W,
                        Y, nullptr, Hs, workspace, workspace_bytes, stream);
+}
+
+mux_status mux_linear_fwd_hs(int32_t num_segs, const int32_t* seg_off, const int32_t* seg_task,
+                             int32_t num_adapters, const mux_adapter* adapters, int32_t max_rows, int32_t K, int32_t N,
+                             int32_t r_cap, const mux_bf16* X_, const mux_bf16* W_, mux_bf16* Y_,
+                             const mux_bf16* Hs_, void* workspace, size_t workspace_bytes, cudaStream_t stream) {
+  auto X = reinterpret_cast<const __nv_bfloat16*>(X_);
+  return linear_common(false, num_segs, seg_off, seg_task, num_adapters, adapters, max_rows, K, N, r_cap, X, X,
+                       reinterpret_cast<const __nv_bfloat16*>(W_), reinterpret_cast<__nv_bfloat16*>(Y_),
+                       reinterpret_cast<const __nv_bfloat16*>(Hs_), nullptr, workspace, workspace_bytes, stream, 3,
+                       nullptr, nullptr, /*hs_given=*/true);
+}
+
+mux_status mux_linear_shrink(int32_t num_segs, const int32_t* seg_off, const int32_t* seg_task,
+                             int32_t num_adapters, const mux_adapter* adapters, int32_t max_rows, int32_t K, int32_t N,
+                             int32_t r_cap, const mux_bf16* X_, int32_t row_begin, int32_t row_end, mux_bf16* Hs_,
+                             void* workspace, size_t workspace_bytes, cudaStream_t stream) {
+  auto X = reinterpret_cast<const __nv_bfloat16*>(X_);
+  return linear_common(false, num_segs, seg_off, seg_task, num_adapters, adapters, max_rows, K, N, r_cap, X, X,
+                       nullptr, nullptr, nullptr, reinterpret_cast<__nv_bfloat16*>(Hs_), workspace, workspace_bytes,
+                       stream, 3, nullptr, nullptr, false, /*shrink_only=*/true, row_begin, row_end);
 }
 
 mux_status mux_linear_bwd(int32_t num_segs, const int32_t* seg_off, const int32_t* seg_task,

@@ -31,7 +31,7 @@ EXPORTS = ("mux_last_error", "mux_version", "mux_pack_bound_rows", "mux_pack_wor
            "mux_linear_bwd", "mux_linear_bwd_part", "mux_pack_row_start", "mux_attn_fwd", "mux_attn_workspace_size", "mux_attn_bwd",
            "mux_rope", "mux_rmsnorm_fwd", "mux_rmsnorm_bwd", "mux_swiglu_fwd", "mux_swiglu_bwd", "mux_add", "mux_rs_flags_elems", "mux_linear_fwd_rs",
            "mux_linear_bwd_dx_rs", "mux_rs_reduce", "mux_ag_push", "mux_ag_release", "mux_linear_fwd_ag",
-           "mux_linear_bwd_ag")
+           "mux_linear_bwd_ag", "mux_linear_fwd_hs", "mux_linear_shrink")
 
 
 class MuxError(RuntimeError):
@@ -82,6 +82,10 @@ def lib():
         L.mux_linear_workspace_size.argtypes = [I32, I32, I32, I32, I32]
         L.mux_linear_fwd.restype = ctypes.c_int
         L.mux_linear_fwd.argtypes = [I32, P, P, I32, P, I32, I32, I32, I32, P, P, P, P, P, SZ, P]
+        L.mux_linear_fwd_hs.restype = ctypes.c_int
+        L.mux_linear_fwd_hs.argtypes = [I32, P, P, I32, P, I32, I32, I32, I32, P, P, P, P, P, SZ, P]
+        L.mux_linear_shrink.restype = ctypes.c_int
+        L.mux_linear_shrink.argtypes = [I32, P, P, I32, P, I32, I32, I32, I32, P, I32, I32, P, P, SZ, P]
         L.mux_linear_bwd.restype = ctypes.c_int
         L.mux_linear_bwd.argtypes = [I32, P, P, I32, P, I32, I32, I32, I32, P, P, P, P, P, P, SZ, P]
         L.mux_linear_bwd_part.restype = ctypes.c_int
@@ -279,6 +283,41 @@ def linear_fwd(seg_off: torch.Tensor, seg_task: Sequence[int], adapters: Sequenc
                                 _ptr(X), _ptr(W), _ptr(Y), _ptr(Hs), _ptr(workspace), workspace.numel(),
                                 _stream(stream)))
     return Y, Hs
+
+
+def linear_fwd_hs(seg_off: torch.Tensor, seg_task: Sequence[int], adapters: Sequence[Adapter],
+                  X: torch.Tensor, W: torch.Tensor, Hs: torch.Tensor, r_cap: int, Y: torch.Tensor = None,
+                  workspace: torch.Tensor = None, stream=None):
+    """mux_linear_fwd_hs: forward with the shrink Hs given (input).  Returns Y."""
+    max_rows, K = X.shape
+    N = W.shape[0]
+    if Y is None:
+        Y = torch.empty(max_rows, N, dtype=torch.bfloat16, device=X.device)
+    S = len(seg_task)
+    if workspace is None:
+        workspace = torch.zeros(linear_workspace_size(S, max_rows, K, N, r_cap), dtype=torch.uint8, device=X.device)
+    _check(lib().mux_linear_fwd_hs(S, _ptr(seg_off), _i32_host(seg_task), len(adapters),
+                                   _adapter_table(adapters, False), max_rows, K, N, r_cap, _ptr(X), _ptr(W),
+                                   _ptr(Y), _ptr(Hs), _ptr(workspace), workspace.numel(), _stream(stream)))
+    return Y
+
+
+def linear_shrink(seg_off: torch.Tensor, seg_task: Sequence[int], adapters: Sequence[Adapter],
+                  X: torch.Tensor, N: int, r_cap: int, row_begin: int = 0, row_end: int = None,
+                  Hs: torch.Tensor = None, workspace: torch.Tensor = None, stream=None):
+    """mux_linear_shrink: Hs rows of the pair row blocks in [row_begin, row_end).  Returns Hs."""
+    max_rows, K = X.shape
+    if row_end is None:
+        row_end = max_rows
+    if Hs is None:
+        Hs = torch.empty(max_rows, r_cap, dtype=torch.bfloat16, device=X.device)
+    S = len(seg_task)
+    if workspace is None:
+        workspace = torch.zeros(linear_workspace_size(S, max_rows, K, N, r_cap), dtype=torch.uint8, device=X.device)
+    _check(lib().mux_linear_shrink(S, _ptr(seg_off), _i32_host(seg_task), len(adapters),
+                                   _adapter_table(adapters, False), max_rows, K, N, r_cap, _ptr(X), row_begin,
+                                   row_end, _ptr(Hs), _ptr(workspace), workspace.numel(), _stream(stream)))
+    return Hs
 
 
 def linear_bwd(seg_off: torch.Tensor, seg_task: Sequence[int], adapters: Sequence[Adapter],

@@ -141,6 +141,18 @@ class MuxBackend:
         return self.mux.linear_fwd(seg_off, seg_task, adapters, X, W, r_cap, Y=Y, Hs=Hs,
                                    workspace=self._ws(W, X, seg_task, r_cap))
 
+    def shrink(self, seg_off, seg_task, adapters, X, W, r_cap, row_begin, row_end):
+        """Hs rows [row_begin, row_end) of the full (gathered) X only (mux_linear_shrink)."""
+        Hs = self._buf(("Hs", W.data_ptr()), (X.shape[0], r_cap), torch.bfloat16, X.device)
+        return self.mux.linear_shrink(seg_off, seg_task, adapters, X, W.shape[0], r_cap, row_begin, row_end, Hs=Hs,
+                                      workspace=self._ws(W, X, seg_task, r_cap))
+
+    def fwd_hs(self, seg_off, seg_task, adapters, X, W, Hs, r_cap):
+        """Forward with the shrink given (mux_linear_fwd_hs): no shrink tiles in the GEMM."""
+        Y = self._buf(("Y", W.data_ptr()), (X.shape[0], W.shape[0]), torch.bfloat16, X.device)
+        return self.mux.linear_fwd_hs(seg_off, seg_task, adapters, X, W, Hs, r_cap, Y=Y,
+                                      workspace=self._ws(W, X, seg_task, r_cap))
+
     def bwd(self, seg_off, seg_task, adapters, dY, X, W, Hs, r_cap):
         dX = self._buf(("dX", W.data_ptr()), tuple(X.shape), torch.bfloat16, X.device)
         dX = self.mux.linear_bwd(seg_off, seg_task, adapters, dY, X, W, Hs, r_cap, dX=dX,
@@ -252,9 +264,16 @@ def shard_row(W: torch.Tensor, adapters: Sequence, p: int, r: int, make_adapter)
 
 
 class ColumnParallelMuxLinear:
-    def __init__(self, backend, W_shard, adapters_shard, r_cap, group=None, fused_rs=False, fused_ag=False):
+    """shared_shrink: A_t is replicated, so Hs = s_t X A_t^T is the same on every rank.  Instead of
+    each rank recomputing all T rows of it inside its fused GEMM (shrink tiles over the gathered X),
+    each rank shrinks only its own R/p rows (mux_linear_shrink), the Hs rows are all-gathered
+    (T x r_cap, ~1/(K/r_cap) of X's gather) and the GEMM runs without shrink tiles
+    (mux_linear_fwd_hs).  R/p must be a multiple of 256 (pair row blocks)."""
+
+    def __init__(self, backend, W_shard, adapters_shard, r_cap, group=None, fused_rs=False, fused_ag=False,
+                 shared_shrink=False):
         self.be, self.W, self.ads, self.r_cap, self.group = backend, W_shard, adapters_shard, r_cap, group
-        self.fused_rs, self.fused_ag = fused_rs, fused_ag
+        self.fused_rs, self.fused_ag, self.shared_shrink = fused_rs, fused_ag, shared_shrink
         self._rs = self._ag = self._ag_held = None
 
     def forward(self, seg_off, seg_task, x_rows):
@@ -263,6 +282,12 @@ class ColumnParallelMuxLinear:
             Y, self.Hs, self.X = self.be.fwd_ag(self, seg_off, seg_task, x_rows)
             return Y
         self.X = all_gather_rows(x_rows, self.group)
+        if self.shared_shrink:
+            rows_p = x_rows.shape[0]
+            r0 = rows_p * _world(self.group)[1]
+            Hs = self.be.shrink(seg_off, seg_task, self.ads, self.X, self.W, self.r_cap, r0, r0 + rows_p)
+            self.Hs = all_gather_rows(Hs[r0:r0 + rows_p].contiguous(), self.group)
+            return self.be.fwd_hs(seg_off, seg_task, self.ads, self.X, self.W, self.Hs, self.r_cap)
         Y, self.Hs = self.be.fwd(seg_off, seg_task, self.ads, self.X, self.W, self.r_cap)
         return Y
 

@@ -174,3 +174,19 @@ def test_elementwise_ops_reject(mux):
     assert L.mux_swiglu_bwd(4, 16, A16, 16, A16, 16, A16, 16, A16, 16, A16, 12, None) == 1
     assert L.mux_pack_row_start(-1, A16, A16, 16, A16, None) == 1
     assert L.mux_swiglu_fwd(0, 16, A16, 16, A16, 16, A16, 16, None) == 0        # empty: no-op
+
+
+def test_fwd_hs_and_shrink_validation(mux):
+    """mux_linear_fwd_hs needs its input Hs; mux_linear_shrink needs an output Hs and a row range
+    that starts on a 256-row pair block (host-side checks, nothing launched)."""
+    L = mux.lib()
+    ads = _adapters(1)
+    st = (ctypes.c_int32 * 1)(0)
+    r = L.mux_linear_fwd_hs(1, 0x3000, st, 1, ads, 128, 256, 256, 16, 0x4000, 0x5000, 0x6000, None, 0x8000,
+                            1 << 30, None)
+    assert r == 1 and "Hs" in L.mux_last_error().decode()
+    r = L.mux_linear_shrink(1, 0x3000, st, 1, ads, 512, 256, 256, 16, 0x4000, 100, 512, 0x7000, 0x8000,
+                            1 << 30, None)
+    assert r == 1 and "row range" in L.mux_last_error().decode()
+    r = L.mux_linear_shrink(1, 0x3000, st, 1, ads, 512, 256, 256, 16, 0x4000, 0, 512, None, 0x8000, 1 << 30, None)
+    assert r == 1 and "Hs" in L.mux_last_error().decode()

@@ -240,3 +240,34 @@ def test_all_segments_empty():
     assert torch.all(Y == 3.0) and torch.all(dX == 5.0)
     for a in ads:
         assert torch.all(a.dA == 0) and torch.all(a.dB == 0)
+
+
+def test_shrink_and_fwd_with_given_hs_bit_identical():
+    """mux_linear_shrink over the whole range and over 256-row sub-ranges reproduces mux_linear_fwd's
+    Hs bit for bit (rows outside a sub-range untouched), and mux_linear_fwd_hs fed that Hs
+    reproduces Y bit for bit (the tensor-parallel shared-shrink path)."""
+    from paper_2603_02885_b200 import mux
+    from gpu_harness import to_dev_bf16
+    p = Problem(320, 640, [192, 64, 256, 128, 128], [16, 4, 64, 8, 0], seg_task=[0, 1, 2, 3, 4], seed=91,
+                r_cap=64, max_rows=1024)
+    seg_off = torch.from_numpy(p.seg_off).cuda()
+    X, W = to_dev_bf16(p.X), to_dev_bf16(p.W)
+    ads = p.gpu_adapters()
+    Y, Hs = mux.linear_fwd(seg_off, p.seg_task, ads, X, W, p.r_cap)
+    Hs_full = mux.linear_shrink(seg_off, p.seg_task, ads, X, p.N, p.r_cap)
+    Y2 = mux.linear_fwd_hs(seg_off, p.seg_task, ads, X, W, Hs, p.r_cap)
+    torch.cuda.synchronize()
+    R = p.R
+    assert torch.equal(Hs_full[:R].view(torch.int16), Hs[:R].view(torch.int16))
+    assert torch.equal(Y2[:R].view(torch.int16), Y[:R].view(torch.int16))
+    for lo, hi in ((0, 256), (256, 512), (512, 1024), (256, 1024)):
+        part = torch.full((p.max_rows, p.r_cap), float("nan"), device="cuda").bfloat16()
+        mux.linear_shrink(seg_off, p.seg_task, ads, X, p.N, p.r_cap, lo, hi, Hs=part)
+        torch.cuda.synchronize()
+        a, b = max(lo, 0), min(hi, R)
+        if b > a:
+            assert torch.equal(part[a:b].view(torch.int16), Hs[a:b].view(torch.int16)), (lo, hi)
+        outside = torch.cat([part[:lo], part[max(hi, lo):]])
+        assert torch.isnan(outside.float()).all(), (lo, hi)
+    with pytest.raises(mux.MuxError):
+        mux.linear_shrink(seg_off, p.seg_task, ads, X, p.N, p.r_cap, 100, 356)

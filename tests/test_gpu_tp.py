@@ -31,7 +31,8 @@ def pg():
     dist.destroy_process_group()
 
 
-def test_tp_world1_equals_direct(pg):
+@pytest.mark.parametrize("shared_shrink", [False, True])
+def test_tp_world1_equals_direct(pg, shared_shrink):
     if True:
         g = torch.Generator(device="cuda").manual_seed(3)
         R, K, N = 512, 256, 384
@@ -57,7 +58,7 @@ def test_tp_world1_equals_direct(pg):
         be = tp.MuxBackend()
         W1p, a1p = tp.shard_column(W1, a1, 1, 0, mk)
         W2p, a2p = tp.shard_row(W2, a2, 1, 0, mk)
-        up = tp.ColumnParallelMuxLinear(be, W1p, a1p, 32)
+        up = tp.ColumnParallelMuxLinear(be, W1p, a1p, 32, shared_shrink=shared_shrink)
         down = tp.RowParallelMuxLinear(be, W2p, a2p, 32)
         h = up.forward(seg_off, st, X)
         y = down.forward(seg_off, st, h)

@@ -43,6 +43,24 @@ class OracleBackend:
                                 X.numpy(), W.numpy(), r_cap)
         return torch.from_numpy(Y), torch.from_numpy(Hs)
 
+    def shrink(self, seg_off, seg_task, ads, X, W, r_cap, row_begin, row_end):
+        # rows outside the range are NaN: only the all-gathered own rows may reach the forward
+        _, Hs = self.fwd(seg_off, seg_task, ads, X, W, r_cap)
+        Hs = Hs.clone()
+        Hs[:row_begin] = float("nan")
+        Hs[row_end:] = float("nan")
+        return Hs
+
+    def fwd_hs(self, seg_off, seg_task, ads, X, W, Hs, r_cap):
+        # Eq. 1 with the given (gathered) shrink: Y = X W^T + Hs B_t^T on each segment's rows
+        Y = X.numpy() @ W.numpy().T
+        so, Hn = seg_off.numpy(), Hs.numpy()
+        for s, t in enumerate(seg_task):
+            a = ads[t]
+            if a.rank:
+                Y[so[s]:so[s + 1]] += Hn[so[s]:so[s + 1], :a.rank] @ a.B.numpy().T
+        return torch.from_numpy(Y)
+
     def bwd(self, seg_off, seg_task, ads, dY, X, W, Hs, r_cap):
         # the oracle recomputes H from X (fp64), which equals the saved Hs / s
         dX, Gs, grads = olin.linear_bwd(seg_off.numpy(), seg_task, [a.A.numpy() for a in ads],
@@ -52,7 +70,7 @@ class OracleBackend:
                 [torch.from_numpy(g[1]) for g in grads])
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, shared_shrink=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -65,7 +83,7 @@ def _worker(rank, world, port, q):
         W1p, a1p = tp.shard_column(T(W1), ads1, world, rank, mk)
         W2p, a2p = tp.shard_row(T(W2), ads2, world, rank, mk)
         be = OracleBackend()
-        up = tp.ColumnParallelMuxLinear(be, W1p, a1p, 16)
+        up = tp.ColumnParallelMuxLinear(be, W1p, a1p, 16, shared_shrink=shared_shrink)
         down = tp.RowParallelMuxLinear(be, W2p, a2p, 16)
         so = T(seg_off)
         st = [0, 1, 2]
@@ -90,12 +108,14 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("world", [2, 4, 8])
-def test_tp_column_row_matches_single_process(world):
+@pytest.mark.parametrize("world,shared_shrink", [(2, False), (4, False), (8, False), (2, True), (4, True)])
+def test_tp_column_row_matches_single_process(world, shared_shrink):
+    """shared_shrink: each rank shrinks only its own rows (NaN elsewhere) and the Hs rows are
+    all-gathered before the forward with the shrink given."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, shared_shrink)) for r in range(world)]
     for p in procs:
         p.start()
     res = sorted([q.get(timeout=240) for _ in range(world)], key=lambda x: x[0])

@@ -19,13 +19,17 @@ def main():
     mux._lib = None
     L = mux.lib()
     L.mux_debug_counters.argtypes = [ctypes.c_void_p, ctypes.c_int]
-    R = 11648
+    R = int(os.environ.get("MUX_ROWS", "11648"))
     rank = int(sys.argv[1]) if len(sys.argv) > 1 else 16
-    for K, N in [(4096, 4096), (4096, 11008), (11008, 4096)]:
+    shapes = [(4096, 4096), (4096, 11008), (11008, 4096)]
+    if len(sys.argv) > 2:  # e.g. 512x4096,4096x512 (tensor-parallel shard shapes)
+        shapes = [tuple(int(v) for v in x.split("x")) for x in sys.argv[2].split(",")]
+    for K, N in shapes:
         X = torch.randn(R, K, device="cuda").bfloat16()
         W = (torch.randn(N, K, device="cuda") / K ** 0.5).bfloat16()
         dY = torch.randn(R, N, device="cuda").bfloat16()
-        seg_off = torch.tensor([0, 2944, 5888, 8768, R], dtype=torch.int32, device="cuda")
+        q4 = R // 4 // 64 * 64
+        seg_off = torch.tensor([0, q4, 2 * q4, 3 * q4, R], dtype=torch.int32, device="cuda")
         ads = []
         for t in range(4):
             B = mux.make_B_storage(N, rank)

@@ -1,0 +1,125 @@
+#!/usr/bin/env python
+"""Per-rank compute of tensor parallelism measured on one B200:
+every linear of a config-4 / config-5 block at its p-way Megatron shard shape
+(column-parallel q, k, v, gate, up: N/p; row-parallel o, down: K/p; sequence
+parallelism gives every rank all T rows at the GEMM), fused fwd+bwd of the
+packed multi-task call (16 / 32 tasks, ranks as the config), device time of a
+CUDA graph.  Beside it, the per-rank collective bytes of one block step
+(AG before q/k/v and gate/up, RS after o and down, and the mirrored pair in
+backward: 8 collectives of (p-1)/p * T * H * 2 bytes) and the time they take at
+the NVLink 5 per-direction peak of 900 GB/s — what must hide under the compute
+for TP to scale.  One GPU only: the collectives themselves are not run here.
+usage: python tools/tp_shard_profile.py [--out profiles/r01_tp_shard_profile.jsonl]
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+NVLINK_GBS = 900.0
+COLUMN = {"q", "k", "v", "gate", "up"}
+
+
+def time_graph(fn, reps=3):
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for _ in range(reps):
+            fn()
+    g.replay()
+    torch.cuda.synchronize()
+    vals = []
+    for _ in range(5):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        g.replay()
+        b.record()
+        torch.cuda.synchronize()
+        vals.append(a.elapsed_time(b) / reps)
+    del g
+    return statistics.median(vals)
+
+
+def block_at(mux, wl, p, shared_shrink=False):
+    M = wl.num_tasks
+    seg = -(-wl.valid_tokens // M // 64) * 64
+    R = seg * M
+    seg_off = torch.tensor([i * seg for i in range(M + 1)], dtype=torch.int32, device="cuda")
+    st = list(range(M))
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    r_cap = max(16, -(-max(wl.ranks) // 16) * 16)
+    total_ms, flops, per = 0.0, 0.0, []
+    for L in wl.linears:
+        K, N = (L.K, L.N // p) if L.name in COLUMN else (L.K // p, L.N)
+        W = (torch.randn(N, K, device="cuda", generator=gen) / K ** 0.5).bfloat16()
+        ads = []
+        for r in wl.ranks:
+            B = mux.make_B_storage(N, r)
+            B.copy_(torch.randn(N, r, device="cuda", generator=gen).bfloat16())
+            ads.append(mux.Adapter((torch.randn(r, K, device="cuda", generator=gen) / K ** 0.5).bfloat16(), B, r,
+                                   2.0, torch.empty(r, K, device="cuda"), torch.empty(N, r, device="cuda")))
+        X = torch.randn(R, K, device="cuda", generator=gen).bfloat16()
+        dY = torch.randn(R, N, device="cuda", generator=gen).bfloat16()
+        Y = torch.empty(R, N, dtype=torch.bfloat16, device="cuda")
+        Hs = torch.empty(R, r_cap, dtype=torch.bfloat16, device="cuda")
+        dX = torch.empty(R, K, dtype=torch.bfloat16, device="cuda")
+        ws = torch.zeros(mux.linear_workspace_size(M, R, K, N, r_cap), dtype=torch.uint8, device="cuda")
+
+        hi = -(-R // p // 256) * 256  # this rank's rows (rounded to pair blocks)
+
+        def step():
+            if shared_shrink and L.name in COLUMN:
+                # tp.py shared_shrink: own rows' shrink, (Hs all-gather: T x r_cap, not run), then
+                # the fused GEMM without shrink tiles
+                mux.linear_shrink(seg_off, st, ads, X, N, r_cap, 0, hi, Hs=Hs, workspace=ws)
+                mux.linear_fwd_hs(seg_off, st, ads, X, W, Hs, r_cap, Y=Y, workspace=ws)
+            else:
+                mux.linear_fwd(seg_off, st, ads, X, W, r_cap, Y=Y, Hs=Hs, workspace=ws)
+            mux.linear_bwd(seg_off, st, ads, dY, X, W, Hs, r_cap, dX=dX, workspace=ws)
+
+        ms = time_graph(step)
+        f = sum(seg * (4 * K * N + 6 * r * (K + N)) for r in wl.ranks)  # SURVEY §8(d) per token
+        per.append({"linear": L.name, "K": K, "N": N, "ms": round(ms, 4), "tflops": round(f / ms / 1e9, 1)})
+        total_ms += ms
+        flops += f
+        del W, ads, X, dY, Y, Hs, dX, ws
+        torch.cuda.empty_cache()
+    H = wl.linears[0].K
+    comm_bytes = 8 * (p - 1) / p * R * H * 2
+    comm_ms = comm_bytes / (NVLINK_GBS * 1e9) * 1e3
+    return {"config": wl.config_id, "tp": p, "shared_shrink": shared_shrink, "rows": R, "tasks": M, "compute_ms_per_rank": round(total_ms, 3),
+            "tflops_per_rank": round(flops / total_ms / 1e9, 1), "comm_bytes_per_rank": int(comm_bytes),
+            "comm_ms_at_900GBs": round(comm_ms, 3), "comm_over_compute": round(comm_ms / total_ms, 3),
+            "linears": per}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default=None)
+    ap.add_argument("--points", default="4:1,4:2,4:4,4:8,5:1,5:8")
+    ap.add_argument("--shared-shrink", action="store_true", help="column layers: own-rows shrink + fwd_hs")
+    a = ap.parse_args()
+    from paper_2603_02885_b200 import mux
+    import synth
+    out = open(a.out, "w") if a.out else None
+    for pt in a.points.split(","):
+        cid, p = pt.split(":")
+        r = block_at(mux, synth.configs.workload(cid), int(p), a.shared_shrink)
+        line = json.dumps(r)
+        print(line, flush=True)
+        if out:
+            out.write(line + "\n")
+
+
+if __name__ == "__main__":
+    main()
