@@ -77,18 +77,36 @@ struct PairGroups {
   int hm[4];
 };
 
+// Binary search over the (non-decreasing) segment offsets: the segment s with
+// so[s] <= row < so[s+1], or -1.  Empty segments are skipped by construction
+// (the largest s with so[s] <= row is taken).
 __device__ __forceinline__ int seg_containing(const int* so, int S, int row) {
-  for (int s = 0; s < S; ++s)
-    if (so[s] <= row && row < so[s + 1]) return s;
-  return -1;
+  if (S <= 0 || row < so[0] || row >= so[S]) return -1;
+  int lo = 0, hi = S;  // so[lo] <= row < so[hi]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (so[mid] <= row) lo = mid; else hi = mid;
+  }
+  return lo;
 }
 
+// Runs once per tile in the producer and the MMA issuer: the first quarter's
+// segment by binary search, the next quarters by advancing from it (a linear
+// search per quarter was ~2.5 k cycles per tile at 16 segments, which the
+// producer could not hide behind short reductions).
 __device__ __forceinline__ PairGroups pair_groups(const GemmParams& p, const int* so, int m) {
   PairGroups g;
   g.n = 0;
+  const int S = p.num_segs;
+  const int row0 = m * kPairRows;
+  int s = seg_containing(so, S, row0);
+  if (s < 0 && S > 0 && row0 < so[0]) s = 0;  // rows before the first segment: start from segment 0
   for (int h = 0; h < 4; ++h) {
-    const int s = seg_containing(so, p.num_segs, m * kPairRows + kRowQuarter * h);
-    if (s < 0 || p.seg_rank[s] == 0) continue;
+    const int row = row0 + kRowQuarter * h;
+    if (s < 0 || row >= so[S]) break;
+    while (s + 1 < S && so[s + 1] <= row) ++s;
+    if (!(so[s] <= row && row < so[s + 1])) continue;
+    if (p.seg_rank[s] == 0) continue;
     int f = -1;
     for (int i = 0; i < g.n; ++i)
       if (g.seg[i] == s) f = i;
@@ -337,7 +355,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             __syncwarp();
             advance();
           }
+#ifdef MUX_DIAG_NO_FLAG
+          if (false) {  // timing-only diagnostic: no wait for the shrink tile (results may race)
+#else
           if (g.n > 0 && p.has_side) {
+#endif
             // the side tile of this row block must have published Hs/Gs (a caller-given
             // Hs was written by an earlier kernel in stream order)
             if (elect_one_sync()) {
