@@ -180,15 +180,36 @@ class MuxStep:
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
-    """Samples SM clock, power and throttle reasons through NVML every 2 ms in
-    a background thread while the timed region runs (nvidia-smi's 100 ms
-    floor would see only a handful of samples of a sub-second region)."""
+    """Samples SM clock, power and throttle reasons through NVML every 2 ms
+    while the timed region runs (nvidia-smi's 100 ms floor would see only a
+    handful of samples of a sub-second region).  The sampler is a separate
+    process (no GIL contention with the launching thread; an in-process
+    thread once got a single sample on a busy host), with an in-process
+    thread as the fallback."""
+
+    _CHILD = r"""
+import json, select, sys, time
+import pynvml as nv
+nv.nvmlInit()
+h = nv.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
+print("ready", flush=True)
+out = []
+while not select.select([sys.stdin], [], [], 0)[0]:
+    try:
+        out.append((nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM), nv.nvmlDeviceGetPowerUsage(h) / 1000.0,
+                    nv.nvmlDeviceGetCurrentClocksEventReasons(h)))
+    except Exception:
+        pass
+    time.sleep(0.002)
+print(json.dumps(out), flush=True)
+"""
 
     def __init__(self, gpu_index):
         self.idx = gpu_index
         self.samples = []
         self.stop_evt = None
         self.th = None
+        self.proc = None
         self.err = None
 
     def start(self):
@@ -201,6 +222,18 @@ class ClockSampler:
         except Exception as e:  # noqa: BLE001
             self.err = f"nvml unavailable: {e}"
             return
+        try:
+            import subprocess
+            self.proc = subprocess.Popen([sys.executable, "-c", self._CHILD, str(self.idx)], stdin=subprocess.PIPE,
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL)
+            if self.proc.stdout.readline().strip() != b"ready":
+                raise RuntimeError("sampler process did not start")
+            time.sleep(0.01)
+            return
+        except Exception:  # noqa: BLE001
+            if self.proc is not None:
+                self.proc.kill()
+            self.proc = None
         self.stop_evt = threading.Event()
 
         def loop():
@@ -218,10 +251,20 @@ class ClockSampler:
         time.sleep(0.01)
 
     def stop(self):
-        if self.th is None:
+        src = "nvml, 2 ms, timed region only"
+        if self.proc is not None:
+            try:
+                out, _ = self.proc.communicate(b"stop\n", timeout=30)
+                self.samples = [tuple(x) for x in json.loads(out.decode().strip().splitlines()[-1])]
+                src += " (sampler process)"
+            except Exception as e:  # noqa: BLE001
+                self.proc.kill()
+                return {"sm_mhz": None, "sm_max_mhz": self.smax, "reasons": [f"sampler process failed: {e}"]}
+        elif self.th is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [self.err or "no sampler"]}
-        self.stop_evt.set()
-        self.th.join()
+        else:
+            self.stop_evt.set()
+            self.th.join()
         import pynvml as nv
         names = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
                  "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
@@ -234,7 +277,7 @@ class ClockSampler:
         reasons = sorted({n for (_, _, r) in self.samples for n, b in names.items() if r & b})
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": self.smax, "reasons": reasons,
                 "samples": len(sm), "power_w_max": max(x[1] for x in self.samples),
-                "sm_mhz_min": min(sm), "source": "nvml, 2 ms, timed region only"}
+                "sm_mhz_min": min(sm), "source": src}
 
 
 # ------------------------------------------------------------------ cpu / reference arm
