@@ -54,7 +54,7 @@ def _problem():
     return W1, a1, W2, a2, X, dY
 
 
-def _worker(rank, world, port, q, boxes, fused_ag):
+def _worker(rank, world, port, q, boxes, fused_ag, shared_shrink=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch.distributed as dist
     torch.cuda.set_device(0)
@@ -82,7 +82,8 @@ def _worker(rank, world, port, q, boxes, fused_ag):
         be.rs_exchange = exchange
         W1p, a1p = tp.shard_column(W1, a1, world, rank, mk)
         W2p, a2p = tp.shard_row(W2, a2, world, rank, mk)
-        up = tp.ColumnParallelMuxLinear(be, W1p, a1p, 32, fused_rs=True, fused_ag=fused_ag)
+        up = tp.ColumnParallelMuxLinear(be, W1p, a1p, 32, fused_rs=True, fused_ag=fused_ag,
+                                        shared_shrink=shared_shrink)
         down = tp.RowParallelMuxLinear(be, W2p, a2p, 32, fused_rs=True, fused_ag=fused_ag)
         rows = R // world
         for _ in range(2):   # twice: receive slots and flags reused
@@ -108,8 +109,10 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("fused_ag", [False, True])
-def test_fused_rs_two_processes_one_gpu(fused_ag):
+@pytest.mark.parametrize("fused_ag,shared_shrink", [(False, False), (True, False), (False, True)])
+def test_fused_rs_two_processes_one_gpu(fused_ag, shared_shrink):
+    """shared_shrink: each process shrinks its own 256 rows (mux_linear_shrink), the Hs rows are
+    all-gathered over the process group, and the column GEMM runs with the shrink given."""
     from paper_2603_02885_b200 import mux
     from gpu_harness import TOL, rel_err
     world = 2
@@ -117,7 +120,8 @@ def test_fused_rs_two_processes_one_gpu(fused_ag):
     q = ctx.Queue()
     port = _free_port()
     boxes = [ctx.Queue() for _ in range(world)]
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q, boxes, fused_ag)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, boxes, fused_ag, shared_shrink))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = sorted([q.get(timeout=300) for _ in range(world)], key=lambda x: x[0])
