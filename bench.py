@@ -364,9 +364,17 @@ def main_arm(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # MUX_BENCH_DIST_BACKEND=gloo (test only): exercise the N > 1 path with several ranks sharing
+    # the visible GPUs (device = LOCAL_RANK mod count); the driver's runs use NCCL, one GPU per rank
+    backend = os.environ.get("MUX_BENCH_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     mux.lib()
 
     w = Workload(args.config, rank_seed=rank)
@@ -570,11 +578,17 @@ def tp_arm(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    backend = os.environ.get("MUX_BENCH_DIST_BACKEND", "nccl")  # gloo: test-only, ranks may share a GPU
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if not dist.is_initialized():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29511")
-        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend, rank=rank, world_size=world)
     w = Workload(args.config)
     h = w.host_tensors()
     i32 = dict(dtype=torch.int32, device="cuda")
