@@ -268,7 +268,9 @@ class ColumnParallelMuxLinear:
     each rank recomputing all T rows of it inside its fused GEMM (shrink tiles over the gathered X),
     each rank shrinks only its own R/p rows (mux_linear_shrink), the Hs rows are all-gathered
     (T x r_cap, ~1/(K/r_cap) of X's gather) and the GEMM runs without shrink tiles
-    (mux_linear_fwd_hs).  R/p must be a multiple of 256 (pair row blocks)."""
+    (mux_linear_fwd_hs).  R/p must be a multiple of 256 (pair row blocks).  It applies to the
+    NCCL all-gather path; with fused_ag the gathered rows arrive inside the GEMM, which then
+    computes the shrink itself."""
 
     def __init__(self, backend, W_shard, adapters_shard, r_cap, group=None, fused_rs=False, fused_ag=False,
                  shared_shrink=False):
