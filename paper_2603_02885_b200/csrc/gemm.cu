@@ -186,10 +186,14 @@ __device__ __forceinline__ Tile tile_at(int t, int num_m, int num_n, int group_m
 #define PROF_ADD(acc, t0)
 #endif
 
-template <bool kBwd>
+template <bool kBwd, bool kNarrow>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     mux_gemm_kernel(const __grid_constant__ GemmParams p) {
   using Ly = GemmLayout<kBwd>;
+  // kNarrow: 256 x 128 pair tiles (64 output columns per CTA) for narrow outputs, where 256-wide
+  // tiles leave most CTA pairs idle (e.g. 512-column tensor-parallel shards: 2 tiles per row block)
+  constexpr int kTileN = kNarrow ? 128 : kBN;
+  constexpr int kHalves = kTileN / 128;  // 64-column boxes per CTA
   constexpr int kBK = Ly::kBK;
   constexpr int kKSub = Ly::kKSub;
   constexpr int kStages = Ly::kStages;
@@ -250,7 +254,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
 
   const int total_rows = so[p.num_segs];
   const int num_m = (total_rows + kPairRows - 1) / kPairRows;
-  const int num_n = (p.nout + kBN - 1) / kBN;
+  const int num_n = (p.nout + kTileN - 1) / kTileN;
   const int side_lo = min(p.side_m_lo, num_m);
   const int total_tiles = p.has_main ? num_m * (num_n + (p.has_side ? 1 : 0))
                                      : max(0, min(p.side_m_hi, num_m) - side_lo);
@@ -329,7 +333,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             }
           }
         } else {
-          const int col_c = tl.n * kBN + (kBN / 2) * rk;  // this CTA's half of N
+          const int col_c = tl.n * kTileN + (kTileN / 2) * rk;  // this CTA's half of N
           for (int kb = 0; kb < num_kb; ++kb) {
             PROF_T0(tw_);
             mbar_wait(&empty_bar[stage], phase ^ 1u);
@@ -338,13 +342,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
               const uint32_t sa = pipe_u + stage * kStageBytes;
               const uint32_t sb = sa + kStageA;
               const uint32_t fbl = full_leader + 8u * stage;
-              if (leader) mbar_arrive_expect_tx_u32(full_u + 8u * stage, 2u * kStageBytes);
+              if (leader) mbar_arrive_expect_tx_u32(full_u + 8u * stage, 2u * (kStageA + kKSub * kHalves * kBox));
               const int k0 = kb * kBK;
 #pragma unroll
               for (int s2 = 0; s2 < kKSub; ++s2) {
                 tma_load_2d_pair_u32(&p.map_a, fbl, sa + s2 * kSubA, k0 + 64 * s2, row_c);
 #pragma unroll
-                for (int i = 0; i < 2; ++i) {
+                for (int i = 0; i < kHalves; ++i) {
                   if (!kBwd)  // W [N, K] K-major rows n: k-subtile s2, rows 64i..
                     tma_load_2d_pair_u32(&p.map_w, fbl, sb + s2 * kSubA + i * kBox, k0 + 64 * s2, col_c + 64 * i);
                   else        // W viewed [k_out (MN), n (red)]: atom i, K-rows 64*s2..
@@ -385,10 +389,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
               const uint32_t sa = pipe_u + stage * kStageBytes;
               const uint32_t sb = sa + kStageA;
               const uint32_t fbl = full_leader + 8u * stage;
-              if (leader) mbar_arrive_expect_tx_u32(full_u + 8u * stage, 2u * (kSubA + 2 * kBox));
+              if (leader) mbar_arrive_expect_tx_u32(full_u + 8u * stage, 2u * (kSubA + kHalves * kBox));
               tma_load_2d_pair_u32(&p.map_side, fbl, sa, 0, row_c);
 #pragma unroll
-              for (int j = 0; j < 2; ++j) {
+              for (int j = 0; j < kHalves; ++j) {
                 if (!kBwd)  // B_t [N, r] K-major rows n: box {64 j, 64 n}
                   tma_load_2d_pair_u32(&p.map_lora_b[ad], fbl, sb + j * kBox, 0, col_c + 64 * j);
                 else        // A_t [r, K] viewed [k_out (MN), j (red)]: atom j, K-rows 0..63
@@ -406,7 +410,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     // The whole warp runs the loop (warp-uniform values stay in uniform
     // registers); one elected lane issues tcgen05.mma / tcgen05.commit.
     if (leader) {
-      constexpr uint32_t kIdescMain = idesc_bf16(kPairRows, kBN, false, kBwd);
+      constexpr uint32_t kIdescMain = idesc_bf16(kPairRows, kTileN, false, kBwd);
       constexpr uint32_t kIdescSide = idesc_bf16(kPairRows, kSideN, false, kBwd);
       // B operand per CTA: K-major rows of 128 B (SBO 1024), or MN-major atoms
       // of 64 elements x 64 K-rows (LBO 8 KB between atoms, SBO 1024).
@@ -577,14 +581,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         if (lane == 0) flag_arrive(p.flags + tl.m, epoch);
       } else {
         const bool valid = row_w < total_rows;
-        const int col_t = tl.n * kBN;
+        const int col_t = tl.n * kTileN;
 #pragma unroll 1
-        for (int c = 0; c < kBN / 64; ++c) {
+        for (int c = 0; c < kTileN / 64; ++c) {
           uint32_t v0[32], v1[32];
           tmem_ld32(t_addr + c * 64, v0);
           tmem_ld32(t_addr + c * 64 + 32, v1);
           tmem_ld_wait();
-          if (c == kBN / 64 - 1) {
+          if (c == kTileN / 64 - 1) {
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(tempty_leader);
@@ -668,11 +672,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
 }
 
 // ---------------------------------------------------------------- launchers
-template <bool kBwd>
+template <bool kBwd, bool kNarrow>
 cudaError_t launch_gemm_impl(const GemmParams& p, int grid, cudaStream_t stream) {
   static std::atomic<uint64_t> configured{0};
   cudaError_t ce = once_per_device(configured, [] {
-    return cudaFuncSetAttribute(mux_gemm_kernel<kBwd>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    return cudaFuncSetAttribute(mux_gemm_kernel<kBwd, kNarrow>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(GemmLayout<kBwd>::kSmemBytes));
   });
   if (ce != cudaSuccess) return ce;
@@ -686,12 +690,13 @@ cudaError_t launch_gemm_impl(const GemmParams& p, int grid, cudaStream_t stream)
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, mux_gemm_kernel<kBwd>, p);
+  return cudaLaunchKernelEx(&cfg, mux_gemm_kernel<kBwd, kNarrow>, p);
 }
 
-// grid must be even (clusters of 2)
-cudaError_t launch_gemm(const GemmParams& p, bool bwd, int grid, cudaStream_t stream) {
-  return bwd ? launch_gemm_impl<true>(p, grid, stream) : launch_gemm_impl<false>(p, grid, stream);
+// grid must be even (clusters of 2); narrow: 256 x 128 tiles (see kNarrow)
+cudaError_t launch_gemm(const GemmParams& p, bool bwd, bool narrow, int grid, cudaStream_t stream) {
+  if (narrow) return bwd ? launch_gemm_impl<true, true>(p, grid, stream) : launch_gemm_impl<false, true>(p, grid, stream);
+  return bwd ? launch_gemm_impl<true, false>(p, grid, stream) : launch_gemm_impl<false, false>(p, grid, stream);
 }
 
 }  // namespace mux

@@ -14,6 +14,12 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+// fused GEMM: outputs this narrow use 256 x 128 tiles (only where a 256-wide tile would be at least
+// half empty: wider narrow tiles lose more to the doubled A-operand feed than they gain in balance,
+// profiles/r01_gemm_ab_narrow.jsonl)
+#ifndef MUX_NARROW_MAX_NOUT
+#define MUX_NARROW_MAX_NOUT 128
+#endif
 // fused GEMM: reductions this short schedule every shrink tile before the main tiles
 #ifndef MUX_SIDE_FIRST_MAX_KRED
 #define MUX_SIDE_FIRST_MAX_KRED 2048
@@ -22,7 +28,7 @@
 #include "common.h"
 
 namespace mux {
-cudaError_t launch_gemm(const GemmParams& p, bool bwd, int grid, cudaStream_t stream);
+cudaError_t launch_gemm(const GemmParams& p, bool bwd, bool narrow, int grid, cudaStream_t stream);
 cudaError_t launch_grad(const GradParams& p, int grid, cudaStream_t stream);
 cudaError_t launch_grad_simt(const GradParams& p, int grid, cudaStream_t stream);
 size_t pack_workspace_bytes(int M, int S);
@@ -477,7 +483,10 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
     p.seg_scale[s] = a.scale;
   }
   const int num_m_max = (max_rows + kPairRows - 1) / kPairRows;
-  const int num_n = (nout + kBN - 1) / kBN;
+  // narrow outputs (<= MUX_NARROW_MAX_NOUT columns): 256 x 128 tiles, twice as many work items
+  const bool narrow = nout <= MUX_NARROW_MAX_NOUT;
+  const int tile_n = narrow ? kBN / 2 : kBN;
+  const int num_n = (nout + tile_n - 1) / tile_n;
   const long long side_blocks = p.has_main ? (p.has_side ? num_m_max : 0)
                                            : std::max(0, std::min(p.side_m_hi, num_m_max) - std::min(p.side_m_lo, num_m_max));
   const long long tiles_max = side_blocks + (p.has_main ? static_cast<long long>(num_m_max) * num_n : 0);
@@ -490,7 +499,7 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
   if (e != cudaSuccess) return cuda_fail(e, "debug segment check launch");
 #endif
   if (parts & 1) {
-    e = launch_gemm(p, bwd, grid, stream);
+    e = launch_gemm(p, bwd, narrow, grid, stream);
     if (e != cudaSuccess) return cuda_fail(e, bwd ? "mux_linear_bwd dX launch" : "mux_linear_fwd launch");
   }
 
