@@ -37,6 +37,21 @@ CASES = [("2", 0), ("2", 1), ("2", 2), ("3a", 2), ("3b", 0), ("3c", 1), ("4", 0)
 
 @pytest.mark.parametrize("cid,li", CASES)
 def test_full_size_linear(cid, li):
+    _full_size(cid, li)
+
+
+# tensor-parallel shards at TP 8: each rank's local linear is itself a multiplexed
+# linear on a slice; these exercise the narrow-tile path (config 5 k: N = 1024/8 = 128), the
+# short-reduction schedule (config 5 o: K = 8192/8 = 1024; config 4 q's dX: N = 512) at full rows
+TP_CASES = [("5", 1, 8, "col", 3), ("5", 3, 8, "row", 5), ("4", 0, 8, "col", 0), ("4", 6, 8, "row", 7)]
+
+
+@pytest.mark.parametrize("cid,li,p,kind,part", TP_CASES)
+def test_full_size_tp_shard(cid, li, p, kind, part):
+    _full_size(cid, li, (p, kind, part))
+
+
+def _full_size(cid, li, shard=None):
     wl = synth.workload(cid)
     off, lens = wl.csr()
     L = wl.linears[li]
@@ -54,20 +69,34 @@ def test_full_size_linear(cid, li):
     # token-major inputs -> packed rows (GPU: mux_pack_apply; oracle: numpy placement)
     Xtok = synth.token_input(wl, li, "X", L.K)
     dYtok = synth.token_input(wl, li, "dY", L.N)
+    W = synth.weight(wl, li)
+    A, B = zip(*[synth.adapter(wl, li, t) for t in range(wl.num_tasks)])
+    K, N = L.K, L.N
+    if shard is not None:  # Megatron shard of this rank: column = N slice, row = K slice
+        p, kind, part = shard
+        c = np.ascontiguousarray
+        if kind == "col":
+            N //= p
+            n0 = part * N
+            W, dYtok = c(W[n0:n0 + N]), c(dYtok[:, n0:n0 + N])
+            B = tuple(c(b[n0:n0 + N]) for b in B)
+        else:
+            K //= p
+            k0 = part * K
+            W, Xtok = c(W[:, k0:k0 + K]), c(Xtok[:, k0:k0 + K])
+            A = tuple(c(a[:, k0:k0 + K]) for a in A)
     X = mux.pack_apply(o["row_src"], to_dev_bf16(Xtok), max_rows)
     dY = mux.pack_apply(o["row_src"], to_dev_bf16(dYtok), max_rows)
     rs = ref["row_src"][:R]
-    Xp = np.zeros((R, L.K), np.uint16)
+    Xp = np.zeros((R, K), np.uint16)
     Xp[rs >= 0] = Xtok[rs[rs >= 0]]
-    dYp = np.zeros((R, L.N), np.uint16)
+    dYp = np.zeros((R, N), np.uint16)
     dYp[rs >= 0] = dYtok[rs[rs >= 0]]
     assert np.array_equal(from_dev_bf16(X)[:R], Xp)
-    W = synth.weight(wl, li)
-    A, B = zip(*[synth.adapter(wl, li, t) for t in range(wl.num_tasks)])
     r_cap = 16 * -(-max(wl.ranks) // 16)
     ads = []
     for t, r in enumerate(wl.ranks):
-        Bs = mux.make_B_storage(L.N, r)
+        Bs = mux.make_B_storage(N, r)
         Bs.copy_(to_dev_bf16(B[t]))
         ads.append(mux.Adapter(to_dev_bf16(A[t]), Bs, r, wl.scales[t]))
     seg_task = list(range(wl.num_tasks))
@@ -92,5 +121,5 @@ def test_full_size_linear(cid, li):
     if len(pad):
         assert np.all(bf16_to_f64(from_dev_bf16(Y)[pad]) == 0.0)
     worst = max(errs.values())
-    print(cid, L.name, R, "worst", worst)
+    print(cid, L.name, shard, R, "worst", worst)
     assert worst <= TOL, errs
