@@ -27,9 +27,13 @@
 // tasks; their adapter MMAs carry the tcgen05 disable-output-lane mask of every
 // other task's rows, so a row is only ever multiplied by its own task's
 // weights (NaN isolation).
-// Side tiles come first in their band and never wait, so every dependency
-// points to a lower tile index: with all CTAs resident the lowest unfinished
-// tile always progresses (no deadlock).
+// Side tiles come first in their band (or, for reductions <= 2048, before all
+// main tiles) and never wait, so every dependency points to a lower tile
+// index: with all CTAs resident the lowest unfinished tile always progresses
+// (no deadlock).  Variants of the same kernel: has_main = 0 runs side tiles
+// only, over a row-block range (mux_linear_shrink); has_side = 0 runs main
+// tiles only, with Hs given by the caller (mux_linear_fwd_hs); kNarrow uses
+// 256 x 128 pair tiles (outputs <= 128 columns).
 //
 // Roles (256 threads per CTA): warp 0 = TMA producer (both CTAs), warp 1 = MMA
 // issuer (leader CTA), warp 2 = TMEM allocator, warps 4..7 = epilogue
