@@ -277,6 +277,11 @@ MUX_API mux_status mux_linear_bwd_part(int32_t part, int32_t num_segs, const int
  * overwriting its slot, and publishes call seq when its last tile landed;
  * mux_rs_reduce waits for all sources' call seq, then acknowledges.  Both are
  * stream-ordered (no host synchronisation).
+ * Waits on another rank's flag (here and in the all-gather below) give up
+ * after MUX_PEER_TIMEOUT_S seconds (environment, read once per process;
+ * default 600, 0 = never) by trapping, which the caller sees as a sticky
+ * CUDA error: rank skew (a checkpoint or an eval on one rank) is normal, only
+ * a protocol bug never completes.  Waits inside one GPU keep an 8 s watchdog.
  * ------------------------------------------------------------------------- */
 typedef struct {
   int32_t world;                                  /* 1 .. MUX_RS_MAX_WORLD */

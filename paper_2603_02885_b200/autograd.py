@@ -24,10 +24,13 @@ class _MuxLinearFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, X, seg_off, W, mod, *params):
         ads = mod._adapters()
-        Y, Hs = mux.linear_fwd(seg_off, mod._seg_task, ads, X.contiguous(), W, mod.r_cap,
-                               workspace=mod._workspace(X.shape[0]))
-        ctx.save_for_backward(X, seg_off, Hs)
+        seg_task = list(mod._seg_task)
+        Xc = X.contiguous()       # the tensor the kernel reads is the one backward re-reads
+        Y, Hs = mux.linear_fwd(seg_off, seg_task, ads, Xc, W, mod.r_cap,
+                               workspace=mod._workspace(Xc.shape[0], len(seg_task)))
+        ctx.save_for_backward(Xc, seg_off, Hs)
         ctx.mod = mod
+        ctx.seg_task = seg_task   # this call's segment -> adapter map (the module may be re-called)
         return Y
 
     @staticmethod
@@ -36,8 +39,8 @@ class _MuxLinearFn(torch.autograd.Function):
         mod = ctx.mod
         ads = mod._adapters()
         want_dx = ctx.needs_input_grad[0]
-        dX = mux.linear_bwd(seg_off, mod._seg_task, ads, dY.contiguous(), X, mod.W, Hs, mod.r_cap,
-                            want_dx=want_dx, workspace=mod._workspace(X.shape[0]))
+        dX = mux.linear_bwd(seg_off, ctx.seg_task, ads, dY.contiguous(), X, mod.W, Hs, mod.r_cap,
+                            want_dx=want_dx, workspace=mod._workspace(X.shape[0], len(ctx.seg_task)))
         grads: List = []
         for t, a in enumerate(ads):
             if a.rank == 0:
@@ -77,9 +80,8 @@ class MuxLoRALinear(torch.nn.Module):
         return [mux.Adapter(self.A[t].data if r else None, self.B[t].data if r else None, r, self.scales[t])
                 for t, r in enumerate(self.ranks)]
 
-    def _workspace(self, rows: int):
-        need = mux.linear_workspace_size(max(1, len(self._seg_task)), rows, self.W.shape[1], self.W.shape[0],
-                                         self.r_cap)
+    def _workspace(self, rows: int, num_segs: int):
+        need = mux.linear_workspace_size(max(1, num_segs), rows, self.W.shape[1], self.W.shape[0], self.r_cap)
         if self._ws is None or self._ws.numel() < need:
             self._ws = torch.zeros(need, dtype=torch.uint8, device=self.W.device)
         return self._ws

@@ -44,20 +44,25 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str = Non
     lib = LIB if out is None else os.path.join(HERE, out)
     if not force and not stale(lib):
         return lib
-    objs = []
+    from concurrent.futures import ThreadPoolExecutor
     bdir = os.path.join(HERE, "build" if out is None else "build_" + os.path.splitext(out)[0])
     os.makedirs(bdir, exist_ok=True)
-    for src in sources():
+
+    def compile_one(src):
         obj = os.path.join(bdir, os.path.basename(src) + ".o")
         cmd = [NVCC, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"), "-c", src,
                "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        if r.returncode != 0:
-            sys.stderr.write(r.stdout + r.stderr)
-            raise RuntimeError(f"nvcc failed on {src}")
-        if verbose:
-            sys.stderr.write(r.stderr)
-        objs.append(obj)
+        return obj, subprocess.run(cmd, capture_output=True, text=True)
+
+    objs = []
+    with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
+        for src, (obj, r) in zip(sources(), ex.map(compile_one, sources())):
+            if r.returncode != 0:
+                sys.stderr.write(r.stdout + r.stderr)
+                raise RuntimeError(f"nvcc failed on {src}")
+            if verbose:
+                sys.stderr.write(r.stderr)
+            objs.append(obj)
     tmp = lib + ".tmp"
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
            "-o", tmp, *objs]

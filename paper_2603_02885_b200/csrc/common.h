@@ -77,6 +77,7 @@ struct GemmParams {
   int32_t ag_rows;
   unsigned long long ag_seq;
   const unsigned long long* ag_flags;
+  unsigned long long peer_wait_ns;  // limit of a wait on another rank's flag (0 = none; ptx.cuh)
   int32_t seg_adapter[MUX_MAX_SEGMENTS];
   int32_t seg_rank[MUX_MAX_SEGMENTS];
   float seg_scale[MUX_MAX_SEGMENTS];
@@ -145,6 +146,7 @@ struct RsReduceParams {
   unsigned long long* ack[MUX_RS_MAX_WORLD];  // rank s's ack slot for this rank (peer)
   uint4* out;                             // [rows, cols], row stride ldo8 * 8 elements
   long long ldo8;
+  unsigned long long peer_wait_ns;        // limit of the wait for the sources' ready flags (0 = none)
 };
 
 }  // namespace mux

@@ -295,7 +295,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
               if (ld_acquire_sys_u64(f) < p.ag_seq) {
                 const uint64_t t0 = globaltimer_ns();
                 while (ld_acquire_sys_u64(f) < p.ag_seq)
-                  if (globaltimer_ns() - t0 > kWatchdogNs) __trap();
+                  if (peer_wait_expired(t0, p.peer_wait_ns)) __trap();
               }
               fence_async_global();  // the rows the copy engine wrote -> this CTA's TMA reads
             }
@@ -529,7 +529,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           if (ld_acquire_sys_u64(f) + 1ull < p.rs_seq) {
             const uint64_t t0 = globaltimer_ns();
             while (ld_acquire_sys_u64(f) + 1ull < p.rs_seq)
-              if (globaltimer_ns() - t0 > kWatchdogNs) __trap();
+              if (peer_wait_expired(t0, p.peer_wait_ns)) __trap();
           }
         }
       }

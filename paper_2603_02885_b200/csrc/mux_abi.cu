@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -200,6 +201,18 @@ unsigned long long* dbg_counters() {
   return d;
 }
 #endif
+
+// limit of a device-side wait on another rank (fused AG/RS flags): MUX_PEER_TIMEOUT_S seconds,
+// default 600, 0 = wait forever (rank skew is normal; only a protocol bug never completes)
+unsigned long long peer_wait_ns() {
+  static const unsigned long long ns = [] {
+    const char* e = std::getenv("MUX_PEER_TIMEOUT_S");
+    double s = 600.0;
+    if (e && *e) s = std::atof(e);
+    return s <= 0.0 ? 0ull : static_cast<unsigned long long>(s * 1e9);
+  }();
+  return ns;
+}
 
 int num_sms() {
   int dev = 0;
@@ -438,6 +451,7 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
     p.ag_seq = ag->seq;
     p.ag_flags = ag->flags[ag->rank];
   }
+  p.peer_wait_ns = peer_wait_ns();
   if (rs) {
     if (rs->world < 1 || rs->world > MUX_RS_MAX_WORLD || rs->rank < 0 || rs->rank >= rs->world)
       return fail(MUX_ERR_INVALID_ARGUMENT, "rs: world=%d rank=%d", rs->world, rs->rank);
@@ -866,6 +880,7 @@ mux_status mux_rs_reduce(const mux_rs* rs, int32_t cols, mux_bf16* out, int64_t 
   for (int s2 = 0; s2 < rs->world; ++s2) q.ack[s2] = rs->flags[s2] + rs->world + rs->rank;
   q.out = reinterpret_cast<uint4*>(out);
   q.ldo8 = ldo / 8;
+  q.peer_wait_ns = peer_wait_ns();
   cudaError_t e = launch_rs_reduce(q, num_sms(), stream);
   if (e != cudaSuccess) return cuda_fail(e, "mux_rs_reduce launch");
   return MUX_OK;

@@ -48,6 +48,12 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
 // Watchdog for every spin in the library: a wait that never completes (a
 // protocol bug) traps after kWatchdogNs instead of hanging the GPU.
 constexpr uint64_t kWatchdogNs = 8000000000ull;
+// Waits on ANOTHER RANK (fused all-gather / reduce-scatter flags) use the caller's limit instead:
+// normal rank skew (a checkpoint save or an eval on one rank) must not kill the context.  The
+// host sets it from MUX_PEER_TIMEOUT_S (default 600 s; 0 = wait forever, as NCCL does).
+__device__ __forceinline__ bool peer_wait_expired(uint64_t t0, unsigned long long limit_ns) {
+  return limit_ns != 0ull && globaltimer_ns() - t0 > limit_ns;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   if (mbar_try_wait(a, parity)) return;

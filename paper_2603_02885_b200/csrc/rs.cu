@@ -26,7 +26,7 @@ __global__ void __launch_bounds__(256) mux_rs_reduce_kernel(const __grid_constan
       if (ld_acquire_sys_u64(f) < p.seq) {
         const uint64_t t0 = globaltimer_ns();
         while (ld_acquire_sys_u64(f) < p.seq)
-          if (globaltimer_ns() - t0 > kWatchdogNs) __trap();
+          if (peer_wait_expired(t0, p.peer_wait_ns)) __trap();
       }
     }
   }

@@ -157,6 +157,61 @@ def _dev_i32(x, device) -> torch.Tensor:
     return torch.as_tensor(list(x), dtype=torch.int32, device=device)
 
 
+# ---------------------------------------------------------------- host-side argument checks
+def _need(cond: bool, msg: str):
+    if not cond:
+        raise ValueError(msg)
+
+
+def _check_mat(name: str, t: Optional[torch.Tensor], shape, dtype=torch.bfloat16, device=None, dense=True):
+    """t must be a `dtype` tensor of `shape` on `device` whose rows are contiguous (and, with
+    dense=True, packed back to back: the ABI takes no leading dimension for it)."""
+    if t is None:
+        return
+    _need(isinstance(t, torch.Tensor), f"{name} must be a torch.Tensor")
+    _need(t.dtype == dtype, f"{name}: dtype {t.dtype}, expected {dtype}")
+    _need(tuple(t.shape) == tuple(shape), f"{name}: shape {tuple(t.shape)}, expected {tuple(shape)}")
+    _need(t.is_cuda, f"{name} must be a CUDA tensor")
+    if device is not None:
+        _need(t.device == device, f"{name} is on {t.device}, expected {device}")
+    if t.dim() == 2 and t.numel() > 0:
+        _need(t.stride(1) == 1, f"{name}: rows must be contiguous")
+        if dense:
+            _need(t.stride(0) == t.shape[1], f"{name}: must be contiguous (row stride {t.stride(0)})")
+
+
+def _check_linear(seg_off, seg_task, adapters, X, W, r_cap, K=None, N=None, *, Y=None, Hs=None, dY=None,
+                  dX=None, rows=None, grads=False):
+    """Everything the C side cannot check through raw pointers: dtypes, shapes, contiguity, device.
+    A mismatch raises ValueError before any launch (the C side then validates sizes/alignment)."""
+    if X is not None:
+        _need(X.dim() == 2, "X must be 2-D [rows, K]")
+        rows, K = X.shape if rows is None else (rows, X.shape[1])
+    _need(K is not None and rows is not None, "K and rows are required")
+    _need(W is not None or N is not None, "W [N, K] (or N) is required")
+    if W is not None:
+        _need(W.dim() == 2, "W must be 2-D [N, K]")
+        N = W.shape[0] if N is None else N
+    dev = W.device if W is not None else X.device
+    _check_mat("X", X, (rows, K), device=dev)
+    _check_mat("W", W, (N, K), device=dev)
+    _check_mat("Y", Y, (rows, N), device=dev)
+    _check_mat("Hs", Hs, (rows, r_cap), device=dev)
+    _check_mat("dY", dY, (rows, N), device=dev)
+    _check_mat("dX", dX, (rows, K), device=dev)
+    _need(isinstance(seg_off, torch.Tensor) and seg_off.dtype == torch.int32 and seg_off.is_cuda
+          and seg_off.is_contiguous() and seg_off.numel() == len(seg_task) + 1,
+          f"seg_off must be a contiguous int32 CUDA tensor of len(seg_task)+1 = {len(seg_task) + 1} entries")
+    for i, a in enumerate(adapters):
+        if a.rank == 0:
+            continue
+        _check_mat(f"adapters[{i}].A", a.A, (a.rank, K), device=dev)
+        _check_mat(f"adapters[{i}].B", a.B, (N, a.rank), device=dev, dense=False)
+        if grads:
+            _check_mat(f"adapters[{i}].dA", a.dA, (a.rank, K), torch.float32, dev)
+            _check_mat(f"adapters[{i}].dB", a.dB, (N, a.rank), torch.float32, dev)
+
+
 # ---------------------------------------------------------------- packing
 def pack_bound_rows(total_tokens: int, num_seqs: int, chunk_size_or_max: int) -> int:
     return int(lib().mux_pack_bound_rows(total_tokens, num_seqs, chunk_size_or_max))
@@ -274,6 +329,7 @@ def linear_fwd(seg_off: torch.Tensor, seg_task: Sequence[int], adapters: Sequenc
         Y = torch.empty(max_rows, N, dtype=torch.bfloat16, device=dev)
     if Hs is None and want_hs:
         Hs = torch.empty(max_rows, r_cap, dtype=torch.bfloat16, device=dev)
+    _check_linear(seg_off, seg_task, adapters, X, W, r_cap, Y=Y, Hs=Hs)
     S = len(seg_task)
     if workspace is None:
         workspace = torch.zeros(linear_workspace_size(S, max_rows, K, N, r_cap), dtype=torch.uint8, device=dev)
@@ -293,6 +349,8 @@ def linear_fwd_hs(seg_off: torch.Tensor, seg_task: Sequence[int], adapters: Sequ
     N = W.shape[0]
     if Y is None:
         Y = torch.empty(max_rows, N, dtype=torch.bfloat16, device=X.device)
+    _need(Hs is not None, "linear_fwd_hs needs Hs")
+    _check_linear(seg_off, seg_task, adapters, X, W, r_cap, Y=Y, Hs=Hs)
     S = len(seg_task)
     if workspace is None:
         workspace = torch.zeros(linear_workspace_size(S, max_rows, K, N, r_cap), dtype=torch.uint8, device=X.device)
@@ -311,6 +369,7 @@ def linear_shrink(seg_off: torch.Tensor, seg_task: Sequence[int], adapters: Sequ
         row_end = max_rows
     if Hs is None:
         Hs = torch.empty(max_rows, r_cap, dtype=torch.bfloat16, device=X.device)
+    _check_linear(seg_off, seg_task, adapters, X, None, r_cap, N=N, Hs=Hs)
     S = len(seg_task)
     if workspace is None:
         workspace = torch.zeros(linear_workspace_size(S, max_rows, K, N, r_cap), dtype=torch.uint8, device=X.device)
@@ -338,6 +397,7 @@ def linear_bwd(seg_off: torch.Tensor, seg_task: Sequence[int], adapters: Sequenc
                 a.dA = torch.empty(a.rank, K, dtype=torch.float32, device=dev)
             if a.dB is None:
                 a.dB = torch.empty(N, a.rank, dtype=torch.float32, device=dev)
+    _check_linear(seg_off, seg_task, adapters, X, W, r_cap, Hs=Hs, dY=dY, dX=dX, grads=True)
     S = len(seg_task)
     if workspace is None:
         workspace = torch.zeros(linear_workspace_size(S, max_rows, K, N, r_cap), dtype=torch.uint8, device=dev)
@@ -497,6 +557,8 @@ def linear_fwd_rs(rs: _Rs, seg_off, seg_task, adapters, X, W, r_cap: int, Hs=Non
     N = W.shape[0]
     if Hs is None:
         Hs = torch.empty(max_rows, r_cap, dtype=torch.bfloat16, device=X.device)
+    _check_linear(seg_off, seg_task, adapters, X, W, r_cap, Hs=Hs)
+    _need(max_rows == rs.world * rs.rows_per_rank, "X rows must equal world * rows_per_rank")
     S = len(seg_task)
     if workspace is None:
         workspace = torch.zeros(linear_workspace_size(S, max_rows, K, N, r_cap), dtype=torch.uint8, device=X.device)
@@ -511,6 +573,8 @@ def linear_bwd_dx_rs(rs: _Rs, seg_off, seg_task, adapters, dY, X, W, Hs, r_cap: 
     (follow with linear_bwd(..., part=BWD_GRADS) on the same workspace for dA/dB)."""
     max_rows, K = X.shape
     N = W.shape[0]
+    _check_linear(seg_off, seg_task, adapters, X, W, r_cap, Hs=Hs, dY=dY)
+    _need(max_rows == rs.world * rs.rows_per_rank, "X rows must equal world * rows_per_rank")
     _check(lib().mux_linear_bwd_dx_rs(len(seg_task), _ptr(seg_off), _i32_host(seg_task), len(adapters),
                                       _adapter_table(adapters, True), max_rows, K, N, r_cap, _ptr(dY), _ptr(X),
                                       _ptr(W), _ptr(Hs), ctypes.byref(rs), _ptr(workspace), workspace.numel(),
@@ -548,6 +612,7 @@ def linear_fwd_ag(ag: _Rs, seg_off, seg_task, adapters, K: int, W, r_cap: int, Y
         Y = torch.empty(max_rows, N, dtype=torch.bfloat16, device=dev)
     if Hs is None:
         Hs = torch.empty(max_rows, r_cap, dtype=torch.bfloat16, device=dev)
+    _check_linear(seg_off, seg_task, adapters, None, W, r_cap, K=K, rows=max_rows, Y=Y, Hs=Hs)
     S = len(seg_task)
     if workspace is None:
         workspace = torch.zeros(linear_workspace_size(S, max_rows, K, N, r_cap), dtype=torch.uint8, device=dev)
@@ -571,6 +636,8 @@ def linear_bwd_ag(ag: _Rs, seg_off, seg_task, adapters, X, W, Hs, r_cap: int, dX
                 a.dA = torch.empty(a.rank, K, dtype=torch.float32, device=dev)
             if a.dB is None:
                 a.dB = torch.empty(N, a.rank, dtype=torch.float32, device=dev)
+    _check_linear(seg_off, seg_task, adapters, X, W, r_cap, Hs=Hs, dX=dX, grads=True)
+    _need(max_rows == ag.world * ag.rows_per_rank, "X rows must equal world * rows_per_rank")
     S = len(seg_task)
     if workspace is None:
         workspace = torch.zeros(linear_workspace_size(S, max_rows, K, N, r_cap), dtype=torch.uint8, device=dev)

@@ -176,19 +176,32 @@ class MuxBackend:
         return cur
 
     def _push(self, ag, rows_t):
+        """Push this rank's rows to every rank on the copy stream.  Returns the event that marks
+        the end of all pushes: the source must not be rewritten (or freed) before it, so the
+        caller makes its compute stream wait on it when it releases the gather (by then every
+        push has long finished, so the wait costs nothing and keeps the overlap)."""
         if getattr(self, "copy_stream", None) is None:
             self.copy_stream = torch.cuda.Stream()
         ev = torch.cuda.Event()
         ev.record()
         self.copy_stream.wait_event(ev)           # this rank's rows are ready
         self.mux.ag_push(ag, rows_t, stream=self.copy_stream)
+        rows_t.record_stream(self.copy_stream)    # the allocator keeps the block until the pushes end
+        done = torch.cuda.Event()
+        done.record(self.copy_stream)
+        return done
 
     def fwd_ag(self, lay, seg_off, seg_task, x_rows):
         p, _ = _world(lay.group)
         rows, K = x_rows.shape
+        if lay._ag_held is not None:
+            # the previous forward's gather is still held for its backward: pushing again would
+            # wait forever for this rank's own release (and the GEMM would trap on the flags)
+            raise RuntimeError("fused_ag: forward called again before the backward of the previous call; "
+                               "call release_ag() first for forward-only use")
         fb = self._ag_for(lay, "_ag", rows, K, x_rows.device)
         ag = fb.next()
-        self._push(ag, x_rows)
+        lay._ag_pushed = self._push(ag, x_rows)
         R, N = rows * p, lay.W.shape[0]
         Y = self._buf(("Y", lay.W.data_ptr()), (R, N), torch.bfloat16, x_rows.device)
         Hs = self._buf(("Hs", lay.W.data_ptr()), (R, lay.r_cap), torch.bfloat16, x_rows.device)
@@ -202,11 +215,12 @@ class MuxBackend:
         rows, N = dy_rows.shape
         fb = self._ag_for(lay, "_ag", rows, N, dy_rows.device)
         ag = fb.next()
-        self._push(ag, dy_rows)
+        pushed = self._push(ag, dy_rows)
         X = lay.X
         dX = self._buf(("dX", lay.W.data_ptr()), tuple(X.shape), torch.bfloat16, X.device)
         self.mux.linear_bwd_ag(ag, seg_off, seg_task, lay.ads, X, lay.W, lay.Hs, lay.r_cap, dX=dX,
                                workspace=self._ws(lay.W, X, seg_task, lay.r_cap))
+        torch.cuda.current_stream().wait_event(pushed)   # dy_rows may be rewritten after this point
         self.mux.ag_release(ag)                   # dY fully consumed (dX GEMM + gradients)
         return dX, [a.dA for a in lay.ads], [a.dB for a in lay.ads]
 
@@ -276,7 +290,7 @@ class ColumnParallelMuxLinear:
                  shared_shrink=False):
         self.be, self.W, self.ads, self.r_cap, self.group = backend, W_shard, adapters_shard, r_cap, group
         self.fused_rs, self.fused_ag, self.shared_shrink = fused_rs, fused_ag, shared_shrink
-        self._rs = self._ag = self._ag_held = None
+        self._rs = self._ag = self._ag_held = self._ag_pushed = None
 
     def forward(self, seg_off, seg_task, x_rows):
         """x_rows [R/p, K] (this rank's row block) -> Y_p [R, N/p]."""
@@ -309,6 +323,9 @@ class ColumnParallelMuxLinear:
     def release_ag(self):
         """The gathered X is no longer needed (after the backward): its owners may push again."""
         if self._ag_held is not None:
+            if self._ag_pushed is not None:   # the pushed source rows may be rewritten after this point
+                torch.cuda.current_stream().wait_event(self._ag_pushed)
+                self._ag_pushed = None
             self.be.mux.ag_release(self._ag_held)
             self._ag_held = None
 

@@ -4,8 +4,14 @@ config 4 structure at a small width): pack -> Dispatch -> block forward
 sequences, o linear + residual, RMSNorm, gate/up LoRA linears, SwiGLU, down
 linear + residual) -> block backward, all through libmux, against the fp64
 oracles composed in the same order (oracle/block.py + oracle/linear.c; the
-oracle keeps fp64 intermediates).  Output, input gradient and every adapter
-gradient of every linear within the north_star tolerance."""
+oracle keeps fp64 intermediates).  Two bars:
+  * stage-wise (every op fed the GPU's own bf16 inputs of that stage): every
+    output within the north_star tolerance TOL = 2e-2;
+  * end to end (the all-fp64 composition, whose intermediates never see a
+    bf16 rounding): E2E_TOL = 5e-2 — NOT the north_star bar, a bound derived
+    for the composition: about forty bf16 roundings in sequence, with
+    attention multiplying q/k rounding errors by the logits' magnitude
+    (DESIGN.md §11c)."""
 import numpy as np
 import pytest
 

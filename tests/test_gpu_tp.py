@@ -184,3 +184,40 @@ def test_tp_fused_rs_world1_equals_direct(pg):
     ref = [Y, dX] + [a.dA for a in a1] + [a.dB for a in a1] + [a.dA for a in a2] + [a.dB for a in a2]
     for a_, b_ in zip(got, ref):
         assert torch.equal(_bits(a_), _bits(b_))
+
+
+def test_tp_fused_ag_world1_double_forward(pg):
+    """fused_ag holds the gather buffer from the forward until the backward re-read X.  A second
+    forward before that backward must raise (pushing again would wait forever for this rank's own
+    release and trap the context); release_ag() makes a forward-only re-call legal; the chain
+    with the all-gather fused equals direct binding calls, bit for bit."""
+    g = torch.Generator(device="cuda").manual_seed(31)
+    R, K, N = 512, 256, 384
+    seg_off = torch.tensor([0, 192, 320, 512], dtype=torch.int32, device="cuda")
+    st = [0, 1, 2]
+    ranks = [16, 8, 32]
+    W = (torch.randn(N, K, device="cuda", generator=g) / K ** 0.5).bfloat16()
+    ads = []
+    for r in ranks:
+        B = mux.make_B_storage(N, r)
+        B.copy_(torch.randn(N, r, device="cuda", generator=g).bfloat16())
+        ads.append(mux.Adapter((torch.randn(r, K, device="cuda", generator=g) / K ** 0.5).bfloat16(), B, r, 2.0))
+    X = torch.randn(R, K, device="cuda", generator=g).bfloat16()
+    dY = torch.randn(R, N, device="cuda", generator=g).bfloat16()
+    mk = lambda A, B, r, s: mux.Adapter(A, B, r, s)  # noqa: E731
+    Wp, ap = tp.shard_column(W, ads, 1, 0, mk)
+    up = tp.ColumnParallelMuxLinear(tp.MuxBackend(), Wp, ap, 32, fused_ag=True)
+    up.forward(seg_off, st, X)
+    with pytest.raises(RuntimeError, match="before the backward"):
+        up.forward(seg_off, st, X)
+    up.release_ag()                      # forward-only use: give the gather back, then call again
+    y = up.forward(seg_off, st, X).clone()
+    dx, dA, dB = up.backward(seg_off, st, dY)
+    torch.cuda.synchronize()
+    got = [y, dx.clone()] + [t.clone() for t in dA + dB]
+    Y, Hs = mux.linear_fwd(seg_off, st, ads, X, W, 32)
+    dX = mux.linear_bwd(seg_off, st, ads, dY, X, W, Hs, 32)
+    torch.cuda.synchronize()
+    ref = [Y, dX] + [a.dA for a in ads] + [a.dB for a in ads]
+    for a_, b_ in zip(got, ref):
+        assert torch.equal(_bits(a_), _bits(b_))

@@ -171,3 +171,62 @@ def test_attention_bwd_finite_differences():
     np.testing.assert_allclose(dv, _fd(lambda t: f(q, k, t), v, do), rtol=1e-6, atol=1e-8)
     pads = rs < 0
     assert (dq[pads] == 0).all() and (dk[pads] == 0).all() and (dv[pads] == 0).all()
+
+
+# ------------------------------------------------------------------ hand-computed values
+# These pin the constants the identities above cannot see (they hold for any
+# frequency schedule, pairing, logit scale or eps).  Expected numbers are
+# written out by hand from the stated definitions, not produced by the oracle.
+COS = {3.0: -0.9899924966004454, 0.3: 0.955336489125606, 0.03: 0.9995500337489875, 0.003: 0.9999955000033750}
+SIN = {3.0: 0.1411200080598672, 0.3: 0.29552020666133955, 0.03: 0.029995500202495664, 0.003: 0.0029999955000020251}
+
+
+def test_rope_d8_position3_hand_values():
+    """d = 8, base 1e4: inv_freq_i = base^(-2i/d) = 1, 1e-1, 1e-2, 1e-3 (i = 0..3); rotate-half pairing
+    (i, i + d/2).  Row 3 of a sequence that starts at row 0 has position 3: angles 3, 0.3, 0.03, 0.003.
+    x = [1,1,1,1, 0,0,0,0] -> [cos a_i | sin a_i];  x = [0,0,0,0, 1,1,1,1] -> [-sin a_i | cos a_i].
+    An interleaved pairing ((2i, 2i+1)) or an exponent of -i/d instead of -2i/d fails this."""
+    angles = (3.0, 0.3, 0.03, 0.003)
+    x = np.zeros((4, 2, 8))
+    x[3, 0, :4] = 1.0
+    x[3, 1, 4:] = 1.0
+    y = ob.rope_fwd(x, np.zeros(4, dtype=int), base=10000.0)
+    np.testing.assert_allclose(y[3, 0], [COS[a] for a in angles] + [SIN[a] for a in angles], rtol=0, atol=1e-15)
+    np.testing.assert_allclose(y[3, 1], [-SIN[a] for a in angles] + [COS[a] for a in angles], rtol=0, atol=1e-15)
+    # position 0 (row 0) is the identity
+    np.testing.assert_array_equal(ob.rope_fwd(x[[3, 3]], np.array([1, 1]))[1], x[3])
+
+
+def test_attention_two_keys_hand_value():
+    """Nonzero logits pin the scale: d = 2, scale 0.5, query row 1 q = [2, 0], keys k0 = [0, 0],
+    k1 = [ln 3, 0] -> logits 0 and 0.5 * 2 * ln 3 = ln 3 -> softmax [1/4, 3/4]; v0 = [4, 0],
+    v1 = [0, 8] -> o1 = [1, 6], lse1 = ln(1 + 3) = ln 4.  Row 0 sees only itself: o0 = v0,
+    lse0 = 0.5 <q0, k0> = 0 for q0 = [0, 0]."""
+    ln3 = 1.0986122886681098
+    q = np.array([[[0.0, 0.0]], [[2.0, 0.0]]])
+    k = np.array([[[0.0, 0.0]], [[ln3, 0.0]]])
+    v = np.array([[[4.0, 0.0]], [[0.0, 8.0]]])
+    o, lse = ob.attention_fwd(q, k, v, np.array([0, 0]), 0.5)
+    np.testing.assert_allclose(o[1, 0], [1.0, 6.0], rtol=1e-15)
+    assert lse[1, 0] == pytest.approx(1.3862943611198906, rel=1e-15)   # ln 4
+    np.testing.assert_allclose(o[0, 0], [4.0, 0.0])
+    assert lse[0, 0] == 0.0
+    # backward of <dO, o> with dO = [1, 0] at row 1 only: dV = P^T dO -> dv0 = 1/4 [1,0], dv1 = 3/4 [1,0]
+    do = np.zeros_like(q)
+    do[1, 0] = [1.0, 0.0]
+    dq, dk, dv = ob.attention_bwd(do, q, k, v, np.array([0, 0]), 0.5)
+    np.testing.assert_allclose(dv[:, 0], [[0.25, 0.0], [0.75, 0.0]], rtol=1e-15)
+    # dP = dO V^T = [4, 0]; dS = P (dP - <P, dP>) = [1/4 (4 - 1), 3/4 (0 - 1)] = [3/4, -3/4]
+    # dq1 = scale * dS K = 0.5 * (-3/4) * [ln 3, 0];  dk0 = 0.5 * 3/4 * q1, dk1 = 0.5 * (-3/4) * q1
+    np.testing.assert_allclose(dq[1, 0], [-0.375 * ln3, 0.0], rtol=1e-14)
+    np.testing.assert_allclose(dk[:, 0], [[0.75, 0.0], [-0.75, 0.0]], rtol=1e-14)
+
+
+def test_rmsnorm_eps_hand_values():
+    """eps inside the root, added to the mean square: x = [3, 4] (mean square 12.5), eps = 3.5 ->
+    rms = sqrt(16) = 4, y = x / 4 * w = [1.5, -1] for w = [2, -1].  Backward of y_0 (dy = [1, 0]):
+    d/dx_0 (2 x_0 / s) = 2/s - x_0^2 / s^3 = 1/2 - 9/64,  d/dx_1 = -x_0 x_1 / s^3 = -12/64  (s = 4)."""
+    x = np.array([[3.0, 4.0]])
+    w = np.array([2.0, -1.0])
+    np.testing.assert_allclose(ob.rmsnorm_fwd(x, w, 3.5), [[1.5, -1.0]], rtol=1e-15)
+    np.testing.assert_allclose(ob.rmsnorm_bwd(np.array([[1.0, 0.0]]), x, w, 3.5), [[0.359375, -0.1875]], rtol=1e-15)
