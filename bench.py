@@ -72,7 +72,16 @@ class Workload:
         self.cap = wl.pack_capacity
         self.max_cap = max(self.cap) if self.cap else 512
         self.linears = wl.linears
-        self.flops = sum(flops_per_token(L.K, L.N, max(wl.ranks)) for L in wl.linears) * self.T
+        # algorithmic FLOPs at each task's own rank: sum_t T_t * sum_L (4KN + 6 r_t (K+N))
+        self.task_tokens = [int(x.sum()) for x in wl.task_lens]
+        self.flops = sum(Tt * flops_per_token(L.K, L.N, r) for Tt, r in zip(self.task_tokens, wl.ranks)
+                         for L in wl.linears)
+
+    def fwd_flops(self, L, K=None, N=None):
+        """forward GEMM FLOPs of one call on linear L (or a K x N shard of it): sum_t T_t (2KN + 2 r_t (K+N))."""
+        K = L.K if K is None else K
+        N = L.N if N is None else N
+        return sum(Tt * (2 * K * N + 2 * r * (K + N)) for Tt, r in zip(self.task_tokens, self.wl.ranks))
 
     def host_tensors(self):
         wl = self.wl
@@ -308,7 +317,19 @@ def oracle_sample(w: Workload, rows_per_task: int, seed_off=0):
     return run, R
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_baseline(w: Workload, target_s=12.0):
+    """The oracle as it stands on the host cores (OpenMP over all of them), plus the same sample on
+    one thread (core count, 1-thread figure and CPU model on record)."""
     from oracle import linear as olin
     olin.build()
     run, R = oracle_sample(w, 2)
@@ -320,10 +341,23 @@ def cpu_baseline(w: Workload, target_s=12.0):
     t0 = time.perf_counter()
     run()
     dt = time.perf_counter() - t0
-    return {"value": R / dt, "unit": UNIT, "cores": olin.num_threads(), "kind": "oracle",
+    cores = olin.num_threads()
+    # one thread, a quarter of the rows (the per-token cost does not depend on the row count)
+    rows1 = max(1, rows_per_task // 4)
+    run1, R1 = oracle_sample(w, rows1)
+    olin.set_num_threads(1)
+    try:
+        t0 = time.perf_counter()
+        run1()
+        dt1 = time.perf_counter() - t0
+    finally:
+        olin.set_num_threads(cores)
+    return {"value": R / dt, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
             "sample": f"{R} tokens ({w.M} tasks x {rows_per_task} rows, ranks {w.wl.ranks}) through the "
                       f"3 config-2 linear shapes, full fp64 fwd+bwd (Y, Hs, dX, dA, dB); {dt:.1f} s",
-            "seconds": dt}
+            "seconds": dt,
+            "one_thread": {"value": R1 / dt1, "unit": UNIT, "cores": 1, "seconds": dt1,
+                           "sample": f"{R1} tokens ({w.M} tasks x {rows1} rows), same shapes"}}
 
 
 def reference_arm(args):
@@ -431,29 +465,17 @@ def main_arm(args):
     # roofline of the dominant kernel (fused tcgen05 GEMM, forward calls)
     fwd_ms = sum(a.elapsed_time(b) for (_, a, b) in ev_pairs["fwd"])
     bwd_ms = sum(a.elapsed_time(b) for (_, a, b) in ev_pairs["bwd"])
-    fwd_flops = sum((2 * L.K * L.N + 2 * max(w.wl.ranks) * (L.K + L.N)) * w.T for L in w.linears) * args.steps
+    fwd_flops = sum(w.fwd_flops(L) for L in w.linears) * args.steps
     # the events bracket each layer's backward call on the main stream: with the adapter gradients
     # overlapped on the side stream that is the dX GEMM (2KN + 2r(K+N) per token), else dX + gradients
-    r_ = max(w.wl.ranks)
-    bwd_flops = sum((2 * L.K * L.N + (2 if ms.overlap_grads else 4) * r_ * (L.K + L.N)) * w.T
-                    for L in w.linears) * args.steps
+    bwd_flops = sum(Tt * (2 * L.K * L.N + (2 if ms.overlap_grads else 4) * r * (L.K + L.N))
+                    for L in w.linears for Tt, r in zip(w.task_tokens, w.wl.ranks)) * args.steps
     pk = peaks()
     achieved = fwd_flops / (fwd_ms * 1e-3) / 1e12
-    traffic, traffic_src = None, None
-    tp = os.path.join(ROOT, "profiles", "gemm_fwd_traffic.json")
-    if os.path.exists(tp):
-        tj = json.load(open(tp))
-        traffic, traffic_src = tj.get("mean_bytes_per_launch"), tj.get("source")
-    # the GEMM launches are timed inside a long back-to-back step (the whole
-    # timed region runs under the power cap), so the denominator is the
-    # measured *sustained* bf16 peak; the burst fraction is reported beside it
-    roof = {"bound": "tensor", "achieved": achieved, "peak": pk["bf16_tflops_sustained"], "unit": "TFLOP/s",
-            "frac": achieved / pk["bf16_tflops_sustained"], "frac_of_burst": achieved / pk["bf16_tflops"],
-            "traffic": traffic, "traffic_source": traffic_src,
-            "algorithmic_bytes_per_launch": sum(2 * (w.T * (L.K + L.N) + L.K * L.N) for L in w.linears)
-            / len(w.linears),
-            "kernel": "mux_gemm_kernel<fwd> (fused backbone + LoRA; events around each mux_linear_fwd call)",
-            "peak_source": pk["source"] + " sustained bf16 (cuBLAS 8192^3 back to back for 4 s)"}
+    roof = _roofline(achieved, pk, ms_total, clk, len(w.linears),
+                     "mux_gemm_kernel<fwd> (fused backbone + LoRA; events around each mux_linear_fwd call)")
+    roof["algorithmic_bytes_per_launch"] = sum(2 * (w.T * (L.K + L.N) + L.K * L.N) for L in w.linears) / len(w.linears)
+    roof["traffic"], roof["traffic_source"] = traffic_of_this_build()
 
     # ---------------- e2e: same step through the public API with host buffers.
     # Every step copies its inputs host->device (pinned) and its result (all
@@ -559,26 +581,14 @@ def main_arm(args):
 
 
 # ------------------------------------------------------------------ tensor-parallel arm
-def tp_arm(args):
-    """--mode tp: the config-2 tasks tensor-parallel over the N ranks (strong
-    scaling).  Megatron pairing over the 3-layer stack: L0 column-parallel
-    (AG of the row-sharded input), L1 row-parallel (RS of the output), L2
-    column-parallel; backward mirrors it (RS / AG / AR of dA or dB, see
-    paper_2603_02885_b200/tp.py).  `--htasks g` splits the tasks into g
-    hTasks (contiguous task groups, each packed and multiplexed on its own)
-    whose subgraphs are interleaved by Alg. 1 so one hTask's collectives
-    overlap another's GEMMs (orchestrate.py, NEXT-1; `--comm-ctas c` caps
-    NCCL's CTAs).  Every rank's compute is the fused kernels."""
-    if args.comm_ctas:
-        os.environ["NCCL_MAX_CTAS"] = str(args.comm_ctas)
-    import torch
+def dist_setup(torch):
+    """One process per GPU (torchrun env).  NCCL over NVLink on the driver's runs;
+    MUX_BENCH_DIST_BACKEND=gloo is test-only (ranks may then share the visible GPUs)."""
     import torch.distributed as dist
-    from paper_2603_02885_b200 import mux, orchestrate, tp
-
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    backend = os.environ.get("MUX_BENCH_DIST_BACKEND", "nccl")  # gloo: test-only, ranks may share a GPU
+    backend = os.environ.get("MUX_BENCH_DIST_BACKEND", "nccl")
     if backend != "nccl":
         local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
@@ -589,16 +599,59 @@ def tp_arm(args):
             dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend, rank=rank, world_size=world)
-    w = Workload(args.config)
-    h = w.host_tensors()
-    i32 = dict(dtype=torch.int32, device="cuda")
+    return dist, world, rank, local, backend
+
+
+def timed_backend_cls(tp, torch):
+    class TimedMuxBackend(tp.MuxBackend):
+        """tp.MuxBackend whose forward GEMM calls (the roofline's dominant kernel) are bracketed by
+        CUDA events on the launching stream while `record` is a list; FLOPs per call are
+        sum_t T_t (2 K N + 2 r_t (K + N)) over the call's tasks (`task_tokens`, host-known)."""
+        record = None
+        task_tokens = None
+
+        def _flops(self, ads, K, N):
+            return sum(Tt * (2 * K * N + 2 * a.rank * (K + N)) for Tt, a in zip(self.task_tokens, ads))
+
+        def _timed(self, fn, flops, *a):
+            if self.record is None:
+                return fn(*a)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            out = fn(*a)
+            e1.record()
+            self.record.append((e0, e1, flops))
+            return out
+
+        def fwd(self, seg_off, seg_task, ads, X, W, r_cap):
+            return self._timed(super().fwd, self._flops(ads, X.shape[1], W.shape[0]), seg_off, seg_task, ads, X, W,
+                               r_cap)
+
+        def fwd_rs(self, lay, seg_off, seg_task, X):
+            return self._timed(super().fwd_rs, self._flops(lay.ads, X.shape[1], lay.W.shape[0]), lay, seg_off,
+                               seg_task, X)
+
+        def fwd_ag(self, lay, seg_off, seg_task, x_rows):
+            return self._timed(super().fwd_ag, self._flops(lay.ads, x_rows.shape[1], lay.W.shape[0]), lay, seg_off,
+                               seg_task, x_rows)
+    return TimedMuxBackend
+
+
+def _gen(torch, seed, shape, std):
+    g = torch.Generator(device="cuda").manual_seed(int(seed) & 0x7FFFFFFFFFFFFFFF)
+    return (torch.randn(*shape, device="cuda", generator=g) * std).bfloat16()
+
+
+def _tp_chain(args, w, torch, mux, tp, orchestrate, Backend, world, rank):
+    """Config-2-style layer stack (3 linears) tensor-parallel: L0 column (AG of the row-sharded
+    input), L1 row (RS of its output), L2 column; backward mirrors it.  `--htasks g` splits the tasks
+    into g hTasks interleaved by Alg. 1 (orchestrate.py, NEXT-1)."""
     plan_note = None
     if args.htasks == 0:
-        # NEXT-4 feeding NEXT-1: the planner's Eq. 6 fusion over the measured operator profile
         from paper_2603_02885_b200 import planner
         prof = planner.load_profile(os.path.join(ROOT, "profiles", "r01_op_profile.json"))
         L = planner.htask_latency([planner.stage_from_profile(prof, n_gpus=world)], C=1)
-        tasks_ = [planner.Task(str(t), int(w.wl.task_lens[t].sum()), w.wl.ranks[t]) for t in range(w.M)]
+        tasks_ = [planner.Task(str(t), w.task_tokens[t], w.wl.ranks[t]) for t in range(w.M)]
         plan = planner.fuse_tasks(tasks_, L, S=1)
         groups = [[int(t.name) for t in h] for h in plan.htasks]
         plan_note = {"planner_cost_ms": plan.cost, "groups": groups}
@@ -606,99 +659,380 @@ def tp_arm(args):
         g = max(1, min(args.htasks, w.M))
         groups = [list(range(w.M))[i * w.M // g:(i + 1) * w.M // g] for i in range(g)]
     r_cap = 16 * -(-max(w.wl.ranks) // 16)
-    kinds = ["col", "row", "col"]
+    kinds = ["col", "row", "col"][:len(w.linears)]
     mk = lambda A, B, r, sc: mux.Adapter(A, B, r, sc)  # noqa: E731
+    seed = w.wl.seed
     Wsh = []
     for li, L in enumerate(w.linears):
-        W = _bits_to_dev(h[f"W{li}"], torch)
-        if kinds[li] == "col":
-            Wsh.append(tp.shard_column(W, [], world, rank, mk)[0])
-        else:
-            Wsh.append(tp.shard_row(W, [], world, rank, mk)[0])
+        W = _gen(torch, seed * 97 + li, (L.N, L.K), L.K ** -0.5)
+        Wsh.append((tp.shard_column if kinds[li] == "col" else tp.shard_row)(W, [], world, rank, mk)[0])
         del W
-    X1tok_all = _bits_to_dev(h["X1"], torch)
-    tok_off = np.concatenate([[0], np.cumsum([int(x.sum()) for x in w.wl.task_lens])])
-    htasks = []
+    K0, Nl = w.linears[0].K, w.linears[-1].N
+    i32 = dict(dtype=torch.int32, device="cuda")
+    htasks, launches, grads, h2d = [], 0, [], []
     for hi, tasks in enumerate(groups):
         lens = [w.wl.task_lens[t] for t in tasks]
         off = np.concatenate([[0], np.cumsum([len(x) for x in lens])]).astype(np.int32)
         T_h = int(sum(int(x.sum()) for x in lens))
         S_h = int(off[-1])
         bound = int(mux.pack_bound_rows(T_h, S_h, 64))
-        # row blocks split evenly over ranks (256-row blocks for the fused reduce-scatter)
         blk = 256 if (args.fused_rs or args.fused_ag) else 64
+        # every rank owns an equal contiguous row block (sequence parallel); rows are sized on the
+        # pack bound (the host never reads the device-side row count)
         max_rows = -(-bound // (blk * world)) * blk * world
         pk = mux.alloc_pack_outputs(len(tasks), S_h, max_rows, max_rows // 64)
-        be = tp.MuxBackend()
+        be = Backend()
+        be.task_tokens = [w.task_tokens[t] for t in tasks]
         layers = []
         for li, L in enumerate(w.linears):
             ads = []
             for t in tasks:
-                B = mux.make_B_storage(L.N, w.wl.ranks[t])
-                B.copy_(_bits_to_dev(h[f"B{li}_{t}"], torch))
-                ads.append(mux.Adapter(_bits_to_dev(h[f"A{li}_{t}"], torch), B, w.wl.ranks[t], w.wl.scales[t]))
+                r = w.wl.ranks[t]
+                B = mux.make_B_storage(L.N, r)
+                B.copy_(_gen(torch, seed * 131 + li * 1000 + t, (L.N, r), r ** -0.5))
+                ads.append(mux.Adapter(_gen(torch, seed * 137 + li * 1000 + t, (r, L.K), L.K ** -0.5), B, r,
+                                       w.wl.scales[t]))
             shard = tp.shard_column if kinds[li] == "col" else tp.shard_row
             _, ap_ = shard(torch.empty(L.N, L.K, dtype=torch.bfloat16, device="meta"), ads, world, rank, mk)
             cls = tp.ColumnParallelMuxLinear if kinds[li] == "col" else tp.RowParallelMuxLinear
             layers.append(cls(be, Wsh[li], ap_, r_cap, fused_rs=args.fused_rs, fused_ag=args.fused_ag))
         rows = max_rows // world
-        nl = w.linears[-1].N // world
+        # token-major inputs: every rank holds the full buffer; its data loader moves its 1/p share
+        Xtok = _gen(torch, seed * 7 + hi, (T_h, K0), 1.0)
+        # loss gradient of the last (column-parallel) layer: this rank's output-column shard
+        dYtok = _gen(torch, seed * 11 + hi, (T_h, Nl), 1.0)[:, rank * (Nl // world):(rank + 1) * (Nl // world)]
+        dYtok = dYtok.contiguous()
         ht = {"tasks": tasks, "T": T_h, "max_rows": max_rows, "rows": rows, "pk": pk, "layers": layers,
-              "tso": torch.tensor(off, **i32),
-              "sl": torch.tensor(np.concatenate(lens).astype(np.int32), **i32),
-              "cap": torch.tensor([w.cap[t] for t in tasks], **i32) if w.cap else None,
-              "X1tok": torch.cat([X1tok_all[int(tok_off[t]):int(tok_off[t + 1])] for t in tasks]).contiguous(),
-              "x_rows": torch.empty(rows, w.linears[0].K, dtype=torch.bfloat16, device="cuda"),
-              "dY": torch.randn(max_rows, nl, device="cuda",
-                                generator=torch.Generator(device="cuda").manual_seed(rank + 7 * hi)).bfloat16()}
+              "tso": torch.tensor(off, **i32), "sl": torch.tensor(np.concatenate(lens).astype(np.int32), **i32),
+              "cap": torch.tensor([w.cap[t] for t in tasks], **i32) if w.cap else None, "Xtok": Xtok,
+              "x_rows": torch.empty(rows, K0, dtype=torch.bfloat16, device="cuda"),
+              "dYtok": dYtok, "dY": torch.empty(max_rows, Nl // world, dtype=torch.bfloat16, device="cuda")}
+        lo, hi_ = rank * T_h // world, (rank + 1) * T_h // world
+        h2d += [ht["tso"], ht["sl"], Xtok[lo:hi_], dYtok]
 
         def dispatch(e, ht=ht):
             mux.pack_chunks(ht["tso"], ht["sl"], ht["cap"], 0, 64, max_rows=ht["max_rows"],
                             max_chunks=ht["max_rows"] // 64, out=ht["pk"])
-            mux.pack_apply(ht["pk"]["row_src"][rank * ht["rows"]:(rank + 1) * ht["rows"]], ht["X1tok"],
+            mux.pack_apply(ht["pk"]["row_src"][rank * ht["rows"]:(rank + 1) * ht["rows"]], ht["Xtok"],
                            ht["rows"], out=ht["x_rows"])
+            # the loss gradient in the last layer's layout [R, N/p] (Dispatch of its token-major shard)
+            mux.pack_apply(ht["pk"]["row_src"], ht["dYtok"], ht["max_rows"], out=ht["dY"])
             return ht["x_rows"]
-        lat = [2.0 * max_rows * L.K * L.N / world for L in w.linears]   # modeled GEMM cost per layer pass
+        lat = [2.0 * max_rows * L.K * L.N / world for L in w.linears]
         ht["ops"] = orchestrate.linear_chain_ops(layers, kinds, ht["pk"]["seg_off"], list(range(len(tasks))),
                                                  dispatch, ht["dY"], lat)
         htasks.append(ht)
+        launches += 3 + len(layers) + 2 * len(layers)   # pack + 2 Dispatch + fwd GEMMs + (dX + grads)
+        grads.append(layers)
     dags = [orchestrate.build_subgraphs(i, ht["ops"]) for i, ht in enumerate(htasks)]
     schedule = orchestrate.subgraph_schedule(dags)
 
     def step():
         orchestrate.run_schedule(schedule, [dict() for _ in htasks])
 
+    def result_tensors():
+        out = []
+        for layers in grads:
+            for li, lay in enumerate(layers):
+                col = kinds[li] == "col"
+                for a in lay.ads:
+                    if a.rank == 0:
+                        continue
+                    out.append(a.dB if col else a.dA)
+                    if rank == 0:
+                        out.append(a.dA if col else a.dB)
+        return out
+
+    desc = {"parallelism": f"tp{world} (L0 column, L1 row, L2 column; sequence-parallel AG/RS)",
+            "htasks": [ht["tasks"] for ht in htasks], "schedule": [f"h{sg.htask}.{sg.index}" for sg, _ in schedule],
+            "planner": plan_note, "max_rows": [ht["max_rows"] for ht in htasks],
+            "reduce_scatter": "fused into the GEMM epilogue (peer stores)" if args.fused_rs else "NCCL",
+            "all_gather": "copy-engine push, consumed per row block by the GEMM" if args.fused_ag else "NCCL"}
+    bes = [ht["layers"][0].be for ht in htasks]
+    return step, launches, h2d, result_tensors, desc, bes
+
+
+def _tp_block(args, w, torch, mux, tp, Backend, world, rank):
+    """7-linear configs (4: LLaMA-7B block, 16 tasks; 5: LLaMA-70B shapes, 32 tasks): the whole
+    decoder block tensor-parallel (tp_block.py): head-sharded attention between column q/k/v and
+    row o, SwiGLU between column gate/up and row down, sequence-parallel RMSNorm/residuals."""
+    from paper_2603_02885_b200 import tp_block
+    from paper_2603_02885_b200.block import LINEARS
+    wl = w.wl
+    assert [L.name for L in wl.linears] == list(LINEARS), "TP block needs a 7-linear decoder config"
+    hidden, ffn = wl.linears[0].K, wl.linears[4].N
+    heads, kv_heads = wl.linears[0].N // 128, wl.linears[1].N // 128
+    shape = tp_block.TPBlockShape(hidden=hidden, ffn=ffn, heads=heads, kv_heads=kv_heads, p=world)
+    seed = wl.seed
+    r_cap = 16 * -(-max(wl.ranks) // 16)
+    mk = lambda A, B, r, sc: mux.Adapter(A, B, r, sc)  # noqa: E731
+    Wp, ap = {}, {}
+    for li, L in enumerate(wl.linears):
+        n = L.name
+        W = _gen(torch, seed * 97 + li, (L.N, L.K), (0.5 if n in ("q", "k") else 1.0) * L.K ** -0.5)
+        ads = []
+        for t in range(w.M):
+            r = wl.ranks[t]
+            B = _gen(torch, seed * 131 + li * 1000 + t, (L.N, r), r ** -0.5)
+            A = _gen(torch, seed * 137 + li * 1000 + t, (r, L.K), L.K ** -0.5)
+            ads.append(mux.Adapter(A, B, r, wl.scales[t]))
+        fn = tp.shard_column if n in tp_block.COLUMN else tp.shard_row
+        Wp[n], sh_ads = fn(W, ads, world, rank, mk)
+        ap[n] = []
+        for a in sh_ads:    # B rows need 16-byte alignment: copy into padded storage
+            Bs = mux.make_B_storage(a.B.shape[0], a.rank)
+            Bs.copy_(a.B)
+            ap[n].append(mux.Adapter(a.A.contiguous(), Bs, a.rank, a.scale))
+        del W, ads
+    for i in (1, 2):
+        Wp[f"norm{i}"] = (1.0 + 0.1 * torch.randn(hidden, device="cuda",
+                                                   generator=torch.Generator(device="cuda").manual_seed(seed + i))
+                          ).bfloat16()
+    be = Backend()
+    be.task_tokens = list(w.task_tokens)
+    blk = tp_block.TPDecoderBlock(be, shape, Wp, ap, r_cap)
+    i32 = dict(dtype=torch.int32, device="cuda")
+    tso, sl = torch.tensor(w.off, **i32), torch.tensor(w.lens, **i32)
+    cap = torch.tensor(w.cap, **i32) if w.cap else None
+    bound = int(mux.pack_bound_rows(w.T, w.S, 64))
+    max_rows = -(-bound // (64 * world)) * 64 * world
+    rows = max_rows // world
+    pk = mux.alloc_pack_outputs(w.M, w.S, max_rows, max_rows // 64)
+    rs = torch.empty(max_rows, **i32)
+    Xtok = _gen(torch, seed * 7, (w.T, hidden), 1.0)
+    dYtok = _gen(torch, seed * 11, (w.T, hidden), 1.0)
+    x_rows = torch.empty(rows, hidden, dtype=torch.bfloat16, device="cuda")
+    dy_rows = torch.empty(rows, hidden, dtype=torch.bfloat16, device="cuda")
+    st = list(range(w.M))
+    mine = slice(rank * rows, (rank + 1) * rows)
+
+    def step():
+        mux.pack_chunks(tso, sl, cap, 0, 64, max_rows=max_rows, max_chunks=max_rows // 64, out=pk)
+        mux.row_start(sl, pk["seq_row"], max_rows, out=rs)
+        mux.pack_apply(pk["row_src"][mine], Xtok, rows, out=x_rows)
+        blk.forward(x_rows, pk["seg_off"], st, rs)
+        mux.pack_apply(pk["row_src"][mine], dYtok, rows, out=dy_rows)
+        blk.backward(dy_rows)
+
+    lo, hi = rank * w.T // world, (rank + 1) * w.T // world
+    h2d = [tso, sl, Xtok[lo:hi], dYtok[lo:hi]]
+
+    def result_tensors():
+        out = []
+        for n, (dA, dB) in blk.adapter_grads().items():
+            col = n in tp_block.COLUMN
+            for a_, b_ in zip(dA, dB):
+                if a_ is None:
+                    continue
+                out.append(b_ if col else a_)
+                if rank == 0:
+                    out.append(a_ if col else b_)
+        return out
+
+    pairs = sum(int(L) * (int(L) + 1) // 2 for x in wl.task_lens for L in x)
+    attn_flops = 12 * 128 * heads * pairs
+    desc = {"parallelism": f"tp{world} decoder block (column q/k/v/gate/up, head-sharded attention, row o/down; "
+                           "sequence-parallel RMSNorm/residuals; 8 NCCL AG/RS per step)",
+            "hidden": hidden, "ffn": ffn, "heads": heads, "kv_heads": kv_heads, "max_rows": max_rows,
+            "attention_flops": attn_flops}
+    launches = 4 + tp_block.TPDecoderBlock.LAUNCHES_FWD + tp_block.TPDecoderBlock.LAUNCHES_BWD
+    return step, launches, h2d, result_tensors, desc, [be]
+
+
+def tp_arm(args):
+    """--mode tp (the default for --gpus N > 1): the workload tensor-parallel over the N ranks
+    (strong scaling: the same tokens as N = 1, split over N GPUs).  Config 2 (3 linears): the layer
+    stack L0 column / L1 row / L2 column (Megatron pairing; sequence-parallel AG/RS).
+    Configs 4/5 (7 linears): the whole decoder block (tp_block.py).  Every rank's compute is the
+    fused libmux kernels; collectives are NCCL (or fused into the GEMMs: --fused-rs/--fused-ag).
+    Beside it (N > 1) the task-sharded replicas of the same config are timed as a secondary field
+    ("weak" scaling: tasks are independent and the backbone frozen, so no collective at all)."""
+    if args.comm_ctas:
+        os.environ["NCCL_MAX_CTAS"] = str(args.comm_ctas)
+    import torch
+    from paper_2603_02885_b200 import mux, orchestrate, tp
+    dist, world, rank, local, backend = dist_setup(torch)
+    mux.lib()
+    w = Workload(args.config)
+    Backend = timed_backend_cls(tp, torch)
+    if len(w.linears) == 7:
+        step, launches, h2d_src, result_tensors, desc, bes = _tp_block(args, w, torch, mux, tp, Backend, world, rank)
+        flops = w.flops + desc["attention_flops"]
+    else:
+        step, launches, h2d_src, result_tensors, desc, bes = _tp_chain(args, w, torch, mux, tp, orchestrate,
+                                                                       Backend, world, rank)
+        flops = w.flops
+    stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    rec = []
+    for be in bes:
+        be.record = rec
+    clocks = ClockSampler(local)
     dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s0.record()
+    s0.record(stream)
     for _ in range(args.steps):
         step()
-    s1.record()
+    s1.record(stream)
     torch.cuda.synchronize()
+    dist.barrier()
+    clk = clocks.stop()
+    for be in bes:
+        be.record = None
     t = torch.tensor([s0.elapsed_time(s1) / args.steps], dtype=torch.float64, device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
+    # dominant kernel: the fused forward GEMM launches on this rank (max time over ranks)
+    f_ms = torch.tensor([sum(a.elapsed_time(b) for a, b, _ in rec)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(f_ms, op=dist.ReduceOp.MAX)
+    f_flops = sum(f for _, _, f in rec)
+    pk = peaks()
+    achieved = f_flops / (float(f_ms.item()) * 1e-3) / 1e12 if rec else None
+    roof = _roofline(achieved, pk, ms * args.steps, clk, len(rec) // max(1, args.steps),
+                     "mux_gemm_kernel<fwd> on this rank's shard (events around each forward call; max over ranks)")
+
+    # e2e through the public API with host buffers: each rank copies its share of the inputs
+    e2e = None
+    if not args.no_e2e:
+        e2e = _e2e_generic(torch, dist, stream, step, h2d_src, result_tensors(), args, w.T)
+    line = {"metric": METRIC, "value": w.T / (ms * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded device normals)", "mode": "tp",
+            "config": dict({"workload": f"config {args.config}: " + w.wl.description, "valid_tokens": w.T,
+                            "tasks": w.M, "ranks": w.wl.ranks, "dist_backend": backend,
+                            "l2": "inputs larger than L2 (weights + activations per step > 126 MB)"}, **desc),
+            "tflops_per_gpu_algorithmic": flops / (ms * 1e-3) / 1e12 / world,
+            "frac_of_peak_per_gpu": {"measured_burst": flops / (ms * 1e-3) / 1e12 / world / pk["bf16_tflops"],
+                                     "measured_sustained": flops / (ms * 1e-3) / 1e12 / world
+                                     / pk["bf16_tflops_sustained"]},
+            "roofline": roof, "clocks": clk, "gpu_launches": launches * args.steps, "e2e": e2e}
+    if world > 1 and not args.no_replicas:
+        line["replicas"] = _replicas_secondary(args, torch, dist, world, rank)
     if rank == 0:
-        print(json.dumps({"metric": METRIC, "value": w.T / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
-                          "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-                          "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
-                          "data": "synthetic", "mode": "tp",
-                          "config": {"workload": f"config {args.config}: " + w.wl.description,
-                                     "parallelism": f"tp{world} (L0 column, L1 row, L2 column; sequence-parallel "
-                                                    "AG/RS over NCCL)", "valid_tokens": w.T,
-                                     "htasks": [ht["tasks"] for ht in htasks],
-                                     "schedule": [f"h{sg.htask}.{sg.index}" for sg, _ in schedule],
-                                     "nccl_max_ctas": args.comm_ctas or None, "planner": plan_note,
-                                     "reduce_scatter": "fused into the GEMM epilogue (peer stores)" if args.fused_rs
-                                     else "NCCL",
-                                     "all_gather": "copy-engine push, consumed per row block by the GEMM"
-                                     if args.fused_ag else "NCCL",
-                                     "max_rows": [ht["max_rows"] for ht in htasks]},
-                          "tflops_per_gpu_algorithmic": w.flops / (ms * 1e-3) / 1e12 / world}), flush=True)
+        print(json.dumps(line), flush=True)
     dist.destroy_process_group()
+
+
+def _replicas_secondary(args, torch, dist, world, rank):
+    """Task-sharded replicas (no collective): every rank runs its own hTask of the config-2 shape."""
+    from paper_2603_02885_b200 import mux
+    w = Workload("2", rank_seed=rank)
+    ms_ = MuxStep(w, torch, mux)
+    for _ in range(args.warmup):
+        ms_.step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(args.steps):
+        ms_.step()
+    b.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([a.elapsed_time(b) / args.steps], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    tt = torch.tensor([w.T], dtype=torch.int64, device="cuda")
+    dist.all_reduce(tt)
+    return {"value": int(tt.item()) / (float(t.item()) * 1e-3), "unit": UNIT, "ms_per_step": float(t.item()),
+            "scaling": "weak", "workload": "config 2 per rank (own seeded tasks), no collective in the data path"}
+
+
+def traffic_of_this_build():
+    """DRAM bytes per forward-GEMM launch from the ncu --set full capture in profiles/gemm_fwd_traffic.json
+    (tools/traffic_json.py), used only if it was captured on THIS libmux.so (sha256 match); else null."""
+    import hashlib
+    tp_ = os.path.join(ROOT, "profiles", "gemm_fwd_traffic.json")
+    lib = os.path.join(ROOT, "paper_2603_02885_b200", "libmux.so")
+    if not os.path.exists(tp_) or not os.path.exists(lib):
+        return None, "no capture"
+    tj = json.load(open(tp_))
+    sha = hashlib.sha256(open(lib, "rb").read()).hexdigest()[:16]
+    if tj.get("libmux_sha16") != sha:
+        return None, f"capture is of another build ({tj.get('libmux_sha16')} != {sha}): not reported"
+    return tj.get("mean_bytes_per_launch"), tj.get("source")
+
+
+def _roofline(achieved, pk, timed_ms, clk, launches_per_step, kernel):
+    """frac against the measured BURST bf16 peak when the timed region is short (< 1 s) and the clocks
+    were not throttled (the burst figure is cuBLAS timed alone for ~ the same duration); against the
+    sustained peak otherwise.  Both are reported."""
+    throttled = bool(set(clk.get("reasons") or []) & {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                                                       "sw_power_cap"})
+    use_burst = timed_ms < 1000.0 and not throttled
+    peak = pk["bf16_tflops"] if use_burst else pk["bf16_tflops_sustained"]
+    return {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": None if achieved is None else achieved / peak,
+            "frac_of_burst": None if achieved is None else achieved / pk["bf16_tflops"],
+            "frac_of_sustained": None if achieved is None else achieved / pk["bf16_tflops_sustained"],
+            "peak_kind": ("burst" if use_burst else "sustained") + f" (timed region {timed_ms:.0f} ms, "
+                                                                   f"throttled={throttled})",
+            "peak_source": pk["source"], "kernel": kernel, "launches_per_step": launches_per_step}
+
+
+def _e2e_generic(torch, dist, stream, step, h2d_src, results, args, tokens):
+    """The same step with its inputs copied host->device (pinned, prefetched one step ahead on a copy
+    stream into a second slot) and its result read back device->host every step."""
+    pin = lambda t: t.detach().cpu().pin_memory()  # noqa: E731
+    host = [pin(t) for t in h2d_src]
+    slots = [[torch.empty_like(t) for t in h2d_src] for _ in range(2)]
+    h_res = [torch.empty(g.shape, dtype=g.dtype, pin_memory=True) for g in results]
+    h2d = sum(x.numel() * x.element_size() for x in host)
+    d2h = sum(g.numel() * g.element_size() for g in results)
+    cs = torch.cuda.Stream()
+    copied = [torch.cuda.Event() for _ in range(2)]
+    consumed = [torch.cuda.Event() for _ in range(2)]
+    done, read = torch.cuda.Event(), torch.cuda.Event()
+
+    def run(n):
+        for ev in consumed:
+            ev.record(stream)
+        read.record(stream)
+
+        def h2d_copy(i):
+            with torch.cuda.stream(cs):
+                cs.wait_event(consumed[i % 2])
+                for d_, h_ in zip(slots[i % 2], host):
+                    d_.copy_(h_, non_blocking=True)
+                copied[i % 2].record(cs)
+        h2d_copy(0)
+        for i in range(n):
+            if i + 1 < n:
+                h2d_copy(i + 1)
+            stream.wait_event(copied[i % 2])
+            for d_, s_ in zip(h2d_src, slots[i % 2]):     # the step reads its inputs from their home
+                d_.copy_(s_, non_blocking=True)
+            consumed[i % 2].record(stream)
+            stream.wait_event(read)                        # the previous read-back is done with the result
+            step()
+            done.record(stream)
+            with torch.cuda.stream(cs):
+                cs.wait_event(done)
+                for g, hg in zip(results, h_res):
+                    hg.copy_(g, non_blocking=True)
+                read.record(cs)
+
+    run(max(1, args.warmup))
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    cs.wait_event(e0)
+    run(args.steps)
+    stream.wait_stream(cs)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    te = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device="cuda")
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_ms = float(te.item())
+    return {"value": tokens / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms,
+            "what": "per rank: pinned H2D of the sequence metadata and this rank's 1/p share of the token-major "
+                    "input and loss gradient (a sharded data loader's bytes; prefetched one step ahead on a copy "
+                    "stream, staged into the device buffers the step reads); D2H of this rank's adapter-gradient "
+                    "shards (replicated all-reduced gradients only on rank 0), overlapped with the next step"}
 
 
 def block_arm(args):
@@ -797,6 +1131,25 @@ def block_arm(args):
                       "clocks": clocks}), flush=True)
 
 
+def spawn_ranks(n: int) -> int:
+    """`python bench.py --gpus N` without torchrun: re-launch this command under torch.distributed.run,
+    one process per GPU on this node (rendezvous on 127.0.0.1); rank 0 prints the JSON line.  NCCL's
+    INIT/NVLS log goes to stderr (NCCL_DEBUG=INFO), so the rank count and NVLS use are on record."""
+    import socket
+    import subprocess
+    s_ = socket.socket()
+    s_.bind(("127.0.0.1", 0))
+    port = s_.getsockname()[1]
+    s_.close()
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT,NVLS")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -810,8 +1163,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-rows", type=int, default=4, help="rows per task per reference-arm step")
-    ap.add_argument("--mode", default="replicas", choices=["replicas", "tp", "block"],
-                    help="N>1: task-sharded replicas (default, weak scaling) or tensor parallel (strong)")
+    ap.add_argument("--mode", default="auto", choices=["auto", "replicas", "tp", "block"],
+                    help="auto: N=1 -> the single-GPU step (replicas x1), N>1 -> tensor parallel (strong scaling, "
+                         "the north_star TP path) with the task-sharded replicas as a secondary field")
+    ap.add_argument("--no-replicas", action="store_true", help="--mode tp, N>1: skip the secondary replicas timing")
     ap.add_argument("--htasks", type=int, default=1,
                     help="--mode tp: hTasks interleaved by Alg. 1 (NEXT-1); 0 = chosen by the planner (NEXT-4)")
     ap.add_argument("--comm-ctas", type=int, default=0, help="--mode tp: NCCL_MAX_CTAS for the overlapped collectives")
@@ -822,6 +1177,10 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl != "reference":
+        sys.exit(spawn_ranks(args.gpus))
+    if args.mode == "auto":
+        args.mode = "tp" if int(os.environ.get("WORLD_SIZE", "1")) > 1 else "replicas"
     if args.impl == "reference":
         reference_arm(args)
     elif args.mode == "tp":

@@ -211,3 +211,13 @@ int oracle_num_threads(void) {
   return 1;
 #endif
 }
+
+/* thread count of the OpenMP loops (timing only: the result does not depend on it) */
+void oracle_set_num_threads(int n) {
+#ifdef _OPENMP
+  extern void omp_set_num_threads(int);
+  omp_set_num_threads(n > 0 ? n : 1);
+#else
+  (void)n;
+#endif
+}

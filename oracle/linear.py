@@ -44,11 +44,17 @@ def lib():
         _lib.oracle_linear_bwd.argtypes = [ctypes.c_int, P, P, ctypes.c_int, P, ctypes.c_int64,
                                            ctypes.c_int64, ctypes.c_int, P, P, P, P, ctypes.c_int64, P, P]
         _lib.oracle_num_threads.restype = ctypes.c_int
+        _lib.oracle_set_num_threads.argtypes = [ctypes.c_int]
     return _lib
 
 
 def num_threads() -> int:
     return int(lib().oracle_num_threads())
+
+
+def set_num_threads(n: int) -> None:
+    """OpenMP thread count (timing only; results are bitwise the same at any count)."""
+    lib().oracle_set_num_threads(int(n))
 
 
 def widen(x) -> np.ndarray:

@@ -159,6 +159,33 @@ class MuxBackend:
                                  workspace=self._ws(W, X, seg_task, r_cap))
         return dX, [a.dA for a in adapters], [a.dB for a in adapters]
 
+    # ---- decoder-block ops (tp_block.py): libmux kernels, fresh outputs (caching allocator)
+    def rmsnorm_fwd(self, x, w, eps, res=None):
+        return self.mux.rmsnorm_fwd(x, w, eps, res=res)
+
+    def rmsnorm_bwd(self, dy, x, w, eps, resid=None):
+        return self.mux.rmsnorm_bwd(dy, x, w, eps, resid=resid)
+
+    def rope(self, x, row_start, heads, head_dim, base, inverse=False):
+        return self.mux.rope_(x, row_start, heads, head_dim, base, inverse=inverse)
+
+    def attn_fwd(self, q, k, v, row_start, heads, kv_heads, scale):
+        return self.mux.attn_fwd(q, k, v, row_start, heads, kv_heads, scale)
+
+    def attn_bwd(self, dO, q, k, v, o, lse, row_start, heads, kv_heads, scale):
+        ws = self._buf(("attn_ws", q.shape[0], heads), (self.mux.attn_workspace_size(q.shape[0], heads),),
+                       torch.uint8, q.device)
+        return self.mux.attn_bwd(dO, q, k, v, o, lse, row_start, heads, kv_heads, scale, workspace=ws)
+
+    def swiglu_fwd(self, g, u):
+        return self.mux.swiglu_fwd(g, u)
+
+    def swiglu_bwd(self, dh, g, u):
+        return self.mux.swiglu_bwd(dh, g, u)
+
+    def add(self, a, b):
+        return self.mux.add(a, b)
+
     # fused GEMM -> reduce-scatter (peer stores + owner-side sum; see FusedRs)
     rs_exchange = None  # optional buffer-mapping hook for FusedRs (default: symmetric memory)
 
@@ -307,6 +334,23 @@ class ColumnParallelMuxLinear:
         Y, self.Hs = self.be.fwd(seg_off, seg_task, self.ads, self.X, self.W, self.r_cap)
         return Y
 
+    def forward_full(self, seg_off, seg_task, X):
+        """X [R, K] already gathered (one all-gather shared by several column layers reading the
+        same input, e.g. q/k/v or gate/up) -> Y_p [R, N/p]."""
+        self.X = X
+        Y, self.Hs = self.be.fwd(seg_off, seg_task, self.ads, X, self.W, self.r_cap)
+        return Y
+
+    def backward_partial(self, seg_off, seg_task, dY_cols):
+        """dY_p [R, N/p] -> this rank's partial dX [R, K] (the caller sums the partials of the layers
+        that shared the input, then reduce-scatters once); dA_t all-reduced, dB_{t,p} local."""
+        dXp, dA, dB = self.be.bwd(seg_off, seg_task, self.ads, dY_cols, self.X, self.W, self.Hs, self.r_cap)
+        for g in dA:
+            if g is not None:
+                all_reduce_(g, self.group)
+        self.dA, self.dB = dA, dB
+        return dXp, dA, dB
+
     def backward(self, seg_off, seg_task, dY_cols):
         """dY_p [R, N/p] -> dX rows [R/p, K]; dA_t all-reduced, dB_{t,p} local."""
         if self.fused_rs:
@@ -317,6 +361,7 @@ class ColumnParallelMuxLinear:
         for g in dA:
             if g is not None:
                 all_reduce_(g, self.group)
+        self.dA, self.dB = dA, dB
         self.release_ag()
         return (reduce_scatter_rows(dXp, self.group) if dX_rows is None else dX_rows), dA, dB
 
@@ -355,4 +400,5 @@ class RowParallelMuxLinear:
         for g in dB:
             if g is not None:
                 all_reduce_(g, self.group)
+        self.dA, self.dB = dA, dB
         return dXp, dA, dB

@@ -1,0 +1,130 @@
+"""A tensor-parallel LLaMA decoder block with all seven linears multiplexed
+(Megatron TP P:870 with sequence
+parallelism P:205): the block of block.py split over the p ranks of a process
+group, one process per GPU.
+
+Per rank (R packed rows, hidden H, FFN F, p ranks; x_rows = this rank's
+contiguous row block [R/p, H], the same segment table on every rank):
+
+  forward                                            collectives
+    h1_rows = RMSNorm(x_rows)                        (rows are local)
+    h1 = AG(h1_rows)                       [R, H]    AG  (one, shared by q/k/v)
+    q_p, k_p, v_p = column-parallel q/k/v  [R, Hq/p·d], [R, Hkv/p·d]
+    RoPE(q_p, k_p); a_p = attention over this rank's heads (head-sharded,
+      GQA groups stay on one rank: Hkv % p == 0)
+    o_rows = RS(row-parallel o(a_p))       [R/p, H]  RS
+    x2_rows = x_rows + o_rows; h2_rows = RMSNorm(x2_rows)   (one fused pass)
+    h2 = AG(h2_rows)                       [R, H]    AG  (one, shared by gate/up)
+    m_p = SwiGLU(gate_p(h2), up_p(h2))     [R, F/p]
+    y_rows = x2_rows + RS(row-parallel down(m_p))    RS
+  backward mirrors it: AG(dy) -> down dX -> SwiGLU' -> gate/up dX partials,
+    summed, RS -> RMSNorm' (+ residual dy) -> AG -> o dX -> attention' ->
+    RoPE^T -> q/k/v dX partials, summed, RS -> RMSNorm' (+ residual).
+  Adapter gradients: column layers all-reduce dA_t (Gs_p is a partial sum over
+  ranks), row layers all-reduce dB_t (Hs_p is) — tp.py.
+
+Eight big collectives per block step ((p-1)/p · R · H · 2 bytes each), as
+SURVEY §8(e) counts.  Every arithmetic step runs in the backend: `tp.MuxBackend`
+(libmux kernels) on the product path, an fp64 oracle backend in the CPU tests.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Dict, List, Sequence
+
+import torch
+
+from . import tp
+from .block import LINEARS, BlockShape
+
+COLUMN = ("q", "k", "v", "gate", "up")
+ROW = ("o", "down")
+
+
+@dataclass
+class TPBlockShape(BlockShape):
+    """BlockShape split over p ranks (heads and FFN columns)."""
+    p: int = 1
+
+    def __post_init__(self):
+        if self.heads % self.p or self.kv_heads % self.p or self.ffn % self.p or self.hidden % self.p:
+            raise ValueError(f"heads {self.heads}, kv_heads {self.kv_heads}, ffn {self.ffn} and hidden "
+                             f"{self.hidden} must divide by p = {self.p}")
+
+
+def shard_block(weights: Dict[str, torch.Tensor], adapters: Dict[str, Sequence], p: int, r: int, make_adapter):
+    """This rank's shards: column-parallel q/k/v/gate/up (rows of W, rows of B_t), row-parallel o/down
+    (columns of W, columns of A_t); the norm weights are replicated."""
+    W, ads = {}, {}
+    for name in LINEARS:
+        fn = tp.shard_column if name in COLUMN else tp.shard_row
+        W[name], ads[name] = fn(weights[name], adapters[name], p, r, make_adapter)
+    W["norm1"], W["norm2"] = weights["norm1"], weights["norm2"]
+    return W, ads
+
+
+class TPDecoderBlock:
+    """weights / adapters: this rank's shards (shard_block); backend: tp.MuxBackend or a test backend
+    with the same op methods (fwd/bwd linears + rmsnorm/rope/attention/swiglu/add)."""
+
+    def __init__(self, backend, shape: TPBlockShape, weights: Dict[str, torch.Tensor],
+                 adapters: Dict[str, List], r_cap: int, group=None):
+        self.be, self.s, self.w, self.r_cap, self.group = backend, shape, weights, r_cap, group
+        self.lin = {}
+        for name in LINEARS:
+            cls = tp.ColumnParallelMuxLinear if name in COLUMN else tp.RowParallelMuxLinear
+            self.lin[name] = cls(backend, weights[name], adapters[name], r_cap, group=group)
+
+    # ------------------------------------------------------------------ forward
+    def forward(self, x_rows, seg_off, seg_task, row_start):
+        s, be, lin = self.s, self.be, self.lin
+        hq, hkv = s.heads // s.p, s.kv_heads // s.p
+        self.seg_off, self.seg_task, self.row_start = seg_off, list(seg_task), row_start
+        st = self.seg_task
+        self.x_rows = x_rows
+        h1 = tp.all_gather_rows(be.rmsnorm_fwd(x_rows, self.w["norm1"], s.eps), self.group)
+        q = lin["q"].forward_full(seg_off, st, h1)
+        k = lin["k"].forward_full(seg_off, st, h1)
+        v = lin["v"].forward_full(seg_off, st, h1)
+        q = be.rope(q, row_start, hq, s.head_dim, s.rope_base)
+        k = be.rope(k, row_start, hkv, s.head_dim, s.rope_base)
+        a, lse = be.attn_fwd(q, k, v, row_start, hq, hkv, s.head_dim ** -0.5)
+        o_rows = lin["o"].forward(seg_off, st, a)                       # RS inside
+        h2_rows, x2_rows = be.rmsnorm_fwd(o_rows, self.w["norm2"], s.eps, res=x_rows)
+        h2 = tp.all_gather_rows(h2_rows, self.group)
+        g = lin["gate"].forward_full(seg_off, st, h2)
+        u = lin["up"].forward_full(seg_off, st, h2)
+        m = be.swiglu_fwd(g, u)
+        d_rows = lin["down"].forward(seg_off, st, m)                    # RS inside
+        self.saved = dict(q=q, k=k, v=v, a=a, lse=lse, x2_rows=x2_rows, g=g, u=u)
+        return be.add(x2_rows, d_rows)
+
+    # ------------------------------------------------------------------ backward
+    def backward(self, dy_rows):
+        s, be, lin, sv = self.s, self.be, self.lin, self.saved
+        hq, hkv = s.heads // s.p, s.kv_heads // s.p
+        so, st = self.seg_off, self.seg_task
+        dm, _, _ = lin["down"].backward(so, st, dy_rows)                 # AG(dy) inside; AR(dB)
+        dg, du = be.swiglu_bwd(dm, sv["g"], sv["u"])
+        dh2 = be.add(lin["gate"].backward_partial(so, st, dg)[0], lin["up"].backward_partial(so, st, du)[0])
+        dh2_rows = tp.reduce_scatter_rows(dh2, self.group)
+        dx2_rows = be.rmsnorm_bwd(dh2_rows, sv["x2_rows"], self.w["norm2"], s.eps, resid=dy_rows)
+        da, _, _ = lin["o"].backward(so, st, dx2_rows)                   # AG(dx2) inside; AR(dB)
+        dq, dk, dv = be.attn_bwd(da, sv["q"], sv["k"], sv["v"], sv["a"], sv["lse"], self.row_start, hq, hkv,
+                                 s.head_dim ** -0.5)
+        dq = be.rope(dq, self.row_start, hq, s.head_dim, s.rope_base, inverse=True)
+        dk = be.rope(dk, self.row_start, hkv, s.head_dim, s.rope_base, inverse=True)
+        dh1 = be.add(lin["q"].backward_partial(so, st, dq)[0], lin["k"].backward_partial(so, st, dk)[0])
+        dh1 = be.add(dh1, lin["v"].backward_partial(so, st, dv)[0])
+        dh1_rows = tp.reduce_scatter_rows(dh1, self.group)
+        return be.rmsnorm_bwd(dh1_rows, self.x_rows, self.w["norm1"], s.eps, resid=dx2_rows)
+
+    def adapter_grads(self):
+        """{linear: ([dA_t], [dB_t])} of this rank (after backward)."""
+        return {n: (self.lin[n].dA, self.lin[n].dB) for n in LINEARS}
+
+    # libmux launches per step at world p > 1 (for the bench's gpu_launches): forward = 2 norms +
+    # 7 fused linears + 2 RoPE + attention + SwiGLU + add = 14 (+ 2 owner-side sums with fused RS);
+    # backward = 7 dX GEMMs + 7 gradient kernels + SwiGLU + 2 norms + attention (4) + 2 RoPE + 3 adds
+    LAUNCHES_FWD = 14
+    LAUNCHES_BWD = 26

@@ -13,6 +13,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from oracle import linear as olin
+from tp_oracle_backend import OracleBackend
 
 K, N, R = 32, 48, 256          # up: K -> N (column), down: N -> K (row)
 SEG = [64, 128, 64]
@@ -32,42 +33,6 @@ def _problem():
     B2 = [rng.standard_normal((K, r)) for r in RANKS]
     dY2 = rng.standard_normal((R, K))
     return seg_off, X, W1, W2, A1, B1, A2, B2, dY2
-
-
-class OracleBackend:
-    """fp64 oracle as the per-rank local linear (torch fp64 CPU tensors in/out)."""
-
-    def fwd(self, seg_off, seg_task, ads, X, W, r_cap):
-        Y, Hs = olin.linear_fwd(seg_off.numpy(), seg_task, [a.A.numpy() for a in ads],
-                                [a.B.numpy() for a in ads], [a.rank for a in ads], [a.scale for a in ads],
-                                X.numpy(), W.numpy(), r_cap)
-        return torch.from_numpy(Y), torch.from_numpy(Hs)
-
-    def shrink(self, seg_off, seg_task, ads, X, W, r_cap, row_begin, row_end):
-        # rows outside the range are NaN: only the all-gathered own rows may reach the forward
-        _, Hs = self.fwd(seg_off, seg_task, ads, X, W, r_cap)
-        Hs = Hs.clone()
-        Hs[:row_begin] = float("nan")
-        Hs[row_end:] = float("nan")
-        return Hs
-
-    def fwd_hs(self, seg_off, seg_task, ads, X, W, Hs, r_cap):
-        # Eq. 1 with the given (gathered) shrink: Y = X W^T + Hs B_t^T on each segment's rows
-        Y = X.numpy() @ W.numpy().T
-        so, Hn = seg_off.numpy(), Hs.numpy()
-        for s, t in enumerate(seg_task):
-            a = ads[t]
-            if a.rank:
-                Y[so[s]:so[s + 1]] += Hn[so[s]:so[s + 1], :a.rank] @ a.B.numpy().T
-        return torch.from_numpy(Y)
-
-    def bwd(self, seg_off, seg_task, ads, dY, X, W, Hs, r_cap):
-        # the oracle recomputes H from X (fp64), which equals the saved Hs / s
-        dX, Gs, grads = olin.linear_bwd(seg_off.numpy(), seg_task, [a.A.numpy() for a in ads],
-                                        [a.B.numpy() for a in ads], [a.rank for a in ads],
-                                        [a.scale for a in ads], dY.numpy(), X.numpy(), W.numpy(), r_cap)
-        return (torch.from_numpy(dX), [torch.from_numpy(g[0]) for g in grads],
-                [torch.from_numpy(g[1]) for g in grads])
 
 
 def _worker(rank, world, port, q, shared_shrink=False):
