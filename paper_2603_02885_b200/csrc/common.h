@@ -28,6 +28,8 @@ struct GemmCfg {
 };
 constexpr int kRowQuarter = 64; // segment granularity inside a pair tile (chunk minimum)
 constexpr int kSideN = 128;     // N of the shrink MMA (rank padded to 64 in CTA 0's half)
+constexpr int kSkMaxClusters = 120;          // stream-K range table in shared memory (misc area)
+constexpr int kSkSlotFloats = 2 * 4 * 256 * 32;  // one cluster's partial 256 x 256 fp32 tile
 
 struct GemmParams {
   // A operand of the main product: X (fwd) / dY (bwd): dims {Kred, rows}, box {64, 128}
@@ -78,6 +80,13 @@ struct GemmParams {
   unsigned long long ag_seq;
   const unsigned long long* ag_flags;
   unsigned long long peer_wait_ns;  // limit of a wait on another rank's flag (0 = none; ptx.cuh)
+  // Stream-K schedule of the main tiles (sk = 1, chosen on the host where whole tiles leave the last
+  // round of clusters half idle, e.g. 512-column tensor-parallel shards; see gemm.cu): cluster c's
+  // first piece of a split tile is a partial accumulator in sk_part slot c, published on sk_flags[c].
+  int32_t sk;
+  int32_t sk_side_cost_x4;          // a shrink tile's k-block, in quarters of a main k-block (balance)
+  unsigned long long* sk_flags;     // [kSkMaxClusters] epoch-tagged (workspace)
+  float* sk_part;                   // [kSkMaxClusters][2 CTAs][4 warps][256 cols][32 lanes] fp32
   int32_t seg_adapter[MUX_MAX_SEGMENTS];
   int32_t seg_rank[MUX_MAX_SEGMENTS];
   float seg_scale[MUX_MAX_SEGMENTS];

@@ -178,6 +178,63 @@ __device__ __forceinline__ Tile tile_at(int t, int num_m, int num_n, int group_m
   return r;
 }
 
+// ---- stream-K (p.sk): balance the main tiles' k-block units over the clusters.
+// Every cluster first runs its shrink (side) tiles, round-robin as in the data-parallel schedule;
+// then one contiguous range of main-tile k-block units [b[c], b[c+1]) in tile-major order
+// (tile = m * num_n + n, k fastest), sized so that every cluster's side + main work is equal (a
+// side tile's k-block counts sk_side_cost_x4 / 4 main k-blocks).  A range that starts inside a
+// tile computes a partial accumulator (k-blocks [k0, k1) of that tile) into cluster c's slot of
+// sk_part and publishes it on sk_flags[c]; the piece holding k-block 0 of a tile — at the END of
+// an earlier cluster's range — runs the LoRA extension blocks, waits for the partials of every
+// later cluster whose range starts inside the tile and adds them in ascending cluster order
+// (deterministic).  A partial piece is the first item of its cluster's main range and never
+// waits on anything, so the finalizing piece (last item of an earlier range) cannot deadlock.
+__device__ void sk_compute_bounds(const GemmParams& p, int num_m, int num_n, int num_kb, int ncl, int* b) {
+  const long long n_side = p.has_side ? num_m : 0;
+  const long long w = (static_cast<long long>(p.sk_side_cost_x4) * num_kb + 3) / 4;
+  const long long U = static_cast<long long>(num_m) * num_n * num_kb;
+  const long long L = U + n_side * w;
+  long long side_before = 0, prev = 0;
+  b[0] = 0;
+  for (int c = 1; c <= ncl; ++c) {
+    const long long ns = (c - 1 < n_side) ? (n_side - 1 - (c - 1)) / ncl + 1 : 0;  // side tiles of cluster c-1
+    side_before += ns * w;
+    long long a = (c == ncl) ? U : (L * c) / ncl - side_before;
+    a = a < prev ? prev : (a > U ? U : a);
+    b[c] = static_cast<int>(a);
+    prev = a;
+  }
+}
+
+struct SkPiece {
+  int k0, k1;   // k-block range of the piece
+  bool fin;     // holds k-block 0: runs the extension blocks, adds the partials, stores the tile
+  int tile;     // main tile index (m * num_n + n), stream-K only
+};
+
+// Every role walks the same item sequence: f(tile, piece).
+template <typename F>
+__device__ __forceinline__ void for_each_item(const GemmParams& p, int cid, int ncl, int num_m, int num_n,
+                                              int side_lo, int total_tiles, int num_kb, const int* skb, F&& f) {
+  if (!p.sk) {
+    for (int t = cid; t < total_tiles; t += ncl)
+      f(tile_at(t, num_m, num_n, p.group_m, p.has_main != 0, p.has_side != 0, side_lo, p.side_first != 0),
+        SkPiece{0, num_kb, true, 0});
+    return;
+  }
+  const int n_side = p.has_side ? num_m : 0;
+  for (int t = cid; t < n_side; t += ncl) f(Tile{t, 0, true}, SkPiece{0, num_kb, true, 0});
+  const int end = skb[cid + 1];
+  for (int u = skb[cid]; u < end;) {
+    const int tile = u / num_kb;
+    const int k0 = u - tile * num_kb;
+    const int k1 = min(num_kb, end - tile * num_kb);
+    const int m = tile / num_n;
+    f(Tile{m, tile - m * num_n, false}, SkPiece{k0, k1, k0 == 0, tile});
+    u = tile * num_kb + k1;
+  }
+}
+
 // Opt-in instrumentation (-DMUX_PROFILE, experiment builds only): per-role
 // cycles spent waiting on each barrier, accumulated into GemmParams::dbg:
 //   [0] MMA total  [1] MMA wait full  [2] MMA wait tmem-empty
@@ -217,6 +274,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty_bar + 2);
   int* so = reinterpret_cast<int*>(misc + 256);  // seg_off copy, <= 65 ints
+  int* skb = reinterpret_cast<int*>(misc + 528);  // stream-K range table, <= kSkMaxClusters + 1 ints
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -249,6 +307,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   griddep_wait();
   griddep_launch_dependents();
   for (int i = threadIdx.x; i <= p.num_segs; i += blockDim.x) so[i] = p.seg_off[i];
+  if (p.sk && threadIdx.x == 96) {  // warp 3 has no role: the stream-K range table
+    const int rows = p.seg_off[p.num_segs];
+    sk_compute_bounds(p, (rows + kPairRows - 1) / kPairRows, (p.nout + (kNarrow ? 128 : kBN) - 1) / (kNarrow ? 128 : kBN),
+                      (p.kred + GemmCfg<kBwd>::kBK - 1) / GemmCfg<kBwd>::kBK, ncl, skb);
+  }
   const unsigned long long epoch = *reinterpret_cast<volatile unsigned long long*>(p.epoch) + 1ull;
   tc_fence_before();
   __syncthreads();
@@ -283,8 +346,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       const uint32_t full_u = smem_u32(full_bar);
       const uint32_t full_leader = mapa_shared(full_u, 0);  // stage s barrier: + 8 s
       uint32_t ag_ok = 0;  // owners whose rows have landed in the gather buffer (fused all-gather)
-      for (int t = cid; t < total_tiles; t += ncl) {
-        const Tile tl = tile_at(t, num_m, num_n, p.group_m, p.has_main != 0, p.has_side != 0, side_lo, p.side_first != 0);
+      for_each_item(p, cid, ncl, num_m, num_n, side_lo, total_tiles, num_kb, skb, [&](const Tile& tl, const SkPiece& pc) {
         const PairGroups g = pair_groups(p, so, tl.m);
         const int row_c = tl.m * kPairRows + kBM * rk;  // this CTA's rows
         if (p.ag_world > 0) {
@@ -338,7 +400,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           }
         } else {
           const int col_c = tl.n * kTileN + (kTileN / 2) * rk;  // this CTA's half of N
-          for (int kb = 0; kb < num_kb; ++kb) {
+          for (int kb = pc.k0; kb < pc.k1; ++kb) {
             PROF_T0(tw_);
             mbar_wait(&empty_bar[stage], phase ^ 1u);
             PROF_ADD(pw_empty, tw_);
@@ -366,7 +428,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
 #ifdef MUX_DIAG_NO_FLAG
           if (false) {  // timing-only diagnostic: no wait for the shrink tile (results may race)
 #else
-          if (g.n > 0 && p.has_side) {
+          if (pc.fin && g.n > 0 && p.has_side) {
 #endif
             // the side tile of this row block must have published Hs/Gs (a caller-given
             // Hs was written by an earlier kernel in stream order)
@@ -383,7 +445,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             }
             __syncwarp();
           }
-          for (int i = 0; i < g.n; ++i) {
+          for (int i = 0; i < (pc.fin ? g.n : 0); ++i) {  // LoRA expand: the tile's final piece only
             // extension block: reduction = rank (<= 64): first k-subtile only
             const int ad = p.seg_adapter[g.seg[i]];
             PROF_T0(tw_);
@@ -407,7 +469,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             advance();
           }
         }
-      }
+      });
     }
   } else if (warp == 1) {
     // =========================== MMA issuer (leader CTA) ================
@@ -439,8 +501,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       auto advance = [&]() {
         if (++stage == kStages) { stage = 0; phase ^= 1u; }
       };
-      for (int t = cid; t < total_tiles; t += ncl) {
-        const Tile tl = tile_at(t, num_m, num_n, p.group_m, p.has_main != 0, p.has_side != 0, side_lo, p.side_first != 0);
+      for_each_item(p, cid, ncl, num_m, num_n, side_lo, total_tiles, num_kb, skb, [&](const Tile& tl, const SkPiece& pc) {
         const PairGroups g = pair_groups(p, so, tl.m);
         PROF_T0(tw_);
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1u);
@@ -475,7 +536,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             }
           }
         } else {
-          for (int kb = 0; kb < num_kb; ++kb) {
+          for (int kb = pc.k0; kb < pc.k1; ++kb) {
             PROF_T0(tw_);
             mbar_wait(&full_bar[stage], phase);
             PROF_ADD(mw_full, tw_);
@@ -486,13 +547,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
               for (int k = 0; k < kBK / 16; ++k)
                 mma_bf16_pair_nomask(d_tmem, make_desc(a_lo + a_off(k), kHi), make_desc(b_lo + b_off(k), kHi),
-                                     kIdescMain, (kb | k) != 0);
+                                     kIdescMain, ((kb - pc.k0) | k) != 0);
               mma_commit_pair_mc(&empty_bar[stage], kPairMask);
             }
             __syncwarp();
             advance();
           }
-          for (int i = 0; i < g.n; ++i) {
+          for (int i = 0; i < (pc.fin ? g.n : 0); ++i) {  // LoRA expand: the tile's final piece only
             PROF_T0(tw_);
             mbar_wait(&full_bar[stage], phase);
             PROF_ADD(mw_full, tw_);
@@ -515,7 +576,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         if (elect_one_sync()) mma_commit_pair_mc(&tfull_bar[acc], kPairMask);
         __syncwarp();
         if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
-      }
+      });
     }
   } else if (warp >= 4) {
     // =========================== epilogue (both CTAs) ===================
@@ -539,8 +600,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     uint32_t acc_phase = 0;
     uint8_t* bufs = epi + q * 2 * kEpiBuf;
     int buf_sel = 0;
-    for (int t = cid; t < total_tiles; t += ncl) {
-      const Tile tl = tile_at(t, num_m, num_n, p.group_m, p.has_main != 0, p.has_side != 0, side_lo, p.side_first != 0);
+    for_each_item(p, cid, ncl, num_m, num_n, side_lo, total_tiles, num_kb, skb, [&](const Tile& tl, const SkPiece& pc) {
       PROF_T0(tw_);
       mbar_wait(&tfull_bar[acc], acc_phase);
       PROF_ADD(ew_tfull, tw_);
@@ -583,7 +643,51 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         __threadfence();
         __syncwarp();
         if (lane == 0) flag_arrive(p.flags + tl.m, epoch);
+      } else if (!pc.fin) {
+        // stream-K partial (the first piece of this cluster's range): fp32 accumulator into this
+        // cluster's slot, laid out [CTA][warp][col / 4][lane][4] so every access is coalesced
+        float4* slot = reinterpret_cast<float4*>(p.sk_part + static_cast<size_t>(cid) * kSkSlotFloats +
+                                                 (static_cast<size_t>(crank) * 4 + q) * (256 * 32));
+#pragma unroll 1
+        for (int c = 0; c < kTileN / 64; ++c) {
+          uint32_t v0[32], v1[32];
+          tmem_ld32(t_addr + c * 64, v0);
+          tmem_ld32(t_addr + c * 64 + 32, v1);
+          tmem_ld_wait();
+          if (c == kTileN / 64 - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(tempty_leader);
+          }
+#pragma unroll
+          for (int g4 = 0; g4 < 16; ++g4) {
+            const uint32_t* v = g4 < 8 ? v0 : v1;
+            const int b = (g4 & 7) * 4;
+            __stcg(slot + (c * 16 + g4) * 32 + lane, make_float4(__uint_as_float(v[b]), __uint_as_float(v[b + 1]),
+                                                                 __uint_as_float(v[b + 2]), __uint_as_float(v[b + 3])));
+          }
+        }
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) flag_arrive(p.sk_flags + cid, epoch);
       } else {
+        // stream-K: the later clusters whose ranges start inside this tile hold its other k-blocks
+        const int t_end = (pc.tile + 1) * num_kb;
+        if (p.sk) {
+          if (lane == 0) {
+            const unsigned long long want = (epoch << 8) | 8ull;
+            for (int c2 = cid + 1; c2 < ncl && skb[c2] < t_end; ++c2) {
+              if (skb[c2 + 1] == skb[c2]) continue;  // empty range: no partial
+              const unsigned long long* f = p.sk_flags + c2;
+              if (ld_acquire_gpu_u64(f) != want) {
+                const uint64_t t0 = globaltimer_ns();
+                while (ld_acquire_gpu_u64(f) != want)
+                  if (globaltimer_ns() - t0 > kWatchdogNs) __trap();
+              }
+            }
+          }
+          __syncwarp();
+        }
         const bool valid = row_w < total_rows;
         const int col_t = tl.n * kTileN;
 #pragma unroll 1
@@ -592,6 +696,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           tmem_ld32(t_addr + c * 64, v0);
           tmem_ld32(t_addr + c * 64 + 32, v1);
           tmem_ld_wait();
+          if (p.sk) {  // + the partials, ascending cluster order (deterministic)
+            for (int c2 = cid + 1; c2 < ncl && skb[c2] < t_end; ++c2) {
+              if (skb[c2 + 1] == skb[c2]) continue;
+              const float4* src = reinterpret_cast<const float4*>(
+                                      p.sk_part + static_cast<size_t>(c2) * kSkSlotFloats +
+                                      (static_cast<size_t>(crank) * 4 + q) * (256 * 32)) + (c * 16) * 32 + lane;
+#pragma unroll
+              for (int g4 = 0; g4 < 16; ++g4) {
+                const float4 x = __ldcg(src + g4 * 32);
+                uint32_t* v = g4 < 8 ? v0 : v1;
+                const int b = (g4 & 7) * 4;
+                v[b] = __float_as_uint(__uint_as_float(v[b]) + x.x);
+                v[b + 1] = __float_as_uint(__uint_as_float(v[b + 1]) + x.y);
+                v[b + 2] = __float_as_uint(__uint_as_float(v[b + 2]) + x.z);
+                v[b + 3] = __float_as_uint(__uint_as_float(v[b + 3]) + x.w);
+              }
+            }
+          }
           if (c == kTileN / 64 - 1) {
             tc_fence_before();
             __syncwarp();
@@ -630,7 +752,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         }
       }
       if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
-    }
+    });
     if (lane == 0) {
       tma_store_wait<0>();
       if (p.rs_world > 0) fence_async_global();  // bulk stores -> generic-proxy release below

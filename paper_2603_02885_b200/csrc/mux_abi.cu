@@ -228,27 +228,38 @@ int num_sms() {
 // ---- linear-layer workspace: [epoch, done][flags][Gs][Hs scratch]
 // Zero-filled once by the caller; the GEMM kernel keeps it consistent across
 // launches (epoch-tagged flags, see ptx.cuh flag_arrive), so no per-call memset.
+// ---- linear-layer workspace: [epoch, done][flags][Gs][Hs scratch][stream-K flags][stream-K partials]
 struct LinearWs {
   unsigned long long* epoch;
   unsigned int* done;
   unsigned long long* flags;
   __nv_bfloat16* gs;
   __nv_bfloat16* hs;
+  unsigned long long* sk_flags;
+  float* sk_part;
+  int sk_slots;
   size_t bytes;
 };
+int num_sms();
 LinearWs carve_linear_ws(void* base, int32_t max_rows, int32_t r_cap) {
   LinearWs w{};
   const size_t n_m = (static_cast<size_t>(max_rows) + kPairRows - 1) / kPairRows;
   const size_t h = 256;
   const size_t f = align256(n_m * sizeof(unsigned long long));
   const size_t g = align256(static_cast<size_t>(max_rows) * r_cap * 2);
+  // one partial 256 x 256 fp32 tile per CTA pair of a full-device launch (stream-K, gemm.cu)
+  w.sk_slots = std::min(kSkMaxClusters, num_sms() / 2);
+  const size_t skf = align256(static_cast<size_t>(kSkMaxClusters) * sizeof(unsigned long long));
+  const size_t skp = static_cast<size_t>(w.sk_slots) * kSkSlotFloats * sizeof(float);
   uint8_t* b = reinterpret_cast<uint8_t*>(base);
   w.epoch = reinterpret_cast<unsigned long long*>(b);
   w.done = reinterpret_cast<unsigned int*>(b ? b + 8 : nullptr);
   w.flags = reinterpret_cast<unsigned long long*>(b ? b + h : nullptr);
   w.gs = reinterpret_cast<__nv_bfloat16*>(b ? b + h + f : nullptr);
   w.hs = reinterpret_cast<__nv_bfloat16*>(b ? b + h + f + g : nullptr);
-  w.bytes = h + f + 2 * g;
+  w.sk_flags = reinterpret_cast<unsigned long long*>(b ? b + h + f + 2 * g : nullptr);
+  w.sk_part = reinterpret_cast<float*>(b ? b + h + f + 2 * g + skf : nullptr);
+  w.bytes = h + f + 2 * g + skf + skp;
   return w;
 }
 
@@ -507,6 +518,26 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
   // one CTA pair (cluster of 2) per tile in flight; grid = #SMs rounded to pairs
   const long long pairs = std::min<long long>(tiles_max, num_sms() / 2);
   const int grid = static_cast<int>(2 * std::max<long long>(pairs, 1));
+  // Stream-K (gemm.cu) where whole tiles quantize badly onto the CTA pairs: the data-parallel
+  // schedule needs ceil(tiles / pairs) rounds of whole tiles, the balanced one (side tiles weighted
+  // kSkSideCostX4 / 4) about (main + side) / pairs.  MUX_SK=0/1 forces it off/on (A/B runs).
+  {
+    const char* sk_e = std::getenv("MUX_SK");  // read per call: tests compare both schedules in one process
+    const int sk_env = (sk_e && *sk_e) ? std::atoi(sk_e) : -1;
+    static const int side_cost_x4 = [] {
+      const char* e = std::getenv("MUX_SK_SIDE_COST_X4");
+      return (e && *e) ? std::atoi(e) : 3;
+    }();
+    const int num_kb = (kred + GemmCfg<false>::kBK - 1) / GemmCfg<false>::kBK;
+    const long long main_tiles = p.has_main ? static_cast<long long>(num_m_max) * num_n : 0;
+    const double ideal = (main_tiles + side_blocks * side_cost_x4 / 4.0) / pairs;
+    const double rounds = static_cast<double>((tiles_max + pairs - 1) / pairs);
+    const bool fits = p.has_main && pairs <= ws.sk_slots && pairs <= kSkMaxClusters && num_kb >= 2;
+    p.sk = fits && (sk_env == 1 || (sk_env < 0 && ideal < 0.85 * rounds)) ? 1 : 0;
+    p.sk_side_cost_x4 = side_cost_x4;
+    p.sk_flags = ws.sk_flags;
+    p.sk_part = ws.sk_part;
+  }
   cudaError_t e = cudaSuccess;
 #ifdef MUX_DEBUG_CHECKS
   e = launch_check_segments(num_segs, seg_off, max_rows, stream);

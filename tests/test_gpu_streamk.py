@@ -1,0 +1,100 @@
+"""Stream-K schedule of the fused GEMM (gemm.cu `for_each_item`, chosen on the host where whole
+256-row x 256-column tiles quantize badly onto the 74 CTA pairs, e.g. 512-column tensor-parallel
+shards; MUX_SK=1 forces it, MUX_SK=0 disables it).  A tile's k-blocks may be split over several
+clusters: the partial accumulators are summed in fp32 by the piece holding k-block 0, which also
+runs the LoRA extension blocks.  With integer inputs every fp32 partial sum is exact, so the split
+schedule must equal both the fp64 oracle and the data-parallel schedule BIT FOR BIT; with normal
+inputs it stays within the north_star tolerance.  Covers: narrow (128-column) tiles, ragged K/N,
+straddling tasks, many contributors per tile (a 256-row problem spread over every cluster), forward
+and backward (dX), and the whole linear/fused-reduce-scatter GPU suites re-run under MUX_SK=1."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from gpu_harness import Problem, compare, TOL  # noqa: E402
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _with_sk(mode, fn):
+    old = os.environ.get("MUX_SK")
+    os.environ["MUX_SK"] = str(mode)
+    try:
+        return fn()
+    finally:
+        if old is None:
+            del os.environ["MUX_SK"]
+        else:
+            os.environ["MUX_SK"] = old
+
+
+def _same(a, b):
+    for k in ("Y", "Hs", "dX"):
+        assert np.array_equal(a[k], b[k]), k
+    for k in ("dA", "dB"):
+        for x, y in zip(a[k], b[k]):
+            assert (x is None and y is None) or np.array_equal(x, y), k
+
+
+CASES = [
+    # K, N, segment rows, ranks
+    (4096, 256, [256], [16]),                       # one tile over every cluster: ~40 partials per tile
+    (512, 512, [64, 128, 64, 192, 256], [8, 16, 32, 64]),   # straddling tasks, short reduction
+    (1376, 328, [128, 64, 320], [16, 4, 48]),       # K, N multiples of 8 only: ragged k-block and tile
+    (2048, 128, [512, 256, 256], [8, 64, 16]),      # narrow (256 x 128) tiles
+    (256, 1024, [192, 64], [32, 8]),                # few k-blocks per tile
+]
+
+
+@pytest.mark.parametrize("case", range(len(CASES)))
+def test_streamk_integer_bit_exact(case):
+    K, N, segs, ranks = CASES[case]
+    scales = [float(1 + t % 2) for t in range(len(ranks))]
+    prob = Problem(K, N, segs, ranks, variant="int", scales=scales, seed=700 + case)
+    ref = prob.run_oracle()
+    sk = _with_sk(1, prob.run_gpu)
+    compare(prob, sk, ref, exact=True)
+    dp = _with_sk(0, prob.run_gpu)
+    _same(sk, dp)
+
+
+@pytest.mark.parametrize("case", range(len(CASES)))
+def test_streamk_normal_within_tolerance(case):
+    K, N, segs, ranks = CASES[case]
+    prob = Problem(K, N, segs, ranks, seed=800 + case)
+    errs = compare(prob, _with_sk(1, prob.run_gpu), prob.run_oracle())
+    assert max(errs.values()) <= TOL, errs
+
+
+def test_streamk_auto_at_tp8_shard_shape():
+    """Config-4 q/k/v column shard at TP 8 (K = 4096 -> N = 512, 16 tasks, ~21.5k rows): the host picks
+    stream-K by itself; sampled rows of Y/dX and all adapter gradients within tolerance."""
+    rng = np.random.default_rng(5)
+    segs = [int(x) * 64 for x in rng.integers(18, 24, size=16)]
+    ranks = [(8, 16, 32, 64)[t % 4] for t in range(16)]
+    prob = Problem(4096, 512, segs, ranks, seed=900)
+    R = prob.R
+    rows = np.unique(np.concatenate([np.arange(0, 64), np.arange(R - 64, R),
+                                     rng.integers(0, R, size=256)])).astype(np.int64)
+    gpu = prob.run_gpu()
+    ref = prob.run_oracle(rows=rows)
+    errs = compare(prob, gpu, ref, rows=rows)
+    assert max(errs.values()) <= TOL, errs
+
+
+def test_linear_and_rs_suites_under_forced_streamk():
+    env = dict(os.environ, MUX_SK="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu",
+                        os.path.join(HERE, "test_gpu_linear.py"), os.path.join(HERE, "test_gpu_rs.py"),
+                        "-k", "not debug_build"],
+                       capture_output=True, text=True, env=env, cwd=os.path.dirname(HERE), timeout=1500)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
