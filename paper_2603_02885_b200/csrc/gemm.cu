@@ -181,7 +181,8 @@ __device__ __forceinline__ Tile tile_at(int t, int num_m, int num_n, int group_m
 // ---- stream-K (p.sk): balance the main tiles' k-block units over the clusters.
 // Every cluster first runs its shrink (side) tiles, round-robin as in the data-parallel schedule;
 // then one contiguous range of main-tile k-block units [b[c], b[c+1]) in tile-major order
-// (tile = m * num_n + n, k fastest), sized so that every cluster's side + main work is equal (a
+// (tile = n * num_m + m, k fastest: the clusters' ranges advance in lockstep, so the pairs working
+// at the same moment cover one stretch of row blocks under every output tile and share it in L2), sized so that every cluster's side + main work is equal (a
 // side tile's k-block counts sk_side_cost_x4 / 4 main k-blocks).  A range that starts inside a
 // tile computes a partial accumulator (k-blocks [k0, k1) of that tile) into cluster c's slot of
 // sk_part and publishes it on sk_flags[c]; the piece holding k-block 0 of a tile — at the END of
@@ -209,7 +210,7 @@ __device__ void sk_compute_bounds(const GemmParams& p, int num_m, int num_n, int
 struct SkPiece {
   int k0, k1;   // k-block range of the piece
   bool fin;     // holds k-block 0: runs the extension blocks, adds the partials, stores the tile
-  int tile;     // main tile index (m * num_n + n), stream-K only
+  int tile;     // main tile index (n * num_m + m), stream-K only
 };
 
 // Every role walks the same item sequence: f(tile, piece).
@@ -229,8 +230,8 @@ __device__ __forceinline__ void for_each_item(const GemmParams& p, int cid, int 
     const int tile = u / num_kb;
     const int k0 = u - tile * num_kb;
     const int k1 = min(num_kb, end - tile * num_kb);
-    const int m = tile / num_n;
-    f(Tile{m, tile - m * num_n, false}, SkPiece{k0, k1, k0 == 0, tile});
+    const int n = tile / num_m;   // row block fastest: the clusters running at the same time share
+    f(Tile{tile - n * num_m, n, false}, SkPiece{k0, k1, k0 == 0, tile});  // A rows and W tiles in L2
     u = tile * num_kb + k1;
   }
 }

@@ -518,12 +518,15 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
   // one CTA pair (cluster of 2) per tile in flight; grid = #SMs rounded to pairs
   const long long pairs = std::min<long long>(tiles_max, num_sms() / 2);
   const int grid = static_cast<int>(2 * std::max<long long>(pairs, 1));
-  // Stream-K (gemm.cu) where whole tiles quantize badly onto the CTA pairs: the data-parallel
-  // schedule needs ceil(tiles / pairs) rounds of whole tiles, the balanced one (side tiles weighted
-  // kSkSideCostX4 / 4) about (main + side) / pairs.  MUX_SK=0/1 forces it off/on (A/B runs).
+  // Stream-K (gemm.cu) is built and parity-tested but OFF by default: interleaved A/B on the
+  // tensor-parallel shard shapes it targets (profiles/r02_sk_ab_*.jsonl: 512-column outputs and
+  // 512-deep reductions, 21.5k rows, 16 tasks) has it 5-25 % SLOWER than whole tiles, because the
+  // kernel is bound by the operand feed, not by idle CTA pairs: a last round with a third of the
+  // pairs busy runs those tiles faster, and the split adds partial traffic.  MUX_SK=1 forces it
+  // (tests, A/B); MUX_SK=-1 enables the quantization heuristic (balanced load < 0.85 x rounds).
   {
     const char* sk_e = std::getenv("MUX_SK");  // read per call: tests compare both schedules in one process
-    const int sk_env = (sk_e && *sk_e) ? std::atoi(sk_e) : -1;
+    const int sk_env = (sk_e && *sk_e) ? std::atoi(sk_e) : 0;
     static const int side_cost_x4 = [] {
       const char* e = std::getenv("MUX_SK_SIDE_COST_X4");
       return (e && *e) ? std::atoi(e) : 3;

@@ -205,11 +205,18 @@ def _check_linear(seg_off, seg_task, adapters, X, W, r_cap, K=None, N=None, *, Y
     for i, a in enumerate(adapters):
         if a.rank == 0:
             continue
+        # memoised per adapter object on the tensors it holds (a call with 64 adapters would
+        # otherwise spend more host time here than the GPU spends on a short GEMM)
+        key = (K, N, dev, grads, id(a.A), id(a.B), id(a.dA), id(a.dB),
+               a.A.data_ptr() if a.A is not None else 0, a.B.data_ptr() if a.B is not None else 0)
+        if getattr(a, "_checked", None) == key:
+            continue
         _check_mat(f"adapters[{i}].A", a.A, (a.rank, K), device=dev)
         _check_mat(f"adapters[{i}].B", a.B, (N, a.rank), device=dev, dense=False)
         if grads:
             _check_mat(f"adapters[{i}].dA", a.dA, (a.rank, K), torch.float32, dev)
             _check_mat(f"adapters[{i}].dB", a.dB, (N, a.rank), torch.float32, dev)
+        a._checked = key
 
 
 # ---------------------------------------------------------------- packing
