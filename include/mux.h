@@ -341,6 +341,48 @@ MUX_API mux_status mux_linear_bwd_ag(int32_t num_segs, const int32_t* seg_off, c
                                      size_t workspace_bytes, cudaStream_t stream);
 
 /* ---------------------------------------------------------------------------
+ * Collectives reduced / broadcast inside the NVSwitch (NVLink SHARP, "NVLS";
+ * NEXT-1: the paper offloads the overlapped collectives to NVLink
+ * SHARP so they need only ~8 CTAs).  The caller (e.g. with the CUDA driver's
+ * cuMulticastCreate / cuMulticastBindMem; paper_2603_02885_b200/nvls.py)
+ * gives every rank one copy of a symmetric buffer of world * rows_per_rank *
+ * cols bf16 and of a flag block of mux_nvls_flags_elems() zeroed uint64, both
+ * also bound to a multicast object: uc_* = this rank's copy, mc_* = the
+ * multicast address.  seq numbers the calls on one mux_nvls (1, 2, ...), the
+ * same on all ranks; ctas = CTAs used (0 = 16).  Waits on other ranks obey
+ * MUX_PEER_TIMEOUT_S.  Errors: MUX_ERR_INVALID_ARGUMENT, MUX_ERR_CUDA.
+ *
+ * mux_nvls_reduce_scatter: every rank has written its partial [world *
+ *   rows_per_rank, cols] into uc_buf (stream order: e.g. mux_linear_fwd with Y
+ *   = uc_buf); out [rows_per_rank, cols] (row stride ldo) = the sum over ranks
+ *   of their copies' rows [rank * rows_per_rank, ...), read with
+ *   multimem.ld_reduce (summed in the switch, fp32 accumulation).  Returns
+ *   (in stream order) once every rank has read every copy, so uc_buf may be
+ *   rewritten by the next call.
+ * mux_nvls_all_gather: rows [rows_per_rank, cols] (row stride ld) are stored
+ *   once to the multicast address (multimem.st): afterwards every rank's uc_buf
+ *   holds all ranks' rows.  Waits for the previous call's mux_nvls_release
+ *   on every rank before storing.
+ * mux_nvls_release: this rank is done reading uc_buf of the last all-gather.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  int32_t world;                   /* 1 .. MUX_RS_MAX_WORLD */
+  int32_t rank;
+  int32_t rows_per_rank;
+  uint64_t seq;                    /* > 0, increasing per call */
+  mux_bf16* uc_buf;                /* this rank's copy [world * rows_per_rank][cols] (16-byte aligned) */
+  mux_bf16* mc_buf;                /* multicast address of the buffer */
+  unsigned long long* uc_flags;    /* this rank's copy of the flag block */
+  unsigned long long* mc_flags;    /* multicast address of the flag block */
+} mux_nvls;
+MUX_API size_t mux_nvls_flags_elems(void);
+MUX_API mux_status mux_nvls_reduce_scatter(const mux_nvls* nv, int32_t cols, mux_bf16* out, int64_t ldo,
+                                           int32_t ctas, cudaStream_t stream);
+MUX_API mux_status mux_nvls_all_gather(const mux_nvls* nv, const mux_bf16* rows, int64_t ld, int32_t cols,
+                                       int32_t ctas, cudaStream_t stream);
+MUX_API mux_status mux_nvls_release(const mux_nvls* nv, cudaStream_t stream);
+
+/* ---------------------------------------------------------------------------
  * Decoder-block ops (NEXT-3).  Row-major bf16 matrices with an explicit row
  * stride `ld*` in ELEMENTS (a multiple of 8: 16-byte rows), so q/k/v or
  * gate/up can be column slices of one fused projection output.  fp32 math.

@@ -159,3 +159,7 @@ struct RsReduceParams {
 };
 
 }  // namespace mux
+
+// library-internal (hidden) helpers defined in mux_abi.cu, shared by the other ABI translation units
+mux_status mux_set_error(mux_status st, const char* msg);   // thread-local mux_last_error() message
+unsigned long long mux_peer_wait_ns();                       // MUX_PEER_TIMEOUT_S in ns (0 = none)

@@ -318,6 +318,9 @@ mux_status fill_adapter_maps(GemmParams& p, int32_t num_adapters, const mux_adap
 
 }  // namespace
 
+mux_status mux_set_error(mux_status st, const char* msg) { return fail(st, "%s", msg); }
+unsigned long long mux_peer_wait_ns() { return peer_wait_ns(); }
+
 extern "C" {
 
 const char* mux_last_error(void) { return g_err.c_str(); }

@@ -31,7 +31,8 @@ EXPORTS = ("mux_last_error", "mux_version", "mux_pack_bound_rows", "mux_pack_wor
            "mux_linear_bwd", "mux_linear_bwd_part", "mux_pack_row_start", "mux_attn_fwd", "mux_attn_workspace_size", "mux_attn_bwd",
            "mux_rope", "mux_rmsnorm_fwd", "mux_rmsnorm_bwd", "mux_swiglu_fwd", "mux_swiglu_bwd", "mux_add", "mux_rs_flags_elems", "mux_linear_fwd_rs",
            "mux_linear_bwd_dx_rs", "mux_rs_reduce", "mux_ag_push", "mux_ag_release", "mux_linear_fwd_ag",
-           "mux_linear_bwd_ag", "mux_linear_fwd_hs", "mux_linear_shrink")
+           "mux_linear_bwd_ag", "mux_linear_fwd_hs", "mux_linear_shrink", "mux_nvls_flags_elems",
+           "mux_nvls_reduce_scatter", "mux_nvls_all_gather", "mux_nvls_release")
 
 
 class MuxError(RuntimeError):
@@ -128,6 +129,14 @@ def lib():
         L.mux_linear_fwd_ag.argtypes = [I32, P, P, I32, P, I32, I32, I32, I32, P, P, P, P, P, SZ, P]
         L.mux_linear_bwd_ag.restype = ctypes.c_int
         L.mux_linear_bwd_ag.argtypes = [I32, P, P, I32, P, I32, I32, I32, I32, P, P, P, P, P, P, SZ, P]
+        L.mux_nvls_flags_elems.restype = SZ
+        L.mux_nvls_flags_elems.argtypes = []
+        L.mux_nvls_reduce_scatter.restype = ctypes.c_int
+        L.mux_nvls_reduce_scatter.argtypes = [P, I32, P, I64, I32, P]
+        L.mux_nvls_all_gather.restype = ctypes.c_int
+        L.mux_nvls_all_gather.argtypes = [P, P, I64, I32, I32, P]
+        L.mux_nvls_release.restype = ctypes.c_int
+        L.mux_nvls_release.argtypes = [P, P]
         _lib = L
     return _lib
 
@@ -653,3 +662,43 @@ def linear_bwd_ag(ag: _Rs, seg_off, seg_task, adapters, X, W, Hs, r_cap: int, dX
                                    _ptr(X), _ptr(W), _ptr(Hs), _ptr(dX), _ptr(workspace), workspace.numel(),
                                    _stream(stream)))
     return dX
+
+
+# ---------------------------------------------------------------- NVLS (in-switch) collectives
+class _Nvls(ctypes.Structure):
+    _fields_ = [("world", ctypes.c_int32), ("rank", ctypes.c_int32), ("rows_per_rank", ctypes.c_int32),
+                ("seq", ctypes.c_uint64), ("uc_buf", ctypes.c_void_p), ("mc_buf", ctypes.c_void_p),
+                ("uc_flags", ctypes.c_void_p), ("mc_flags", ctypes.c_void_p)]
+
+
+def make_nvls(world: int, rank: int, rows_per_rank: int, seq: int, uc_buf: int, mc_buf: int, uc_flags: int,
+              mc_flags: int) -> _Nvls:
+    """mux_nvls descriptor (raw device addresses: this rank's copy and the multicast address)."""
+    d = _Nvls()
+    d.world, d.rank, d.rows_per_rank, d.seq = world, rank, rows_per_rank, seq
+    d.uc_buf, d.mc_buf, d.uc_flags, d.mc_flags = uc_buf, mc_buf, uc_flags, mc_flags
+    return d
+
+
+def nvls_flags_elems() -> int:
+    return int(lib().mux_nvls_flags_elems())
+
+
+def nvls_reduce_scatter(nv: _Nvls, out: torch.Tensor, ctas: int = 0, stream=None) -> torch.Tensor:
+    """mux_nvls_reduce_scatter: out [rows_per_rank, cols] = in-switch sum of every rank's rows."""
+    _need(out.dtype == torch.bfloat16 and out.dim() == 2 and out.shape[0] == nv.rows_per_rank,
+          "out must be bf16 [rows_per_rank, cols]")
+    _check(lib().mux_nvls_reduce_scatter(ctypes.byref(nv), out.shape[1], _ptr(out), _ld(out), ctas, _stream(stream)))
+    return out
+
+
+def nvls_all_gather(nv: _Nvls, rows: torch.Tensor, ctas: int = 0, stream=None):
+    """mux_nvls_all_gather: this rank's rows [rows_per_rank, cols] into every rank's copy."""
+    _need(rows.dtype == torch.bfloat16 and rows.dim() == 2 and rows.shape[0] == nv.rows_per_rank,
+          "rows must be bf16 [rows_per_rank, cols]")
+    _check(lib().mux_nvls_all_gather(ctypes.byref(nv), _ptr(rows), _ld(rows), rows.shape[1], ctas, _stream(stream)))
+
+
+def nvls_release(nv: _Nvls, stream=None):
+    """mux_nvls_release: this rank is done reading the last all-gather's buffer."""
+    _check(lib().mux_nvls_release(ctypes.byref(nv), _stream(stream)))

@@ -75,6 +75,42 @@ def all_reduce_(x: torch.Tensor, group=None) -> torch.Tensor:
     return x
 
 
+class NvlsCollectives:
+    """All-gather / reduce-scatter over rows reduced or broadcast inside the NVSwitch (NVLink SHARP,
+    NEXT-1; libmux mux_nvls_*), one multicast-bound buffer per (name, shape).  `ag(name, x_rows)`
+    returns the gathered [R, cols] rows (valid until `release(name)`); `rs_buffer(name, R, cols)` is
+    the [R, cols] buffer a GEMM writes its partial into, `rs(name, out)` reduces it into this rank's
+    rows.  `ctas` caps the CTAs of each collective (P:791-796 uses 8 with NVLink SHARP)."""
+
+    def __init__(self, group=None, ctas: int = 8):
+        self.group, self.ctas = group, ctas
+        self.bufs = {}
+
+    def _get(self, name, rows, cols, device):
+        b = self.bufs.get(name)
+        if b is None or b.rows != rows or b.cols != cols:
+            from .nvls import NvlsBuffer
+            b = self.bufs[name] = NvlsBuffer(self.group, rows, cols, device)
+        return b
+
+    def ag(self, name, x_rows):
+        b = self._get(name, x_rows.shape[0], x_rows.shape[1], x_rows.device)
+        return b.all_gather(x_rows, self.ctas)
+
+    def release(self, name):
+        self.bufs[name].release()
+
+    def rs_buffer(self, name, R, cols, device):
+        p = dist.get_world_size(self.group) if dist.is_initialized() else 1
+        return self._get(name, R // p, cols, device).uc
+
+    def rs(self, name, out=None):
+        b = self.bufs[name]
+        if out is None:
+            out = torch.empty(b.rows, b.cols, dtype=torch.bfloat16, device=b.uc.device)
+        return b.reduce_scatter(out, self.ctas)
+
+
 class FusedRs:
     """Receive buffers and flags of mux's fused GEMM -> reduce-scatter, allocated with torch
     symmetric memory (every rank maps every rank's buffers over NVLink)."""
@@ -134,9 +170,10 @@ class MuxBackend:
         n = self.mux.linear_workspace_size(len(seg_task), R, K, W.shape[0], r_cap)
         return self._buf(("ws", W.data_ptr()), (n,), torch.uint8, X.device, zero=True)
 
-    def fwd(self, seg_off, seg_task, adapters, X, W, r_cap):
+    def fwd(self, seg_off, seg_task, adapters, X, W, r_cap, Y=None):
         R = X.shape[0]
-        Y = self._buf(("Y", W.data_ptr()), (R, W.shape[0]), torch.bfloat16, X.device)
+        if Y is None:
+            Y = self._buf(("Y", W.data_ptr()), (R, W.shape[0]), torch.bfloat16, X.device)
         Hs = self._buf(("Hs", W.data_ptr()), (R, r_cap), torch.bfloat16, X.device)
         return self.mux.linear_fwd(seg_off, seg_task, adapters, X, W, r_cap, Y=Y, Hs=Hs,
                                    workspace=self._ws(W, X, seg_task, r_cap))
@@ -153,8 +190,9 @@ class MuxBackend:
         return self.mux.linear_fwd_hs(seg_off, seg_task, adapters, X, W, Hs, r_cap, Y=Y,
                                       workspace=self._ws(W, X, seg_task, r_cap))
 
-    def bwd(self, seg_off, seg_task, adapters, dY, X, W, Hs, r_cap):
-        dX = self._buf(("dX", W.data_ptr()), tuple(X.shape), torch.bfloat16, X.device)
+    def bwd(self, seg_off, seg_task, adapters, dY, X, W, Hs, r_cap, dX=None):
+        if dX is None:
+            dX = self._buf(("dX", W.data_ptr()), tuple(X.shape), torch.bfloat16, X.device)
         dX = self.mux.linear_bwd(seg_off, seg_task, adapters, dY, X, W, Hs, r_cap, dX=dX,
                                  workspace=self._ws(W, X, seg_task, r_cap))
         return dX, [a.dA for a in adapters], [a.dB for a in adapters]
@@ -183,8 +221,8 @@ class MuxBackend:
     def swiglu_bwd(self, dh, g, u):
         return self.mux.swiglu_bwd(dh, g, u)
 
-    def add(self, a, b):
-        return self.mux.add(a, b)
+    def add(self, a, b, out=None):
+        return self.mux.add(a, b, y=out)
 
     # fused GEMM -> reduce-scatter (peer stores + owner-side sum; see FusedRs)
     rs_exchange = None  # optional buffer-mapping hook for FusedRs (default: symmetric memory)
@@ -314,15 +352,25 @@ class ColumnParallelMuxLinear:
     computes the shrink itself."""
 
     def __init__(self, backend, W_shard, adapters_shard, r_cap, group=None, fused_rs=False, fused_ag=False,
-                 shared_shrink=False):
+                 shared_shrink=False, nvls=None):
         self.be, self.W, self.ads, self.r_cap, self.group = backend, W_shard, adapters_shard, r_cap, group
         self.fused_rs, self.fused_ag, self.shared_shrink = fused_rs, fused_ag, shared_shrink
+        self.nvls = nvls    # NvlsCollectives: AG(X) and RS(dX) inside the NVSwitch
         self._rs = self._ag = self._ag_held = self._ag_pushed = None
+        self._nvls_held = False
 
     def forward(self, seg_off, seg_task, x_rows):
         """x_rows [R/p, K] (this rank's row block) -> Y_p [R, N/p]."""
         if self.fused_ag:
             Y, self.Hs, self.X = self.be.fwd_ag(self, seg_off, seg_task, x_rows)
+            return Y
+        if self.nvls is not None:
+            if self._nvls_held:
+                raise RuntimeError("nvls: forward called again before the backward of the previous call; "
+                                   "call release_ag() first for forward-only use")
+            self.X = self.nvls.ag(("ag", id(self)), x_rows)
+            self._nvls_held = True
+            Y, self.Hs = self.be.fwd(seg_off, seg_task, self.ads, self.X, self.W, self.r_cap)
             return Y
         self.X = all_gather_rows(x_rows, self.group)
         if self.shared_shrink:
@@ -355,6 +403,13 @@ class ColumnParallelMuxLinear:
         """dY_p [R, N/p] -> dX rows [R/p, K]; dA_t all-reduced, dB_{t,p} local."""
         if self.fused_rs:
             dX_rows, dA, dB = self.be.bwd_rs(self, seg_off, seg_task, dY_cols)
+        elif self.nvls is not None:   # the partial dX goes straight into the multicast-bound buffer
+            R, K = self.X.shape
+            buf = self.nvls.rs_buffer(("rs", id(self)), R, K, self.X.device)
+            _, dA, dB = self.be.bwd(seg_off, seg_task, self.ads, dY_cols, self.X, self.W, self.Hs, self.r_cap,
+                                    dX=buf)
+            self.release_ag()
+            dX_rows = self.nvls.rs(("rs", id(self)))
         else:
             dXp, dA, dB = self.be.bwd(seg_off, seg_task, self.ads, dY_cols, self.X, self.W, self.Hs, self.r_cap)
             dX_rows = None
@@ -367,6 +422,9 @@ class ColumnParallelMuxLinear:
 
     def release_ag(self):
         """The gathered X is no longer needed (after the backward): its owners may push again."""
+        if self._nvls_held:
+            self.nvls.release(("ag", id(self)))
+            self._nvls_held = False
         if self._ag_held is not None:
             if self._ag_pushed is not None:   # the pushed source rows may be rewritten after this point
                 torch.cuda.current_stream().wait_event(self._ag_pushed)
@@ -376,9 +434,11 @@ class ColumnParallelMuxLinear:
 
 
 class RowParallelMuxLinear:
-    def __init__(self, backend, W_shard, adapters_shard, r_cap, group=None, fused_rs=False, fused_ag=False):
+    def __init__(self, backend, W_shard, adapters_shard, r_cap, group=None, fused_rs=False, fused_ag=False,
+                 nvls=None):
         self.be, self.W, self.ads, self.r_cap, self.group = backend, W_shard, adapters_shard, r_cap, group
         self.fused_rs, self.fused_ag = fused_rs, fused_ag
+        self.nvls = nvls    # NvlsCollectives: RS(Y) and AG(dY) inside the NVSwitch
         self._rs = self._ag = None
 
     def forward(self, seg_off, seg_task, x_cols):
@@ -387,6 +447,10 @@ class RowParallelMuxLinear:
         if self.fused_rs:
             Y_rows, self.Hs = self.be.fwd_rs(self, seg_off, seg_task, x_cols)
             return Y_rows
+        if self.nvls is not None:     # the partial Y goes straight into the multicast-bound buffer
+            buf = self.nvls.rs_buffer(("rs", id(self)), x_cols.shape[0], self.W.shape[0], x_cols.device)
+            _, self.Hs = self.be.fwd(seg_off, seg_task, self.ads, x_cols, self.W, self.r_cap, Y=buf)
+            return self.nvls.rs(("rs", id(self)))
         Yp, self.Hs = self.be.fwd(seg_off, seg_task, self.ads, x_cols, self.W, self.r_cap)
         return reduce_scatter_rows(Yp, self.group)
 
@@ -394,6 +458,10 @@ class RowParallelMuxLinear:
         """dY rows [R/p, N] -> dX_p [R, K/p]; dB_t all-reduced, dA_{t,p} local."""
         if self.fused_ag:
             dXp, dA, dB = self.be.bwd_ag(self, seg_off, seg_task, dy_rows)
+        elif self.nvls is not None:
+            dY = self.nvls.ag(("ag", id(self)), dy_rows)
+            dXp, dA, dB = self.be.bwd(seg_off, seg_task, self.ads, dY, self.X, self.W, self.Hs, self.r_cap)
+            self.nvls.release(("ag", id(self)))
         else:
             dY = all_gather_rows(dy_rows, self.group)
             dXp, dA, dB = self.be.bwd(seg_off, seg_task, self.ads, dY, self.X, self.W, self.Hs, self.r_cap)

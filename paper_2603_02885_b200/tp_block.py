@@ -68,12 +68,29 @@ class TPDecoderBlock:
     with the same op methods (fwd/bwd linears + rmsnorm/rope/attention/swiglu/add)."""
 
     def __init__(self, backend, shape: TPBlockShape, weights: Dict[str, torch.Tensor],
-                 adapters: Dict[str, List], r_cap: int, group=None):
-        self.be, self.s, self.w, self.r_cap, self.group = backend, shape, weights, r_cap, group
+                 adapters: Dict[str, List], r_cap: int, group=None, nvls=None):
+        """nvls: a tp.NvlsCollectives — every all-gather / reduce-scatter of the block inside the
+        NVSwitch (NVLink SHARP) instead of NCCL."""
+        self.be, self.s, self.w, self.r_cap, self.group, self.nvls = backend, shape, weights, r_cap, group, nvls
         self.lin = {}
         for name in LINEARS:
             cls = tp.ColumnParallelMuxLinear if name in COLUMN else tp.RowParallelMuxLinear
-            self.lin[name] = cls(backend, weights[name], adapters[name], r_cap, group=group)
+            self.lin[name] = cls(backend, weights[name], adapters[name], r_cap, group=group,
+                                 nvls=nvls if name in ROW else None)
+
+    def _ag(self, name, rows):
+        return self.nvls.ag(name, rows) if self.nvls is not None else tp.all_gather_rows(rows, self.group)
+
+    def _rs_sum(self, name, parts):
+        """reduce-scatter over rows of the sum of this rank's partials (one collective for the layers
+        that shared an input); with NVLS the last add writes straight into the multicast buffer."""
+        out = None
+        if self.nvls is not None:
+            out = self.nvls.rs_buffer(name, parts[0].shape[0], parts[0].shape[1], parts[0].device)
+        acc = parts[0]
+        for i, x in enumerate(parts[1:]):
+            acc = self.be.add(acc, x, out=out if i == len(parts) - 2 else None)
+        return self.nvls.rs(name) if self.nvls is not None else tp.reduce_scatter_rows(acc, self.group)
 
     # ------------------------------------------------------------------ forward
     def forward(self, x_rows, seg_off, seg_task, row_start):
@@ -82,7 +99,7 @@ class TPDecoderBlock:
         self.seg_off, self.seg_task, self.row_start = seg_off, list(seg_task), row_start
         st = self.seg_task
         self.x_rows = x_rows
-        h1 = tp.all_gather_rows(be.rmsnorm_fwd(x_rows, self.w["norm1"], s.eps), self.group)
+        h1 = self._ag("h1", be.rmsnorm_fwd(x_rows, self.w["norm1"], s.eps))
         q = lin["q"].forward_full(seg_off, st, h1)
         k = lin["k"].forward_full(seg_off, st, h1)
         v = lin["v"].forward_full(seg_off, st, h1)
@@ -91,7 +108,7 @@ class TPDecoderBlock:
         a, lse = be.attn_fwd(q, k, v, row_start, hq, hkv, s.head_dim ** -0.5)
         o_rows = lin["o"].forward(seg_off, st, a)                       # RS inside
         h2_rows, x2_rows = be.rmsnorm_fwd(o_rows, self.w["norm2"], s.eps, res=x_rows)
-        h2 = tp.all_gather_rows(h2_rows, self.group)
+        h2 = self._ag("h2", h2_rows)
         g = lin["gate"].forward_full(seg_off, st, h2)
         u = lin["up"].forward_full(seg_off, st, h2)
         m = be.swiglu_fwd(g, u)
@@ -106,17 +123,21 @@ class TPDecoderBlock:
         so, st = self.seg_off, self.seg_task
         dm, _, _ = lin["down"].backward(so, st, dy_rows)                 # AG(dy) inside; AR(dB)
         dg, du = be.swiglu_bwd(dm, sv["g"], sv["u"])
-        dh2 = be.add(lin["gate"].backward_partial(so, st, dg)[0], lin["up"].backward_partial(so, st, du)[0])
-        dh2_rows = tp.reduce_scatter_rows(dh2, self.group)
+        dh2_rows = self._rs_sum("dh2", [lin["gate"].backward_partial(so, st, dg)[0],
+                                        lin["up"].backward_partial(so, st, du)[0]])
+        if self.nvls is not None:
+            self.nvls.release("h2")          # gate/up backward were the last readers of the gathered h2
         dx2_rows = be.rmsnorm_bwd(dh2_rows, sv["x2_rows"], self.w["norm2"], s.eps, resid=dy_rows)
         da, _, _ = lin["o"].backward(so, st, dx2_rows)                   # AG(dx2) inside; AR(dB)
         dq, dk, dv = be.attn_bwd(da, sv["q"], sv["k"], sv["v"], sv["a"], sv["lse"], self.row_start, hq, hkv,
                                  s.head_dim ** -0.5)
         dq = be.rope(dq, self.row_start, hq, s.head_dim, s.rope_base, inverse=True)
         dk = be.rope(dk, self.row_start, hkv, s.head_dim, s.rope_base, inverse=True)
-        dh1 = be.add(lin["q"].backward_partial(so, st, dq)[0], lin["k"].backward_partial(so, st, dk)[0])
-        dh1 = be.add(dh1, lin["v"].backward_partial(so, st, dv)[0])
-        dh1_rows = tp.reduce_scatter_rows(dh1, self.group)
+        dh1_rows = self._rs_sum("dh1", [lin["q"].backward_partial(so, st, dq)[0],
+                                        lin["k"].backward_partial(so, st, dk)[0],
+                                        lin["v"].backward_partial(so, st, dv)[0]])
+        if self.nvls is not None:
+            self.nvls.release("h1")
         return be.rmsnorm_bwd(dh1_rows, self.x_rows, self.w["norm1"], s.eps, resid=dx2_rows)
 
     def adapter_grads(self):
