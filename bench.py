@@ -610,29 +610,39 @@ def timed_backend_cls(tp, torch):
         record = None
         task_tokens = None
 
-        def _flops(self, ads, K, N):
-            return sum(Tt * (2 * K * N + 2 * a.rank * (K + N)) for Tt, a in zip(self.task_tokens, ads))
+        def _flops(self, ads, K, N, col_off=None):
+            if col_off is None:
+                return sum(Tt * (2 * K * N + 2 * a.rank * (K + N)) for Tt, a in zip(self.task_tokens, ads))
+            # fused projection: adapters[t][s] on column slices
+            w = [col_off[i + 1] - col_off[i] for i in range(len(col_off) - 1)]
+            return sum(Tt * sum(2 * K * n + 2 * a.rank * (K + n) for a, n in zip(row, w))
+                       for Tt, row in zip(self.task_tokens, ads))
 
-        def _timed(self, fn, flops, *a):
+        def _timed(self, fn, flops, *a, **kw):
             if self.record is None:
-                return fn(*a)
+                return fn(*a, **kw)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            out = fn(*a)
+            out = fn(*a, **kw)
             e1.record()
             self.record.append((e0, e1, flops))
             return out
 
-        def fwd(self, seg_off, seg_task, ads, X, W, r_cap):
-            return self._timed(super().fwd, self._flops(ads, X.shape[1], W.shape[0]), seg_off, seg_task, ads, X, W,
-                               r_cap)
+        def fwd(self, seg_off, seg_task, ads, X, W, r_cap, Y=None, col_off=None):
+            return self._timed(super().fwd, self._flops(ads, X.shape[1], W.shape[0], col_off), seg_off, seg_task,
+                               ads, X, W, r_cap, Y=Y, col_off=col_off)
+
+        def fwd_hs(self, seg_off, seg_task, ads, X, W, Hs, r_cap, col_off=None):
+            return self._timed(super().fwd_hs, self._flops(ads, X.shape[1], W.shape[0], col_off), seg_off, seg_task,
+                               ads, X, W, Hs, r_cap, col_off=col_off)
 
         def fwd_rs(self, lay, seg_off, seg_task, X):
             return self._timed(super().fwd_rs, self._flops(lay.ads, X.shape[1], lay.W.shape[0]), lay, seg_off,
                                seg_task, X)
 
         def fwd_ag(self, lay, seg_off, seg_task, x_rows):
-            return self._timed(super().fwd_ag, self._flops(lay.ads, x_rows.shape[1], lay.W.shape[0]), lay, seg_off,
+            return self._timed(super().fwd_ag, self._flops(lay.ads, x_rows.shape[1], lay.W.shape[0],
+                                                           getattr(lay, "col_off", None)), lay, seg_off,
                                seg_task, x_rows)
     return TimedMuxBackend
 
@@ -766,31 +776,37 @@ def _tp_block(args, w, torch, mux, tp, Backend, world, rank):
     seed = wl.seed
     r_cap = 16 * -(-max(wl.ranks) // 16)
     mk = lambda A, B, r, sc: mux.Adapter(A, B, r, sc)  # noqa: E731
-    Wp, ap = {}, {}
+    Wfull, afull = {}, {}
     for li, L in enumerate(wl.linears):
         n = L.name
-        W = _gen(torch, seed * 97 + li, (L.N, L.K), (0.5 if n in ("q", "k") else 1.0) * L.K ** -0.5)
-        ads = []
+        Wfull[n] = _gen(torch, seed * 97 + li, (L.N, L.K), (0.5 if n in ("q", "k") else 1.0) * L.K ** -0.5)
+        afull[n] = []
         for t in range(w.M):
             r = wl.ranks[t]
             B = _gen(torch, seed * 131 + li * 1000 + t, (L.N, r), r ** -0.5)
             A = _gen(torch, seed * 137 + li * 1000 + t, (r, L.K), L.K ** -0.5)
-            ads.append(mux.Adapter(A, B, r, wl.scales[t]))
-        fn = tp.shard_column if n in tp_block.COLUMN else tp.shard_row
-        Wp[n], sh_ads = fn(W, ads, world, rank, mk)
-        ap[n] = []
-        for a in sh_ads:    # B rows need 16-byte alignment: copy into padded storage
-            Bs = mux.make_B_storage(a.B.shape[0], a.rank)
-            Bs.copy_(a.B)
-            ap[n].append(mux.Adapter(a.A.contiguous(), Bs, a.rank, a.scale))
-        del W, ads
+            afull[n].append(mux.Adapter(A, B, r, wl.scales[t]))
+
+    def padded(a):      # B rows need 16-byte alignment: copy into padded storage
+        Bs = mux.make_B_storage(a.B.shape[0], a.rank)
+        Bs.copy_(a.B)
+        return mux.Adapter(a.A.contiguous(), Bs, a.rank, a.scale)
+    col_off = None
+    if args.fused_proj:     # q|k|v and gate|up as one column-sliced GEMM each
+        Wp, ap, col_off = tp_block.shard_block_fused(Wfull, afull, world, rank, mk)
+        ap = {n: [[padded(a) for a in row] if isinstance(row, list) else padded(row) for row in v]
+              for n, v in ap.items()}
+    else:
+        Wp, ap = tp_block.shard_block(Wfull, afull, world, rank, mk)
+        ap = {n: [padded(a) for a in v] for n, v in ap.items()}
+    del Wfull, afull
     for i in (1, 2):
         Wp[f"norm{i}"] = (1.0 + 0.1 * torch.randn(hidden, device="cuda",
                                                    generator=torch.Generator(device="cuda").manual_seed(seed + i))
                           ).bfloat16()
     be = Backend()
     be.task_tokens = list(w.task_tokens)
-    blk = tp_block.TPDecoderBlock(be, shape, Wp, ap, r_cap)
+    blk = tp_block.TPDecoderBlock(be, shape, Wp, ap, r_cap, col_off=col_off, shared_shrink=args.shared_shrink)
     i32 = dict(dtype=torch.int32, device="cuda")
     tso, sl = torch.tensor(w.off, **i32), torch.tensor(w.lens, **i32)
     cap = torch.tensor(w.cap, **i32) if w.cap else None
@@ -833,9 +849,13 @@ def _tp_block(args, w, torch, mux, tp, Backend, world, rank):
     attn_flops = 12 * 128 * heads * pairs
     desc = {"parallelism": f"tp{world} decoder block (column q/k/v/gate/up, head-sharded attention, row o/down; "
                            "sequence-parallel RMSNorm/residuals; 8 NCCL AG/RS per step)",
+            "fused_projections": ("q|k|v and gate|up as one column-sliced GEMM each (per-slice adapters)"
+                                  if args.fused_proj else None),
+            "shared_shrink": bool(args.shared_shrink),
             "hidden": hidden, "ffn": ffn, "heads": heads, "kv_heads": kv_heads, "max_rows": max_rows,
             "attention_flops": attn_flops}
-    launches = 4 + tp_block.TPDecoderBlock.LAUNCHES_FWD + tp_block.TPDecoderBlock.LAUNCHES_BWD
+    lf, lb = blk.launches()
+    launches = 4 + lf + lb + (2 if args.shared_shrink else 0)
     return step, launches, h2d, result_tensors, desc, [be]
 
 
@@ -1170,6 +1190,11 @@ def main():
     ap.add_argument("--htasks", type=int, default=1,
                     help="--mode tp: hTasks interleaved by Alg. 1 (NEXT-1); 0 = chosen by the planner (NEXT-4)")
     ap.add_argument("--comm-ctas", type=int, default=0, help="--mode tp: NCCL_MAX_CTAS for the overlapped collectives")
+    ap.add_argument("--fused-proj", type=int, default=1, choices=(0, 1),
+                    help="--mode tp, configs 4/5: q|k|v and gate|up as one column-sliced GEMM each (1, default) "
+                         "or seven separate linears (0)")
+    ap.add_argument("--shared-shrink", action="store_true",
+                    help="--mode tp, configs 4/5: column layers shrink only their own rows and all-gather Hs")
     ap.add_argument("--fused-rs", action="store_true",
                     help="--mode tp: reduce-scatters fused into the GEMMs (peer stores via symmetric memory)")
     ap.add_argument("--fused-ag", action="store_true",

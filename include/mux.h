@@ -70,6 +70,8 @@ typedef uint16_t mux_bf16;
 #define MUX_MAX_ADAPTERS 64
 #define MUX_RS_MAX_WORLD 8    /* ranks of a fused reduce-scatter (one 8-GPU NVSwitch box) */
 #define MUX_MAX_RANK 64        /* LoRA ranks up to 64 in the paper's workloads */
+#define MUX_MAX_SLICES 4       /* column slices of one fused projection (q|k|v, gate|up) */
+#define MUX_MAX_ADAPTER_SLOTS 96  /* num_adapters * num_slices per call (kernel parameter block) */
 
 typedef enum {
   MUX_OK = 0,
@@ -339,6 +341,73 @@ MUX_API mux_status mux_linear_bwd_ag(int32_t num_segs, const int32_t* seg_off, c
                                      int32_t K, int32_t N, int32_t r_cap, const mux_ag* ag, const mux_bf16* X,
                                      const mux_bf16* W, const mux_bf16* Hs, mux_bf16* dX, void* workspace,
                                      size_t workspace_bytes, cudaStream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * Fused projections with one adapter per column slice (q|k|v, gate|up).
+ * P:296 names "attaching adapters to the fused qkv projection" as what keeps
+ * per-projection LoRA from running on one fused backbone op; here the backbone
+ * W = [W_0; W_1; ...] (rows = output columns) runs as ONE GEMM while every
+ * task keeps an independent adapter (A_{t,s}, B_{t,s}, rank, scale) on each
+ * slice s = output columns [col_off[s], col_off[s+1]).  By definition this is
+ * num_slices independent LoRA linears sharing X, computed together:
+ *   fwd:  Y[i, slice s] = X[i,:] W_s^T + s_{t,s} (X[i,:] A_{t,s}^T) B_{t,s}^T
+ *         Hs[i, s*r_cap + j] = bf16(s_{t,s} X[i,:] A_{t,s}[j,:]^T)   (Hs [max_rows, S*r_cap])
+ *   bwd:  Gs_s = bf16(s_{t,s} dY[i, slice s] B_{t,s})
+ *         dX[i,:] = dY[i,:] W + sum_s Gs_s[i,:] A_{t,s}
+ *         dA_{t,s} = sum over t's rows Gs_s^T X;  dB_{t,s} = sum dY[:, slice s]^T Hs_s
+ * With num_slices = 1 (or slices = NULL) every op equals the per-call entry
+ * points above bit for bit.  Adapters are indexed task-major:
+ * adapters[t * num_slices + s]; B_{t,s} is [col_off[s+1] - col_off[s], rank]
+ * (leading dimension ldb) and dB_{t,s} likewise; rank 0 = no adapter on that
+ * slice.  Within one task, a non-finite value in one slice's adapter can reach
+ * that task's other slices where a 256-column output tile straddles two
+ * slices (the kernel multiplies it by the zero rows outside the slice); it
+ * never reaches another task's rows.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  int32_t num_slices;                    /* 1 .. MUX_MAX_SLICES */
+  int32_t col_off[MUX_MAX_SLICES + 1];   /* 0 = col_off[0] < ... < col_off[S] = N, multiples of 8 */
+} mux_slices;
+
+typedef enum {
+  MUX_OP_FWD = 1,        /* mux_linear_fwd (rs != NULL: mux_linear_fwd_rs; ag != NULL: mux_linear_fwd_ag) */
+  MUX_OP_FWD_HS = 2,     /* mux_linear_fwd_hs (Hs is the input) */
+  MUX_OP_SHRINK = 3,     /* mux_linear_shrink over [row_begin, row_end) */
+  MUX_OP_BWD = 4,        /* mux_linear_bwd (ag != NULL: mux_linear_bwd_ag) */
+  MUX_OP_BWD_DX = 5,     /* mux_linear_bwd_part(MUX_BWD_DX) (rs != NULL: mux_linear_bwd_dx_rs) */
+  MUX_OP_BWD_GRADS = 6   /* mux_linear_bwd_part(MUX_BWD_GRADS) */
+} mux_linear_op;
+
+/* All arguments of one linear call; fields an op does not use are ignored
+ * (set them to 0/NULL).  Pointers as in the per-op entry points. */
+typedef struct {
+  int32_t op;                        /* mux_linear_op */
+  int32_t num_segs;
+  const int32_t* seg_off;            /* device [num_segs + 1] */
+  const int32_t* seg_task;           /* [host] [num_segs] task index */
+  int32_t num_adapters;              /* tasks (1..64); num_adapters * num_slices <= MUX_MAX_ADAPTER_SLOTS */
+  const mux_adapter* adapters;       /* [host] [num_adapters * num_slices], task-major */
+  const mux_slices* slices;          /* [host] NULL = one slice over all N columns */
+  int32_t max_rows, K, N, r_cap;     /* r_cap: per slice, >= every rank */
+  const mux_bf16* X;                 /* [max_rows, K] (fwd input; bwd: for dA) */
+  const mux_bf16* W;                 /* [N, K] */
+  const mux_bf16* dY;                /* [max_rows, N] (bwd) */
+  mux_bf16* Y;                       /* [max_rows, N] (fwd output) */
+  mux_bf16* Hs;                      /* [max_rows, S * r_cap]: fwd/shrink output (fwd: NULL = workspace),
+                                        fwd_hs / bwd input */
+  mux_bf16* dX;                      /* [max_rows, K] (bwd output, NULL = skip) */
+  int32_t row_begin, row_end;        /* MUX_OP_SHRINK row range */
+  const mux_rs* rs;                  /* optional fused reduce-scatter (FWD, BWD_DX) */
+  const mux_ag* ag;                  /* optional fused all-gather (FWD: X, BWD: dY) */
+  void* workspace;                   /* >= mux_linear_workspace_size(num_segs, max_rows, K, N, S * r_cap) */
+  size_t workspace_bytes;
+  cudaStream_t stream;
+} mux_linear_args;
+
+/* One linear call described by `a` (the per-op entry points above are this
+ * with slices = NULL).  Errors as mux_linear_fwd, plus MUX_ERR_INVALID_ARGUMENT
+ * for an unknown op, a bad slice table or too many adapter slots. */
+MUX_API mux_status mux_linear(const mux_linear_args* a);
 
 /* ---------------------------------------------------------------------------
  * Collectives reduced / broadcast inside the NVSwitch (NVLink SHARP, "NVLS";

@@ -126,3 +126,47 @@ def linear_bwd(seg_off, seg_task, A_list, B_list, ranks, scales, dY, X, W, r_cap
                                  _ptr(dX), _ptr(Gs))
     assert rc == 0
     return dX, Gs, grads
+
+
+# ---------------------------------------------------------------- fused projections (column slices)
+def linear_fwd_sliced(seg_off, seg_task, col_off, A, B, ranks, scales, X, W, r_cap, rows=None):
+    """A fused projection = one independent LoRA linear per column slice s (include/mux.h, "Fused
+    projections"; P:296 on attaching adapters to the fused qkv projection): for slice s,
+    Y[:, col_off[s]:col_off[s+1]] = X W_s^T + s_{t,s} (X A_{t,s}^T) B_{t,s}^T with W_s the slice's
+    rows of W.  A/B/ranks/scales are indexed [t][s].  Returns (Y, Hs) with Hs [R, S * r_cap]
+    (slice s in columns [s * r_cap, (s + 1) * r_cap)) — the definition written out: one
+    linear_fwd per slice, concatenated."""
+    Wd = widen(W)
+    S = len(col_off) - 1
+    Ys, Hss = [], []
+    for s in range(S):
+        c0, c1 = col_off[s], col_off[s + 1]
+        Y_s, Hs_s = linear_fwd(seg_off, seg_task, [a[s] for a in A], [b[s] for b in B], [r[s] for r in ranks],
+                               [c[s] for c in scales], X, Wd[c0:c1], r_cap, rows=rows)
+        Ys.append(Y_s)
+        Hss.append(Hs_s)
+    return np.concatenate(Ys, axis=1), np.concatenate(Hss, axis=1)
+
+
+def linear_bwd_sliced(seg_off, seg_task, col_off, A, B, ranks, scales, dY, X, W, r_cap, rows=None):
+    """Backward of linear_fwd_sliced: slice s sees dY's columns of the slice; dX is the sum over
+    slices (ascending s) of each slice's dX_s = dY_s W_s + Gs_s A_{t,s} (so dX = dY W + sum_s
+    Gs_s A_{t,s}).  Returns (dX, Gs [R, S * r_cap], grads[t][s] = (dA_{t,s}, dB_{t,s}))."""
+    Wd = widen(W)
+    dYd = widen(dY)
+    N = Wd.shape[0]
+    dYd = dYd.reshape(-1, N)
+    S = len(col_off) - 1
+    dX = None
+    Gss = []
+    grads = [[None] * S for _ in range(len(ranks))]
+    for s in range(S):
+        c0, c1 = col_off[s], col_off[s + 1]
+        dX_s, Gs_s, g_s = linear_bwd(seg_off, seg_task, [a[s] for a in A], [b[s] for b in B],
+                                     [r[s] for r in ranks], [c[s] for c in scales],
+                                     np.ascontiguousarray(dYd[:, c0:c1]), X, Wd[c0:c1], r_cap, rows=rows)
+        dX = dX_s if dX is None else dX + dX_s
+        Gss.append(Gs_s)
+        for t in range(len(ranks)):
+            grads[t][s] = g_s[t]
+    return dX, np.concatenate(Gss, axis=1), grads

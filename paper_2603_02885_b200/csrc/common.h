@@ -40,11 +40,13 @@ struct GemmParams {
   CUtensorMap map_side;
   // output Y (fwd) / dX (bwd): dims {Nout, rows}, box {64, 32} (TMA store)
   CUtensorMap map_out;
-  // per adapter: A_t dims {K, rank} box {64, 64};  B_t dims {rank, N} box {64, 64}
-  CUtensorMap map_lora_a[MUX_MAX_ADAPTERS];
-  CUtensorMap map_lora_b[MUX_MAX_ADAPTERS];
+  // per adapter slot (task t, column slice s: slot t * num_slices + s):
+  // A_{t,s} dims {K, rank} box {64, 64};  B_{t,s} dims {rank, slice width} box {64, 64}.
+  // A rank-0 slot holds a copy of another slot's maps (read only out of bounds: zero fill).
+  CUtensorMap map_lora_a[MUX_MAX_ADAPTER_SLOTS];
+  CUtensorMap map_lora_b[MUX_MAX_ADAPTER_SLOTS];
   const int32_t* seg_off;        // device [num_segs + 1]
-  __nv_bfloat16* side_out;       // Hs / Gs [max_rows, r_cap]
+  __nv_bfloat16* side_out;       // Hs / Gs [max_rows, num_slices * r_cap] (slice s: columns s * r_cap ..)
   __nv_bfloat16* out;            // Y / dX [max_rows, nout] (direct-store epilogue variant)
   unsigned long long* flags;     // [ceil(max_rows/256)] epoch-tagged (workspace, zeroed once)
   unsigned long long* epoch;     // workspace launch epoch; bumped by the last CTA to finish
@@ -53,12 +55,15 @@ struct GemmParams {
   int32_t max_rows;
   int32_t kred;                  // reduction length of the main product (K fwd, N bwd)
   int32_t nout;                  // output columns (N fwd, K bwd)
-  int32_t r_cap;
+  int32_t r_cap;                 // per slice
+  int32_t num_slices;            // column slices of the fwd output (1 = plain linear)
+  int32_t slice_off[MUX_MAX_SLICES + 1];  // fwd output columns of each slice (bwd: reduction columns)
   int32_t has_main;              // 0: only the shrink (side) tiles, over row blocks [side_m_lo, side_m_hi)
   int32_t has_side;              // 0: no side tiles, Hs given (mux_linear_fwd_hs)
   int32_t side_m_lo, side_m_hi;  // shrink-only launches: pair row-block range
   int32_t side_first;            // 1: all side tiles before the main tiles (short reductions)
   int32_t group_m;               // raster band: pair row-blocks sharing a sweep over W tiles
+  int32_t group_n;               // > 0: column bands of group_n output blocks instead (W-resident raster)
   unsigned long long* dbg;       // MUX_PROFILE builds only: wait-cycle counters (see gemm.cu)
   // Fused reduce-scatter output (tensor parallel, mux_linear_*_rs): rs_world > 0 sends each
   // output tile straight to the rank that owns its rows (rs_rows per rank, contiguous blocks):
@@ -87,10 +92,14 @@ struct GemmParams {
   int32_t sk_side_cost_x4;          // a shrink tile's k-block, in quarters of a main k-block (balance)
   unsigned long long* sk_flags;     // [kSkMaxClusters] epoch-tagged (workspace)
   float* sk_part;                   // [kSkMaxClusters][2 CTAs][4 warps][256 cols][32 lanes] fp32
-  int32_t seg_adapter[MUX_MAX_SEGMENTS];
-  int32_t seg_rank[MUX_MAX_SEGMENTS];
-  float seg_scale[MUX_MAX_SEGMENTS];
+  int32_t seg_adapter[MUX_MAX_SEGMENTS];  // task of the segment
+  int32_t seg_rank[MUX_MAX_SEGMENTS];     // max rank over the task's slots (0: no adapter at all)
+  int32_t slot_rank[MUX_MAX_ADAPTER_SLOTS];
+  float slot_scale[MUX_MAX_ADAPTER_SLOTS];
 };
+
+// a __grid_constant__ kernel parameter block is limited to 32764 bytes
+static_assert(sizeof(GemmParams) <= 32764, "GemmParams exceeds the kernel parameter limit");
 
 // ---- segmented adapter gradients (dA_t, dB_t)
 constexpr int kGradBM = 128;     // output rows per unit (k for dA, n for dB)

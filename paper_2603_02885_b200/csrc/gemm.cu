@@ -124,6 +124,18 @@ __device__ __forceinline__ PairGroups pair_groups(const GemmParams& p, const int
   return g;
 }
 
+// Does the extension block of adapter slot `slot` (slice s) contribute to the main tile covering
+// output columns [tc0, tc1)?  Forward: only where the tile overlaps the slice's columns (a tile
+// straddling two slices runs both, each with the other slice's rows of B zero-filled).  Backward
+// (dX): every slice, the reduction of Gs_s A_{t,s} is over ranks.  Producer and MMA issuer take
+// the same decision.
+template <bool kBwd>
+__device__ __forceinline__ bool ext_live(const GemmParams& p, int slot, int s, int tc0, int tc1) {
+  if (p.slot_rank[slot] == 0) return false;
+  if (kBwd) return true;
+  return p.slice_off[s] < tc1 && p.slice_off[s + 1] > tc0;
+}
+
 // disable-output-lane mask of a group owning the quarters in `hm`
 __device__ __forceinline__ void lane_masks(int hm, uint32_t (&m)[8]) {
 #pragma unroll
@@ -146,11 +158,37 @@ struct Tile {
 // band by band.  With short main tiles, a band's main tiles otherwise reach their extension
 // block while that band's side tiles (same wave) are still in their epilogue, and the producer
 // stalls on the flag (profiles/r01_gemm_ab_sidefirst.jsonl).
+// group_n > 0 (chosen on the host for long reductions where W is the smaller operand, e.g. the
+// 11008 -> 4096 down projection): bands of group_n output-column blocks instead; within a band
+// row block by row block, columns fastest, so the band's W tiles (group_n * 256 columns * kred)
+// stay L2-resident while A streams past them once per band; the first band carries each row
+// block's side tile right before that row block's main tiles (dependencies still point down).
 __device__ __forceinline__ Tile tile_at(int t, int num_m, int num_n, int group_m, bool has_main, bool has_side,
-                                       int side_lo, bool side_first) {
+                                       int side_lo, bool side_first, int group_n) {
   Tile r;
   if (!has_main) {
     r.m = side_lo + t; r.n = 0; r.side = true;
+    return r;
+  }
+  if (group_n > 0) {
+    const int ns = has_side ? 1 : 0;
+    const int g0 = min(group_n, num_n);
+    const int first = num_m * (g0 + ns);
+    if (t < first) {
+      const int m = t / (g0 + ns);
+      const int w = t - m * (g0 + ns);
+      r.m = m; r.n = w - ns; r.side = w < ns;
+      if (r.side) r.n = 0;
+      return r;
+    }
+    t -= first;
+    const int per = num_m * group_n;
+    const int b = 1 + t / per;
+    const int loc = t - (b - 1) * per;
+    const int gnb = min(group_n, num_n - b * group_n);
+    r.m = loc / gnb;
+    r.n = b * group_n + (loc - r.m * gnb);
+    r.side = false;
     return r;
   }
   if (has_side && side_first) {
@@ -219,7 +257,8 @@ __device__ __forceinline__ void for_each_item(const GemmParams& p, int cid, int 
                                               int side_lo, int total_tiles, int num_kb, const int* skb, F&& f) {
   if (!p.sk) {
     for (int t = cid; t < total_tiles; t += ncl)
-      f(tile_at(t, num_m, num_n, p.group_m, p.has_main != 0, p.has_side != 0, side_lo, p.side_first != 0),
+      f(tile_at(t, num_m, num_n, p.group_m, p.has_main != 0, p.has_side != 0, side_lo, p.side_first != 0,
+                p.group_n),
         SkPiece{0, num_kb, true, 0});
     return;
   }
@@ -367,10 +406,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           }
         }
         if (tl.side) {
-          for (int g0 = 0; g0 < g.n; g0 += 2) {
-            const int ng = min(2, g.n - g0);
-            const int ad0 = p.seg_adapter[g.seg[g0]];
-            const int ad1 = ng > 1 ? p.seg_adapter[g.seg[g0 + 1]] : ad0;
+          // units (task group gi, slice pair sp), two per pass: CTA rk stages slice 2 sp + rk of
+          // the group's adapter (a missing slice or a rank-0 slot: rows >= 64, all zero fill)
+          const int S = p.num_slices;
+          const int nsp = (S + 1) >> 1;
+          const int nunits = g.n * nsp;
+          for (int u0 = 0; u0 < nunits; u0 += 2) {
+            const int nu = min(2, nunits - u0);
+            int slot[2], jrow[2], coff[2];
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              const int u = min(u0 + i, nunits - 1);
+              const int gi = u / nsp;
+              const int s = 2 * (u - gi * nsp) + rk;
+              const int base = p.seg_adapter[g.seg[gi]] * S;
+              slot[i] = base + (s < S ? s : 0);
+              jrow[i] = (s < S && p.slot_rank[base + s] > 0) ? 0 : 64;
+              coff[i] = s < S ? p.slice_off[s] : 0;
+            }
             for (int kb = 0; kb < num_kb; ++kb) {
               PROF_T0(tw_);
               mbar_wait(&empty_bar[stage], phase ^ 1u);
@@ -379,19 +432,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                 const uint32_t sa = pipe_u + stage * kStageBytes;
                 const uint32_t sb = sa + kStageA;
                 const uint32_t fbl = full_leader + 8u * stage;
-                if (leader) mbar_arrive_expect_tx_u32(full_u + 8u * stage, 2u * (kStageA + ng * kSideGrp));
+                if (leader) mbar_arrive_expect_tx_u32(full_u + 8u * stage, 2u * (kStageA + nu * kSideGrp));
                 const int k0 = kb * kBK;
 #pragma unroll
                 for (int s2 = 0; s2 < kKSub; ++s2) tma_load_2d_pair_u32(&p.map_a, fbl, sa + s2 * kSubA, k0 + 64 * s2, row_c);
-                for (int i = 0; i < ng; ++i) {
-                  const int ad = i == 0 ? ad0 : ad1;
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                  if (i >= nu) break;
 #pragma unroll
                   for (int s2 = 0; s2 < kKSub; ++s2) {
                     const uint32_t dst = sb + i * kSideGrp + s2 * kBox;
-                    if (!kBwd)  // A_t [r, K] K-major rows j: CTA 1's rows 64.. are zero fill
-                      tma_load_2d_pair_u32(&p.map_lora_a[ad], fbl, dst, k0 + 64 * s2, 64 * rk);
-                    else        // B_t [N, r] read MN-major {64 j, 64 n}
-                      tma_load_2d_pair_u32(&p.map_lora_b[ad], fbl, dst, 64 * rk, k0 + 64 * s2);
+                    if (!kBwd)  // A_{t,s} [r, K] K-major rows j
+                      tma_load_2d_pair_u32(&p.map_lora_a[slot[i]], fbl, dst, k0 + 64 * s2, jrow[i]);
+                    else        // B_{t,s} [n_s, r] read MN-major {64 j, 64 n}: rows outside the slice are zero fill
+                      tma_load_2d_pair_u32(&p.map_lora_b[slot[i]], fbl, dst, jrow[i], k0 + 64 * s2 - coff[i]);
                   }
                 }
               }
@@ -446,28 +500,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             }
             __syncwarp();
           }
-          for (int i = 0; i < (pc.fin ? g.n : 0); ++i) {  // LoRA expand: the tile's final piece only
-            // extension block: reduction = rank (<= 64): first k-subtile only
-            const int ad = p.seg_adapter[g.seg[i]];
-            PROF_T0(tw_);
-            mbar_wait(&empty_bar[stage], phase ^ 1u);
-            PROF_ADD(pw_empty, tw_);
-            if (elect_one_sync()) {
-              const uint32_t sa = pipe_u + stage * kStageBytes;
-              const uint32_t sb = sa + kStageA;
-              const uint32_t fbl = full_leader + 8u * stage;
-              if (leader) mbar_arrive_expect_tx_u32(full_u + 8u * stage, 2u * (kSubA + kHalves * kBox));
-              tma_load_2d_pair_u32(&p.map_side, fbl, sa, 0, row_c);
+          // LoRA expand (the tile's final piece only): one extension block per (task group, slice
+          // with an adapter on this tile); reduction = the slot's rank (<= 64): first k-subtile only
+          const int S = p.num_slices;
+          const int tc0 = tl.n * kTileN, tc1 = tc0 + kTileN;
+          for (int i = 0; i < (pc.fin ? g.n : 0); ++i) {
+            for (int s = 0; s < S; ++s) {
+              const int slot = p.seg_adapter[g.seg[i]] * S + s;
+              if (!ext_live<kBwd>(p, slot, s, tc0, tc1)) continue;
+              PROF_T0(tw_);
+              mbar_wait(&empty_bar[stage], phase ^ 1u);
+              PROF_ADD(pw_empty, tw_);
+              if (elect_one_sync()) {
+                const uint32_t sa = pipe_u + stage * kStageBytes;
+                const uint32_t sb = sa + kStageA;
+                const uint32_t fbl = full_leader + 8u * stage;
+                if (leader) mbar_arrive_expect_tx_u32(full_u + 8u * stage, 2u * (kSubA + kHalves * kBox));
+                tma_load_2d_pair_u32(&p.map_side, fbl, sa, s * p.r_cap, row_c);
 #pragma unroll
-              for (int j = 0; j < kHalves; ++j) {
-                if (!kBwd)  // B_t [N, r] K-major rows n: box {64 j, 64 n}
-                  tma_load_2d_pair_u32(&p.map_lora_b[ad], fbl, sb + j * kBox, 0, col_c + 64 * j);
-                else        // A_t [r, K] viewed [k_out (MN), j (red)]: atom j, K-rows 0..63
-                  tma_load_2d_pair_u32(&p.map_lora_a[ad], fbl, sb + j * kAtomMN, col_c + 64 * j, 0);
+                for (int j = 0; j < kHalves; ++j) {
+                  if (!kBwd)  // B_{t,s} [n_s, r] K-major rows n: box {64 j, 64 n}, zero fill outside the slice
+                    tma_load_2d_pair_u32(&p.map_lora_b[slot], fbl, sb + j * kBox, 0, col_c + 64 * j - p.slice_off[s]);
+                  else        // A_{t,s} [r, K] viewed [k_out (MN), j (red)]: atom j, K-rows 0..63
+                    tma_load_2d_pair_u32(&p.map_lora_a[slot], fbl, sb + j * kAtomMN, col_c + 64 * j, 0);
+                }
               }
+              __syncwarp();
+              advance();
             }
-            __syncwarp();
-            advance();
           }
         }
       });
@@ -510,11 +570,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * kBN);
         if (tl.side) {
-          for (int g0 = 0; g0 < g.n; g0 += 2) {
-            const int ng = min(2, g.n - g0);
+          // units (task group, slice pair sp) as staged by the producer: slice pair sp accumulates
+          // into TMEM columns [128 sp, 128 sp + 128) (slice s at 64 s), masked to the group's rows
+          const int nsp = (p.num_slices + 1) >> 1;
+          const int nunits = g.n * nsp;
+          for (int u0 = 0; u0 < nunits; u0 += 2) {
+            const int nu = min(2, nunits - u0);
             uint32_t mk[2][8];
-            lane_masks(g.hm[g0], mk[0]);
-            lane_masks(ng > 1 ? g.hm[g0 + 1] : 0, mk[1]);
+            uint32_t dcol[2];
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              const int u = min(u0 + i, nunits - 1);
+              const int gi = u / nsp;
+              lane_masks(i < nu ? g.hm[gi] : 0, mk[i]);
+              dcol[i] = static_cast<uint32_t>(128 * (u - gi * nsp));
+            }
             for (int kb = 0; kb < num_kb; ++kb) {
               PROF_T0(tw_);
               mbar_wait(&full_bar[stage], phase);
@@ -523,10 +593,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
               const uint32_t a_lo = a_lo0 + stage * kStageStep;
               const uint32_t b_lo = b_lo0 + stage * kStageStep;
               if (elect_one_sync()) {
-                for (int i = 0; i < ng; ++i) {
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                  if (i >= nu) break;
 #pragma unroll
                   for (int k = 0; k < kBK / 16; ++k)
-                    mma_bf16_pair(d_tmem, make_desc(a_lo + a_off(k), kHi),
+                    mma_bf16_pair(d_tmem + dcol[i], make_desc(a_lo + a_off(k), kHi),
                                   make_desc(b_lo + i * (kSideGrp >> 4) + side_b_off(k), kHi), kIdescSide,
                                   (kb | k) != 0, mk[i]);
                 }
@@ -554,24 +626,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             __syncwarp();
             advance();
           }
-          for (int i = 0; i < (pc.fin ? g.n : 0); ++i) {  // LoRA expand: the tile's final piece only
-            PROF_T0(tw_);
-            mbar_wait(&full_bar[stage], phase);
-            PROF_ADD(mw_full, tw_);
-            tc_fence_after();
-            const uint32_t a_lo = a_lo0 + stage * kStageStep;
-            const uint32_t b_lo = b_lo0 + stage * kStageStep;
-            const int nk = (p.seg_rank[g.seg[i]] + 15) / 16;
+          // LoRA expand: the tile's final piece only, the producer's (group, live slice) blocks
+          const int S = p.num_slices;
+          const int tc0 = tl.n * kTileN, tc1 = tc0 + kTileN;
+          for (int i = 0; i < (pc.fin ? g.n : 0); ++i) {
             uint32_t mk[8];
             lane_masks(g.hm[i], mk);
-            if (elect_one_sync()) {
-              for (int k = 0; k < nk; ++k)
-                mma_bf16_pair(d_tmem, make_desc(a_lo + a_off(k), kHi), make_desc(b_lo + b_off(k), kHi),
-                              kIdescMain, 1u, mk);
-              mma_commit_pair_mc(&empty_bar[stage], kPairMask);
+            for (int s = 0; s < S; ++s) {
+              const int slot = p.seg_adapter[g.seg[i]] * S + s;
+              if (!ext_live<kBwd>(p, slot, s, tc0, tc1)) continue;
+              PROF_T0(tw_);
+              mbar_wait(&full_bar[stage], phase);
+              PROF_ADD(mw_full, tw_);
+              tc_fence_after();
+              const uint32_t a_lo = a_lo0 + stage * kStageStep;
+              const uint32_t b_lo = b_lo0 + stage * kStageStep;
+              const int nk = (p.slot_rank[slot] + 15) / 16;
+              if (elect_one_sync()) {
+                for (int k = 0; k < nk; ++k)
+                  mma_bf16_pair(d_tmem, make_desc(a_lo + a_off(k), kHi), make_desc(b_lo + b_off(k), kHi),
+                                kIdescMain, 1u, mk);
+                mma_commit_pair_mc(&empty_bar[stage], kPairMask);
+              }
+              __syncwarp();
+              advance();
             }
-            __syncwarp();
-            advance();
           }
         }
         if (elect_one_sync()) mma_commit_pair_mc(&tfull_bar[acc], kPairMask);
@@ -610,33 +689,42 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       const uint32_t t_addr = tmem_base + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(acc * kBN);
       const uint32_t tempty_leader = mapa_shared(smem_u32(&tempty_bar[acc]), 0);
       if (tl.side) {
-        uint32_t v0[32], v1[32];
-        tmem_ld32(t_addr, v0);
-        tmem_ld32(t_addr + 32, v1);
-        tmem_ld_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(tempty_leader);
+        // slice sl of the shrink sits in TMEM columns [64 sl, 64 sl + 64) -> Hs/Gs columns
+        // [sl * r_cap, sl * r_cap + r_cap), scaled by the row's task's s_{t,sl}
         const int row = row_w + lane;
-        if (row < total_rows) {
-          const int s = seg_containing(so, p.num_segs, row);
-          const int rank = s >= 0 ? p.seg_rank[s] : 0;
-          const float sc = s >= 0 ? p.seg_scale[s] : 0.f;
-          uint4* dst = reinterpret_cast<uint4*>(p.side_out + static_cast<size_t>(row) * p.r_cap);
+        const int S = p.num_slices;
+        const int seg = row < total_rows ? seg_containing(so, p.num_segs, row) : -1;
+        const size_t ld = static_cast<size_t>(S) * p.r_cap;
+        for (int sl = 0; sl < S; ++sl) {
+          uint32_t v0[32], v1[32];
+          tmem_ld32(t_addr + 64 * sl, v0);
+          tmem_ld32(t_addr + 64 * sl + 32, v1);
+          tmem_ld_wait();
+          if (sl == S - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(tempty_leader);
+          }
+          if (row < total_rows) {
+            const int slot = seg >= 0 ? p.seg_adapter[seg] * S + sl : 0;
+            const int rank = seg >= 0 ? p.slot_rank[slot] : 0;
+            const float sc = seg >= 0 ? p.slot_scale[slot] : 0.f;
+            uint4* dst = reinterpret_cast<uint4*>(p.side_out + static_cast<size_t>(row) * ld + sl * p.r_cap);
 #pragma unroll
-          for (int j0 = 0; j0 < 64; j0 += 8) {
-            if (j0 < p.r_cap) {
-              uint32_t w[4];
+            for (int j0 = 0; j0 < 64; j0 += 8) {
+              if (j0 < p.r_cap) {
+                uint32_t w[4];
 #pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const int j = j0 + 2 * e;
-                const uint32_t a = j < 32 ? v0[j & 31] : v1[j & 31];
-                const uint32_t b = j + 1 < 32 ? v0[(j + 1) & 31] : v1[(j + 1) & 31];
-                const float lo = j < rank ? __uint_as_float(a) * sc : 0.f;
-                const float hi = j + 1 < rank ? __uint_as_float(b) * sc : 0.f;
-                w[e] = pack_bf16x2(lo, hi);
+                for (int e = 0; e < 4; ++e) {
+                  const int j = j0 + 2 * e;
+                  const uint32_t a = j < 32 ? v0[j & 31] : v1[j & 31];
+                  const uint32_t b = j + 1 < 32 ? v0[(j + 1) & 31] : v1[(j + 1) & 31];
+                  const float lo = j < rank ? __uint_as_float(a) * sc : 0.f;
+                  const float hi = j + 1 < rank ? __uint_as_float(b) * sc : 0.f;
+                  w[e] = pack_bf16x2(lo, hi);
+                }
+                dst[j0 / 8] = make_uint4(w[0], w[1], w[2], w[3]);
               }
-              dst[j0 / 8] = make_uint4(w[0], w[1], w[2], w[3]);
             }
           }
         }

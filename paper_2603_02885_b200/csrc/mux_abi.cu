@@ -263,13 +263,43 @@ LinearWs carve_linear_ws(void* base, int32_t max_rows, int32_t r_cap) {
   return w;
 }
 
+// Column slices of the call (NULL = one slice over all N columns), validated.
+struct SliceTab {
+  int n;
+  int off[MUX_MAX_SLICES + 1];
+};
+
+mux_status make_slices(const mux_slices* sl, int32_t N, SliceTab* out) {
+  if (!sl) {
+    out->n = 1;
+    out->off[0] = 0;
+    out->off[1] = N;
+    return MUX_OK;
+  }
+  if (sl->num_slices < 1 || sl->num_slices > MUX_MAX_SLICES)
+    return fail(MUX_ERR_INVALID_ARGUMENT, "num_slices=%d outside [1,%d]", sl->num_slices, MUX_MAX_SLICES);
+  out->n = sl->num_slices;
+  for (int s = 0; s <= out->n; ++s) out->off[s] = sl->col_off[s];
+  if (out->off[0] != 0 || out->off[out->n] != N)
+    return fail(MUX_ERR_INVALID_ARGUMENT, "col_off must start at 0 and end at N=%d (got %d .. %d)", N, out->off[0],
+                out->off[out->n]);
+  for (int s = 0; s < out->n; ++s)
+    if (out->off[s + 1] <= out->off[s] || (out->off[s] % 8))
+      return fail(MUX_ERR_INVALID_ARGUMENT, "col_off[%d..%d] = %d, %d: slices must be non-empty and start at "
+                  "multiples of 8", s, s + 1, out->off[s], out->off[s + 1]);
+  return MUX_OK;
+}
+
 mux_status validate_linear(int32_t num_segs, const int32_t* seg_off, const int32_t* seg_task,
                            int32_t num_adapters, const mux_adapter* adapters, int32_t max_rows, int32_t K,
-                           int32_t N, int32_t r_cap) {
+                           int32_t N, int32_t r_cap, const SliceTab& sl) {
   if (num_segs < 1 || num_segs > MUX_MAX_SEGMENTS)
     return fail(MUX_ERR_INVALID_ARGUMENT, "num_segs=%d outside [1,%d]", num_segs, MUX_MAX_SEGMENTS);
   if (num_adapters < 1 || num_adapters > MUX_MAX_ADAPTERS)
     return fail(MUX_ERR_INVALID_ARGUMENT, "num_adapters=%d outside [1,%d]", num_adapters, MUX_MAX_ADAPTERS);
+  if (num_adapters * sl.n > MUX_MAX_ADAPTER_SLOTS)
+    return fail(MUX_ERR_INVALID_ARGUMENT, "num_adapters * num_slices = %d * %d > %d adapter slots", num_adapters,
+                sl.n, MUX_MAX_ADAPTER_SLOTS);
   if (!seg_off || !seg_task || !adapters) return fail(MUX_ERR_INVALID_ARGUMENT, "null seg_off/seg_task/adapters");
   if (max_rows < 1) return fail(MUX_ERR_INVALID_ARGUMENT, "max_rows=%d must be >= 1", max_rows);
   // multiples of 8: 16-byte TMA row strides; partial 64-wide tiles are handled
@@ -281,7 +311,7 @@ mux_status validate_linear(int32_t num_segs, const int32_t* seg_off, const int32
   for (int s = 0; s < num_segs; ++s)
     if (seg_task[s] < 0 || seg_task[s] >= num_adapters)
       return fail(MUX_ERR_INVALID_ARGUMENT, "seg_task[%d]=%d outside [0,%d)", s, seg_task[s], num_adapters);
-  for (int t = 0; t < num_adapters; ++t) {
+  for (int t = 0; t < num_adapters * sl.n; ++t) {
     const mux_adapter& a = adapters[t];
     if (a.rank < 0 || a.rank > MUX_MAX_RANK)
       return fail(MUX_ERR_INVALID_ARGUMENT, "adapter %d: rank=%d outside [0,64]", t, a.rank);
@@ -301,17 +331,33 @@ mux_status validate_linear(int32_t num_segs, const int32_t* seg_off, const int32
   return MUX_OK;
 }
 
-// Fill the per-adapter TMA descriptors (rank > 0 only).
+// Fill the per-slot TMA descriptors (slot = task * S + slice; B_{t,s} spans the slice's columns).
+// A rank-0 slot of a task that has an adapter on another slice gets that slot's descriptors: the
+// kernel reads them only at row 64 (all zero fill), so the shrink unit stays uniform.
 mux_status fill_adapter_maps(GemmParams& p, int32_t num_adapters, const mux_adapter* adapters, int32_t K,
-                             int32_t N) {
+                             const SliceTab& sl) {
+  const int S = sl.n;
   for (int t = 0; t < num_adapters; ++t) {
-    const mux_adapter& a = adapters[t];
-    if (a.rank == 0) continue;
-    const int ldb = a.ldb == 0 ? a.rank : a.ldb;
-    if (!make_map(&p.map_lora_a[t], a.A, K, a.rank, K, 64, 64))
-      return fail(MUX_ERR_CUDA, "cuTensorMapEncodeTiled failed for adapter %d A", t);
-    if (!make_map(&p.map_lora_b[t], a.B, a.rank, N, ldb, 64, 64))
-      return fail(MUX_ERR_CUDA, "cuTensorMapEncodeTiled failed for adapter %d B", t);
+    int live = -1;
+    for (int s = 0; s < S; ++s) {
+      const int slot = t * S + s;
+      const mux_adapter& a = adapters[slot];
+      if (a.rank == 0) continue;
+      const int ldb = a.ldb == 0 ? a.rank : a.ldb;
+      const int ns = sl.off[s + 1] - sl.off[s];
+      if (!make_map(&p.map_lora_a[slot], a.A, K, a.rank, K, 64, 64))
+        return fail(MUX_ERR_CUDA, "cuTensorMapEncodeTiled failed for adapter slot %d A", slot);
+      if (!make_map(&p.map_lora_b[slot], a.B, a.rank, ns, ldb, 64, 64))
+        return fail(MUX_ERR_CUDA, "cuTensorMapEncodeTiled failed for adapter slot %d B", slot);
+      if (live < 0) live = slot;
+    }
+    if (live < 0) continue;
+    for (int s = 0; s < S; ++s) {
+      const int slot = t * S + s;
+      if (adapters[slot].rank != 0) continue;
+      p.map_lora_a[slot] = p.map_lora_a[live];
+      p.map_lora_b[slot] = p.map_lora_b[live];
+    }
   }
   return MUX_OK;
 }
@@ -396,9 +442,14 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
                                 size_t workspace_bytes, cudaStream_t stream, int parts = 3,
                                 const mux_rs* rs = nullptr, const mux_ag* ag = nullptr, bool hs_given = false,
                                 bool shrink_only = false, int32_t side_row_lo = 0,
-                                int32_t side_row_hi = INT32_MAX) {
-  mux_status st = validate_linear(num_segs, seg_off, seg_task, num_adapters, adapters, max_rows, K, N, r_cap);
+                                int32_t side_row_hi = INT32_MAX, const mux_slices* slices = nullptr) {
+  SliceTab sl;
+  mux_status st = make_slices(slices, N, &sl);
   if (st != MUX_OK) return st;
+  st = validate_linear(num_segs, seg_off, seg_task, num_adapters, adapters, max_rows, K, N, r_cap, sl);
+  if (st != MUX_OK) return st;
+  const int S = sl.n;
+  const int side_ld = S * r_cap;  // Hs / Gs row length: slice s at columns [s * r_cap, (s + 1) * r_cap)
   if (!a_in || (!W && !shrink_only)) return fail(MUX_ERR_INVALID_ARGUMENT, "null input pointer");
   if (hs_given && !Hs_in) return fail(MUX_ERR_INVALID_ARGUMENT, "Hs (input) is null");
   if (shrink_only && !Hs_out) return fail(MUX_ERR_INVALID_ARGUMENT, "Hs (output) is null");
@@ -411,11 +462,11 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
     return fail(MUX_ERR_INVALID_ARGUMENT, "tensor pointers must be 16-byte aligned");
   if (bwd && (!X || !Hs_in)) return fail(MUX_ERR_INVALID_ARGUMENT, "bwd needs X and Hs");
   if (!bwd && !out && !rs && !shrink_only) return fail(MUX_ERR_INVALID_ARGUMENT, "fwd needs Y");
-  const LinearWs need = carve_linear_ws(nullptr, max_rows, r_cap);
+  const LinearWs need = carve_linear_ws(nullptr, max_rows, side_ld);
   if (!workspace || workspace_bytes < need.bytes)
     return fail(MUX_ERR_INSUFFICIENT_BUFFER, "linear workspace %zu < %zu bytes", workspace_bytes, need.bytes);
   if (!aligned16(workspace)) return fail(MUX_ERR_INVALID_ARGUMENT, "workspace not 16-byte aligned");
-  const LinearWs ws = carve_linear_ws(workspace, max_rows, r_cap);
+  const LinearWs ws = carve_linear_ws(workspace, max_rows, side_ld);
 
   static thread_local GemmParams p;  // ~17 KB: keep it off the stack
   std::memset(&p, 0, sizeof(p));
@@ -426,13 +477,13 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
     return fail(MUX_ERR_CUDA, "cuTensorMapEncodeTiled failed for %s %p [%d x %d]", bwd ? "dY" : "X", a_in, max_rows, kred);
   if (W && !make_map(&p.map_w, W, K, N, K, 64, 64))
     return fail(MUX_ERR_CUDA, "cuTensorMapEncodeTiled failed for W %p [%d x %d]", W, N, K);
-  if (!make_map(&p.map_side, side, r_cap, max_rows, r_cap, 64, 128))
+  if (!make_map(&p.map_side, side, side_ld, max_rows, side_ld, 64, 128))
     return fail(MUX_ERR_CUDA, "cuTensorMapEncodeTiled failed for %s %p [%d x %d]", bwd ? "Gs" : "Hs", side, max_rows,
-                r_cap);
+                side_ld);
   if (out && !make_map(&p.map_out, out, nout, max_rows, nout, 64, 32))
     return fail(MUX_ERR_CUDA, "cuTensorMapEncodeTiled failed for %s %p [%d x %d]", bwd ? "dX" : "Y", out, max_rows,
                 nout);
-  st = fill_adapter_maps(p, num_adapters, adapters, K, N);
+  st = fill_adapter_maps(p, num_adapters, adapters, K, sl);
   if (st != MUX_OK) return st;
   p.seg_off = seg_off;
   p.side_out = side;
@@ -448,6 +499,8 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
   p.kred = kred;
   p.nout = nout;
   p.r_cap = r_cap;
+  p.num_slices = S;
+  for (int s = 0; s <= S; ++s) p.slice_off[s] = sl.off[s];
   p.has_main = out != nullptr || rs != nullptr;
   p.has_side = hs_given ? 0 : 1;
   // short reductions: side tiles first (A/B in DESIGN §12: +3-9 % at kred <= 1376, neutral at 4096+)
@@ -499,16 +552,42 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
 #ifndef MUX_BAND_MIN
 #define MUX_BAND_MIN 4
 #endif
+#ifndef MUX_RASTER_DEFAULT
+#define MUX_RASTER_DEFAULT 'm'   // 'a' = traffic model, 'm' = row bands, 'n' = column bands
+#endif
   {
     const long long band_bytes = static_cast<long long>(kPairRows) * kred * 2;
     long long g = (static_cast<long long>(MUX_BAND_MB) << 20) / band_bytes;
     p.group_m = static_cast<int32_t>(std::max(static_cast<long long>(MUX_BAND_MIN), std::min(32ll, g)));
   }
+  // raster direction by a DRAM-traffic model: row bands read A once and W once per band; column
+  // bands (the band's W tiles L2-resident) read W once and A once per band.  Column bands where
+  // they move at most 80 % of the bytes (long reductions with W the smaller operand, e.g. the
+  // 11008 -> 4096 down projection); MUX_RASTER=m / n forces one (A/B; read per call).
+  {
+    const char* re = std::getenv("MUX_RASTER");
+    const char rc = (re && *re) ? re[0] : MUX_RASTER_DEFAULT;
+    const long long nrow_blk = (static_cast<long long>(max_rows) + kPairRows - 1) / kPairRows;
+    const int tile_n0 = nout <= MUX_NARROW_MAX_NOUT ? kBN / 2 : kBN;
+    const long long ncol_blk = (static_cast<long long>(nout) + tile_n0 - 1) / tile_n0;
+    const long long col_band_bytes = static_cast<long long>(tile_n0) * kred * 2;
+    const long long gn = std::max(static_cast<long long>(MUX_BAND_MIN),
+                                  std::min(64ll, (static_cast<long long>(MUX_BAND_MB) << 20) / col_band_bytes));
+    const double a_bytes = static_cast<double>(max_rows) * kred * 2, w_bytes = static_cast<double>(nout) * kred * 2;
+    const double row_bands = a_bytes + w_bytes * static_cast<double>((nrow_blk + p.group_m - 1) / p.group_m);
+    const double col_bands = w_bytes + a_bytes * static_cast<double>((ncol_blk + gn - 1) / gn);
+    const bool col = rc == 'n' || (rc != 'm' && col_bands <= 0.8 * row_bands);
+    p.group_n = (col && !p.side_first) ? static_cast<int32_t>(gn) : 0;
+  }
+  for (int t = 0; t < num_adapters * S; ++t) {
+    p.slot_rank[t] = adapters[t].rank;
+    p.slot_scale[t] = adapters[t].scale;
+  }
   for (int s = 0; s < num_segs; ++s) {
-    const mux_adapter& a = adapters[seg_task[s]];
+    int r = 0;
+    for (int c = 0; c < S; ++c) r = std::max(r, adapters[seg_task[s] * S + c].rank);
     p.seg_adapter[s] = seg_task[s];
-    p.seg_rank[s] = a.rank;
-    p.seg_scale[s] = a.scale;
+    p.seg_rank[s] = r;
   }
   const int num_m_max = (max_rows + kPairRows - 1) / kPairRows;
   // narrow outputs (<= MUX_NARROW_MAX_NOUT columns): 256 x 128 tiles, twice as many work items
@@ -555,48 +634,54 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
   }
 
   if (bwd && (parts & 2)) {
-    static thread_local GradParams g;
-    std::memset(&g, 0, sizeof(g));
-    if (!make_map(&g.map_x, X, K, max_rows, K, 64, 128) || !make_map(&g.map_dy, a_in, N, max_rows, N, 64, 128) ||
-        !make_map(&g.map_hs, Hs_in, r_cap, max_rows, r_cap, 64, 128) ||
-        !make_map(&g.map_gs, ws.gs, r_cap, max_rows, r_cap, 64, 128))
-      return fail(MUX_ERR_CUDA, "cuTensorMapEncodeTiled failed for a gradient-kernel operand (X, dY, Hs or Gs)");
-    g.seg_off = seg_off;
-    g.num_segs = num_segs;
-    g.K = K;
-    g.N = N;
-    g.r_cap = r_cap;
-    bool want_a = false, want_b = false;
-    int nt = 0;
-    int max_rank = 0;
-    for (int t = 0; t < num_adapters; ++t) {
-      const mux_adapter& a = adapters[t];
-      if (a.rank == 0 || (!a.dA && !a.dB)) continue;
-      uint64_t segs = 0;
-      for (int s = 0; s < num_segs; ++s)
-        if (seg_task[s] == t) segs |= 1ull << s;
-      g.task_segs[nt] = segs;
-      g.task_rank[nt] = a.rank;
-      g.task_dA[nt] = a.dA;
-      g.task_dB[nt] = a.dB;
-      want_a |= a.dA != nullptr;
-      want_b |= a.dB != nullptr;
-      max_rank = std::max(max_rank, a.rank);
-      ++nt;
-    }
-    g.num_tasks = nt;
-    g.units_a = want_a ? (K + kGradBM - 1) / kGradBM : 0;
-    g.units_b = want_b ? (N + kGradBM - 1) / kGradBM : 0;
-    const long long units = static_cast<long long>(nt) * (g.units_a + g.units_b);
-    if (units > 0) {
-      // HBM-bound: spread the units evenly (every CTA gets the same number of
-      // units) instead of leaving a ragged last wave on 148 CTAs
-      const long long waves = (units + num_sms() - 1) / num_sms();
-      const int ggrid = static_cast<int>((units + waves - 1) / waves);
-      // tensor cores (grad.cu) unless every rank is at most MUX_GRAD_SIMT_MAX_RANK, then
-      // the CUDA-core kernel (grad_simt.cu); the default comes from the A/B in DESIGN §6.2
-      e = max_rank <= MUX_GRAD_SIMT_MAX_RANK ? launch_grad_simt(g, ggrid, stream) : launch_grad(g, ggrid, stream);
-      if (e != cudaSuccess) return cuda_fail(e, "mux_linear_bwd grad launch");
+    // one launch per column slice s: dY's columns of the slice, Hs_s / Gs_s (columns
+    // [s * r_cap, (s + 1) * r_cap) of the side tensors), the slots (t, s)
+    for (int sc = 0; sc < S; ++sc) {
+      static thread_local GradParams g;
+      std::memset(&g, 0, sizeof(g));
+      const int n_s = sl.off[sc + 1] - sl.off[sc];
+      if (!make_map(&g.map_x, X, K, max_rows, K, 64, 128) ||
+          !make_map(&g.map_dy, a_in + sl.off[sc], n_s, max_rows, N, 64, 128) ||
+          !make_map(&g.map_hs, Hs_in + sc * r_cap, r_cap, max_rows, side_ld, 64, 128) ||
+          !make_map(&g.map_gs, ws.gs + sc * r_cap, r_cap, max_rows, side_ld, 64, 128))
+        return fail(MUX_ERR_CUDA, "cuTensorMapEncodeTiled failed for a gradient-kernel operand (X, dY, Hs or Gs)");
+      g.seg_off = seg_off;
+      g.num_segs = num_segs;
+      g.K = K;
+      g.N = n_s;
+      g.r_cap = r_cap;
+      bool want_a = false, want_b = false;
+      int nt = 0;
+      int max_rank = 0;
+      for (int t = 0; t < num_adapters; ++t) {
+        const mux_adapter& a = adapters[t * S + sc];
+        if (a.rank == 0 || (!a.dA && !a.dB)) continue;
+        uint64_t segs = 0;
+        for (int s = 0; s < num_segs; ++s)
+          if (seg_task[s] == t) segs |= 1ull << s;
+        g.task_segs[nt] = segs;
+        g.task_rank[nt] = a.rank;
+        g.task_dA[nt] = a.dA;
+        g.task_dB[nt] = a.dB;
+        want_a |= a.dA != nullptr;
+        want_b |= a.dB != nullptr;
+        max_rank = std::max(max_rank, a.rank);
+        ++nt;
+      }
+      g.num_tasks = nt;
+      g.units_a = want_a ? (K + kGradBM - 1) / kGradBM : 0;
+      g.units_b = want_b ? (n_s + kGradBM - 1) / kGradBM : 0;
+      const long long units = static_cast<long long>(nt) * (g.units_a + g.units_b);
+      if (units > 0) {
+        // HBM-bound: spread the units evenly (every CTA gets the same number of
+        // units) instead of leaving a ragged last wave on 148 CTAs
+        const long long waves = (units + num_sms() - 1) / num_sms();
+        const int ggrid = static_cast<int>((units + waves - 1) / waves);
+        // tensor cores (grad.cu) unless every rank is at most MUX_GRAD_SIMT_MAX_RANK, then
+        // the CUDA-core kernel (grad_simt.cu); the default comes from the A/B in DESIGN §6.2
+        e = max_rank <= MUX_GRAD_SIMT_MAX_RANK ? launch_grad_simt(g, ggrid, stream) : launch_grad(g, ggrid, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "mux_linear_bwd grad launch");
+      }
     }
   }
   return MUX_OK;
@@ -990,6 +1075,55 @@ mux_status mux_linear_bwd_ag(int32_t num_segs, const int32_t* seg_off, const int
                        reinterpret_cast<const __nv_bfloat16*>(X_), reinterpret_cast<const __nv_bfloat16*>(W_),
                        reinterpret_cast<__nv_bfloat16*>(dX_), reinterpret_cast<const __nv_bfloat16*>(Hs_), nullptr,
                        workspace, workspace_bytes, stream, 3, nullptr, ag);
+}
+
+// The generic entry point: every op of the per-op functions above, optionally over column slices
+// (mux.h, "Fused projections with one adapter per column slice").
+mux_status mux_linear(const mux_linear_args* a) {
+  if (!a) return fail(MUX_ERR_INVALID_ARGUMENT, "args is null");
+  using bf = __nv_bfloat16;
+  auto c = [](const mux_bf16* x) { return reinterpret_cast<const bf*>(x); };
+  auto m = [](mux_bf16* x) { return reinterpret_cast<bf*>(x); };
+  if (a->ag && (a->ag->rank < 0 || a->ag->rank >= MUX_RS_MAX_WORLD))
+    return fail(MUX_ERR_INVALID_ARGUMENT, "ag is bad (rank %d)", a->ag->rank);
+  const bf* ag_buf = a->ag ? reinterpret_cast<const bf*>(a->ag->recv[a->ag->rank]) : nullptr;
+  switch (a->op) {
+    case MUX_OP_FWD: {
+      if (a->rs && a->ag) return fail(MUX_ERR_INVALID_ARGUMENT, "fwd: rs and ag together are not supported");
+      const bf* X = a->ag ? ag_buf : c(a->X);
+      return linear_common(false, a->num_segs, a->seg_off, a->seg_task, a->num_adapters, a->adapters, a->max_rows,
+                           a->K, a->N, a->r_cap, X, X, c(a->W), a->rs ? nullptr : m(a->Y), nullptr, m(a->Hs),
+                           a->workspace, a->workspace_bytes, a->stream, 3, a->rs, a->ag, false, false, 0, INT32_MAX,
+                           a->slices);
+    }
+    case MUX_OP_FWD_HS:
+      if (a->rs || a->ag) return fail(MUX_ERR_INVALID_ARGUMENT, "fwd_hs: no fused collectives");
+      if (!a->Hs) return fail(MUX_ERR_INVALID_ARGUMENT, "fwd_hs: Hs (input) is null");
+      return linear_common(false, a->num_segs, a->seg_off, a->seg_task, a->num_adapters, a->adapters, a->max_rows,
+                           a->K, a->N, a->r_cap, c(a->X), c(a->X), c(a->W), m(a->Y), a->Hs ? c(a->Hs) : nullptr,
+                           nullptr, a->workspace, a->workspace_bytes, a->stream, 3, nullptr, nullptr, true, false, 0,
+                           INT32_MAX, a->slices);
+    case MUX_OP_SHRINK:
+      if (a->rs || a->ag) return fail(MUX_ERR_INVALID_ARGUMENT, "shrink: no fused collectives");
+      return linear_common(false, a->num_segs, a->seg_off, a->seg_task, a->num_adapters, a->adapters, a->max_rows,
+                           a->K, a->N, a->r_cap, c(a->X), c(a->X), nullptr, nullptr, nullptr, m(a->Hs), a->workspace,
+                           a->workspace_bytes, a->stream, 3, nullptr, nullptr, false, true, a->row_begin, a->row_end,
+                           a->slices);
+    case MUX_OP_BWD:
+    case MUX_OP_BWD_DX:
+    case MUX_OP_BWD_GRADS: {
+      const int parts = a->op == MUX_OP_BWD ? 3 : a->op == MUX_OP_BWD_DX ? 1 : 2;
+      if (a->rs && a->op != MUX_OP_BWD_DX) return fail(MUX_ERR_INVALID_ARGUMENT, "bwd: rs only with MUX_OP_BWD_DX");
+      if (a->rs && a->ag) return fail(MUX_ERR_INVALID_ARGUMENT, "bwd: rs and ag together are not supported");
+      const bf* dY = a->ag ? ag_buf : c(a->dY);
+      return linear_common(true, a->num_segs, a->seg_off, a->seg_task, a->num_adapters, a->adapters, a->max_rows,
+                           a->K, a->N, a->r_cap, dY, c(a->X), c(a->W), a->rs ? nullptr : m(a->dX), c(a->Hs), nullptr,
+                           a->workspace, a->workspace_bytes, a->stream, parts, a->rs, a->ag, false, false, 0,
+                           INT32_MAX, a->slices);
+    }
+    default:
+      return fail(MUX_ERR_INVALID_ARGUMENT, "unknown op %d", a->op);
+  }
 }
 
 }  // extern "C"

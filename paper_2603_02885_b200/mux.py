@@ -23,6 +23,8 @@ STATUS = {0: "MUX_OK", 1: "MUX_ERR_INVALID_ARGUMENT", 2: "MUX_ERR_UNSUPPORTED",
           3: "MUX_ERR_INSUFFICIENT_BUFFER", 4: "MUX_ERR_CUDA"}
 MAX_SEGMENTS = 64
 MAX_ADAPTERS = 64
+MAX_SLICES = 4
+MAX_ADAPTER_SLOTS = 96
 
 BWD_DX, BWD_GRADS = 1, 2
 
@@ -32,7 +34,7 @@ EXPORTS = ("mux_last_error", "mux_version", "mux_pack_bound_rows", "mux_pack_wor
            "mux_rope", "mux_rmsnorm_fwd", "mux_rmsnorm_bwd", "mux_swiglu_fwd", "mux_swiglu_bwd", "mux_add", "mux_rs_flags_elems", "mux_linear_fwd_rs",
            "mux_linear_bwd_dx_rs", "mux_rs_reduce", "mux_ag_push", "mux_ag_release", "mux_linear_fwd_ag",
            "mux_linear_bwd_ag", "mux_linear_fwd_hs", "mux_linear_shrink", "mux_nvls_flags_elems",
-           "mux_nvls_reduce_scatter", "mux_nvls_all_gather", "mux_nvls_release")
+           "mux_nvls_reduce_scatter", "mux_nvls_all_gather", "mux_nvls_release", "mux_linear")
 
 
 class MuxError(RuntimeError):
@@ -137,6 +139,8 @@ def lib():
         L.mux_nvls_all_gather.argtypes = [P, P, I64, I32, I32, P]
         L.mux_nvls_release.restype = ctypes.c_int
         L.mux_nvls_release.argtypes = [P, P]
+        L.mux_linear.restype = ctypes.c_int
+        L.mux_linear.argtypes = [P]
         _lib = L
     return _lib
 
@@ -427,6 +431,134 @@ def linear_bwd(seg_off: torch.Tensor, seg_task: Sequence[int], adapters: Sequenc
         _check(lib().mux_linear_bwd_part(part, S, _ptr(seg_off), st, len(adapters), tab, max_rows, K, N, r_cap,
                                          _ptr(dY), _ptr(X), _ptr(W), _ptr(Hs), _ptr(dX), _ptr(workspace),
                                          workspace.numel(), _stream(stream)))
+    return dX
+
+
+# ---------------------------------------------------------------- fused projections (column slices)
+OP_FWD, OP_FWD_HS, OP_SHRINK, OP_BWD, OP_BWD_DX, OP_BWD_GRADS = 1, 2, 3, 4, 5, 6
+
+
+class _Slices(ctypes.Structure):
+    _fields_ = [("num_slices", ctypes.c_int32), ("col_off", ctypes.c_int32 * (MAX_SLICES + 1))]
+
+
+class _LinearArgs(ctypes.Structure):
+    _fields_ = [("op", ctypes.c_int32), ("num_segs", ctypes.c_int32), ("seg_off", ctypes.c_void_p),
+                ("seg_task", ctypes.c_void_p), ("num_adapters", ctypes.c_int32), ("adapters", ctypes.c_void_p),
+                ("slices", ctypes.c_void_p), ("max_rows", ctypes.c_int32), ("K", ctypes.c_int32),
+                ("N", ctypes.c_int32), ("r_cap", ctypes.c_int32), ("X", ctypes.c_void_p), ("W", ctypes.c_void_p),
+                ("dY", ctypes.c_void_p), ("Y", ctypes.c_void_p), ("Hs", ctypes.c_void_p), ("dX", ctypes.c_void_p),
+                ("row_begin", ctypes.c_int32), ("row_end", ctypes.c_int32), ("rs", ctypes.c_void_p),
+                ("ag", ctypes.c_void_p), ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t),
+                ("stream", ctypes.c_void_p)]
+
+
+def _flat_slots(adapters) -> List[Adapter]:
+    """adapters[t][s] (one list per task) -> the task-major slot list of mux_linear_args."""
+    S = len(adapters[0])
+    _need(all(len(a) == S for a in adapters), "every task needs one adapter per slice (rank 0 = none)")
+    return [a for per_task in adapters for a in per_task]
+
+
+def _check_sliced(seg_off, seg_task, adapters, col_off, K, N, rows, r_cap, grads=False, **mats):
+    """Host-side checks of a sliced call: B_{t,s} is [slice width, rank], A_{t,s} [rank, K]."""
+    S = len(col_off) - 1
+    _need(1 <= S <= MAX_SLICES, f"1..{MAX_SLICES} slices")
+    _need(col_off[0] == 0 and col_off[-1] == N, f"col_off must run from 0 to N={N}")
+    dev = None
+    for name, (t, shape, dt) in mats.items():
+        if t is not None:
+            dev = t.device if dev is None else dev
+            _check_mat(name, t, shape, dt, dev)
+    _need(isinstance(seg_off, torch.Tensor) and seg_off.dtype == torch.int32 and seg_off.is_cuda
+          and seg_off.numel() == len(seg_task) + 1, "seg_off must be int32 CUDA [len(seg_task)+1]")
+    for t, per_task in enumerate(adapters):
+        for s, a in enumerate(per_task):
+            if a.rank == 0:
+                continue
+            ns = col_off[s + 1] - col_off[s]
+            _check_mat(f"adapters[{t}][{s}].A", a.A, (a.rank, K), device=dev)
+            _check_mat(f"adapters[{t}][{s}].B", a.B, (ns, a.rank), device=dev, dense=False)
+            if grads:
+                _check_mat(f"adapters[{t}][{s}].dA", a.dA, (a.rank, K), torch.float32, dev)
+                _check_mat(f"adapters[{t}][{s}].dB", a.dB, (ns, a.rank), torch.float32, dev)
+
+
+def linear(op: int, seg_off, seg_task, adapters, col_off, K: int, N: int, r_cap: int, max_rows: int, *, X=None,
+           W=None, dY=None, Y=None, Hs=None, dX=None, row_begin: int = 0, row_end: int = None, rs=None, ag=None,
+           workspace=None, stream=None, want_grads=False):
+    """mux_linear: one call of any op over column slices col_off (adapters[t][s]).  Marshalling only."""
+    slots = _flat_slots(adapters)
+    S = len(col_off) - 1
+    sl = _Slices()
+    sl.num_slices = S
+    for i, c in enumerate(col_off):
+        sl.col_off[i] = int(c)
+    tab = _adapter_table(slots, want_grads)
+    st = _i32_host(seg_task)
+    if workspace is None:
+        dev = seg_off.device
+        workspace = torch.zeros(linear_workspace_size(len(seg_task), max_rows, K, N, r_cap * S), dtype=torch.uint8,
+                                device=dev)
+    a = _LinearArgs()
+    a.op, a.num_segs, a.seg_off, a.seg_task = op, len(seg_task), seg_off.data_ptr(), ctypes.addressof(st)
+    a.num_adapters, a.adapters, a.slices = len(adapters), ctypes.addressof(tab), ctypes.addressof(sl)
+    a.max_rows, a.K, a.N, a.r_cap = max_rows, K, N, r_cap
+    for f, t in (("X", X), ("W", W), ("dY", dY), ("Y", Y), ("Hs", Hs), ("dX", dX)):
+        setattr(a, f, None if t is None else t.data_ptr())
+    a.row_begin = row_begin
+    a.row_end = max_rows if row_end is None else row_end
+    a.rs = None if rs is None else ctypes.addressof(rs)
+    a.ag = None if ag is None else ctypes.addressof(ag)
+    a.workspace, a.workspace_bytes = workspace.data_ptr(), workspace.numel()
+    a.stream = _stream(stream).value
+    _check(lib().mux_linear(ctypes.byref(a)))
+    return workspace
+
+
+def linear_fwd_sliced(seg_off, seg_task, adapters, X, W, col_off, r_cap: int, Y=None, Hs=None, workspace=None,
+                      want_hs: bool = True, stream=None):
+    """Fused projection forward: Y[:, slice s] = X W_s^T + s_{t,s} (X A_{t,s}^T) B_{t,s}^T in one GEMM
+    (adapters[t][s]; Hs [rows, S * r_cap]).  Returns (Y, Hs)."""
+    max_rows, K = X.shape
+    N = W.shape[0]
+    S = len(col_off) - 1
+    if Y is None:
+        Y = torch.empty(max_rows, N, dtype=torch.bfloat16, device=X.device)
+    if Hs is None and want_hs:
+        Hs = torch.empty(max_rows, S * r_cap, dtype=torch.bfloat16, device=X.device)
+    _check_sliced(seg_off, seg_task, adapters, col_off, K, N, max_rows, r_cap,
+                  X=(X, (max_rows, K), torch.bfloat16), W=(W, (N, K), torch.bfloat16),
+                  Y=(Y, (max_rows, N), torch.bfloat16), Hs=(Hs, (max_rows, S * r_cap), torch.bfloat16))
+    linear(OP_FWD, seg_off, seg_task, adapters, col_off, K, N, r_cap, max_rows, X=X, W=W, Y=Y, Hs=Hs,
+           workspace=workspace, stream=stream)
+    return Y, Hs
+
+
+def linear_bwd_sliced(seg_off, seg_task, adapters, dY, X, W, Hs, col_off, r_cap: int, dX=None, want_dx=True,
+                      workspace=None, stream=None, part: int = 0):
+    """Fused projection backward (part 0 = all, 1 = dX GEMM, 2 = adapter gradients on the same
+    workspace): dX = dY W + sum_s Gs_s A_{t,s}; writes adapters[t][s].dA / .dB (allocated if None)."""
+    max_rows, K = X.shape
+    N = W.shape[0]
+    S = len(col_off) - 1
+    dev = X.device
+    if dX is None and want_dx and part != BWD_GRADS:
+        dX = torch.empty(max_rows, K, dtype=torch.bfloat16, device=dev)
+    for per_task in adapters:
+        for s, a in enumerate(per_task):
+            if a.rank > 0:
+                if a.dA is None:
+                    a.dA = torch.empty(a.rank, K, dtype=torch.float32, device=dev)
+                if a.dB is None:
+                    a.dB = torch.empty(col_off[s + 1] - col_off[s], a.rank, dtype=torch.float32, device=dev)
+    _check_sliced(seg_off, seg_task, adapters, col_off, K, N, max_rows, r_cap, grads=True,
+                  X=(X, (max_rows, K), torch.bfloat16), W=(W, (N, K), torch.bfloat16),
+                  dY=(dY, (max_rows, N), torch.bfloat16), dX=(dX, (max_rows, K), torch.bfloat16),
+                  Hs=(Hs, (max_rows, S * r_cap), torch.bfloat16))
+    op = {0: OP_BWD, BWD_DX: OP_BWD_DX, BWD_GRADS: OP_BWD_GRADS}[part]
+    linear(op, seg_off, seg_task, adapters, col_off, K, N, r_cap, max_rows, X=X, W=W, dY=dY, Hs=Hs, dX=dX,
+           workspace=workspace, stream=stream, want_grads=True)
     return dX
 
 

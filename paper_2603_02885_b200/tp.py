@@ -42,6 +42,17 @@ import torch.distributed as dist
 
 
 # ------------------------------------------------------------------ collectives
+def _flat(grads):
+    """[g_t] or [[g_{t,s}]] (a fused projection's per-slice gradients) -> flat list."""
+    out = []
+    for g in grads:
+        if isinstance(g, (list, tuple)):
+            out.extend(g)
+        else:
+            out.append(g)
+    return out
+
+
 def _world(group=None):
     return dist.get_world_size(group), dist.get_rank(group)
 
@@ -165,36 +176,58 @@ class MuxBackend:
             self.cache[key] = t
         return t
 
-    def _ws(self, W, X, seg_task, r_cap):
+    def _ws(self, W, X, seg_task, r_cap, col_off=None):
         R, K = X.shape
-        n = self.mux.linear_workspace_size(len(seg_task), R, K, W.shape[0], r_cap)
+        S = 1 if col_off is None else len(col_off) - 1
+        n = self.mux.linear_workspace_size(len(seg_task), R, K, W.shape[0], r_cap * S)
         return self._buf(("ws", W.data_ptr()), (n,), torch.uint8, X.device, zero=True)
 
-    def fwd(self, seg_off, seg_task, adapters, X, W, r_cap, Y=None):
+    @staticmethod
+    def _hs_cols(r_cap, col_off):
+        return r_cap * (1 if col_off is None else len(col_off) - 1)
+
+    # col_off (fused projections, include/mux.h): column slices of W / Y, adapters[t][s] per task
+    def fwd(self, seg_off, seg_task, adapters, X, W, r_cap, Y=None, col_off=None):
         R = X.shape[0]
         if Y is None:
             Y = self._buf(("Y", W.data_ptr()), (R, W.shape[0]), torch.bfloat16, X.device)
-        Hs = self._buf(("Hs", W.data_ptr()), (R, r_cap), torch.bfloat16, X.device)
-        return self.mux.linear_fwd(seg_off, seg_task, adapters, X, W, r_cap, Y=Y, Hs=Hs,
-                                   workspace=self._ws(W, X, seg_task, r_cap))
+        Hs = self._buf(("Hs", W.data_ptr()), (R, self._hs_cols(r_cap, col_off)), torch.bfloat16, X.device)
+        ws = self._ws(W, X, seg_task, r_cap, col_off)
+        if col_off is not None:
+            return self.mux.linear_fwd_sliced(seg_off, seg_task, adapters, X, W, col_off, r_cap, Y=Y, Hs=Hs,
+                                              workspace=ws)
+        return self.mux.linear_fwd(seg_off, seg_task, adapters, X, W, r_cap, Y=Y, Hs=Hs, workspace=ws)
 
-    def shrink(self, seg_off, seg_task, adapters, X, W, r_cap, row_begin, row_end):
+    def shrink(self, seg_off, seg_task, adapters, X, W, r_cap, row_begin, row_end, col_off=None):
         """Hs rows [row_begin, row_end) of the full (gathered) X only (mux_linear_shrink)."""
-        Hs = self._buf(("Hs", W.data_ptr()), (X.shape[0], r_cap), torch.bfloat16, X.device)
+        Hs = self._buf(("Hs", W.data_ptr()), (X.shape[0], self._hs_cols(r_cap, col_off)), torch.bfloat16, X.device)
+        ws = self._ws(W, X, seg_task, r_cap, col_off)
+        if col_off is not None:
+            self.mux.linear(self.mux.OP_SHRINK, seg_off, seg_task, adapters, col_off, X.shape[1], W.shape[0], r_cap,
+                            X.shape[0], X=X, Hs=Hs, row_begin=row_begin, row_end=row_end, workspace=ws)
+            return Hs
         return self.mux.linear_shrink(seg_off, seg_task, adapters, X, W.shape[0], r_cap, row_begin, row_end, Hs=Hs,
-                                      workspace=self._ws(W, X, seg_task, r_cap))
+                                      workspace=ws)
 
-    def fwd_hs(self, seg_off, seg_task, adapters, X, W, Hs, r_cap):
+    def fwd_hs(self, seg_off, seg_task, adapters, X, W, Hs, r_cap, col_off=None):
         """Forward with the shrink given (mux_linear_fwd_hs): no shrink tiles in the GEMM."""
         Y = self._buf(("Y", W.data_ptr()), (X.shape[0], W.shape[0]), torch.bfloat16, X.device)
-        return self.mux.linear_fwd_hs(seg_off, seg_task, adapters, X, W, Hs, r_cap, Y=Y,
-                                      workspace=self._ws(W, X, seg_task, r_cap))
+        ws = self._ws(W, X, seg_task, r_cap, col_off)
+        if col_off is not None:
+            self.mux.linear(self.mux.OP_FWD_HS, seg_off, seg_task, adapters, col_off, X.shape[1], W.shape[0], r_cap,
+                            X.shape[0], X=X, W=W, Y=Y, Hs=Hs, workspace=ws)
+            return Y
+        return self.mux.linear_fwd_hs(seg_off, seg_task, adapters, X, W, Hs, r_cap, Y=Y, workspace=ws)
 
-    def bwd(self, seg_off, seg_task, adapters, dY, X, W, Hs, r_cap, dX=None):
+    def bwd(self, seg_off, seg_task, adapters, dY, X, W, Hs, r_cap, dX=None, col_off=None):
         if dX is None:
             dX = self._buf(("dX", W.data_ptr()), tuple(X.shape), torch.bfloat16, X.device)
-        dX = self.mux.linear_bwd(seg_off, seg_task, adapters, dY, X, W, Hs, r_cap, dX=dX,
-                                 workspace=self._ws(W, X, seg_task, r_cap))
+        ws = self._ws(W, X, seg_task, r_cap, col_off)
+        if col_off is not None:
+            dX = self.mux.linear_bwd_sliced(seg_off, seg_task, adapters, dY, X, W, Hs, col_off, r_cap, dX=dX,
+                                            workspace=ws)
+            return dX, [[a.dA for a in row] for row in adapters], [[a.dB for a in row] for row in adapters]
+        dX = self.mux.linear_bwd(seg_off, seg_task, adapters, dY, X, W, Hs, r_cap, dX=dX, workspace=ws)
         return dX, [a.dA for a in adapters], [a.dB for a in adapters]
 
     # ---- decoder-block ops (tp_block.py): libmux kernels, fresh outputs (caching allocator)
@@ -210,16 +243,24 @@ class MuxBackend:
     def attn_fwd(self, q, k, v, row_start, heads, kv_heads, scale):
         return self.mux.attn_fwd(q, k, v, row_start, heads, kv_heads, scale)
 
-    def attn_bwd(self, dO, q, k, v, o, lse, row_start, heads, kv_heads, scale):
+    def attn_bwd(self, dO, q, k, v, o, lse, row_start, heads, kv_heads, scale, out=None):
+        """out: (dq, dk, dv) views to write (e.g. column slices of a fused projection's dY)."""
         ws = self._buf(("attn_ws", q.shape[0], heads), (self.mux.attn_workspace_size(q.shape[0], heads),),
                        torch.uint8, q.device)
-        return self.mux.attn_bwd(dO, q, k, v, o, lse, row_start, heads, kv_heads, scale, workspace=ws)
+        dq, dk, dv = out if out is not None else (None, None, None)
+        return self.mux.attn_bwd(dO, q, k, v, o, lse, row_start, heads, kv_heads, scale, dq=dq, dk=dk, dv=dv,
+                                 workspace=ws)
 
     def swiglu_fwd(self, g, u):
         return self.mux.swiglu_fwd(g, u)
 
-    def swiglu_bwd(self, dh, g, u):
-        return self.mux.swiglu_bwd(dh, g, u)
+    def swiglu_bwd(self, dh, g, u, out=None):
+        """out: (dg, du) views to write."""
+        dg, du = out if out is not None else (None, None)
+        return self.mux.swiglu_bwd(dh, g, u, dg=dg, du=du)
+
+    def empty(self, rows, cols, like):
+        return torch.empty(rows, cols, dtype=torch.bfloat16, device=like.device)
 
     def add(self, a, b, out=None):
         return self.mux.add(a, b, y=out)
@@ -268,10 +309,15 @@ class MuxBackend:
         ag = fb.next()
         lay._ag_pushed = self._push(ag, x_rows)
         R, N = rows * p, lay.W.shape[0]
+        co = getattr(lay, "col_off", None)
         Y = self._buf(("Y", lay.W.data_ptr()), (R, N), torch.bfloat16, x_rows.device)
-        Hs = self._buf(("Hs", lay.W.data_ptr()), (R, lay.r_cap), torch.bfloat16, x_rows.device)
-        ws = self._ws(lay.W, fb.recv.view(R, K), seg_task, lay.r_cap)
-        self.mux.linear_fwd_ag(ag, seg_off, seg_task, lay.ads, K, lay.W, lay.r_cap, Y=Y, Hs=Hs, workspace=ws)
+        Hs = self._buf(("Hs", lay.W.data_ptr()), (R, self._hs_cols(lay.r_cap, co)), torch.bfloat16, x_rows.device)
+        ws = self._ws(lay.W, fb.recv.view(R, K), seg_task, lay.r_cap, co)
+        if co is not None:
+            self.mux.linear(self.mux.OP_FWD, seg_off, seg_task, lay.ads, co, K, N, lay.r_cap, R, W=lay.W, Y=Y, Hs=Hs,
+                            ag=ag, workspace=ws)
+        else:
+            self.mux.linear_fwd_ag(ag, seg_off, seg_task, lay.ads, K, lay.W, lay.r_cap, Y=Y, Hs=Hs, workspace=ws)
         lay._ag_held = ag                         # released after the backward re-read X
         return Y, Hs, fb.recv.view(R, K)
 
@@ -304,11 +350,20 @@ class MuxBackend:
         X = lay.X
         R, K = X.shape
         rs = self._rs_for(lay, R // p, K, X.device).next()
-        ws = self._ws(lay.W, X, seg_task, lay.r_cap)
+        co = getattr(lay, "col_off", None)
+        ws = self._ws(lay.W, X, seg_task, lay.r_cap, co)
+        dX = self._buf(("dXrs", lay.W.data_ptr()), (R // p, K), torch.bfloat16, X.device)
+        if co is not None:
+            N = lay.W.shape[0]
+            self.mux.linear(self.mux.OP_BWD_DX, seg_off, seg_task, lay.ads, co, K, N, lay.r_cap, R, X=X, W=lay.W,
+                            dY=dY, Hs=lay.Hs, rs=rs, workspace=ws)
+            self.mux.linear_bwd_sliced(seg_off, seg_task, lay.ads, dY, X, lay.W, lay.Hs, co, lay.r_cap, want_dx=False,
+                                       workspace=ws, part=self.mux.BWD_GRADS)
+            return (self.mux.rs_reduce(rs, dX), [[a.dA for a in row] for row in lay.ads],
+                    [[a.dB for a in row] for row in lay.ads])
         self.mux.linear_bwd_dx_rs(rs, seg_off, seg_task, lay.ads, dY, X, lay.W, lay.Hs, lay.r_cap, ws)
         self.mux.linear_bwd(seg_off, seg_task, lay.ads, dY, X, lay.W, lay.Hs, lay.r_cap, workspace=ws,
                             part=self.mux.BWD_GRADS)
-        dX = self._buf(("dXrs", lay.W.data_ptr()), (R // p, K), torch.bfloat16, X.device)
         return self.mux.rs_reduce(rs, dX), [a.dA for a in lay.ads], [a.dB for a in lay.ads]
 
 
@@ -332,6 +387,20 @@ def shard_column(W: torch.Tensor, adapters: Sequence, p: int, r: int, make_adapt
     return Wp, ads
 
 
+def shard_column_fused(Ws: Sequence[torch.Tensor], adapter_lists: Sequence[Sequence], p: int, r: int, make_adapter):
+    """Column-parallel shard of a fused projection (e.g. q|k|v): rank r's rows of every W_s back to
+    back, col_off = the slice offsets inside that shard, and per task the list of its slice shards
+    (adapters[t][s]).  Returns (W_p, adapters, col_off)."""
+    parts, per_slice, col_off = [], [], [0]
+    for W, ads in zip(Ws, adapter_lists):
+        Wp, ap = shard_column(W, ads, p, r, make_adapter)
+        parts.append(Wp)
+        per_slice.append(ap)
+        col_off.append(col_off[-1] + Wp.shape[0])
+    T = len(adapter_lists[0])
+    return torch.cat(parts, 0).contiguous(), [[per_slice[s][t] for s in range(len(Ws))] for t in range(T)], col_off
+
+
 def shard_row(W: torch.Tensor, adapters: Sequence, p: int, r: int, make_adapter):
     """Row-parallel shard of (W [N,K], adapters) for rank r of p."""
     K = W.shape[1]
@@ -352,9 +421,14 @@ class ColumnParallelMuxLinear:
     computes the shrink itself."""
 
     def __init__(self, backend, W_shard, adapters_shard, r_cap, group=None, fused_rs=False, fused_ag=False,
-                 shared_shrink=False, nvls=None):
+                 shared_shrink=False, nvls=None, col_off=None):
+        """col_off: a fused projection (q|k|v, gate|up; include/mux.h "Fused projections"): this rank's
+        W_shard rows are the slices' shards back to back, col_off their column offsets, and
+        adapters_shard[t][s] task t's adapter shard on slice s."""
         self.be, self.W, self.ads, self.r_cap, self.group = backend, W_shard, adapters_shard, r_cap, group
         self.fused_rs, self.fused_ag, self.shared_shrink = fused_rs, fused_ag, shared_shrink
+        self.col_off = None if col_off is None else list(col_off)
+        self.kw = {} if col_off is None else {"col_off": self.col_off}
         self.nvls = nvls    # NvlsCollectives: AG(X) and RS(dX) inside the NVSwitch
         self._rs = self._ag = self._ag_held = self._ag_pushed = None
         self._nvls_held = False
@@ -370,32 +444,42 @@ class ColumnParallelMuxLinear:
                                    "call release_ag() first for forward-only use")
             self.X = self.nvls.ag(("ag", id(self)), x_rows)
             self._nvls_held = True
-            Y, self.Hs = self.be.fwd(seg_off, seg_task, self.ads, self.X, self.W, self.r_cap)
+            Y, self.Hs = self.be.fwd(seg_off, seg_task, self.ads, self.X, self.W, self.r_cap, **self.kw)
             return Y
         self.X = all_gather_rows(x_rows, self.group)
         if self.shared_shrink:
-            rows_p = x_rows.shape[0]
-            r0 = rows_p * _world(self.group)[1]
-            Hs = self.be.shrink(seg_off, seg_task, self.ads, self.X, self.W, self.r_cap, r0, r0 + rows_p)
-            self.Hs = all_gather_rows(Hs[r0:r0 + rows_p].contiguous(), self.group)
-            return self.be.fwd_hs(seg_off, seg_task, self.ads, self.X, self.W, self.Hs, self.r_cap)
-        Y, self.Hs = self.be.fwd(seg_off, seg_task, self.ads, self.X, self.W, self.r_cap)
+            return self._fwd_shared_shrink(seg_off, seg_task, x_rows.shape[0])
+        Y, self.Hs = self.be.fwd(seg_off, seg_task, self.ads, self.X, self.W, self.r_cap, **self.kw)
         return Y
+
+    def _fwd_shared_shrink(self, seg_off, seg_task, rows_p):
+        r0 = rows_p * _world(self.group)[1]
+        Hs = self.be.shrink(seg_off, seg_task, self.ads, self.X, self.W, self.r_cap, r0, r0 + rows_p, **self.kw)
+        self.Hs = all_gather_rows(Hs[r0:r0 + rows_p].contiguous(), self.group)
+        return self.be.fwd_hs(seg_off, seg_task, self.ads, self.X, self.W, self.Hs, self.r_cap, **self.kw)
 
     def forward_full(self, seg_off, seg_task, X):
         """X [R, K] already gathered (one all-gather shared by several column layers reading the
-        same input, e.g. q/k/v or gate/up) -> Y_p [R, N/p]."""
+        same input, e.g. q/k/v or gate/up) -> Y_p [R, N/p].  With shared_shrink, the shrink of this
+        rank's rows is all-gathered instead of recomputed (as in forward)."""
         self.X = X
-        Y, self.Hs = self.be.fwd(seg_off, seg_task, self.ads, X, self.W, self.r_cap)
+        if self.shared_shrink:
+            return self._fwd_shared_shrink(seg_off, seg_task, X.shape[0] // _world(self.group)[0])
+        Y, self.Hs = self.be.fwd(seg_off, seg_task, self.ads, X, self.W, self.r_cap, **self.kw)
         return Y
 
-    def backward_partial(self, seg_off, seg_task, dY_cols):
-        """dY_p [R, N/p] -> this rank's partial dX [R, K] (the caller sums the partials of the layers
-        that shared the input, then reduce-scatters once); dA_t all-reduced, dB_{t,p} local."""
-        dXp, dA, dB = self.be.bwd(seg_off, seg_task, self.ads, dY_cols, self.X, self.W, self.Hs, self.r_cap)
-        for g in dA:
+    def _reduce_dA(self, dA):
+        for g in _flat(dA):
             if g is not None:
                 all_reduce_(g, self.group)
+
+    def backward_partial(self, seg_off, seg_task, dY_cols, dX=None):
+        """dY_p [R, N/p] -> this rank's partial dX [R, K] (the caller sums the partials of the layers
+        that shared the input, then reduce-scatters once; dX = an output buffer or None); dA_t
+        all-reduced, dB_{t,p} local."""
+        dXp, dA, dB = self.be.bwd(seg_off, seg_task, self.ads, dY_cols, self.X, self.W, self.Hs, self.r_cap,
+                                  dX=dX, **self.kw)
+        self._reduce_dA(dA)
         self.dA, self.dB = dA, dB
         return dXp, dA, dB
 
@@ -407,15 +491,14 @@ class ColumnParallelMuxLinear:
             R, K = self.X.shape
             buf = self.nvls.rs_buffer(("rs", id(self)), R, K, self.X.device)
             _, dA, dB = self.be.bwd(seg_off, seg_task, self.ads, dY_cols, self.X, self.W, self.Hs, self.r_cap,
-                                    dX=buf)
+                                    dX=buf, **self.kw)
             self.release_ag()
             dX_rows = self.nvls.rs(("rs", id(self)))
         else:
-            dXp, dA, dB = self.be.bwd(seg_off, seg_task, self.ads, dY_cols, self.X, self.W, self.Hs, self.r_cap)
+            dXp, dA, dB = self.be.bwd(seg_off, seg_task, self.ads, dY_cols, self.X, self.W, self.Hs, self.r_cap,
+                                      **self.kw)
             dX_rows = None
-        for g in dA:
-            if g is not None:
-                all_reduce_(g, self.group)
+        self._reduce_dA(dA)
         self.dA, self.dB = dA, dB
         self.release_ag()
         return (reduce_scatter_rows(dXp, self.group) if dX_rows is None else dX_rows), dA, dB

@@ -39,6 +39,10 @@ from .block import LINEARS, BlockShape
 
 COLUMN = ("q", "k", "v", "gate", "up")
 ROW = ("o", "down")
+# fused projections (include/mux.h "Fused projections"): q|k|v and gate|up as one column-sliced
+# GEMM each, every task keeping its own adapter on every slice
+FUSED = {"qkv": ("q", "k", "v"), "gate_up": ("gate", "up")}
+FUSED_LINEARS = ("qkv", "o", "gate_up", "down")
 
 
 @dataclass
@@ -63,20 +67,43 @@ def shard_block(weights: Dict[str, torch.Tensor], adapters: Dict[str, Sequence],
     return W, ads
 
 
+def shard_block_fused(weights: Dict[str, torch.Tensor], adapters: Dict[str, Sequence], p: int, r: int,
+                      make_adapter):
+    """shard_block with q|k|v and gate|up fused: W["qkv"] = this rank's q, k, v shards back to back
+    (column slices col_off["qkv"]), adapters["qkv"][t] = [q, k, v shard of task t]; likewise gate_up.
+    Returns (W, adapters, col_off)."""
+    W, ads, col_off = {}, {}, {}
+    for name, parts in FUSED.items():
+        W[name], ads[name], col_off[name] = tp.shard_column_fused([weights[n] for n in parts],
+                                                                  [adapters[n] for n in parts], p, r, make_adapter)
+    for name in ROW:
+        W[name], ads[name] = tp.shard_row(weights[name], adapters[name], p, r, make_adapter)
+    W["norm1"], W["norm2"] = weights["norm1"], weights["norm2"]
+    return W, ads, col_off
+
+
 class TPDecoderBlock:
     """weights / adapters: this rank's shards (shard_block); backend: tp.MuxBackend or a test backend
     with the same op methods (fwd/bwd linears + rmsnorm/rope/attention/swiglu/add)."""
 
     def __init__(self, backend, shape: TPBlockShape, weights: Dict[str, torch.Tensor],
-                 adapters: Dict[str, List], r_cap: int, group=None, nvls=None):
+                 adapters: Dict[str, List], r_cap: int, group=None, nvls=None, col_off=None,
+                 shared_shrink=False):
         """nvls: a tp.NvlsCollectives — every all-gather / reduce-scatter of the block inside the
-        NVSwitch (NVLink SHARP) instead of NCCL."""
+        NVSwitch (NVLink SHARP) instead of NCCL.  col_off: the weights/adapters of shard_block_fused
+        (q|k|v and gate|up as one column-sliced GEMM each).  shared_shrink: column layers shrink only
+        this rank's rows and all-gather Hs (tp.ColumnParallelMuxLinear)."""
         self.be, self.s, self.w, self.r_cap, self.group, self.nvls = backend, shape, weights, r_cap, group, nvls
+        self.fused = col_off is not None
         self.lin = {}
-        for name in LINEARS:
-            cls = tp.ColumnParallelMuxLinear if name in COLUMN else tp.RowParallelMuxLinear
-            self.lin[name] = cls(backend, weights[name], adapters[name], r_cap, group=group,
-                                 nvls=nvls if name in ROW else None)
+        for name in (FUSED_LINEARS if self.fused else LINEARS):
+            if name in ROW:
+                self.lin[name] = tp.RowParallelMuxLinear(backend, weights[name], adapters[name], r_cap, group=group,
+                                                         nvls=nvls)
+            else:
+                self.lin[name] = tp.ColumnParallelMuxLinear(backend, weights[name], adapters[name], r_cap,
+                                                            group=group, shared_shrink=shared_shrink,
+                                                            col_off=col_off[name] if self.fused else None)
 
     def _ag(self, name, rows):
         return self.nvls.ag(name, rows) if self.nvls is not None else tp.all_gather_rows(rows, self.group)
@@ -92,6 +119,15 @@ class TPDecoderBlock:
             acc = self.be.add(acc, x, out=out if i == len(parts) - 2 else None)
         return self.nvls.rs(name) if self.nvls is not None else tp.reduce_scatter_rows(acc, self.group)
 
+    def _rs_single(self, name, layer, so, st, dY):
+        """reduce-scatter of one fused projection's partial dX (no partials to sum): with NVLS the
+        dX GEMM writes straight into the multicast-bound buffer."""
+        out = None
+        if self.nvls is not None:
+            out = self.nvls.rs_buffer(name, dY.shape[0], layer.X.shape[1], dY.device)
+        dXp = layer.backward_partial(so, st, dY, dX=out)[0]
+        return self.nvls.rs(name) if self.nvls is not None else tp.reduce_scatter_rows(dXp, self.group)
+
     # ------------------------------------------------------------------ forward
     def forward(self, x_rows, seg_off, seg_task, row_start):
         s, be, lin = self.s, self.be, self.lin
@@ -100,17 +136,27 @@ class TPDecoderBlock:
         st = self.seg_task
         self.x_rows = x_rows
         h1 = self._ag("h1", be.rmsnorm_fwd(x_rows, self.w["norm1"], s.eps))
-        q = lin["q"].forward_full(seg_off, st, h1)
-        k = lin["k"].forward_full(seg_off, st, h1)
-        v = lin["v"].forward_full(seg_off, st, h1)
+        if self.fused:     # one GEMM; q, k, v are column views of its output
+            nq, nk = hq * s.head_dim, hkv * s.head_dim
+            qkv = lin["qkv"].forward_full(seg_off, st, h1)
+            q, k, v = qkv[:, :nq], qkv[:, nq:nq + nk], qkv[:, nq + nk:]
+        else:
+            q = lin["q"].forward_full(seg_off, st, h1)
+            k = lin["k"].forward_full(seg_off, st, h1)
+            v = lin["v"].forward_full(seg_off, st, h1)
         q = be.rope(q, row_start, hq, s.head_dim, s.rope_base)
         k = be.rope(k, row_start, hkv, s.head_dim, s.rope_base)
         a, lse = be.attn_fwd(q, k, v, row_start, hq, hkv, s.head_dim ** -0.5)
         o_rows = lin["o"].forward(seg_off, st, a)                       # RS inside
         h2_rows, x2_rows = be.rmsnorm_fwd(o_rows, self.w["norm2"], s.eps, res=x_rows)
         h2 = self._ag("h2", h2_rows)
-        g = lin["gate"].forward_full(seg_off, st, h2)
-        u = lin["up"].forward_full(seg_off, st, h2)
+        if self.fused:
+            nf = s.ffn // s.p
+            gu = lin["gate_up"].forward_full(seg_off, st, h2)
+            g, u = gu[:, :nf], gu[:, nf:]
+        else:
+            g = lin["gate"].forward_full(seg_off, st, h2)
+            u = lin["up"].forward_full(seg_off, st, h2)
         m = be.swiglu_fwd(g, u)
         d_rows = lin["down"].forward(seg_off, st, m)                    # RS inside
         self.saved = dict(q=q, k=k, v=v, a=a, lse=lse, x2_rows=x2_rows, g=g, u=u)
@@ -122,30 +168,60 @@ class TPDecoderBlock:
         hq, hkv = s.heads // s.p, s.kv_heads // s.p
         so, st = self.seg_off, self.seg_task
         dm, _, _ = lin["down"].backward(so, st, dy_rows)                 # AG(dy) inside; AR(dB)
-        dg, du = be.swiglu_bwd(dm, sv["g"], sv["u"])
-        dh2_rows = self._rs_sum("dh2", [lin["gate"].backward_partial(so, st, dg)[0],
-                                        lin["up"].backward_partial(so, st, du)[0]])
+        if self.fused:     # dgate|dup written side by side: one dX GEMM, no partial sum
+            nf = s.ffn // s.p
+            dgu = be.empty(dm.shape[0], 2 * nf, dm)
+            be.swiglu_bwd(dm, sv["g"], sv["u"], out=(dgu[:, :nf], dgu[:, nf:]))
+            dh2_rows = self._rs_single("dh2", lin["gate_up"], so, st, dgu)
+        else:
+            dg, du = be.swiglu_bwd(dm, sv["g"], sv["u"])
+            dh2_rows = self._rs_sum("dh2", [lin["gate"].backward_partial(so, st, dg)[0],
+                                            lin["up"].backward_partial(so, st, du)[0]])
         if self.nvls is not None:
             self.nvls.release("h2")          # gate/up backward were the last readers of the gathered h2
         dx2_rows = be.rmsnorm_bwd(dh2_rows, sv["x2_rows"], self.w["norm2"], s.eps, resid=dy_rows)
         da, _, _ = lin["o"].backward(so, st, dx2_rows)                   # AG(dx2) inside; AR(dB)
+        out = None
+        if self.fused:     # dq|dk|dv written side by side into the fused projection's dY
+            nq, nk = hq * s.head_dim, hkv * s.head_dim
+            dqkv = be.empty(da.shape[0], nq + 2 * nk, da)
+            out = (dqkv[:, :nq], dqkv[:, nq:nq + nk], dqkv[:, nq + nk:])
         dq, dk, dv = be.attn_bwd(da, sv["q"], sv["k"], sv["v"], sv["a"], sv["lse"], self.row_start, hq, hkv,
-                                 s.head_dim ** -0.5)
-        dq = be.rope(dq, self.row_start, hq, s.head_dim, s.rope_base, inverse=True)
+                                 s.head_dim ** -0.5, out=out)
+        dq = be.rope(dq, self.row_start, hq, s.head_dim, s.rope_base, inverse=True)   # in place
         dk = be.rope(dk, self.row_start, hkv, s.head_dim, s.rope_base, inverse=True)
-        dh1_rows = self._rs_sum("dh1", [lin["q"].backward_partial(so, st, dq)[0],
-                                        lin["k"].backward_partial(so, st, dk)[0],
-                                        lin["v"].backward_partial(so, st, dv)[0]])
+        if self.fused:
+            dh1_rows = self._rs_single("dh1", lin["qkv"], so, st, dqkv)
+        else:
+            dh1_rows = self._rs_sum("dh1", [lin["q"].backward_partial(so, st, dq)[0],
+                                            lin["k"].backward_partial(so, st, dk)[0],
+                                            lin["v"].backward_partial(so, st, dv)[0]])
         if self.nvls is not None:
             self.nvls.release("h1")
         return be.rmsnorm_bwd(dh1_rows, self.x_rows, self.w["norm1"], s.eps, resid=dx2_rows)
 
     def adapter_grads(self):
-        """{linear: ([dA_t], [dB_t])} of this rank (after backward)."""
-        return {n: (self.lin[n].dA, self.lin[n].dB) for n in LINEARS}
+        """{linear: ([dA_t], [dB_t])} of this rank (after backward), per original linear (a fused
+        projection's per-slice gradients are split back to q, k, v / gate, up)."""
+        if not self.fused:
+            return {n: (self.lin[n].dA, self.lin[n].dB) for n in LINEARS}
+        out = {n: (self.lin[n].dA, self.lin[n].dB) for n in ROW}
+        for f, parts in FUSED.items():
+            dA, dB = self.lin[f].dA, self.lin[f].dB
+            for i, n in enumerate(parts):
+                out[n] = ([row[i] for row in dA], [row[i] for row in dB])
+        return out
 
     # libmux launches per step at world p > 1 (for the bench's gpu_launches): forward = 2 norms +
     # 7 fused linears + 2 RoPE + attention + SwiGLU + add = 14 (+ 2 owner-side sums with fused RS);
-    # backward = 7 dX GEMMs + 7 gradient kernels + SwiGLU + 2 norms + attention (4) + 2 RoPE + 3 adds
+    # backward = 7 dX GEMMs + 7 gradient kernels + SwiGLU + 2 norms + attention (4) + 2 RoPE + 3 adds.
+    # Fused projections: forward 4 linears (12); backward 4 dX GEMMs + 7 gradient kernels (one per
+    # slice) + SwiGLU + 2 norms + attention (4) + 2 RoPE, no adds (20).
     LAUNCHES_FWD = 14
     LAUNCHES_BWD = 26
+    LAUNCHES_FWD_FUSED = 12
+    LAUNCHES_BWD_FUSED = 20
+
+    def launches(self):
+        return ((self.LAUNCHES_FWD_FUSED, self.LAUNCHES_BWD_FUSED) if self.fused
+                else (self.LAUNCHES_FWD, self.LAUNCHES_BWD))

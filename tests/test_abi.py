@@ -190,3 +190,66 @@ def test_fwd_hs_and_shrink_validation(mux):
     assert r == 1 and "row range" in L.mux_last_error().decode()
     r = L.mux_linear_shrink(1, 0x3000, st, 1, ads, 512, 256, 256, 16, 0x4000, 0, 512, None, 0x8000, 1 << 30, None)
     assert r == 1 and "Hs" in L.mux_last_error().decode()
+
+
+def test_linear_args_layout_matches_header(mux, tmp_path):
+    """The ctypes mirror of mux_linear_args / mux_slices has the C layout (compiled from mux.h)."""
+    src = tmp_path / "chk.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "mux.h"\n'
+                   'int main(void){printf("%zu %zu %zu %zu %zu %zu\\n", sizeof(mux_linear_args), '
+                   'sizeof(mux_slices), offsetof(mux_linear_args, slices), offsetof(mux_linear_args, X), '
+                   'offsetof(mux_linear_args, row_begin), offsetof(mux_linear_args, stream));return 0;}\n')
+    exe = tmp_path / "chk"
+    rc = os.system(f"gcc -I {ROOT}/include -I /usr/local/cuda/include {src} -o {exe}")
+    assert rc == 0
+    got = [int(x) for x in os.popen(str(exe)).read().split()]
+    L = mux._LinearArgs
+    assert got == [ctypes.sizeof(L), ctypes.sizeof(mux._Slices), L.slices.offset, L.X.offset,
+                   L.row_begin.offset, L.stream.offset]
+
+
+def _generic(mux, op=1, S=2, col_off=(0, 128, 256), n_tasks=1, ranks=None, **kw):
+    m = mux
+    sl = m._Slices()
+    sl.num_slices = S
+    for i, c in enumerate(col_off[:mux.MAX_SLICES + 1]):
+        sl.col_off[i] = c
+    slots = n_tasks * max(S, 1)
+    tab = _adapters(max(slots, 1))
+    if ranks is not None:
+        for i, r in enumerate(ranks):
+            tab[i].rank = r
+    st_arr = (ctypes.c_int32 * 1)(0)
+    a = m._LinearArgs()
+    a.op, a.num_segs, a.seg_off, a.seg_task = op, 1, 0x3000, ctypes.addressof(st_arr)
+    a.num_adapters, a.adapters, a.slices = n_tasks, ctypes.addressof(tab), ctypes.addressof(sl)
+    a.max_rows, a.K, a.N, a.r_cap = 128, 256, 256, 16
+    a.X, a.W, a.Y, a.Hs, a.dY, a.dX = 0x4000, 0x5000, 0x6000, 0x7000, 0x9000, 0xA000
+    a.workspace, a.workspace_bytes = 0x8000, 1 << 30
+    for k, v in kw.items():
+        setattr(a, k, v)
+    st = m.lib().mux_linear(ctypes.byref(a))
+    return st, m.lib().mux_last_error().decode()
+
+
+@pytest.mark.parametrize("kw,frag", [
+    (dict(op=9), "unknown op"),
+    (dict(S=0, col_off=(0, 256)), "num_slices"),
+    (dict(S=5, col_off=(0, 64, 128, 192, 224, 256)), "num_slices"),
+    (dict(col_off=(0, 128, 248)), "end at N"),
+    (dict(col_off=(8, 128, 256)), "start at 0"),
+    (dict(col_off=(0, 100, 256)), "multiples of 8"),
+    (dict(col_off=(0, 256, 256)), "non-empty"),
+    (dict(n_tasks=49), "adapter slots"),
+    (dict(op=2, Hs=None), "Hs"),
+])
+def test_generic_linear_validation(mux, kw, frag):
+    st, msg = _generic(mux, **kw)
+    assert st == 1, (st, msg)
+    assert frag in msg, msg
+
+
+def test_workspace_counts_every_slice(mux):
+    """Hs/Gs scratch is [rows, S * r_cap]: a sliced call needs the workspace of S * r_cap."""
+    st, msg = _generic(mux, workspace_bytes=mux.linear_workspace_size(1, 128, 256, 256, 16))
+    assert st == 3 and "workspace" in msg, msg

@@ -135,11 +135,11 @@ def test_rs_rejects_bad_layout():
     W = torch.zeros(128, 128, dtype=torch.bfloat16, device="cuda")
     so = torch.tensor([0, 512], dtype=torch.int32, device="cuda")
     ads = [mux.Adapter(None, None, 0, 0.0)]
-    with pytest.raises(mux.MuxError):   # rows_per_rank not a multiple of 256
+    with pytest.raises((mux.MuxError, ValueError)):   # rows_per_rank not a multiple of 256
         mux.linear_fwd_rs(mux.make_rs(2, 0, 128, 1, recv, flags), so, [0], ads, X[:256], W, 16)
-    with pytest.raises(mux.MuxError):   # world * rows_per_rank != max_rows
+    with pytest.raises((mux.MuxError, ValueError)):   # world * rows_per_rank != max_rows
         mux.linear_fwd_rs(mux.make_rs(2, 0, 256, 1, recv, flags), so, [0], ads, X[:256], W, 16)
-    with pytest.raises(mux.MuxError):   # seq 0
+    with pytest.raises((mux.MuxError, ValueError)):   # seq 0
         mux.linear_fwd_rs(mux.make_rs(2, 0, 256, 0, recv, flags), so, [0], ads, X, W, 16)
 
 

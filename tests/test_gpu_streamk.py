@@ -95,6 +95,9 @@ def test_linear_and_rs_suites_under_forced_streamk():
     env = dict(os.environ, MUX_SK="1")
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu",
                         os.path.join(HERE, "test_gpu_linear.py"), os.path.join(HERE, "test_gpu_rs.py"),
-                        "-k", "not debug_build"],
+                        # fwd vs fwd_hs bit identity does not hold under stream-K: with and without shrink
+                        # tiles the balanced k-ranges split the main tiles at different k-blocks, so the
+                        # fp32 partials are summed in a different order (both within tolerance)
+                        "-k", "not debug_build and not given_hs_bit_identical"],
                        capture_output=True, text=True, env=env, cwd=os.path.dirname(HERE), timeout=1500)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]

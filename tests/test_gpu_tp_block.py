@@ -40,7 +40,11 @@ def _rel(a, b):
     return float((a.float() - b.float()).abs().max() / b.float().abs().max().clamp_min(1e-30))
 
 
-def test_tp_block_world1_matches_block(pg):
+@pytest.mark.parametrize("fused,shared_shrink", [(False, False), (True, False), (True, True)])
+def test_tp_block_world1_matches_block(pg, fused, shared_shrink):
+    """fused: q|k|v and gate|up as one column-sliced GEMM each (include/mux.h "Fused projections");
+    the output columns of a slice get the same backbone sum and the same adapter product (plus exact
+    zeros where a tile straddles two slices), so the forward is still the DecoderBlock's bit for bit."""
     g = torch.Generator(device="cuda").manual_seed(17)
     shape = BlockShape(hidden=256, ffn=384, heads=2, kv_heads=1)
     lens = [100, 30, 200, 64, 1, 50]
@@ -81,15 +85,22 @@ def test_tp_block_world1_matches_block(pg):
     torch.cuda.synchronize()
 
     mk = lambda A, B, r, s: mux.Adapter(A, B, r, s)  # noqa: E731
-    Wp, ap = tp_block.shard_block(W, ads2, 1, 0, mk)
+    col_off = None
+    if fused:
+        Wp, ap, col_off = tp_block.shard_block_fused(W, ads2, 1, 0, mk)
+    else:
+        Wp, ap = tp_block.shard_block(W, ads2, 1, 0, mk)
     tshape = tp_block.TPBlockShape(hidden=256, ffn=384, heads=2, kv_heads=1, p=1)
-    blk = tp_block.TPDecoderBlock(tp.MuxBackend(), tshape, Wp, ap, 16)
+    blk = tp_block.TPDecoderBlock(tp.MuxBackend(), tshape, Wp, ap, 16, col_off=col_off, shared_shrink=shared_shrink)
     for _ in range(2):   # twice: cached buffers are reused
         y = blk.forward(x, pk["seg_off"], st, rs)
         dx = blk.backward(dy)
     torch.cuda.synchronize()
-    assert torch.equal(y.view(torch.int16), y_ref.view(torch.int16))
-    assert _rel(dx, dx_ref) <= 2e-2
+    # rows >= seg_off[M] belong to no segment: the linears leave them unwritten (mux.h), so the block's
+    # output there is whatever the buffers held; compare the packed rows
+    n = int(mux.read_info(pk["info"])["total_rows"])
+    assert torch.equal(y[:n].view(torch.int16), y_ref[:n].view(torch.int16))
+    assert _rel(dx[:n], dx_ref[:n]) <= 2e-2
     got = blk.adapter_grads()
     for n in LINEARS:
         for t in range(M):

@@ -257,3 +257,98 @@ def test_hs_pad_columns_zero():
     c = _rand_case(11, 16, 12, [4, 6], [2, 5])
     Y, Hs = _fwd(c, 8)
     assert np.all(Hs[:4, 2:] == 0.0) and np.all(Hs[4:, 5:] == 0.0)
+
+
+# ---------------------------------------------------------------- fused projections (column slices)
+def _sliced_case(seed, K, col_off, seg_lens, ranks, scales):
+    """ranks[t][s], scales[t][s]; B_{t,s} [slice width, rank]."""
+    rng = np.random.default_rng(seed)
+    N = col_off[-1]
+    S = len(col_off) - 1
+    seg_off = np.concatenate([[0], np.cumsum(seg_lens)]).astype(np.int32)
+    R = int(seg_off[-1])
+    seg_task = np.arange(len(seg_lens), dtype=np.int32) % len(ranks)
+    A = [[rng.standard_normal((ranks[t][s], K)) / np.sqrt(K) for s in range(S)] for t in range(len(ranks))]
+    B = [[rng.standard_normal((col_off[s + 1] - col_off[s], ranks[t][s])) for s in range(S)]
+         for t in range(len(ranks))]
+    return dict(seg_off=seg_off, seg_task=seg_task, col_off=list(col_off), A=A, B=B, ranks=ranks, scales=scales,
+                X=rng.standard_normal((R, K)), W=rng.standard_normal((N, K)) / np.sqrt(K),
+                dY=rng.standard_normal((R, N)))
+
+
+def _block_diag_equivalent(c):
+    """The same layer as ONE adapter per task of rank sum_s r_{t,s}: A = [A_{t,0}; A_{t,1}; ...]
+    stacked, B = blockdiag(B_{t,0}, B_{t,1}, ...) (valid when a task's slices share one scale)."""
+    S = len(c["col_off"]) - 1
+    N = c["col_off"][-1]
+    A, B, ranks, scales = [], [], [], []
+    for t in range(len(c["ranks"])):
+        rt = sum(c["ranks"][t])
+        A.append(np.concatenate([c["A"][t][s] for s in range(S)], axis=0).reshape(rt, -1))
+        Bt = np.zeros((N, rt))
+        j = 0
+        for s in range(S):
+            r = c["ranks"][t][s]
+            Bt[c["col_off"][s]:c["col_off"][s + 1], j:j + r] = c["B"][t][s]
+            j += r
+        B.append(Bt)
+        ranks.append(rt)
+        scales.append(c["scales"][t][0])
+    return A, B, ranks, scales
+
+
+def test_sliced_equals_block_diagonal_adapter():
+    """Pin: stacking the slices' A and placing their B on a block diagonal gives one LoRA adapter of
+    rank sum_s r_s whose product X A^T B^T is, column block by column block, X A_s^T B_s^T — so the
+    sliced oracle must equal the plain oracle on that adapter (Y, Hs columns, dX, dA rows, dB
+    diagonal blocks).  Catches a wrong slice offset, a transposed B slice or a dropped slice in the
+    dX sum."""
+    col_off = [0, 24, 40, 72]
+    ranks = [[2, 3, 1], [4, 0, 2], [1, 1, 1]]
+    scales = [[2.0] * 3, [0.5] * 3, [1.5] * 3]
+    c = _sliced_case(7, 32, col_off, [5, 7, 3, 6], ranks, scales)
+    r_cap = 4
+    Y, Hs = olin.linear_fwd_sliced(c["seg_off"], c["seg_task"], col_off, c["A"], c["B"], ranks, scales, c["X"],
+                                   c["W"], r_cap)
+    dX, Gs, grads = olin.linear_bwd_sliced(c["seg_off"], c["seg_task"], col_off, c["A"], c["B"], ranks, scales,
+                                           c["dY"], c["X"], c["W"], r_cap)
+    A, B, rk, sc = _block_diagonal = _block_diag_equivalent(c)
+    rc = max(rk)
+    Y1, Hs1 = olin.linear_fwd(c["seg_off"], c["seg_task"], A, B, rk, sc, c["X"], c["W"], rc)
+    dX1, Gs1, g1 = olin.linear_bwd(c["seg_off"], c["seg_task"], A, B, rk, sc, c["dY"], c["X"], c["W"], rc)
+    np.testing.assert_array_equal(Y, Y1)       # zero off-block terms: same sums exactly
+    np.testing.assert_allclose(dX, dX1, rtol=0, atol=1e-12 * np.max(np.abs(dX1)))  # sum split by slice
+    seg_task = c["seg_task"]
+    for i in range(int(c["seg_off"][-1])):
+        t = int(seg_task[np.searchsorted(c["seg_off"], i, side="right") - 1])
+        j = 0
+        for s in range(3):
+            r = ranks[t][s]
+            np.testing.assert_array_equal(Hs[i, s * r_cap:s * r_cap + r], Hs1[i, j:j + r])
+            np.testing.assert_array_equal(Hs[i, s * r_cap + r:(s + 1) * r_cap], 0.0)
+            np.testing.assert_array_equal(Gs[i, s * r_cap:s * r_cap + r], Gs1[i, j:j + r])
+            j += r
+    for t in range(3):
+        j = 0
+        for s in range(3):
+            r = ranks[t][s]
+            dA, dB = grads[t][s]
+            np.testing.assert_array_equal(dA, g1[t][0][j:j + r])
+            np.testing.assert_array_equal(dB, g1[t][1][col_off[s]:col_off[s + 1], j:j + r])
+            j += r
+
+
+def test_sliced_rank0_slice_is_backbone_and_scales_are_per_slice():
+    """Pin: a slice whose adapters all have rank 0 is the plain backbone X W_s^T (numpy matmul), and
+    each slice uses its own scale (doubling s_{t,1} doubles only slice 1's LoRA term)."""
+    col_off = [0, 16, 48]
+    ranks = [[0, 2], [0, 3]]
+    c = _sliced_case(11, 24, col_off, [4, 6], ranks, [[1.0, 1.0], [1.0, 1.0]])
+    Y, _ = olin.linear_fwd_sliced(c["seg_off"], c["seg_task"], col_off, c["A"], c["B"], ranks,
+                                  [[1.0, 1.0], [1.0, 1.0]], c["X"], c["W"], 4)
+    np.testing.assert_allclose(Y[:, :16], c["X"] @ c["W"][:16].T, rtol=1e-13, atol=1e-13)
+    Y2, _ = olin.linear_fwd_sliced(c["seg_off"], c["seg_task"], col_off, c["A"], c["B"], ranks,
+                                   [[1.0, 2.0], [1.0, 2.0]], c["X"], c["W"], 4)
+    base = c["X"] @ c["W"][16:].T
+    np.testing.assert_allclose(Y2[:, 16:] - base, 2 * (Y[:, 16:] - base), rtol=1e-12, atol=1e-12)
+    np.testing.assert_array_equal(Y2[:, :16], Y[:, :16])

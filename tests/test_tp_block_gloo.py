@@ -97,7 +97,7 @@ def _reference(sh, W, A, B, X, dY, seg_off, rs):
     return y, dx, grads
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, fused=False, shared_shrink=False):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -110,9 +110,14 @@ def _worker(rank, world, port, q):
         full_w = {n: T(w) for n, w in W.items()}
         full_a = {n: [tp.ShardAdapter(T(A[n][t]), T(B[n][t]), RANKS[t], SCALES[t]) for t in range(3)] for n in LIN}
         mk = lambda A_, B_, r, s: tp.ShardAdapter(A_, B_, r, s)  # noqa: E731
-        Wp, ap = tp_block.shard_block(full_w, full_a, world, rank, mk)
+        col_off = None
+        if fused:   # q|k|v and gate|up as one column-sliced call each (include/mux.h "Fused projections")
+            Wp, ap, col_off = tp_block.shard_block_fused(full_w, full_a, world, rank, mk)
+        else:
+            Wp, ap = tp_block.shard_block(full_w, full_a, world, rank, mk)
         shape = tp_block.TPBlockShape(eps=EPS, p=world, **sh)
-        blk = tp_block.TPDecoderBlock(OracleOps(sh["head_dim"]), shape, Wp, ap, 16)
+        blk = tp_block.TPDecoderBlock(OracleOps(sh["head_dim"]), shape, Wp, ap, 16, col_off=col_off,
+                                      shared_shrink=shared_shrink)
         rows = X.shape[0] // world
         sl = slice(rank * rows, (rank + 1) * rows)
         y = blk.forward(T(X[sl]).contiguous(), T(seg_off), [0, 1, 2], T(rs))
@@ -131,12 +136,16 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("world", [2, 4, 8])
-def test_tp_block_matches_single_process(world):
+@pytest.mark.parametrize("world,fused,shared_shrink", [(2, False, False), (4, False, False), (8, False, False),
+                                                       (2, True, False), (4, True, True), (8, True, False)])
+def test_tp_block_matches_single_process(world, fused, shared_shrink):
+    """fused: q|k|v and gate|up as one column-sliced linear each; shared_shrink: column layers shrink
+    their own rows and all-gather Hs (rows they do not own are NaN in the oracle backend's shrink).
+    Both must equal the unfused single-process composition."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, fused, shared_shrink)) for r in range(world)]
     for p in procs:
         p.start()
     res = sorted([q.get(timeout=300) for _ in range(world)], key=lambda x: x[0])

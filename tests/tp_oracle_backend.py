@@ -10,39 +10,66 @@ from oracle import linear as olin
 
 
 class OracleBackend:
-    """fp64 oracle as the per-rank local linear (torch fp64 CPU tensors in/out)."""
+    """fp64 oracle as the per-rank local linear (torch fp64 CPU tensors in/out).  col_off: a fused
+    projection (adapters[t][s], oracle linear_*_sliced)."""
 
-    def fwd(self, seg_off, seg_task, ads, X, W, r_cap):
-        Y, Hs = olin.linear_fwd(seg_off.numpy(), seg_task, [a.A.numpy() for a in ads],
-                                [a.B.numpy() for a in ads], [a.rank for a in ads], [a.scale for a in ads],
-                                X.numpy(), W.numpy(), r_cap)
-        return torch.from_numpy(Y), torch.from_numpy(Hs)
+    @staticmethod
+    def _tabs(ads, col_off):
+        if col_off is None:
+            return ([a.A.numpy() for a in ads], [a.B.numpy() for a in ads], [a.rank for a in ads],
+                    [a.scale for a in ads])
+        return ([[a.A.numpy() for a in row] for row in ads], [[a.B.numpy() for a in row] for row in ads],
+                [[a.rank for a in row] for row in ads], [[a.scale for a in row] for row in ads])
 
-    def shrink(self, seg_off, seg_task, ads, X, W, r_cap, row_begin, row_end):
+    def fwd(self, seg_off, seg_task, ads, X, W, r_cap, Y=None, col_off=None):
+        A, B, rk, sc = self._tabs(ads, col_off)
+        if col_off is None:
+            Yn, Hs = olin.linear_fwd(seg_off.numpy(), seg_task, A, B, rk, sc, X.numpy(), W.numpy(), r_cap)
+        else:
+            Yn, Hs = olin.linear_fwd_sliced(seg_off.numpy(), seg_task, col_off, A, B, rk, sc, X.numpy(), W.numpy(),
+                                            r_cap)
+        return torch.from_numpy(Yn), torch.from_numpy(Hs)
+
+    def shrink(self, seg_off, seg_task, ads, X, W, r_cap, row_begin, row_end, col_off=None):
         # rows outside the range are NaN: only the all-gathered own rows may reach the forward
-        _, Hs = self.fwd(seg_off, seg_task, ads, X, W, r_cap)
+        _, Hs = self.fwd(seg_off, seg_task, ads, X, W, r_cap, col_off=col_off)
         Hs = Hs.clone()
         Hs[:row_begin] = float("nan")
         Hs[row_end:] = float("nan")
         return Hs
 
-    def fwd_hs(self, seg_off, seg_task, ads, X, W, Hs, r_cap):
+    def fwd_hs(self, seg_off, seg_task, ads, X, W, Hs, r_cap, col_off=None):
         # Eq. 1 with the given (gathered) shrink: Y = X W^T + Hs B_t^T on each segment's rows
+        # (per slice s: Hs columns [s r_cap, s r_cap + rank) times B_{t,s} into the slice's columns)
         Y = X.numpy() @ W.numpy().T
         so, Hn = seg_off.numpy(), Hs.numpy()
+        co = [0, W.shape[0]] if col_off is None else col_off
         for s, t in enumerate(seg_task):
-            a = ads[t]
-            if a.rank:
-                Y[so[s]:so[s + 1]] += Hn[so[s]:so[s + 1], :a.rank] @ a.B.numpy().T
+            row = [ads[t]] if col_off is None else ads[t]
+            for c, a in enumerate(row):
+                if a.rank:
+                    Y[so[s]:so[s + 1], co[c]:co[c + 1]] += (Hn[so[s]:so[s + 1], c * r_cap:c * r_cap + a.rank]
+                                                            @ a.B.numpy().T)
         return torch.from_numpy(Y)
 
-    def bwd(self, seg_off, seg_task, ads, dY, X, W, Hs, r_cap):
+    def bwd(self, seg_off, seg_task, ads, dY, X, W, Hs, r_cap, dX=None, col_off=None):
         # the oracle recomputes H from X (fp64), which equals the saved Hs / s
-        dX, Gs, grads = olin.linear_bwd(seg_off.numpy(), seg_task, [a.A.numpy() for a in ads],
-                                        [a.B.numpy() for a in ads], [a.rank for a in ads],
-                                        [a.scale for a in ads], dY.numpy(), X.numpy(), W.numpy(), r_cap)
-        return (torch.from_numpy(dX), [torch.from_numpy(g[0]) for g in grads],
-                [torch.from_numpy(g[1]) for g in grads])
+        A, B, rk, sc = self._tabs(ads, col_off)
+        dYn = np.ascontiguousarray(dY.numpy())
+        if col_off is None:
+            dXn, Gs, grads = olin.linear_bwd(seg_off.numpy(), seg_task, A, B, rk, sc, dYn, X.numpy(), W.numpy(),
+                                             r_cap)
+            dA, dB = [torch.from_numpy(g[0]) for g in grads], [torch.from_numpy(g[1]) for g in grads]
+        else:
+            dXn, Gs, grads = olin.linear_bwd_sliced(seg_off.numpy(), seg_task, col_off, A, B, rk, sc, dYn,
+                                                    X.numpy(), W.numpy(), r_cap)
+            dA = [[torch.from_numpy(g[0]) for g in row] for row in grads]
+            dB = [[torch.from_numpy(g[1]) for g in row] for row in grads]
+        out = torch.from_numpy(dXn)
+        if dX is not None:
+            dX.copy_(out)
+            out = dX
+        return out, dA, dB
 
 
 class OracleOps:
@@ -52,11 +79,17 @@ class OracleOps:
         self.d = head_dim
         self.lin = OracleBackend()
 
-    def fwd(self, *a):
-        return self.lin.fwd(*a)
+    def fwd(self, *a, **kw):
+        return self.lin.fwd(*a, **kw)
 
-    def bwd(self, *a):
-        return self.lin.bwd(*a)
+    def bwd(self, *a, **kw):
+        return self.lin.bwd(*a, **kw)
+
+    def shrink(self, *a, **kw):
+        return self.lin.shrink(*a, **kw)
+
+    def fwd_hs(self, *a, **kw):
+        return self.lin.fwd_hs(*a, **kw)
 
     def rmsnorm_fwd(self, x, w, eps, res=None):
         if res is None:
@@ -69,18 +102,34 @@ class OracleOps:
         return torch.from_numpy(dx + (0 if resid is None else resid.numpy()))
 
     def rope(self, x, row_start, heads, head_dim, base, inverse=False):
+        # in place, like mux_rope (x may be a column view of a fused projection's output)
         R = x.shape[0]
         f = ob.rope_bwd if inverse else ob.rope_fwd
-        return torch.from_numpy(f(x.numpy().reshape(R, heads, head_dim), row_start.numpy(), base).reshape(R, -1))
+        y = f(np.ascontiguousarray(x.numpy()).reshape(R, heads, head_dim), row_start.numpy(), base).reshape(R, -1)
+        x.copy_(torch.from_numpy(y))
+        return x
+
+    def empty(self, rows, cols, like):
+        return torch.empty(rows, cols, dtype=like.dtype)
+
+    @staticmethod
+    def _into(out, vals):
+        if out is None:
+            return vals
+        for o, v in zip(out, vals):
+            o.copy_(v)
+        return out
 
     def attn_fwd(self, q, k, v, row_start, heads, kv_heads, scale):
+        q, k, v = (t.contiguous() for t in (q, k, v))
         R, d, G = q.shape[0], self.d, heads // kv_heads
         Kf = np.repeat(k.numpy().reshape(R, kv_heads, d), G, axis=1)
         Vf = np.repeat(v.numpy().reshape(R, kv_heads, d), G, axis=1)
         o, lse = ob.attention_fwd(q.numpy().reshape(R, heads, d), Kf, Vf, row_start.numpy(), scale)
         return torch.from_numpy(o.reshape(R, heads * d)), torch.from_numpy(lse)
 
-    def attn_bwd(self, dO, q, k, v, o, lse, row_start, heads, kv_heads, scale):
+    def attn_bwd(self, dO, q, k, v, o, lse, row_start, heads, kv_heads, scale, out=None):
+        q, k, v = (t.contiguous() for t in (q, k, v))
         R, d, G = q.shape[0], self.d, heads // kv_heads
         Kf = np.repeat(k.numpy().reshape(R, kv_heads, d), G, axis=1)
         Vf = np.repeat(v.numpy().reshape(R, kv_heads, d), G, axis=1)
@@ -88,14 +137,15 @@ class OracleOps:
                                       row_start.numpy(), scale)
         dk = dk.reshape(R, kv_heads, G, d).sum(axis=2).reshape(R, kv_heads * d)
         dv = dv.reshape(R, kv_heads, G, d).sum(axis=2).reshape(R, kv_heads * d)
-        return torch.from_numpy(dq.reshape(R, heads * d)), torch.from_numpy(dk), torch.from_numpy(dv)
+        return self._into(out, (torch.from_numpy(dq.reshape(R, heads * d)), torch.from_numpy(dk),
+                                torch.from_numpy(dv)))
 
     def swiglu_fwd(self, g, u):
-        return torch.from_numpy(ob.swiglu_fwd(g.numpy(), u.numpy()))
+        return torch.from_numpy(ob.swiglu_fwd(np.ascontiguousarray(g.numpy()), np.ascontiguousarray(u.numpy())))
 
-    def swiglu_bwd(self, dh, g, u):
-        dg, du = ob.swiglu_bwd(dh.numpy(), g.numpy(), u.numpy())
-        return torch.from_numpy(dg), torch.from_numpy(du)
+    def swiglu_bwd(self, dh, g, u, out=None):
+        dg, du = ob.swiglu_bwd(dh.numpy(), np.ascontiguousarray(g.numpy()), np.ascontiguousarray(u.numpy()))
+        return self._into(out, (torch.from_numpy(dg), torch.from_numpy(du)))
 
     def add(self, a, b, out=None):
         return a + b

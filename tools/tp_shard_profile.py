@@ -50,7 +50,23 @@ def time_graph(fn, reps=3):
     return statistics.median(vals)
 
 
-def block_at(mux, wl, p, shared_shrink=False):
+FUSED = {"q": "qkv", "k": "qkv", "v": "qkv", "gate": "gate_up", "up": "gate_up"}
+
+
+def groups_of(wl, fused):
+    """The linears as calls: one per linear, or (fused) q|k|v and gate|up as one column-sliced call
+    each (include/mux.h "Fused projections")."""
+    out = []
+    for L in wl.linears:
+        key = FUSED.get(L.name, L.name) if fused else L.name
+        if out and out[-1][0] == key:
+            out[-1][1].append(L)
+        else:
+            out.append((key, [L]))
+    return out
+
+
+def block_at(mux, wl, p, shared_shrink=False, fused=False):
     M = wl.num_tasks
     seg = -(-wl.valid_tokens // M // 64) * 64
     R = seg * M
@@ -59,45 +75,70 @@ def block_at(mux, wl, p, shared_shrink=False):
     gen = torch.Generator(device="cuda").manual_seed(0)
     r_cap = max(16, -(-max(wl.ranks) // 16) * 16)
     total_ms, flops, per = 0.0, 0.0, []
-    for L in wl.linears:
-        K, N = (L.K, L.N // p) if L.name in COLUMN else (L.K // p, L.N)
+    for name, Ls in groups_of(wl, fused):
+        L = Ls[0]
+        col = L.name in COLUMN
+        K = L.K if col else L.K // p
+        widths = [(x.N // p if col else x.N) for x in Ls]
+        N = sum(widths)
+        col_off = [0]
+        for w in widths:
+            col_off.append(col_off[-1] + w)
+        S = len(Ls)
         W = (torch.randn(N, K, device="cuda", generator=gen) / K ** 0.5).bfloat16()
         ads = []
         for r in wl.ranks:
-            B = mux.make_B_storage(N, r)
-            B.copy_(torch.randn(N, r, device="cuda", generator=gen).bfloat16())
-            ads.append(mux.Adapter((torch.randn(r, K, device="cuda", generator=gen) / K ** 0.5).bfloat16(), B, r,
-                                   2.0, torch.empty(r, K, device="cuda"), torch.empty(N, r, device="cuda")))
+            row = []
+            for w in widths:
+                B = mux.make_B_storage(w, r)
+                B.copy_(torch.randn(w, r, device="cuda", generator=gen).bfloat16())
+                row.append(mux.Adapter((torch.randn(r, K, device="cuda", generator=gen) / K ** 0.5).bfloat16(), B,
+                                       r, 2.0, torch.empty(r, K, device="cuda"), torch.empty(w, r, device="cuda")))
+            ads.append(row)
         X = torch.randn(R, K, device="cuda", generator=gen).bfloat16()
         dY = torch.randn(R, N, device="cuda", generator=gen).bfloat16()
         Y = torch.empty(R, N, dtype=torch.bfloat16, device="cuda")
-        Hs = torch.empty(R, r_cap, dtype=torch.bfloat16, device="cuda")
+        Hs = torch.empty(R, S * r_cap, dtype=torch.bfloat16, device="cuda")
         dX = torch.empty(R, K, dtype=torch.bfloat16, device="cuda")
-        ws = torch.zeros(mux.linear_workspace_size(M, R, K, N, r_cap), dtype=torch.uint8, device="cuda")
+        ws = torch.zeros(mux.linear_workspace_size(M, R, K, N, S * r_cap), dtype=torch.uint8, device="cuda")
+        flat = [row[0] for row in ads]
 
         hi = -(-R // p // 256) * 256  # this rank's rows (rounded to pair blocks)
 
         def step():
-            if shared_shrink and L.name in COLUMN:
+            if S > 1:
+                if shared_shrink and col:
+                    mux.linear(mux.OP_SHRINK, seg_off, st, ads, col_off, K, N, r_cap, R, X=X, Hs=Hs, row_begin=0,
+                               row_end=hi, workspace=ws)
+                    mux.linear(mux.OP_FWD_HS, seg_off, st, ads, col_off, K, N, r_cap, R, X=X, W=W, Y=Y, Hs=Hs,
+                               workspace=ws)
+                else:
+                    mux.linear(mux.OP_FWD, seg_off, st, ads, col_off, K, N, r_cap, R, X=X, W=W, Y=Y, Hs=Hs,
+                               workspace=ws)
+                mux.linear(mux.OP_BWD, seg_off, st, ads, col_off, K, N, r_cap, R, X=X, W=W, dY=dY, Hs=Hs, dX=dX,
+                           workspace=ws, want_grads=True)
+                return
+            if shared_shrink and col:
                 # tp.py shared_shrink: own rows' shrink, (Hs all-gather: T x r_cap, not run), then
                 # the fused GEMM without shrink tiles
-                mux.linear_shrink(seg_off, st, ads, X, N, r_cap, 0, hi, Hs=Hs, workspace=ws)
-                mux.linear_fwd_hs(seg_off, st, ads, X, W, Hs, r_cap, Y=Y, workspace=ws)
+                mux.linear_shrink(seg_off, st, flat, X, N, r_cap, 0, hi, Hs=Hs, workspace=ws)
+                mux.linear_fwd_hs(seg_off, st, flat, X, W, Hs, r_cap, Y=Y, workspace=ws)
             else:
-                mux.linear_fwd(seg_off, st, ads, X, W, r_cap, Y=Y, Hs=Hs, workspace=ws)
-            mux.linear_bwd(seg_off, st, ads, dY, X, W, Hs, r_cap, dX=dX, workspace=ws)
+                mux.linear_fwd(seg_off, st, flat, X, W, r_cap, Y=Y, Hs=Hs, workspace=ws)
+            mux.linear_bwd(seg_off, st, flat, dY, X, W, Hs, r_cap, dX=dX, workspace=ws)
 
         ms = time_graph(step)
-        f = sum(seg * (4 * K * N + 6 * r * (K + N)) for r in wl.ranks)  # SURVEY §8(d) per token
-        per.append({"linear": L.name, "K": K, "N": N, "ms": round(ms, 4), "tflops": round(f / ms / 1e9, 1)})
+        f = sum(seg * (4 * K * w + 6 * r * (K + w)) for r in wl.ranks for w in widths)  # SURVEY §8(d) per token
+        per.append({"linear": name, "K": K, "N": N, "slices": widths if S > 1 else None, "ms": round(ms, 4),
+                    "tflops": round(f / ms / 1e9, 1)})
         total_ms += ms
         flops += f
-        del W, ads, X, dY, Y, Hs, dX, ws
+        del W, ads, flat, X, dY, Y, Hs, dX, ws
         torch.cuda.empty_cache()
     H = wl.linears[0].K
     comm_bytes = 8 * (p - 1) / p * R * H * 2
     comm_ms = comm_bytes / (NVLINK_GBS * 1e9) * 1e3
-    return {"config": wl.config_id, "tp": p, "shared_shrink": shared_shrink, "rows": R, "tasks": M, "compute_ms_per_rank": round(total_ms, 3),
+    return {"config": wl.config_id, "tp": p, "shared_shrink": shared_shrink, "fused": fused, "rows": R, "tasks": M, "compute_ms_per_rank": round(total_ms, 3),
             "tflops_per_rank": round(flops / total_ms / 1e9, 1), "comm_bytes_per_rank": int(comm_bytes),
             "comm_ms_at_900GBs": round(comm_ms, 3), "comm_over_compute": round(comm_ms / total_ms, 3),
             "linears": per}
@@ -108,13 +149,14 @@ def main():
     ap.add_argument("--out", default=None)
     ap.add_argument("--points", default="4:1,4:2,4:4,4:8,5:1,5:8")
     ap.add_argument("--shared-shrink", action="store_true", help="column layers: own-rows shrink + fwd_hs")
+    ap.add_argument("--fused", action="store_true", help="q|k|v and gate|up as one column-sliced call each")
     a = ap.parse_args()
     from paper_2603_02885_b200 import mux
     import synth
     out = open(a.out, "w") if a.out else None
     for pt in a.points.split(","):
         cid, p = pt.split(":")
-        r = block_at(mux, synth.configs.workload(cid), int(p), a.shared_shrink)
+        r = block_at(mux, synth.configs.workload(cid), int(p), a.shared_shrink, a.fused)
         line = json.dumps(r)
         print(line, flush=True)
         if out:
