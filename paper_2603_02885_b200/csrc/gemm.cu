@@ -27,6 +27,14 @@
 // tasks; their adapter MMAs carry the tcgen05 disable-output-lane mask of every
 // other task's rows, so a row is only ever multiplied by its own task's
 // weights (NaN isolation).
+// Fused projections (num_slices > 1, e.g. q|k|v): every task has one adapter per
+// column slice of W.  A side tile then computes the shrink of every slice in one
+// pass over A: per (task group, slice pair) unit, CTA rk stages slice 2 sp + rk of
+// the adapter, so one N = 128 MMA yields two slices (TMEM columns 64 s); a main
+// tile runs one extension block per (task, slice overlapping the tile), the
+// slice's B_t rows addressed relative to the slice start so rows outside it are
+// TMA zero fill (a tile straddling two slices runs both).  The dX tiles run an
+// extension block per (task, slice): Gs_s A_{t,s} contributes to every column.
 // Side tiles come first in their band (or, for reductions <= 2048, before all
 // main tiles) and never wait, so every dependency points to a lower tile
 // index: with all CTAs resident the lowest unfinished tile always progresses

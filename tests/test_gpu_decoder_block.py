@@ -73,8 +73,7 @@ def _oracle_block(shape, W, A, B, ranks, scales, seg_off, seg_task, rs, X, dY, r
     return y, dx, grads, inter
 
 
-@pytest.mark.parametrize("kv_heads", [2, 1])
-def test_decoder_block_matches_oracle(kv_heads):
+def _inputs(kv_heads):
     shape = BlockShape(hidden=256, ffn=384, heads=2, kv_heads=kv_heads)
     task_lens = [np.array([100, 30], np.int32), np.array([200], np.int32), np.array([64, 1, 50], np.int32)]
     ranks, scales = [4, 8, 16], [2.0, 2.0, 2.0]
@@ -114,6 +113,18 @@ def test_decoder_block_matches_oracle(kv_heads):
             Bst = mux.make_B_storage(dims[n][1], r)
             Bst.copy_(to_dev_bf16(Bb[n][t]))
             ads[n].append(mux.Adapter(to_dev_bf16(Ab[n][t]), Bst, r, scales[t]))
+    return dict(shape=shape, ranks=ranks, scales=scales, r_cap=r_cap, M=M, lens=lens, ref=ref, max_rows=max_rows,
+                Wb=Wb, Ab=Ab, Bb=Bb, Xtok=Xtok, dYb=dYb, pk=pk, rs_dev=rs_dev, x=x, W=W, ads=ads)
+
+
+@pytest.mark.parametrize("kv_heads", [2, 1])
+def test_decoder_block_matches_oracle(kv_heads):
+    I = _inputs(kv_heads)  # noqa: E741
+    shape, ranks, scales, r_cap, M, lens, ref, max_rows = (I[k] for k in ("shape", "ranks", "scales", "r_cap", "M",
+                                                                          "lens", "ref", "max_rows"))
+    Wb, Ab, Bb, Xtok, dYb, pk, rs_dev, x, W, ads = (I[k] for k in ("Wb", "Ab", "Bb", "Xtok", "dYb", "pk", "rs_dev",
+                                                                  "x", "W", "ads"))
+    dims = shape.linear_dims()
     blk = DecoderBlock(shape, W, ads, r_cap)
     y = blk.forward(x, pk["seg_off"], list(range(M)), rs_dev)
     dx = blk.backward(to_dev_bf16(dYb))
@@ -197,3 +208,40 @@ def test_decoder_block_matches_oracle(kv_heads):
     worst = max(errs.values())
     print("end-to-end worst", worst, sorted(errs.items(), key=lambda kv: -kv[1])[:6])
     assert worst <= E2E_TOL, errs
+
+
+@pytest.mark.parametrize("kv_heads", [2, 1])
+def test_fused_projection_block_matches_oracle(kv_heads):
+    """q|k|v and gate|up as one column-sliced GEMM each (DecoderBlock(fused=True), include/mux.h
+    "Fused projections"): the forward equals the unfused block bit for bit (each output column gets
+    the same backbone sum and adapter product, plus exact zeros where a tile straddles two slices);
+    dx and every adapter gradient are within the end-to-end bound of the all-fp64 composition
+    (the slices' dX partials are summed in fp32 inside the GEMM instead of in the norm's backward)."""
+    I = _inputs(kv_heads)  # noqa: E741
+    shape, r_cap, M, max_rows = I["shape"], I["r_cap"], I["M"], I["max_rows"]
+    ref_blk = DecoderBlock(shape, I["W"], I["ads"], r_cap)
+    y_ref = ref_blk.forward(I["x"], I["pk"]["seg_off"], list(range(M)), I["rs_dev"]).clone()
+    ads2 = {n: [mux.Adapter(a.A, a.B, a.rank, a.scale) for a in I["ads"][n]] for n in LINEARS}
+    blk = DecoderBlock(shape, I["W"], ads2, r_cap, fused=True)
+    y = blk.forward(I["x"], I["pk"]["seg_off"], list(range(M)), I["rs_dev"])
+    dx = blk.backward(to_dev_bf16(I["dYb"]))
+    torch.cuda.synchronize()
+    valid_rows = torch.from_numpy(I["ref"]["row_src"] >= 0).cuda()
+    assert torch.equal(y[valid_rows].view(torch.int16), y_ref[valid_rows].view(torch.int16))
+    f = bf16_to_f64
+    ref = I["ref"]
+    rs = ob.row_seq_start(ref["seq_row"], I["lens"], max_rows)
+    X = np.zeros((max_rows, shape.hidden))
+    X[ref["row_src"] >= 0] = f(I["Xtok"])[ref["row_src"][ref["row_src"] >= 0]]
+    Wo = {n: f(b) for n, b in I["Wb"].items()}
+    Ao = {n: [f(a) for a in I["Ab"][n]] for n in LINEARS}
+    Bo = {n: [f(b) for b in I["Bb"][n]] for n in LINEARS}
+    ry, rdx, rgrads, _ = _oracle_block(shape, Wo, Ao, Bo, I["ranks"], I["scales"], ref["seg_off"], list(range(M)), rs,
+                                       X, f(I["dYb"]), r_cap)
+    valid = rs >= 0
+    errs = {"y": rel_err(f(from_dev_bf16(y))[valid], ry[valid]), "dx": rel_err(f(from_dev_bf16(dx))[valid], rdx[valid])}
+    for n in LINEARS:
+        for t in range(M):
+            errs[f"dA_{n}{t}"] = rel_err(ads2[n][t].dA.cpu().numpy(), rgrads[n][t][0])
+            errs[f"dB_{n}{t}"] = rel_err(ads2[n][t].dB.cpu().numpy(), rgrads[n][t][1])
+    assert max(errs.values()) <= E2E_TOL, errs
