@@ -35,6 +35,13 @@ sys.path.insert(0, ROOT)
 
 import synth  # noqa: E402
 
+# fused projections (q|k|v, gate|up as one column-sliced GEMM): the interleaved GEMM A/B in
+# profiles/r02_fused_ab_v2.jsonl has the fused call at 0.68-0.99x the time of the separate calls (the
+# gain grows as the shards narrow: 0.69 for TP-8 q|k|v dX); whole steps at full width are a wash
+# (profiles/r02_bench_{tp4,block4}_ab.jsonl: TP arm at world 1 +0.5 %, the one-GPU block -1.8 %, the
+# attention and SwiGLU then read strided column views).  So auto fuses where a shard is narrower than
+# the full 4096-wide 7B projections (every TP > 1 shard, and config 5's 1024-wide k/v)
+FUSE_BELOW_COLS = 4096
 METRIC = "multiplexed tokens/s fwd+bwd at 1/2/4/8 B200; % of BF16 tensor-core peak"
 UNIT = "tokens/s"
 
@@ -811,7 +818,11 @@ def _tp_block(args, w, torch, mux, tp, Backend, world, rank):
         Bs.copy_(a.B)
         return mux.Adapter(a.A.contiguous(), Bs, a.rank, a.scale)
     col_off = None
-    if args.fused_proj:     # q|k|v and gate|up as one column-sliced GEMM each
+    fuse = args.fused_proj
+    if fuse < 0:            # auto: fuse where a per-rank projection shard is narrow (profiles/r02_fused_ab.jsonl)
+        fuse = int(min(L.N // world for L in wl.linears if L.name in tp_block.COLUMN) < FUSE_BELOW_COLS)
+    args.fused_proj = fuse
+    if fuse:                # q|k|v and gate|up as one column-sliced GEMM each
         Wp, ap, col_off = tp_block.shard_block_fused(Wfull, afull, world, rank, mk)
         ap = {n: [[padded(a) for a in row] if isinstance(row, list) else padded(row) for row in v]
               for n, v in ap.items()}
@@ -1105,6 +1116,9 @@ def block_arm(args):
             B.copy_(_bits_to_dev(h[f"B{li}_{t}"], torch))
             ads[n].append(mux.Adapter(_bits_to_dev(h[f"A{li}_{t}"], torch), B, wl.ranks[t], wl.scales[t]))
     r_cap = 16 * -(-max(wl.ranks) // 16)
+    if args.fused_proj < 0:     # auto (one GPU: full-width projections)
+        args.fused_proj = int(min(L.N for L in wl.linears if L.name in ("q", "k", "v", "gate", "up"))
+                              < FUSE_BELOW_COLS)
     blk = DecoderBlock(shape, W, ads, r_cap, fused=bool(args.fused_proj))
     blk.overlap_grads = not args.no_overlap_grads
     i32 = dict(dtype=torch.int32, device=dev)
@@ -1206,9 +1220,10 @@ def main():
     ap.add_argument("--htasks", type=int, default=1,
                     help="--mode tp: hTasks interleaved by Alg. 1 (NEXT-1); 0 = chosen by the planner (NEXT-4)")
     ap.add_argument("--comm-ctas", type=int, default=0, help="--mode tp: NCCL_MAX_CTAS for the overlapped collectives")
-    ap.add_argument("--fused-proj", type=int, default=1, choices=(0, 1),
-                    help="--mode tp / block, configs 4/5: q|k|v and gate|up as one column-sliced GEMM each "
-                         "(1, default) or seven separate linears (0)")
+    ap.add_argument("--fused-proj", type=int, default=-1, choices=(-1, 0, 1),
+                    help="--mode tp / block, configs 4/5: q|k|v and gate|up as one column-sliced GEMM each (1), "
+                         "seven separate linears (0), or auto (-1, default: fused where a per-rank projection "
+                         f"shard is narrower than {FUSE_BELOW_COLS} columns)")
     ap.add_argument("--shared-shrink", action="store_true",
                     help="--mode tp, configs 4/5: column layers shrink only their own rows and all-gather Hs")
     ap.add_argument("--fused-rs", action="store_true",

@@ -460,18 +460,26 @@ def _flat_slots(adapters) -> List[Adapter]:
     return [a for per_task in adapters for a in per_task]
 
 
-def _check_sliced(seg_off, seg_task, adapters, col_off, K, N, rows, r_cap, grads=False, **mats):
-    """Host-side checks of a sliced call: B_{t,s} is [slice width, rank], A_{t,s} [rank, K]."""
-    S = len(col_off) - 1
-    _need(1 <= S <= MAX_SLICES, f"1..{MAX_SLICES} slices")
-    _need(col_off[0] == 0 and col_off[-1] == N, f"col_off must run from 0 to N={N}")
-    dev = None
-    for name, (t, shape, dt) in mats.items():
-        if t is not None:
-            dev = t.device if dev is None else dev
-            _check_mat(name, t, shape, dt, dev)
-    _need(isinstance(seg_off, torch.Tensor) and seg_off.dtype == torch.int32 and seg_off.is_cuda
-          and seg_off.numel() == len(seg_task) + 1, "seg_off must be int32 CUDA [len(seg_task)+1]")
+# Prepared adapter tables of sliced calls: (id(adapters), K, N, col_off, grads) -> (fingerprint, table).
+# The fingerprint (every slot's object, rank, scale and tensor addresses) is ~30 us for 48 slots; the
+# per-slot shape checks and the ctypes table (~2 ms together) run only when it changes.
+_SLICED_TABLES = {}
+
+
+def _slots_fingerprint(slots, grads):
+    p = lambda t: 0 if t is None else t.data_ptr()  # noqa: E731
+    return tuple((id(a), a.rank, a.scale, p(a.A), p(a.B), p(a.dA) if grads else 0, p(a.dB) if grads else 0)
+                 for a in slots)
+
+
+def _sliced_table(adapters, col_off, K, N, grads, dev):
+    """The ctypes adapter table of a sliced call, validated once per distinct adapter set."""
+    slots = _flat_slots(adapters)
+    key = (id(adapters), K, N, tuple(col_off), grads)
+    fp = _slots_fingerprint(slots, grads)
+    hit = _SLICED_TABLES.get(key)
+    if hit is not None and hit[0] == fp:
+        return hit[1]
     for t, per_task in enumerate(adapters):
         for s, a in enumerate(per_task):
             if a.rank == 0:
@@ -482,19 +490,39 @@ def _check_sliced(seg_off, seg_task, adapters, col_off, K, N, rows, r_cap, grads
             if grads:
                 _check_mat(f"adapters[{t}][{s}].dA", a.dA, (a.rank, K), torch.float32, dev)
                 _check_mat(f"adapters[{t}][{s}].dB", a.dB, (ns, a.rank), torch.float32, dev)
+    tab = _adapter_table(slots, grads)
+    if len(_SLICED_TABLES) > 256:
+        _SLICED_TABLES.clear()
+    _SLICED_TABLES[key] = (fp, tab)
+    return tab
+
+
+def _check_sliced(seg_off, seg_task, adapters, col_off, K, N, rows, r_cap, grads=False, **mats):
+    """Host-side checks of a sliced call (the tensors; the adapters are checked by _sliced_table:
+    B_{t,s} is [slice width, rank], A_{t,s} [rank, K])."""
+    S = len(col_off) - 1
+    _need(1 <= S <= MAX_SLICES, f"1..{MAX_SLICES} slices")
+    _need(col_off[0] == 0 and col_off[-1] == N, f"col_off must run from 0 to N={N}")
+    dev = None
+    for name, (t, shape, dt) in mats.items():
+        if t is not None:
+            dev = t.device if dev is None else dev
+            _check_mat(name, t, shape, dt, dev)
+    _need(isinstance(seg_off, torch.Tensor) and seg_off.dtype == torch.int32 and seg_off.is_cuda
+          and seg_off.numel() == len(seg_task) + 1, "seg_off must be int32 CUDA [len(seg_task)+1]")
 
 
 def linear(op: int, seg_off, seg_task, adapters, col_off, K: int, N: int, r_cap: int, max_rows: int, *, X=None,
            W=None, dY=None, Y=None, Hs=None, dX=None, row_begin: int = 0, row_end: int = None, rs=None, ag=None,
            workspace=None, stream=None, want_grads=False):
     """mux_linear: one call of any op over column slices col_off (adapters[t][s]).  Marshalling only."""
-    slots = _flat_slots(adapters)
     S = len(col_off) - 1
+    _need(1 <= S <= MAX_SLICES, f"1..{MAX_SLICES} slices")
     sl = _Slices()
     sl.num_slices = S
     for i, c in enumerate(col_off):
         sl.col_off[i] = int(c)
-    tab = _adapter_table(slots, want_grads)
+    tab = _sliced_table(adapters, col_off, K, N, want_grads, seg_off.device)
     st = _i32_host(seg_task)
     if workspace is None:
         dev = seg_off.device

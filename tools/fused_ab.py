@@ -23,6 +23,7 @@ SETS = {  # name: (K, slice widths)
     "qkv4": (4096, [1024, 1024, 1024]), "gu4": (4096, [2752, 2752]),
     "qkv8": (4096, [512, 512, 512]), "gu8": (4096, [1376, 1376]),
     "qkv70b8": (8192, [1024, 128, 128]), "gu70b8": (8192, [3584, 3584]),
+    "o8": (512, [4096]), "down8": (1376, [4096]),   # one slice: per-pass times of the row-parallel shards
 }
 
 

@@ -11,7 +11,7 @@
 // racecheck does not model mbarrier complete_tx ordering of async-proxy writes.
 // The result is checked on the host (every stage's sum), so the probe also proves the data is right.
 //
-// build: nvcc -gencode arch=compute_100a,code=sm_100a -O2 -o racecheck_probe racecheck_probe.cu
+// build: nvcc -gencode arch=compute_100a,code=sm_100a -O2 -lineinfo -o racecheck_probe racecheck_probe.cu
 // run:   compute-sanitizer --tool racecheck ./racecheck_probe
 #include <cstdio>
 #include <cstdint>
@@ -85,6 +85,50 @@ __global__ void probe(const int* __restrict__ src, long long* __restrict__ sums)
   }
 }
 
+// Second pattern: tcgen05.alloc writes the allocated TMEM address into shared memory (a write by the
+// tensor-memory unit, not by an SM instruction); every thread reads it after the documented ordering
+// tcgen05.fence::before_thread_sync -> bar.sync -> tcgen05.fence::after_thread_sync (gemm.cu does the
+// same, with a cluster barrier).  racecheck's GEMM report is on exactly this slot (tmem_holder).
+__global__ void probe_tmem(unsigned* out) {
+  __shared__ uint32_t holder;
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(smem_u32(&holder))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t base = holder;
+  out[threadIdx.x] = base;
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(base) : "memory");
+}
+
+// Third: the GEMM's own form — a CTA pair (cluster of 2) allocating with tcgen05.alloc.cta_group::2
+// from a warp of each CTA, then tcgen05.fence::before_thread_sync, bar.sync, barrier.cluster
+// arrive/wait, tcgen05.fence::after_thread_sync, and every thread reads the address slot.
+__global__ void __cluster_dims__(2, 1, 1) probe_tmem_pair(unsigned* out) {
+  __shared__ uint32_t holder;
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(smem_u32(&holder))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t base = holder;
+  out[blockIdx.x * blockDim.x + threadIdx.x] = base;
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 32;" ::"r"(base) : "memory");
+}
+
 int main() {
   const size_t n = static_cast<size_t>(kIters) * kStageElems;
   int* h = new int[n];
@@ -106,5 +150,25 @@ int main() {
     bad += want != got[i];
   }
   printf("racecheck_probe: %s, %d of %d stage sums wrong\n", cudaGetErrorString(e), bad, kIters);
-  return bad != 0 || e != cudaSuccess;
+  unsigned* dt;
+  unsigned ht[128];
+  cudaMalloc(&dt, sizeof(ht));
+  probe_tmem<<<1, 128>>>(dt);
+  cudaError_t e2 = cudaDeviceSynchronize();
+  cudaMemcpy(ht, dt, sizeof(ht), cudaMemcpyDeviceToHost);
+  int same = 1;
+  for (int i = 1; i < 128; ++i) same &= ht[i] == ht[0];
+  printf("racecheck_probe tmem: %s, every thread read the same TMEM address: %s\n", cudaGetErrorString(e2),
+         same ? "yes" : "no");
+  unsigned* dp;
+  unsigned hp[256];
+  cudaMalloc(&dp, sizeof(hp));
+  probe_tmem_pair<<<2, 128>>>(dp);
+  cudaError_t e3 = cudaDeviceSynchronize();
+  cudaMemcpy(hp, dp, sizeof(hp), cudaMemcpyDeviceToHost);
+  int same2 = 1;
+  for (int i = 1; i < 256; ++i) same2 &= hp[i] == hp[0];
+  printf("racecheck_probe tmem pair: %s, every thread of both CTAs read the same TMEM address: %s\n",
+         cudaGetErrorString(e3), same2 ? "yes" : "no");
+  return bad != 0 || e != cudaSuccess || e2 != cudaSuccess || !same || e3 != cudaSuccess || !same2;
 }
