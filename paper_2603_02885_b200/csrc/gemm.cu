@@ -463,15 +463,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           }
         } else {
           const int col_c = tl.n * kTileN + (kTileN / 2) * rk;  // this CTA's half of N
-          // the shrink flag of this row block is needed only before the extension blocks (end of the
-          // tile): read it now, relaxed, so its L2 round trip (~1k cycles, a fifth of an 8-k-block
-          // tile) overlaps the backbone k-loop instead of stalling the producer after it
-#ifndef MUX_NO_FLAG_PREFETCH
-          const bool need_flag = pc.fin && g.n > 0 && p.has_side;
-          const unsigned long long flag_early = need_flag ? ld_relaxed_gpu_u64(p.flags + tl.m) : 0ull;
-#else
-          const unsigned long long flag_early = 0ull;  // A/B build: the flag is read after the k-loop
-#endif
           for (int kb = pc.k0; kb < pc.k1; ++kb) {
             PROF_T0(tw_);
             mbar_wait(&empty_bar[stage], phase ^ 1u);
@@ -507,9 +498,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             if (elect_one_sync()) {
               const unsigned long long* flag = p.flags + tl.m;
               const unsigned long long want = (epoch << 8) | 8ull;
-              if (flag_early == want) {
-                fence_acq_rel_gpu();  // relaxed read that saw the release + fence = acquire
-              } else if (ld_acquire_gpu_u64(flag) != want) {
+              if (ld_acquire_gpu_u64(flag) != want) {
                 const uint64_t t0 = globaltimer_ns();
                 while (ld_acquire_gpu_u64(flag) != want) {
                   if (globaltimer_ns() - t0 > kWatchdogNs) __trap();
