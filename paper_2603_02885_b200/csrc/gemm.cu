@@ -63,6 +63,9 @@ constexpr uint32_t kSubA = kBM * 128;                // 16 KB: one k-subtile of 
 constexpr uint32_t kEpiBuf = 32 * 128;               // 32 rows x 64 bf16 (one TMA store box)
 constexpr uint32_t kSmemEpi = 4 * 2 * kEpiBuf;
 constexpr uint32_t kSmemMisc = 1024;
+// per-row-block task groups, computed once per launch by all threads (8 B per pair row block)
+constexpr int kGroupTab = 128;                       // row blocks covered (32768 rows); beyond: on the fly
+constexpr uint32_t kSmemGroups = kGroupTab * 8;
 
 template <bool kBwd>
 struct GemmLayout {
@@ -75,18 +78,23 @@ struct GemmLayout {
   static constexpr uint32_t kAtomMN = kBK * 128;            // MN-major atom: kBK K-rows x 128 B
   static constexpr uint32_t kSideGrp = kKSub * kBox;        // side-tile B of one task group
   static constexpr uint32_t kSmemPipe = kStages * kStageBytes;
-  static constexpr uint32_t kSmemBytes = kSmemPipe + kSmemEpi + kSmemMisc + 1024;
+  static constexpr uint32_t kSmemBytes = kSmemPipe + kSmemEpi + kSmemMisc + kSmemGroups + 1024;
+  static_assert(kSmemBytes <= 232448, "exceeds the 227 KB of dynamic shared memory per block");
 };
 constexpr uint32_t kTmemCols = 512;
 constexpr int kGemmThreads = 256;
 constexpr uint16_t kPairMask = 0x3;
 
-// Tasks present in a 256-row pair tile.  hm = bit h set: the group owns rows
-// [64h, 64h+64) of the tile.
+// Tasks present in a 256-row pair tile, packed in registers (a dynamically indexed array here sat
+// in local memory: ~3k cycles of dependent LDL/STL per tile in the producer and the MMA issuer,
+// a third of an 8-k-block tile, profiles/r02_gemm_waits_tp.jsonl): group i's segment in byte i of
+// seg4, its quarter mask in nibble i of hm4 (bit h set: the group owns rows [64h, 64h+64)).
 struct PairGroups {
   int n;
-  int seg[4];
-  int hm[4];
+  uint32_t seg4;
+  uint32_t hm4;
+  __device__ __forceinline__ int seg(int i) const { return static_cast<int>((seg4 >> (8 * i)) & 0xFFu); }
+  __device__ __forceinline__ int hm(int i) const { return static_cast<int>((hm4 >> (4 * i)) & 0xFu); }
 };
 
 // Binary search over the (non-decreasing) segment offsets: the segment s with
@@ -109,25 +117,26 @@ __device__ __forceinline__ int seg_containing(const int* so, int S, int row) {
 __device__ __forceinline__ PairGroups pair_groups(const GemmParams& p, const int* so, int m) {
   PairGroups g;
   g.n = 0;
+  g.seg4 = 0u;
+  g.hm4 = 0u;
   const int S = p.num_segs;
   const int row0 = m * kPairRows;
   int s = seg_containing(so, S, row0);
   if (s < 0 && S > 0 && row0 < so[0]) s = 0;  // rows before the first segment: start from segment 0
+  int last = -1;                              // segments are contiguous row ranges: a quarter's segment
+#pragma unroll                                // is either the previous quarter's or a new group
   for (int h = 0; h < 4; ++h) {
     const int row = row0 + kRowQuarter * h;
     if (s < 0 || row >= so[S]) break;
     while (s + 1 < S && so[s + 1] <= row) ++s;
     if (!(so[s] <= row && row < so[s + 1])) continue;
     if (p.seg_rank[s] == 0) continue;
-    int f = -1;
-    for (int i = 0; i < g.n; ++i)
-      if (g.seg[i] == s) f = i;
-    if (f < 0) {
-      g.seg[g.n] = s;
-      g.hm[g.n] = 0;
-      f = g.n++;
+    if (s != last) {
+      g.seg4 |= static_cast<uint32_t>(s) << (8 * g.n);
+      ++g.n;
+      last = s;
     }
-    g.hm[f] |= 1 << h;
+    g.hm4 |= (1u << h) << (4 * (g.n - 1));
   }
   return g;
 }
@@ -287,6 +296,8 @@ __device__ __forceinline__ void for_each_item(const GemmParams& p, int cid, int 
 // cycles spent waiting on each barrier, accumulated into GemmParams::dbg:
 //   [0] MMA total  [1] MMA wait full  [2] MMA wait tmem-empty
 //   [3] producer total [4] producer wait empty  [5] epilogue total [6] epilogue wait tmem-full
+//   [7] producer per-tile setup (task lookup)  [8] producer TMA issue  [9] producer shrink-flag wait
+//   [10] epilogue wait for its smem staging buffer (TMA store read)  [11] main tiles (producer 0s)
 #ifdef MUX_PROFILE
 #define PROF_T0(v) const long long v = clock64()
 #define PROF_ADD(acc, t0) acc += clock64() - (t0)
@@ -323,6 +334,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty_bar + 2);
   int* so = reinterpret_cast<int*>(misc + 256);  // seg_off copy, <= 65 ints
   int* skb = reinterpret_cast<int*>(misc + 528);  // stream-K range table, <= kSkMaxClusters + 1 ints
+  uint2* gtab = reinterpret_cast<uint2*>(misc + kSmemMisc);  // [kGroupTab] {seg4, hm4 | n << 24}
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -369,6 +381,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
 
   const int total_rows = so[p.num_segs];
   const int num_m = (total_rows + kPairRows - 1) / kPairRows;
+  // the task groups of every pair row block, once per launch (the producer and the MMA issuer
+  // would otherwise each rebuild them per tile on their critical path)
+  const bool tab_ok = num_m <= kGroupTab;
+  if (tab_ok) {
+    for (int m = threadIdx.x; m < num_m; m += blockDim.x) {
+      const PairGroups g = pair_groups(p, so, m);
+      gtab[m] = make_uint2(g.seg4, g.hm4 | (static_cast<uint32_t>(g.n) << 24));
+    }
+  }
+  __syncthreads();
+  auto groups_of = [&](int m) -> PairGroups {
+    if (!tab_ok) return pair_groups(p, so, m);
+    const uint2 e = gtab[m];
+    PairGroups g;
+    g.seg4 = e.x;
+    g.hm4 = e.y & 0xFFFFu;
+    g.n = static_cast<int>(e.y >> 24);
+    return g;
+  };
   const int num_n = (p.nout + kTileN - 1) / kTileN;
   const int side_lo = min(p.side_m_lo, num_m);
   const int total_tiles = p.has_main ? num_m * (num_n + (p.has_side ? 1 : 0))
@@ -377,6 +408,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
 
 #ifdef MUX_PROFILE
   long long pw_empty = 0, mw_full = 0, mw_tempty = 0, ew_tfull = 0;
+  long long p_setup = 0, p_issue = 0, p_flag = 0, e_store = 0, n_tiles = 0;
   const long long t_role0 = clock64();
 #endif
   if (warp == 0) {
@@ -395,7 +427,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       const uint32_t full_leader = mapa_shared(full_u, 0);  // stage s barrier: + 8 s
       uint32_t ag_ok = 0;  // owners whose rows have landed in the gather buffer (fused all-gather)
       for_each_item(p, cid, ncl, num_m, num_n, side_lo, total_tiles, num_kb, skb, [&](const Tile& tl, const SkPiece& pc) {
-        const PairGroups g = pair_groups(p, so, tl.m);
+        PROF_T0(ts_);
+        const PairGroups g = groups_of(tl.m);
         const int row_c = tl.m * kPairRows + kBM * rk;  // this CTA's rows
         if (p.ag_world > 0) {
           const int owner = (tl.m * kPairRows) / p.ag_rows;
@@ -427,7 +460,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
               const int u = min(u0 + i, nunits - 1);
               const int gi = u / nsp;
               const int s = 2 * (u - gi * nsp) + rk;
-              const int base = p.seg_adapter[g.seg[gi]] * S;
+              const int base = p.seg_adapter[g.seg(gi)] * S;
               slot[i] = base + (s < S ? s : 0);
               jrow[i] = (s < S && p.slot_rank[base + s] > 0) ? 0 : 64;
               coff[i] = s < S ? p.slice_off[s] : 0;
@@ -463,10 +496,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           }
         } else {
           const int col_c = tl.n * kTileN + (kTileN / 2) * rk;  // this CTA's half of N
+          PROF_ADD(p_setup, ts_);
+#ifdef MUX_PROFILE
+          ++n_tiles;
+#endif
           for (int kb = pc.k0; kb < pc.k1; ++kb) {
             PROF_T0(tw_);
             mbar_wait(&empty_bar[stage], phase ^ 1u);
             PROF_ADD(pw_empty, tw_);
+            PROF_T0(ti_);
             if (elect_one_sync()) {
               const uint32_t sa = pipe_u + stage * kStageBytes;
               const uint32_t sb = sa + kStageA;
@@ -486,8 +524,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
               }
             }
             __syncwarp();
+            PROF_ADD(p_issue, ti_);
             advance();
           }
+          PROF_T0(tf_);
 #ifdef MUX_DIAG_NO_FLAG
           if (false) {  // timing-only diagnostic: no wait for the shrink tile (results may race)
 #else
@@ -508,13 +548,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             }
             __syncwarp();
           }
+          PROF_ADD(p_flag, tf_);
           // LoRA expand (the tile's final piece only): one extension block per (task group, slice
           // with an adapter on this tile); reduction = the slot's rank (<= 64): first k-subtile only
           const int S = p.num_slices;
           const int tc0 = tl.n * kTileN, tc1 = tc0 + kTileN;
           for (int i = 0; i < (pc.fin ? g.n : 0); ++i) {
             for (int s = 0; s < S; ++s) {
-              const int slot = p.seg_adapter[g.seg[i]] * S + s;
+              const int slot = p.seg_adapter[g.seg(i)] * S + s;
               if (!ext_live<kBwd>(p, slot, s, tc0, tc1)) continue;
               PROF_T0(tw_);
               mbar_wait(&empty_bar[stage], phase ^ 1u);
@@ -571,7 +612,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         if (++stage == kStages) { stage = 0; phase ^= 1u; }
       };
       for_each_item(p, cid, ncl, num_m, num_n, side_lo, total_tiles, num_kb, skb, [&](const Tile& tl, const SkPiece& pc) {
-        const PairGroups g = pair_groups(p, so, tl.m);
+        const PairGroups g = groups_of(tl.m);
         PROF_T0(tw_);
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1u);
         PROF_ADD(mw_tempty, tw_);
@@ -590,7 +631,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             for (int i = 0; i < 2; ++i) {
               const int u = min(u0 + i, nunits - 1);
               const int gi = u / nsp;
-              lane_masks(i < nu ? g.hm[gi] : 0, mk[i]);
+              lane_masks(i < nu ? g.hm(gi) : 0, mk[i]);
               dcol[i] = static_cast<uint32_t>(128 * (u - gi * nsp));
             }
             for (int kb = 0; kb < num_kb; ++kb) {
@@ -639,9 +680,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           const int tc0 = tl.n * kTileN, tc1 = tc0 + kTileN;
           for (int i = 0; i < (pc.fin ? g.n : 0); ++i) {
             uint32_t mk[8];
-            lane_masks(g.hm[i], mk);
+            lane_masks(g.hm(i), mk);
             for (int s = 0; s < S; ++s) {
-              const int slot = p.seg_adapter[g.seg[i]] * S + s;
+              const int slot = p.seg_adapter[g.seg(i)] * S + s;
               if (!ext_live<kBwd>(p, slot, s, tc0, tc1)) continue;
               PROF_T0(tw_);
               mbar_wait(&full_bar[stage], phase);
@@ -817,8 +858,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             if (lane == 0) mbar_arrive_cluster(tempty_leader);
           }
           uint8_t* buf = bufs + buf_sel * kEpiBuf;
+          PROF_T0(tsw_);
           if (lane == 0) tma_store_wait_read<1>();
           __syncwarp();
+          PROF_ADD(e_store, tsw_);
           uint8_t* rowp = buf + lane * 128;
 #pragma unroll
           for (int ch = 0; ch < 8; ++ch) {
@@ -866,10 +909,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     if (warp == 0 && lane == 0) {
       atomicAdd(p.dbg + 3, static_cast<unsigned long long>(tot));
       atomicAdd(p.dbg + 4, static_cast<unsigned long long>(pw_empty));
+      atomicAdd(p.dbg + 7, static_cast<unsigned long long>(p_setup));
+      atomicAdd(p.dbg + 8, static_cast<unsigned long long>(p_issue));
+      atomicAdd(p.dbg + 9, static_cast<unsigned long long>(p_flag));
+      atomicAdd(p.dbg + 11, static_cast<unsigned long long>(n_tiles));
     }
     if (warp == 4 && lane == 0) {
       atomicAdd(p.dbg + 5, static_cast<unsigned long long>(tot));
       atomicAdd(p.dbg + 6, static_cast<unsigned long long>(ew_tfull));
+      atomicAdd(p.dbg + 10, static_cast<unsigned long long>(e_store));
     }
   }
 #endif
