@@ -67,13 +67,21 @@ constexpr uint32_t kSmemMisc = 1024;
 constexpr int kGroupTab = 128;                       // row blocks covered (32768 rows); beyond: on the fly
 constexpr uint32_t kSmemGroups = kGroupTab * 8;
 
-template <bool kBwd>
+// kTileN = output columns of a pair tile: 128 (narrow), 256 (standard: two 256-column TMEM
+// accumulators, the epilogue of tile i overlaps the mainloop of tile i+1) or 512 (wide: one
+// 512-column accumulator filled by two N = 256 MMAs per k-step; each CTA stages 256 B rows, so the
+// operand feed per FLOP is 3/4 of the standard tile's, at the cost of the epilogue overlap —
+// cuBLAS's own choice on these shapes, profiles/r02_cublas_kernels.csv).
+template <bool kBwd, int kTileN = 256>
 struct GemmLayout {
-  static constexpr int kBK = GemmCfg<kBwd>::kBK;
-  static constexpr int kKSub = GemmCfg<kBwd>::kKSub;
-  static constexpr int kStages = GemmCfg<kBwd>::kStages;
+  static constexpr bool kWide = kTileN == 512;
+  static constexpr int kBK = kWide ? 64 : GemmCfg<kBwd>::kBK;
+  static constexpr int kKSub = kBK / 64;
+  static constexpr int kStages = kWide ? 4 : GemmCfg<kBwd>::kStages;
+  static constexpr int kBoxesB = kWide ? 4 : 2;             // 64-row B boxes per CTA per k-subtile
+  static constexpr uint32_t kBSub = kBoxesB * kBox;         // one k-subtile of this CTA's B (K-major)
   static constexpr uint32_t kStageA = kKSub * kSubA;
-  static constexpr uint32_t kStageB = kKSub * 2 * kBox;     // this CTA's half of B (128 columns)
+  static constexpr uint32_t kStageB = kKSub * kBSub;        // this CTA's share of B
   static constexpr uint32_t kStageBytes = kStageA + kStageB;
   static constexpr uint32_t kAtomMN = kBK * 128;            // MN-major atom: kBK K-rows x 128 B
   static constexpr uint32_t kSideGrp = kKSub * kBox;        // side-tile B of one task group
@@ -306,14 +314,16 @@ __device__ __forceinline__ void for_each_item(const GemmParams& p, int cid, int 
 #define PROF_ADD(acc, t0)
 #endif
 
-template <bool kBwd, bool kNarrow>
+template <bool kBwd, int kTileN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     mux_gemm_kernel(const __grid_constant__ GemmParams p) {
-  using Ly = GemmLayout<kBwd>;
-  // kNarrow: 256 x 128 pair tiles (64 output columns per CTA) for narrow outputs, where 256-wide
-  // tiles leave most CTA pairs idle (e.g. 512-column tensor-parallel shards: 2 tiles per row block)
-  constexpr int kTileN = kNarrow ? 128 : kBN;
-  constexpr int kHalves = kTileN / 128;  // 64-column boxes per CTA
+  using Ly = GemmLayout<kBwd, kTileN>;
+  // kTileN = 128: 256 x 128 pair tiles (64 output columns per CTA) for narrow outputs, where 256-wide
+  // tiles leave most CTA pairs idle (e.g. 128-column tensor-parallel shards); 512: wide tiles
+  constexpr bool kWide = Ly::kWide;
+  constexpr int kHalves = kTileN / 128;  // 64-row B boxes per CTA
+  constexpr int kAccs = kWide ? 1 : 2;   // TMEM accumulators (512 columns in total)
+  constexpr uint32_t kBSub = Ly::kBSub;
   constexpr int kBK = Ly::kBK;
   constexpr int kKSub = Ly::kKSub;
   constexpr int kStages = Ly::kStages;
@@ -369,7 +379,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   for (int i = threadIdx.x; i <= p.num_segs; i += blockDim.x) so[i] = p.seg_off[i];
   if (p.sk && threadIdx.x == 96) {  // warp 3 has no role: the stream-K range table
     const int rows = p.seg_off[p.num_segs];
-    sk_compute_bounds(p, (rows + kPairRows - 1) / kPairRows, (p.nout + (kNarrow ? 128 : kBN) - 1) / (kNarrow ? 128 : kBN),
+    sk_compute_bounds(p, (rows + kPairRows - 1) / kPairRows, (p.nout + kTileN - 1) / kTileN,
                       (p.kred + GemmCfg<kBwd>::kBK - 1) / GemmCfg<kBwd>::kBK, ncl, skb);
   }
   const unsigned long long epoch = *reinterpret_cast<volatile unsigned long long*>(p.epoch) + 1ull;
@@ -495,7 +505,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             }
           }
         } else {
-          const int col_c = tl.n * kTileN + (kTileN / 2) * rk;  // this CTA's half of N
+          // this CTA's B columns: box i covers output columns bcol(i) .. +63 (standard / narrow: the
+          // CTA's half of the tile; wide: the CTA's half of each 256-column MMA half)
+          const int col_c = tl.n * kTileN + (kWide ? 128 : kTileN / 2) * rk;
+          auto bcol = [&](int i) { return col_c + 256 * (i >> 1) + 64 * (i & 1); };
           PROF_ADD(p_setup, ts_);
 #ifdef MUX_PROFILE
           ++n_tiles;
@@ -517,9 +530,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
                 for (int i = 0; i < kHalves; ++i) {
                   if (!kBwd)  // W [N, K] K-major rows n: k-subtile s2, rows 64i..
-                    tma_load_2d_pair_u32(&p.map_w, fbl, sb + s2 * kSubA + i * kBox, k0 + 64 * s2, col_c + 64 * i);
+                    tma_load_2d_pair_u32(&p.map_w, fbl, sb + s2 * kBSub + i * kBox, k0 + 64 * s2, bcol(i));
                   else        // W viewed [k_out (MN), n (red)]: atom i, K-rows 64*s2..
-                    tma_load_2d_pair_u32(&p.map_w, fbl, sb + i * kAtomMN + s2 * kBox, col_c + 64 * i, k0 + 64 * s2);
+                    tma_load_2d_pair_u32(&p.map_w, fbl, sb + i * kAtomMN + s2 * kBox, bcol(i), k0 + 64 * s2);
                 }
               }
             }
@@ -569,9 +582,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
                 for (int j = 0; j < kHalves; ++j) {
                   if (!kBwd)  // B_{t,s} [n_s, r] K-major rows n: box {64 j, 64 n}, zero fill outside the slice
-                    tma_load_2d_pair_u32(&p.map_lora_b[slot], fbl, sb + j * kBox, 0, col_c + 64 * j - p.slice_off[s]);
+                    tma_load_2d_pair_u32(&p.map_lora_b[slot], fbl, sb + j * kBox, 0, bcol(j) - p.slice_off[s]);
                   else        // A_{t,s} [r, K] viewed [k_out (MN), j (red)]: atom j, K-rows 0..63
-                    tma_load_2d_pair_u32(&p.map_lora_a[slot], fbl, sb + j * kAtomMN, col_c + 64 * j, 0);
+                    tma_load_2d_pair_u32(&p.map_lora_a[slot], fbl, sb + j * kAtomMN, bcol(j), 0);
                 }
               }
               __syncwarp();
@@ -586,7 +599,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     // The whole warp runs the loop (warp-uniform values stay in uniform
     // registers); one elected lane issues tcgen05.mma / tcgen05.commit.
     if (leader) {
-      constexpr uint32_t kIdescMain = idesc_bf16(kPairRows, kTileN, false, kBwd);
+      constexpr uint32_t kIdescMain = idesc_bf16(kPairRows, kWide ? 256 : kTileN, false, kBwd);
+      // wide tiles: the second N = 256 MMA reads rows 128.. of this CTA's B share and writes TMEM
+      // columns 256..
+      constexpr uint32_t kBHalf2 = (kBwd ? 2 * kAtomMN : 2 * kBox) >> 4;
       constexpr uint32_t kIdescSide = idesc_bf16(kPairRows, kSideN, false, kBwd);
       // B operand per CTA: K-major rows of 128 B (SBO 1024), or MN-major atoms
       // of 64 elements x 64 K-rows (LBO 8 KB between atoms, SBO 1024).
@@ -594,7 +610,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       // start-address offset (16 B units) of k-step k (16 reduction elements)
       auto a_off = [](int k) -> uint32_t { return ((k >> 2) * kSubA + (k & 3) * 32) >> 4; };
       auto b_off = [](int k) -> uint32_t {
-        return kBwd ? (k * 16 * 128) >> 4 : ((k >> 2) * kSubA + (k & 3) * 32) >> 4;
+        return kBwd ? (k * 16 * 128) >> 4 : ((k >> 2) * kBSub + (k & 3) * 32) >> 4;
       };
       auto side_b_off = [](int k) -> uint32_t {
         return kBwd ? (k * 16 * 128) >> 4 : ((k >> 2) * kBox + (k & 3) * 32) >> 4;
@@ -667,9 +683,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             const uint32_t b_lo = b_lo0 + stage * kStageStep;
             if (elect_one_sync()) {
 #pragma unroll
-              for (int k = 0; k < kBK / 16; ++k)
+              for (int k = 0; k < kBK / 16; ++k) {
                 mma_bf16_pair_nomask(d_tmem, make_desc(a_lo + a_off(k), kHi), make_desc(b_lo + b_off(k), kHi),
                                      kIdescMain, ((kb - pc.k0) | k) != 0);
+                if (kWide)
+                  mma_bf16_pair_nomask(d_tmem + 256, make_desc(a_lo + a_off(k), kHi),
+                                       make_desc(b_lo + kBHalf2 + b_off(k), kHi), kIdescMain,
+                                       ((kb - pc.k0) | k) != 0);
+              }
               mma_commit_pair_mc(&empty_bar[stage], kPairMask);
             }
             __syncwarp();
@@ -692,9 +713,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
               const uint32_t b_lo = b_lo0 + stage * kStageStep;
               const int nk = (p.slot_rank[slot] + 15) / 16;
               if (elect_one_sync()) {
-                for (int k = 0; k < nk; ++k)
+                for (int k = 0; k < nk; ++k) {
                   mma_bf16_pair(d_tmem, make_desc(a_lo + a_off(k), kHi), make_desc(b_lo + b_off(k), kHi),
                                 kIdescMain, 1u, mk);
+                  if (kWide)
+                    mma_bf16_pair(d_tmem + 256, make_desc(a_lo + a_off(k), kHi),
+                                  make_desc(b_lo + kBHalf2 + b_off(k), kHi), kIdescMain, 1u, mk);
+                }
                 mma_commit_pair_mc(&empty_bar[stage], kPairMask);
               }
               __syncwarp();
@@ -704,7 +729,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         }
         if (elect_one_sync()) mma_commit_pair_mc(&tfull_bar[acc], kPairMask);
         __syncwarp();
-        if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
+        if (++acc == kAccs) { acc = 0; acc_phase ^= 1u; }
       });
     }
   } else if (warp >= 4) {
@@ -891,7 +916,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           buf_sel ^= 1;
         }
       }
-      if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
+      if (++acc == kAccs) { acc = 0; acc_phase ^= 1u; }
     });
     if (lane == 0) {
       tma_store_wait<0>();
@@ -943,31 +968,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
 }
 
 // ---------------------------------------------------------------- launchers
-template <bool kBwd, bool kNarrow>
+template <bool kBwd, int kTileN>
 cudaError_t launch_gemm_impl(const GemmParams& p, int grid, cudaStream_t stream) {
   static std::atomic<uint64_t> configured{0};
   cudaError_t ce = once_per_device(configured, [] {
-    return cudaFuncSetAttribute(mux_gemm_kernel<kBwd, kNarrow>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(GemmLayout<kBwd>::kSmemBytes));
+    return cudaFuncSetAttribute(mux_gemm_kernel<kBwd, kTileN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(GemmLayout<kBwd, kTileN>::kSmemBytes));
   });
   if (ce != cudaSuccess) return ce;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kGemmThreads);
-  cfg.dynamicSmemBytes = GemmLayout<kBwd>::kSmemBytes;
+  cfg.dynamicSmemBytes = GemmLayout<kBwd, kTileN>::kSmemBytes;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, mux_gemm_kernel<kBwd, kNarrow>, p);
+  return cudaLaunchKernelEx(&cfg, mux_gemm_kernel<kBwd, kTileN>, p);
 }
 
-// grid must be even (clusters of 2); narrow: 256 x 128 tiles (see kNarrow)
-cudaError_t launch_gemm(const GemmParams& p, bool bwd, bool narrow, int grid, cudaStream_t stream) {
-  if (narrow) return bwd ? launch_gemm_impl<true, true>(p, grid, stream) : launch_gemm_impl<false, true>(p, grid, stream);
-  return bwd ? launch_gemm_impl<true, false>(p, grid, stream) : launch_gemm_impl<false, false>(p, grid, stream);
+// grid must be even (clusters of 2); tile_n = output columns of a pair tile (128, 256 or 512)
+cudaError_t launch_gemm(const GemmParams& p, bool bwd, int tile_n, int grid, cudaStream_t stream) {
+  switch (tile_n) {
+    case 128: return bwd ? launch_gemm_impl<true, 128>(p, grid, stream) : launch_gemm_impl<false, 128>(p, grid, stream);
+    case 512: return bwd ? launch_gemm_impl<true, 512>(p, grid, stream) : launch_gemm_impl<false, 512>(p, grid, stream);
+    default: return bwd ? launch_gemm_impl<true, 256>(p, grid, stream) : launch_gemm_impl<false, 256>(p, grid, stream);
+  }
 }
 
 }  // namespace mux

@@ -21,6 +21,10 @@
 #ifndef MUX_NARROW_MAX_NOUT
 #define MUX_NARROW_MAX_NOUT 128
 #endif
+// fused GEMM: outputs at least this wide use 256 x 512 pair tiles (gemm.cu kTileN = 512)
+#ifndef MUX_WIDE_MIN_NOUT
+#define MUX_WIDE_MIN_NOUT (1 << 30)
+#endif
 // fused GEMM: reductions this short schedule every shrink tile before the main tiles
 #ifndef MUX_SIDE_FIRST_MAX_KRED
 #define MUX_SIDE_FIRST_MAX_KRED 2048
@@ -29,7 +33,7 @@
 #include "common.h"
 
 namespace mux {
-cudaError_t launch_gemm(const GemmParams& p, bool bwd, bool narrow, int grid, cudaStream_t stream);
+cudaError_t launch_gemm(const GemmParams& p, bool bwd, int tile_n, int grid, cudaStream_t stream);
 cudaError_t launch_grad(const GradParams& p, int grid, cudaStream_t stream);
 cudaError_t launch_grad_simt(const GradParams& p, int grid, cudaStream_t stream);
 size_t pack_workspace_bytes(int M, int S);
@@ -590,9 +594,15 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
     p.seg_rank[s] = r;
   }
   const int num_m_max = (max_rows + kPairRows - 1) / kPairRows;
-  // narrow outputs (<= MUX_NARROW_MAX_NOUT columns): 256 x 128 tiles, twice as many work items
-  const bool narrow = nout <= MUX_NARROW_MAX_NOUT;
-  const int tile_n = narrow ? kBN / 2 : kBN;
+  // narrow outputs (<= MUX_NARROW_MAX_NOUT columns): 256 x 128 tiles, twice as many work items;
+  // wide outputs (>= MUX_WIDE_MIN_NOUT): 256 x 512 tiles; MUX_TILE_N=128/256/512 forces one (A/B,
+  // read per call)
+  int tile_n = nout <= MUX_NARROW_MAX_NOUT ? kBN / 2 : nout >= MUX_WIDE_MIN_NOUT ? 2 * kBN : kBN;
+  {
+    const char* te = std::getenv("MUX_TILE_N");
+    const int tv = (te && *te) ? std::atoi(te) : 0;
+    if (tv == 128 || tv == 256 || tv == 512) tile_n = tv;
+  }
   const int num_n = (nout + tile_n - 1) / tile_n;
   const long long side_blocks = p.has_main ? (p.has_side ? num_m_max : 0)
                                            : std::max(0, std::min(p.side_m_hi, num_m_max) - std::min(p.side_m_lo, num_m_max));
@@ -617,7 +627,8 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
     const long long main_tiles = p.has_main ? static_cast<long long>(num_m_max) * num_n : 0;
     const double ideal = (main_tiles + side_blocks * side_cost_x4 / 4.0) / pairs;
     const double rounds = static_cast<double>((tiles_max + pairs - 1) / pairs);
-    const bool fits = p.has_main && pairs <= ws.sk_slots && pairs <= kSkMaxClusters && num_kb >= 2;
+    const bool fits = p.has_main && pairs <= ws.sk_slots && pairs <= kSkMaxClusters && num_kb >= 2 &&
+                      tile_n <= kBN;  // partial slots hold 256-column tiles
     p.sk = fits && (sk_env == 1 || (sk_env < 0 && ideal < 0.85 * rounds)) ? 1 : 0;
     p.sk_side_cost_x4 = side_cost_x4;
     p.sk_flags = ws.sk_flags;
@@ -629,7 +640,7 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
   if (e != cudaSuccess) return cuda_fail(e, "debug segment check launch");
 #endif
   if (parts & 1) {
-    e = launch_gemm(p, bwd, narrow, grid, stream);
+    e = launch_gemm(p, bwd, tile_n, grid, stream);
     if (e != cudaSuccess) return cuda_fail(e, bwd ? "mux_linear_bwd dX launch" : "mux_linear_fwd launch");
   }
 

@@ -7,6 +7,7 @@ clock drift under the power cap hits both alike.  --once runs every (shape, pass
 time for an ncu DRAM-traffic capture (ncu -k regex:mux_gemm ... --once: launches in the order
 shape x pass x mode).
 usage: python tools/raster_ab.py [--modes m,n] [--out profiles/r02_raster_ab.jsonl] [--once]
+       python tools/raster_ab.py --var MUX_TILE_N --modes 256,512   (any per-call env switch of libmux)
 """
 import argparse
 import json
@@ -26,12 +27,16 @@ def main():
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--rounds", type=int, default=9)
     ap.add_argument("--modes", default="m,n")
+    ap.add_argument("--var", default="MUX_RASTER")
+    ap.add_argument("--tasks", type=int, default=4)
+    ap.add_argument("--rank", type=int, default=16)
     ap.add_argument("--shapes", default="4096x4096,4096x11008,11008x4096")
     ap.add_argument("--once", action="store_true")
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
     from paper_2603_02885_b200 import mux
-    R, T = a.rows, 4
+    R, T = a.rows, a.tasks
+    V = a.var
     modes = a.modes.split(",")
     torch.manual_seed(0)
     out = open(a.out, "a") if a.out else None
@@ -43,35 +48,37 @@ def main():
         seg = R // T // 64 * 64
         seg_off = torch.tensor([i * seg if i < T else R for i in range(T + 1)], dtype=torch.int32, device="cuda")
         ads = []
+        rk = a.rank
+        rc = max(16, -(-rk // 16) * 16)
         for _ in range(T):
-            B = mux.make_B_storage(N, 16)
-            B.copy_(torch.randn(N, 16, device="cuda").bfloat16())
-            ads.append(mux.Adapter((torch.randn(16, K, device="cuda") / K ** 0.5).bfloat16(), B, 16, 2.0))
+            B = mux.make_B_storage(N, rk)
+            B.copy_(torch.randn(N, rk, device="cuda").bfloat16())
+            ads.append(mux.Adapter((torch.randn(rk, K, device="cuda") / K ** 0.5).bfloat16(), B, rk, 2.0))
         Y = torch.empty(R, N, dtype=torch.bfloat16, device="cuda")
-        Hs = torch.empty(R, 16, dtype=torch.bfloat16, device="cuda")
+        Hs = torch.empty(R, rc, dtype=torch.bfloat16, device="cuda")
         dX = torch.empty(R, K, dtype=torch.bfloat16, device="cuda")
-        ws = torch.zeros(mux.linear_workspace_size(T, R, K, N, 16), dtype=torch.uint8, device="cuda")
+        ws = torch.zeros(mux.linear_workspace_size(T, R, K, N, rc), dtype=torch.uint8, device="cuda")
         st = list(range(T))
-        mux.linear_fwd(seg_off, st, ads, X, W, 16, Y=Y, Hs=Hs, workspace=ws)
+        mux.linear_fwd(seg_off, st, ads, X, W, rc, Y=Y, Hs=Hs, workspace=ws)
         passes = {
-            "fwd": lambda: mux.linear_fwd(seg_off, st, ads, X, W, 16, Y=Y, Hs=Hs, workspace=ws),
-            "dx": lambda: mux.linear_bwd(seg_off, st, ads, dY, X, W, Hs, 16, dX=dX, workspace=ws, part=mux.BWD_DX),
+            "fwd": lambda: mux.linear_fwd(seg_off, st, ads, X, W, rc, Y=Y, Hs=Hs, workspace=ws),
+            "dx": lambda: mux.linear_bwd(seg_off, st, ads, dY, X, W, Hs, rc, dX=dX, workspace=ws, part=mux.BWD_DX),
         }
-        flops = R * (2 * K * N + 2 * 16 * (K + N))
+        flops = R * (2 * K * N + 2 * rk * (K + N))
         for pname, fn in passes.items():
             if a.once:
                 for m in modes:
-                    os.environ["MUX_RASTER"] = m
+                    os.environ[V] = m
                     fn()
                 torch.cuda.synchronize()
                 continue
             times = {m: [] for m in modes}
             for m in modes:       # warm-up
-                os.environ["MUX_RASTER"] = m
+                os.environ[V] = m
                 fn()
             for _ in range(a.rounds):
                 for m in modes:
-                    os.environ["MUX_RASTER"] = m
+                    os.environ[V] = m
                     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     e0.record()
                     for _ in range(a.iters):
@@ -81,7 +88,7 @@ def main():
                     times[m].append(e0.elapsed_time(e1) / a.iters)
             for m in modes:
                 med = statistics.median(times[m])
-                line = {"shape": f"{K}x{N}", "pass": pname, "raster": m, "rows": R, "ms": round(med, 4),
+                line = {"shape": f"{K}x{N}", "pass": pname, V: m, "rows": R, "ms": round(med, 4),
                         "tflops": round(flops / med / 1e9, 1),
                         "spread": round((max(times[m]) - min(times[m])) / med, 3)}
                 print(json.dumps(line), flush=True)
@@ -89,7 +96,7 @@ def main():
                     out.write(json.dumps(line) + "\n")
         del X, W, dY, Y, Hs, dX, ws, ads
         torch.cuda.empty_cache()
-    os.environ.pop("MUX_RASTER", None)
+    os.environ.pop(V, None)
 
 
 if __name__ == "__main__":
