@@ -832,12 +832,16 @@ def _tp_block(args, w, torch, mux, tp, Backend, world, rank):
     del Wfull, afull
     be = Backend()
     be.task_tokens = list(w.task_tokens)
-    blk = tp_block.TPDecoderBlock(be, shape, Wp, ap, r_cap, col_off=col_off, shared_shrink=args.shared_shrink)
+    if args.shared_shrink < 0:   # auto: at N > 1 each rank shrinks 1/N of the rows (tp.py shared_shrink)
+        args.shared_shrink = int(world > 1)
+    blk = tp_block.TPDecoderBlock(be, shape, Wp, ap, r_cap, col_off=col_off,
+                                  shared_shrink=bool(args.shared_shrink))
     i32 = dict(dtype=torch.int32, device="cuda")
     tso, sl = torch.tensor(w.off, **i32), torch.tensor(w.lens, **i32)
     cap = torch.tensor(w.cap, **i32) if w.cap else None
     packed = _packed_rows_once(torch, mux, w.off, w.lens, w.cap)   # sized once at setup (see _tp_chain)
-    max_rows = -(-packed // (64 * world)) * 64 * world
+    blk_rows = 256 if args.shared_shrink else 64   # shared shrink: per-rank rows in whole pair row blocks
+    max_rows = -(-packed // (blk_rows * world)) * blk_rows * world
     rows = max_rows // world
     pk = mux.alloc_pack_outputs(w.M, w.S, max_rows, max_rows // 64)
     rs = torch.empty(max_rows, **i32)
@@ -1224,8 +1228,9 @@ def main():
                     help="--mode tp / block, configs 4/5: q|k|v and gate|up as one column-sliced GEMM each (1), "
                          "seven separate linears (0), or auto (-1, default: fused where a per-rank projection "
                          f"shard is narrower than {FUSE_BELOW_COLS} columns)")
-    ap.add_argument("--shared-shrink", action="store_true",
-                    help="--mode tp, configs 4/5: column layers shrink only their own rows and all-gather Hs")
+    ap.add_argument("--shared-shrink", type=int, default=-1, choices=(-1, 0, 1),
+                    help="--mode tp, configs 4/5: column layers shrink only their own rows and all-gather Hs "
+                         "(1), recompute every row's shrink on every rank (0), or auto (-1: on for N > 1)")
     ap.add_argument("--fused-rs", action="store_true",
                     help="--mode tp: reduce-scatters fused into the GEMMs (peer stores via symmetric memory)")
     ap.add_argument("--fused-ag", action="store_true",
