@@ -20,11 +20,14 @@ constexpr int kBN = 256;        // output columns per tile (TMEM columns per acc
 // Reduction depth per pipeline stage: 64 (6 stages) for the forward kernel,
 // 128 (3 stages) for the backward dX kernel (measured best for each,
 // profiles/r01_gemm_ab_bk.jsonl).  Both keep 192 KB of operands in flight.
+#ifndef MUX_BWD_BK
+#define MUX_BWD_BK 128   // A/B builds: 64 (then 6 stages)
+#endif
 template <bool kBwd>
 struct GemmCfg {
-  static constexpr int kBK = kBwd ? 128 : 64;
+  static constexpr int kBK = kBwd ? MUX_BWD_BK : 64;
   static constexpr int kKSub = kBK / 64;  // 128 B swizzle rows (64 bf16) per stage row
-  static constexpr int kStages = kBwd ? 3 : 6;
+  static constexpr int kStages = kBwd ? (MUX_BWD_BK == 64 ? 6 : 3) : 6;
 };
 constexpr int kRowQuarter = 64; // segment granularity inside a pair tile (chunk minimum)
 constexpr int kSideN = 128;     // N of the shrink MMA (rank padded to 64 in CTA 0's half)
