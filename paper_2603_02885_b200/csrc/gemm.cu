@@ -674,6 +674,73 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             }
           }
         } else {
+          if constexpr (kWide) {
+            // Wide tiles: one accumulator, drained by the epilogue in two halves (tempty_bar[0] after
+            // columns 0-255, tempty_bar[1] after 256-511).  The tile starts as soon as half 0 is free
+            // (waited above); the second half's MMAs of the first k-blocks are held back — their
+            // stages stay occupied, up to kStages - 1 of them — until half 1 has drained, so the
+            // previous tile's epilogue overlaps this tile's first k-blocks.
+            const uint32_t h1_bar = smem_u32(&tempty_bar[1]);
+            bool h1 = false;
+            int pend = 0, pst = 0, pkb = 0;
+            auto h1_mmas = [&](int st, int kbb) {
+              const uint32_t a2 = a_lo0 + st * kStageStep;
+              const uint32_t b2 = b_lo0 + st * kStageStep + kBHalf2;
+#pragma unroll
+              for (int k = 0; k < kBK / 16; ++k)
+                mma_bf16_pair_nomask(d_tmem + 256, make_desc(a2 + a_off(k), kHi), make_desc(b2 + b_off(k), kHi),
+                                     kIdescMain, (kbb | k) != 0);
+              mma_commit_pair_mc(&empty_bar[st], kPairMask);
+            };
+            auto flush = [&]() {  // half 1 is free: its held-back MMAs, oldest stage first
+              for (int i = 0; i < pend; ++i) {
+                int st = pst + i;
+                if (st >= kStages) st -= kStages;
+                if (elect_one_sync()) h1_mmas(st, pkb + i);
+                __syncwarp();
+              }
+              pend = 0;
+            };
+            for (int kb = 0; kb < num_kb; ++kb) {
+              PROF_T0(tw_);
+              mbar_wait(&full_bar[stage], phase);
+              PROF_ADD(mw_full, tw_);
+              tc_fence_after();
+              const uint32_t a_lo = a_lo0 + stage * kStageStep;
+              const uint32_t b_lo = b_lo0 + stage * kStageStep;
+              if (elect_one_sync()) {
+#pragma unroll
+                for (int k = 0; k < kBK / 16; ++k)
+                  mma_bf16_pair_nomask(d_tmem, make_desc(a_lo + a_off(k), kHi), make_desc(b_lo + b_off(k), kHi),
+                                       kIdescMain, (kb | k) != 0);
+              }
+              __syncwarp();
+              if (!h1) {
+                h1 = __all_sync(0xffffffffu, mbar_test_wait(h1_bar, acc_phase ^ 1u));
+                if (!h1 && pend == kStages - 1) {
+                  mbar_wait(&tempty_bar[1], acc_phase ^ 1u);
+                  h1 = true;
+                }
+                if (h1) {
+                  tc_fence_after();
+                  flush();
+                }
+              }
+              if (h1) {
+                if (elect_one_sync()) h1_mmas(stage, kb);
+                __syncwarp();
+              } else {
+                if (pend == 0) { pst = stage; pkb = kb; }
+                ++pend;
+              }
+              advance();
+            }
+            if (!h1) {
+              mbar_wait(&tempty_bar[1], acc_phase ^ 1u);
+              tc_fence_after();
+              flush();
+            }
+          } else {
           for (int kb = pc.k0; kb < pc.k1; ++kb) {
             PROF_T0(tw_);
             mbar_wait(&full_bar[stage], phase);
@@ -683,18 +750,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             const uint32_t b_lo = b_lo0 + stage * kStageStep;
             if (elect_one_sync()) {
 #pragma unroll
-              for (int k = 0; k < kBK / 16; ++k) {
+              for (int k = 0; k < kBK / 16; ++k)
                 mma_bf16_pair_nomask(d_tmem, make_desc(a_lo + a_off(k), kHi), make_desc(b_lo + b_off(k), kHi),
                                      kIdescMain, ((kb - pc.k0) | k) != 0);
-                if (kWide)
-                  mma_bf16_pair_nomask(d_tmem + 256, make_desc(a_lo + a_off(k), kHi),
-                                       make_desc(b_lo + kBHalf2 + b_off(k), kHi), kIdescMain,
-                                       ((kb - pc.k0) | k) != 0);
-              }
               mma_commit_pair_mc(&empty_bar[stage], kPairMask);
             }
             __syncwarp();
             advance();
+          }
           }
           // LoRA expand: the tile's final piece only, the producer's (group, live slice) blocks
           const int S = p.num_slices;
@@ -762,6 +825,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       const int row_w = tl.m * kPairRows + kBM * static_cast<int>(crank) + 32 * q;  // first row of this warp
       const uint32_t t_addr = tmem_base + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(acc * kBN);
       const uint32_t tempty_leader = mapa_shared(smem_u32(&tempty_bar[acc]), 0);
+      // wide tiles: the second half of the accumulator has its own barrier (see the MMA issuer)
+      const uint32_t tempty_leader1 = mapa_shared(smem_u32(&tempty_bar[1]), 0);
       if (tl.side) {
         // slice sl of the shrink sits in TMEM columns [64 sl, 64 sl + 64) -> Hs/Gs columns
         // [sl * r_cap, sl * r_cap + r_cap), scaled by the row's task's s_{t,sl}
@@ -777,7 +842,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           if (sl == S - 1) {
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(tempty_leader);
+            if (lane == 0) {
+              mbar_arrive_cluster(tempty_leader);
+              if (kWide) mbar_arrive_cluster(tempty_leader1);  // side tiles never touch half 1
+            }
           }
           if (row < total_rows) {
             const int slot = seg >= 0 ? p.seg_adapter[seg] * S + sl : 0;
@@ -877,10 +945,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
               }
             }
           }
-          if (c == kTileN / 64 - 1) {
+          if (kWide && c == kTileN / 128 - 1) {  // wide: half 0 drained, the next tile may start
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(tempty_leader);
+          }
+          if (c == kTileN / 64 - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(kWide ? tempty_leader1 : tempty_leader);
           }
           uint8_t* buf = bufs + buf_sel * kEpiBuf;
           PROF_T0(tsw_);
