@@ -147,6 +147,59 @@ int main(void) {
   CK(cudaMemcpy(ga, gA[0], sizeof(ga), cudaMemcpyDeviceToHost));
   printf("Y[0,0:4] = %.4f %.4f %.4f %.4f   dA_0[0,0:2] = %.4f %.4f\n", bf2f(y[0]), bf2f(y[1]), bf2f(y[2]),
          bf2f(y[3]), ga[0], ga[1]);
+  /* a fused projection through the generic entry point: W2 = [W; W] (512 output columns in two
+   * slices), each task with one adapter per slice (slice 0: the adapters above, slice 1: the same A
+   * with scale 1); slice 0 of the output must equal the plain call's Y bit for bit. */
+  {
+    mux_bf16 *dW2, *dY2, *dHs2;
+    CK(cudaMalloc((void**)&dW2, sizeof(short) * 2 * N * K));
+    CK(cudaMalloc((void**)&dY2, sizeof(short) * max_rows * 2 * N));
+    CK(cudaMalloc((void**)&dHs2, sizeof(short) * max_rows * 2 * R_CAP));
+    CK(cudaMemcpy(dW2, dW, sizeof(short) * N * K, cudaMemcpyDeviceToDevice));
+    CK(cudaMemcpy(dW2 + (size_t)N * K, dW, sizeof(short) * N * K, cudaMemcpyDeviceToDevice));
+    mux_adapter ad2[4];
+    for (int t = 0; t < 2; ++t) {
+      ad2[2 * t] = ad[t];
+      ad2[2 * t + 1] = ad[t];
+      ad2[2 * t + 1].scale = 1.0f;
+    }
+    mux_slices sl = {2, {0, N, 2 * N, 0, 0}};
+    size_t wsb2 = mux_linear_workspace_size(2, max_rows, K, 2 * N, 2 * R_CAP);
+    void* ws2;
+    CK(cudaMalloc(&ws2, wsb2));
+    CK(cudaMemset(ws2, 0, wsb2));
+    mux_linear_args a;
+    memset(&a, 0, sizeof(a));
+    a.op = MUX_OP_FWD;
+    a.num_segs = 2;
+    a.seg_off = d_seg;
+    a.seg_task = seg_task;
+    a.num_adapters = 2;
+    a.adapters = ad2;
+    a.slices = &sl;
+    a.max_rows = max_rows;
+    a.K = K;
+    a.N = 2 * N;
+    a.r_cap = R_CAP;
+    a.X = dX;
+    a.W = dW2;
+    a.Y = dY2;
+    a.Hs = dHs2;
+    a.workspace = ws2;
+    a.workspace_bytes = wsb2;
+    MK(mux_linear(&a));
+    CK(cudaDeviceSynchronize());
+    unsigned short* y1 = malloc(sizeof(short) * info.total_rows * N);
+    unsigned short* y2 = malloc(sizeof(short) * info.total_rows * 2 * N);
+    CK(cudaMemcpy(y1, dY, sizeof(short) * info.total_rows * N, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(y2, dY2, sizeof(short) * info.total_rows * 2 * N, cudaMemcpyDeviceToHost));
+    int same = 1;
+    for (int r = 0; r < info.total_rows; ++r)
+      for (int c = 0; c < N; ++c) same &= y1[(size_t)r * N + c] == y2[(size_t)r * 2 * N + c];
+    printf("sliced: slice 0 == plain Y: %s\n", same ? "yes" : "no");
+    free(y1);
+    free(y2);
+  }
   /* an invalid call: K not a multiple of 8 -> MUX_ERR_INVALID_ARGUMENT, nothing launched */
   mux_status bad = mux_linear_fwd(2, d_seg, seg_task, 2, ad, max_rows, 100, N, R_CAP, dX, dW, dY, dHs, ws, wsb, 0);
   printf("invalid K -> status %d (%s)\n", (int)bad, mux_last_error());

@@ -35,3 +35,4 @@ def test_c_example_runs():
     assert out.returncode == 0, out.stdout + out.stderr
     assert "ok" in out.stdout and "status 1" in out.stdout, out.stdout
     assert "rows 192 (valid 184)" in out.stdout, out.stdout
+    assert "sliced: slice 0 == plain Y: yes" in out.stdout, out.stdout
