@@ -679,7 +679,7 @@ def _tp_chain(args, w, torch, mux, tp, orchestrate, Backend, world, rank):
     plan_note = None
     if args.htasks == 0:
         from paper_2603_02885_b200 import planner
-        prof = planner.load_profile(os.path.join(ROOT, "profiles", "r01_op_profile.json"))
+        prof = planner.load_profile(os.path.join(ROOT, "profiles", "r02_op_profile.json"))
         L = planner.htask_latency([planner.stage_from_profile(prof, n_gpus=world)], C=1)
         tasks_ = [planner.Task(str(t), w.task_tokens[t], w.wl.ranks[t]) for t in range(w.M)]
         plan = planner.fuse_tasks(tasks_, L, S=1)

@@ -25,7 +25,7 @@ separate hTasks interleaved by orchestrate.py.
 
 Measured profiles: `OpProfile` interpolates a table of (tokens, ms) measured
 on the B200 with the fused kernels (tools/op_profile.py ->
-profiles/r01_op_profile.json), piecewise linear, extrapolated linearly from
+profiles/r02_op_profile.json), piecewise linear, extrapolated linearly from
 the last two points.
 """
 from __future__ import annotations
@@ -172,7 +172,7 @@ def fuse_tasks(tasks: Sequence[Task], L: Callable[[Sequence[int]], float], S: in
 
 # ------------------------------------------------------------------ measured profiles
 def load_profile(path: str) -> dict:
-    """profiles/r01_op_profile.json (tools/op_profile.py): per linear shape, a
+    """profiles/r02_op_profile.json (tools/op_profile.py): per linear shape, a
     table of fused fwd+bwd latency (ms) vs packed tokens for rank-0 (BaseOp
     only) and rank-r adapters."""
     with open(path) as f:

@@ -6,7 +6,7 @@ the task-count sweep of SURVEY §8(d) config 2 (the B200 analogue of P:528,
 1. For each config-2 linear (4096->4096, 4096->11008, 11008->4096): fused
    fwd+bwd latency (mux_linear_fwd + mux_linear_bwd, one segment) at packed
    token counts x in --tokens, with rank 0 (BaseOp only, t_o(x)) and with one
-   rank-r adapter (t_o(x) + t_a(x)).  -> profiles/r01_op_profile.json
+   rank-r adapter (t_o(x) + t_a(x)).  -> profiles/r02_op_profile.json
 2. Task-count sweep: m tasks x --per-task tokens each, rank r, multiplexed in
    one call per linear vs the same m tasks run one after another (temporal
    interleaving on one GPU), tokens/s of each; and the planner's choice for
@@ -87,7 +87,7 @@ def main():
     ap.add_argument("--sweep", default="1,2,4,8,16")
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--rounds", type=int, default=5)
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_op_profile.json"))
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r02_op_profile.json"))
     a = ap.parse_args()
     from paper_2603_02885_b200 import mux, planner
     toks = [int(v) for v in a.tokens.split(",")]
