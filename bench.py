@@ -498,19 +498,25 @@ def main_arm(args):
         h_grads = [torch.empty(g.shape, dtype=g.dtype, pin_memory=True) for g in grads]
         h2d = sum(x.numel() * x.element_size() for x in h_in[0])
         d2h = sum(g.numel() * g.element_size() for g in grads)
-        copy_stream = torch.cuda.Stream()
-        copied = [torch.cuda.Event() for _ in range(2)]
+        # two H2D streams (the layer input and the loss gradient, 90 MB each at config 2, on separate
+        # copy engines: one stream alone moved ~41 GB/s and bounded the step) and one D2H stream
+        h2d_streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+        d2h_stream = torch.cuda.Stream()
+        copied = [[torch.cuda.Event() for _ in range(2)] for _ in range(2)]   # [slot][h2d stream]
         consumed = [torch.cuda.Event() for _ in range(2)]
         step_done = torch.cuda.Event()
         d2h_done = torch.cuda.Event()
 
         def h2d_copy(i):
             slot = i % 2
-            with torch.cuda.stream(copy_stream):
-                copy_stream.wait_event(consumed[slot])
-                for dst, src in zip((ms.tso[slot], ms.sl[slot], ms.X1tok[slot], ms.dY3tok[slot]), h_in[i % 2]):
-                    dst.copy_(src, non_blocking=True)
-                copied[slot].record(copy_stream)
+            dsts = (ms.tso[slot], ms.sl[slot], ms.X1tok[slot], ms.dY3tok[slot])
+            for j, cs in enumerate(h2d_streams):
+                with torch.cuda.stream(cs):
+                    cs.wait_event(consumed[slot])
+                    for k, (dst, src) in enumerate(zip(dsts, h_in[slot])):
+                        if (k == 3) == (j == 1):   # stream 1: dY; stream 0: metadata and X
+                            dst.copy_(src, non_blocking=True)
+                    copied[slot][j].record(cs)
 
         def e2e_run(n):
             for ev in consumed:
@@ -521,17 +527,18 @@ def main_arm(args):
                 slot = i % 2
                 if i + 1 < n:
                     h2d_copy(i + 1)
-                stream.wait_event(copied[slot])
-                # the gradient read-back of step i-1 (copy stream) must finish
-                # before this step's backward overwrites dA/dB
+                for ev in copied[slot]:
+                    stream.wait_event(ev)
+                # the gradient read-back of step i-1 must finish before this step's backward
+                # overwrites dA/dB
                 ms.step(slot=slot, before_bwd=lambda: stream.wait_event(d2h_done))
                 consumed[slot].record(stream)
                 step_done.record(stream)
-                with torch.cuda.stream(copy_stream):
-                    copy_stream.wait_event(step_done)
+                with torch.cuda.stream(d2h_stream):
+                    d2h_stream.wait_event(step_done)
                     for g, hg in zip(grads, h_grads):
                         hg.copy_(g, non_blocking=True)
-                    d2h_done.record(copy_stream)
+                    d2h_done.record(d2h_stream)
 
         e2e_run(max(1, args.warmup))
         torch.cuda.synchronize()
@@ -540,9 +547,11 @@ def main_arm(args):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        copy_stream.wait_event(e0)
+        for cs in h2d_streams + [d2h_stream]:
+            cs.wait_event(e0)
         e2e_run(args.steps)
-        stream.wait_stream(copy_stream)
+        for cs in h2d_streams + [d2h_stream]:
+            stream.wait_stream(cs)
         e1.record(stream)
         torch.cuda.synchronize()
         te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
@@ -552,8 +561,8 @@ def main_arm(args):
         e2e = {"value": T_all / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms,
                "what": "pinned H2D of seq metadata + token-major layer input X and loss gradient dY (prefetched "
-                       "one step ahead on a copy stream); D2H of every adapter gradient dA_t/dB_t (fp32) on "
-                       "the copy stream, overlapped with the next step's forward"}
+                       "one step ahead on two copy streams); D2H of every adapter gradient dA_t/dB_t (fp32) on "
+                       "a third stream, overlapped with the next step's forward"}
 
     value = T_all / (ms_step * 1e-3)
     tflops = w.flops / (ms_step * 1e-3) / 1e12
@@ -1031,8 +1040,12 @@ def _e2e_generic(torch, dist, stream, step, h2d_src, results, args, tokens):
     h_res = [torch.empty(g.shape, dtype=g.dtype, pin_memory=True) for g in results]
     h2d = sum(x.numel() * x.element_size() for x in host)
     d2h = sum(g.numel() * g.element_size() for g in results)
+    # the inputs alternate over two H2D streams by size (separate copy engines), the read-back has its own
+    h2ds = [torch.cuda.Stream(), torch.cuda.Stream()]
     cs = torch.cuda.Stream()
-    copied = [torch.cuda.Event() for _ in range(2)]
+    order = sorted(range(len(host)), key=lambda k: -host[k].numel() * host[k].element_size())
+    lane_of = {k: j % 2 for j, k in enumerate(order)}
+    copied = [[torch.cuda.Event() for _ in range(2)] for _ in range(2)]
     consumed = [torch.cuda.Event() for _ in range(2)]
     done, read = torch.cuda.Event(), torch.cuda.Event()
 
@@ -1042,16 +1055,19 @@ def _e2e_generic(torch, dist, stream, step, h2d_src, results, args, tokens):
         read.record(stream)
 
         def h2d_copy(i):
-            with torch.cuda.stream(cs):
-                cs.wait_event(consumed[i % 2])
-                for d_, h_ in zip(slots[i % 2], host):
-                    d_.copy_(h_, non_blocking=True)
-                copied[i % 2].record(cs)
+            for j, hs in enumerate(h2ds):
+                with torch.cuda.stream(hs):
+                    hs.wait_event(consumed[i % 2])
+                    for k, (d_, h_) in enumerate(zip(slots[i % 2], host)):
+                        if lane_of[k] == j:
+                            d_.copy_(h_, non_blocking=True)
+                    copied[i % 2][j].record(hs)
         h2d_copy(0)
         for i in range(n):
             if i + 1 < n:
                 h2d_copy(i + 1)
-            stream.wait_event(copied[i % 2])
+            for ev in copied[i % 2]:
+                stream.wait_event(ev)
             for d_, s_ in zip(h2d_src, slots[i % 2]):     # the step reads its inputs from their home
                 d_.copy_(s_, non_blocking=True)
             consumed[i % 2].record(stream)
@@ -1069,9 +1085,11 @@ def _e2e_generic(torch, dist, stream, step, h2d_src, results, args, tokens):
     dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    cs.wait_event(e0)
+    for s_ in h2ds + [cs]:
+        s_.wait_event(e0)
     run(args.steps)
-    stream.wait_stream(cs)
+    for s_ in h2ds + [cs]:
+        stream.wait_stream(s_)
     e1.record(stream)
     torch.cuda.synchronize()
     te = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device="cuda")
@@ -1080,8 +1098,8 @@ def _e2e_generic(torch, dist, stream, step, h2d_src, results, args, tokens):
     return {"value": tokens / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms,
             "what": "per rank: pinned H2D of the sequence metadata and this rank's 1/p share of the token-major "
-                    "input and loss gradient (a sharded data loader's bytes; prefetched one step ahead on a copy "
-                    "stream, staged into the device buffers the step reads); D2H of this rank's adapter-gradient "
+                    "input and loss gradient (a sharded data loader's bytes; prefetched one step ahead on two copy "
+                    "streams, staged into the device buffers the step reads); D2H of this rank's adapter-gradient "
                     "shards (replicated all-reduced gradients only on rank 0), overlapped with the next step"}
 
 
