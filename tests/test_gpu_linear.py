@@ -271,3 +271,14 @@ def test_shrink_and_fwd_with_given_hs_bit_identical():
         assert torch.isnan(outside.float()).all(), (lo, hi)
     with pytest.raises(mux.MuxError):
         mux.linear_shrink(seg_off, p.seg_task, ads, X, p.N, p.r_cap, 100, 356)
+
+
+def test_more_row_blocks_than_the_group_table():
+    """> 128 pair row blocks (64 segments, 36 608 rows): the GEMM computes the tile task groups on the
+    fly instead of from its per-launch shared-memory table (gemm.cu kGroupTab); integer inputs
+    bit-exact, 64-row-granular segments straddling tiles across the whole range, 16 tasks."""
+    segs = [64 * (5 + (i * 5) % 9) for i in range(64)]
+    ranks = [(4, 8, 16, 32)[t % 4] for t in range(16)]
+    p = Problem(128, 128, segs, ranks, variant="int", seg_task=[s % 16 for s in range(64)], seed=31)
+    assert p.R > 128 * 256
+    _run(p, exact=True)
