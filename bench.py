@@ -686,6 +686,8 @@ def _tp_chain(args, w, torch, mux, tp, orchestrate, Backend, world, rank):
     input), L1 row (RS of its output), L2 column; backward mirrors it.  `--htasks g` splits the tasks
     into g hTasks interleaved by Alg. 1 (orchestrate.py, NEXT-1)."""
     plan_note = None
+    if args.htasks < 0:
+        args.htasks = 2 if world > 1 else 1
     if args.htasks == 0:
         from paper_2603_02885_b200 import planner
         prof = planner.load_profile(os.path.join(ROOT, "profiles", "r02_op_profile.json"))
@@ -1239,8 +1241,10 @@ def main():
                     help="auto: N=1 -> the single-GPU step (replicas x1), N>1 -> tensor parallel (strong scaling, "
                          "the north_star TP path) with the task-sharded replicas as a secondary field")
     ap.add_argument("--no-replicas", action="store_true", help="--mode tp, N>1: skip the secondary replicas timing")
-    ap.add_argument("--htasks", type=int, default=1,
-                    help="--mode tp: hTasks interleaved by Alg. 1 (NEXT-1); 0 = chosen by the planner (NEXT-4)")
+    ap.add_argument("--htasks", type=int, default=-1,
+                    help="--mode tp, config 2: hTasks interleaved by Alg. 1 (NEXT-1) so one hTask's collectives "
+                         "overlap another's GEMMs; 0 = chosen by the planner (NEXT-4); -1 (default) = 2 for N > 1 "
+                         "(at N = 1 the collectives are local copies: 1)")
     ap.add_argument("--comm-ctas", type=int, default=0, help="--mode tp: NCCL_MAX_CTAS for the overlapped collectives")
     ap.add_argument("--fused-proj", type=int, default=-1, choices=(-1, 0, 1),
                     help="--mode tp / block, configs 4/5: q|k|v and gate|up as one column-sliced GEMM each (1), "
