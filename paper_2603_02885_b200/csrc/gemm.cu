@@ -341,7 +341,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   uint64_t* empty_bar = full_bar + kStages;
   uint64_t* tfull_bar = empty_bar + kStages;
   uint64_t* tempty_bar = tfull_bar + 2;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  // the TMEM address slot sits apart from the mbarriers (which peer CTAs and the async proxy write)
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(misc + 192);
+  static_assert((2 * GemmLayout<kBwd, kTileN>::kStages + 4) * 8 <= 192, "mbarriers overlap the TMEM slot");
   int* so = reinterpret_cast<int*>(misc + 256);  // seg_off copy, <= 65 ints
   int* skb = reinterpret_cast<int*>(misc + 528);  // stream-K range table, <= kSkMaxClusters + 1 ints
   uint2* gtab = reinterpret_cast<uint2*>(misc + kSmemMisc);  // [kGroupTab] {seg4, hm4 | n << 24}
