@@ -16,7 +16,8 @@ from typing import List, Optional, Sequence
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmux.so")
+# MUX_LIB_FILE selects an experiment build under this directory (A/B only, e.g. libmux_direct.so)
+LIB_PATH = os.path.join(_HERE, os.environ.get("MUX_LIB_FILE", "libmux.so"))
 
 MUX_OK = 0
 STATUS = {0: "MUX_OK", 1: "MUX_ERR_INVALID_ARGUMENT", 2: "MUX_ERR_UNSUPPORTED",
