@@ -205,3 +205,29 @@ def test_sliced_nan_stays_in_its_task():
         for s in range(3):
             if p.ranks[t][s]:
                 assert np.isfinite(g["dA"][t][s]).all() and np.isfinite(g["dB"][t][s]).all()
+
+
+@pytest.mark.parametrize("case", range(12))
+def test_sliced_fuzz_integer_bit_exact(case):
+    """Random fused projections: 1-4 slices of random widths (multiples of 8, some below one 64-column
+    box), 1-6 tasks with random ranks per slice (0 allowed), random 64-row segments (a task may own
+    several), K a multiple of 8; integer inputs, every output bit-exact against the oracle."""
+    rng = np.random.default_rng(4000 + case)
+    S = int(rng.integers(1, 5))
+    widths = [int(8 * rng.integers(1, 48)) for _ in range(S)]
+    col_off = [0]
+    for w in widths:
+        col_off.append(col_off[-1] + w)
+    T = int(rng.integers(1, 7))
+    ranks = [[int(rng.choice([0, 4, 8, 16, 24, 32, 48, 64])) for _ in range(S)] for _ in range(T)]
+    if all(r == 0 for row in ranks for r in row):
+        ranks[0][0] = 16
+    nseg = int(rng.integers(1, 9))
+    seg_lens = [64 * int(rng.integers(0, 6)) for _ in range(nseg)]
+    if sum(seg_lens) == 0:
+        seg_lens[0] = 64
+    seg_task = [int(rng.integers(0, T)) for _ in range(nseg)]
+    K = int(8 * rng.integers(2, 80))
+    p = SlicedProblem(K=K, col_off=col_off, seg_lens=seg_lens, ranks=ranks, seg_task=seg_task, variant="int",
+                      seed=5000 + case)
+    check(p, exact=True)
