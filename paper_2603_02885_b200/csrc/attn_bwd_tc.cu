@@ -90,8 +90,12 @@ __global__ void __launch_bounds__(256) mux_attn_bwd_pre_kernel(int R, int H, con
 
 // =========================================================================== dQ
 // smem: Q 32 KB | dO 32 KB | dS 16 KB | K 16 KB, V 16 KB  (112 KB) | barriers
-constexpr int kDqStages = 1;
-__global__ void __launch_bounds__(kThreadsB, 2) mux_attn_dq_tc_kernel(const __grid_constant__ AttnBwdTcParams p) {
+#ifndef MUX_DQ_STAGES
+#define MUX_DQ_STAGES 1   // A/B builds: 2 (then 144 KB of smem, one CTA per SM)
+#endif
+constexpr int kDqStages = MUX_DQ_STAGES;
+__global__ void __launch_bounds__(kThreadsB, kDqStages == 1 ? 2 : 1)
+    mux_attn_dq_tc_kernel(const __grid_constant__ AttnBwdTcParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   if ((smem_u32(smem) & 1023u) != 0) __trap();
   constexpr uint32_t oQ = 0, oDO = 2 * kSub128, oDS = 4 * kSub128, oKV = 5 * kSub128;
@@ -311,10 +315,14 @@ __global__ void __launch_bounds__(kThreadsB, 2) mux_attn_dq_tc_kernel(const __gr
 // =========================================================================== dK, dV
 // smem: K 32 KB | [dK: V 32 KB] | P^T or dS^T 16 KB | Q 16 KB, dO 16 KB (one stage) | scalars | barriers
 // Q/dO ring depth: dV (no V tile) fits two stages in 112 KB, dK one; either way two CTAs share an SM
+#ifndef MUX_DK_STAGES
+#define MUX_DK_STAGES 1   // A/B builds: 2 (then 144 KB of smem for dK, one CTA per SM)
+#endif
 template <bool kDK>
-constexpr int qd_stages() { return kDK ? 1 : 2; }
+constexpr int qd_stages() { return kDK ? MUX_DK_STAGES : 2; }
 template <bool kDK>
-__global__ void __launch_bounds__(kThreadsB, 2) mux_attn_dkdv_tc_kernel(const __grid_constant__ AttnBwdTcParams p) {
+__global__ void __launch_bounds__(kThreadsB, (kDK && MUX_DK_STAGES > 1) ? 1 : 2)
+    mux_attn_dkdv_tc_kernel(const __grid_constant__ AttnBwdTcParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   if ((smem_u32(smem) & 1023u) != 0) __trap();
   constexpr uint32_t oK = 0, oV = 2 * kSub128, oT = (kDK ? 4 : 2) * kSub128, oQD = oT + kSub128;
