@@ -375,7 +375,10 @@ typedef enum {
   MUX_OP_SHRINK = 3,     /* mux_linear_shrink over [row_begin, row_end) */
   MUX_OP_BWD = 4,        /* mux_linear_bwd (ag != NULL: mux_linear_bwd_ag) */
   MUX_OP_BWD_DX = 5,     /* mux_linear_bwd_part(MUX_BWD_DX) (rs != NULL: mux_linear_bwd_dx_rs) */
-  MUX_OP_BWD_GRADS = 6   /* mux_linear_bwd_part(MUX_BWD_GRADS) */
+  MUX_OP_BWD_GRADS = 6,  /* mux_linear_bwd_part(MUX_BWD_GRADS) */
+  MUX_OP_SHRINK_BWD = 7  /* Gs[i, s*r_cap + j] = bf16(s_{t,s} dY[i, slice s] B_{t,s}[:, j]) for the pair row
+                            blocks overlapping [row_begin, row_end) into Gs (no X, W, Hs): the per-rank
+                            part of a row-parallel backward whose Gs rows are then all-gathered */
 } mux_linear_op;
 
 /* All arguments of one linear call; fields an op does not use are ignored
@@ -402,6 +405,9 @@ typedef struct {
   void* workspace;                   /* >= mux_linear_workspace_size(num_segs, max_rows, K, N, S * r_cap) */
   size_t workspace_bytes;
   cudaStream_t stream;
+  mux_bf16* Gs;                      /* [max_rows, S * r_cap] backward: NULL = in the workspace; else the
+                                        output of MUX_OP_SHRINK_BWD, or the given Gs of BWD / BWD_DX /
+                                        BWD_GRADS (then no shrink tiles run; e.g. all-gathered rows) */
 } mux_linear_args;
 
 /* One linear call described by `a` (the per-op entry points above are this

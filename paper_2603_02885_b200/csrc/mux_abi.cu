@@ -446,7 +446,12 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
                                 size_t workspace_bytes, cudaStream_t stream, int parts = 3,
                                 const mux_rs* rs = nullptr, const mux_ag* ag = nullptr, bool hs_given = false,
                                 bool shrink_only = false, int32_t side_row_lo = 0,
-                                int32_t side_row_hi = INT32_MAX, const mux_slices* slices = nullptr) {
+                                int32_t side_row_hi = INT32_MAX, const mux_slices* slices = nullptr,
+                                __nv_bfloat16* Gs_ext = nullptr) {
+  // Gs_ext (backward only): the caller's Gs [max_rows, S * r_cap] instead of the workspace's — the
+  // output of a shrink-only launch, otherwise an input (no shrink tiles; e.g. the rows of a
+  // row-parallel layer's Gs computed once per rank and all-gathered, tp.py shared_shrink)
+  const bool gs_given = bwd && Gs_ext != nullptr && !shrink_only;
   SliceTab sl;
   mux_status st = make_slices(slices, N, &sl);
   if (st != MUX_OK) return st;
@@ -456,15 +461,16 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
   const int side_ld = S * r_cap;  // Hs / Gs row length: slice s at columns [s * r_cap, (s + 1) * r_cap)
   if (!a_in || (!W && !shrink_only)) return fail(MUX_ERR_INVALID_ARGUMENT, "null input pointer");
   if (hs_given && !Hs_in) return fail(MUX_ERR_INVALID_ARGUMENT, "Hs (input) is null");
-  if (shrink_only && !Hs_out) return fail(MUX_ERR_INVALID_ARGUMENT, "Hs (output) is null");
+  if (shrink_only && !(bwd ? Gs_ext : Hs_out))
+    return fail(MUX_ERR_INVALID_ARGUMENT, "%s (output) is null", bwd ? "Gs" : "Hs");
   if (shrink_only && (side_row_lo < 0 || side_row_lo % kPairRows || side_row_hi < side_row_lo ||
                       (side_row_hi % kPairRows && side_row_hi < max_rows)))
     return fail(MUX_ERR_INVALID_ARGUMENT, "row range [%d, %d): begin a multiple of 256, end a multiple of 256 or "
                 ">= max_rows (%d)", side_row_lo, side_row_hi, max_rows);
   if (!aligned16(a_in) || (W && !aligned16(W)) || (out && !aligned16(out)) || (X && !aligned16(X)) ||
-      (Hs_in && !aligned16(Hs_in)) || (Hs_out && !aligned16(Hs_out)))
+      (Hs_in && !aligned16(Hs_in)) || (Hs_out && !aligned16(Hs_out)) || (Gs_ext && !aligned16(Gs_ext)))
     return fail(MUX_ERR_INVALID_ARGUMENT, "tensor pointers must be 16-byte aligned");
-  if (bwd && (!X || !Hs_in)) return fail(MUX_ERR_INVALID_ARGUMENT, "bwd needs X and Hs");
+  if (bwd && !shrink_only && (!X || !Hs_in)) return fail(MUX_ERR_INVALID_ARGUMENT, "bwd needs X and Hs");
   if (!bwd && !out && !rs && !shrink_only) return fail(MUX_ERR_INVALID_ARGUMENT, "fwd needs Y");
   const LinearWs need = carve_linear_ws(nullptr, max_rows, side_ld);
   if (!workspace || workspace_bytes < need.bytes)
@@ -476,7 +482,8 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
   std::memset(&p, 0, sizeof(p));
   const int kred = bwd ? N : K;
   const int nout = bwd ? K : N;
-  __nv_bfloat16* side = bwd ? ws.gs : hs_given ? const_cast<__nv_bfloat16*>(Hs_in) : (Hs_out ? Hs_out : ws.hs);
+  __nv_bfloat16* side = bwd ? (Gs_ext ? Gs_ext : ws.gs)
+                            : hs_given ? const_cast<__nv_bfloat16*>(Hs_in) : (Hs_out ? Hs_out : ws.hs);
   if (!make_map(&p.map_a, a_in, kred, max_rows, kred, 64, 128))
     return fail(MUX_ERR_CUDA, "cuTensorMapEncodeTiled failed for %s %p [%d x %d]", bwd ? "dY" : "X", a_in, max_rows, kred);
   if (W && !make_map(&p.map_w, W, K, N, K, 64, 64))
@@ -506,7 +513,7 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
   p.num_slices = S;
   for (int s = 0; s <= S; ++s) p.slice_off[s] = sl.off[s];
   p.has_main = out != nullptr || rs != nullptr;
-  p.has_side = hs_given ? 0 : 1;
+  p.has_side = (hs_given || gs_given) ? 0 : 1;
   // short reductions: side tiles first (A/B in DESIGN §12: +3-9 % at kred <= 1376, neutral at 4096+)
   p.side_first = kred <= MUX_SIDE_FIRST_MAX_KRED ? 1 : 0;
   p.side_m_lo = side_row_lo / kPairRows;
@@ -654,7 +661,7 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
       if (!make_map(&g.map_x, X, K, max_rows, K, 64, 128) ||
           !make_map(&g.map_dy, a_in + sl.off[sc], n_s, max_rows, N, 64, 128) ||
           !make_map(&g.map_hs, Hs_in + sc * r_cap, r_cap, max_rows, side_ld, 64, 128) ||
-          !make_map(&g.map_gs, ws.gs + sc * r_cap, r_cap, max_rows, side_ld, 64, 128))
+          !make_map(&g.map_gs, (Gs_ext ? Gs_ext : ws.gs) + sc * r_cap, r_cap, max_rows, side_ld, 64, 128))
         return fail(MUX_ERR_CUDA, "cuTensorMapEncodeTiled failed for a gradient-kernel operand (X, dY, Hs or Gs)");
       g.seg_off = seg_off;
       g.num_segs = num_segs;
@@ -1130,7 +1137,16 @@ mux_status mux_linear(const mux_linear_args* a) {
       return linear_common(true, a->num_segs, a->seg_off, a->seg_task, a->num_adapters, a->adapters, a->max_rows,
                            a->K, a->N, a->r_cap, dY, c(a->X), c(a->W), a->rs ? nullptr : m(a->dX), c(a->Hs), nullptr,
                            a->workspace, a->workspace_bytes, a->stream, parts, a->rs, a->ag, false, false, 0,
-                           INT32_MAX, a->slices);
+                           INT32_MAX, a->slices, m(a->Gs));
+    }
+    case MUX_OP_SHRINK_BWD: {
+      if (a->rs) return fail(MUX_ERR_INVALID_ARGUMENT, "shrink_bwd: no fused reduce-scatter");
+      if (!a->Gs) return fail(MUX_ERR_INVALID_ARGUMENT, "shrink_bwd: Gs (output) is null");
+      const bf* dY = a->ag ? ag_buf : c(a->dY);
+      return linear_common(true, a->num_segs, a->seg_off, a->seg_task, a->num_adapters, a->adapters, a->max_rows,
+                           a->K, a->N, a->r_cap, dY, nullptr, nullptr, nullptr, nullptr, nullptr, a->workspace,
+                           a->workspace_bytes, a->stream, 3, nullptr, a->ag, false, true, a->row_begin, a->row_end,
+                           a->slices, m(a->Gs));
     }
     default:
       return fail(MUX_ERR_INVALID_ARGUMENT, "unknown op %d", a->op);

@@ -436,7 +436,7 @@ def linear_bwd(seg_off: torch.Tensor, seg_task: Sequence[int], adapters: Sequenc
 
 
 # ---------------------------------------------------------------- fused projections (column slices)
-OP_FWD, OP_FWD_HS, OP_SHRINK, OP_BWD, OP_BWD_DX, OP_BWD_GRADS = 1, 2, 3, 4, 5, 6
+OP_FWD, OP_FWD_HS, OP_SHRINK, OP_BWD, OP_BWD_DX, OP_BWD_GRADS, OP_SHRINK_BWD = 1, 2, 3, 4, 5, 6, 7
 
 
 class _Slices(ctypes.Structure):
@@ -451,7 +451,7 @@ class _LinearArgs(ctypes.Structure):
                 ("dY", ctypes.c_void_p), ("Y", ctypes.c_void_p), ("Hs", ctypes.c_void_p), ("dX", ctypes.c_void_p),
                 ("row_begin", ctypes.c_int32), ("row_end", ctypes.c_int32), ("rs", ctypes.c_void_p),
                 ("ag", ctypes.c_void_p), ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t),
-                ("stream", ctypes.c_void_p)]
+                ("stream", ctypes.c_void_p), ("Gs", ctypes.c_void_p)]
 
 
 def _flat_slots(adapters) -> List[Adapter]:
@@ -514,8 +514,8 @@ def _check_sliced(seg_off, seg_task, adapters, col_off, K, N, rows, r_cap, grads
 
 
 def linear(op: int, seg_off, seg_task, adapters, col_off, K: int, N: int, r_cap: int, max_rows: int, *, X=None,
-           W=None, dY=None, Y=None, Hs=None, dX=None, row_begin: int = 0, row_end: int = None, rs=None, ag=None,
-           workspace=None, stream=None, want_grads=False):
+           W=None, dY=None, Y=None, Hs=None, dX=None, Gs=None, row_begin: int = 0, row_end: int = None, rs=None,
+           ag=None, workspace=None, stream=None, want_grads=False):
     """mux_linear: one call of any op over column slices col_off (adapters[t][s]).  Marshalling only."""
     S = len(col_off) - 1
     _need(1 <= S <= MAX_SLICES, f"1..{MAX_SLICES} slices")
@@ -533,7 +533,7 @@ def linear(op: int, seg_off, seg_task, adapters, col_off, K: int, N: int, r_cap:
     a.op, a.num_segs, a.seg_off, a.seg_task = op, len(seg_task), seg_off.data_ptr(), ctypes.addressof(st)
     a.num_adapters, a.adapters, a.slices = len(adapters), ctypes.addressof(tab), ctypes.addressof(sl)
     a.max_rows, a.K, a.N, a.r_cap = max_rows, K, N, r_cap
-    for f, t in (("X", X), ("W", W), ("dY", dY), ("Y", Y), ("Hs", Hs), ("dX", dX)):
+    for f, t in (("X", X), ("W", W), ("dY", dY), ("Y", Y), ("Hs", Hs), ("dX", dX), ("Gs", Gs)):
         setattr(a, f, None if t is None else t.data_ptr())
     a.row_begin = row_begin
     a.row_end = max_rows if row_end is None else row_end
@@ -587,6 +587,52 @@ def linear_bwd_sliced(seg_off, seg_task, adapters, dY, X, W, Hs, col_off, r_cap:
                   Hs=(Hs, (max_rows, S * r_cap), torch.bfloat16))
     op = {0: OP_BWD, BWD_DX: OP_BWD_DX, BWD_GRADS: OP_BWD_GRADS}[part]
     linear(op, seg_off, seg_task, adapters, col_off, K, N, r_cap, max_rows, X=X, W=W, dY=dY, Hs=Hs, dX=dX,
+           workspace=workspace, stream=stream, want_grads=True)
+    return dX
+
+
+def linear_shrink_bwd(seg_off, seg_task, adapters, dY, K: int, r_cap: int, row_begin: int = 0, row_end: int = None,
+                      Gs=None, col_off=None, workspace=None, stream=None):
+    """mux_linear(MUX_OP_SHRINK_BWD): Gs = bf16(s_t dY B_t) for the pair row blocks overlapping
+    [row_begin, row_end) (rows outside are not written).  adapters: per task (or [t][s] with col_off).
+    Returns Gs [rows, S * r_cap]."""
+    max_rows, N = dY.shape
+    nested = adapters if col_off is not None else [[a] for a in adapters]
+    co = col_off if col_off is not None else [0, N]
+    S = len(co) - 1
+    if Gs is None:
+        Gs = torch.empty(max_rows, S * r_cap, dtype=torch.bfloat16, device=dY.device)
+    _check_sliced(seg_off, seg_task, nested, co, K, N, max_rows, r_cap,
+                  dY=(dY, (max_rows, N), torch.bfloat16), Gs=(Gs, (max_rows, S * r_cap), torch.bfloat16))
+    linear(OP_SHRINK_BWD, seg_off, seg_task, nested, co, K, N, r_cap, max_rows, dY=dY, Gs=Gs, row_begin=row_begin,
+           row_end=max_rows if row_end is None else row_end, workspace=workspace, stream=stream)
+    return Gs
+
+
+def linear_bwd_gs(seg_off, seg_task, adapters, dY, X, W, Hs, Gs, r_cap: int, dX=None, col_off=None,
+                  workspace=None, stream=None, part: int = 0):
+    """mux_linear backward with Gs given (no shrink tiles; e.g. all-gathered rows of a row-parallel
+    layer's Gs): dX = dY W + Gs A_t, dA_t = Gs^T X, dB_t = dY^T Hs.  Returns dX."""
+    max_rows, K = X.shape
+    N = W.shape[0]
+    nested = adapters if col_off is not None else [[a] for a in adapters]
+    co = col_off if col_off is not None else [0, N]
+    if dX is None and part != BWD_GRADS:
+        dX = torch.empty(max_rows, K, dtype=torch.bfloat16, device=X.device)
+    for s_, per_task in enumerate(zip(*nested)):
+        for a in per_task:
+            if a.rank > 0:
+                if a.dA is None:
+                    a.dA = torch.empty(a.rank, K, dtype=torch.float32, device=X.device)
+                if a.dB is None:
+                    a.dB = torch.empty(co[s_ + 1] - co[s_], a.rank, dtype=torch.float32, device=X.device)
+    S = len(co) - 1
+    _check_sliced(seg_off, seg_task, nested, co, K, N, max_rows, r_cap, grads=True,
+                  X=(X, (max_rows, K), torch.bfloat16), W=(W, (N, K), torch.bfloat16),
+                  dY=(dY, (max_rows, N), torch.bfloat16), dX=(dX, (max_rows, K), torch.bfloat16),
+                  Hs=(Hs, (max_rows, S * r_cap), torch.bfloat16), Gs=(Gs, (max_rows, S * r_cap), torch.bfloat16))
+    op = {0: OP_BWD, BWD_DX: OP_BWD_DX, BWD_GRADS: OP_BWD_GRADS}[part]
+    linear(op, seg_off, seg_task, nested, co, K, N, r_cap, max_rows, X=X, W=W, dY=dY, Hs=Hs, dX=dX, Gs=Gs,
            workspace=workspace, stream=stream, want_grads=True)
     return dX
 

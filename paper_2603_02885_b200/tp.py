@@ -219,10 +219,26 @@ class MuxBackend:
             return Y
         return self.mux.linear_fwd_hs(seg_off, seg_task, adapters, X, W, Hs, r_cap, Y=Y, workspace=ws)
 
-    def bwd(self, seg_off, seg_task, adapters, dY, X, W, Hs, r_cap, dX=None, col_off=None):
+    def shrink_bwd(self, seg_off, seg_task, adapters, dY, W, r_cap, row_begin, row_end, col_off=None):
+        """Gs rows [row_begin, row_end) of the full (gathered) dY only (mux_linear MUX_OP_SHRINK_BWD)."""
+        R = dY.shape[0]
+        Gs = self._buf(("Gs", W.data_ptr()), (R, self._hs_cols(r_cap, col_off)), torch.bfloat16, dY.device)
+        n = self.mux.linear_workspace_size(len(seg_task), R, W.shape[1], W.shape[0], self._hs_cols(r_cap, col_off))
+        ws = self._buf(("ws", W.data_ptr()), (n,), torch.uint8, dY.device, zero=True)
+        return self.mux.linear_shrink_bwd(seg_off, seg_task, adapters, dY, W.shape[1], r_cap, row_begin, row_end,
+                                          Gs=Gs, col_off=col_off, workspace=ws)
+
+    def bwd(self, seg_off, seg_task, adapters, dY, X, W, Hs, r_cap, dX=None, col_off=None, Gs=None):
+        """Gs: the shrink of dY given (all-gathered rows; no shrink tiles in the dX GEMM)."""
         if dX is None:
             dX = self._buf(("dX", W.data_ptr()), tuple(X.shape), torch.bfloat16, X.device)
         ws = self._ws(W, X, seg_task, r_cap, col_off)
+        if Gs is not None:
+            dX = self.mux.linear_bwd_gs(seg_off, seg_task, adapters, dY, X, W, Hs, Gs, r_cap, dX=dX, col_off=col_off,
+                                        workspace=ws)
+            if col_off is not None:
+                return dX, [[a.dA for a in row] for row in adapters], [[a.dB for a in row] for row in adapters]
+            return dX, [a.dA for a in adapters], [a.dB for a in adapters]
         if col_off is not None:
             dX = self.mux.linear_bwd_sliced(seg_off, seg_task, adapters, dY, X, W, Hs, col_off, r_cap, dX=dX,
                                             workspace=ws)
@@ -517,10 +533,15 @@ class ColumnParallelMuxLinear:
 
 
 class RowParallelMuxLinear:
+    """shared_shrink: B_t is replicated and every rank holds the full gathered dY, so Gs = s_t dY B_t is the
+    same on every rank: each rank shrinks only its own R/p rows (MUX_OP_SHRINK_BWD), the Gs rows are
+    all-gathered (T x r_cap) and the dX GEMM runs without shrink tiles (the backward mirror of
+    ColumnParallelMuxLinear's shared_shrink; R/p a multiple of 256)."""
+
     def __init__(self, backend, W_shard, adapters_shard, r_cap, group=None, fused_rs=False, fused_ag=False,
-                 nvls=None):
+                 nvls=None, shared_shrink=False):
         self.be, self.W, self.ads, self.r_cap, self.group = backend, W_shard, adapters_shard, r_cap, group
-        self.fused_rs, self.fused_ag = fused_rs, fused_ag
+        self.fused_rs, self.fused_ag, self.shared_shrink = fused_rs, fused_ag, shared_shrink
         self.nvls = nvls    # NvlsCollectives: RS(Y) and AG(dY) inside the NVSwitch
         self._rs = self._ag = None
 
@@ -547,7 +568,13 @@ class RowParallelMuxLinear:
             self.nvls.release(("ag", id(self)))
         else:
             dY = all_gather_rows(dy_rows, self.group)
-            dXp, dA, dB = self.be.bwd(seg_off, seg_task, self.ads, dY, self.X, self.W, self.Hs, self.r_cap)
+            Gs = None
+            if self.shared_shrink:
+                rows_p = dy_rows.shape[0]
+                r0 = rows_p * _world(self.group)[1]
+                Gs_own = self.be.shrink_bwd(seg_off, seg_task, self.ads, dY, self.W, self.r_cap, r0, r0 + rows_p)
+                Gs = all_gather_rows(Gs_own[r0:r0 + rows_p].contiguous(), self.group)
+            dXp, dA, dB = self.be.bwd(seg_off, seg_task, self.ads, dY, self.X, self.W, self.Hs, self.r_cap, Gs=Gs)
         for g in dB:
             if g is not None:
                 all_reduce_(g, self.group)

@@ -92,14 +92,14 @@ class TPDecoderBlock:
         """nvls: a tp.NvlsCollectives — every all-gather / reduce-scatter of the block inside the
         NVSwitch (NVLink SHARP) instead of NCCL.  col_off: the weights/adapters of shard_block_fused
         (q|k|v and gate|up as one column-sliced GEMM each).  shared_shrink: column layers shrink only
-        this rank's rows and all-gather Hs (tp.ColumnParallelMuxLinear)."""
+        this rank's rows and all-gather Hs, row layers likewise for Gs in the backward (tp.py)."""
         self.be, self.s, self.w, self.r_cap, self.group, self.nvls = backend, shape, weights, r_cap, group, nvls
         self.fused = col_off is not None
         self.lin = {}
         for name in (FUSED_LINEARS if self.fused else LINEARS):
             if name in ROW:
                 self.lin[name] = tp.RowParallelMuxLinear(backend, weights[name], adapters[name], r_cap, group=group,
-                                                         nvls=nvls)
+                                                         nvls=nvls, shared_shrink=shared_shrink)
             else:
                 self.lin[name] = tp.ColumnParallelMuxLinear(backend, weights[name], adapters[name], r_cap,
                                                             group=group, shared_shrink=shared_shrink,

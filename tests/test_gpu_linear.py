@@ -282,3 +282,33 @@ def test_more_row_blocks_than_the_group_table():
     p = Problem(128, 128, segs, ranks, variant="int", seg_task=[s % 16 for s in range(64)], seed=31)
     assert p.R > 128 * 256
     _run(p, exact=True)
+
+
+def test_shrink_bwd_and_bwd_with_given_gs_bit_identical():
+    """MUX_OP_SHRINK_BWD over the whole range, fed back as the given Gs of the backward (no shrink tiles;
+    the row-parallel shared-shrink path, tp.py), reproduces mux_linear_bwd's dX, dA and dB bit for bit;
+    over a 256-row sub-range it writes exactly those rows."""
+    from paper_2603_02885_b200 import mux
+    from gpu_harness import to_dev_bf16
+    p = Problem(320, 640, [192, 64, 256, 128, 128], [16, 4, 64, 8, 0], seg_task=[0, 1, 2, 3, 4], seed=93,
+                r_cap=64, max_rows=1024)
+    seg_off = torch.from_numpy(p.seg_off).cuda()
+    X, W, dY = to_dev_bf16(p.X), to_dev_bf16(p.W), to_dev_bf16(p.dY)
+    ads = p.gpu_adapters()
+    _, Hs = mux.linear_fwd(seg_off, p.seg_task, ads, X, W, p.r_cap)
+    dX = mux.linear_bwd(seg_off, p.seg_task, ads, dY, X, W, Hs, p.r_cap)
+    ref = {"dX": dX.clone(), "dA": [None if a.dA is None else a.dA.clone() for a in ads],
+           "dB": [None if a.dB is None else a.dB.clone() for a in ads]}
+    Gs = mux.linear_shrink_bwd(seg_off, p.seg_task, ads, dY, p.K, p.r_cap)
+    dX2 = mux.linear_bwd_gs(seg_off, p.seg_task, ads, dY, X, W, Hs, Gs, p.r_cap)
+    torch.cuda.synchronize()
+    R = p.R
+    assert torch.equal(dX2[:R].view(torch.int16), ref["dX"][:R].view(torch.int16))
+    for t, a in enumerate(ads):
+        if a.rank:
+            assert torch.equal(a.dA, ref["dA"][t]) and torch.equal(a.dB, ref["dB"][t]), t
+    part = torch.full((p.max_rows, p.r_cap), float("nan"), device="cuda").bfloat16()
+    mux.linear_shrink_bwd(seg_off, p.seg_task, ads, dY, p.K, p.r_cap, 256, 512, Gs=part)
+    torch.cuda.synchronize()
+    assert torch.equal(part[256:512].view(torch.int16), Gs[256:512].view(torch.int16))
+    assert torch.isnan(torch.cat([part[:256], part[512:]]).float()).all()

@@ -137,10 +137,12 @@ def _free_port():
 
 
 @pytest.mark.parametrize("world,fused,shared_shrink", [(2, False, False), (4, False, False), (8, False, False),
-                                                       (2, True, False), (4, True, True), (8, True, False)])
+                                                       (2, True, False), (4, True, True), (8, True, False),
+                                                       (8, False, True)])
 def test_tp_block_matches_single_process(world, fused, shared_shrink):
     """fused: q|k|v and gate|up as one column-sliced linear each; shared_shrink: column layers shrink
-    their own rows and all-gather Hs (rows they do not own are NaN in the oracle backend's shrink).
+    their own rows and all-gather Hs, row layers likewise Gs in the backward (rows they do not own are
+    NaN in the oracle backend's shrinks).
     Both must equal the unfused single-process composition."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()

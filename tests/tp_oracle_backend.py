@@ -52,10 +52,30 @@ class OracleBackend:
                                                             @ a.B.numpy().T)
         return torch.from_numpy(Y)
 
-    def bwd(self, seg_off, seg_task, ads, dY, X, W, Hs, r_cap, dX=None, col_off=None):
+    def shrink_bwd(self, seg_off, seg_task, ads, dY, W, r_cap, row_begin, row_end, col_off=None):
+        # Gs = s dY B_t of the oracle; rows outside the range are NaN: only the all-gathered own rows may
+        # reach the backward
+        A, B, rk, sc = self._tabs(ads, col_off)
+        N = W.shape[0]
+        K = W.shape[1]
+        dYn = np.ascontiguousarray(dY.numpy())
+        Xz = np.zeros((dYn.shape[0], K))
+        if col_off is None:
+            _, Gs, _ = olin.linear_bwd(seg_off.numpy(), seg_task, A, B, rk, sc, dYn, Xz, W.numpy(), r_cap)
+        else:
+            _, Gs, _ = olin.linear_bwd_sliced(seg_off.numpy(), seg_task, col_off, A, B, rk, sc, dYn, Xz, W.numpy(),
+                                              r_cap)
+        Gs = torch.from_numpy(Gs.copy())
+        Gs[:row_begin] = float("nan")
+        Gs[row_end:] = float("nan")
+        return Gs
+
+    def bwd(self, seg_off, seg_task, ads, dY, X, W, Hs, r_cap, dX=None, col_off=None, Gs=None):
         # the oracle recomputes H from X (fp64), which equals the saved Hs / s
         A, B, rk, sc = self._tabs(ads, col_off)
         dYn = np.ascontiguousarray(dY.numpy())
+        if Gs is not None:   # the given (gathered) Gs: dX = dY W + Gs A_t, dA_t = Gs^T X on each segment
+            return self._bwd_gs(seg_off, seg_task, ads, dYn, X, W, Gs, r_cap, dX, col_off, A, B, rk, sc)
         if col_off is None:
             dXn, Gs, grads = olin.linear_bwd(seg_off.numpy(), seg_task, A, B, rk, sc, dYn, X.numpy(), W.numpy(),
                                              r_cap)
@@ -64,6 +84,38 @@ class OracleBackend:
             dXn, Gs, grads = olin.linear_bwd_sliced(seg_off.numpy(), seg_task, col_off, A, B, rk, sc, dYn,
                                                     X.numpy(), W.numpy(), r_cap)
             dA = [[torch.from_numpy(g[0]) for g in row] for row in grads]
+            dB = [[torch.from_numpy(g[1]) for g in row] for row in grads]
+        out = torch.from_numpy(dXn)
+        if dX is not None:
+            dX.copy_(out)
+            out = dX
+        return out, dA, dB
+
+    def _bwd_gs(self, seg_off, seg_task, ads, dYn, X, W, Gs, r_cap, dX, col_off, A, B, rk, sc):
+        # dB_t (needs H, not Gs) from the oracle; dX and dA_t from the given Gs
+        if col_off is None:
+            _, _, grads = olin.linear_bwd(seg_off.numpy(), seg_task, A, B, rk, sc, dYn, X.numpy(), W.numpy(), r_cap)
+            rows_ads = [[a] for a in ads]
+        else:
+            _, _, grads = olin.linear_bwd_sliced(seg_off.numpy(), seg_task, col_off, A, B, rk, sc, dYn, X.numpy(),
+                                                 W.numpy(), r_cap)
+            rows_ads = ads
+        so, Gn, Xn = seg_off.numpy(), Gs.numpy(), X.numpy()
+        dXn = dYn @ W.numpy()
+        dAs = [[np.zeros_like(np.asarray(a.A.numpy(), dtype=np.float64)) if a.rank else None for a in row]
+               for row in rows_ads]
+        for s_, t in enumerate(seg_task):
+            lo, hi = so[s_], so[s_ + 1]
+            for c, a in enumerate(rows_ads[t]):
+                if a.rank:
+                    g = Gn[lo:hi, c * r_cap:c * r_cap + a.rank]
+                    dXn[lo:hi] += g @ a.A.numpy()
+                    dAs[t][c] += g.T @ Xn[lo:hi]
+        if col_off is None:
+            dA = [torch.from_numpy(row[0]) if row[0] is not None else None for row in dAs]
+            dB = [torch.from_numpy(g[1]) for g in grads]
+        else:
+            dA = [[torch.from_numpy(x) if x is not None else None for x in row] for row in dAs]
             dB = [[torch.from_numpy(g[1]) for g in row] for row in grads]
         out = torch.from_numpy(dXn)
         if dX is not None:
@@ -90,6 +142,9 @@ class OracleOps:
 
     def fwd_hs(self, *a, **kw):
         return self.lin.fwd_hs(*a, **kw)
+
+    def shrink_bwd(self, *a, **kw):
+        return self.lin.shrink_bwd(*a, **kw)
 
     def rmsnorm_fwd(self, x, w, eps, res=None):
         if res is None:

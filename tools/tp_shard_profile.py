@@ -99,6 +99,7 @@ def block_at(mux, wl, p, shared_shrink=False, fused=False):
         dY = torch.randn(R, N, device="cuda", generator=gen).bfloat16()
         Y = torch.empty(R, N, dtype=torch.bfloat16, device="cuda")
         Hs = torch.empty(R, S * r_cap, dtype=torch.bfloat16, device="cuda")
+        Gs = torch.empty(R, S * r_cap, dtype=torch.bfloat16, device="cuda")
         dX = torch.empty(R, K, dtype=torch.bfloat16, device="cuda")
         ws = torch.zeros(mux.linear_workspace_size(M, R, K, N, S * r_cap), dtype=torch.uint8, device="cuda")
         flat = [row[0] for row in ads]
@@ -125,7 +126,13 @@ def block_at(mux, wl, p, shared_shrink=False, fused=False):
                 mux.linear_fwd_hs(seg_off, st, flat, X, W, Hs, r_cap, Y=Y, workspace=ws)
             else:
                 mux.linear_fwd(seg_off, st, flat, X, W, r_cap, Y=Y, Hs=Hs, workspace=ws)
-            mux.linear_bwd(seg_off, st, flat, dY, X, W, Hs, r_cap, dX=dX, workspace=ws)
+            if shared_shrink and not col:
+                # row-parallel backward: own rows' Gs (MUX_OP_SHRINK_BWD), (Gs all-gather, not run), then
+                # the dX GEMM and gradients with Gs given
+                mux.linear_shrink_bwd(seg_off, st, flat, dY, K, r_cap, 0, hi, Gs=Gs, workspace=ws)
+                mux.linear_bwd_gs(seg_off, st, flat, dY, X, W, Hs, Gs, r_cap, dX=dX, workspace=ws)
+            else:
+                mux.linear_bwd(seg_off, st, flat, dY, X, W, Hs, r_cap, dX=dX, workspace=ws)
 
         ms = time_graph(step)
         f = sum(seg * (4 * K * w + 6 * r * (K + w)) for r in wl.ranks for w in widths)  # SURVEY §8(d) per token
@@ -133,7 +140,7 @@ def block_at(mux, wl, p, shared_shrink=False, fused=False):
                     "tflops": round(f / ms / 1e9, 1)})
         total_ms += ms
         flops += f
-        del W, ads, flat, X, dY, Y, Hs, dX, ws
+        del W, ads, flat, X, dY, Y, Hs, Gs, dX, ws
         torch.cuda.empty_cache()
     H = wl.linears[0].K
     comm_bytes = 8 * (p - 1) / p * R * H * 2
@@ -148,7 +155,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
     ap.add_argument("--points", default="4:1,4:2,4:4,4:8,5:1,5:8")
-    ap.add_argument("--shared-shrink", action="store_true", help="column layers: own-rows shrink + fwd_hs")
+    ap.add_argument("--shared-shrink", action="store_true",
+                    help="column layers: own-rows shrink + fwd_hs; row layers: own-rows Gs + bwd with Gs given")
     ap.add_argument("--fused", action="store_true", help="q|k|v and gate|up as one column-sliced call each")
     a = ap.parse_args()
     from paper_2603_02885_b200 import mux
