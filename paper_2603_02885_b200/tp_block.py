@@ -88,18 +88,19 @@ class TPDecoderBlock:
 
     def __init__(self, backend, shape: TPBlockShape, weights: Dict[str, torch.Tensor],
                  adapters: Dict[str, List], r_cap: int, group=None, nvls=None, col_off=None,
-                 shared_shrink=False):
+                 shared_shrink=False, shared_gs=False):
         """nvls: a tp.NvlsCollectives — every all-gather / reduce-scatter of the block inside the
         NVSwitch (NVLink SHARP) instead of NCCL.  col_off: the weights/adapters of shard_block_fused
         (q|k|v and gate|up as one column-sliced GEMM each).  shared_shrink: column layers shrink only
-        this rank's rows and all-gather Hs, row layers likewise for Gs in the backward (tp.py)."""
+        this rank's rows and all-gather Hs (tp.py).  shared_gs: row layers do the same for Gs in the
+        backward (built and parity-tested; no gain measured, profiles/r02_shared_gs_ab.jsonl)."""
         self.be, self.s, self.w, self.r_cap, self.group, self.nvls = backend, shape, weights, r_cap, group, nvls
         self.fused = col_off is not None
         self.lin = {}
         for name in (FUSED_LINEARS if self.fused else LINEARS):
             if name in ROW:
                 self.lin[name] = tp.RowParallelMuxLinear(backend, weights[name], adapters[name], r_cap, group=group,
-                                                         nvls=nvls, shared_shrink=shared_shrink)
+                                                         nvls=nvls, shared_shrink=shared_gs)
             else:
                 self.lin[name] = tp.ColumnParallelMuxLinear(backend, weights[name], adapters[name], r_cap,
                                                             group=group, shared_shrink=shared_shrink,

@@ -117,7 +117,7 @@ def _worker(rank, world, port, q, fused=False, shared_shrink=False):
             Wp, ap = tp_block.shard_block(full_w, full_a, world, rank, mk)
         shape = tp_block.TPBlockShape(eps=EPS, p=world, **sh)
         blk = tp_block.TPDecoderBlock(OracleOps(sh["head_dim"]), shape, Wp, ap, 16, col_off=col_off,
-                                      shared_shrink=shared_shrink)
+                                      shared_shrink=shared_shrink, shared_gs=shared_shrink)
         rows = X.shape[0] // world
         sl = slice(rank * rows, (rank + 1) * rows)
         y = blk.forward(T(X[sl]).contiguous(), T(seg_off), [0, 1, 2], T(rs))
