@@ -38,9 +38,10 @@ import synth  # noqa: E402
 # fused projections (q|k|v, gate|up as one column-sliced GEMM): the interleaved GEMM A/B in
 # profiles/r02_fused_ab_v2.jsonl has the fused call at 0.68-0.99x the time of the separate calls (the
 # gain grows as the shards narrow: 0.69 for TP-8 q|k|v dX); whole steps at full width are a wash
-# (profiles/r02_bench_{tp4,block4}_ab.jsonl: TP arm at world 1 +0.5 %, the one-GPU block -1.8 %, the
-# attention and SwiGLU then read strided column views).  So auto fuses where a shard is narrower than
-# the full 4096-wide 7B projections (every TP > 1 shard, and config 5's 1024-wide k/v)
+# (profiles/r02_bench_{tp4,block4}_ab.jsonl: TP arm at world 1 +0.5 %, the one-GPU block -1.8 %: its
+# fused gate|up dX reduces over 22016 columns, and a row band of that A re-streams W twice as often as
+# two 11008-deep dX GEMMs do, profiles/r02_block_launches_{fused,unfused}.md).  So auto fuses where a
+# shard is narrower than the full 4096-wide 7B projections (every TP > 1 shard, config 5's k/v)
 FUSE_BELOW_COLS = 4096
 METRIC = "multiplexed tokens/s fwd+bwd at 1/2/4/8 B200; % of BF16 tensor-core peak"
 UNIT = "tokens/s"
