@@ -683,9 +683,12 @@ def _packed_rows_once(torch, mux, task_off, lens, cap):
 
 
 def _tp_chain(args, w, torch, mux, tp, orchestrate, Backend, world, rank):
-    """Config-2-style layer stack (3 linears) tensor-parallel: L0 column (AG of the row-sharded
-    input), L1 row (RS of its output), L2 column; backward mirrors it.  `--htasks g` splits the tasks
-    into g hTasks interleaved by Alg. 1 (orchestrate.py, NEXT-1)."""
+    """Config-2-style layer stack (3 linears) tensor-parallel.  `--chain rcr` (default, Megatron's
+    pairing for o / up / down): L0 row-parallel on the column shard of the input, RS of its output,
+    AG into L1 column-parallel, L2 row-parallel on L1's column-sharded output (no collective), RS;
+    every collective is K wide (4096), none crosses the 11008-wide intermediate.  `--chain crc`: L0
+    column (AG of the row-sharded input), L1 row (RS), L2 column.  Backward mirrors either.
+    `--htasks g` splits the tasks into g hTasks interleaved by Alg. 1 (orchestrate.py, NEXT-1)."""
     plan_note = None
     if args.htasks < 0:
         args.htasks = 2 if world > 1 else 1
@@ -701,7 +704,8 @@ def _tp_chain(args, w, torch, mux, tp, orchestrate, Backend, world, rank):
         g = max(1, min(args.htasks, w.M))
         groups = [list(range(w.M))[i * w.M // g:(i + 1) * w.M // g] for i in range(g)]
     r_cap = 16 * -(-max(w.wl.ranks) // 16)
-    kinds = ["col", "row", "col"][:len(w.linears)]
+    kinds = (["row", "col", "row"] if args.chain == "rcr" else ["col", "row", "col"])[:len(w.linears)]
+    first_row, last_row = kinds[0] == "row", kinds[-1] == "row"
     mk = lambda A, B, r, sc: mux.Adapter(A, B, r, sc)  # noqa: E731
     seed = w.wl.seed
     Wsh = []
@@ -721,11 +725,13 @@ def _tp_chain(args, w, torch, mux, tp, orchestrate, Backend, world, rank):
         # every rank owns an equal contiguous row block (sequence parallel); rows are sized once at
         # setup on this workload's packed row count (the step's lengths are fixed, so every step packs
         # the same rows; the timed loop never reads device data on the host)
-        packed = _packed_rows_once(torch, mux, off, np.concatenate(lens), None)
+        cap_h = [w.cap[t] for t in tasks] if w.cap else None
+        packed = _packed_rows_once(torch, mux, off, np.concatenate(lens), cap_h)
         max_rows = -(-packed // (blk * world)) * blk * world
         pk = mux.alloc_pack_outputs(len(tasks), S_h, max_rows, max_rows // 64)
         be = Backend()
         be.task_tokens = [w.task_tokens[t] for t in tasks]
+        be.pack_info = pk["info"]     # checked after the warm-up (no overflow: every row computed)
         layers = []
         for li, L in enumerate(w.linears):
             ads = []
@@ -740,26 +746,40 @@ def _tp_chain(args, w, torch, mux, tp, orchestrate, Backend, world, rank):
             cls = tp.ColumnParallelMuxLinear if kinds[li] == "col" else tp.RowParallelMuxLinear
             layers.append(cls(be, Wsh[li], ap_, r_cap, fused_rs=args.fused_rs, fused_ag=args.fused_ag))
         rows = max_rows // world
-        # token-major inputs: every rank holds the full buffer; its data loader moves its 1/p share
+        lo, hi_ = rank * T_h // world, (rank + 1) * T_h // world
+        # token-major inputs.  Column-parallel first layer: every rank holds the full buffer and its
+        # data loader moves its 1/p token share (Dispatch gathers this rank's packed row block);
+        # row-parallel first layer: the rank's column shard of every token (Dispatch packs all rows)
         Xtok = _gen(torch, seed * 7 + hi, (T_h, K0), 1.0)
-        # loss gradient of the last (column-parallel) layer: this rank's output-column shard
-        dYtok = _gen(torch, seed * 11 + hi, (T_h, Nl), 1.0)[:, rank * (Nl // world):(rank + 1) * (Nl // world)]
-        dYtok = dYtok.contiguous()
+        if first_row:
+            Xtok = Xtok[:, rank * (K0 // world):(rank + 1) * (K0 // world)].contiguous()
+        # loss gradient in the last layer's output layout: column-parallel -> this rank's column
+        # shard of all rows [R, N/p]; row-parallel -> this rank's row block of full rows [R/p, N]
+        dYtok = _gen(torch, seed * 11 + hi, (T_h, Nl), 1.0)
+        if not last_row:
+            dYtok = dYtok[:, rank * (Nl // world):(rank + 1) * (Nl // world)].contiguous()
+        x_shape = (max_rows, K0 // world) if first_row else (rows, K0)
+        dy_shape = (rows, Nl) if last_row else (max_rows, Nl // world)
         ht = {"tasks": tasks, "T": T_h, "max_rows": max_rows, "rows": rows, "pk": pk, "layers": layers,
               "tso": torch.tensor(off, **i32), "sl": torch.tensor(np.concatenate(lens).astype(np.int32), **i32),
               "cap": torch.tensor([w.cap[t] for t in tasks], **i32) if w.cap else None, "Xtok": Xtok,
-              "x_rows": torch.empty(rows, K0, dtype=torch.bfloat16, device="cuda"),
-              "dYtok": dYtok, "dY": torch.empty(max_rows, Nl // world, dtype=torch.bfloat16, device="cuda")}
-        lo, hi_ = rank * T_h // world, (rank + 1) * T_h // world
-        h2d += [ht["tso"], ht["sl"], Xtok[lo:hi_], dYtok]
+              "x_rows": torch.empty(*x_shape, dtype=torch.bfloat16, device="cuda"),
+              "dYtok": dYtok, "dY": torch.empty(*dy_shape, dtype=torch.bfloat16, device="cuda")}
+        # host->device bytes per step: this rank's 1/p share of each token-major input
+        h2d += [ht["tso"], ht["sl"], Xtok if first_row else Xtok[lo:hi_], dYtok[lo:hi_] if last_row else dYtok]
 
         def dispatch(e, ht=ht):
             mux.pack_chunks(ht["tso"], ht["sl"], ht["cap"], 0, 64, max_rows=ht["max_rows"],
                             max_chunks=ht["max_rows"] // 64, out=ht["pk"])
-            mux.pack_apply(ht["pk"]["row_src"][rank * ht["rows"]:(rank + 1) * ht["rows"]], ht["Xtok"],
-                           ht["rows"], out=ht["x_rows"])
-            # the loss gradient in the last layer's layout [R, N/p] (Dispatch of its token-major shard)
-            mux.pack_apply(ht["pk"]["row_src"], ht["dYtok"], ht["max_rows"], out=ht["dY"])
+            mine = ht["pk"]["row_src"][rank * ht["rows"]:(rank + 1) * ht["rows"]]
+            if first_row:
+                mux.pack_apply(ht["pk"]["row_src"], ht["Xtok"], ht["max_rows"], out=ht["x_rows"])
+            else:
+                mux.pack_apply(mine, ht["Xtok"], ht["rows"], out=ht["x_rows"])
+            if last_row:
+                mux.pack_apply(mine, ht["dYtok"], ht["rows"], out=ht["dY"])
+            else:
+                mux.pack_apply(ht["pk"]["row_src"], ht["dYtok"], ht["max_rows"], out=ht["dY"])
             return ht["x_rows"]
         lat = [2.0 * max_rows * L.K * L.N / world for L in w.linears]
         ht["ops"] = orchestrate.linear_chain_ops(layers, kinds, ht["pk"]["seg_off"], list(range(len(tasks))),
@@ -786,7 +806,9 @@ def _tp_chain(args, w, torch, mux, tp, orchestrate, Backend, world, rank):
                         out.append(a.dA if col else a.dB)
         return out
 
-    desc = {"parallelism": f"tp{world} (L0 column, L1 row, L2 column; sequence-parallel AG/RS)",
+    names = {"col": "column", "row": "row"}
+    desc = {"parallelism": f"tp{world} (" + ", ".join(f"L{i} {names[k]}" for i, k in enumerate(kinds))
+            + "; sequence-parallel AG/RS)",
             "htasks": [ht["tasks"] for ht in htasks], "schedule": [f"h{sg.htask}.{sg.index}" for sg, _ in schedule],
             "planner": plan_note, "max_rows": [ht["max_rows"] for ht in htasks],
             "reduce_scatter": "fused into the GEMM epilogue (peer stores)" if args.fused_rs else "NCCL",
@@ -898,6 +920,7 @@ def _tp_block(args, w, torch, mux, tp, Backend, world, rank):
             "attention_flops": attn_flops}
     lf, lb = blk.launches()
     launches = 4 + lf + lb + (2 if args.shared_shrink else 0)
+    be.pack_info = pk["info"]
     return step, launches, h2d, result_tensors, desc, [be]
 
 
@@ -928,6 +951,11 @@ def tp_arm(args):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    for be in bes:   # setup check outside the timed region: the step's pack fits its buffers
+        if getattr(be, "pack_info", None) is not None:
+            info = mux.read_info(be.pack_info)
+            if info["overflow"]:
+                raise RuntimeError(f"bench: the TP step's pack overflowed its buffers: {info}")
     rec = []
     for be in bes:
         be.record = rec
@@ -1246,6 +1274,9 @@ def main():
                     help="--mode tp, config 2: hTasks interleaved by Alg. 1 (NEXT-1) so one hTask's collectives "
                          "overlap another's GEMMs; 0 = chosen by the planner (NEXT-4); -1 (default) = 2 for N > 1 "
                          "(at N = 1 the collectives are local copies: 1)")
+    ap.add_argument("--chain", default="rcr", choices=("rcr", "crc"),
+                    help="--mode tp, config 2: layer kinds of the 3-linear chain; rcr (default) = row, column, row "
+                         "(collectives 4096 wide), crc = column, row, column (RS/AG of the 11008-wide intermediate)")
     ap.add_argument("--comm-ctas", type=int, default=0, help="--mode tp: NCCL_MAX_CTAS for the overlapped collectives")
     ap.add_argument("--fused-proj", type=int, default=-1, choices=(-1, 0, 1),
                     help="--mode tp / block, configs 4/5: q|k|v and gate|up as one column-sliced GEMM each (1), "

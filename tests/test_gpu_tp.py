@@ -77,14 +77,17 @@ def test_tp_world1_equals_direct(pg, shared_shrink):
             assert torch.equal(_bits(a_), _bits(b_))
 
 
-def test_orchestrated_htasks_world1_equals_direct(pg):
-    """Two hTasks through a column/row/column chain, interleaved by Alg. 1 with
-    asynchronous NCCL collectives (orchestrate.py, NEXT-1), equal each hTask
-    run through the binding directly, bit for bit."""
+@pytest.mark.parametrize("chain", ["crc", "rcr"])
+def test_orchestrated_htasks_world1_equals_direct(pg, chain):
+    """Two hTasks through a column/row/column (crc) or row/column/row (rcr, the bench's config-2
+    chain) layer chain, interleaved by Alg. 1 with asynchronous NCCL collectives (orchestrate.py,
+    NEXT-1), equal each hTask run through the binding directly, bit for bit."""
     g = torch.Generator(device="cuda").manual_seed(11)
     K, N = 256, 512
-    shapes = [(N, K), (K, N), (N, K)]
-    kinds = ["col", "row", "col"]
+    if chain == "crc":
+        shapes, kinds = [(N, K), (K, N), (N, K)], ["col", "row", "col"]
+    else:
+        shapes, kinds = [(K, K), (N, K), (K, N)], ["row", "col", "row"]
     mk = lambda A, B, r, s: mux.Adapter(A, B, r, s)  # noqa: E731
     Ws = [(torch.randn(n, k, device="cuda", generator=g) / k ** 0.5).bfloat16() for n, k in shapes]
     cfgs = [([0, 256, 448], [16, 8]), ([0, 128, 192, 640], [4, 32, 16])]
@@ -102,7 +105,7 @@ def test_orchestrated_htasks_world1_equals_direct(pg):
             ads_all.append(ads)
         R = so_l[-1]
         X = torch.randn(R, K, device="cuda", generator=g).bfloat16()
-        dY = torch.randn(R, N, device="cuda", generator=g).bfloat16()
+        dY = torch.randn(R, shapes[-1][0], device="cuda", generator=g).bfloat16()
         be = tp.MuxBackend()
         lays = []
         for li, kind in enumerate(kinds):

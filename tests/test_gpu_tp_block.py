@@ -119,10 +119,13 @@ def _bench(args, timeout=900):
     return json.loads(lines[0])
 
 
-@pytest.mark.parametrize("config", ["2", "4"])
+@pytest.mark.parametrize("config", ["2", "2crc", "4"])
 def test_bench_gpus2_runs_tp(config):
-    line = _bench(["--gpus", "2", "--steps", "2", "--warmup", "3", "--config", config, "--no-replicas"])
+    extra = ["--chain", "crc"] if config == "2crc" else []
+    line = _bench(["--gpus", "2", "--steps", "2", "--warmup", "3", "--config", config[0], "--no-replicas"] + extra)
     assert line["n_gpus"] == 2 and line["mode"] == "tp" and line["scaling"] == "strong"
     assert line["value"] > 0 and line["e2e"]["value"] > 0
     assert line["roofline"]["achieved"] > 0 and line["gpu_launches"] > 0
+    # a physically possible rate: every packed row computed (a pack overflow would skip rows)
+    assert line["roofline"]["frac_of_burst"] < 1.05 and line["frac_of_peak_per_gpu"]["measured_burst"] < 1.05
     assert line["config"]["dist_backend"] == "gloo"

@@ -114,31 +114,35 @@ HTASKS = [
 ]
 
 
-def _htask_problem(h):
+CHAINS = {"crc": ["col", "row", "col"],   # K0 -> N0 -> K0 -> N0
+          "rcr": ["row", "col", "row"]}   # K0 -> K0 -> N0 -> K0 (Megatron's o / up / down pairing)
+
+
+def _htask_problem(h, chain="crc"):
     cfg = HTASKS[h]
     rng = np.random.default_rng(1000 + h)
     R = sum(cfg["seg"])
     seg_off = np.concatenate([[0], np.cumsum(cfg["seg"])]).astype(np.int32)
     X = rng.standard_normal((R, K0))
-    shapes = [(N0, K0), (K0, N0), (N0, K0)]
+    shapes = [(N0, K0), (K0, N0), (N0, K0)] if chain == "crc" else [(K0, K0), (N0, K0), (K0, N0)]
     Ws = [rng.standard_normal(s) / np.sqrt(s[1]) for s in shapes]
     As = [[rng.standard_normal((r, s[1])) for r in cfg["ranks"]] for s in shapes]
     Bs = [[rng.standard_normal((s[0], r)) for r in cfg["ranks"]] for s in shapes]
-    dY = rng.standard_normal((R, N0))
+    dY = rng.standard_normal((R, shapes[-1][0]))
     return seg_off, X, Ws, As, Bs, dY
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, chain="crc"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_2603_02885_b200 import tp
         from test_tp_gloo import OracleBackend
         T = torch.from_numpy
-        kinds = ["col", "row", "col"]
+        kinds = CHAINS[chain]
 
         def make_layers(h):
-            seg_off, X, Ws, As, Bs, dY = _htask_problem(h)
+            seg_off, X, Ws, As, Bs, dY = _htask_problem(h, chain)
             cfg = HTASKS[h]
             be = OracleBackend()
             lays = []
@@ -150,9 +154,14 @@ def _worker(rank, world, port, q):
                 lays.append((tp.ColumnParallelMuxLinear if kind == "col" else tp.RowParallelMuxLinear)(be, Wp, ap, 16))
             R = X.shape[0]
             rows = R // world
-            nl = N0 // world
-            x_rows = T(X[rank * rows:(rank + 1) * rows]).contiguous()
-            dy = T(dY[:, rank * nl:(rank + 1) * nl]).contiguous()
+            if chain == "crc":     # row block of X in; loss gradient of the column output: N shard
+                nl = dY.shape[1] // world
+                x_rows = T(X[rank * rows:(rank + 1) * rows]).contiguous()
+                dy = T(dY[:, rank * nl:(rank + 1) * nl]).contiguous()
+            else:                  # column shard of X in (all rows); row-parallel output: row block
+                kl = X.shape[1] // world
+                x_rows = T(X[:, rank * kl:(rank + 1) * kl]).contiguous()
+                dy = T(dY[rank * rows:(rank + 1) * rows]).contiguous()
             return T(seg_off), list(range(len(cfg["ranks"]))), lays, x_rows, dy
 
         # orchestrated: both hTasks interleaved by Alg. 1
@@ -236,6 +245,55 @@ def test_two_htasks_orchestrated_tp_world2():
                                        rtol=1e-10, atol=1e-10)
             np.testing.assert_allclose(res[0][3][h][3][1][t], g1[t][1], rtol=1e-10, atol=1e-10)
         # orchestrated == sequential tp.py layer classes, bit for bit
+        for r in res:
+            got, seq = r[3][h], r[4][h]
+            assert np.array_equal(got[0], seq[0]) and np.array_equal(got[1], seq[1])
+            for i in range(3):
+                for t in range(len(st)):
+                    assert np.array_equal(got[2][i][t], seq[2][i][t]) and np.array_equal(got[3][i][t], seq[3][i][t])
+
+
+def test_two_htasks_orchestrated_tp_world2_row_col_row():
+    """The bench's config-2 chain pairing [row, col, row] (every collective is K0 wide: the row-parallel
+    L0 takes the column shard of X, the row-parallel L2 takes L1's column-sharded output with no
+    collective): orchestrated == the sequential tp.py layer classes bit for bit, and == the fp64
+    single-device oracle chain."""
+    from oracle import linear as olin
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, "rcr")) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=240) for _ in range(world)], key=lambda x: x[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for h in range(len(HTASKS)):
+        cfg = HTASKS[h]
+        seg_off, X, Ws, As, Bs, dY = _htask_problem(h, "rcr")
+        st = list(range(len(cfg["ranks"])))
+        args = lambda li: (As[li], Bs[li], cfg["ranks"], cfg["scales"])  # noqa: E731
+        H0, _ = olin.linear_fwd(seg_off, st, *args(0), X, Ws[0], 16)
+        H1, _ = olin.linear_fwd(seg_off, st, *args(1), H0, Ws[1], 16)
+        Y2, _ = olin.linear_fwd(seg_off, st, *args(2), H1, Ws[2], 16)
+        dH1, _, g2 = olin.linear_bwd(seg_off, st, *args(2), dY, H1, Ws[2], 16)
+        dH0, _, g1 = olin.linear_bwd(seg_off, st, *args(1), dH1, H0, Ws[1], 16)
+        dX, _, g0 = olin.linear_bwd(seg_off, st, *args(0), dH0, X, Ws[0], 16)
+        y = np.concatenate([r[3][h][0] for r in res], axis=0)          # row-parallel output: row blocks
+        dx = np.concatenate([r[3][h][1] for r in res], axis=1)         # column shards of dX
+        np.testing.assert_allclose(y, Y2, rtol=1e-10, atol=1e-10)
+        np.testing.assert_allclose(dx, dX, rtol=1e-10, atol=1e-10)
+        for t in range(len(st)):
+            # layers 0 / 2 row: dA K-sharded, dB all-reduced; layer 1 column: dA all-reduced, dB N-sharded
+            for li, g in ((0, g0), (2, g2)):
+                np.testing.assert_allclose(np.concatenate([r[3][h][2][li][t] for r in res], axis=1), g[t][0],
+                                           rtol=1e-10, atol=1e-10)
+                np.testing.assert_allclose(res[0][3][h][3][li][t], g[t][1], rtol=1e-10, atol=1e-10)
+            np.testing.assert_allclose(res[0][3][h][2][1][t], g1[t][0], rtol=1e-10, atol=1e-10)
+            np.testing.assert_allclose(np.concatenate([r[3][h][3][1][t] for r in res]), g1[t][1],
+                                       rtol=1e-10, atol=1e-10)
         for r in res:
             got, seq = r[3][h], r[4][h]
             assert np.array_equal(got[0], seq[0]) and np.array_equal(got[1], seq[1])
