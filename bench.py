@@ -1069,6 +1069,10 @@ def _e2e_generic(torch, dist, stream, step, h2d_src, results, args, tokens):
     host = [pin(t) for t in h2d_src]
     slots = [[torch.empty_like(t) for t in h2d_src] for _ in range(2)]
     h_res = [torch.empty(g.shape, dtype=g.dtype, pin_memory=True) for g in results]
+    # the step rewrites its results in place: each step's results are staged on the device (one
+    # multi-tensor copy, two slots) and read back from the stage, so the next step need not wait for
+    # the read-back
+    stage = [[torch.empty_like(g) for g in results] for _ in range(2)]
     h2d = sum(x.numel() * x.element_size() for x in host)
     d2h = sum(g.numel() * g.element_size() for g in results)
     # the inputs alternate over two H2D streams by size (separate copy engines), the read-back has its own
@@ -1078,12 +1082,11 @@ def _e2e_generic(torch, dist, stream, step, h2d_src, results, args, tokens):
     lane_of = {k: j % 2 for j, k in enumerate(order)}
     copied = [[torch.cuda.Event() for _ in range(2)] for _ in range(2)]
     consumed = [torch.cuda.Event() for _ in range(2)]
-    done, read = torch.cuda.Event(), torch.cuda.Event()
+    done, read = torch.cuda.Event(), [torch.cuda.Event() for _ in range(2)]
 
     def run(n):
-        for ev in consumed:
+        for ev in consumed + read:
             ev.record(stream)
-        read.record(stream)
 
         def h2d_copy(i):
             for j, hs in enumerate(h2ds):
@@ -1102,14 +1105,16 @@ def _e2e_generic(torch, dist, stream, step, h2d_src, results, args, tokens):
             for d_, s_ in zip(h2d_src, slots[i % 2]):     # the step reads its inputs from their home
                 d_.copy_(s_, non_blocking=True)
             consumed[i % 2].record(stream)
-            stream.wait_event(read)                        # the previous read-back is done with the result
             step()
+            if results:
+                stream.wait_event(read[i % 2])             # stage slot free (read back two steps ago)
+                torch._foreach_copy_(stage[i % 2], results)
             done.record(stream)
             with torch.cuda.stream(cs):
                 cs.wait_event(done)
-                for g, hg in zip(results, h_res):
+                for g, hg in zip(stage[i % 2], h_res):
                     hg.copy_(g, non_blocking=True)
-                read.record(cs)
+                read[i % 2].record(cs)
 
     run(max(1, args.warmup))
     torch.cuda.synchronize()
@@ -1131,7 +1136,8 @@ def _e2e_generic(torch, dist, stream, step, h2d_src, results, args, tokens):
             "what": "per rank: pinned H2D of the sequence metadata and this rank's 1/p share of the token-major "
                     "input and loss gradient (a sharded data loader's bytes; prefetched one step ahead on two copy "
                     "streams, staged into the device buffers the step reads); D2H of this rank's adapter-gradient "
-                    "shards (replicated all-reduced gradients only on rank 0), overlapped with the next step"}
+                    "shards (replicated all-reduced gradients only on rank 0), staged on the device and read back "
+                    "overlapped with the next step"}
 
 
 def block_arm(args):

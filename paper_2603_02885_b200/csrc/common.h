@@ -107,7 +107,7 @@ static_assert(sizeof(GemmParams) <= 32764, "GemmParams exceeds the kernel parame
 // ---- segmented adapter gradients (dA_t, dB_t)
 constexpr int kGradBM = 128;     // output rows per unit (k for dA, n for dB)
 constexpr int kGradBK = 128;     // tokens per pipeline stage
-constexpr int kGradStages = 4;
+constexpr int kGradStages = 4;   // at most (fewer when a dA unit stages several Gs boxes: grad.cu)
 
 struct GradParams {
   CUtensorMap map_x;    // X  dims {K, rows} box {64, 128}
@@ -121,10 +121,25 @@ struct GradParams {
   int32_t units_a;                         // ceil(K/128) dA units per task (0 if no task wants dA)
   int32_t units_b;                         // ceil(N/128)
   uint64_t task_segs[MUX_MAX_ADAPTERS];    // bit s set: segment s belongs to the task
+  // CUDA-core kernel (grad_simt.cu): one launch per column slice, one slot per task
   int32_t task_rank[MUX_MAX_ADAPTERS];
   float* task_dA[MUX_MAX_ADAPTERS];
   float* task_dB[MUX_MAX_ADAPTERS];
+  // tcgen05 kernel (grad.cu): every column slice of a fused projection in one launch.  map_dy spans
+  // all N columns, map_hs / map_gs all S * r_cap side columns.  A dA unit (task, 128 k) stages nb_a
+  // 64-column Gs boxes and issues one MMA of N = 64 nb_a per 16 tokens (X read once for all slices);
+  // dB unit u of a task belongs to slice s with b_units_off[s] <= u < b_units_off[s + 1].
+  int32_t num_slices;
+  int32_t slice_off[MUX_MAX_SLICES + 1];
+  int32_t b_units_off[MUX_MAX_SLICES + 1];
+  int32_t nb_a;                            // ceil(S * r_cap / 64) <= 4
+  int32_t stages;                          // pipeline stages (stage_bytes each)
+  uint32_t stage_bytes;
+  int32_t slot_rank[MUX_MAX_ADAPTER_SLOTS];  // slot = (compacted task) * S + slice
+  float* slot_dA[MUX_MAX_ADAPTER_SLOTS];
+  float* slot_dB[MUX_MAX_ADAPTER_SLOTS];
 };
+static_assert(sizeof(GradParams) <= 32764, "GradParams exceeds the kernel parameter limit");
 
 // ---- causal attention forward on tcgen05 (attn_tc.cu)
 struct AttnTcParams {

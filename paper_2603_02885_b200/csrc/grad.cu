@@ -23,17 +23,17 @@ namespace mux {
 
 constexpr uint32_t kGAtom = kGradBK * 128;            // 128 token rows x 128 B = 16 KB
 constexpr uint32_t kGStageA = 2 * kGAtom;             // 128 output rows = 2 MN atoms
-constexpr uint32_t kGStageB = kGAtom;                 // 64 rank columns = 1 MN atom
-constexpr uint32_t kGStageBytes = kGStageA + kGStageB;  // 48 KB
-constexpr uint32_t kGradSmemBytes = kGradStages * kGStageBytes + 1024 + 1024;
-constexpr uint32_t kGradTmemCols = 128;
+constexpr uint32_t kGPipeBytes = kGradStages * (kGStageA + kGAtom);  // 192 KB of stages
+constexpr uint32_t kGradSmemBytes = kGPipeBytes + 1024 + 1024;
+constexpr uint32_t kGradTmemCols = 512;               // 2 accumulators of up to 256 columns
+constexpr uint32_t kGAccStride = 256;
 constexpr int kGradThreads = 256;
 
 __global__ void __launch_bounds__(kGradThreads, 1) mux_grad_kernel(const __grid_constant__ GradParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* pipe = smem;
-  uint8_t* misc = smem + kGradStages * kGStageBytes;
+  uint8_t* misc = smem + kGPipeBytes;
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(misc);
   uint64_t* empty_bar = full_bar + kGradStages;
   uint64_t* tfull_bar = empty_bar + kGradStages;
@@ -43,6 +43,8 @@ __global__ void __launch_bounds__(kGradThreads, 1) mux_grad_kernel(const __grid_
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const int stages = p.stages;
+  const uint32_t stage_bytes = p.stage_bytes;
   if (warp == 0 && lane == 0) {
     tma_prefetch(&p.map_x);
     tma_prefetch(&p.map_dy);
@@ -50,7 +52,7 @@ __global__ void __launch_bounds__(kGradThreads, 1) mux_grad_kernel(const __grid_
     tma_prefetch(&p.map_gs);
   }
   if (warp == 1 && lane == 0) {
-    for (int s = 0; s < kGradStages; ++s) {
+    for (int s = 0; s < stages; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
     }
@@ -71,6 +73,13 @@ __global__ void __launch_bounds__(kGradThreads, 1) mux_grad_kernel(const __grid_
 
   const int per_task = p.units_a + p.units_b;
   const int total_units = p.num_tasks * per_task;
+  const int S = p.num_slices;
+  // slice of dB unit `ub` (units of a task: dA first, then dB slice by slice)
+  auto b_slice = [&](int ub) {
+    int sc = 0;
+    while (sc + 1 < S && ub >= p.b_units_off[sc + 1]) ++sc;
+    return sc;
+  };
 
   if (warp == 0) {
     if (lane == 0) {
@@ -80,37 +89,52 @@ __global__ void __launch_bounds__(kGradThreads, 1) mux_grad_kernel(const __grid_
         const int task = u / per_task;
         const int sub = u - task * per_task;
         const bool is_a = sub < p.units_a;
-        const int m0 = (is_a ? sub : sub - p.units_a) * kGradBM;
+        // dA: rows k of X, all nb_a Gs boxes; dB: rows n of the slice's dY columns, its Hs box
+        int col_a, col_b = 0, nb = 1;
+        if (is_a) {
+          col_a = sub * kGradBM;
+          nb = p.nb_a;
+        } else {
+          const int ub = sub - p.units_a;
+          const int sc = b_slice(ub);
+          col_a = p.slice_off[sc] + (ub - p.b_units_off[sc]) * kGradBM;
+          col_b = sc * p.r_cap;
+        }
         const CUtensorMap* ma = is_a ? &p.map_x : &p.map_dy;
         const CUtensorMap* mb = is_a ? &p.map_gs : &p.map_hs;
+        const uint32_t bytes = kGStageA + static_cast<uint32_t>(nb) * kGAtom;
         const uint64_t segs = p.task_segs[task];
         for (int s = 0; s < p.num_segs; ++s) {
           if (!((segs >> s) & 1ull)) continue;
           for (int tok = so[s]; tok < so[s + 1]; tok += kGradBK) {
             mbar_wait(&empty_bar[stage], phase ^ 1u);
-            uint8_t* sa = pipe + stage * kGStageBytes;
-            mbar_arrive_expect_tx(&full_bar[stage], kGStageBytes);
-            tma_load_2d(ma, &full_bar[stage], sa, m0, tok);
-            tma_load_2d(ma, &full_bar[stage], sa + kGAtom, m0 + 64, tok);
-            tma_load_2d(mb, &full_bar[stage], sa + kGStageA, 0, tok);
-            if (++stage == kGradStages) { stage = 0; phase ^= 1u; }
+            uint8_t* sa = pipe + stage * stage_bytes;
+            mbar_arrive_expect_tx(&full_bar[stage], bytes);
+            tma_load_2d(ma, &full_bar[stage], sa, col_a, tok);
+            tma_load_2d(ma, &full_bar[stage], sa + kGAtom, col_a + 64, tok);
+            for (int b = 0; b < nb; ++b)
+              tma_load_2d(mb, &full_bar[stage], sa + kGStageA + b * kGAtom, is_a ? 64 * b : col_b, tok);
+            if (++stage == stages) { stage = 0; phase ^= 1u; }
           }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t kIdesc = idesc_bf16(kGradBM, 64, true, true);
+      const uint32_t idesc_a = idesc_bf16(kGradBM, 64 * p.nb_a, true, true);
+      constexpr uint32_t kIdescB = idesc_bf16(kGradBM, 64, true, true);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
         const int task = u / per_task;
+        const bool is_a = u - task * per_task < p.units_a;
+        const uint32_t idesc = is_a ? idesc_a : kIdescB;
         const uint64_t segs = p.task_segs[task];
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1u);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * 64);
+        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc) * kGAccStride;
         uint32_t accumulate = 0;
         for (int s = 0; s < p.num_segs; ++s) {
           if (!((segs >> s) & 1ull)) continue;
@@ -118,16 +142,16 @@ __global__ void __launch_bounds__(kGradThreads, 1) mux_grad_kernel(const __grid_
             const int nk = min(kGradBK, so[s + 1] - tok) / 16;
             mbar_wait(&full_bar[stage], phase);
             tc_fence_after();
-            const uint32_t a_base = smem_u32(pipe + stage * kGStageBytes);
+            const uint32_t a_base = smem_u32(pipe + stage * stage_bytes);
             const uint32_t b_base = a_base + kGStageA;
             for (int k = 0; k < nk; ++k) {
               const uint64_t ad = smem_desc(a_base + k * 16 * 128, kGAtom, 1024);
               const uint64_t bd = smem_desc(b_base + k * 16 * 128, kGAtom, 1024);
-              mma_bf16(d_tmem, ad, bd, kIdesc, accumulate);
+              mma_bf16(d_tmem, ad, bd, idesc, accumulate);
               accumulate = 1;
             }
             mma_commit(&empty_bar[stage]);
-            if (++stage == kGradStages) { stage = 0; phase ^= 1u; }
+            if (++stage == stages) { stage = 0; phase ^= 1u; }
           }
         }
         mma_commit(&tfull_bar[acc]);
@@ -142,33 +166,50 @@ __global__ void __launch_bounds__(kGradThreads, 1) mux_grad_kernel(const __grid_
       const int task = u / per_task;
       const int sub = u - task * per_task;
       const bool is_a = sub < p.units_a;
-      const int m0 = (is_a ? sub : sub - p.units_a) * kGradBM;
       const uint64_t segs = p.task_segs[task];
       bool any = false;
       for (int s = 0; s < p.num_segs; ++s)
         if (((segs >> s) & 1ull) && so[s + 1] > so[s]) any = true;
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
+      const uint32_t t_addr =
+          tmem_base + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(acc) * kGAccStride;
       uint32_t v0[32], v1[32];
-      const uint32_t t_addr = tmem_base + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(acc * 64);
-      tmem_ld32(t_addr, v0);
-      tmem_ld32(t_addr + 32, v1);
-      tmem_ld_wait();
+      if (is_a) {
+        // accumulator columns [s * r_cap, s * r_cap + rank_{t,s}) = dA_{t,s} rows (Gs column order)
+        const int m = sub * kGradBM + 32 * q + lane;
+        for (int sc = 0; sc < S; ++sc) {
+          const int slot = task * S + sc;
+          const int rank = p.slot_rank[slot];
+          float* dA = p.slot_dA[slot];
+          if (dA == nullptr) continue;
+          for (int j0 = 0; j0 < rank; j0 += 16) {
+            uint32_t v[16];
+            tmem_ld16(t_addr + static_cast<uint32_t>(sc * p.r_cap + j0), v);
+            tmem_ld_wait();
+            if (m < p.K) {
+#pragma unroll
+              for (int j = 0; j < 16; ++j)
+                if (j0 + j < rank) dA[static_cast<size_t>(j0 + j) * p.K + m] = any ? __uint_as_float(v[j]) : 0.f;
+            }
+          }
+        }
+      } else {
+        tmem_ld32(t_addr, v0);
+        tmem_ld32(t_addr + 32, v1);
+        tmem_ld_wait();
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty_bar[acc]);
-      const int rank = p.task_rank[task];
-      const int m = m0 + 32 * q + lane;
-      if (is_a) {
-        float* dA = p.task_dA[task];
-        if (dA != nullptr && m < p.K) {
-#pragma unroll
-          for (int j = 0; j < 64; ++j)
-            if (j < rank) dA[static_cast<size_t>(j) * p.K + m] = any ? __uint_as_float(j < 32 ? v0[j & 31] : v1[j & 31]) : 0.f;
-        }
-      } else {
-        float* dB = p.task_dB[task];
-        if (dB != nullptr && m < p.N) {
+      if (!is_a) {
+        const int ub = sub - p.units_a;
+        const int sc = b_slice(ub);
+        const int slot = task * S + sc;
+        const int rank = p.slot_rank[slot];
+        const int m = (ub - p.b_units_off[sc]) * kGradBM + 32 * q + lane;   // row of dB_{t,s}
+        float* dB = p.slot_dB[slot];
+        if (dB != nullptr && m < p.slice_off[sc + 1] - p.slice_off[sc]) {
           float* row = dB + static_cast<size_t>(m) * rank;
 #pragma unroll
           for (int j = 0; j < 64; ++j)

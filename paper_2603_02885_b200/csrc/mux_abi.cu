@@ -651,9 +651,75 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
     if (e != cudaSuccess) return cuda_fail(e, bwd ? "mux_linear_bwd dX launch" : "mux_linear_fwd launch");
   }
 
-  if (bwd && (parts & 2)) {
-    // one launch per column slice s: dY's columns of the slice, Hs_s / Gs_s (columns
-    // [s * r_cap, (s + 1) * r_cap) of the side tensors), the slots (t, s)
+  int grad_max_rank = 0;
+  for (int i = 0; i < num_adapters * S; ++i)
+    if (adapters[i].dA || adapters[i].dB) grad_max_rank = std::max(grad_max_rank, adapters[i].rank);
+  if (bwd && (parts & 2) && grad_max_rank > MUX_GRAD_SIMT_MAX_RANK) {
+    // tensor cores (grad.cu): every slice in one launch; X is streamed once for all slices' dA
+    static thread_local GradParams g;
+    std::memset(&g, 0, sizeof(g));
+    __nv_bfloat16* gs_src = Gs_ext ? Gs_ext : ws.gs;
+    if (!make_map(&g.map_x, X, K, max_rows, K, 64, 128) || !make_map(&g.map_dy, a_in, N, max_rows, N, 64, 128) ||
+        !make_map(&g.map_hs, Hs_in, S * r_cap, max_rows, side_ld, 64, 128) ||
+        !make_map(&g.map_gs, gs_src, S * r_cap, max_rows, side_ld, 64, 128))
+      return fail(MUX_ERR_CUDA, "cuTensorMapEncodeTiled failed for a gradient-kernel operand (X, dY, Hs or Gs)");
+    g.seg_off = seg_off;
+    g.num_segs = num_segs;
+    g.K = K;
+    g.N = N;
+    g.r_cap = r_cap;
+    g.num_slices = S;
+    bool want_a = false, want_b = false;
+    int nt = 0;
+    for (int t = 0; t < num_adapters; ++t) {
+      bool live = false;
+      for (int sc = 0; sc < S; ++sc) {
+        const mux_adapter& a = adapters[t * S + sc];
+        live |= a.rank > 0 && (a.dA || a.dB);
+      }
+      if (!live) continue;
+      uint64_t segs = 0;
+      for (int s = 0; s < num_segs; ++s)
+        if (seg_task[s] == t) segs |= 1ull << s;
+      g.task_segs[nt] = segs;
+      for (int sc = 0; sc < S; ++sc) {
+        const mux_adapter& a = adapters[t * S + sc];
+        g.slot_rank[nt * S + sc] = a.rank;
+        g.slot_dA[nt * S + sc] = a.rank > 0 ? a.dA : nullptr;
+        g.slot_dB[nt * S + sc] = a.rank > 0 ? a.dB : nullptr;
+        want_a |= a.rank > 0 && a.dA != nullptr;
+        want_b |= a.rank > 0 && a.dB != nullptr;
+      }
+      ++nt;
+    }
+    g.num_tasks = nt;
+    g.nb_a = (S * r_cap + 63) / 64;
+    g.units_a = want_a ? (K + kGradBM - 1) / kGradBM : 0;
+    g.slice_off[0] = 0;
+    g.b_units_off[0] = 0;
+    for (int sc = 0; sc < S; ++sc) {
+      g.slice_off[sc + 1] = sl.off[sc + 1];
+      const int n_s = sl.off[sc + 1] - sl.off[sc];
+      g.b_units_off[sc + 1] = g.b_units_off[sc] + (want_b ? (n_s + kGradBM - 1) / kGradBM : 0);
+    }
+    for (int sc = S + 1; sc <= MUX_MAX_SLICES; ++sc) g.slice_off[sc] = g.b_units_off[sc] = 0;
+    g.units_b = g.b_units_off[S];
+    // stage = 128 rows of X / dY (32 KB) + the B boxes (16 KB each): 4 stages of 48 KB down to 2 of 96 KB
+    g.stage_bytes = 2u * kGradBK * 128u + static_cast<uint32_t>(std::max(g.nb_a, 1)) * kGradBK * 128u;
+    g.stages = std::min<int>(kGradStages, (kGradStages * 3u * kGradBK * 128u) / g.stage_bytes);
+    const long long units = static_cast<long long>(nt) * (g.units_a + g.units_b);
+    if (units > 0) {
+      // HBM-bound: spread the units evenly (every CTA gets the same number of units) instead of
+      // leaving a ragged last wave on 148 CTAs
+      const long long waves = (units + num_sms() - 1) / num_sms();
+      const int ggrid = static_cast<int>((units + waves - 1) / waves);
+      e = launch_grad(g, ggrid, stream);
+      if (e != cudaSuccess) return cuda_fail(e, "mux_linear_bwd grad launch");
+    }
+  } else if (bwd && (parts & 2)) {
+    // CUDA-core kernel (grad_simt.cu, MUX_GRAD_SIMT_MAX_RANK builds): one launch per column slice s:
+    // dY's columns of the slice, Hs_s / Gs_s (columns [s * r_cap, (s + 1) * r_cap) of the side
+    // tensors), the slots (t, s)
     for (int sc = 0; sc < S; ++sc) {
       static thread_local GradParams g;
       std::memset(&g, 0, sizeof(g));
@@ -695,9 +761,9 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
         // units) instead of leaving a ragged last wave on 148 CTAs
         const long long waves = (units + num_sms() - 1) / num_sms();
         const int ggrid = static_cast<int>((units + waves - 1) / waves);
-        // tensor cores (grad.cu) unless every rank is at most MUX_GRAD_SIMT_MAX_RANK, then
-        // the CUDA-core kernel (grad_simt.cu); the default comes from the A/B in DESIGN §6.2
-        e = max_rank <= MUX_GRAD_SIMT_MAX_RANK ? launch_grad_simt(g, ggrid, stream) : launch_grad(g, ggrid, stream);
+        // every rank is at most MUX_GRAD_SIMT_MAX_RANK (0 by default: DESIGN §6.2's A/B)
+        (void)max_rank;
+        e = launch_grad_simt(g, ggrid, stream);
         if (e != cudaSuccess) return cuda_fail(e, "mux_linear_bwd grad launch");
       }
     }

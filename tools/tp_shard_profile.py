@@ -66,7 +66,7 @@ def groups_of(wl, fused):
     return out
 
 
-def block_at(mux, wl, p, shared_shrink=False, fused=False):
+def block_at(mux, wl, p, shared_shrink=False, fused=False, parts=False):
     M = wl.num_tasks
     seg = -(-wl.valid_tokens // M // 64) * 64
     R = seg * M
@@ -135,9 +135,31 @@ def block_at(mux, wl, p, shared_shrink=False, fused=False):
                 mux.linear_bwd(seg_off, st, flat, dY, X, W, Hs, r_cap, dX=dX, workspace=ws)
 
         ms = time_graph(step)
+        split = None
+        if parts and S > 1:
+            # the same call split into its launches: forward (with its shrink), dX GEMM, adapter gradients
+            def fwd():
+                if shared_shrink and col:
+                    mux.linear(mux.OP_SHRINK, seg_off, st, ads, col_off, K, N, r_cap, R, X=X, Hs=Hs, row_begin=0,
+                               row_end=hi, workspace=ws)
+                    mux.linear(mux.OP_FWD_HS, seg_off, st, ads, col_off, K, N, r_cap, R, X=X, W=W, Y=Y, Hs=Hs,
+                               workspace=ws)
+                else:
+                    mux.linear(mux.OP_FWD, seg_off, st, ads, col_off, K, N, r_cap, R, X=X, W=W, Y=Y, Hs=Hs,
+                               workspace=ws)
+
+            def dx():
+                mux.linear(mux.OP_BWD_DX, seg_off, st, ads, col_off, K, N, r_cap, R, X=X, W=W, dY=dY, Hs=Hs, dX=dX,
+                           Gs=Gs, workspace=ws)
+
+            def grads():
+                mux.linear(mux.OP_BWD_GRADS, seg_off, st, ads, col_off, K, N, r_cap, R, X=X, W=W, dY=dY, Hs=Hs,
+                           Gs=Gs, workspace=ws, want_grads=True)
+            dx()
+            split = {k: round(time_graph(fn), 4) for k, fn in (("fwd", fwd), ("dx", dx), ("grads", grads))}
         f = sum(seg * (4 * K * w + 6 * r * (K + w)) for r in wl.ranks for w in widths)  # SURVEY §8(d) per token
         per.append({"linear": name, "K": K, "N": N, "slices": widths if S > 1 else None, "ms": round(ms, 4),
-                    "tflops": round(f / ms / 1e9, 1)})
+                    "tflops": round(f / ms / 1e9, 1), **({"parts_ms": split} if split else {})})
         total_ms += ms
         flops += f
         del W, ads, flat, X, dY, Y, Hs, Gs, dX, ws
@@ -158,13 +180,14 @@ def main():
     ap.add_argument("--shared-shrink", action="store_true",
                     help="column layers: own-rows shrink + fwd_hs; row layers: own-rows Gs + bwd with Gs given")
     ap.add_argument("--fused", action="store_true", help="q|k|v and gate|up as one column-sliced call each")
+    ap.add_argument("--parts", action="store_true", help="--fused calls: also time fwd / dX / gradients apart")
     a = ap.parse_args()
     from paper_2603_02885_b200 import mux
     import synth
     out = open(a.out, "w") if a.out else None
     for pt in a.points.split(","):
         cid, p = pt.split(":")
-        r = block_at(mux, synth.configs.workload(cid), int(p), a.shared_shrink, a.fused)
+        r = block_at(mux, synth.configs.workload(cid), int(p), a.shared_shrink, a.fused, a.parts)
         line = json.dumps(r)
         print(line, flush=True)
         if out:
