@@ -136,7 +136,7 @@ def block_at(mux, wl, p, shared_shrink=False, fused=False, parts=False):
 
         ms = time_graph(step)
         split = None
-        if parts and S > 1:
+        if parts:
             # the same call split into its launches: forward (with its shrink), dX GEMM, adapter gradients
             def fwd():
                 if shared_shrink and col:
@@ -180,7 +180,8 @@ def main():
     ap.add_argument("--shared-shrink", action="store_true",
                     help="column layers: own-rows shrink + fwd_hs; row layers: own-rows Gs + bwd with Gs given")
     ap.add_argument("--fused", action="store_true", help="q|k|v and gate|up as one column-sliced call each")
-    ap.add_argument("--parts", action="store_true", help="--fused calls: also time fwd / dX / gradients apart")
+    ap.add_argument("--parts", action="store_true", help="also time fwd / dX / gradients apart (through mux_linear; a row layer's dX part computes Gs "
+                         "in the GEMM)")
     a = ap.parse_args()
     from paper_2603_02885_b200 import mux
     import synth
