@@ -1032,7 +1032,8 @@ def _replicas_secondary(args, torch, dist, world, rank):
 
 def traffic_of_this_build():
     """DRAM bytes per forward-GEMM launch from the ncu --set full capture in profiles/gemm_fwd_traffic.json
-    (tools/traffic_json.py), used only if it was captured on THIS libmux.so (sha256 match); else null."""
+    (tools/traffic_json.py), used only if it was captured on THIS libmux.so or on a build of the same GEMM
+    sources and flags (sha256 match, build.gemm_source_sha16); else null."""
     import hashlib
     tp_ = os.path.join(ROOT, "profiles", "gemm_fwd_traffic.json")
     lib = os.path.join(ROOT, "paper_2603_02885_b200", "libmux.so")
@@ -1040,17 +1041,26 @@ def traffic_of_this_build():
         return None, "no capture"
     tj = json.load(open(tp_))
     sha = hashlib.sha256(open(lib, "rb").read()).hexdigest()[:16]
-    if tj.get("libmux_sha16") != sha:
-        return None, f"capture is of another build ({tj.get('libmux_sha16')} != {sha}): not reported"
+    from paper_2603_02885_b200.build import gemm_source_sha16
+    src = gemm_source_sha16()
+    if tj.get("libmux_sha16") != sha and tj.get("gemm_src_sha16") != src:
+        return None, (f"capture is of another build (so {tj.get('libmux_sha16')} != {sha}, GEMM sources "
+                      f"{tj.get('gemm_src_sha16')} != {src}): not reported")
     return tj.get("mean_bytes_per_launch"), tj.get("source")
 
 
 def _roofline(achieved, pk, timed_ms, clk, launches_per_step, kernel):
-    """frac against the measured BURST bf16 peak when the timed region is short (< 1 s) and the clocks
-    were not throttled (the burst figure is cuBLAS timed alone for ~ the same duration); against the
-    sustained peak otherwise.  Both are reported."""
-    throttled = bool(set(clk.get("reasons") or []) & {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
-                                                       "sw_power_cap"})
+    """frac against the measured BURST bf16 peak unless the clocks were actually held down: the burst
+    figure is cuBLAS timed alone for ~ the same duration, the sustained one back to back for 4 s at
+    the board's power cap.  A short region (< 1 s) whose MEDIAN SM clock stayed within 10 % of the
+    maximum takes burst even if a few samples saw sw_power_cap (the cap then bit only briefly);
+    a long region, a median clock well below max or a thermal/hw slowdown takes sustained.  Both
+    fractions are reported."""
+    reasons = set(clk.get("reasons") or [])
+    hard = bool(reasons & {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"})
+    sm, sm_max = clk.get("sm_mhz"), clk.get("sm_max_mhz")
+    held_down = sm is not None and sm_max and sm < 0.9 * sm_max
+    throttled = hard or held_down or (sm is None and "sw_power_cap" in reasons)
     use_burst = timed_ms < 1000.0 and not throttled
     peak = pk["bf16_tflops"] if use_burst else pk["bf16_tflops_sustained"]
     return {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",

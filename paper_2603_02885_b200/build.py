@@ -38,6 +38,21 @@ def stale(lib: str = None) -> bool:
     return any(os.path.getmtime(f) > t for f in sources() + headers())
 
 
+# sources that decide what the fused GEMM does on the device (kernel, its headers, the host-side
+# schedule choices: raster bands, tile width, side-first); a DRAM-traffic capture stays valid for a
+# build as long as these and the flags are unchanged (bench.py roofline.traffic)
+GEMM_SOURCES = ("gemm.cu", "common.h", "ptx.cuh", "launch.cuh", "mux_abi.cu")
+
+
+def gemm_source_sha16() -> str:
+    import hashlib
+    h = hashlib.sha256(" ".join(NVCC_FLAGS).encode())
+    for f in GEMM_SOURCES:
+        h.update(f.encode())
+        h.update(open(os.path.join(CSRC, f), "rb").read())
+    return h.hexdigest()[:16]
+
+
 def build(force: bool = False, verbose: bool = False, defines=(), out: str = None) -> str:
     """Build libmux.so; `defines`/`out` build an experiment variant (A/B
     timing only, e.g. defines=("MUX_BK=128",), out="libmux_bk128.so")."""

@@ -97,7 +97,8 @@ def test_linear_and_rs_suites_under_forced_streamk():
                         os.path.join(HERE, "test_gpu_linear.py"), os.path.join(HERE, "test_gpu_rs.py"),
                         # fwd vs fwd_hs bit identity does not hold under stream-K: with and without shrink
                         # tiles the balanced k-ranges split the main tiles at different k-blocks, so the
-                        # fp32 partials are summed in a different order (both within tolerance)
-                        "-k", "not debug_build and not given_hs_bit_identical"],
+                        # fp32 partials are summed in a different order (both within tolerance); the same
+                        # holds for the backward with Gs given (no shrink tiles) vs the fused backward
+                        "-k", "not debug_build and not given_hs_bit_identical and not given_gs_bit_identical"],
                        capture_output=True, text=True, env=env, cwd=os.path.dirname(HERE), timeout=1500)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]

@@ -12,6 +12,9 @@ import json
 import subprocess
 import sys
 
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2603_02885_b200.build import gemm_source_sha16  # noqa: E402
+
 rep = sys.argv[1]
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
@@ -33,6 +36,7 @@ lib = sys.argv[2] if len(sys.argv) > 2 else os.path.join(os.path.dirname(os.path
                                                           "paper_2603_02885_b200", "libmux.so")
 out = {"source": f"ncu --set full ({rep}), forward GEMM launches of one bench step", "per_launch": per,
        "libmux_sha16": hashlib.sha256(open(lib, "rb").read()).hexdigest()[:16],
+       "gemm_src_sha16": gemm_source_sha16(),
        "mean_bytes_per_launch": sum(x["dram_bytes"] for x in per) / max(1, len(per))}
 json.dump(out, open("profiles/gemm_fwd_traffic.json", "w"), indent=1)
 print(json.dumps(out, indent=1))
