@@ -34,6 +34,8 @@ constexpr int kSideN = 128;     // N of the shrink MMA (rank padded to 64 in CTA
 constexpr int kSkMaxClusters = 120;          // stream-K range table in shared memory (misc area)
 constexpr int kSkSlotFloats = 2 * 4 * 256 * 32;  // one cluster's partial 256 x 256 fp32 tile
 
+constexpr int kMaxCarrySlots = 32;
+
 struct GemmParams {
   // A operand of the main product: X (fwd) / dY (bwd): dims {Kred, rows}, box {64, 128}
   CUtensorMap map_a;
@@ -48,10 +50,15 @@ struct GemmParams {
   // A rank-0 slot holds a copy of another slot's maps (read only out of bounds: zero fill).
   CUtensorMap map_lora_a[MUX_MAX_ADAPTER_SLOTS];
   CUtensorMap map_lora_b[MUX_MAX_ADAPTER_SLOTS];
+  // carrier shrink operand per adapter (carry = 1, one slice, <= kMaxCarrySlots adapters):
+  // fwd A_t dims {K, rank} box {64, 8} (128 B swizzle, K-major);
+  // bwd B_t dims {rank, N} box {16, 128} (32 B swizzle: the MMA's N = rank is contiguous, MN-major)
+  CUtensorMap map_shrink[kMaxCarrySlots];
   const int32_t* seg_off;        // device [num_segs + 1]
   __nv_bfloat16* side_out;       // Hs / Gs [max_rows, num_slices * r_cap] (slice s: columns s * r_cap ..)
   __nv_bfloat16* out;            // Y / dX [max_rows, nout] (direct-store epilogue variant)
-  unsigned long long* flags;     // [ceil(max_rows/256)] epoch-tagged (workspace, zeroed once)
+  unsigned long long* flags;     // [ceil(max_rows/256)] shrink-published counters (workspace, zeroed once;
+                                 // the last CTA of every launch resets them)
   unsigned long long* epoch;     // workspace launch epoch; bumped by the last CTA to finish
   unsigned int* done;            // CTAs finished in this launch (reset by the last one)
   int32_t num_segs;
@@ -67,6 +74,7 @@ struct GemmParams {
   int32_t side_first;            // 1: all side tiles before the main tiles (short reductions)
   int32_t group_m;               // raster band: pair row-blocks sharing a sweep over W tiles
   int32_t group_n;               // > 0: column bands of group_n output blocks instead (W-resident raster)
+  int32_t carry;                 // 1: shrink on carrier main tiles, no side tiles (gemm.cu), from map_shrink
   unsigned long long* dbg;       // MUX_PROFILE builds only: wait-cycle counters (see gemm.cu)
   // Fused reduce-scatter output (tensor parallel, mux_linear_*_rs): rs_world > 0 sends each
   // output tile straight to the rank that owns its rows (rs_rows per rank, contiguous blocks):

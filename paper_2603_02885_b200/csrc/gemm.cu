@@ -61,7 +61,6 @@ namespace mux {
 constexpr uint32_t kBox = 64 * 128;                  // 8 KB: one {64 x 128 B} TMA box
 constexpr uint32_t kSubA = kBM * 128;                // 16 KB: one k-subtile of A
 constexpr uint32_t kEpiBuf = 32 * 128;               // 32 rows x 64 bf16 (one TMA store box)
-constexpr uint32_t kSmemEpi = 4 * 2 * kEpiBuf;
 constexpr uint32_t kSmemMisc = 1024;
 // per-row-block task groups, computed once per launch by all threads (8 B per pair row block)
 constexpr int kGroupTab = 128;                       // row blocks covered (32768 rows); beyond: on the fly
@@ -72,9 +71,20 @@ constexpr uint32_t kSmemGroups = kGroupTab * 8;
 // 512-column accumulator filled by two N = 256 MMAs per k-step; each CTA stages 256 B rows, so the
 // operand feed per FLOP is 3/4 of the standard tile's, at the cost of the epilogue overlap —
 // cuBLAS's own choice on these shapes, profiles/r02_cublas_kernels.csv).
+// Carrier shrink (standard tiles): the shrink Hs = s_t X A_t^T (bwd: Gs = s_t dY B_t) rides on the
+// first main tiles of each row block instead of a side tile (no second pass over X / dY).  Per stage
+// each CTA stages kShrinkRows of the 32 stacked adapter rows of the carrier's task groups (fwd: A_t
+// K-major, {64 k x 8 rows} boxes, 128 B swizzle; bwd: B_t MN-major, one {16 j x 128 n} box, 32 B
+// swizzle), so one N = 32 MMA per k-step accumulates the shrink into the other accumulator's first
+// columns.
+constexpr int kShrinkRows = 16;                       // per CTA: MMA N = 32 stacked adapter rows
+constexpr uint32_t kShrinkSub = kShrinkRows * 128;    // 2 KB per 64-deep k-subtile per CTA
+
 template <bool kBwd, int kTileN = 256>
 struct GemmLayout {
   static constexpr bool kWide = kTileN == 512;
+  static constexpr bool kCarry = kTileN == 256;              // instantiations that can carry the shrink
+  static constexpr int kEpiBufs = kCarry ? 1 : 2;           // TMA-store staging buffers per epilogue warp
   static constexpr int kBK = kWide ? 64 : GemmCfg<kBwd>::kBK;
   static constexpr int kKSub = kBK / 64;
   static constexpr int kStages = kWide ? 4 : GemmCfg<kBwd>::kStages;
@@ -86,7 +96,10 @@ struct GemmLayout {
   static constexpr uint32_t kAtomMN = kBK * 128;            // MN-major atom: kBK K-rows x 128 B
   static constexpr uint32_t kSideGrp = kKSub * kBox;        // side-tile B of one task group
   static constexpr uint32_t kSmemPipe = kStages * kStageBytes;
-  static constexpr uint32_t kSmemBytes = kSmemPipe + kSmemEpi + kSmemMisc + kSmemGroups + 1024;
+  static constexpr uint32_t kShrinkStage = kKSub * kShrinkSub;  // fwd 16 rows x 128 B; bwd 128 k-rows x 32 B
+  static constexpr uint32_t kSmemShrink = kCarry ? kStages * kShrinkStage : 0;
+  static constexpr uint32_t kSmemEpiL = 4 * kEpiBufs * kEpiBuf;
+  static constexpr uint32_t kSmemBytes = kSmemPipe + kSmemShrink + kSmemEpiL + kSmemMisc + kSmemGroups + 1024;
   static_assert(kSmemBytes <= 232448, "exceeds the 227 KB of dynamic shared memory per block");
 };
 constexpr uint32_t kTmemCols = 512;
@@ -170,7 +183,35 @@ __device__ __forceinline__ void lane_masks(int hm, uint32_t (&m)[8]) {
 struct Tile {
   int m, n;
   bool side;
+  bool carrier;  // carrier mode: this main tile also computes (part of) its row block's shrink
 };
+
+// Carrier schedule (p.carry, forward): no side tiles.  Every row block's first `nc` main tiles
+// (n < nc) carry its shrink — carrier j the task groups [j * gpc, (j + 1) * gpc), gpc = 32 / r_cap —
+// and come first (carrier 0 of every row block, then carrier 1, ...); then the other main tiles in
+// row bands as usual.  A carrier waits only for its own shrink (published by its own epilogue
+// before the tile's extension blocks); every other tile depends on lower-indexed carriers.
+__device__ __forceinline__ Tile tile_at_carry(int t, int num_m, int num_n, int nc, int group_m) {
+  Tile r;
+  r.side = false;
+  if (t < num_m * nc) {
+    r.n = t / num_m;
+    r.m = t - r.n * num_m;
+    r.carrier = true;
+    return r;
+  }
+  t -= num_m * nc;
+  const int nn = num_n - nc;
+  const int per_band = group_m * nn;
+  const int band = t / per_band;
+  const int first_m = band * group_m;
+  const int gm = min(num_m - first_m, group_m);
+  const int w = t - band * per_band;
+  r.m = first_m + w % gm;
+  r.n = nc + w / gm;
+  r.carrier = false;
+  return r;
+}
 
 // Raster: bands of `group_m` pair row-blocks.  Each band is [its side tiles]
 // then [its main tiles, row block fastest], so the side tiles' pass over the
@@ -191,6 +232,7 @@ struct Tile {
 __device__ __forceinline__ Tile tile_at(int t, int num_m, int num_n, int group_m, bool has_main, bool has_side,
                                        int side_lo, bool side_first, int group_n) {
   Tile r;
+  r.carrier = false;
   if (!has_main) {
     r.m = side_lo + t; r.n = 0; r.side = true;
     return r;
@@ -279,7 +321,13 @@ struct SkPiece {
 // Every role walks the same item sequence: f(tile, piece).
 template <typename F>
 __device__ __forceinline__ void for_each_item(const GemmParams& p, int cid, int ncl, int num_m, int num_n,
-                                              int side_lo, int total_tiles, int num_kb, const int* skb, F&& f) {
+                                              int side_lo, int total_tiles, int num_kb, const int* skb, int nc,
+                                              F&& f) {
+  if (nc > 0) {
+    for (int t = cid; t < num_m * num_n; t += ncl)
+      f(tile_at_carry(t, num_m, num_n, nc, p.group_m), SkPiece{0, num_kb, true, 0});
+    return;
+  }
   if (!p.sk) {
     for (int t = cid; t < total_tiles; t += ncl)
       f(tile_at(t, num_m, num_n, p.group_m, p.has_main != 0, p.has_side != 0, side_lo, p.side_first != 0,
@@ -288,14 +336,14 @@ __device__ __forceinline__ void for_each_item(const GemmParams& p, int cid, int 
     return;
   }
   const int n_side = p.has_side ? num_m : 0;
-  for (int t = cid; t < n_side; t += ncl) f(Tile{t, 0, true}, SkPiece{0, num_kb, true, 0});
+  for (int t = cid; t < n_side; t += ncl) f(Tile{t, 0, true, false}, SkPiece{0, num_kb, true, 0});
   const int end = skb[cid + 1];
   for (int u = skb[cid]; u < end;) {
     const int tile = u / num_kb;
     const int k0 = u - tile * num_kb;
     const int k1 = min(num_kb, end - tile * num_kb);
     const int n = tile / num_m;   // row block fastest: the clusters running at the same time share
-    f(Tile{tile - n * num_m, n, false}, SkPiece{k0, k1, k0 == 0, tile});  // A rows and W tiles in L2
+    f(Tile{tile - n * num_m, n, false, false}, SkPiece{k0, k1, k0 == 0, tile});  // A rows and W tiles in L2
     u = tile * num_kb + k1;
   }
 }
@@ -332,20 +380,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   constexpr uint32_t kAtomMN = Ly::kAtomMN;
   constexpr uint32_t kSideGrp = Ly::kSideGrp;
   constexpr uint32_t kSmemPipe = Ly::kSmemPipe;
+  constexpr bool kCarry = Ly::kCarry;
+  constexpr int kEpiBufs = Ly::kEpiBufs;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* pipe = smem;
-  uint8_t* epi = smem + kSmemPipe;
-  uint8_t* misc = epi + kSmemEpi;
+  uint8_t* shrink_area = smem + kSmemPipe;  // carrier shrink B: [stage][16 rows x 128 B] per CTA
+  uint8_t* epi = shrink_area + Ly::kSmemShrink;
+  uint8_t* misc = epi + Ly::kSmemEpiL;
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(misc);
   uint64_t* empty_bar = full_bar + kStages;
   uint64_t* tfull_bar = empty_bar + kStages;
   uint64_t* tempty_bar = tfull_bar + 2;
+  uint64_t* sfull_bar = tempty_bar + 2;   // carrier: its shrink accumulator is complete
+  uint64_t* sempty_bar = sfull_bar + 1;   // carrier: the epilogue has read it (8 warps of the pair)
   // the TMEM address slot sits apart from the mbarriers (which peer CTAs and the async proxy write)
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(misc + 192);
-  static_assert((2 * GemmLayout<kBwd, kTileN>::kStages + 4) * 8 <= 192, "mbarriers overlap the TMEM slot");
+  static_assert((2 * GemmLayout<kBwd, kTileN>::kStages + 6) * 8 <= 192, "mbarriers overlap the TMEM slot");
   int* so = reinterpret_cast<int*>(misc + 256);  // seg_off copy, <= 65 ints
   int* skb = reinterpret_cast<int*>(misc + 528);  // stream-K range table, <= kSkMaxClusters + 1 ints
+  int* s_gmax = reinterpret_cast<int*>(misc + 1016);  // max task groups over the row blocks (carrier mode)
   uint2* gtab = reinterpret_cast<uint2*>(misc + kSmemMisc);  // [kGroupTab] {seg4, hm4 | n << 24}
 
   const int warp = threadIdx.x >> 5;
@@ -372,6 +426,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       mbar_init(&tfull_bar[a], 1);
       mbar_init(&tempty_bar[a], 8);
     }
+    mbar_init(sfull_bar, 1);
+    mbar_init(sempty_bar, 8);
+    *s_gmax = 0;
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc_pair<kTmemCols>(tmem_holder);
@@ -396,13 +453,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   // the task groups of every pair row block, once per launch (the producer and the MMA issuer
   // would otherwise each rebuild them per tile on their critical path)
   const bool tab_ok = num_m <= kGroupTab;
-  if (tab_ok) {
+  const bool carry = kCarry && p.carry && p.has_main && p.has_side;
+  if (tab_ok || carry) {
+    int gm = 0;
     for (int m = threadIdx.x; m < num_m; m += blockDim.x) {
       const PairGroups g = pair_groups(p, so, m);
-      gtab[m] = make_uint2(g.seg4, g.hm4 | (static_cast<uint32_t>(g.n) << 24));
+      if (tab_ok) gtab[m] = make_uint2(g.seg4, g.hm4 | (static_cast<uint32_t>(g.n) << 24));
+      gm = max(gm, g.n);
     }
+    if (carry && gm > 0) atomicMax(s_gmax, gm);
   }
   __syncthreads();
+  // carrier mode: nc carrier tiles per row block, each carrying gpc task groups (32 stacked rows).
+  // A carrier's extension blocks wait for every carrier of its row block, so with nc > 1 all of them
+  // must be first items of their clusters (one wave) to be deadlock-free; otherwise this launch
+  // falls back to side tiles (same decision in every CTA: it depends on seg_off only).
+  const int gpc = carry ? kShrinkRows * 2 / p.r_cap : 1;
+  int nc = carry ? max(1, (*s_gmax + gpc - 1) / gpc) : 0;
+  if (nc > 1 && num_m * nc > ncl) nc = 0;
   auto groups_of = [&](int m) -> PairGroups {
     if (!tab_ok) return pair_groups(p, so, m);
     const uint2 e = gtab[m];
@@ -414,7 +482,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   };
   const int num_n = (p.nout + kTileN - 1) / kTileN;
   const int side_lo = min(p.side_m_lo, num_m);
-  const int total_tiles = p.has_main ? num_m * (num_n + (p.has_side ? 1 : 0))
+  const int total_tiles = p.has_main ? num_m * (num_n + (p.has_side && nc == 0 ? 1 : 0))
                                      : max(0, min(p.side_m_hi, num_m) - side_lo);
   const int num_kb = (p.kred + kBK - 1) / kBK;  // a partial last block reads TMA zero fill
 
@@ -438,7 +506,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       const uint32_t full_u = smem_u32(full_bar);
       const uint32_t full_leader = mapa_shared(full_u, 0);  // stage s barrier: + 8 s
       uint32_t ag_ok = 0;  // owners whose rows have landed in the gather buffer (fused all-gather)
-      for_each_item(p, cid, ncl, num_m, num_n, side_lo, total_tiles, num_kb, skb, [&](const Tile& tl, const SkPiece& pc) {
+      for_each_item(p, cid, ncl, num_m, num_n, side_lo, total_tiles, num_kb, skb, nc, [&](const Tile& tl, const SkPiece& pc) {
         PROF_T0(ts_);
         const PairGroups g = groups_of(tl.m);
         const int row_c = tl.m * kPairRows + kBM * rk;  // this CTA's rows
@@ -511,6 +579,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           // CTA's half of the tile; wide: the CTA's half of each 256-column MMA half)
           const int col_c = tl.n * kTileN + (kWide ? 128 : kTileN / 2) * rk;
           auto bcol = [&](int i) { return col_c + 256 * (i >> 1) + 64 * (i & 1); };
+          // carrier: this CTA stages stacked adapter rows [16 rk, 16 rk + 16) of the carried groups
+          // (group gl at stacked rows gl * r_cap ..): fwd two {64 k x 8 rows} boxes, bwd one
+          // {16 j x 128 n} box; rows of a group this carrier does not have are not loaded (their MMA
+          // columns are never read)
+          constexpr int kUnits = kBwd ? 1 : 2;
+          constexpr uint32_t kUnitBytes = kBwd ? Ly::kShrinkStage : 8 * 128;
+          int sh_slot[2] = {0, 0}, sh_row[2] = {0, 0};
+          uint32_t sh_mask = 0u, sh_bytes = 0u;  // this CTA's live units; both CTAs' bytes (leader)
+          if (kCarry && tl.carrier) {
+#pragma unroll
+            for (int c2 = 0; c2 < 2; ++c2)
+#pragma unroll
+              for (int s8 = 0; s8 < kUnits; ++s8) {
+                const int i = kShrinkRows * c2 + 8 * s8;
+                const int gl = i / p.r_cap;
+                const int gi = tl.n * gpc + gl;
+                if (gi >= g.n) continue;
+                sh_bytes += kUnitBytes;
+                if (c2 == rk) {
+                  sh_mask |= 1u << s8;
+                  sh_slot[s8] = p.seg_adapter[g.seg(gi)];
+                  sh_row[s8] = i - gl * p.r_cap;
+                }
+              }
+          }
           PROF_ADD(p_setup, ts_);
 #ifdef MUX_PROFILE
           ++n_tiles;
@@ -524,8 +617,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
               const uint32_t sa = pipe_u + stage * kStageBytes;
               const uint32_t sb = sa + kStageA;
               const uint32_t fbl = full_leader + 8u * stage;
-              if (leader) mbar_arrive_expect_tx_u32(full_u + 8u * stage, 2u * (kStageA + kKSub * kHalves * kBox));
+              if (leader)
+                mbar_arrive_expect_tx_u32(full_u + 8u * stage, 2u * (kStageA + kKSub * kHalves * kBox) + sh_bytes);
               const int k0 = kb * kBK;
+              if (kCarry) {
+                const uint32_t sh = smem_u32(shrink_area) + stage * Ly::kShrinkStage;
+#pragma unroll
+                for (int s8 = 0; s8 < kUnits; ++s8)
+                  if ((sh_mask >> s8) & 1u) {
+                    if (!kBwd)  // A_t rows j .. j + 7, k-columns k0 .. k0 + 63
+                      tma_load_2d_pair_u32(&p.map_shrink[sh_slot[s8]], fbl, sh + s8 * 1024u, k0, sh_row[s8]);
+                    else        // B_t columns j .. j + 15 of rows n = k0 .. k0 + 127
+                      tma_load_2d_pair_u32(&p.map_shrink[sh_slot[s8]], fbl, sh, sh_row[s8], k0);
+                  }
+              }
 #pragma unroll
               for (int s2 = 0; s2 < kKSub; ++s2) {
                 tma_load_2d_pair_u32(&p.map_a, fbl, sa + s2 * kSubA, k0 + 64 * s2, row_c);
@@ -548,11 +653,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
 #else
           if (pc.fin && g.n > 0 && p.has_side) {
 #endif
-            // the side tile of this row block must have published Hs/Gs (a caller-given
-            // Hs was written by an earlier kernel in stream order)
+            // the side tile (carrier mode: every carrier) of this row block must have published
+            // Hs/Gs (a caller-given Hs was written by an earlier kernel in stream order)
             if (elect_one_sync()) {
               const unsigned long long* flag = p.flags + tl.m;
-              const unsigned long long want = (epoch << 8) | 8ull;
+              // row-block flags are plain counters (8 epilogue warps per shrink tile / carrier),
+              // reset to 0 by the last CTA of every launch
+              const unsigned long long want = 8ull * static_cast<unsigned long long>(nc > 0 ? nc : 1);
               if (ld_acquire_gpu_u64(flag) != want) {
                 const uint64_t t0 = globaltimer_ns();
                 while (ld_acquire_gpu_u64(flag) != want) {
@@ -626,13 +733,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
+      bool prev_carrier = false;
+      uint32_t se_phase = 0;
+      // carrier shrink: M = 256, N = 32 (16 stacked adapter rows per CTA), both operands K-major
+      constexpr uint32_t kIdescShrink = idesc_bf16(kPairRows, 2 * kShrinkRows, false, kBwd);
+      // fwd: K-major 128 B swizzle (8-row groups 1 KB apart); bwd: MN-major 32 B swizzle, one atom of 16
+      // columns, 8-row groups 256 B apart, a k-step (16 rows) = 512 B
+      constexpr uint32_t kShHi = kBwd ? desc_hi_sw32(256) : desc_hi(1024);
+      const uint32_t sh_lo0 = desc_lo(smem_u32(shrink_area), 16);
       auto advance = [&]() {
         if (++stage == kStages) { stage = 0; phase ^= 1u; }
       };
-      for_each_item(p, cid, ncl, num_m, num_n, side_lo, total_tiles, num_kb, skb, [&](const Tile& tl, const SkPiece& pc) {
+      for_each_item(p, cid, ncl, num_m, num_n, side_lo, total_tiles, num_kb, skb, nc, [&](const Tile& tl, const SkPiece& pc) {
         const PairGroups g = groups_of(tl.m);
         PROF_T0(tw_);
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1u);
+        if (kCarry && prev_carrier) {  // the previous carrier's shrink sat in this accumulator
+          mbar_wait(sempty_bar, se_phase);
+          se_phase ^= 1u;
+        }
+        if (kCarry && tl.carrier)  // this carrier's shrink goes to the other accumulator: wait for the
+          mbar_wait(&tempty_bar[acc ^ 1], (acc ? acc_phase ^ 1u : acc_phase) ^ 1u);  // previous tile's drain
+        prev_carrier = kCarry && tl.carrier;
         PROF_ADD(mw_tempty, tw_);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * kBN);
@@ -755,10 +877,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
               for (int k = 0; k < kBK / 16; ++k)
                 mma_bf16_pair_nomask(d_tmem, make_desc(a_lo + a_off(k), kHi), make_desc(b_lo + b_off(k), kHi),
                                      kIdescMain, ((kb - pc.k0) | k) != 0);
+              if (kCarry && tl.carrier) {  // the shrink from the same A stage into the other accumulator
+                const uint32_t s_lo = sh_lo0 + stage * (Ly::kShrinkStage >> 4);
+#pragma unroll
+                for (int k = 0; k < kBK / 16; ++k)
+                  mma_bf16_pair_nomask(tmem_base + static_cast<uint32_t>((acc ^ 1) * kBN),
+                                       make_desc(a_lo + a_off(k), kHi),
+                                       make_desc(s_lo + (kBwd ? (k * 512) >> 4 : ((k & 3) * 32) >> 4), kShHi),
+                                       kIdescShrink, (kb | k) != 0);
+              }
               mma_commit_pair_mc(&empty_bar[stage], kPairMask);
             }
             __syncwarp();
             advance();
+          }
+          if (kCarry && tl.carrier) {  // shrink complete: the epilogue publishes Hs before the extension
+            if (elect_one_sync()) mma_commit_pair_mc(sfull_bar, kPairMask);
+            __syncwarp();
           }
           }
           // LoRA expand: the tile's final piece only, the producer's (group, live slice) blocks
@@ -817,15 +952,71 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     }
     int acc = 0;
     uint32_t acc_phase = 0;
-    uint8_t* bufs = epi + q * 2 * kEpiBuf;
+    uint32_t sf_phase = 0;
+    uint8_t* bufs = epi + q * kEpiBufs * kEpiBuf;
     int buf_sel = 0;
-    for_each_item(p, cid, ncl, num_m, num_n, side_lo, total_tiles, num_kb, skb, [&](const Tile& tl, const SkPiece& pc) {
-      PROF_T0(tw_);
-      mbar_wait(&tfull_bar[acc], acc_phase);
-      PROF_ADD(ew_tfull, tw_);
-      tc_fence_after();
+    for_each_item(p, cid, ncl, num_m, num_n, side_lo, total_tiles, num_kb, skb, nc, [&](const Tile& tl, const SkPiece& pc) {
       const int row_w = tl.m * kPairRows + kBM * static_cast<int>(crank) + 32 * q;  // first row of this warp
       const uint32_t t_addr = tmem_base + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(acc * kBN);
+      if (!(kCarry && tl.carrier)) {
+        PROF_T0(tw_);
+        mbar_wait(&tfull_bar[acc], acc_phase);
+        PROF_ADD(ew_tfull, tw_);
+        tc_fence_after();
+      } else {
+        // carrier: its shrink (other accumulator, columns [gl * r_cap, ..) for carried group gl) is
+        // complete after the main k-loop; publish Hs rows of the carried groups (carrier 0 also
+        // writes the zero rows of segments without an adapter) before this tile's extension blocks
+        mbar_wait(sfull_bar, sf_phase);
+        sf_phase ^= 1u;
+        tc_fence_after();
+        uint32_t v[32];
+        tmem_ld32(tmem_base + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>((acc ^ 1) * kBN), v);
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(sempty_bar), 0));
+        const int row = row_w + lane;
+        if (row < total_rows) {
+          const PairGroups g = groups_of(tl.m);
+          const int seg = seg_containing(so, p.num_segs, row);
+          int gi = -1;
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (i < g.n && g.seg(i) == seg) gi = i;
+          if ((gi >= 0 ? gi / gpc : 0) == tl.n) {
+            const int gl = gi >= 0 ? gi - tl.n * gpc : 0;
+            const int rank = gi >= 0 ? p.slot_rank[p.seg_adapter[seg]] : 0;
+            const float sc = gi >= 0 ? p.slot_scale[p.seg_adapter[seg]] : 0.f;
+            uint4* dst = reinterpret_cast<uint4*>(p.side_out + static_cast<size_t>(row) * p.r_cap);
+#pragma unroll
+            for (int j0 = 0; j0 < 32; j0 += 8) {
+              if (j0 < p.r_cap) {
+                uint32_t w[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const int j = j0 + 2 * e;
+                  // group gl's column j: stacked column gl * r_cap + j (gl = 1 only when r_cap = 16)
+                  const uint32_t a = (gl != 0 && j < 16) ? v[16 + (j & 15)] : v[j];
+                  const uint32_t b = (gl != 0 && j + 1 < 16) ? v[16 + ((j + 1) & 15)] : v[j + 1];
+                  const float lo = j < rank ? __uint_as_float(a) * sc : 0.f;
+                  const float hi = j + 1 < rank ? __uint_as_float(b) * sc : 0.f;
+                  w[e] = pack_bf16x2(lo, hi);
+                }
+                dst[j0 / 8] = make_uint4(w[0], w[1], w[2], w[3]);
+              }
+            }
+          }
+        }
+        fence_async_global();
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) red_add_release_gpu_u64(p.flags + tl.m, 1ull);
+        PROF_T0(tw2_);
+        mbar_wait(&tfull_bar[acc], acc_phase);
+        PROF_ADD(ew_tfull, tw2_);
+        tc_fence_after();
+      }
       const uint32_t tempty_leader = mapa_shared(smem_u32(&tempty_bar[acc]), 0);
       // wide tiles: the second half of the accumulator has its own barrier (see the MMA issuer)
       const uint32_t tempty_leader1 = mapa_shared(smem_u32(&tempty_bar[1]), 0);
@@ -875,7 +1066,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         fence_async_global();
         __threadfence();
         __syncwarp();
-        if (lane == 0) flag_arrive(p.flags + tl.m, epoch);
+        if (lane == 0) red_add_release_gpu_u64(p.flags + tl.m, 1ull);
       } else if (!pc.fin) {
         // stream-K partial (the first piece of this cluster's range): fp32 accumulator into this
         // cluster's slot, laid out [CTA][warp][col / 4][lane][4] so every access is coalesced
@@ -959,7 +1150,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           }
           uint8_t* buf = bufs + buf_sel * kEpiBuf;
           PROF_T0(tsw_);
-          if (lane == 0) tma_store_wait_read<1>();
+          if (lane == 0) tma_store_wait_read<kEpiBufs - 1>();
           __syncwarp();
           PROF_ADD(e_store, tsw_);
           uint8_t* rowp = buf + lane * 128;
@@ -988,7 +1179,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             }
             tma_store_commit();
           }
-          buf_sel ^= 1;
+          if (kEpiBufs == 2) buf_sel ^= 1;
         }
       }
       if (++acc == kAccs) { acc = 0; acc_phase ^= 1u; }
@@ -1034,7 +1225,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     if (p.rs_world > 0) __threadfence_system();
     else __threadfence();
     if (atomicAdd(p.done, 1u) == gridDim.x - 1) {
+      __threadfence();  // every CTA's flag arrivals are ordered before this reset
       *p.done = 0u;
+      for (int m = 0; m < num_m; ++m) p.flags[m] = 0ull;
       *reinterpret_cast<volatile unsigned long long*>(p.epoch) = epoch;
       __threadfence_system();
       for (int d = 0; d < p.rs_world; ++d) st_release_sys_u64(p.rs_ready[d], p.rs_seq);

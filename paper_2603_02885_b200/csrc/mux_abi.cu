@@ -134,9 +134,10 @@ struct MapKey {
   const void* ptr;
   uint64_t inner, outer, stride;
   uint32_t box_inner, box_outer;
+  int swizzle;
   bool operator==(const MapKey& o) const {
     return ptr == o.ptr && inner == o.inner && outer == o.outer && stride == o.stride &&
-           box_inner == o.box_inner && box_outer == o.box_outer;
+           box_inner == o.box_inner && box_outer == o.box_outer && swizzle == o.swizzle;
   }
 };
 struct MapKeyHash {
@@ -146,6 +147,7 @@ struct MapKeyHash {
     h ^= k.outer * 0xC2B2AE3D27D4EB4Full + (h << 6) + (h >> 2);
     h ^= k.stride * 0x165667B19E3779F9ull + (h << 6) + (h >> 2);
     h ^= (static_cast<uint64_t>(k.box_inner) << 32 | k.box_outer) + (h << 6) + (h >> 2);
+    h ^= static_cast<size_t>(k.swizzle) * 0x9E3779B97F4A7C15ull;
     return h;
   }
 };
@@ -156,10 +158,10 @@ std::mutex g_map_mu;
 std::unordered_map<MapKey, CUtensorMap, MapKeyHash> g_maps;
 
 // 2D bf16 tensor [outer, inner] with row stride `stride` elements, box
-// {box_inner, box_outer}, 128 B swizzle, zero fill out of bounds.
+// {box_inner, box_outer}, 128 B swizzle (or 32 B: swizzle = 32), zero fill out of bounds.
 bool make_map(CUtensorMap* out, const void* ptr, uint64_t inner, uint64_t outer, uint64_t stride,
-              uint32_t box_inner, uint32_t box_outer) {
-  MapKey key{ptr, inner, outer, stride, box_inner, box_outer};
+              uint32_t box_inner, uint32_t box_outer, int swizzle = 128) {
+  MapKey key{ptr, inner, outer, stride, box_inner, box_outer, swizzle};
   {
     std::lock_guard<std::mutex> g(g_map_mu);
     auto it = g_maps.find(key);
@@ -185,7 +187,8 @@ bool make_map(CUtensorMap* out, const void* ptr, uint64_t inner, uint64_t outer,
   cuuint32_t estr[2] = {1, 1};
   CUtensorMap m;
   CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return false;
   *out = m;
@@ -640,6 +643,45 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
     p.sk_side_cost_x4 = side_cost_x4;
     p.sk_flags = ws.sk_flags;
     p.sk_part = ws.sk_part;
+  }
+  // Carrier shrink (gemm.cu tile_at_carry): the shrink rides on the first main tiles of each row
+  // block instead of side tiles, which re-read X / dY and, at config 2, push the tile count just past
+  // a wave of CTA pairs (profiles/r02_shrink_cost.jsonl: side tiles 10-12 % of four of the six
+  // GEMMs).  Needs one slice, r_cap <= 32 (32 stacked adapter rows per carrier), <= 32 adapters,
+  // standard tiles, no stream-K, and enough column tiles for the carriers (<= 4 task groups per row
+  // block).  MUX_CARRY=0 keeps the side tiles, 2 forces carriers at short reductions too (A/B; read
+  // per call).
+  {
+#ifndef MUX_CARRY_DEFAULT
+#define MUX_CARRY_DEFAULT 1
+#endif
+    const char* ce = std::getenv("MUX_CARRY");
+    const int cv = (ce && *ce) ? std::atoi(ce) : MUX_CARRY_DEFAULT;
+    int live = 0;
+    for (int i = 0; i < num_segs; ++i) live += p.seg_rank[i] > 0 ? 1 : 0;
+    const int gpc = r_cap <= 32 ? 32 / r_cap : 1;
+    const int nc_max = std::max(1, (std::min(4, live) + gpc - 1) / gpc);
+    // Short reductions (<= MUX_SIDE_FIRST_MAX_KRED) keep the side tiles, all first: there a
+    // carrier's own shrink round trip (epilogue -> Hs -> flag -> extension block) is as long as a
+    // whole tile (profiles/r02_carry1_ab_tp_fwd.jsonl: 512 -> 4096 +13 %).  Wide outputs (>
+    // MUX_CARRY_MAX_NOUT) keep them too: one side tile per 43 main tiles costs ~1 % there, and the
+    // carriers measured slower (profiles/r02_carry2_ab_cfg2.jsonl: 4096 -> 11008 forward +6 %).
+#ifndef MUX_CARRY_MAX_NOUT
+#define MUX_CARRY_MAX_NOUT 8192
+#endif
+    if (cv != 0 && p.has_main && p.has_side && S == 1 && r_cap <= 32 && tile_n == kBN && !p.sk &&
+        nc_max <= num_n && num_adapters <= kMaxCarrySlots &&
+        (cv == 2 || (kred > MUX_SIDE_FIRST_MAX_KRED && nout <= MUX_CARRY_MAX_NOUT))) {
+      p.carry = 1;
+      for (int t = 0; t < num_adapters; ++t) {
+        const mux_adapter& a = adapters[t];
+        if (a.rank == 0) continue;
+        const int ldb = a.ldb == 0 ? a.rank : a.ldb;
+        const bool ok = bwd ? make_map(&p.map_shrink[t], a.B, a.rank, N, ldb, 16, 128, 32)  // B_t MN-major
+                            : make_map(&p.map_shrink[t], a.A, K, a.rank, K, 64, 8);        // A_t K-major
+        if (!ok) return fail(MUX_ERR_CUDA, "cuTensorMapEncodeTiled failed for the shrink map of adapter %d", t);
+      }
+    }
   }
   cudaError_t e = cudaSuccess;
 #ifdef MUX_DEBUG_CHECKS

@@ -174,6 +174,10 @@ __device__ __forceinline__ void flag_arrive(unsigned long long* f, unsigned long
     old = got;
   }
 }
+// fire-and-forget release add (a counter flag: no round trip, no CAS retries under contention)
+__device__ __forceinline__ void red_add_release_gpu_u64(unsigned long long* f, unsigned long long v) {
+  asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(f), "l"(v) : "memory");
+}
 // system-scope acquire / release on flags shared with peer GPUs (NVLink)
 __device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
   unsigned long long v;
@@ -374,6 +378,10 @@ __device__ __forceinline__ void mma_bf16_pair_nomask(uint32_t d_tmem, uint64_t a
 // b bytes adds b >> 4 (no carry: smem addresses < 256 KB).
 __host__ __device__ constexpr uint32_t desc_hi(uint32_t sbo_bytes) {
   return ((sbo_bytes >> 4) & 0x3FFFu) | (1u << 14) | (2u << 29);
+}
+// the same with the 32 B swizzle layout (6): MN-major atoms of 16 bf16 x 8 K-rows (256 B)
+__host__ __device__ constexpr uint32_t desc_hi_sw32(uint32_t sbo_bytes) {
+  return ((sbo_bytes >> 4) & 0x3FFFu) | (1u << 14) | (6u << 29);
 }
 __device__ __forceinline__ uint32_t desc_lo(uint32_t saddr, uint32_t lbo_bytes) {
   return ((saddr >> 4) & 0x3FFFu) | (((lbo_bytes >> 4) & 0x3FFFu) << 16);

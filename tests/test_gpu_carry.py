@@ -1,0 +1,93 @@
+"""GPU parity of the carrier shrink (gemm.cu tile_at_carry): the shrink
+Hs = s_t X A_t^T (bwd: Gs = s_t dY B_t) computed on the first main tiles of each row block
+from the same staged A tiles, instead of side tiles that re-read X / dY.  Every case runs the
+fused forward + backward twice — carriers (MUX_CARRY=2: also at these short reductions, where
+the default keeps side tiles) and side tiles (MUX_CARRY=0) — against the fp64 oracle: integer inputs bit-exact, and both schedules must
+give the same bits (the main product and each shrink element accumulate in the same order).
+Covers one carrier per row block (2 task groups at r_cap 16), several carriers in one wave
+(4 groups of 64-row segments, r_cap 32), the device-side fallback to side tiles when several
+carriers per row block would not fit one wave, rank-0 and rank < r_cap adapters."""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from gpu_harness import Problem, compare  # noqa: E402
+
+
+def _run_env(p, carry):
+    old = os.environ.get("MUX_CARRY")
+    os.environ["MUX_CARRY"] = carry
+    try:
+        return p.run_gpu()
+    finally:
+        if old is None:
+            del os.environ["MUX_CARRY"]
+        else:
+            os.environ["MUX_CARRY"] = old
+
+
+def _both(p, exact, rows=None):
+    # MUX_CARRY=2: carriers also at reductions <= 2048, where the default keeps side tiles
+    g1 = _run_env(p, "2")
+    g0 = _run_env(p, "0")
+    ref = p.run_oracle(rows=rows)
+    e1 = compare(p, g1, ref, rows=rows, exact=exact)
+    compare(p, g0, ref, rows=rows, exact=exact)
+    for k in ("Y", "Hs", "dX"):
+        assert np.array_equal(g1[k], g0[k]), f"{k}: carrier and side-tile schedules differ"
+    for t, r in enumerate(p.ranks):
+        if r:
+            assert np.array_equal(g1["dA"][t], g0["dA"][t]) and np.array_equal(g1["dB"][t], g0["dB"][t]), t
+    return e1
+
+
+def test_one_carrier_per_row_block_int():
+    """4 tasks rank 16 (config-2 structure at K = N = 1024): row blocks hold <= 2 task groups, one
+    carrier each (r_cap 16 stacks two groups); fwd and bwd (dX: 4 column tiles)."""
+    p = Problem(1024, 1024, [448, 320, 1216, 576], [16, 16, 16, 16], variant="int", seed=301)
+    _both(p, exact=True)
+
+
+def test_four_groups_several_carriers_one_wave_int():
+    """64-row segments: every row block holds 4 task groups; r_cap 32 (ranks 4/8/32/16, a rank-4
+    adapter's second 8-row slab is all zero fill) -> 4 carriers per row block, all in one wave."""
+    segs = [64] * 24
+    p = Problem(1024, 1280, segs, [4, 8, 32, 16], seg_task=[s % 4 for s in range(24)], variant="int",
+                scales=[1.0, 2.0, 0.5, 1.0], seed=302)
+    _both(p, exact=True)
+
+
+def test_two_carriers_r16_with_rank0_int():
+    """r_cap 16 with up to 4 groups per row block -> 2 carriers; a rank-0 task's rows get Hs = 0
+    from carrier 0 and never take part in a shrink MMA."""
+    segs = [64, 64, 64, 64, 64, 64, 128, 192, 64, 256]
+    p = Problem(768, 1024, segs, [16, 0, 8, 16, 4], seg_task=[0, 2, 3, 4, 1, 0, 2, 3, 1, 4], variant="int",
+                seed=303)
+    _both(p, exact=True)
+
+
+def test_fallback_to_side_tiles_int():
+    """A row block with 4 groups at r_cap 32 (4 carriers) and 31 row blocks: 124 carriers do not fit
+    one wave of CTA pairs, so the launch runs side tiles (same results)."""
+    segs = [64, 64, 64, 64] + [128] * 60
+    p = Problem(1024, 1024, segs, [32, 16, 8, 4], seg_task=[s % 4 for s in range(64)], variant="int",
+                seed=304)
+    _both(p, exact=True)
+
+
+def test_normal_values_config2_like():
+    """Floating-point inputs, 4 tasks rank 16, 4096 x 4096, 3 072 rows: sampled rows of Y / dX and all
+    of Hs, dA, dB within the north_star tolerance; carrier and side-tile schedules bit-identical."""
+    p = Problem(4096, 4096, [768, 704, 896, 704], [16, 16, 16, 16], seed=305)
+    rng = np.random.default_rng(3)
+    rows = np.unique(np.concatenate([np.arange(0, 32), np.arange(p.R - 32, p.R),
+                                     rng.integers(0, p.R, size=96)])).astype(np.int64)
+    errs = _both(p, exact=False, rows=rows)
+    print(errs)
