@@ -663,15 +663,10 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
     const int nc_max = std::max(1, (std::min(4, live) + gpc - 1) / gpc);
     // Short reductions (<= MUX_SIDE_FIRST_MAX_KRED) keep the side tiles, all first: there a
     // carrier's own shrink round trip (epilogue -> Hs -> flag -> extension block) is as long as a
-    // whole tile (profiles/r02_carry1_ab_tp_fwd.jsonl: 512 -> 4096 +13 %).  Wide outputs (>
-    // MUX_CARRY_MAX_NOUT) keep them too: one side tile per 43 main tiles costs ~1 % there, and the
-    // carriers measured slower (profiles/r02_carry2_ab_cfg2.jsonl: 4096 -> 11008 forward +6 %).
-#ifndef MUX_CARRY_MAX_NOUT
-#define MUX_CARRY_MAX_NOUT 8192
-#endif
+    // whole tile (profiles/r02_carry1_ab_tp_fwd.jsonl: 512 -> 4096 +13 %).  The kernel itself falls
+    // back to side tiles when the carriers would not fit one wave of CTA pairs.
     if (cv != 0 && p.has_main && p.has_side && S == 1 && r_cap <= 32 && tile_n == kBN && !p.sk &&
-        nc_max <= num_n && num_adapters <= kMaxCarrySlots &&
-        (cv == 2 || (kred > MUX_SIDE_FIRST_MAX_KRED && nout <= MUX_CARRY_MAX_NOUT))) {
+        nc_max <= num_n && num_adapters <= kMaxCarrySlots && (cv == 2 || kred > MUX_SIDE_FIRST_MAX_KRED)) {
       p.carry = 1;
       for (int t = 0; t < num_adapters; ++t) {
         const mux_adapter& a = adapters[t];

@@ -91,3 +91,14 @@ def test_normal_values_config2_like():
                                      rng.integers(0, p.R, size=96)])).astype(np.int64)
     errs = _both(p, exact=False, rows=rows)
     print(errs)
+
+
+def test_fallback_more_row_blocks_than_pairs():
+    """One carrier per row block but 76 row blocks on 74 CTA pairs: a carrier would be some cluster's
+    second item (it would wait for the previous tile's epilogue), so the launch runs side tiles.
+    Sampled rows of Y / dX, all of Hs / dA / dB; both schedules bit-identical."""
+    p = Problem(1024, 1024, [4864, 4864, 4864, 4864], [16, 16, 8, 16], seed=306)
+    rng = np.random.default_rng(4)
+    rows = np.unique(np.concatenate([np.arange(0, 16), np.arange(p.R - 16, p.R),
+                                     rng.integers(0, p.R, size=64)])).astype(np.int64)
+    _both(p, exact=False, rows=rows)

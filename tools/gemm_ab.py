@@ -40,6 +40,9 @@ def main():
     ap.add_argument("--shapes", default="4096x4096,4096x11008,11008x4096")
     ap.add_argument("--no-cublas", action="store_true")
     ap.add_argument("--fwd-only", action="store_true")
+    ap.add_argument("--env-ab", default="",
+                    help="VAR=a,b: time every lib once per value of the environment variable VAR (read per "
+                         "call by libmux, e.g. MUX_CARRY=1,0)")
     a = ap.parse_args()
     from paper_2603_02885_b200 import mux
     handles = {}
@@ -71,17 +74,25 @@ def main():
         if not a.no_cublas:
             cands[("cublas", "fwd")] = (lambda: torch.matmul(X, W.t()), 2 * R * K * N)
             cands[("cublas", "dX")] = (lambda: torch.matmul(dY, W), 2 * R * K * N)
+        var, vals = (a.env_ab.split("=", 1) + [""])[:2] if a.env_ab else ("", "")
         for lib, h in handles.items():
+          for val in (vals.split(",") if var else [None]):
             ws = torch.zeros(mux.linear_workspace_size(a.tasks, R, K, N, r_cap), dtype=torch.uint8, device="cuda")
 
-            def fwd(h=h, ws=ws):
+            def setenv(val=val):
+                if val is not None:
+                    os.environ[var] = val
+
+            def fwd(h=h, ws=ws, setenv=setenv):
                 mux._lib = h
+                setenv()
                 mux.linear_fwd(seg_off, st, ads, X, W, r_cap, Y=Y, Hs=Hs, workspace=ws)
 
-            def bwd(h=h, ws=ws):
+            def bwd(h=h, ws=ws, setenv=setenv):
                 mux._lib = h
+                setenv()
                 mux.linear_bwd(seg_off, st, ads, dY, X, W, Hs, r_cap, dX=dX, workspace=ws)
-            name = os.path.basename(lib)
+            name = os.path.basename(lib) + (f"[{var}={val}]" if val is not None else "")
             cands[(name, "fwd")] = (fwd, 2 * R * K * N + 2 * R * a.rank * (K + N))
             if not a.fwd_only:
                 cands[(name, "bwd(dX+grads)")] = (bwd, 2 * R * K * N + 4 * R * a.rank * (K + N))
