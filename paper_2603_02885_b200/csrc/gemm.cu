@@ -394,11 +394,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   uint64_t* tempty_bar = tfull_bar + 2;
   uint64_t* sfull_bar = tempty_bar + 2;   // carrier: its shrink accumulator is complete
   uint64_t* sempty_bar = sfull_bar + 1;   // carrier: the epilogue has read it (8 warps of the pair)
-  uint64_t* fok_full = sempty_bar + 1;    // [2] warp 3 has seen the item's shrink flag complete
-  uint64_t* fok_empty = fok_full + 2;     // [2] the producer has consumed that slot
   // the TMEM address slot sits apart from the mbarriers (which peer CTAs and the async proxy write)
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(misc + 192);
-  static_assert((2 * GemmLayout<kBwd, kTileN>::kStages + 10) * 8 <= 192, "mbarriers overlap the TMEM slot");
+  static_assert((2 * GemmLayout<kBwd, kTileN>::kStages + 6) * 8 <= 192, "mbarriers overlap the TMEM slot");
   int* so = reinterpret_cast<int*>(misc + 256);  // seg_off copy, <= 65 ints
   int* skb = reinterpret_cast<int*>(misc + 528);  // stream-K range table, <= kSkMaxClusters + 1 ints
   int* s_gmax = reinterpret_cast<int*>(misc + 1016);  // max task groups over the row blocks (carrier mode)
@@ -430,10 +428,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     }
     mbar_init(sfull_bar, 1);
     mbar_init(sempty_bar, 8);
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&fok_full[b], 1);
-      mbar_init(&fok_empty[b], 1);
-    }
     *s_gmax = 0;
     fence_mbar_init();
   }
@@ -515,8 +509,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       const uint32_t full_u = smem_u32(full_bar);
       const uint32_t full_leader = mapa_shared(full_u, 0);  // stage s barrier: + 8 s
       uint32_t ag_ok = 0;  // owners whose rows have landed in the gather buffer (fused all-gather)
-      int fslot = 0;       // warp 3's flag hand-over ring
-      uint32_t fphase = 0;
       for_each_item(p, cid, ncl, num_m, num_n, side_lo, total_tiles, num_kb, skb, nc, [&](const Tile& tl, const SkPiece& pc) {
         PROF_T0(ts_);
         const PairGroups g = groups_of(tl.m);
@@ -665,16 +657,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           if (pc.fin && g.n > 0 && p.has_side) {
 #endif
             // the side tile (carrier mode: every carrier) of this row block must have published
-            // Hs/Gs (a caller-given Hs was written by an earlier kernel in stream order).  Warp 3
-            // polls the flag ahead of time (acquire, gpu scope) and hands it over through an
-            // mbarrier, so the L2 round trip is off this warp's serial path.
-            mbar_wait(&fok_full[fslot], fphase);
+            // Hs/Gs (a caller-given Hs was written by an earlier kernel in stream order).  (Polling
+            // it from the idle warp 3 ahead of time and handing it over through an mbarrier was
+            // measured: no gain, profiles/r02_fok_ab_cfg2.jsonl.)
             if (elect_one_sync()) {
-              fence_async_global();  // Hs / Gs rows (generic stores elsewhere) -> this CTA's TMA reads
-              mbar_arrive(&fok_empty[fslot]);
+              const unsigned long long* flag = p.flags + tl.m;
+              // row-block flags are plain counters (8 epilogue warps per shrink tile / carrier),
+              // reset to 0 by the last CTA of every launch
+              const unsigned long long want = 8ull * static_cast<unsigned long long>(nc > 0 ? nc : 1);
+              if (ld_acquire_gpu_u64(flag) != want) {
+                const uint64_t t0 = globaltimer_ns();
+                while (ld_acquire_gpu_u64(flag) != want) {
+                  if (globaltimer_ns() - t0 > kWatchdogNs) __trap();
+                }
+              }
+              fence_async_global();
             }
             __syncwarp();
-            if (++fslot == 2) { fslot = 0; fphase ^= 1u; }
           }
           PROF_ADD(p_flag, tf_);
           // LoRA expand (the tile's final piece only): one extension block per (task group, slice
@@ -938,35 +937,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         if (++acc == kAccs) { acc = 0; acc_phase ^= 1u; }
       });
     }
-  } else if (warp == 3) {
-    // =========================== shrink-flag poller (warp 3) =============
-    // Same item sequence as the producer: for every tile whose extension blocks need this launch's
-    // Hs / Gs, wait until the row block's flag counter is complete (8 epilogue warps per shrink
-    // tile / carrier; reset to 0 by the last CTA of every launch) and hand it to the producer.  At
-    // most two items ahead (fok_empty).
-#ifndef MUX_DIAG_NO_FLAG
-    int fslot = 0;
-    uint32_t fphase = 0;
-    const unsigned long long want = 8ull * static_cast<unsigned long long>(nc > 0 ? nc : 1);
-    for_each_item(p, cid, ncl, num_m, num_n, side_lo, total_tiles, num_kb, skb, nc, [&](const Tile& tl, const SkPiece& pc) {
-      if (tl.side || !pc.fin || !p.has_side) return;
-      const PairGroups g = groups_of(tl.m);
-      if (g.n == 0) return;
-      mbar_wait(&fok_empty[fslot], fphase ^ 1u);
-      if (lane == 0) {
-        const unsigned long long* flag = p.flags + tl.m;
-        if (ld_acquire_gpu_u64(flag) != want) {
-          const uint64_t t0 = globaltimer_ns();
-          while (ld_acquire_gpu_u64(flag) != want) {
-            if (globaltimer_ns() - t0 > kWatchdogNs) __trap();
-          }
-        }
-        mbar_arrive(&fok_full[fslot]);
-      }
-      __syncwarp();
-      if (++fslot == 2) { fslot = 0; fphase ^= 1u; }
-    });
-#endif
   } else if (warp >= 4) {
     // =========================== epilogue (both CTAs) ===================
     const int q = warp & 3;  // TMEM lane quadrant = this CTA's rows 32q .. 32q+31
