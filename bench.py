@@ -420,6 +420,11 @@ def main_arm(args):
     mux.lib()
 
     w = Workload(args.config, rank_seed=rank)
+    bad = [i for i in range(1, len(w.linears)) if w.linears[i].K != w.linears[i - 1].N]
+    if bad:  # e.g. config 4's seven block linears (gate's N = 11008 is not up's K = 4096)
+        raise SystemExit(f"bench.py: config {args.config}'s linears do not chain as one layer stack (linear {bad[0]} "
+                         f"has K = {w.linears[bad[0]].K}, the previous N = {w.linears[bad[0] - 1].N}); "
+                         f"use --mode block (or --mode tp) for it")
     ms = MuxStep(w, torch, mux)
     ms.overlap_grads = not args.no_overlap_grads
     stream = torch.cuda.current_stream()

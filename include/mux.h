@@ -171,9 +171,10 @@ typedef struct {
 
 /* Bytes of device workspace mux_linear_fwd / mux_linear_bwd need.  The
  * workspace must be zero-filled once before its first use; it may then be
- * reused by any number of calls on the same stream (it carries an
- * epoch-tagged set of per-row-block flags, so no per-call reset is needed),
- * but must not be shared by calls that can run concurrently. */
+ * reused by any number of calls on the same stream (it carries per-row-block
+ * shrink flags that every launch leaves reset, and an epoch-tagged stream-K
+ * flag set, so no per-call reset is needed), but must not be shared by calls
+ * that can run concurrently. */
 MUX_API size_t mux_linear_workspace_size(int32_t num_segs, int32_t max_rows, int32_t K, int32_t N,
                                  int32_t r_cap);
 

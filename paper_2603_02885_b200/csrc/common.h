@@ -74,7 +74,8 @@ struct GemmParams {
   int32_t side_first;            // 1: all side tiles before the main tiles (short reductions)
   int32_t group_m;               // raster band: pair row-blocks sharing a sweep over W tiles
   int32_t group_n;               // > 0: column bands of group_n output blocks instead (W-resident raster)
-  int32_t carry;                 // 1: shrink on carrier main tiles, no side tiles (gemm.cu), from map_shrink
+  int32_t carry;                 // 1: shrink on carrier main tiles, no side tiles (gemm.cu), from map_shrink;
+                                 // 2: also when one carrier per row block spans several waves
   unsigned long long* dbg;       // MUX_PROFILE builds only: wait-cycle counters (see gemm.cu)
   // Fused reduce-scatter output (tensor parallel, mux_linear_*_rs): rs_world > 0 sends each
   // output tile straight to the rank that owns its rows (rs_rows per rank, contiguous blocks):

@@ -473,7 +473,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   // Otherwise this launch runs side tiles (same decision in every CTA: it depends on seg_off only).
   const int gpc = carry ? kShrinkRows * 2 / p.r_cap : 1;
   int nc = carry ? max(1, (*s_gmax + gpc - 1) / gpc) : 0;
-  if (num_m * nc > ncl) nc = 0;
+  if (num_m * nc > ncl && !(p.carry == 2 && nc == 1)) nc = 0;  // carry 2: one carrier may span waves
   auto groups_of = [&](int m) -> PairGroups {
     if (!tab_ok) return pair_groups(p, so, m);
     const uint2 e = gtab[m];

@@ -666,8 +666,9 @@ static mux_status linear_common(bool bwd, int32_t num_segs, const int32_t* seg_o
     // whole tile (profiles/r02_carry1_ab_tp_fwd.jsonl: 512 -> 4096 +13 %).  The kernel itself falls
     // back to side tiles when the carriers would not fit one wave of CTA pairs.
     if (cv != 0 && p.has_main && p.has_side && S == 1 && r_cap <= 32 && tile_n == kBN && !p.sk &&
-        nc_max <= num_n && num_adapters <= kMaxCarrySlots && (cv == 2 || kred > MUX_SIDE_FIRST_MAX_KRED)) {
-      p.carry = 1;
+        nc_max <= num_n && num_adapters <= kMaxCarrySlots && (cv >= 2 || kred > MUX_SIDE_FIRST_MAX_KRED)) {
+      // MUX_CARRY=3: also when one carrier per row block spans more than one wave (A/B)
+      p.carry = cv == 3 ? 2 : 1;
       for (int t = 0; t < num_adapters; ++t) {
         const mux_adapter& a = adapters[t];
         if (a.rank == 0) continue;

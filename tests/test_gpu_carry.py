@@ -33,9 +33,10 @@ def _run_env(p, carry):
             os.environ["MUX_CARRY"] = old
 
 
-def _both(p, exact, rows=None):
+def _both(p, exact, rows=None, carry="2"):
     # MUX_CARRY=2: carriers also at reductions <= 2048, where the default keeps side tiles
-    g1 = _run_env(p, "2")
+    # (3: and one carrier per row block even when the carriers span several waves)
+    g1 = _run_env(p, carry)
     g0 = _run_env(p, "0")
     ref = p.run_oracle(rows=rows)
     e1 = compare(p, g1, ref, rows=rows, exact=exact)
@@ -102,3 +103,14 @@ def test_fallback_more_row_blocks_than_pairs():
     rows = np.unique(np.concatenate([np.arange(0, 16), np.arange(p.R - 16, p.R),
                                      rng.integers(0, p.R, size=64)])).astype(np.int64)
     _both(p, exact=False, rows=rows)
+
+
+def test_one_carrier_spanning_waves():
+    """MUX_CARRY=3: one carrier per row block with 76 row blocks on 74 CTA pairs (some carriers are
+    their cluster's second item and first wait for the previous tile's epilogue to drain the other
+    accumulator); integer inputs bit-exact and bit-identical to side tiles."""
+    p = Problem(1024, 2048, [4864, 4864, 4864, 4864], [16, 16, 8, 16], variant="int", seed=307)
+    rng = np.random.default_rng(5)
+    rows = np.unique(np.concatenate([np.arange(0, 16), np.arange(p.R - 16, p.R),
+                                     rng.integers(0, p.R, size=64)])).astype(np.int64)
+    _both(p, exact=True, rows=rows, carry="3")
