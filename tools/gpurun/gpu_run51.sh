@@ -1,4 +1,5 @@
 # Multi-wave carriers (MUX_CARRY=3) on the config-4 decoder block (22 592 rows = 89 row blocks > 74 pairs)
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/r02_smoke_v5.log 2>&1; tail -1 gpurun_out/r02_smoke_v5.log
 timeout 900 python -m pytest tests/test_gpu_carry.py -m gpu -x -q > gpurun_out/r02_carry5_tests.log 2>&1; echo "pytest rc=$?" >> gpurun_out/r02_carry5_tests.log
 tail -2 gpurun_out/r02_carry5_tests.log
 if grep -q "pytest rc=0" gpurun_out/r02_carry5_tests.log; then
