@@ -18,7 +18,7 @@ torch = pytest.importorskip("torch")
 if not torch.cuda.is_available():
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
-from gpu_harness import Problem, compare  # noqa: E402
+from gpu_harness import Problem, bf16_to_f64, compare  # noqa: E402
 
 
 def _run_env(p, carry):
@@ -114,3 +114,23 @@ def test_one_carrier_spanning_waves():
     rows = np.unique(np.concatenate([np.arange(0, 16), np.arange(p.R - 16, p.R),
                                      rng.integers(0, p.R, size=64)])).astype(np.int64)
     _both(p, exact=True, rows=rows, carry="3")
+
+
+def test_nan_isolation_with_carriers():
+    """P:500 with the stacked shrink: a carrier's N = 32 MMA multiplies every row of its row block by
+    every carried group's adapter rows (the other groups' columns are discarded per row), so NaN in
+    task 1's X rows and in task 2's A / B must still never reach task 0 (3 groups in row block 0 ->
+    2 carriers at r_cap 16), forward and backward, and both schedules must agree bit for bit."""
+    p = Problem(1024, 1024, [64, 64, 128, 256, 512], [8, 16, 8], seg_task=[0, 1, 2, 0, 1], seed=308)
+    p.X[70, 5] = np.uint16(0x7FC0)       # task 1's row, in row block 0 with tasks 0 and 2
+    p.A[2][1, 7] = np.uint16(0x7FC0)     # task 2's A: its stacked shrink columns become NaN
+    p.B[2][3, 2] = np.uint16(0x7FC0)     # task 2's B: its Gs and expand
+    outs = [_run_env(p, c) for c in ("2", "0")]
+    for g in outs:
+        Y, Hs, dX = (bf16_to_f64(g[k]) for k in ("Y", "Hs", "dX"))
+        t0 = np.r_[0:64, 256:512]        # task 0's rows (segments 0 and 3)
+        assert np.all(np.isfinite(Y[t0])) and np.all(np.isfinite(Hs[t0])) and np.all(np.isfinite(dX[t0]))
+        assert np.all(np.isfinite(g["dA"][0])) and np.all(np.isfinite(g["dB"][0]))
+        assert np.isnan(Y[70]).any() and np.isnan(Y[128:256]).any()
+    for k in ("Y", "Hs", "dX"):  # same values (NaN payloads may differ)
+        assert np.array_equal(bf16_to_f64(outs[0][k]), bf16_to_f64(outs[1][k]), equal_nan=True), k
