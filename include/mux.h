@@ -71,6 +71,7 @@ typedef uint16_t mux_bf16;
 #define MUX_RS_MAX_WORLD 8    /* ranks of a fused reduce-scatter (one 8-GPU NVSwitch box) */
 #define MUX_MAX_RANK 64        /* LoRA ranks up to 64 in the paper's workloads */
 #define MUX_MAX_SLICES 4       /* column slices of one fused projection (q|k|v, gate|up) */
+#define MUX_MAX_ROWS 524288    /* max_rows of a linear call (the workspace's fixed row-block flag region) */
 #define MUX_MAX_ADAPTER_SLOTS 96  /* num_adapters * num_slices per call (kernel parameter block) */
 
 typedef enum {
@@ -171,7 +172,8 @@ typedef struct {
 
 /* Bytes of device workspace mux_linear_fwd / mux_linear_bwd need.  The
  * workspace must be zero-filled once before its first use; it may then be
- * reused by any number of calls on the same stream (it carries per-row-block
+ * reused by any number of calls on the same stream, with any max_rows <=
+ * MUX_MAX_ROWS and r_cap (it carries a fixed-size region of per-row-block
  * shrink flags that every launch leaves reset, and an epoch-tagged stream-K
  * flag set, so no per-call reset is needed), but must not be shared by calls
  * that can run concurrently. */

@@ -232,10 +232,13 @@ int num_sms() {
   return n;
 }
 
-// ---- linear-layer workspace: [epoch, done][flags][Gs][Hs scratch]
-// Zero-filled once by the caller; the GEMM kernel keeps it consistent across
-// launches (epoch-tagged flags, see ptx.cuh flag_arrive), so no per-call memset.
 // ---- linear-layer workspace: [epoch, done][flags][Gs][Hs scratch][stream-K flags][stream-K partials]
+// Zero-filled once by the caller; the GEMM kernel keeps it consistent across launches, so no
+// per-call memset: the row-block flags are counters that the last CTA of every launch resets, in a
+// region of FIXED size and offset (MUX_MAX_ROWS / 256 entries) — calls with different max_rows or
+// r_cap may share the workspace, and the Gs / Hs scratch of one must never land on another's flags
+// (it did when the region was sized by max_rows: garbage counters, a watchdog trap).  The stream-K
+// flags are epoch-tagged (ptx.cuh flag_arrive), robust to whatever the region held before.
 struct LinearWs {
   unsigned long long* epoch;
   unsigned int* done;
@@ -252,7 +255,8 @@ LinearWs carve_linear_ws(void* base, int32_t max_rows, int32_t r_cap) {
   LinearWs w{};
   const size_t n_m = (static_cast<size_t>(max_rows) + kPairRows - 1) / kPairRows;
   const size_t h = 256;
-  const size_t f = align256(n_m * sizeof(unsigned long long));
+  (void)n_m;
+  const size_t f = align256(static_cast<size_t>(MUX_MAX_ROWS / kPairRows) * sizeof(unsigned long long));
   const size_t g = align256(static_cast<size_t>(max_rows) * r_cap * 2);
   // one partial 256 x 256 fp32 tile per CTA pair of a full-device launch (stream-K, gemm.cu)
   w.sk_slots = std::min(kSkMaxClusters, num_sms() / 2);
@@ -308,7 +312,8 @@ mux_status validate_linear(int32_t num_segs, const int32_t* seg_off, const int32
     return fail(MUX_ERR_INVALID_ARGUMENT, "num_adapters * num_slices = %d * %d > %d adapter slots", num_adapters,
                 sl.n, MUX_MAX_ADAPTER_SLOTS);
   if (!seg_off || !seg_task || !adapters) return fail(MUX_ERR_INVALID_ARGUMENT, "null seg_off/seg_task/adapters");
-  if (max_rows < 1) return fail(MUX_ERR_INVALID_ARGUMENT, "max_rows=%d must be >= 1", max_rows);
+  if (max_rows < 1 || max_rows > MUX_MAX_ROWS)
+    return fail(MUX_ERR_INVALID_ARGUMENT, "max_rows=%d outside [1, %d]", max_rows, MUX_MAX_ROWS);
   // multiples of 8: 16-byte TMA row strides; partial 64-wide tiles are handled
   // by TMA zero fill (loads) and clipping (stores)
   if (K < 8 || N < 8 || (K % 8) || (N % 8))

@@ -134,3 +134,36 @@ def test_nan_isolation_with_carriers():
         assert np.isnan(Y[70]).any() and np.isnan(Y[128:256]).any()
     for k in ("Y", "Hs", "dX"):  # same values (NaN payloads may differ)
         assert np.array_equal(bf16_to_f64(outs[0][k]), bf16_to_f64(outs[1][k]), equal_nan=True), k
+
+
+def test_workspace_shared_across_row_counts():
+    """One workspace shared by calls with different max_rows (the contract allows it): small calls'
+    Gs / Hs scratch must never land on a larger call's row-block flags (with a flag region sized by
+    max_rows it did, and the 16-task call below waited on garbage counters until the watchdog
+    trapped).  Results equal those with a fresh workspace, bit for bit."""
+    from paper_2603_02885_b200 import mux
+    g = torch.Generator(device="cuda").manual_seed(9)
+    K = N = 4096
+    per, m = 1024, 16
+    W = (torch.randn(N, K, device="cuda", generator=g) / K ** 0.5).bfloat16()
+    ads = []
+    for _ in range(m):
+        B = mux.make_B_storage(N, 16)
+        B.copy_(torch.randn(N, 16, device="cuda", generator=g).bfloat16())
+        ads.append(mux.Adapter((torch.randn(16, K, device="cuda", generator=g) / K ** 0.5).bfloat16(), B, 16, 2.0))
+    X = torch.randn(m * per, K, device="cuda", generator=g).bfloat16()
+    dY = torch.randn(m * per, N, device="cuda", generator=g).bfloat16()
+    ws = torch.zeros(mux.linear_workspace_size(m, m * per, K, N, 16), dtype=torch.uint8, device="cuda")
+
+    def call(rows, tasks, workspace):
+        so = torch.tensor([i * per for i in range(tasks + 1)], dtype=torch.int32, device="cuda")
+        Y, Hs = mux.linear_fwd(so, list(range(tasks)), ads[:tasks], X[:rows], W, 16, workspace=workspace)
+        dX = mux.linear_bwd(so, list(range(tasks)), ads[:tasks], dY[:rows], X[:rows], W, Hs, 16, workspace=workspace)
+        torch.cuda.synchronize()
+        return Y.clone(), Hs.clone(), dX.clone()
+
+    for rows, tasks in ((per, 1), (2 * per, 2), (m * per, m), (per, 1), (m * per, m)):
+        got = call(rows, tasks, ws)
+        fresh = call(rows, tasks, torch.zeros_like(ws))
+        for a, b in zip(got, fresh):
+            assert torch.equal(a.view(torch.int16), b.view(torch.int16)), (rows, tasks)
