@@ -167,3 +167,23 @@ def test_workspace_shared_across_row_counts():
         fresh = call(rows, tasks, torch.zeros_like(ws))
         for a, b in zip(got, fresh):
             assert torch.equal(a.view(torch.int16), b.view(torch.int16)), (rows, tasks)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_carrier_fuzz_int(seed):
+    """Random problems (widths 768-2048, 1-8 tasks of ranks 0/4/8/16/32, 64-row-granular segments,
+    several segments per task): integer inputs bit-exact vs the oracle under carriers (forced) and
+    side tiles, both schedules bit-identical."""
+    rng = np.random.default_rng(1000 + seed)
+    K = int(rng.choice([768, 1024, 1280, 2048]))
+    N = int(rng.choice([768, 1024, 1536, 2048]))
+    T = int(rng.integers(1, 9))
+    ranks = [int(r) for r in rng.choice([0, 4, 8, 16, 32], size=T)]
+    if max(ranks) == 0:
+        ranks[0] = 16
+    S = int(rng.integers(T, min(2 * T, 12) + 1))
+    segs = [64 * int(x) for x in rng.integers(1, 9, size=S)]
+    seg_task = [s % T for s in range(S)]
+    rng.shuffle(seg_task)
+    p = Problem(K, N, segs, ranks, seg_task=seg_task, variant="int", seed=2000 + seed)
+    _both(p, exact=True)
