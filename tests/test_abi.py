@@ -81,6 +81,7 @@ def _fwd(mux, **kw):
     (dict(N=0), "multiples of 8"),
     (dict(r_cap=24), "r_cap"),
     (dict(max_rows=0), "max_rows"),
+    (dict(max_rows=524288 + 256), "max_rows"),   # MUX_MAX_ROWS: the workspace's fixed flag region
     (dict(seg_task=(ctypes.c_int32 * 1)(3)), "seg_task"),
     (dict(ads=_adapters(1, rank=65)), "rank"),
     (dict(ads=_adapters(1, rank=32), r_cap=16), "r_cap"),
@@ -253,3 +254,13 @@ def test_workspace_counts_every_slice(mux):
     """Hs/Gs scratch is [rows, S * r_cap]: a sliced call needs the workspace of S * r_cap."""
     st, msg = _generic(mux, workspace_bytes=mux.linear_workspace_size(1, 128, 256, 256, 16))
     assert st == 3 and "workspace" in msg, msg
+
+
+def test_workspace_flag_region_is_fixed(mux):
+    """The row-block flags sit in a fixed-size region at a fixed offset, so calls with different
+    max_rows (or r_cap) can share one workspace: the size grows only by the Gs / Hs scratch
+    (2 bytes per row and r_cap column, twice), never by a max_rows-sized flag array."""
+    a = mux.linear_workspace_size(4, 1024, 4096, 4096, 16)
+    b = mux.linear_workspace_size(4, 1024 + 256 * 64, 4096, 4096, 16)
+    assert b - a == 2 * (256 * 64) * 16 * 2
+    assert a >= 256 + (524288 // 256) * 8 + 2 * 1024 * 16 * 2
