@@ -48,3 +48,30 @@ def test_reference_arm_is_not_spawned(monkeypatch):
     monkeypatch.setattr(sys, "argv", ["bench.py", "--impl", "reference", "--gpus", "8"])
     bench.main()
     assert seen == [8]
+
+
+PK = {"bf16_tflops": 1644.7, "bf16_tflops_sustained": 1397.9, "source": "measured"}
+
+
+@pytest.mark.parametrize("timed_ms,clk,kind", [
+    # a short region whose median clock stayed at max takes the burst peak even if sw_power_cap showed up
+    (200.0, {"sm_mhz": 1965, "sm_max_mhz": 1965, "reasons": ["sw_power_cap"]}, "burst"),
+    (200.0, {"sm_mhz": 1882, "sm_max_mhz": 1965, "reasons": []}, "burst"),
+    # the clock held > 10 % below max: sustained
+    (200.0, {"sm_mhz": 1700, "sm_max_mhz": 1965, "reasons": ["sw_power_cap"]}, "sustained"),
+    # thermal / hw slowdown: sustained
+    (200.0, {"sm_mhz": 1965, "sm_max_mhz": 1965, "reasons": ["hw_thermal_slowdown"]}, "sustained"),
+    # a long region: sustained
+    (1500.0, {"sm_mhz": 1965, "sm_max_mhz": 1965, "reasons": []}, "sustained"),
+    # no clock samples but a power cap reported: sustained
+    (200.0, {"reasons": ["sw_power_cap"]}, "sustained"),
+])
+def test_roofline_peak_choice(timed_ms, clk, kind):
+    """roofline.frac's denominator: the measured burst bf16 peak unless the clocks
+    were actually held down or the region is long; both fractions always reported."""
+    r = bench._roofline(1300.0, PK, timed_ms, clk, 3, "k")
+    assert r["peak_kind"].startswith(kind), r
+    assert r["peak"] == (PK["bf16_tflops"] if kind == "burst" else PK["bf16_tflops_sustained"])
+    assert abs(r["frac"] - 1300.0 / r["peak"]) < 1e-12
+    assert abs(r["frac_of_burst"] - 1300.0 / 1644.7) < 1e-12
+    assert abs(r["frac_of_sustained"] - 1300.0 / 1397.9) < 1e-12
